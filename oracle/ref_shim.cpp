@@ -1,0 +1,307 @@
+// TEST INFRASTRUCTURE ONLY — never linked into the product.
+//
+// A thin extern "C" shim over the *unmodified* reference decoder headers and
+// sources under /root/reference/proj (compiled in place by oracle/Makefile,
+// output only into oracle/_ref/).  It exposes exactly the calls the parity
+// tests and bench.py's cpu_baseline / --impl reference leg need:
+//
+//   polref_create/decode/destroy  -> FrameDecoder<R>(code, tree, kind, L)
+//                                    + decode()  (proj/include/polar/decoders.hpp:37-85)
+//                                    with the tree chosen as run_montecarlo
+//                                    does (proj/src/sim.cpp:161-164)
+//   polref_list_decode            -> ListDecoder<R>::decode + alive/metric
+//                                    introspection (list_decoder.hpp:77-93)
+//   polref_tree                   -> PruneTree (prune_tree.hpp:49-73)
+//   polref_crc / polref_crc_check -> CrcEngine::compute/check (crc.cpp:121-154)
+//   polref_construct_frozen       -> construct_frozen (code.cpp:63-77)
+//   polref_channel                -> run_frame's input side: FrameRng,
+//                                    random_payload, encode_systematic,
+//                                    transmit (sim.cpp:45-51, channel.hpp)
+//
+// Payload and codeword outputs are packed MSB-first, the BitVector byte
+// convention (bit_vector.hpp:11-14, 57-59).
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <optional>
+#include <string>
+#include <thread>
+#include <variant>
+#include <vector>
+
+#include "polar/channel.hpp"
+#include "polar/code.hpp"
+#include "polar/crc.hpp"
+#include "polar/decoders.hpp"
+#include "polar/errors.hpp"
+#include "polar/prune_tree.hpp"
+
+using namespace polar;
+
+namespace {
+
+void set_err(char* err, int errlen, const std::string& msg) {
+    if (err && errlen > 0) {
+        std::snprintf(err, std::size_t(errlen), "%s", msg.c_str());
+    }
+}
+
+BitVector mask_from_bytes(const std::uint8_t* b, int n) {
+    BitVector v(static_cast<std::size_t>(n));
+    for (int i = 0; i < n; ++i) v.set(std::size_t(i), b[i] != 0);
+    return v;
+}
+
+void pack_bits(const BitVector& v, std::uint8_t* out) {
+    const std::size_t nb = (v.size() + 7) / 8;
+    for (std::size_t k = 0; k < nb; ++k) out[k] = v.byte(k);
+}
+
+std::optional<CrcSpec> crc_opt(const char* spec) {
+    if (!spec || !*spec) return std::nullopt;
+    return CrcSpec::parse(spec);
+}
+
+struct Handle {
+    PolarCode code;
+    std::unique_ptr<PruneTree> tree;
+    DecoderKind kind;
+    int l;
+    int precision; // 0 f32, 1 int8, 2 int16
+};
+
+template <class R>
+void decode_range(const Handle& h, const R* llr, std::int64_t f0, std::int64_t f1,
+                  std::uint8_t* payload, std::uint8_t* codeword,
+                  std::uint8_t* crc_ok, std::uint8_t* esc, double* metric) {
+    FrameDecoder<R> dec(h.code, *h.tree, h.kind, h.l);
+    const std::size_t pbytes = std::size_t(h.code.payload_size() + 7) / 8;
+    const std::size_t cbytes = std::size_t(h.code.n + 7) / 8;
+    for (std::int64_t f = f0; f < f1; ++f) {
+        const DecodeResult r = dec.decode(llr + std::size_t(f) * std::size_t(h.code.n));
+        if (payload) pack_bits(r.payload, payload + std::size_t(f) * pbytes);
+        if (codeword) pack_bits(r.codeword, codeword + std::size_t(f) * cbytes);
+        if (crc_ok) crc_ok[f] = r.crc_ok ? 1 : 0;
+        if (esc) esc[f] = std::uint8_t(r.escalation_level);
+        if (metric) metric[f] = r.metric;
+    }
+}
+
+template <class F>
+void parallel_frames(std::int64_t nframes, int nthreads, F&& fn) {
+    if (nthreads <= 1 || nframes < 2) {
+        fn(std::int64_t(0), nframes);
+        return;
+    }
+    const int nt = int(std::min<std::int64_t>(nthreads, nframes));
+    std::vector<std::thread> pool;
+    for (int t = 0; t < nt; ++t) {
+        const std::int64_t a = nframes * t / nt, b = nframes * (t + 1) / nt;
+        pool.emplace_back([&fn, a, b] { fn(a, b); });
+    }
+    for (auto& th : pool) th.join();
+}
+
+} // namespace
+
+extern "C" {
+
+void* polref_create(int n, int k, const std::uint8_t* frozen, const char* crc_spec,
+                    int kind, int l, int precision, int r0, int r1, int rep,
+                    int spc, int rep_max, int spc_max, char* err, int errlen) {
+    try {
+        auto h = std::make_unique<Handle>();
+        h->code = make_code(n, k, mask_from_bytes(frozen, n), crc_opt(crc_spec));
+        h->kind = DecoderKind(kind);
+        PruningConfig pc{r0 != 0, r1 != 0, rep != 0, spc != 0, rep_max, spc_max};
+        // sim.cpp:161-164: the pruned tree only for SSC-family decoders
+        h->tree = std::make_unique<PruneTree>(
+            h->code.frozen, decoder_uses_pruning(h->kind) ? pc : PruningConfig::none());
+        h->l = l;
+        h->precision = precision;
+        // construct once to surface ConfigError at create time
+        switch (precision) {
+        case 0: FrameDecoder<float>(h->code, *h->tree, h->kind, l); break;
+        case 1: FrameDecoder<std::int8_t>(h->code, *h->tree, h->kind, l); break;
+        case 2: FrameDecoder<std::int16_t>(h->code, *h->tree, h->kind, l); break;
+        default: throw ConfigError("bad precision");
+        }
+        return h.release();
+    } catch (const std::exception& e) {
+        set_err(err, errlen, e.what());
+        return nullptr;
+    }
+}
+
+void polref_destroy(void* h) { delete static_cast<Handle*>(h); }
+
+int polref_payload_bits(void* hv) {
+    return static_cast<Handle*>(hv)->code.payload_size();
+}
+
+int polref_decode(void* hv, const void* llr, std::int64_t nframes, int nthreads,
+                  std::uint8_t* payload, std::uint8_t* codeword, std::uint8_t* crc_ok,
+                  std::uint8_t* esc, double* metric) {
+    const Handle& h = *static_cast<Handle*>(hv);
+    try {
+        parallel_frames(nframes, nthreads, [&](std::int64_t a, std::int64_t b) {
+            switch (h.precision) {
+            case 0:
+                decode_range<float>(h, static_cast<const float*>(llr), a, b, payload,
+                                    codeword, crc_ok, esc, metric);
+                break;
+            case 1:
+                decode_range<std::int8_t>(h, static_cast<const std::int8_t*>(llr), a,
+                                          b, payload, codeword, crc_ok, esc, metric);
+                break;
+            default:
+                decode_range<std::int16_t>(h, static_cast<const std::int16_t*>(llr),
+                                           a, b, payload, codeword, crc_ok, esc,
+                                           metric);
+                break;
+            }
+        });
+    } catch (const std::exception&) {
+        return 1;
+    }
+    return 0;
+}
+
+// One frame through ListDecoder<R> directly, with post-decode introspection.
+int polref_list_decode(void* hv, const void* llr, int l, int select_by_crc,
+                       std::uint8_t* payload, std::uint8_t* codeword,
+                       std::uint8_t* crc_ok, double* metric, std::uint8_t* alive,
+                       double* slot_metric, char* err, int errlen) {
+    const Handle& h = *static_cast<Handle*>(hv);
+    try {
+        auto run = [&](auto tag) {
+            using R = decltype(tag);
+            ListDecoder<R> dec(h.code, *h.tree, h.l, PsumLayout::copy);
+            const DecodeResult r =
+                dec.decode(static_cast<const R*>(llr), l, select_by_crc != 0);
+            pack_bits(r.payload, payload);
+            pack_bits(r.codeword, codeword);
+            *crc_ok = r.crc_ok;
+            *metric = r.metric;
+            for (int p = 0; p < h.l; ++p) {
+                alive[p] = dec.is_alive(p) ? 1 : 0;
+                slot_metric[p] = dec.is_alive(p) ? dec.metric_of(p) : 0.0;
+            }
+        };
+        if (h.precision == 0) run(float{});
+        else if (h.precision == 1) run(std::int8_t{});
+        else run(std::int16_t{});
+    } catch (const std::exception& e) {
+        set_err(err, errlen, e.what());
+        return 1;
+    }
+    return 0;
+}
+
+// Node list: 6 ints per node (kind, depth, leaf_begin, size, left, right).
+int polref_tree(const std::uint8_t* frozen, int n, int r0, int r1, int rep, int spc,
+                int rep_max, int spc_max, std::int32_t* out, int max_nodes, char* err,
+                int errlen) {
+    try {
+        PruneTree t(mask_from_bytes(frozen, n),
+                    PruningConfig{r0 != 0, r1 != 0, rep != 0, spc != 0, rep_max, spc_max});
+        const int cnt = int(t.node_count());
+        if (cnt > max_nodes) throw ConfigError("node buffer too small");
+        for (int i = 0; i < cnt; ++i) {
+            const TreeNode& nd = t.node(i);
+            out[6 * i + 0] = int(nd.kind);
+            out[6 * i + 1] = nd.depth;
+            out[6 * i + 2] = nd.leaf_begin;
+            out[6 * i + 3] = nd.size;
+            out[6 * i + 4] = nd.left;
+            out[6 * i + 5] = nd.right;
+        }
+        return cnt;
+    } catch (const std::exception& e) {
+        set_err(err, errlen, e.what());
+        return -1;
+    }
+}
+
+// CRC of `len` bits given as 0/1 bytes.
+int polref_crc(const char* spec, const std::uint8_t* bits, std::int64_t len,
+               std::uint64_t* out, char* err, int errlen) {
+    try {
+        CrcEngine eng(CrcSpec::parse(spec));
+        BitVector v(static_cast<std::size_t>(len));
+        for (std::int64_t i = 0; i < len; ++i) v.set(std::size_t(i), bits[i] != 0);
+        *out = eng.compute(v);
+        return 0;
+    } catch (const std::exception& e) {
+        set_err(err, errlen, e.what());
+        return 1;
+    }
+}
+
+int polref_crc_check(const char* spec, const std::uint8_t* bits, std::int64_t len) {
+    try {
+        CrcEngine eng(CrcSpec::parse(spec));
+        BitVector v(static_cast<std::size_t>(len));
+        for (std::int64_t i = 0; i < len; ++i) v.set(std::size_t(i), bits[i] != 0);
+        return eng.check(v) ? 1 : 0;
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
+int polref_construct_frozen(int n, int reliable, double design, std::uint8_t* out,
+                            char* err, int errlen) {
+    try {
+        const BitVector m = construct_frozen(n, reliable, design);
+        for (int i = 0; i < n; ++i) out[i] = m.get(std::size_t(i)) ? 1 : 0;
+        return 0;
+    } catch (const std::exception& e) {
+        set_err(err, errlen, e.what());
+        return 1;
+    }
+}
+
+// run_frame's input side (sim.cpp:48-51) for frames [frame0, frame0+nframes):
+// info bits as 0/1 bytes (k per frame) and channel LLRs in the requested
+// representation (precision 0 f32, 1 int8, 2 int16; scale <= 0 = default).
+int polref_channel(int n, int k, const std::uint8_t* frozen, const char* crc_spec,
+                   double ebn0_db, std::uint64_t seed, std::uint64_t frame0,
+                   std::int64_t nframes, int precision, float scale,
+                   std::uint8_t* info_out, void* llr_out, int nthreads, char* err,
+                   int errlen) {
+    try {
+        const PolarCode code = make_code(n, k, mask_from_bytes(frozen, n), crc_opt(crc_spec));
+        const double sigma2 = awgn_sigma2(code, ebn0_db);
+        parallel_frames(nframes, nthreads, [&](std::int64_t a, std::int64_t b) {
+            for (std::int64_t f = a; f < b; ++f) {
+                FrameRng rng(seed, frame0 + std::uint64_t(f));
+                const BitVector info = random_payload(rng, std::size_t(k));
+                const BitVector x = encode_systematic(code, info);
+                if (info_out)
+                    for (int i = 0; i < k; ++i)
+                        info_out[std::size_t(f) * std::size_t(k) + std::size_t(i)] =
+                            info.get(std::size_t(i));
+                const std::size_t off = std::size_t(f) * std::size_t(n);
+                if (precision == 0)
+                    transmit<float>(code, x, sigma2, rng,
+                                    scale > 0 ? scale : default_quant_scale<float>(),
+                                    static_cast<float*>(llr_out) + off);
+                else if (precision == 1)
+                    transmit<std::int8_t>(code, x, sigma2, rng,
+                                          scale > 0 ? scale : default_quant_scale<std::int8_t>(),
+                                          static_cast<std::int8_t*>(llr_out) + off);
+                else
+                    transmit<std::int16_t>(code, x, sigma2, rng,
+                                           scale > 0 ? scale : default_quant_scale<std::int16_t>(),
+                                           static_cast<std::int16_t*>(llr_out) + off);
+            }
+        });
+        return 0;
+    } catch (const std::exception& e) {
+        set_err(err, errlen, e.what());
+        return 1;
+    }
+}
+
+} // extern "C"
