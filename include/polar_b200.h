@@ -1,0 +1,153 @@
+/* polar_b200.h — C ABI of the B200-native batched polar decoder.
+ *
+ * Drop-in for the reference's decoder API (a header-only C++ template
+ * interface, no FFI of its own):
+ *
+ *   reference                                              here
+ *   ------------------------------------------------------ -------------------
+ *   make_code(n, k, frozen, crc)  code.hpp:43-45,          pl_code (validated
+ *                                 code.cpp:79-126           in pl_create)
+ *   CrcSpec / CrcSpec::parse      crc.hpp:16-26,            pl_crc, pl_crc_parse
+ *                                 crc.cpp:42-84
+ *   PruningConfig                 prune_tree.hpp:25-34      pl_pruning
+ *   PruneTree(frozen, cfg)        prune_tree.hpp:49-73,     built inside
+ *                                 sim.cpp:161-164            pl_create; exported
+ *                                                            for tests: pl_tree_build
+ *   DecoderKind                   decoders.hpp:10-18        PL_KIND_*
+ *   FrameDecoder<R>(code, tree,   decoders.hpp:37-55        pl_create
+ *                   kind, l)
+ *   FrameDecoder<R>::decode(R*)   decoders.hpp:60-85        pl_decode (a batch of
+ *     -> DecodeResult             decode_result.hpp:7-14     frames per call)
+ *   ConfigError / ParseError      errors.hpp:9-21           PL_ERR_CONFIG /
+ *                                                            PL_ERR_PARSE +
+ *                                                            pl_last_error
+ *   CrcEngine::compute            crc.cpp:121-144           pl_crc_compute
+ *
+ * Plain pointers and sizes only.  Device pointers are CUDA global-memory
+ * pointers; `stream` is a cudaStream_t passed as void*.  A handle is not
+ * thread-safe (the reference's FrameDecoder is not either);
+ * use one handle per host thread / stream.  There is no CPU fallback: every
+ * decode runs the sm_100a kernels or fails with PL_ERR_CUDA.
+ */
+#ifndef POLAR_B200_H
+#define POLAR_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (the C face of the reference's exceptions) */
+#define PL_OK 0
+#define PL_ERR_CONFIG 1 /* ConfigError: bad code / decoder / tree parameters */
+#define PL_ERR_PARSE 2  /* ParseError: malformed CRC spec text */
+#define PL_ERR_CUDA 3   /* device failure (no GPU, launch error, OOM) */
+#define PL_ERR_ARG 4    /* null pointer / bad size passed to the ABI */
+
+/* DecoderKind, decoders.hpp:10-18 — same order */
+#define PL_KIND_SC 0
+#define PL_KIND_SSC 1
+#define PL_KIND_SCL 2
+#define PL_KIND_SSCL 3
+#define PL_KIND_CA_SSCL 4
+#define PL_KIND_PA_SSCL 5
+#define PL_KIND_FA_SSCL 6
+
+/* LLR representation (llr.hpp:12-33): float32 or int8 saturated to +-127 */
+#define PL_F32 0
+#define PL_I8 1
+
+typedef struct pl_crc {
+    int32_t width; /* 0 = code without CRC; else 1..64 */
+    int32_t reflect;
+    uint64_t poly; /* normal form without the top bit (crc.hpp:16-20) */
+    uint64_t init;
+    uint64_t xorout;
+} pl_crc;
+
+typedef struct pl_code {
+    int32_t n;             /* block length, power of two, 2..16384 */
+    int32_t k;             /* information bits, CRC excluded (code.hpp:31) */
+    const uint8_t* frozen; /* n bytes, nonzero = frozen; host memory */
+    pl_crc crc;
+} pl_code;
+
+typedef struct pl_pruning { /* PruningConfig, prune_tree.hpp:25-34 */
+    int32_t rate_zero, rate_one, repetition, single_parity;
+    int32_t rep_max; /* 0 = unlimited, else >= 2 */
+    int32_t spc_max; /* 0 = unlimited, else >= 4 */
+} pl_pruning;
+
+typedef struct pl_decoder {
+    int32_t kind;      /* PL_KIND_* */
+    int32_t l;         /* list size (Lmax for PA/FA); power of two <= 32 */
+    int32_t precision; /* PL_F32 / PL_I8 */
+    pl_pruning pruning;
+} pl_decoder;
+
+typedef struct pl_handle pl_handle;
+
+/* Build a decoder for one or more codes (mixed-code batches select a code
+ * per frame).  Validates exactly what make_code, PruneTree and FrameDecoder
+ * validate and returns PL_ERR_CONFIG where they throw ConfigError.  The
+ * handle owns copies of all code data and its device tables. */
+int pl_create(const pl_code* codes, int32_t ncodes, const pl_decoder* dec,
+              int32_t device, pl_handle** out);
+
+/* Message of the last failure on this handle ("" if none).  With a NULL
+ * handle: the last pl_create / pl_crc_parse failure of the calling thread. */
+const char* pl_last_error(const pl_handle* h);
+
+void pl_destroy(pl_handle* h);
+
+/* Strides of the batch buffers (elements for LLRs, bytes for the rest). */
+int64_t pl_llr_stride(const pl_handle* h);      /* max n over codes */
+int64_t pl_payload_stride(const pl_handle* h);  /* max ceil((k+c)/8) */
+int64_t pl_codeword_stride(const pl_handle* h); /* max ceil(n/8) */
+
+/* Decode nframes frames resident in device memory.
+ *   llr      frame-major, pl_llr_stride elements per frame (float or int8)
+ *   code_id  per-frame code index, NULL = code 0 for every frame
+ *   payload  pl_payload_stride bytes per frame: the payload (message + CRC)
+ *            packed MSB-first, DecodeResult::payload (decode_result.hpp:9)
+ *   codeword optional (NULL), pl_codeword_stride bytes per frame, MSB-first
+ *   crc_ok   1 byte per frame (optional)
+ *   esc      escalation level per frame: the list size that produced the
+ *            answer, 1 = SC (optional)
+ *   metric   path metric of the returned candidate, float (optional)
+ * Asynchronous on `stream`. */
+int pl_decode(pl_handle* h, const void* llr, const int32_t* code_id, int64_t nframes,
+              uint8_t* payload, uint8_t* codeword, uint8_t* crc_ok, uint8_t* esc,
+              float* metric, void* stream);
+
+/* Same with HOST buffers: the call stages through pinned memory, overlaps
+ * host<->device copies with decoding in chunks and returns when the outputs
+ * are in host memory. */
+int pl_decode_host(pl_handle* h, const void* llr, const int32_t* code_id,
+                   int64_t nframes, uint8_t* payload, uint8_t* codeword,
+                   uint8_t* crc_ok, uint8_t* esc, float* metric);
+
+/* Kernel launches issued by the last pl_decode / pl_decode_host call. */
+int64_t pl_last_launches(const pl_handle* h);
+
+/* ---- host-side helpers (no GPU needed) ---------------------------------- */
+
+/* CrcSpec::parse (crc.cpp:42-84): "32-GZIP", "16-CCITT", "8" or
+ * "width:poly:reflect:init:xorout" (hex fields). */
+int pl_crc_parse(const char* text, pl_crc* out);
+
+/* CrcEngine::compute over `len` bits given one per byte (crc.cpp:121-144). */
+int pl_crc_compute(const pl_crc* spec, const uint8_t* bits, int64_t len,
+                   uint64_t* out);
+
+/* PruneTree node list (prune_tree.cpp:38-71), 6 ints per node:
+ * kind, depth, leaf_begin, size, left, right.  Returns the node count, or
+ * -1 (bad arguments / buffer too small). */
+int32_t pl_tree_build(const uint8_t* frozen, int32_t n, const pl_pruning* cfg,
+                      int32_t* out, int32_t max_nodes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* POLAR_B200_H */

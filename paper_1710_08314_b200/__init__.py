@@ -1,0 +1,26 @@
+"""B200-native batched polar decoder (SC / SSC / SCL / CA-SCL / PA / FA-SCL).
+
+A drop-in for the reference's decoder path (FrameDecoder<R>::decode,
+/root/reference/proj/include/polar/decoders.hpp:60-85) built as hand-written
+sm_100a kernels behind a C ABI (include/polar_b200.h).  ``polar`` mirrors
+the reference's C++ interface in Python over that ABI.
+"""
+from .polar import (  # noqa: F401
+    ConfigError,
+    CrcSpec,
+    DecodeResult,
+    DecoderKind,
+    DeviceError,
+    FrameDecoder,
+    ParseError,
+    PolarCode,
+    Precision,
+    PruningConfig,
+    channel,
+    construct_frozen,
+    construct_frozen_ga,
+    crc_compute,
+    make_code,
+    prune_tree,
+    unpack_msb,
+)

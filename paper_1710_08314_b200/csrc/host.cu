@@ -1,0 +1,851 @@
+// Host side of the C ABI (include/polar_b200.h): validation, decode tree
+// and schedule construction, CRC syndrome tables, device residency of the
+// per-code tables, and the per-kind launch sequence including the fully
+// adaptive ladder (decoders.hpp:60-85) as stream-ordered rungs over
+// compacted frame lists.
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/polar_b200.h"
+#include "polar_dev.h"
+
+namespace {
+
+thread_local std::string g_thread_err;
+
+struct ConfigError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct ParseError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ---- CRC engine (crc.cpp:86-154 semantics) ------------------------------
+uint64_t bit_reverse(uint64_t v, int width) {
+    uint64_t r = 0;
+    for (int i = 0; i < width; ++i) {
+        r = (r << 1) | (v & 1);
+        v >>= 1;
+    }
+    return r;
+}
+
+struct Crc {
+    pl_crc spec{};
+    uint64_t table[256]{};
+    uint64_t rpoly = 0, poly_top = 0, init_reg = 0;
+
+    explicit Crc(const pl_crc& s) : spec(s) {
+        if (s.width < 1 || s.width > 64)
+            throw ConfigError("CRC width must be in [1, 64], got " + std::to_string(s.width));
+        const uint64_t mask = s.width == 64 ? ~0ull : ((1ull << s.width) - 1);
+        if ((s.poly & ~mask) || (s.init & ~mask) || (s.xorout & ~mask))
+            throw ConfigError("CRC poly/init/xorout do not fit in " + std::to_string(s.width) +
+                              " bits");
+        if ((s.poly & 1) == 0) throw ConfigError("CRC poly must have its x^0 term set");
+        if (s.reflect) {
+            rpoly = bit_reverse(s.poly, s.width);
+            init_reg = bit_reverse(s.init, s.width);
+            for (int b = 0; b < 256; ++b) {
+                uint64_t r = uint64_t(b);
+                for (int i = 0; i < 8; ++i) r = (r >> 1) ^ ((r & 1) ? rpoly : 0);
+                table[b] = r;
+            }
+        } else {
+            poly_top = s.poly << (64 - s.width);
+            init_reg = s.init << (64 - s.width);
+            for (int b = 0; b < 256; ++b) {
+                uint64_t r = uint64_t(b) << 56;
+                for (int i = 0; i < 8; ++i) {
+                    const bool top = r >> 63;
+                    r <<= 1;
+                    if (top) r ^= poly_top;
+                }
+                table[b] = r;
+            }
+        }
+    }
+
+    // bits one per byte, index order; whole bytes MSB-first through the table,
+    // trailing bits folded one at a time
+    uint64_t compute(const uint8_t* bits, size_t len) const {
+        uint64_t reg = init_reg;
+        const size_t nbytes = len / 8;
+        auto byte_at = [&](size_t k) {
+            unsigned v = 0;
+            for (int j = 0; j < 8; ++j) v = (v << 1) | (bits[8 * k + j] & 1u);
+            return v;
+        };
+        if (spec.reflect) {
+            for (size_t k = 0; k < nbytes; ++k) reg = (reg >> 8) ^ table[(reg ^ byte_at(k)) & 0xFF];
+            for (size_t i = nbytes * 8; i < len; ++i) {
+                reg ^= uint64_t(bits[i] & 1u);
+                const bool lo = reg & 1;
+                reg >>= 1;
+                if (lo) reg ^= rpoly;
+            }
+            return reg ^ spec.xorout;
+        }
+        for (size_t k = 0; k < nbytes; ++k)
+            reg = (reg << 8) ^ table[((reg >> 56) ^ byte_at(k)) & 0xFF];
+        for (size_t i = nbytes * 8; i < len; ++i) {
+            reg ^= uint64_t(bits[i] & 1u) << 63;
+            const bool top = reg >> 63;
+            reg <<= 1;
+            if (top) reg ^= poly_top;
+        }
+        return (reg >> (64 - spec.width)) ^ spec.xorout;
+    }
+};
+
+pl_crc parse_crc(const std::string& text) {
+    if (text == "32-GZIP") return pl_crc{32, 1, 0x04C11DB7, 0xFFFFFFFF, 0xFFFFFFFF};
+    if (text == "16-CCITT") return pl_crc{16, 0, 0x1021, 0xFFFF, 0x0000};
+    if (text == "8") return pl_crc{8, 0, 0x07, 0x00, 0x00};
+    std::vector<std::string> f(1);
+    for (char c : text) {
+        if (c == ':') f.emplace_back();
+        else f.back().push_back(c);
+    }
+    if (f.size() != 5)
+        throw ParseError("CRC spec '" + text +
+                         "': expected a preset name or width:poly:reflect:init:xorout");
+    auto hex = [](const std::string& s, const char* what) {
+        if (s.empty()) throw ParseError(std::string("CRC spec: empty ") + what + " field");
+        size_t pos = 0;
+        uint64_t v = 0;
+        try {
+            v = std::stoull(s, &pos, 16);
+        } catch (const std::exception&) {
+            throw ParseError("CRC spec: bad hex value '" + s + "' for " + what);
+        }
+        if (pos != s.size()) throw ParseError("CRC spec: bad hex value '" + s + "' for " + what);
+        return v;
+    };
+    pl_crc c{};
+    try {
+        size_t pos = 0;
+        c.width = std::stoi(f[0], &pos, 10);
+        if (pos != f[0].size()) throw std::invalid_argument("");
+    } catch (const std::exception&) {
+        throw ParseError("CRC spec: bad width '" + f[0] + "'");
+    }
+    c.poly = hex(f[1], "poly");
+    if (f[2] == "0") c.reflect = 0;
+    else if (f[2] == "1") c.reflect = 1;
+    else throw ParseError("CRC spec: reflect field must be 0 or 1, got '" + f[2] + "'");
+    c.init = hex(f[3], "init");
+    c.xorout = hex(f[4], "xorout");
+    return c;
+}
+
+// ---- decode tree (prune_tree.cpp:38-71) --------------------------------
+enum Kind : int { NK_BRANCH, NK_FROZEN, NK_INFO, NK_R0, NK_R1, NK_REP, NK_SPC };
+
+struct Node {
+    int kind, depth, lb, size, left, right;
+};
+
+void check_pruning(const pl_pruning& c) {
+    if (c.rep_max < 0 || c.spc_max < 0 || (c.rep_max && c.rep_max < 2) || (c.spc_max && c.spc_max < 4))
+        throw ConfigError("node size caps must be 0 (unlimited), >= 2 for repetition and >= 4 for "
+                          "single-parity");
+}
+
+int build_tree(std::vector<Node>& out, const uint8_t* frozen, int lo, int size, int depth,
+               const pl_pruning& c) {
+    const int idx = int(out.size());
+    out.push_back(Node{NK_BRANCH, depth, lo, size, -1, -1});
+    int nfrozen = 0;
+    for (int i = 0; i < size; ++i) nfrozen += frozen[lo + i] != 0;
+    int kind = NK_BRANCH;
+    if (size == 1) kind = nfrozen ? NK_FROZEN : NK_INFO;
+    else if (c.repetition && nfrozen == size - 1 && !frozen[lo + size - 1] &&
+             (c.rep_max == 0 || size <= c.rep_max))
+        kind = NK_REP;
+    else if (c.single_parity && nfrozen == 1 && frozen[lo] && (c.spc_max == 0 || size <= c.spc_max))
+        kind = NK_SPC;
+    else if (c.rate_zero && nfrozen == size) kind = NK_R0;
+    else if (c.rate_one && nfrozen == 0) kind = NK_R1;
+    out[size_t(idx)].kind = kind;
+    if (kind == NK_BRANCH && size > 1) {
+        const int l = build_tree(out, frozen, lo, size / 2, depth + 1, c);
+        const int r = build_tree(out, frozen, lo + size / 2, size / 2, depth + 1, c);
+        out[size_t(idx)].left = l;
+        out[size_t(idx)].right = r;
+    }
+    return idx;
+}
+
+int ilog2i(int v) {
+    int r = 0;
+    while ((1 << r) < v) ++r;
+    return r;
+}
+
+// list schedule: the walk of list_decoder.hpp:174-224
+void emit_list(const std::vector<Node>& t, int ni, std::vector<uint32_t>& s) {
+    const Node& nd = t[size_t(ni)];
+    const int lg = ilog2i(nd.size);
+    switch (nd.kind) {
+    case NK_BRANCH:
+        s.push_back(plb::op_pack(plb::OP_F, nd.depth, lg, nd.lb));
+        emit_list(t, nd.left, s);
+        s.push_back(plb::op_pack(plb::OP_G, nd.depth, lg, nd.lb));
+        emit_list(t, nd.right, s);
+        s.push_back(plb::op_pack(plb::OP_H, nd.depth, lg, nd.lb));
+        break;
+    case NK_FROZEN:
+    case NK_R0: s.push_back(plb::op_pack(plb::OP_FROZEN, nd.depth, lg, nd.lb)); break;
+    case NK_INFO: s.push_back(plb::op_pack(plb::OP_INFO, nd.depth, lg, nd.lb)); break;
+    case NK_R1: s.push_back(plb::op_pack(plb::OP_R1, nd.depth, lg, nd.lb)); break;
+    case NK_REP: s.push_back(plb::op_pack(plb::OP_REP, nd.depth, lg, nd.lb)); break;
+    case NK_SPC: s.push_back(plb::op_pack(plb::OP_SPC, nd.depth, lg, nd.lb)); break;
+    }
+}
+
+// unabridged recursion of sc_decoder.hpp:99-112
+void emit_sc_subtree(int depth, int m, int base, int frozen_at, std::vector<uint32_t>& s) {
+    if (m == 1) {
+        s.push_back(plb::op_pack(base == frozen_at ? plb::OP_FROZEN : plb::OP_INFO, depth, 0, base));
+        return;
+    }
+    const int lg = ilog2i(m);
+    s.push_back(plb::op_pack(plb::OP_F, depth, lg, base));
+    emit_sc_subtree(depth + 1, m / 2, base, frozen_at, s);
+    s.push_back(plb::op_pack(plb::OP_G, depth, lg, base));
+    emit_sc_subtree(depth + 1, m / 2, base + m / 2, frozen_at, s);
+    s.push_back(plb::op_pack(plb::OP_H, depth, lg, base));
+}
+
+// SC schedule: the walk of sc_decoder.hpp:58-94
+void emit_sc(const std::vector<Node>& t, int ni, std::vector<uint32_t>& s) {
+    const Node& nd = t[size_t(ni)];
+    const int lg = ilog2i(nd.size);
+    switch (nd.kind) {
+    case NK_BRANCH:
+        s.push_back(plb::op_pack(plb::OP_F, nd.depth, lg, nd.lb));
+        emit_sc(t, nd.left, s);
+        s.push_back(plb::op_pack(plb::OP_G, nd.depth, lg, nd.lb));
+        emit_sc(t, nd.right, s);
+        s.push_back(plb::op_pack(plb::OP_H, nd.depth, lg, nd.lb));
+        break;
+    case NK_FROZEN:
+    case NK_R0: s.push_back(plb::op_pack(plb::OP_FROZEN, nd.depth, lg, nd.lb)); break;
+    case NK_INFO: s.push_back(plb::op_pack(plb::OP_INFO, nd.depth, lg, nd.lb)); break;
+    case NK_R1: emit_sc_subtree(nd.depth, nd.size, nd.lb, -1, s); break;
+    case NK_SPC: emit_sc_subtree(nd.depth, nd.size, nd.lb, nd.lb, s); break;
+    case NK_REP: s.push_back(plb::op_pack(plb::OP_REP, nd.depth, lg, nd.lb)); break;
+    }
+}
+
+bool uses_list(int k) { return k != PL_KIND_SC && k != PL_KIND_SSC; }
+bool uses_crc(int k) { return k == PL_KIND_CA_SSCL || k == PL_KIND_PA_SSCL || k == PL_KIND_FA_SSCL; }
+bool adaptive(int k) { return k == PL_KIND_PA_SSCL || k == PL_KIND_FA_SSCL; }
+bool uses_pruning(int k) { return k != PL_KIND_SC && k != PL_KIND_SCL; }
+
+// Host image of one code's device tables.
+struct HostCode {
+    int n = 0, k = 0, stages = 0, psize = 0, width = 0;
+    std::vector<uint8_t> frozen;
+    std::vector<uint32_t> sched_list, sched_sc;
+    std::vector<uint16_t> info_pos;
+    std::vector<uint64_t> crc_tab;
+    uint64_t crc_c0 = 0;
+};
+
+HostCode make_host_code(const pl_code& c, const pl_decoder& dec) {
+    if (c.n < 2 || (c.n & (c.n - 1)) != 0)
+        throw ConfigError("N must be a power of two >= 2 (got " + std::to_string(c.n) + ")");
+    if (c.n > 16384) throw ConfigError("N > 16384 is not supported by the GPU decoder");
+    if (c.k < 1) throw ConfigError("K must be at least 1 (got " + std::to_string(c.k) + ")");
+    if (!c.frozen) throw ConfigError("frozen mask is null");
+    HostCode h;
+    h.n = c.n;
+    h.k = c.k;
+    h.stages = ilog2i(c.n);
+    h.frozen.assign(c.frozen, c.frozen + c.n);
+    for (auto& b : h.frozen) b = b ? 1 : 0;
+    h.width = c.crc.width;
+    std::unique_ptr<Crc> crc;
+    if (c.crc.width) crc = std::make_unique<Crc>(c.crc);
+    int open = 0;
+    for (int i = 0; i < c.n; ++i) open += h.frozen[size_t(i)] == 0;
+    if (open != c.k + h.width)
+        throw ConfigError("frozen mask leaves " + std::to_string(open) +
+                          " information positions, need K + CRC bits = " +
+                          std::to_string(c.k + h.width));
+    h.psize = c.k + h.width;
+    for (int i = 0; i < c.n; ++i)
+        if (!h.frozen[size_t(i)]) h.info_pos.push_back(uint16_t(i));
+
+    static const pl_pruning none{0, 0, 0, 0, 0, 0};
+    const pl_pruning& pc = uses_pruning(dec.kind) ? dec.pruning : none;
+    std::vector<Node> tree;
+    tree.reserve(size_t(2 * c.n));
+    build_tree(tree, h.frozen.data(), 0, c.n, 0, pc);
+    emit_list(tree, 0, h.sched_list);
+    emit_sc(tree, 0, h.sched_sc);
+
+    if (crc) {
+        // affine map: crc(m) = c0 ^ XOR_i m_i col_i over the K message bits;
+        // the tail bits enter the syndrome at their MSB-first weight
+        std::vector<uint8_t> msg(size_t(c.k), 0);
+        const uint64_t c0 = crc->compute(msg.data(), msg.size());
+        std::vector<uint64_t> colpos(size_t(c.n), 0);
+        for (int j = 0; j < c.k; ++j) {
+            msg[size_t(j)] = 1;
+            colpos[h.info_pos[size_t(j)]] = crc->compute(msg.data(), msg.size()) ^ c0;
+            msg[size_t(j)] = 0;
+        }
+        for (int j = 0; j < h.width; ++j)
+            colpos[h.info_pos[size_t(c.k + j)]] = 1ull << (h.width - 1 - j);
+        const int nbytes = (c.n + 7) / 8;
+        h.crc_tab.assign(size_t(nbytes) * 256, 0);
+        for (int j = 0; j < nbytes; ++j)
+            for (int v = 0; v < 256; ++v) {
+                uint64_t acc = 0;
+                for (int b = 0; b < 8; ++b)
+                    if (((v >> b) & 1) && 8 * j + b < c.n) acc ^= colpos[size_t(8 * j + b)];
+                h.crc_tab[size_t(j) * 256 + size_t(v)] = acc;
+            }
+        h.crc_c0 = c0;
+    }
+    return h;
+}
+
+struct RungCfg {
+    int l = 1;
+    int seg_max = 0;
+    int smem_per_warp = 0;
+    int64_t gscratch_per_warp = 0;
+    int grid = 0;
+};
+
+} // namespace
+
+struct pl_handle {
+    int device = 0;
+    pl_decoder dec{};
+    std::vector<HostCode> codes;
+    int nmax = 0;
+    int64_t pstride = 0, cstride = 0;
+    int esz = 4;
+    int sms = 0;
+    std::string err;
+    // device residency
+    std::vector<void*> allocs;
+    plb::DevCode* d_codes = nullptr;
+    void* d_gscratch = nullptr;
+    int64_t gscratch_bytes = 0;
+    RungCfg sc_cfg;
+    std::vector<RungCfg> rungs; // list rungs in ladder order
+    // per-call control buffers
+    unsigned long long* d_work = nullptr; // one counter per launch
+    int32_t* d_counts = nullptr;          // fail counts per launch
+    int32_t* d_lists[2] = {nullptr, nullptr};
+    int64_t list_cap = 0;
+    int64_t launches = 0;
+    // host staging for pl_decode_host
+    cudaStream_t s_compute = nullptr, s_h2d = nullptr, s_d2h = nullptr;
+    int64_t stage_frames = 0;
+    void* d_in[2] = {nullptr, nullptr};
+    int32_t* d_cid[2] = {nullptr, nullptr};
+    uint8_t* d_out[2] = {nullptr, nullptr};
+    void* h_stage_in[2] = {nullptr, nullptr};
+    uint8_t* h_stage_out[2] = {nullptr, nullptr};
+    cudaEvent_t ev_h2d[2]{}, ev_dec[2]{}, ev_d2h[2]{};
+
+    template <class T>
+    T* dalloc(size_t bytes) {
+        void* p = nullptr;
+        ck(cudaMalloc(&p, std::max<size_t>(bytes, 16)), "cudaMalloc");
+        allocs.push_back(p);
+        return static_cast<T*>(p);
+    }
+};
+
+namespace {
+
+int target_warps_per_sm() {
+    const char* e = std::getenv("PLB_TARGET_WARPS");
+    return e ? std::max(1, std::atoi(e)) : 24;
+}
+
+// Pick where the depth segments live: the most shared-memory-resident
+// layout that still keeps PLB_TARGET_WARPS warps resident per SM, else the
+// layout with the most resident warps.
+RungCfg plan_rung(const pl_handle& h, int l, bool list) {
+    const char* forced = std::getenv("PLB_SEGMAX");
+    const int target = target_warps_per_sm();
+    std::vector<int> cands;
+    if (forced) cands.push_back(std::atoi(forced));
+    else
+        for (int s = h.nmax; s >= 8; s >>= 1) cands.push_back(s);
+    RungCfg best;
+    best.l = l;
+    for (int seg : cands) {
+        RungCfg c;
+        c.l = l;
+        c.seg_max = seg;
+        c.smem_per_warp = int(plb::smem_bytes_per_warp(h.nmax, l, h.esz, seg));
+        c.gscratch_per_warp = plb::gscratch_bytes_per_warp(h.nmax, l, h.esz, seg);
+        const int smem = c.smem_per_warp * plb::kWarpsPerBlock;
+        const int nb = list ? plb::occupancy_list(h.dec.precision, smem)
+                            : plb::occupancy_sc(h.dec.precision, smem);
+        if (nb <= 0) continue;
+        c.grid = nb * h.sms;
+        if (c.grid > best.grid) best = c;
+        if (nb * plb::kWarpsPerBlock >= target) break;
+    }
+    if (best.grid <= 0) throw ConfigError("no launch configuration fits this code / list size on the device");
+    return best;
+}
+
+void ensure_lists(pl_handle& h, int64_t nframes) {
+    if (h.list_cap >= nframes && h.d_lists[0]) return;
+    for (int i = 0; i < 2; ++i)
+        if (h.d_lists[i]) cudaFree(h.d_lists[i]);
+    h.list_cap = std::max<int64_t>(nframes, 1024);
+    for (int i = 0; i < 2; ++i)
+        ck(cudaMalloc(&h.d_lists[i], size_t(h.list_cap) * sizeof(int32_t)), "cudaMalloc lists");
+}
+
+int fail(pl_handle* h, int code, const std::string& msg) {
+    if (h) h->err = msg;
+    g_thread_err = msg;
+    return code;
+}
+
+void run_decode(pl_handle& h, const void* llr, const int32_t* code_id, int64_t nframes,
+                uint8_t* payload, uint8_t* codeword, uint8_t* crc_ok, uint8_t* esc,
+                float* metric, cudaStream_t s) {
+    ck(cudaSetDevice(h.device), "cudaSetDevice");
+    h.launches = 0;
+    if (nframes <= 0) return;
+    const int kind = h.dec.kind;
+    const bool need_lists = adaptive(kind);
+    if (need_lists) ensure_lists(h, nframes);
+    ck(cudaMemsetAsync(h.d_work, 0, 16 * sizeof(unsigned long long), s), "memset");
+    ck(cudaMemsetAsync(h.d_counts, 0, 16 * sizeof(int32_t), s), "memset");
+
+    plb::LaunchParams base{};
+    base.codes = h.d_codes;
+    base.llr = llr;
+    base.llr_stride = h.nmax;
+    base.code_id = code_id;
+    base.nframes = nframes;
+    base.payload = payload;
+    base.payload_stride = h.pstride;
+    base.codeword = codeword;
+    base.codeword_stride = h.cstride;
+    base.crc_ok = crc_ok;
+    base.esc = esc;
+    base.metric = metric;
+    base.gscratch = h.d_gscratch;
+    base.nmax = h.nmax;
+    int slot = 0;
+
+    auto run = [&](const RungCfg& rc, bool list, int select, const int32_t* in_list,
+                   const int32_t* in_count, int32_t* out_list, int32_t* out_count) {
+        plb::LaunchParams p = base;
+        p.work = h.d_work + slot;
+        p.frame_list = in_list;
+        p.frame_count = in_count;
+        p.fail_list = out_list;
+        p.fail_count = out_count;
+        p.l = rc.l;
+        p.select_by_crc = select;
+        p.seg_smem_max = rc.seg_max;
+        p.smem_per_warp = rc.smem_per_warp;
+        p.gscratch_per_warp = rc.gscratch_per_warp;
+        p.esc_level = rc.l;
+        cudaError_t e = list ? plb::launch_list(p, h.dec.precision, rc.grid, s)
+                             : plb::launch_sc(p, h.dec.precision, rc.grid, s);
+        ck(e, list ? "list kernel launch" : "sc kernel launch");
+        ++slot;
+        ++h.launches;
+    };
+
+    switch (kind) {
+    case PL_KIND_SC:
+    case PL_KIND_SSC: run(h.sc_cfg, false, 0, nullptr, nullptr, nullptr, nullptr); break;
+    case PL_KIND_SCL:
+    case PL_KIND_SSCL: run(h.rungs.back(), true, 0, nullptr, nullptr, nullptr, nullptr); break;
+    case PL_KIND_CA_SSCL: run(h.rungs.back(), true, 1, nullptr, nullptr, nullptr, nullptr); break;
+    case PL_KIND_PA_SSCL:
+        run(h.sc_cfg, false, 0, nullptr, nullptr, h.d_lists[0], h.d_counts + 0);
+        run(h.rungs.back(), true, 1, h.d_lists[0], h.d_counts + 0, nullptr, nullptr);
+        break;
+    case PL_KIND_FA_SSCL: {
+        run(h.sc_cfg, false, 0, nullptr, nullptr, h.d_lists[0], h.d_counts + 0);
+        int cur = 0;
+        for (size_t i = 0; i < h.rungs.size(); ++i) {
+            const bool last = i + 1 == h.rungs.size();
+            run(h.rungs[i], true, 1, h.d_lists[cur], h.d_counts + i,
+                last ? nullptr : h.d_lists[cur ^ 1], last ? nullptr : h.d_counts + i + 1);
+            cur ^= 1;
+        }
+        break;
+    }
+    default: throw ConfigError("unhandled decoder variant");
+    }
+}
+
+bool is_device_ptr(const void* p) {
+    if (!p) return true;
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+bool is_pinned_host(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+} // namespace
+
+extern "C" {
+
+int pl_crc_parse(const char* text, pl_crc* out) {
+    if (!text || !out) return fail(nullptr, PL_ERR_ARG, "null argument");
+    try {
+        *out = parse_crc(text);
+        return PL_OK;
+    } catch (const std::exception& e) {
+        return fail(nullptr, PL_ERR_PARSE, e.what());
+    }
+}
+
+int pl_crc_compute(const pl_crc* spec, const uint8_t* bits, int64_t len, uint64_t* out) {
+    if (!spec || (!bits && len) || !out || len < 0) return fail(nullptr, PL_ERR_ARG, "bad argument");
+    try {
+        Crc c(*spec);
+        *out = c.compute(bits, size_t(len));
+        return PL_OK;
+    } catch (const ConfigError& e) {
+        return fail(nullptr, PL_ERR_CONFIG, e.what());
+    }
+}
+
+int32_t pl_tree_build(const uint8_t* frozen, int32_t n, const pl_pruning* cfg, int32_t* out,
+                      int32_t max_nodes) {
+    if (!frozen || !cfg || !out) return -1;
+    try {
+        if (n < 2 || (n & (n - 1)) != 0)
+            throw ConfigError("decode tree needs a power-of-two block length, got " + std::to_string(n));
+        check_pruning(*cfg);
+        std::vector<Node> t;
+        build_tree(t, frozen, 0, n, 0, *cfg);
+        if (int(t.size()) > max_nodes) return -1;
+        for (size_t i = 0; i < t.size(); ++i) {
+            const Node& nd = t[i];
+            int32_t* o = out + 6 * i;
+            o[0] = nd.kind;
+            o[1] = nd.depth;
+            o[2] = nd.lb;
+            o[3] = nd.size;
+            o[4] = nd.left;
+            o[5] = nd.right;
+        }
+        return int32_t(t.size());
+    } catch (const std::exception& e) {
+        g_thread_err = e.what();
+        return -1;
+    }
+}
+
+int pl_create(const pl_code* codes, int32_t ncodes, const pl_decoder* dec, int32_t device,
+              pl_handle** out) {
+    if (!codes || ncodes < 1 || !dec || !out) return fail(nullptr, PL_ERR_ARG, "bad argument");
+    *out = nullptr;
+    pl_handle* h = new pl_handle();
+    try {
+        h->device = device;
+        h->dec = *dec;
+        const int kind = dec->kind;
+        if (kind < PL_KIND_SC || kind > PL_KIND_FA_SSCL) throw ConfigError("unknown decoder kind");
+        if (dec->precision != PL_F32 && dec->precision != PL_I8)
+            throw ConfigError("precision must be PL_F32 or PL_I8");
+        h->esz = dec->precision == PL_F32 ? 4 : 1;
+        // FrameDecoder validation (decoders.hpp:40-55)
+        const int l = uses_list(kind) ? dec->l : 1;
+        h->dec.l = l;
+        if (adaptive(kind) && l < 2)
+            throw ConfigError("adaptive decoding needs a list limit of at least 2, got " + std::to_string(l));
+        if (uses_list(kind) && (l < 1 || (l & (l - 1)) != 0))
+            throw ConfigError("list size must be a power of two, got " + std::to_string(l));
+        if (l > 32) throw ConfigError("list sizes above 32 are not supported by the GPU decoder");
+        if (uses_pruning(kind)) check_pruning(dec->pruning);
+        for (int i = 0; i < ncodes; ++i) {
+            if (uses_crc(kind) && codes[i].crc.width == 0)
+                throw ConfigError("CRC-aided decoding needs a code with a CRC");
+            h->codes.push_back(make_host_code(codes[i], h->dec));
+        }
+        for (const auto& c : h->codes) {
+            h->nmax = std::max(h->nmax, c.n);
+            h->pstride = std::max<int64_t>(h->pstride, (c.psize + 7) / 8);
+            h->cstride = std::max<int64_t>(h->cstride, (c.n + 7) / 8);
+        }
+        // ---- device residency
+        int ndev = 0;
+        ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+        if (device < 0 || device >= ndev) throw CudaError("no such CUDA device");
+        ck(cudaSetDevice(device), "cudaSetDevice");
+        ck(cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device), "attr");
+        std::vector<plb::DevCode> dc(h->codes.size());
+        for (size_t i = 0; i < h->codes.size(); ++i) {
+            const HostCode& c = h->codes[i];
+            plb::DevCode& d = dc[i];
+            d.n = c.n;
+            d.stages = c.stages;
+            d.k = c.k;
+            d.psize = c.psize;
+            d.crc_width = c.width;
+            auto up = [&](const void* src, size_t bytes) {
+                void* p = h->dalloc<void>(bytes);
+                if (bytes) ck(cudaMemcpy(p, src, bytes, cudaMemcpyHostToDevice), "upload");
+                return p;
+            };
+            d.sched_list = static_cast<const uint32_t*>(up(c.sched_list.data(), c.sched_list.size() * 4));
+            d.sched_sc = static_cast<const uint32_t*>(up(c.sched_sc.data(), c.sched_sc.size() * 4));
+            d.nops_list = int(c.sched_list.size());
+            d.nops_sc = int(c.sched_sc.size());
+            d.info_pos = static_cast<const uint16_t*>(up(c.info_pos.data(), c.info_pos.size() * 2));
+            d.crc_tab = c.crc_tab.empty() ? nullptr
+                                          : static_cast<const uint64_t*>(up(c.crc_tab.data(), c.crc_tab.size() * 8));
+            d.crc_c0 = c.crc_c0;
+        }
+        h->d_codes = h->dalloc<plb::DevCode>(dc.size() * sizeof(plb::DevCode));
+        ck(cudaMemcpy(h->d_codes, dc.data(), dc.size() * sizeof(plb::DevCode), cudaMemcpyHostToDevice),
+           "upload codes");
+        // ---- launch plans for every pass this kind can run
+        if (!uses_list(kind) || adaptive(kind)) h->sc_cfg = plan_rung(*h, 1, false);
+        if (kind == PL_KIND_FA_SSCL)
+            for (int ll = 2; ll <= l; ll *= 2) h->rungs.push_back(plan_rung(*h, ll, true));
+        else if (uses_list(kind))
+            h->rungs.push_back(plan_rung(*h, l, true));
+        int64_t gs = 0;
+        auto acc = [&](const RungCfg& r) {
+            gs = std::max<int64_t>(gs, int64_t(r.grid) * plb::kWarpsPerBlock * r.gscratch_per_warp);
+        };
+        if (h->sc_cfg.grid) acc(h->sc_cfg);
+        for (const auto& r : h->rungs) acc(r);
+        h->gscratch_bytes = gs;
+        h->d_gscratch = h->dalloc<void>(size_t(gs));
+        h->d_work = h->dalloc<unsigned long long>(16 * sizeof(unsigned long long));
+        h->d_counts = h->dalloc<int32_t>(16 * sizeof(int32_t));
+        *out = h;
+        return PL_OK;
+    } catch (const ConfigError& e) {
+        int rc = fail(nullptr, PL_ERR_CONFIG, e.what());
+        pl_destroy(h);
+        return rc;
+    } catch (const std::exception& e) {
+        int rc = fail(nullptr, PL_ERR_CUDA, e.what());
+        pl_destroy(h);
+        return rc;
+    }
+}
+
+const char* pl_last_error(const pl_handle* h) {
+    return h ? h->err.c_str() : g_thread_err.c_str();
+}
+
+void pl_destroy(pl_handle* h) {
+    if (!h) return;
+    cudaSetDevice(h->device);
+    for (void* p : h->allocs) cudaFree(p);
+    for (int i = 0; i < 2; ++i) {
+        if (h->d_lists[i]) cudaFree(h->d_lists[i]);
+        if (h->d_in[i]) cudaFree(h->d_in[i]);
+        if (h->d_cid[i]) cudaFree(h->d_cid[i]);
+        if (h->d_out[i]) cudaFree(h->d_out[i]);
+        if (h->h_stage_in[i]) cudaFreeHost(h->h_stage_in[i]);
+        if (h->h_stage_out[i]) cudaFreeHost(h->h_stage_out[i]);
+        if (h->ev_h2d[i]) cudaEventDestroy(h->ev_h2d[i]);
+        if (h->ev_dec[i]) cudaEventDestroy(h->ev_dec[i]);
+        if (h->ev_d2h[i]) cudaEventDestroy(h->ev_d2h[i]);
+    }
+    if (h->s_compute) cudaStreamDestroy(h->s_compute);
+    if (h->s_h2d) cudaStreamDestroy(h->s_h2d);
+    if (h->s_d2h) cudaStreamDestroy(h->s_d2h);
+    delete h;
+}
+
+int64_t pl_llr_stride(const pl_handle* h) { return h ? h->nmax : 0; }
+int64_t pl_payload_stride(const pl_handle* h) { return h ? h->pstride : 0; }
+int64_t pl_codeword_stride(const pl_handle* h) { return h ? h->cstride : 0; }
+int64_t pl_last_launches(const pl_handle* h) { return h ? h->launches : 0; }
+
+int pl_decode(pl_handle* h, const void* llr, const int32_t* code_id, int64_t nframes,
+              uint8_t* payload, uint8_t* codeword, uint8_t* crc_ok, uint8_t* esc, float* metric,
+              void* stream) {
+    if (!h) return fail(nullptr, PL_ERR_ARG, "null handle");
+    if (nframes < 0 || (nframes > 0 && (!llr || !payload)))
+        return fail(h, PL_ERR_ARG, "llr and payload buffers are required");
+    if (nframes > INT32_MAX) return fail(h, PL_ERR_ARG, "too many frames in one call");
+    try {
+        run_decode(*h, llr, code_id, nframes, payload, codeword, crc_ok, esc, metric,
+                   static_cast<cudaStream_t>(stream));
+        h->err.clear();
+        return PL_OK;
+    } catch (const std::exception& e) {
+        return fail(h, PL_ERR_CUDA, e.what());
+    }
+}
+
+int pl_decode_host(pl_handle* h, const void* llr, const int32_t* code_id, int64_t nframes,
+                   uint8_t* payload, uint8_t* codeword, uint8_t* crc_ok, uint8_t* esc,
+                   float* metric) {
+    if (!h) return fail(nullptr, PL_ERR_ARG, "null handle");
+    if (nframes < 0 || (nframes > 0 && (!llr || !payload)))
+        return fail(h, PL_ERR_ARG, "llr and payload buffers are required");
+    try {
+        ck(cudaSetDevice(h->device), "cudaSetDevice");
+        if (!h->s_compute) {
+            ck(cudaStreamCreateWithFlags(&h->s_compute, cudaStreamNonBlocking), "stream");
+            ck(cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking), "stream");
+            ck(cudaStreamCreateWithFlags(&h->s_d2h, cudaStreamNonBlocking), "stream");
+            for (int i = 0; i < 2; ++i) {
+                ck(cudaEventCreateWithFlags(&h->ev_h2d[i], cudaEventDisableTiming), "event");
+                ck(cudaEventCreateWithFlags(&h->ev_dec[i], cudaEventDisableTiming), "event");
+                ck(cudaEventCreateWithFlags(&h->ev_d2h[i], cudaEventDisableTiming), "event");
+            }
+        }
+        const char* cs = std::getenv("PLB_HOST_CHUNK");
+        const int64_t chunk = cs ? std::max<int64_t>(1, std::atoll(cs)) : 65536;
+        const int64_t in_bytes = h->nmax * int64_t(h->esz);
+        // per frame output record: payload | codeword | crc | esc | metric
+        const int64_t ob_pay = h->pstride, ob_cw = codeword ? h->cstride : 0;
+        const int64_t out_rec = ob_pay + ob_cw + 1 + 1 + 4;
+        if (h->stage_frames < chunk) {
+            for (int i = 0; i < 2; ++i) {
+                if (h->d_in[i]) cudaFree(h->d_in[i]);
+                if (h->d_cid[i]) cudaFree(h->d_cid[i]);
+                if (h->d_out[i]) cudaFree(h->d_out[i]);
+                if (h->h_stage_in[i]) cudaFreeHost(h->h_stage_in[i]);
+                if (h->h_stage_out[i]) cudaFreeHost(h->h_stage_out[i]);
+                ck(cudaMalloc(&h->d_in[i], size_t(chunk * in_bytes)), "cudaMalloc");
+                ck(cudaMalloc(&h->d_cid[i], size_t(chunk) * 4), "cudaMalloc");
+                ck(cudaMalloc(&h->d_out[i], size_t(chunk * (h->pstride + h->cstride + 6) + 64)), "cudaMalloc");
+                ck(cudaMallocHost(&h->h_stage_in[i], size_t(chunk * in_bytes)), "cudaMallocHost");
+                ck(cudaMallocHost(&h->h_stage_out[i], size_t(chunk * (h->pstride + h->cstride + 6))),
+                   "cudaMallocHost");
+            }
+            h->stage_frames = chunk;
+        }
+        const bool pin_in = is_pinned_host(llr);
+        const bool pin_out = is_pinned_host(payload) && (!codeword || is_pinned_host(codeword)) &&
+                             (!crc_ok || is_pinned_host(crc_ok)) && (!esc || is_pinned_host(esc)) &&
+                             (!metric || is_pinned_host(metric));
+        const int64_t nchunks = (nframes + chunk - 1) / chunk;
+        int64_t launches = 0;
+        std::vector<int64_t> pending(2, -1);
+        auto finish_chunk = [&](int64_t c) {
+            // unpack a chunk that went through the host staging buffer
+            const int b = int(c & 1);
+            ck(cudaEventSynchronize(h->ev_d2h[b]), "sync");
+            if (pin_out) return;
+            const int64_t f0 = c * chunk, nf = std::min(chunk, nframes - f0);
+            const uint8_t* o = h->h_stage_out[b];
+            std::memcpy(payload + f0 * h->pstride, o, size_t(nf * ob_pay));
+            o += nf * ob_pay;
+            if (codeword) std::memcpy(codeword + f0 * h->cstride, o, size_t(nf * ob_cw));
+            o += nf * ob_cw;
+            if (crc_ok) std::memcpy(crc_ok + f0, o, size_t(nf));
+            o += nf;
+            if (esc) std::memcpy(esc + f0, o, size_t(nf));
+            o += nf;
+            if (metric) std::memcpy(metric + f0, o, size_t(nf) * 4);
+        };
+        for (int64_t c = 0; c < nchunks; ++c) {
+            const int b = int(c & 1);
+            const int64_t f0 = c * chunk, nf = std::min(chunk, nframes - f0);
+            if (pending[size_t(b)] >= 0) {
+                finish_chunk(pending[size_t(b)]);
+                pending[size_t(b)] = -1;
+            }
+            const char* src = static_cast<const char*>(llr) + f0 * in_bytes;
+            if (!pin_in) {
+                std::memcpy(h->h_stage_in[b], src, size_t(nf * in_bytes));
+                src = static_cast<const char*>(h->h_stage_in[b]);
+            }
+            ck(cudaStreamWaitEvent(h->s_h2d, h->ev_dec[b], 0), "wait");
+            ck(cudaMemcpyAsync(h->d_in[b], src, size_t(nf * in_bytes), cudaMemcpyHostToDevice, h->s_h2d),
+               "h2d");
+            if (code_id)
+                ck(cudaMemcpyAsync(h->d_cid[b], code_id + f0, size_t(nf) * 4, cudaMemcpyHostToDevice,
+                                   h->s_h2d),
+                   "h2d");
+            ck(cudaEventRecord(h->ev_h2d[b], h->s_h2d), "record");
+            ck(cudaStreamWaitEvent(h->s_compute, h->ev_h2d[b], 0), "wait");
+            ck(cudaStreamWaitEvent(h->s_compute, h->ev_d2h[b], 0), "wait");
+            uint8_t* o = h->d_out[b];
+            uint8_t* d_pay = o;
+            uint8_t* d_cw = codeword ? o + nf * ob_pay : nullptr;
+            uint8_t* d_ok = o + nf * (ob_pay + ob_cw);
+            uint8_t* d_esc = d_ok + nf;
+            float* d_met = reinterpret_cast<float*>(d_esc + nf);
+            // metric must be 4-byte aligned
+            const uintptr_t mis = reinterpret_cast<uintptr_t>(d_met) & 3u;
+            if (mis) d_met = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(d_met) + (4 - mis));
+            run_decode(*h, h->d_in[b], code_id ? h->d_cid[b] : nullptr, nf, d_pay, d_cw, d_ok, d_esc,
+                       d_met, h->s_compute);
+            launches += h->launches;
+            ck(cudaEventRecord(h->ev_dec[b], h->s_compute), "record");
+            ck(cudaStreamWaitEvent(h->s_d2h, h->ev_dec[b], 0), "wait");
+            auto d2h = [&](void* dst_pinned, uint8_t* dst_stage, const void* srcp, size_t bytes) {
+                void* dst = pin_out ? dst_pinned : static_cast<void*>(dst_stage);
+                ck(cudaMemcpyAsync(dst, srcp, bytes, cudaMemcpyDeviceToHost, h->s_d2h), "d2h");
+            };
+            uint8_t* st = h->h_stage_out[b];
+            d2h(payload + f0 * h->pstride, st, d_pay, size_t(nf * ob_pay));
+            st += nf * ob_pay;
+            if (codeword) d2h(codeword + f0 * h->cstride, st, d_cw, size_t(nf * ob_cw));
+            st += nf * ob_cw;
+            if (crc_ok) d2h(crc_ok + f0, st, d_ok, size_t(nf));
+            st += nf;
+            if (esc) d2h(esc + f0, st, d_esc, size_t(nf));
+            st += nf;
+            if (metric) d2h(metric + f0, st, d_met, size_t(nf) * 4);
+            ck(cudaEventRecord(h->ev_d2h[b], h->s_d2h), "record");
+            pending[size_t(b)] = c;
+        }
+        for (int b = 0; b < 2; ++b)
+            if (pending[size_t(b)] >= 0) finish_chunk(pending[size_t(b)]);
+        // finish in chunk order is not required: chunks write disjoint ranges
+        h->launches = launches;
+        h->err.clear();
+        return PL_OK;
+    } catch (const std::exception& e) {
+        return fail(h, PL_ERR_CUDA, e.what());
+    }
+}
+
+} // extern "C"

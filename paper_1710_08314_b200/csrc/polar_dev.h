@@ -1,0 +1,93 @@
+// Internal interface between the host orchestration (host.cu) and the
+// sm_100a kernels (kernels.cu).  Not part of the public ABI.
+#pragma once
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace plb {
+
+// ---- decode schedule --------------------------------------------------
+// A decode tree (prune_tree.cpp:38-71) flattened into the order the
+// reference's recursive walks visit it (list_decoder.hpp:174-224,
+// sc_decoder.hpp:58-94): a branch node emits F, <left ops>, G, <right ops>,
+// H; every other node emits one leaf op.  One op is a u32:
+//   bits  0..3  op code
+//   bits  4..7  depth d of the node (its LLRs live in depth-d segments)
+//   bits  8..11 log2(size)
+//   bits 12..27 leaf_begin
+enum Op : uint32_t {
+    OP_F = 0,      // child LLRs  <- f(left half, right half)
+    OP_G = 1,      // child LLRs  <- g(left half, right half, left psums)
+    OP_H = 2,      // psums[lb, lb+m/2) ^= psums[lb+m/2, lb+m)
+    OP_FROZEN = 3, // frozen leaf or rate-0 node
+    OP_INFO = 4,   // information leaf
+    OP_R1 = 5,     // rate-1 node (list only; SC schedules expand it)
+    OP_REP = 6,    // repetition node
+    OP_SPC = 7,    // single-parity node (list only; SC schedules expand it)
+};
+
+__host__ __device__ inline uint32_t op_pack(uint32_t op, int depth, int logm, int lb) {
+    return op | (uint32_t(depth) << 4) | (uint32_t(logm) << 8) | (uint32_t(lb) << 12);
+}
+__host__ __device__ inline int op_code(uint32_t w) { return int(w & 15u); }
+__host__ __device__ inline int op_depth(uint32_t w) { return int((w >> 4) & 15u); }
+__host__ __device__ inline int op_logm(uint32_t w) { return int((w >> 8) & 15u); }
+__host__ __device__ inline int op_lb(uint32_t w) { return int(w >> 12); }
+
+// ---- per-code device tables -------------------------------------------
+struct DevCode {
+    int32_t n, stages, k, psize, crc_width, pad;
+    const uint32_t* sched_list; // list-decoder schedule (pruned or full tree)
+    const uint32_t* sched_sc;   // SC-rung schedule (R1/SPC expanded)
+    int32_t nops_list, nops_sc;
+    const uint16_t* info_pos;   // psize open positions, ascending
+    // CRC as an affine map over the decided codeword:
+    // syndrome = crc_c0 ^ XOR_j crc_tab[j][byte_j(codeword)], zero <=> pass.
+    const uint64_t* crc_tab;    // (n/8) x 256
+    uint64_t crc_c0;
+};
+
+// ---- launch parameters ------------------------------------------------
+struct LaunchParams {
+    const DevCode* codes;
+    const void* llr;
+    int64_t llr_stride;        // elements per frame
+    const int32_t* code_id;    // nullable
+    const int32_t* frame_list; // nullable: frames [0, nframes) in order
+    const int32_t* frame_count;// device count for frame_list (nullable)
+    int64_t nframes;           // used when frame_list == nullptr
+    unsigned long long* work;  // work-claim counter (zeroed before launch)
+    int32_t* fail_list;        // nullable: CRC-failed frames appended here
+    int32_t* fail_count;
+    uint8_t* payload;
+    int64_t payload_stride;
+    uint8_t* codeword;         // nullable
+    int64_t codeword_stride;
+    uint8_t* crc_ok;           // nullable
+    uint8_t* esc;              // nullable
+    float* metric;             // nullable
+    void* gscratch;            // global spill for the large LLR segments
+    int64_t gscratch_per_warp; // bytes
+    int32_t l;                 // list size of this pass (1 for SC)
+    int32_t select_by_crc;
+    int32_t seg_smem_max;      // segments with more elements live in gscratch
+    int32_t nmax;              // largest n over the codes
+    int32_t smem_per_warp;     // bytes
+    int32_t esc_level;         // value written to esc[] by this pass
+};
+
+constexpr int kWarpsPerBlock = 4;
+
+// Bytes of shared memory / global scratch one warp needs for a pass.
+int64_t smem_bytes_per_warp(int nmax, int l, int elem_bytes, int seg_smem_max);
+int64_t gscratch_bytes_per_warp(int nmax, int l, int elem_bytes, int seg_smem_max);
+
+// Kernel launchers (kernels.cu).  Return cudaError_t of the launch.
+cudaError_t launch_sc(const LaunchParams& p, int precision, int grid, cudaStream_t s);
+cudaError_t launch_list(const LaunchParams& p, int precision, int grid, cudaStream_t s);
+// Max resident blocks per SM for a kernel at the given dynamic smem.
+int occupancy_sc(int precision, int smem_bytes);
+int occupancy_list(int precision, int smem_bytes);
+
+} // namespace plb

@@ -1,0 +1,380 @@
+"""Host-side mirror of the reference decoder API over the C ABI.
+
+Names, argument meaning and error behaviour follow the reference's C++
+interface (/root/reference/proj/include/polar/):
+
+  reference (C++)                         here (Python, over libpolar_b200.so)
+  --------------------------------------- ------------------------------------
+  CrcSpec{width,poly,reflect,init,xorout} CrcSpec (dataclass), CrcSpec.parse
+    + CrcSpec::parse   crc.hpp:16-26
+  CrcEngine::compute   crc.cpp:121-144    crc_compute
+  PruningConfig        prune_tree.hpp:25-34 PruningConfig, PruningConfig.none()
+  PruneTree            prune_tree.hpp:49-73 prune_tree() -> node array
+  make_code            code.hpp:43-45     make_code -> PolarCode
+  construct_frozen     code.hpp:55        construct_frozen (Bhattacharyya)
+  DecoderKind          decoders.hpp:10-18 DecoderKind
+  FrameDecoder<R>      decoders.hpp:37-103 FrameDecoder (batched: decode_batch;
+    ::decode(const R*) -> DecodeResult      decode() for one frame)
+  ConfigError / ParseError errors.hpp:9-21 ConfigError / ParseError
+
+The decode path has no CPU fallback: if the native library or a GPU is
+missing, constructing a FrameDecoder raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib as L
+
+
+class ConfigError(ValueError):
+    """Invalid code, decoder or tree parameters (errors.hpp:9-11)."""
+
+
+class ParseError(ValueError):
+    """Malformed option string (errors.hpp:14-16)."""
+
+
+class DeviceError(RuntimeError):
+    """CUDA failure inside the native library."""
+
+
+def _raise(rc: int, msg: str):
+    if rc == L.PL_ERR_CONFIG:
+        raise ConfigError(msg)
+    if rc == L.PL_ERR_PARSE:
+        raise ParseError(msg)
+    if rc == L.PL_ERR_ARG:
+        raise ValueError(msg)
+    raise DeviceError(msg)
+
+
+class DecoderKind(enum.IntEnum):
+    """decoders.hpp:10-18 (same order)."""
+    sc = 0
+    ssc = 1
+    scl = 2
+    sscl = 3
+    ca_sscl = 4
+    pa_sscl = 5
+    fa_sscl = 6
+
+    @property
+    def uses_list(self):
+        return self not in (DecoderKind.sc, DecoderKind.ssc)
+
+    @property
+    def uses_crc(self):
+        return self in (DecoderKind.ca_sscl, DecoderKind.pa_sscl, DecoderKind.fa_sscl)
+
+    @property
+    def adaptive(self):
+        return self in (DecoderKind.pa_sscl, DecoderKind.fa_sscl)
+
+    @property
+    def uses_pruning(self):
+        return self not in (DecoderKind.sc, DecoderKind.scl)
+
+
+class Precision(enum.IntEnum):
+    f32 = 0
+    i8 = 1
+
+
+@dataclass(frozen=True)
+class CrcSpec:
+    width: int = 32
+    poly: int = 0x04C11DB7
+    reflect: bool = True
+    init: int = 0xFFFFFFFF
+    xorout: int = 0xFFFFFFFF
+
+    @staticmethod
+    def parse(text: str) -> "CrcSpec":
+        """CrcSpec::parse (crc.cpp:42-84): preset or width:poly:reflect:init:xorout."""
+        out = L.pl_crc()
+        rc = L.lib().pl_crc_parse(text.encode(), C.byref(out))
+        if rc:
+            _raise(rc, L.last_error(None))
+        return CrcSpec(out.width, out.poly, bool(out.reflect), out.init, out.xorout)
+
+    def to_c(self) -> "L.pl_crc":
+        return L.pl_crc(self.width, int(self.reflect), self.poly, self.init, self.xorout)
+
+    def raw(self) -> str:
+        return f"{self.width}:{self.poly:x}:{int(self.reflect)}:{self.init:x}:{self.xorout:x}"
+
+
+def crc_compute(spec: CrcSpec, bits) -> int:
+    b = np.ascontiguousarray(bits, np.uint8)
+    out = C.c_uint64(0)
+    c = spec.to_c()
+    rc = L.lib().pl_crc_compute(C.byref(c), b.ctypes.data_as(C.c_void_p), b.size, C.byref(out))
+    if rc:
+        _raise(rc, L.last_error(None))
+    return int(out.value)
+
+
+@dataclass(frozen=True)
+class PruningConfig:
+    """prune_tree.hpp:25-34: 0 caps mean unlimited."""
+    rate_zero: bool = True
+    rate_one: bool = True
+    repetition: bool = True
+    single_parity: bool = True
+    rep_max: int = 0
+    spc_max: int = 4
+
+    @staticmethod
+    def none() -> "PruningConfig":
+        return PruningConfig(False, False, False, False, 0, 0)
+
+    def to_c(self) -> "L.pl_pruning":
+        return L.pl_pruning(int(self.rate_zero), int(self.rate_one), int(self.repetition),
+                            int(self.single_parity), self.rep_max, self.spc_max)
+
+    def as_tuple(self):
+        return (int(self.rate_zero), int(self.rate_one), int(self.repetition),
+                int(self.single_parity), self.rep_max, self.spc_max)
+
+
+NODE_KINDS = ("branch", "frozen", "info", "R0", "R1", "REP", "SPC")
+
+
+def prune_tree(frozen, cfg: PruningConfig = PruningConfig()) -> np.ndarray:
+    """PruneTree node array, rows (kind, depth, leaf_begin, size, left, right)."""
+    fz = np.ascontiguousarray(frozen, np.uint8)
+    n = fz.size
+    out = np.zeros((2 * n, 6), np.int32)
+    c = cfg.to_c()
+    cnt = L.lib().pl_tree_build(fz.ctypes.data_as(C.c_void_p), n, C.byref(c),
+                                out.ctypes.data_as(C.c_void_p), 2 * n)
+    if cnt < 0:
+        raise ConfigError(L.last_error(None) or "bad decode tree request")
+    return out[:cnt].copy()
+
+
+@dataclass
+class PolarCode:
+    """code.hpp:29-41 (puncturing lives in the channel, never in the decoder)."""
+    n: int
+    k: int
+    frozen: np.ndarray
+    crc: CrcSpec | None = None
+    info_pos: np.ndarray = field(default=None)
+
+    @property
+    def crc_width(self) -> int:
+        return self.crc.width if self.crc else 0
+
+    @property
+    def payload_size(self) -> int:
+        return self.k + self.crc_width
+
+    def rate(self) -> float:
+        return self.k / self.n
+
+    def to_c(self) -> "L.pl_code":
+        c = L.pl_code()
+        c.n = self.n
+        c.k = self.k
+        c.frozen = self.frozen.ctypes.data_as(C.POINTER(C.c_uint8))
+        c.crc = self.crc.to_c() if self.crc else L.pl_crc(0, 0, 0, 0, 0)
+        return c
+
+
+def make_code(n: int, k: int, frozen, crc: CrcSpec | str | None = None) -> PolarCode:
+    """make_code (code.cpp:79-126): validates N, K and the open-position count."""
+    if isinstance(crc, str):
+        crc = CrcSpec.parse(crc)
+    fz = (np.ascontiguousarray(frozen).astype(np.uint8) != 0).astype(np.uint8)
+    if n < 2 or n & (n - 1):
+        raise ConfigError(f"N must be a power of two >= 2 (got {n})")
+    if k < 1:
+        raise ConfigError(f"K must be at least 1 (got {k})")
+    if fz.size != n:
+        raise ConfigError(f"frozen mask has {fz.size} bits, code has N = {n}")
+    w = crc.width if crc else 0
+    open_ = int(n - fz.sum())
+    if open_ != k + w:
+        raise ConfigError(f"frozen mask leaves {open_} information positions, need K + CRC bits = {k + w}")
+    return PolarCode(n, k, fz, crc, np.flatnonzero(fz == 0).astype(np.int32))
+
+
+def construct_frozen(n: int, reliable: int, design_erasure: float) -> np.ndarray:
+    """construct_frozen (code.cpp:63-77), Bhattacharyya ordering."""
+    out = np.zeros(n, np.uint8)
+    rc = L.lib().pl_construct_frozen_bhat(n, reliable, design_erasure,
+                                          out.ctypes.data_as(C.c_void_p))
+    if rc:
+        raise ConfigError("bad construction request")
+    return out
+
+
+def construct_frozen_ga(n: int, reliable: int, design_ebn0_db: float, rate: float) -> np.ndarray:
+    """Gaussian-approximation construction (absent from the reference)."""
+    out = np.zeros(n, np.uint8)
+    rc = L.lib().pl_construct_frozen_ga(n, reliable, design_ebn0_db, rate,
+                                        out.ctypes.data_as(C.c_void_p))
+    if rc:
+        raise ConfigError("bad construction request")
+    return out
+
+
+def channel(code: PolarCode, ebn0_db: float, seed: int, frame0: int, nframes: int,
+            precision: str = "f32", scale: float = 0.0, nthreads: int = 0):
+    """run_frame's inputs (sim.cpp:48-51), frame-keyed like FrameRng."""
+    info = np.zeros((nframes, code.k), np.uint8)
+    dt = np.float32 if precision == "f32" else np.int8
+    llr = np.zeros((nframes, code.n), dt)
+    c = code.to_c()
+    rc = L.lib().pl_channel_generate(C.byref(c), ebn0_db, seed, frame0, nframes,
+                                     int(Precision[precision]), scale,
+                                     info.ctypes.data_as(C.c_void_p),
+                                     llr.ctypes.data_as(C.c_void_p), nthreads)
+    if rc:
+        _raise(rc, "channel generation failed")
+    return info, llr
+
+
+@dataclass
+class DecodeResult:
+    """decode_result.hpp:7-14 (payload/codeword as 0/1 numpy arrays)."""
+    codeword: np.ndarray | None
+    payload: np.ndarray
+    crc_ok: bool
+    escalation_level: int
+    metric: float
+
+
+def unpack_msb(packed: np.ndarray, nbits: int) -> np.ndarray:
+    return np.unpackbits(np.ascontiguousarray(packed, np.uint8), axis=-1)[..., :nbits]
+
+
+class FrameDecoder:
+    """FrameDecoder<R> (decoders.hpp:37-103) on the GPU, over a batch.
+
+    ``codes`` is one PolarCode or a list of them (mixed-code batches pick a
+    code per frame with ``code_id``).  ``precision`` is "f32" or "i8".
+    """
+
+    def __init__(self, codes, kind, l: int = 8, precision: str = "f32",
+                 pruning: PruningConfig = PruningConfig(), device: int = 0):
+        import torch  # device memory and streams only
+
+        self._torch = torch
+        if isinstance(codes, PolarCode):
+            codes = [codes]
+        self.codes = list(codes)
+        self.kind = DecoderKind(kind) if not isinstance(kind, str) else DecoderKind[kind]
+        self.l = l if self.kind.uses_list else 1
+        self.precision = Precision[precision] if isinstance(precision, str) else Precision(precision)
+        self.pruning = pruning
+        self.device = device
+        arr = (L.pl_code * len(self.codes))(*[c.to_c() for c in self.codes])
+        dec = L.pl_decoder(int(self.kind), l, int(self.precision), pruning.to_c())
+        h = C.c_void_p()
+        rc = L.lib().pl_create(arr, len(self.codes), C.byref(dec), device, C.byref(h))
+        if rc:
+            _raise(rc, L.last_error(None))
+        self._h = h
+        lib = L.lib()
+        self.llr_stride = int(lib.pl_llr_stride(h))
+        self.payload_stride = int(lib.pl_payload_stride(h))
+        self.codeword_stride = int(lib.pl_codeword_stride(h))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            L.lib().pl_destroy(h)
+            self._h = None
+
+    @property
+    def llr_dtype(self):
+        return self._torch.float32 if self.precision == Precision.f32 else self._torch.int8
+
+    def alloc_outputs(self, nframes: int, codeword: bool = False):
+        t = self._torch
+        dev = f"cuda:{self.device}"
+        return {
+            "payload": t.empty((nframes, self.payload_stride), dtype=t.uint8, device=dev),
+            "codeword": t.empty((nframes, self.codeword_stride), dtype=t.uint8, device=dev) if codeword else None,
+            "crc_ok": t.empty(nframes, dtype=t.uint8, device=dev),
+            "esc": t.empty(nframes, dtype=t.uint8, device=dev),
+            "metric": t.empty(nframes, dtype=t.float32, device=dev),
+        }
+
+    def decode_batch(self, llr, code_id=None, out=None, codeword: bool = False, stream=None):
+        """Decode a device-resident batch (torch CUDA tensor, frames x stride)."""
+        t = self._torch
+        assert llr.is_cuda and llr.dtype == self.llr_dtype and llr.is_contiguous()
+        nframes = llr.numel() // self.llr_stride
+        if out is None:
+            out = self.alloc_outputs(nframes, codeword)
+        ptr = lambda x: C.c_void_p(x.data_ptr()) if x is not None else None
+        if code_id is not None:
+            assert code_id.is_cuda and code_id.dtype == t.int32
+        s = stream if stream is not None else t.cuda.current_stream(self.device)
+        rc = L.lib().pl_decode(self._h, ptr(llr), ptr(code_id), nframes, ptr(out["payload"]),
+                               ptr(out.get("codeword")), ptr(out["crc_ok"]), ptr(out["esc"]),
+                               ptr(out["metric"]), C.c_void_p(s.cuda_stream))
+        if rc:
+            _raise(rc, L.last_error(self._h))
+        return out
+
+    def decode_host(self, llr: np.ndarray, code_id: np.ndarray | None = None, codeword: bool = False):
+        """Host buffers in, host buffers out (copies overlap decoding)."""
+        llr = np.ascontiguousarray(llr)
+        nframes = llr.size // self.llr_stride
+        o = {
+            "payload": np.zeros((nframes, self.payload_stride), np.uint8),
+            "codeword": np.zeros((nframes, self.codeword_stride), np.uint8) if codeword else None,
+            "crc_ok": np.zeros(nframes, np.uint8),
+            "esc": np.zeros(nframes, np.uint8),
+            "metric": np.zeros(nframes, np.float32),
+        }
+        return self.decode_host_into(llr, o, code_id)
+
+    def decode_host_into(self, llr, o, code_id=None):
+        """Same with caller-provided (ideally pinned) host buffers; accepts
+        numpy arrays or CPU torch tensors."""
+        def ptr(x):
+            if x is None:
+                return None
+            if hasattr(x, "data_ptr"):
+                return C.c_void_p(x.data_ptr())
+            return x.ctypes.data_as(C.c_void_p)
+        nframes = (llr.numel() if hasattr(llr, "numel") else llr.size) // self.llr_stride
+        if code_id is not None and not hasattr(code_id, "data_ptr"):
+            code_id = np.ascontiguousarray(code_id, np.int32)
+        rc = L.lib().pl_decode_host(self._h, ptr(llr), ptr(code_id), nframes, ptr(o["payload"]),
+                                    ptr(o.get("codeword")), ptr(o["crc_ok"]), ptr(o["esc"]),
+                                    ptr(o["metric"]))
+        if rc:
+            _raise(rc, L.last_error(self._h))
+        return o
+
+    def last_launches(self) -> int:
+        return int(L.lib().pl_last_launches(self._h))
+
+    def decode(self, llr) -> DecodeResult:
+        """One frame (reference-shaped convenience; batch for throughput)."""
+        t = self._torch
+        arr = np.ascontiguousarray(llr).reshape(1, -1)
+        x = t.zeros((1, self.llr_stride), dtype=self.llr_dtype)
+        x[:, :arr.shape[1]] = t.from_numpy(arr)
+        o = self.decode_batch(x.cuda(self.device), codeword=True)
+        t.cuda.synchronize(self.device)
+        code = self.codes[0]
+        return DecodeResult(
+            codeword=unpack_msb(o["codeword"].cpu().numpy()[0], code.n),
+            payload=unpack_msb(o["payload"].cpu().numpy()[0], code.payload_size),
+            crc_ok=bool(o["crc_ok"].item()),
+            escalation_level=int(o["esc"].item()),
+            metric=float(o["metric"].item()),
+        )
