@@ -1,0 +1,326 @@
+#!/usr/bin/env python
+"""Benchmark: decoded information throughput (Gb/s) of the B200 polar decoder.
+
+Default workload = BASELINE.json configs[1]: N=2048, K=1723 (+CRC-32 GZIP),
+GA frozen set @4.5 dB, CA-SCL L=8 with R0/R1/REP_8-/SPC4 pruning, int8 LLRs
+(x4, saturated to +-127) from BPSK-AWGN at 3.5 dB, 262 144 frames per GPU.
+One step = one decode of that batch (inputs resident in HBM for `value`;
+host buffers with the copies inside the timed region for `e2e`).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg1]
+  python bench.py --impl reference ...   # the reference's own CPU decoder
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="cfg1")
+    ap.add_argument("--frames", type=int, default=0, help="override frames per GPU")
+    ap.add_argument("--e2e-steps", type=int, default=0)
+    ap.add_argument("--cpu-sample", type=int, default=16384)
+    ap.add_argument("--ref-sample", type=int, default=16384)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--device-channel", action="store_true",
+                    help="generate LLRs on the GPU (Philox) instead of the host FrameRng")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def sample_clocks_start(gpu_index: int):
+    f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+    q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    try:
+        p = subprocess.Popen(["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={q}",
+                              "--format=csv,noheader,nounits", "-lms", "100"],
+                             stdout=f, stderr=subprocess.DEVNULL)
+    except OSError:
+        return None, f
+    return p, f
+
+
+def sample_clocks_stop(p, f):
+    if p is None:
+        return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+    p.terminate()
+    try:
+        p.wait(5)
+    except subprocess.TimeoutExpired:
+        p.kill()
+    f.flush()
+    f.seek(0)
+    rows = [r.split(",") for r in f.read().strip().splitlines() if r.strip()]
+    os.unlink(f.name)
+    sm, smax, reasons = [], None, set()
+    names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    for r in rows:
+        r = [x.strip() for x in r]
+        if len(r) < 9:
+            continue
+        try:
+            sm.append(float(r[1]))
+            smax = float(r[2])
+        except ValueError:
+            continue
+        for nm, v in zip(names, r[5:9]):
+            if v.lower().startswith("active"):
+                reasons.add(nm)
+    return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+            "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def run_reference(args):
+    """The reference's own CPU decoder (oracle/_ref: FrameDecoder<R> compiled
+    from /root/reference/proj), all host threads, bounded sample per step."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    from paper_1710_08314_b200.workload import WORKLOADS
+    wl = WORKLOADS[args.workload]
+    try:
+        from oracle import oracle as O
+        O.Reference.lib()
+    except Exception as e:  # noqa: BLE001
+        print(json.dumps({"impl": "reference", "unavailable": f"oracle/_ref not loadable: {e}"}))
+        return 0
+    import paper_1710_08314_b200 as P
+    code = wl.code()
+    nthr = os.cpu_count() or 1
+    nf = args.ref_sample
+    _, llr = O.ref_channel(code.n, code.k, code.frozen, wl.crc, wl.ebn0_db, 42, 0, nf,
+                           wl.precision, wl.scale, nthr)
+    ref = O.Reference(code.n, code.k, code.frozen, wl.crc, wl.kind, wl.l, wl.precision,
+                      wl.pruning.as_tuple())
+    for _ in range(args.warmup):
+        ref.decode(llr[: max(nthr, nf // 8)], nthr)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        ref.decode(llr, nthr)
+    dt = (time.perf_counter() - t0) / args.steps
+    gbps = code.k * nf / dt / 1e9
+    out = {
+        "impl": "reference", "metric": "decoded info throughput", "value": gbps, "unit": "Gb/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype_of(wl),
+        "data": "synthetic (reference FrameRng/encode_systematic/transmit, seed 42)",
+        "config": {**wl.describe(), "frames_per_step": nf},
+        "cpu_baseline": {"value": gbps, "unit": "Gb/s", "cores": nthr, "kind": "reference",
+                         "sample": f"{nf} frames of {wl.name} per step, FrameDecoder<R> per thread"},
+        "e2e": {"value": gbps, "unit": "Gb/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out))
+    return 0
+
+
+def dtype_of(wl):
+    return "int8" if wl.precision == "i8" else "f32"
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    ws, rank, local = dist_env()
+    import torch
+    import torch.distributed as dist
+
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    torch.cuda.set_device(local)
+    import paper_1710_08314_b200 as P
+    from paper_1710_08314_b200.workload import WORKLOADS, schedule_work
+
+    wl = WORKLOADS[args.workload]
+    F = args.frames or wl.frames
+    code = wl.code()
+    frame0 = rank * F  # weak scaling: each rank decodes its own global frame range
+    if args.device_channel:
+        info_d, llr_d = P.channel_device(code, wl.ebn0_db, 42, frame0, F, wl.precision, wl.scale, local)
+        torch.cuda.synchronize()
+        llr_h = llr_d.cpu().pin_memory()
+        info = info_d.cpu().numpy()
+    else:
+        info, llr_np = P.channel(code, wl.ebn0_db, 42, frame0, F, wl.precision, wl.scale,
+                                 max(1, (os.cpu_count() or 1) // ws))
+        llr_h = torch.from_numpy(llr_np).pin_memory()
+        llr_d = llr_h.cuda(local)
+    dec = P.FrameDecoder(code, wl.kind, wl.l, wl.precision, wl.pruning, device=local)
+    out = dec.alloc_outputs(F)
+    stream = torch.cuda.current_stream(local)
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if ws == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(max(args.warmup, 3) if args.warmup >= 0 else 3):
+        dec.decode_batch(llr_d, out=out)
+    torch.cuda.synchronize()
+
+    # ---- device-resident throughput (value), with live per-kernel timing
+    dec.profile(True)
+    kernel_ms = {}
+    launches = 0
+    clk_p, clk_f = sample_clocks_start(local)
+    barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        dec.decode_batch(llr_d, out=out)
+        launches += dec.last_launches()
+        for kd, l, ms in dec.last_kernel_ms():
+            kernel_ms.setdefault((kd, l), []).append(ms)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = sample_clocks_stop(clk_p, clk_f)
+    dec.profile(False)
+    elapsed = max_over_ranks(ev0.elapsed_time(ev1) / 1e3)
+    ms_per_step = elapsed / args.steps * 1e3
+    total_frames = F * ws
+    value = code.k * total_frames * args.steps / elapsed / 1e9
+
+    # ---- FER / escalation of the batch (sanity of the decode itself)
+    pay = out["payload"].cpu().numpy()
+    bits = np.unpackbits(pay, axis=1)[:, : code.k]
+    frame_err = (bits != info).any(1)
+    esc = out["esc"].cpu().numpy()
+
+    # ---- end to end through the public API with host buffers (pl_decode_host)
+    e2e_steps = args.e2e_steps or max(3, min(args.steps, 10))
+    host_out = {
+        "payload": torch.empty((F, dec.payload_stride), dtype=torch.uint8).pin_memory(),
+        "codeword": None,
+        "crc_ok": torch.empty(F, dtype=torch.uint8).pin_memory(),
+        "esc": torch.empty(F, dtype=torch.uint8).pin_memory(),
+        "metric": torch.empty(F, dtype=torch.float32).pin_memory(),
+    }
+    dec.decode_host_into(llr_h, host_out)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        dec.decode_host_into(llr_h, host_out)
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    e2e_value = code.k * total_frames * e2e_steps / e2e_s / 1e9
+    h2d = F * code.n * (4 if wl.precision == "f32" else 1)
+    d2h = F * (dec.payload_stride + 1 + 1 + 4)
+
+    # ---- roofline of the dominant kernel (live CUDA-event durations)
+    peaks, peak_src = measured_peaks()
+    dom = max(kernel_ms.items(), key=lambda kv: sum(kv[1]))
+    (dkind, dl), dms = dom
+    per_launch_s = float(np.mean(dms)) / 1e3
+    n_launch_frames = F if (dkind == "list" and wl.kind in ("ca_sscl", "sscl", "scl")) or dkind == "sc" \
+        else int((esc >= dl).sum())
+    esz = 4 if wl.precision == "f32" else 1
+    bytes_per_frame = code.n * esz + dec.payload_stride + 1 + 1 + 4
+    achieved_gbs = bytes_per_frame * n_launch_frames / per_launch_s / 1e9
+    ops_per_frame = schedule_work(code, wl.kind, dl, wl.pruning, sc=(dkind == "sc"))
+    sm_count = torch.cuda.get_device_properties(local).multi_processor_count
+    clk = (peaks.get("sm_max_mhz") or 1965.0) * 1e6
+    lane_peak = sm_count * 128 * clk
+    lane_achieved = ops_per_frame * n_launch_frames / per_launch_s
+    all_kernel_s = sum(sum(v) for v in kernel_ms.values()) / 1e3
+
+    result = {
+        "metric": "decoded info throughput (Gb/s) N=2048 K=1723",
+        "value": value, "unit": "Gb/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": dtype_of(wl),
+        "data": "synthetic: BPSK-AWGN frames keyed by (seed 42, global frame index), FrameRng semantics",
+        "config": {**wl.describe(), "frames_per_gpu": F, "global_frames": total_frames,
+                   "parallelism": f"frame-range shards x{ws}",
+                   "l2": "inputs larger than L2 (%.0f MB per GPU per step)" % (h2d / 1e6)},
+        "fer": float(frame_err.mean()), "esc_mean": float(esc.mean()),
+        "gpu_launches": int(launches),
+        "kernel_ms": {f"{k[0]}_L{k[1]}": float(np.mean(v)) for k, v in kernel_ms.items()},
+        "kernel_share_of_step": all_kernel_s / (elapsed if ws == 1 else elapsed),
+        "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peaks["hbm_gbs"],
+                     "unit": "GB/s", "frac": achieved_gbs / peaks["hbm_gbs"], "traffic": None,
+                     "kernel": f"decode_kernel<{dtype_of(wl)}, {dkind}> L={dl}",
+                     "bytes_per_frame": bytes_per_frame, "peak_source": peak_src},
+        "roofline_issue": {"bound": "issue", "achieved": lane_achieved / 1e9,
+                           "peak": lane_peak / 1e9, "unit": "Glane-op/s",
+                           "frac": lane_achieved / lane_peak, "ops_per_frame": ops_per_frame,
+                           "note": "element-ops E(tree,L) per SURVEY 8(d) / (SMs*128 lanes*max clock)"},
+        "clocks": clocks,
+        "e2e": {"value": e2e_value, "unit": "Gb/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "steps": e2e_steps, "api": "pl_decode_host"},
+    }
+
+    # ---- CPU baseline: the reference decoder on this box's cores (rank 0, N=1)
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        try:
+            from oracle import oracle as O
+            nthr = os.cpu_count() or 1
+            S = min(args.cpu_sample, F)
+            ref = O.Reference(code.n, code.k, code.frozen, wl.crc, wl.kind, wl.l, wl.precision,
+                              wl.pruning.as_tuple())
+            sample = llr_h[:S].numpy()
+            t0 = time.perf_counter()
+            r = ref.decode(sample, nthr)
+            dt = time.perf_counter() - t0
+            cpu_gbps = code.k * S / dt / 1e9
+            pb = (code.payload_size + 7) // 8
+            mism = ((pay[:S, :pb] != r.payload).any(1) | (out["crc_ok"].cpu().numpy()[:S] != r.crc_ok)
+                    | (esc[:S] != r.esc)
+                    | (out["metric"].cpu().numpy()[:S] != r.metric.astype(np.float32)))
+            result["cpu_baseline"] = {
+                "value": cpu_gbps, "unit": "Gb/s", "cores": nthr, "kind": "reference",
+                "sample": f"first {S} frames of the step's batch, FrameDecoder<R> per thread "
+                          f"({dt:.1f} s wall, {dt * nthr:.0f} core-s)"}
+            result["parity_vs_reference"] = {"frames": int(S), "mismatching_frames": int(mism.sum()),
+                                             "fields": "payload, crc_ok, esc, metric"}
+        except Exception as e:  # noqa: BLE001
+            result["cpu_baseline"] = {"value": None, "unit": "Gb/s", "cores": 0, "kind": "reference",
+                                      "sample": f"unavailable: {e}"}
+    if rank == 0:
+        print(json.dumps(result))
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -131,6 +131,14 @@ int pl_decode_host(pl_handle* h, const void* llr, const int32_t* code_id,
 /* Kernel launches issued by the last pl_decode / pl_decode_host call. */
 int64_t pl_last_launches(const pl_handle* h);
 
+/* Live kernel timing: with profiling enabled every launch of pl_decode is
+ * bracketed by CUDA events on its stream; pl_last_kernel_ms waits for them
+ * and writes the duration (ms) of each launch of the last pl_decode call and
+ * its kind (0 = SC pass, 1 = list pass) and list size.  Returns the number
+ * of launches written. */
+int pl_profile(pl_handle* h, int32_t enable);
+int32_t pl_last_kernel_ms(pl_handle* h, float* ms, int32_t* kind, int32_t* l, int32_t max);
+
 /* ---- host-side helpers (no GPU needed) ---------------------------------- */
 
 /* CrcSpec::parse (crc.cpp:42-84): "32-GZIP", "16-CCITT", "8" or

@@ -17,7 +17,7 @@ EXPORTS = (
     "pl_create", "pl_last_error", "pl_destroy", "pl_llr_stride", "pl_payload_stride",
     "pl_codeword_stride", "pl_decode", "pl_decode_host", "pl_last_launches", "pl_crc_parse",
     "pl_crc_compute", "pl_tree_build", "pl_construct_frozen_bhat", "pl_construct_frozen_ga",
-    "pl_channel_generate", "pl_channel_generate_device",
+    "pl_channel_generate", "pl_channel_generate_device", "pl_profile", "pl_last_kernel_ms",
 )
 
 
@@ -75,6 +75,9 @@ def lib():
     L.pl_construct_frozen_ga.argtypes = [i32, i32, C.c_double, C.c_double, vp]
     L.pl_channel_generate.argtypes = [vp, C.c_double, u64, u64, i64, i32, C.c_float, vp, vp, i32]
     L.pl_channel_generate_device.argtypes = [vp, C.c_double, u64, u64, i64, i32, C.c_float, vp, vp, vp]
+    L.pl_profile.argtypes = [vp, i32]
+    L.pl_last_kernel_ms.argtypes = [vp, vp, vp, vp, i32]
+    L.pl_last_kernel_ms.restype = i32
     _LIB = L
     return L
 

@@ -363,6 +363,10 @@ struct pl_handle {
     int32_t* d_lists[2] = {nullptr, nullptr};
     int64_t list_cap = 0;
     int64_t launches = 0;
+    // live per-launch timing (pl_profile)
+    bool profiling = false;
+    std::vector<cudaEvent_t> prof_ev; // 2 per launch slot
+    std::vector<int32_t> prof_kind, prof_l;
     // host staging for pl_decode_host
     cudaStream_t s_compute = nullptr, s_h2d = nullptr, s_d2h = nullptr;
     int64_t stage_frames = 0;
@@ -477,9 +481,22 @@ void run_decode(pl_handle& h, const void* llr, const int32_t* code_id, int64_t n
         p.smem_per_warp = rc.smem_per_warp;
         p.gscratch_per_warp = rc.gscratch_per_warp;
         p.esc_level = rc.l;
+        if (h.profiling) {
+            while (h.prof_ev.size() < size_t(2 * (slot + 1))) {
+                cudaEvent_t ev;
+                ck(cudaEventCreate(&ev), "event");
+                h.prof_ev.push_back(ev);
+            }
+            h.prof_kind.resize(size_t(slot + 1));
+            h.prof_l.resize(size_t(slot + 1));
+            h.prof_kind[size_t(slot)] = list ? 1 : 0;
+            h.prof_l[size_t(slot)] = rc.l;
+            ck(cudaEventRecord(h.prof_ev[size_t(2 * slot)], s), "record");
+        }
         cudaError_t e = list ? plb::launch_list(p, h.dec.precision, rc.grid, s)
                              : plb::launch_sc(p, h.dec.precision, rc.grid, s);
         ck(e, list ? "list kernel launch" : "sc kernel launch");
+        if (h.profiling) ck(cudaEventRecord(h.prof_ev[size_t(2 * slot + 1)], s), "record");
         ++slot;
         ++h.launches;
     };
@@ -692,6 +709,7 @@ void pl_destroy(pl_handle* h) {
         if (h->ev_dec[i]) cudaEventDestroy(h->ev_dec[i]);
         if (h->ev_d2h[i]) cudaEventDestroy(h->ev_d2h[i]);
     }
+    for (cudaEvent_t ev : h->prof_ev) cudaEventDestroy(ev);
     if (h->s_compute) cudaStreamDestroy(h->s_compute);
     if (h->s_h2d) cudaStreamDestroy(h->s_h2d);
     if (h->s_d2h) cudaStreamDestroy(h->s_d2h);
@@ -702,6 +720,27 @@ int64_t pl_llr_stride(const pl_handle* h) { return h ? h->nmax : 0; }
 int64_t pl_payload_stride(const pl_handle* h) { return h ? h->pstride : 0; }
 int64_t pl_codeword_stride(const pl_handle* h) { return h ? h->cstride : 0; }
 int64_t pl_last_launches(const pl_handle* h) { return h ? h->launches : 0; }
+
+int pl_profile(pl_handle* h, int32_t enable) {
+    if (!h) return fail(nullptr, PL_ERR_ARG, "null handle");
+    h->profiling = enable != 0;
+    return PL_OK;
+}
+
+int32_t pl_last_kernel_ms(pl_handle* h, float* ms, int32_t* kind, int32_t* l, int32_t max) {
+    if (!h || !h->profiling) return 0;
+    const int32_t n = int32_t(std::min<int64_t>(h->launches, max));
+    for (int32_t i = 0; i < n; ++i) {
+        float t = 0.f;
+        if (cudaEventSynchronize(h->prof_ev[size_t(2 * i + 1)]) != cudaSuccess ||
+            cudaEventElapsedTime(&t, h->prof_ev[size_t(2 * i)], h->prof_ev[size_t(2 * i + 1)]) != cudaSuccess)
+            return -1;
+        if (ms) ms[i] = t;
+        if (kind) kind[i] = h->prof_kind[size_t(i)];
+        if (l) l[i] = h->prof_l[size_t(i)];
+    }
+    return n;
+}
 
 int pl_decode(pl_handle* h, const void* llr, const int32_t* code_id, int64_t nframes,
               uint8_t* payload, uint8_t* codeword, uint8_t* crc_ok, uint8_t* esc, float* metric,

@@ -10,15 +10,16 @@
 // slot: lane s holds the path metric of slot s.
 //
 // LLR storage follows the reference's depth-segment stack (sc_decoder.hpp:
-// 18-20, list_decoder.hpp:45) but with lazy copies: every depth d >= 1 has
+// 18-20, list_decoder.hpp:45) with lazy path copies: every depth d >= 1 has
 // a pool of l buffers of n>>d values and each slot points at one buffer per
 // depth (bufidx[slot][d]).  Duplicating a path (list_decoder.hpp:402-423)
-// copies 16 bytes of pointers instead of up to L*n LLRs; a path that is
-// about to overwrite a depth whose buffer it shares takes a free buffer
-// first ("own").  Depth 0 is the channel frame, read in place from HBM.
-// Small segments live in shared memory, large ones in a per-warp global
-// scratch (L2-resident).  Partial sums are bit-packed, one n-bit row per
-// slot, LSB-first within 32-bit words; h becomes a word XOR.
+// copies a 16-byte pointer row instead of up to L*n LLRs.  An F or G step at
+// depth d rewrites the depth-(d+1) segment of EVERY alive path and no path
+// ever reads the old contents, so the writer of rank r simply takes buffer r:
+// no reference counts, no copy-on-write.  Depth 0 is the channel frame, read
+// in place from HBM.  Small segments live in shared memory, large ones in a
+// per-warp global scratch (L2-resident).  Partial sums are bit-packed, one
+// n-bit row per slot, LSB-first within 32-bit words; h is a word XOR.
 //
 // Bit-exactness: f/g/h, the penalty sums (sequential, index
 // order), the halving REP fold, the (value,index) two-smallest order, the
@@ -39,37 +40,47 @@ __device__ __forceinline__ unsigned lanemask_lt() {
     return r;
 }
 
-__device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) {
-    uint32_t lo = __shfl_sync(FULL, uint32_t(v), src);
-    uint32_t hi = __shfl_sync(FULL, uint32_t(v >> 32), src);
+__device__ __forceinline__ uint32_t shfl_k(uint32_t v, int src) { return __shfl_sync(FULL, v, src); }
+__device__ __forceinline__ uint64_t shfl_k(uint64_t v, int src) {
+    const uint32_t lo = __shfl_sync(FULL, uint32_t(v), src);
+    const uint32_t hi = __shfl_sync(FULL, uint32_t(v >> 32), src);
     return (uint64_t(hi) << 32) | lo;
 }
-__device__ __forceinline__ uint64_t shfl_xor64(uint64_t v, int m, int w = 32) {
-    uint32_t lo = __shfl_xor_sync(FULL, uint32_t(v), m, w);
-    uint32_t hi = __shfl_xor_sync(FULL, uint32_t(v >> 32), m, w);
+__device__ __forceinline__ uint32_t shfl_xor_k(uint32_t v, int m) { return __shfl_xor_sync(FULL, v, m); }
+__device__ __forceinline__ uint64_t shfl_xor_k(uint64_t v, int m) {
+    const uint32_t lo = __shfl_xor_sync(FULL, uint32_t(v), m);
+    const uint32_t hi = __shfl_xor_sync(FULL, uint32_t(v >> 32), m);
     return (uint64_t(hi) << 32) | lo;
 }
+template <typename K>
+__device__ __forceinline__ K kmin(K a, K b) { return a < b ? a : b; }
+template <typename K>
+__device__ __forceinline__ K kmax(K a, K b) { return a < b ? b : a; }
+
 __device__ __forceinline__ int pack_aux(int a, int b) {
     return int((uint32_t(a) & 0xffffu) | (uint32_t(b) << 16));
 }
-__device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
-__device__ __forceinline__ uint64_t umax64(uint64_t a, uint64_t b) { return a < b ? b : a; }
 
 // ---- per-representation arithmetic (llr.hpp:36-69) -------------------
+// Key: a totally ordered (value, index) pair in one integer, used for the
+// stable candidate ranking and for the two-smallest selection.
 template <typename R>
 struct Arith;
 
 template <>
 struct Arith<float> {
-    using M = float; // path-metric type
+    using M = float;      // path-metric type
+    using Key = uint64_t; // float bits << 32 | index  (value >= +0)
     static constexpr bool kFixed = false;
+    static constexpr Key kKeyMax = ~0ull;
     __device__ static M sat(M a, M b) { return a + b; }
-    // |v| as a non-negative float: abs_llr(-0.0f) is -0.0f in the reference
+    // |v| as a non-negative float: abs_llr(-0.0f) is -0.0f in the reference,
     // but every use of a magnitude is an add to a non-negative metric or a
     // (value, index) comparison, where +-0 behave identically.
     __device__ static M mag(float v) { return fabsf(v); }
-    __device__ static uint32_t key(M v) { return __float_as_uint(v); } // v >= +0
-    __device__ static M from_key(uint32_t k) { return __uint_as_float(k); }
+    __device__ static Key make_key(M v, int idx) { return (uint64_t(__float_as_uint(v)) << 32) | uint32_t(idx); }
+    __device__ static int key_idx(Key k) { return int(uint32_t(k)); }
+    __device__ static M key_val(Key k) { return __uint_as_float(uint32_t(k >> 32)); }
     __device__ static M val(float v) { return v; }
     __device__ static float f(float a, float b) {
         // min-sum (llr.hpp:55-59).  The sign comes from the sign bits, which
@@ -87,11 +98,14 @@ struct Arith<float> {
 template <>
 struct Arith<int8_t> {
     using M = int;
+    using Key = uint32_t; // value (0..127) << 16 | index
     static constexpr bool kFixed = true;
+    static constexpr Key kKeyMax = ~0u;
     __device__ static M sat(M a, M b) { return max(-127, min(127, a + b)); }
     __device__ static M mag(int v) { return abs(v); }
-    __device__ static uint32_t key(M v) { return uint32_t(v); } // v in [0, 127]
-    __device__ static M from_key(uint32_t k) { return int(k); }
+    __device__ static Key make_key(M v, int idx) { return (uint32_t(v) << 16) | uint32_t(idx); }
+    __device__ static int key_idx(Key k) { return int(k & 0xffffu); }
+    __device__ static M key_val(Key k) { return int(k >> 16); }
     __device__ static M val(int8_t v) { return int(v); }
     __device__ static int8_t f(int8_t a, int8_t b) {
         const int m = min(abs(int(a)), abs(int(b)));
@@ -117,6 +131,57 @@ template <>
 __device__ __forceinline__ float mfrom<float>(uint32_t b) { return __uint_as_float(b); }
 template <>
 __device__ __forceinline__ int mfrom<int>(uint32_t b) { return int(b); }
+
+// ---- warp bitonic sorts (ascending) -------------------------------------
+// W keys, one per lane, lanes [0, W) sorted.
+template <typename K, int W>
+__device__ __forceinline__ K bitonic_lanes(K key, int lane) {
+#pragma unroll
+    for (int size = 2; size <= W; size <<= 1) {
+#pragma unroll
+        for (int j = size >> 1; j > 0; j >>= 1) {
+            const K o = shfl_xor_k(key, j);
+            const bool asc = (lane & size) == 0;
+            const bool lower = (lane & j) == 0;
+            key = (lower == asc) ? kmin(key, o) : kmax(key, o);
+        }
+    }
+    return key;
+}
+
+// 32*C keys at sorted position s = k*32 + lane (register k of lane).
+template <typename K, int C>
+__device__ __forceinline__ void bitonic_regs(K (&key)[C], int lane) {
+    constexpr int NT = 32 * C;
+#pragma unroll
+    for (int size = 2; size <= NT; size <<= 1) {
+#pragma unroll
+        for (int j = size >> 1; j > 0; j >>= 1) {
+            if (j >= 32) {
+                const int jr = j >> 5;
+#pragma unroll
+                for (int k = 0; k < C; ++k) {
+                    const int kp = k ^ jr;
+                    if (kp > k) {
+                        const bool asc = ((k * 32 + lane) & size) == 0;
+                        const K a = key[k], b = key[kp];
+                        const K lo = kmin(a, b), hi = kmax(a, b);
+                        key[k] = asc ? lo : hi;
+                        key[kp] = asc ? hi : lo;
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < C; ++k) {
+                    const K o = shfl_xor_k(key[k], j);
+                    const bool asc = ((k * 32 + lane) & size) == 0;
+                    const bool lower = (lane & j) == 0;
+                    key[k] = (lower == asc) ? kmin(key[k], o) : kmax(key[k], o);
+                }
+            }
+        }
+    }
+}
 
 // ---- vector access of G consecutive values ----------------------------
 template <int B>
@@ -148,23 +213,13 @@ __device__ __forceinline__ void vst(R* p, const Vec<R, G>& x) {
 struct alignas(16) Fixed {
     uint8_t bufidx[32 * 16]; // [slot][depth] -> buffer index in the depth pool
     uint8_t alive_list[32];  // rank -> slot, ascending
-    int32_t ksrc[32];        // kept candidates by rank
-    int32_t kaux[32];
-    uint32_t kmet[32];
-    uint32_t met_s[32];
+    uint8_t freetab[32];     // k -> k-th free slot, ascending
+    uint32_t met_s[32];      // metric by slot (fork hand-over)
     int32_t st_i1[32], st_i2[32], st_w[32]; // per-rank node statistics
     uint32_t st_a1[32], st_a2[32];
     uint64_t pool[16];       // generic address of each depth pool
 };
 static_assert(sizeof(Fixed) % 16 == 0, "fixed area alignment");
-
-struct Layout {
-    int32_t rw;        // psum row words
-    int32_t psum_off;  // bytes, in shared memory
-    int32_t pool_off[16];
-    uint32_t in_smem;  // depths whose pool is in shared memory
-    int32_t smem_total, gmem_total;
-};
 
 __host__ __device__ inline int ilog2(int v) {
     int r = 0;
@@ -173,29 +228,40 @@ __host__ __device__ inline int ilog2(int v) {
 }
 __host__ __device__ inline int align16(int v) { return (v + 15) & ~15; }
 
-__host__ __device__ inline Layout make_layout(int n, int l, int esz, int segmax) {
-    Layout L{};
+// Shared-memory layout of one warp: Fixed | psum rows | depth pools that fit
+// (segment <= segmax values); larger segments go to the warp's global
+// scratch.  want_d selects which depth's pool offset to return.
+struct LayoutQ {
+    int32_t rw, psum_off, smem_total, gmem_total, pool_off, pool_in_smem;
+};
+__host__ __device__ inline LayoutQ layout_query(int n, int l, int esz, int segmax, int want_d) {
+    LayoutQ q{};
     int off = int(sizeof(Fixed));
-    L.rw = n >= 32 ? n / 32 : 1;
-    L.psum_off = off;
-    off = align16(off + 4 * l * L.rw);
+    q.rw = n >= 32 ? n / 32 : 1;
+    q.psum_off = off;
+    off = align16(off + 4 * l * q.rw);
     int goff = 0;
     const int stages = ilog2(n);
     for (int d = 1; d <= stages; ++d) {
         const int seg = n >> d;
         const int bytes = align16(l * seg * esz);
         if (seg <= segmax) {
-            L.pool_off[d] = off;
+            if (d == want_d) {
+                q.pool_off = off;
+                q.pool_in_smem = 1;
+            }
             off += bytes;
-            L.in_smem |= 1u << d;
         } else {
-            L.pool_off[d] = goff;
+            if (d == want_d) {
+                q.pool_off = goff;
+                q.pool_in_smem = 0;
+            }
             goff += bytes;
         }
     }
-    L.smem_total = off;
-    L.gmem_total = goff;
-    return L;
+    q.smem_total = off;
+    q.gmem_total = goff;
+    return q;
 }
 
 // ---- warp decode context ----------------------------------------------
@@ -204,47 +270,28 @@ struct Ctx {
     using A = Arith<R>;
     using M = typename A::M;
 
-    int lane, n, stages, l;
+    int lane, n, l;
     unsigned lmask;
     const R* chan;
     Fixed* fx;
     uint32_t* ps;
     int rw;
     unsigned alive; // warp-uniform alive-slot mask
-    unsigned dirty; // depths whose buffers may be shared between slots
+    int myrank;     // rank of slot `lane` among the alive slots
     M metric;       // lane s: metric of slot s
 
+    __device__ __forceinline__ R* pool(int d) const { return reinterpret_cast<R*>(fx->pool[d]); }
     __device__ __forceinline__ R* llr(int p, int d) const {
         if (d == 0) return const_cast<R*>(chan);
-        R* base = reinterpret_cast<R*>(fx->pool[d]);
-        return base + int(fx->bufidx[p * 16 + d]) * (n >> d);
+        return pool(d) + int(fx->bufidx[p * 16 + d]) * (n >> d);
     }
     __device__ __forceinline__ uint32_t* row(int p) const { return ps + p * rw; }
     __device__ __forceinline__ bool is_alive() const { return (alive >> lane) & 1u; }
 
-    __device__ void rebuild_alive_list() {
-        if (is_alive()) fx->alive_list[__popc(alive & lanemask_lt())] = uint8_t(lane);
-        __syncwarp();
-    }
-
-    // Give every alive slot an exclusive buffer at depth d1 before it is
-    // overwritten (lazy copy-on-write; contents are dead, nothing is copied).
-    __device__ void own(int d1) {
-        if (!((dirty >> d1) & 1u)) return;
-        dirty &= ~(1u << d1);
-        const bool al = is_alive();
-        const int b = al ? int(fx->bufidx[lane * 16 + d1]) : 64 + lane;
-        const unsigned same = __match_any_sync(FULL, b);
-        const bool need = al && (__ffs(same) - 1) != lane;
-        const unsigned needm = __ballot_sync(FULL, need);
-        if (needm) {
-            const unsigned used = __reduce_or_sync(FULL, al ? (1u << b) : 0u);
-            const unsigned freem = ~used & lmask;
-            if (need) {
-                const int k = __popc(needm & lanemask_lt());
-                fx->bufidx[lane * 16 + d1] = uint8_t(__fns(freem, 0, k + 1));
-            }
-        }
+    __device__ void set_alive(unsigned a) {
+        alive = a;
+        myrank = __popc(alive & lanemask_lt());
+        if (is_alive()) fx->alive_list[myrank] = uint8_t(lane);
         __syncwarp();
     }
 
@@ -283,11 +330,12 @@ template <typename R, int G, bool IS_G>
 __device__ void fg_run(Ctx<R>& cx, int d, int h, int lb, int na) {
     const int cp = h / G; // items per path, power of two
     const int lg = __ffs(cp) - 1;
+    R* const outp = cx.pool(d + 1);
     if (cp >= 32) {
         for (int r = 0; r < na; ++r) {
             const int p = cx.fx->alive_list[r];
             const R* in = cx.llr(p, d);
-            R* out = cx.llr(p, d + 1);
+            R* out = outp + r * h;
             const uint32_t* prow = cx.row(p);
 #pragma unroll 2
             for (int c = cx.lane; c < cp; c += 32) fg_item<R, G, IS_G>(in, out, prow, h, c, lb);
@@ -295,11 +343,11 @@ __device__ void fg_run(Ctx<R>& cx, int d, int h, int lb, int na) {
     } else {
         const int total = na << lg;
         for (int t = cx.lane; t < total; t += 32) {
-            const int p = cx.fx->alive_list[t >> lg];
-            fg_item<R, G, IS_G>(cx.llr(p, d), cx.llr(p, d + 1), cx.row(p), h, t & (cp - 1), lb);
+            const int r = t >> lg;
+            const int p = cx.fx->alive_list[r];
+            fg_item<R, G, IS_G>(cx.llr(p, d), outp + r * h, cx.row(p), h, t & (cp - 1), lb);
         }
     }
-    __syncwarp();
 }
 
 template <typename R, bool IS_G>
@@ -307,7 +355,8 @@ __device__ void op_fg(Ctx<R>& cx, int d, int m, int lb, int na) {
     constexpr int VE = 16 / int(sizeof(R));
     const int h = m >> 1;
     const int G = h < VE ? h : VE;
-    cx.own(d + 1);
+    // the child segment of the path of rank r goes to buffer r (see header)
+    if (cx.is_alive()) cx.fx->bufidx[cx.lane * 16 + d + 1] = uint8_t(cx.myrank);
     switch (G) {
     case 1: fg_run<R, 1, IS_G>(cx, d, h, lb, na); break;
     case 2: fg_run<R, 2, IS_G>(cx, d, h, lb, na); break;
@@ -319,6 +368,7 @@ __device__ void op_fg(Ctx<R>& cx, int d, int m, int lb, int na) {
         }
         break;
     }
+    __syncwarp();
 }
 
 // psums[lb, lb+h) ^= psums[lb+h, lb+2h) for every alive path
@@ -341,12 +391,12 @@ __device__ void op_h(Ctx<R>& cx, int m, int lb, int na) {
     __syncwarp();
 }
 
-// write `bit` over the span [lb, lb+m) of path p's psum row (whole warp)
+// write `bit` over the span [lb, lb+m) of a psum row (whole warp)
 __device__ __forceinline__ void span_fill_warp(uint32_t* row, int lb, int m, int bit, int lane) {
     if (m >= 32) {
         for (int w = lane; w < (m >> 5); w += 32) row[(lb >> 5) + w] = bit ? FULL : 0u;
     } else if (lane == 0) {
-        const uint32_t mk = (m == 32 ? FULL : ((1u << m) - 1u)) << (lb & 31);
+        const uint32_t mk = ((1u << m) - 1u) << (lb & 31);
         uint32_t* w = row + (lb >> 5);
         *w = bit ? (*w | mk) : (*w & ~mk);
     }
@@ -360,7 +410,7 @@ __device__ __forceinline__ void span_fill_lane(uint32_t* row, int lb, int m, int
 
 // Halving fold of the REP node's LLRs (sc_decoder.hpp:116-125,
 // list_decoder.hpp:282-289) for every alive path; the result of rank r goes
-// to st_a1[r].  For m > 32 the first halvings run in the path's depth-(d+1)
+// to st_a1[r].  For m > 32 the first halvings run in the rank's depth-(d+1)
 // buffer, whose contents are dead at a leaf.
 template <typename R>
 __device__ void rep_fold(Ctx<R>& cx, int d, int m, int na) {
@@ -381,11 +431,8 @@ __device__ void rep_fold(Ctx<R>& cx, int d, int m, int na) {
         }
     } else {
         for (int r = 0; r < na; ++r) {
-            const int p = cx.fx->alive_list[r];
-            const R* L = cx.llr(p, d);
-            // scratch: the depth-(d+1) buffer of this path (dead at a leaf).
-            // A shared buffer is fine: paths are folded one after another.
-            R* S = cx.llr(p, d + 1);
+            const R* L = cx.llr(cx.fx->alive_list[r], d);
+            R* S = cx.pool(d + 1) + r * (m >> 1);
             const int h = m >> 1;
             for (int i = cx.lane; i < h; i += 32) S[i] = A::store(A::sat(A::val(L[i]), A::val(L[i + h])));
             __syncwarp();
@@ -417,57 +464,60 @@ __device__ void fork_apply(Ctx<R>& cx, const typename Arith<R>::M (&cm)[CPL],
                            int kind, int lb, int m) {
     using A = Arith<R>;
     using M = typename A::M;
+    using K = typename A::Key;
     const int lane = cx.lane;
-    // 1. stable rank by (metric, emission index)
-    uint64_t key[CPL];
-    int rank[CPL];
+    // 1. stable order by (metric, emission index): a warp bitonic sort of
+    //    the unique keys leaves the candidate of rank r in lane r (register 0)
+    K key[CPL];
 #pragma unroll
     for (int k = 0; k < CPL; ++k) {
         const int i = lane + 32 * k;
-        key[k] = i < ncand ? ((uint64_t(A::key(cm[k])) << 32) | uint32_t(i)) : ~0ull;
-        rank[k] = 0;
+        key[k] = i < ncand ? A::make_key(cm[k], i) : A::kKeyMax;
     }
-#pragma unroll
-    for (int kk = 0; kk < CPL; ++kk) {
-        const int lim = min(32, ncand - 32 * kk);
-        for (int j = 0; j < lim; ++j) {
-            const uint64_t kj = shfl64(key[kk], j);
-#pragma unroll
-            for (int k = 0; k < CPL; ++k) rank[k] += kj < key[k];
-        }
+    if constexpr (CPL == 1) {
+        if (ncand <= 2) key[0] = bitonic_lanes<K, 2>(key[0], lane);
+        else if (ncand <= 4) key[0] = bitonic_lanes<K, 4>(key[0], lane);
+        else if (ncand <= 8) key[0] = bitonic_lanes<K, 8>(key[0], lane);
+        else if (ncand <= 16) key[0] = bitonic_lanes<K, 16>(key[0], lane);
+        else key[0] = bitonic_lanes<K, 32>(key[0], lane);
+    } else {
+        bitonic_regs<K, CPL>(key, lane);
     }
     const int keep = min(cx.l, ncand);
+    const bool kept = lane < keep;
+    const int ci = kept ? A::key_idx(key[0]) : 0;
+    const M cmet = A::key_val(key[0]);
+    int src = 0, aux = 0;
 #pragma unroll
     for (int k = 0; k < CPL; ++k) {
-        const int i = lane + 32 * k;
-        if (i < ncand && rank[k] < keep) {
-            cx.fx->kmet[rank[k]] = mbits<M>(cm[k]);
-            cx.fx->ksrc[rank[k]] = csrc[k];
-            cx.fx->kaux[rank[k]] = caux[k];
+        const int s = __shfl_sync(FULL, csrc[k], ci & 31);
+        const int a = __shfl_sync(FULL, caux[k], ci & 31);
+        if ((ci >> 5) == k) {
+            src = s;
+            aux = a;
         }
     }
-    __syncwarp();
-    // 2. slot assignment: first use of a slot stays, others take the next
-    //    free slot in ascending order
-    const bool kept = lane < keep;
-    const int src = kept ? cx.fx->ksrc[lane] : 64 + lane;
-    const int aux = kept ? cx.fx->kaux[lane] : 0;
+    if (!kept) src = 64 + lane;
+    // 2. slot assignment: the first use of a slot stays in place, the others
+    //    take the free slots in ascending order, in rank order
     const unsigned same = __match_any_sync(FULL, src);
     const bool first = kept && (__ffs(same) - 1) == lane;
     const unsigned surv = __reduce_or_sync(FULL, kept ? (1u << src) : 0u);
-    const unsigned freem = cx.lmask & ~surv;
     const bool dup = kept && !first;
     const unsigned dupm = __ballot_sync(FULL, dup);
     int tgt = src;
-    if (dup) tgt = int(__fns(freem, 0, __popc(dupm & lanemask_lt()) + 1));
-    // 3. duplicates: pointer rows + decided partial sums (incl. the node
-    //    span, which holds the source's hard decisions for R1/SPC)
     if (dupm) {
-        cx.dirty = FULL;
+        const unsigned freem = cx.lmask & ~surv;
+        if ((freem >> lane) & 1u) cx.fx->freetab[__popc(freem & lanemask_lt())] = uint8_t(lane);
+        __syncwarp();
         if (dup) {
+            tgt = cx.fx->freetab[__popc(dupm & lanemask_lt())];
+            // 3. duplicate: the LLR pointer row ...
             *reinterpret_cast<uint4*>(cx.fx->bufidx + tgt * 16) =
                 *reinterpret_cast<const uint4*>(cx.fx->bufidx + src * 16);
         }
+        // ... and the decided partial sums incl. the node span (which holds
+        // the source's hard decisions for R1/SPC)
         const int nw = min(cx.rw, (lb + m + 31) >> 5);
         for (unsigned mm = dupm; mm; mm &= mm - 1) {
             const int dl = __ffs(mm) - 1;
@@ -498,18 +548,17 @@ __device__ void fork_apply(Ctx<R>& cx, const typename Arith<R>::M (&cm)[CPL],
         if (ca >= 0) tr[(lb + ca) >> 5] ^= 1u << ((lb + ca) & 31);
         if (cb >= 0) tr[(lb + cb) >> 5] ^= 1u << ((lb + cb) & 31);
     }
-    if (kept) cx.fx->met_s[tgt] = cx.fx->kmet[lane];
-    cx.alive = __reduce_or_sync(FULL, kept ? (1u << tgt) : 0u);
+    if (kept) cx.fx->met_s[tgt] = mbits<M>(cmet);
+    const unsigned nal = __reduce_or_sync(FULL, kept ? (1u << tgt) : 0u);
     __syncwarp();
-    if (cx.is_alive()) cx.metric = mfrom<M>(cx.fx->met_s[lane]);
-    cx.rebuild_alive_list();
+    if ((nal >> lane) & 1u) cx.metric = mfrom<M>(cx.fx->met_s[lane]);
+    cx.set_alive(nal);
 }
 
 // base metric of the path at rank r (all lanes participate)
 template <typename R>
 __device__ __forceinline__ typename Arith<R>::M base_of(const Ctx<R>& cx, int r) {
-    const int p = cx.fx->alive_list[r];
-    return __shfl_sync(FULL, cx.metric, p);
+    return __shfl_sync(FULL, cx.metric, cx.fx->alive_list[r]);
 }
 
 // frozen leaf / rate-0 node (list_decoder.hpp:227-238)
@@ -518,15 +567,23 @@ __device__ void list_frozen(Ctx<R>& cx, int d, int m, int lb, int na) {
     using A = Arith<R>;
     using M = typename A::M;
     M pen = M(0);
-    if (cx.lane < na) {
+    if (A::kFixed && m >= 32) {
+        // saturating sums of non-negative terms are order-free in int8
+        for (int r = 0; r < na; ++r) {
+            const R* L = cx.llr(cx.fx->alive_list[r], d);
+            int s = 0;
+            for (int i = cx.lane; i < m; i += 32) s += max(0, -int(A::val(L[i])));
+            s = int(__reduce_add_sync(FULL, unsigned(s)));
+            if (cx.lane == r) pen = M(min(s, 127));
+        }
+    } else if (cx.lane < na) {
         const R* L = cx.llr(cx.fx->alive_list[cx.lane], d);
         for (int i = 0; i < m; ++i) {
             const M v = A::val(L[i]);
             if (v < M(0)) pen = A::sat(pen, -v); // sequential: float order matters
         }
     }
-    const int myrank = __popc(cx.alive & lanemask_lt());
-    const M pr = __shfl_sync(FULL, pen, myrank & 31);
+    const M pr = __shfl_sync(FULL, pen, cx.myrank & 31);
     if (cx.is_alive()) cx.metric = A::sat(cx.metric, pr);
     if (m >= 32) {
         const int W = m >> 5;
@@ -540,41 +597,24 @@ __device__ void list_frozen(Ctx<R>& cx, int d, int m, int lb, int na) {
 }
 
 // information leaf (list_decoder.hpp:240-252)
-template <typename R>
+template <typename R, int CPL>
 __device__ void list_info(Ctx<R>& cx, int d, int lb, int na) {
     using A = Arith<R>;
     using M = typename A::M;
-    const int ncand = 2 * na;
-    if (ncand <= 32) {
-        M cm[1];
-        int cs[1], cax[1];
-        const int i = cx.lane, r = min(i >> 1, na - 1), j = i & 1;
+    M cm[CPL];
+    int cs[CPL], cax[CPL];
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) {
+        const int i = cx.lane + 32 * k, r = min(i >> 1, na - 1), j = i & 1;
         const int p = cx.fx->alive_list[r];
         const M v = A::val(cx.llr(p, d)[0]);
         const M base = __shfl_sync(FULL, cx.metric, p);
         const bool hb = v < M(0);
-        const M av = A::mag(v);
-        cm[0] = A::sat(base, (j == 0) == hb ? av : M(0));
-        cs[0] = p;
-        cax[0] = pack_aux(j, -1);
-        fork_apply<R, 1>(cx, cm, cs, cax, ncand, AK_BIT, lb, 1);
-    } else {
-        M cm[2];
-        int cs[2], cax[2];
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            const int i = cx.lane + 32 * k, r = min(i >> 1, na - 1), j = i & 1;
-            const int p = cx.fx->alive_list[r];
-            const M v = A::val(cx.llr(p, d)[0]);
-            const M base = __shfl_sync(FULL, cx.metric, p);
-            const bool hb = v < M(0);
-            const M av = A::mag(v);
-            cm[k] = A::sat(base, (j == 0) == hb ? av : M(0));
-            cs[k] = p;
-            cax[k] = pack_aux(j, -1);
-        }
-        fork_apply<R, 2>(cx, cm, cs, cax, ncand, AK_BIT, lb, 1);
+        cm[k] = A::sat(base, (j == 0) == hb ? A::mag(v) : M(0));
+        cs[k] = p;
+        cax[k] = pack_aux(j, -1);
     }
+    fork_apply<R, CPL>(cx, cm, cs, cax, 2 * na, AK_BIT, lb, 1);
     cx.normalize();
 }
 
@@ -585,6 +625,7 @@ template <typename R>
 __device__ void r1spc_stats(Ctx<R>& cx, int d, int m, int lb, int na) {
     using A = Arith<R>;
     using M = typename A::M;
+    using K = typename A::Key;
     if (m < 32) {
         const int lgm = __ffs(m) - 1;
         const int per = 32 >> lgm;
@@ -594,12 +635,12 @@ __device__ void r1spc_stats(Ctx<R>& cx, int d, int m, int lb, int na) {
             const int p = cx.fx->alive_list[ok ? r : 0];
             const M v = ok ? A::val(cx.llr(p, d)[i]) : M(0);
             const unsigned hb = __ballot_sync(FULL, ok && v < M(0));
-            uint64_t k1 = ok ? ((uint64_t(A::key(A::mag(v))) << 32) | uint32_t(i)) : ~0ull;
-            uint64_t k2 = ~0ull;
+            K k1 = ok ? A::make_key(A::mag(v), i) : A::kKeyMax;
+            K k2 = A::kKeyMax;
             for (int off = 1; off < m; off <<= 1) {
-                const uint64_t o1 = shfl_xor64(k1, off), o2 = shfl_xor64(k2, off);
-                const uint64_t n1 = umin64(k1, o1);
-                k2 = umin64(umax64(k1, o1), umin64(k2, o2));
+                const K o1 = shfl_xor_k(k1, off), o2 = shfl_xor_k(k2, off);
+                const K n1 = kmin(k1, o1);
+                k2 = kmin(kmax(k1, o1), kmin(k2, o2));
                 k1 = n1;
             }
             if (ok && i == 0) {
@@ -607,10 +648,10 @@ __device__ void r1spc_stats(Ctx<R>& cx, int d, int m, int lb, int na) {
                 uint32_t* w = cx.row(p) + (lb >> 5);
                 const uint32_t mk = ((1u << m) - 1u) << (lb & 31);
                 *w = (*w & ~mk) | (bits << (lb & 31));
-                cx.fx->st_i1[r] = int(uint32_t(k1));
-                cx.fx->st_i2[r] = int(uint32_t(k2));
-                cx.fx->st_a1[r] = mbits<M>(A::from_key(uint32_t(k1 >> 32)));
-                cx.fx->st_a2[r] = mbits<M>(A::from_key(uint32_t(k2 >> 32)));
+                cx.fx->st_i1[r] = A::key_idx(k1);
+                cx.fx->st_i2[r] = A::key_idx(k2);
+                cx.fx->st_a1[r] = mbits<M>(A::key_val(k1));
+                cx.fx->st_a2[r] = mbits<M>(A::key_val(k2));
                 cx.fx->st_w[r] = __popc(bits) & 1;
             }
         }
@@ -619,7 +660,7 @@ __device__ void r1spc_stats(Ctx<R>& cx, int d, int m, int lb, int na) {
             const int p = cx.fx->alive_list[r];
             const R* L = cx.llr(p, d);
             uint32_t* w = cx.row(p) + (lb >> 5);
-            uint64_t k1 = ~0ull, k2 = ~0ull;
+            K k1 = A::kKeyMax, k2 = A::kKeyMax;
             int par = 0;
             for (int k = 0; k < (m >> 5); ++k) {
                 const int i = (k << 5) + cx.lane;
@@ -627,7 +668,7 @@ __device__ void r1spc_stats(Ctx<R>& cx, int d, int m, int lb, int na) {
                 const unsigned hb = __ballot_sync(FULL, v < M(0));
                 if (cx.lane == 0) w[k] = hb;
                 par ^= __popc(hb) & 1;
-                const uint64_t kv = (uint64_t(A::key(A::mag(v))) << 32) | uint32_t(i);
+                const K kv = A::make_key(A::mag(v), i);
                 if (kv < k1) {
                     k2 = k1;
                     k1 = kv;
@@ -636,16 +677,16 @@ __device__ void r1spc_stats(Ctx<R>& cx, int d, int m, int lb, int na) {
                 }
             }
             for (int off = 1; off < 32; off <<= 1) {
-                const uint64_t o1 = shfl_xor64(k1, off), o2 = shfl_xor64(k2, off);
-                const uint64_t n1 = umin64(k1, o1);
-                k2 = umin64(umax64(k1, o1), umin64(k2, o2));
+                const K o1 = shfl_xor_k(k1, off), o2 = shfl_xor_k(k2, off);
+                const K n1 = kmin(k1, o1);
+                k2 = kmin(kmax(k1, o1), kmin(k2, o2));
                 k1 = n1;
             }
             if (cx.lane == 0) {
-                cx.fx->st_i1[r] = int(uint32_t(k1));
-                cx.fx->st_i2[r] = int(uint32_t(k2));
-                cx.fx->st_a1[r] = mbits<M>(A::from_key(uint32_t(k1 >> 32)));
-                cx.fx->st_a2[r] = mbits<M>(A::from_key(uint32_t(k2 >> 32)));
+                cx.fx->st_i1[r] = A::key_idx(k1);
+                cx.fx->st_i2[r] = A::key_idx(k2);
+                cx.fx->st_a1[r] = mbits<M>(A::key_val(k1));
+                cx.fx->st_a2[r] = mbits<M>(A::key_val(k2));
                 cx.fx->st_w[r] = par;
             }
         }
@@ -717,11 +758,26 @@ template <typename R, int CPL>
 __device__ void list_rep_cands(Ctx<R>& cx, int d, int lb, int m, int na) {
     using A = Arith<R>;
     using M = typename A::M;
-    // pen_w: sequential sum of the disagreeing magnitudes
-    if (cx.lane < na) {
+    // pen_w: sum of the magnitudes that disagree with the fold's decision,
+    // sequential in index order (float order matters; int8 is order-free)
+    if (A::kFixed && m >= 32) {
+        for (int r = 0; r < na; ++r) {
+            const R* L = cx.llr(cx.fx->alive_list[r], d);
+            const bool w = mfrom<M>(cx.fx->st_a1[r]) < M(0);
+            int s = 0;
+            for (int i = cx.lane; i < m; i += 32) {
+                const int v = int(A::val(L[i]));
+                if (w ? (v > 0) : (v < 0)) s += abs(v);
+            }
+            s = int(__reduce_add_sync(FULL, unsigned(s)));
+            if (cx.lane == 0) {
+                cx.fx->st_w[r] = w;
+                cx.fx->st_a2[r] = mbits<M>(M(min(s, 127)));
+            }
+        }
+    } else if (cx.lane < na) {
         const R* L = cx.llr(cx.fx->alive_list[cx.lane], d);
-        const M s = mfrom<M>(cx.fx->st_a1[cx.lane]);
-        const bool w = s < M(0);
+        const bool w = mfrom<M>(cx.fx->st_a1[cx.lane]) < M(0);
         M pen = M(0);
         for (int i = 0; i < m; ++i) {
             const M v = A::val(L[i]);
@@ -761,7 +817,7 @@ __device__ uint64_t row_syndrome(const DevCode& C, const uint32_t* row, int lane
         syn ^= __ldg(C.crc_tab + (size_t(j) << 8) + byte);
     }
 #pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) syn ^= shfl_xor64(syn, off);
+    for (int off = 16; off >= 1; off >>= 1) syn ^= shfl_xor_k(syn, off);
     return syn ^ C.crc_c0;
 }
 
@@ -802,25 +858,19 @@ __device__ void setup_ctx(Ctx<R>& cx, const LaunchParams& P, const DevCode& C,
                           unsigned char* sm, unsigned char* gs, int frame, int lane, int l) {
     cx.lane = lane;
     cx.n = C.n;
-    cx.stages = C.stages;
     cx.l = l;
     cx.lmask = l >= 32 ? FULL : ((1u << l) - 1u);
     cx.chan = static_cast<const R*>(P.llr) + int64_t(frame) * P.llr_stride;
     cx.fx = reinterpret_cast<Fixed*>(sm);
-    const Layout Ly = make_layout(C.n, l, int(sizeof(R)), P.seg_smem_max);
-    cx.ps = reinterpret_cast<uint32_t*>(sm + Ly.psum_off);
-    cx.rw = Ly.rw;
-    if (lane >= 1 && lane <= C.stages) {
-        unsigned char* base = ((Ly.in_smem >> lane) & 1u) ? sm : gs;
-        cx.fx->pool[lane] = reinterpret_cast<uint64_t>(base + Ly.pool_off[lane]);
-    }
+    const LayoutQ q = layout_query(C.n, l, int(sizeof(R)), P.seg_smem_max, lane);
+    cx.ps = reinterpret_cast<uint32_t*>(sm + q.psum_off);
+    cx.rw = q.rw;
+    if (lane >= 1 && lane <= C.stages)
+        cx.fx->pool[lane] = reinterpret_cast<uint64_t>((q.pool_in_smem ? sm : gs) + q.pool_off);
     if (lane == 0) *reinterpret_cast<uint4*>(cx.fx->bufidx) = make_uint4(0, 0, 0, 0);
-    __syncwarp();
-    cx.alive = 1u;
-    cx.dirty = 0u;
     cx.metric = typename Arith<R>::M(0);
-    if (lane == 0) cx.fx->alive_list[0] = 0;
     __syncwarp();
+    cx.set_alive(1u);
 }
 
 __device__ __forceinline__ long long claim(const LaunchParams& P, int lane) {
@@ -848,7 +898,10 @@ __device__ void list_frame(const LaunchParams& P, const DevCode& C, unsigned cha
         case OP_G: op_fg<R, true>(cx, d, m, lb, na); break;
         case OP_H: op_h(cx, m, lb, na); break;
         case OP_FROZEN: list_frozen(cx, d, m, lb, na); break;
-        case OP_INFO: list_info(cx, d, lb, na); break;
+        case OP_INFO:
+            if (2 * na <= 32) list_info<R, 1>(cx, d, lb, na);
+            else list_info<R, 2>(cx, d, lb, na);
+            break;
         case OP_R1:
             r1spc_stats(cx, d, m, lb, na);
             if (4 * na <= 32) list_r1_cands<R, 1>(cx, lb, m, na);
@@ -872,12 +925,12 @@ __device__ void list_frame(const LaunchParams& P, const DevCode& C, unsigned cha
         }
     }
     // finish (list_decoder.hpp:457-502): stable order by (metric, slot)
-    const bool al = cx.is_alive();
-    const uint64_t okey = al ? ((uint64_t(A::key(cx.metric)) << 32) | uint32_t(lane)) : ~0ull;
-    uint64_t best = okey;
+    using K = typename A::Key;
+    const K okey = cx.is_alive() ? A::make_key(cx.metric, lane) : A::kKeyMax;
+    K best = okey;
 #pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) best = umin64(best, shfl_xor64(best, off));
-    int pick = int(uint32_t(best));
+    for (int off = 16; off >= 1; off >>= 1) best = kmin(best, shfl_xor_k(best, off));
+    int pick = A::key_idx(best);
     int crc_ok = 0;
     if (C.crc_width > 0) {
         if (row_syndrome(C, cx.row(pick), lane) == 0) {
@@ -889,10 +942,10 @@ __device__ void list_frame(const LaunchParams& P, const DevCode& C, unsigned cha
                 if (row_syndrome(C, cx.row(s), lane) == 0) passm |= 1u << s;
             }
             if (passm) {
-                uint64_t bk = ((passm >> lane) & 1u) ? okey : ~0ull;
+                K bk = ((passm >> lane) & 1u) ? okey : A::kKeyMax;
 #pragma unroll
-                for (int off = 16; off >= 1; off >>= 1) bk = umin64(bk, shfl_xor64(bk, off));
-                pick = int(uint32_t(bk));
+                for (int off = 16; off >= 1; off >>= 1) bk = kmin(bk, shfl_xor_k(bk, off));
+                pick = A::key_idx(bk);
                 crc_ok = 1;
             }
         }
@@ -996,10 +1049,10 @@ int occupancy(int smem) {
 } // namespace
 
 int64_t smem_bytes_per_warp(int nmax, int l, int elem_bytes, int seg_smem_max) {
-    return make_layout(nmax, l, elem_bytes, seg_smem_max).smem_total;
+    return layout_query(nmax, l, elem_bytes, seg_smem_max, 0).smem_total;
 }
 int64_t gscratch_bytes_per_warp(int nmax, int l, int elem_bytes, int seg_smem_max) {
-    return make_layout(nmax, l, elem_bytes, seg_smem_max).gmem_total;
+    return layout_query(nmax, l, elem_bytes, seg_smem_max, 0).gmem_total;
 }
 
 cudaError_t launch_sc(const LaunchParams& p, int precision, int grid, cudaStream_t s) {

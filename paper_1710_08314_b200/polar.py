@@ -226,6 +226,26 @@ def construct_frozen_ga(n: int, reliable: int, design_ebn0_db: float, rate: floa
     return out
 
 
+def channel_device(code: PolarCode, ebn0_db: float, seed: int, frame0: int, nframes: int,
+                   precision: str = "f32", scale: float = 0.0, device: int = 0, with_info=True):
+    """Device-side channel (Philox, statistically equivalent to ``channel``)."""
+    import torch
+
+    dev = f"cuda:{device}"
+    dt = torch.float32 if precision == "f32" else torch.int8
+    llr = torch.empty((nframes, code.n), dtype=dt, device=dev)
+    info = torch.empty((nframes, code.k), dtype=torch.uint8, device=dev) if with_info else None
+    c = code.to_c()
+    s = torch.cuda.current_stream(device)
+    rc = L.lib().pl_channel_generate_device(
+        C.byref(c), ebn0_db, seed, frame0, nframes, int(Precision[precision]), scale,
+        C.c_void_p(info.data_ptr()) if info is not None else None, C.c_void_p(llr.data_ptr()),
+        C.c_void_p(s.cuda_stream))
+    if rc:
+        _raise(rc, "device channel generation failed")
+    return info, llr
+
+
 def channel(code: PolarCode, ebn0_db: float, seed: int, frame0: int, nframes: int,
             precision: str = "f32", scale: float = 0.0, nthreads: int = 0):
     """run_frame's inputs (sim.cpp:48-51), frame-keyed like FrameRng."""
@@ -361,6 +381,20 @@ class FrameDecoder:
 
     def last_launches(self) -> int:
         return int(L.lib().pl_last_launches(self._h))
+
+    def profile(self, enable: bool = True):
+        """Bracket every kernel launch with CUDA events (pl_profile)."""
+        L.lib().pl_profile(self._h, int(enable))
+
+    def last_kernel_ms(self):
+        """[(kind 'sc'|'list', l, ms)] for each launch of the last decode."""
+        ms = (C.c_float * 64)()
+        kd = (C.c_int32 * 64)()
+        ll = (C.c_int32 * 64)()
+        n = L.lib().pl_last_kernel_ms(self._h, ms, kd, ll, 64)
+        if n < 0:
+            raise DeviceError("kernel timing failed")
+        return [("list" if kd[i] else "sc", int(ll[i]), float(ms[i])) for i in range(n)]
 
     def decode(self, llr) -> DecodeResult:
         """One frame (reference-shaped convenience; batch for throughput)."""

@@ -1,0 +1,99 @@
+#!/usr/bin/env python
+"""Summarise an ncu report of decode_kernel into markdown (for profiles/).
+
+  python profiles/summarize.py gpurun_out/prof.ncu-rep [--frames F] > profiles/rNN_xxx.md
+
+Reads the key SOL / occupancy / issue metrics from the details page and
+aggregates the source page (instructions executed, warp-stall samples) by
+CUDA source line, so the hot lines are visible without the GUI.
+"""
+import argparse
+import collections
+import csv
+import io
+import subprocess
+
+KEYS = [
+    "Duration", "Executed Instructions", "Executed Ipc Active", "Issue Slots Busy",
+    "Warp Cycles Per Issued Instruction", "Achieved Occupancy", "Theoretical Occupancy",
+    "Registers Per Thread", "Dynamic Shared Memory Per Block", "Block Limit Shared Mem",
+    "Compute (SM) Throughput", "DRAM Throughput", "Memory Throughput", "L1/TEX Hit Rate",
+    "L2 Hit Rate", "Mem Busy", "Avg. Active Threads Per Warp", "Grid Size",
+]
+
+
+def ncu(args):
+    return subprocess.run(["ncu", *args], capture_output=True, text=True).stdout
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("rep")
+    ap.add_argument("--frames", type=int, default=0)
+    ap.add_argument("--top", type=int, default=30)
+    a = ap.parse_args()
+    det = list(csv.reader(io.StringIO(ncu(["-i", a.rep, "--page", "details", "--csv"]))))
+    hdr = det[0]
+    mi, vi, ui = hdr.index("Metric Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    ki = hdr.index("Kernel Name")
+    print(f"# ncu summary: `{a.rep}`\n")
+    print(f"kernel: `{det[1][ki]}`\n")
+    print("| metric | value | unit |\n|---|---|---|")
+    seen = set()
+    for r in det[1:]:
+        if r[mi] in KEYS and r[mi] not in seen:
+            seen.add(r[mi])
+            print(f"| {r[mi]} | {r[vi]} | {r[ui]} |")
+            if r[mi] == "Executed Instructions" and a.frames:
+                v = float(r[vi].replace(",", ""))
+                print(f"| warp-instructions per frame | {v / a.frames:.0f} | inst |")
+    raw = list(csv.reader(io.StringIO(ncu(["-i", a.rep, "--page", "raw", "--csv"]))))
+    if len(raw) > 2:
+        names = raw[0]
+        vals = raw[2]
+        want = ["dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum",
+                "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+                "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+                "smsp__inst_executed.sum", "sm__warps_active.avg.pct_of_peak_sustained_active"]
+        print()
+        for w in want:
+            if w in names:
+                print(f"- `{w}` = {vals[names.index(w)]} {raw[1][names.index(w)]}")
+    src = list(csv.reader(io.StringIO(ncu(["-i", a.rep, "--page", "source", "--csv",
+                                            "--print-source", "cuda,sass"]))))
+    agg = collections.defaultdict(lambda: [0.0, 0.0])
+    text = {}
+    hdr = None
+    cur = None
+    fname = ""
+    for r in src:
+        if r and r[0] == "File Path":
+            fname = r[1].split("/")[-1]
+        if r and r[0] == "Line No":
+            hdr = r
+            ie = hdr.index("Instructions Executed")
+            ss = hdr.index("Warp Stall Sampling (All Samples)")
+            continue
+        if hdr is None or len(r) < len(hdr):
+            continue
+        if r[0].isdigit():
+            cur = (fname, int(r[0]))
+            text[cur] = r[1]
+        try:
+            agg[cur][0] += float(r[ie] or 0)
+            agg[cur][1] += float(r[ss] or 0)
+        except ValueError:
+            pass
+    ti = sum(v[0] for v in agg.values()) or 1
+    ts = sum(v[1] for v in agg.values()) or 1
+    print(f"\n## hot source lines (by warp-stall samples)\n")
+    print("| file:line | inst % | stall % | source |\n|---|---|---|---|")
+    for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1])[: a.top]:
+        if k is None:
+            continue
+        s = text.get(k, "").strip().replace("|", "\\|")[:80]
+        print(f"| {k[0]}:{k[1]} | {v[0] / ti * 100:.1f} | {v[1] / ts * 100:.1f} | `{s}` |")
+
+
+if __name__ == "__main__":
+    main()
