@@ -137,6 +137,11 @@ int64_t pl_last_launches(const pl_handle* h);
  * its kind (0 = SC pass, 1 = list pass) and list size.  Returns the number
  * of launches written. */
 int pl_profile(pl_handle* h, int32_t enable);
+
+/* Device self-test of the packed int8 f/g kernels against their scalar
+ * definitions (llr.hpp:55-69), every operand pair: writes the mismatch
+ * count (0 expected). */
+int pl_kernel_selftest(int32_t device, uint64_t* mismatches);
 int32_t pl_last_kernel_ms(pl_handle* h, float* ms, int32_t* kind, int32_t* l, int32_t max);
 
 /* ---- host-side helpers (no GPU needed) ---------------------------------- */

@@ -721,6 +721,16 @@ int64_t pl_payload_stride(const pl_handle* h) { return h ? h->pstride : 0; }
 int64_t pl_codeword_stride(const pl_handle* h) { return h ? h->cstride : 0; }
 int64_t pl_last_launches(const pl_handle* h) { return h ? h->launches : 0; }
 
+int pl_kernel_selftest(int32_t device, uint64_t* mismatches) {
+    if (!mismatches) return fail(nullptr, PL_ERR_ARG, "null argument");
+    if (cudaSetDevice(device) != cudaSuccess) return fail(nullptr, PL_ERR_CUDA, "no such CUDA device");
+    unsigned long long m = 0;
+    const cudaError_t e = plb::kernel_selftest(&m);
+    if (e != cudaSuccess) return fail(nullptr, PL_ERR_CUDA, cudaGetErrorString(e));
+    *mismatches = m;
+    return PL_OK;
+}
+
 int pl_profile(pl_handle* h, int32_t enable) {
     if (!h) return fail(nullptr, PL_ERR_ARG, "null handle");
     h->profiling = enable != 0;

@@ -119,6 +119,40 @@ struct Arith<int8_t> {
     __device__ static float to_float(M v) { return float(v); }
 };
 
+// ---- int8 f / g on four packed values (SWAR) ---------------------------
+// Bit-exact with Arith<int8_t>::f / ::g for operands in [-127, 127]; checked
+// exhaustively by pl_kernel_selftest.
+// f: |x| = absdiff_u8(x ^ 0x80, 0x80); min(p, q) = (p + q - |p - q|) / 2
+// (bytes <= 127: no carries); the result is negated (two's complement, no
+// carry for m >= 1) where the operand signs differ and m != 0.
+// PRMT with the selector's sign-replicate bit (__byte_perm masks it away)
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+    return d;
+}
+__device__ __forceinline__ uint32_t f_swar(uint32_t a, uint32_t b) {
+    const uint32_t aa = __vabsdiffu4(a ^ 0x80808080u, 0x80808080u);
+    const uint32_t ab = __vabsdiffu4(b ^ 0x80808080u, 0x80808080u);
+    const uint32_t m = (((aa + ab) - __vabsdiffu4(aa, ab)) >> 1) & 0x7f7f7f7fu;
+    const uint32_t sp = (a ^ b) & (m + 0x7f7f7f7fu) & 0x80808080u;
+    return (m ^ prmt(sp, 0, 0xba98)) + (sp >> 7);
+}
+// g in two 16x2 halves: sign-extend, b + (s ? -a : a), clamp to [-127, 127]
+// (the reference clamps to the symmetric range, llr.hpp:61-69), repack.
+// s4 = the four partial-sum bits, element i in bit i.
+__device__ __forceinline__ uint32_t g_swar(uint32_t a, uint32_t b, uint32_t s4) {
+    const uint32_t al = prmt(a, 0, 0x9180), ah = prmt(a, 0, 0xb3a2);
+    const uint32_t bl = prmt(b, 0, 0x9180), bh = prmt(b, 0, 0xb3a2);
+    const uint32_t t = ((s4 * 0x00204081u) & 0x01010101u) << 7; // bit 7 of byte i = s_i
+    const uint32_t ml = prmt(t, 0, 0x9988), mh = prmt(t, 0, 0xbbaa);
+    uint32_t vl = __vadd2(__vadd2(al ^ ml, bl), ml & 0x00010001u);
+    uint32_t vh = __vadd2(__vadd2(ah ^ mh, bh), mh & 0x00010001u);
+    vl = __vmins2(__vmaxs2(vl, 0xff81ff81u), 0x007f007fu);
+    vh = __vmins2(__vmaxs2(vh, 0xff81ff81u), 0x007f007fu);
+    return __byte_perm(vl, vh, 0x6420);
+}
+
 template <typename M>
 __device__ __forceinline__ uint32_t mbits(M v);
 template <>
@@ -239,7 +273,9 @@ __host__ __device__ inline LayoutQ layout_query(int n, int l, int esz, int segma
     int off = int(sizeof(Fixed));
     q.rw = n >= 32 ? n / 32 : 1;
     q.psum_off = off;
-    off = align16(off + 4 * l * q.rw);
+    // rows at an odd word stride: the same word of different slots' rows
+    // falls into different banks
+    off = align16(off + 4 * l * (q.rw | 1));
     int goff = 0;
     const int stages = ilog2(n);
     for (int d = 1; d <= stages; ++d) {
@@ -285,7 +321,7 @@ struct Ctx {
         if (d == 0) return const_cast<R*>(chan);
         return pool(d) + int(fx->bufidx[p * 16 + d]) * (n >> d);
     }
-    __device__ __forceinline__ uint32_t* row(int p) const { return ps + p * rw; }
+    __device__ __forceinline__ uint32_t* row(int p) const { return ps + p * (rw | 1); }
     __device__ __forceinline__ bool is_alive() const { return (alive >> lane) & 1u; }
 
     __device__ void set_alive(unsigned a) {
@@ -314,7 +350,21 @@ __device__ __forceinline__ void fg_item(const R* in, R* out, const uint32_t* pro
     const Vec<R, G> a = vld<R, G>(in + c * G);
     const Vec<R, G> b = vld<R, G>(in + h + c * G);
     Vec<R, G> o;
-    if constexpr (IS_G) {
+    if constexpr (A::kFixed && G >= 4) {
+        constexpr int W = G / 4;
+        const uint32_t* aw = reinterpret_cast<const uint32_t*>(&a.raw);
+        const uint32_t* bw = reinterpret_cast<const uint32_t*>(&b.raw);
+        uint32_t* ow = reinterpret_cast<uint32_t*>(&o.raw);
+        if constexpr (IS_G) {
+            const int pos = lb + c * G;
+            const uint32_t bits = prow[pos >> 5] >> (pos & 31);
+#pragma unroll
+            for (int w = 0; w < W; ++w) ow[w] = g_swar(aw[w], bw[w], (bits >> (4 * w)) & 15u);
+        } else {
+#pragma unroll
+            for (int w = 0; w < W; ++w) ow[w] = f_swar(aw[w], bw[w]);
+        }
+    } else if constexpr (IS_G) {
         const int pos = lb + c * G;
         const uint32_t bits = prow[pos >> 5] >> (pos & 31);
 #pragma unroll
@@ -626,70 +676,58 @@ __device__ void r1spc_stats(Ctx<R>& cx, int d, int m, int lb, int na) {
     using A = Arith<R>;
     using M = typename A::M;
     using K = typename A::Key;
-    if (m < 32) {
-        const int lgm = __ffs(m) - 1;
-        const int per = 32 >> lgm;
-        for (int r0 = 0; r0 < na; r0 += per) {
-            const int r = r0 + (cx.lane >> lgm), i = cx.lane & (m - 1);
-            const bool ok = r < na;
-            const int p = cx.fx->alive_list[ok ? r : 0];
-            const M v = ok ? A::val(cx.llr(p, d)[i]) : M(0);
-            const unsigned hb = __ballot_sync(FULL, ok && v < M(0));
-            K k1 = ok ? A::make_key(A::mag(v), i) : A::kKeyMax;
-            K k2 = A::kKeyMax;
-            for (int off = 1; off < m; off <<= 1) {
-                const K o1 = shfl_xor_k(k1, off), o2 = shfl_xor_k(k2, off);
-                const K n1 = kmin(k1, o1);
-                k2 = kmin(kmax(k1, o1), kmin(k2, o2));
-                k1 = n1;
-            }
-            if (ok && i == 0) {
-                const uint32_t bits = (hb >> (cx.lane & ~(m - 1))) & ((1u << m) - 1u);
-                uint32_t* w = cx.row(p) + (lb >> 5);
-                const uint32_t mk = ((1u << m) - 1u) << (lb & 31);
-                *w = (*w & ~mk) | (bits << (lb & 31));
-                cx.fx->st_i1[r] = A::key_idx(k1);
-                cx.fx->st_i2[r] = A::key_idx(k2);
-                cx.fx->st_a1[r] = mbits<M>(A::key_val(k1));
-                cx.fx->st_a2[r] = mbits<M>(A::key_val(k2));
-                cx.fx->st_w[r] = __popc(bits) & 1;
+    // One pass over all paths: lp lanes per path (na is a power of two, C22),
+    // lane l0 of a group takes values l0, l0+lp, l0+2lp, ... of its path.
+    const int lp = min(m, 32 / na);
+    const int lglp = __ffs(lp) - 1;
+    const int E = m >> lglp;
+    const int r = cx.lane >> lglp, l0 = cx.lane & (lp - 1);
+    const bool ok = r < na;
+    const int p = cx.fx->alive_list[ok ? r : 0];
+    const R* L = cx.llr(p, d);
+    uint32_t* span = cx.row(p) + (lb >> 5);
+    const uint32_t gmask = lp >= 32 ? FULL : ((1u << lp) - 1u);
+    K k1 = A::kKeyMax, k2 = A::kKeyMax;
+    uint32_t acc = 0;
+    int par = 0;
+    for (int k = 0; k < E; ++k) {
+        const int i = l0 + (k << lglp);
+        const M v = ok ? A::val(L[i]) : M(0);
+        const unsigned hb = __ballot_sync(FULL, ok && v < M(0));
+        // this group's lp hard bits = span bits [k*lp, (k+1)*lp)
+        const uint32_t gb = (hb >> (cx.lane & ~(lp - 1))) & gmask;
+        par ^= __popc(gb);
+        acc |= gb << ((k << lglp) & 31);
+        if (m >= 32 && (((k + 1) << lglp) & 31) == 0) {
+            if (ok && l0 == 0) span[(k << lglp) >> 5] = acc;
+            acc = 0;
+        }
+        if (ok) {
+            const K kv = A::make_key(A::mag(v), i);
+            if (kv < k1) {
+                k2 = k1;
+                k1 = kv;
+            } else if (kv < k2) {
+                k2 = kv;
             }
         }
-    } else {
-        for (int r = 0; r < na; ++r) {
-            const int p = cx.fx->alive_list[r];
-            const R* L = cx.llr(p, d);
-            uint32_t* w = cx.row(p) + (lb >> 5);
-            K k1 = A::kKeyMax, k2 = A::kKeyMax;
-            int par = 0;
-            for (int k = 0; k < (m >> 5); ++k) {
-                const int i = (k << 5) + cx.lane;
-                const M v = A::val(L[i]);
-                const unsigned hb = __ballot_sync(FULL, v < M(0));
-                if (cx.lane == 0) w[k] = hb;
-                par ^= __popc(hb) & 1;
-                const K kv = A::make_key(A::mag(v), i);
-                if (kv < k1) {
-                    k2 = k1;
-                    k1 = kv;
-                } else if (kv < k2) {
-                    k2 = kv;
-                }
-            }
-            for (int off = 1; off < 32; off <<= 1) {
-                const K o1 = shfl_xor_k(k1, off), o2 = shfl_xor_k(k2, off);
-                const K n1 = kmin(k1, o1);
-                k2 = kmin(kmax(k1, o1), kmin(k2, o2));
-                k1 = n1;
-            }
-            if (cx.lane == 0) {
-                cx.fx->st_i1[r] = A::key_idx(k1);
-                cx.fx->st_i2[r] = A::key_idx(k2);
-                cx.fx->st_a1[r] = mbits<M>(A::key_val(k1));
-                cx.fx->st_a2[r] = mbits<M>(A::key_val(k2));
-                cx.fx->st_w[r] = par;
-            }
-        }
+    }
+    if (m < 32 && ok && l0 == 0) {
+        const uint32_t mk = ((1u << m) - 1u) << (lb & 31);
+        *span = (*span & ~mk) | (acc << (lb & 31));
+    }
+    for (int off = 1; off < lp; off <<= 1) {
+        const K o1 = shfl_xor_k(k1, off), o2 = shfl_xor_k(k2, off);
+        const K n1 = kmin(k1, o1);
+        k2 = kmin(kmax(k1, o1), kmin(k2, o2));
+        k1 = n1;
+    }
+    if (ok && l0 == 0) {
+        cx.fx->st_i1[r] = A::key_idx(k1);
+        cx.fx->st_i2[r] = A::key_idx(k2);
+        cx.fx->st_a1[r] = mbits<M>(A::key_val(k1));
+        cx.fx->st_a2[r] = mbits<M>(A::key_val(k2));
+        cx.fx->st_w[r] = par & 1;
     }
     __syncwarp();
 }
@@ -1025,6 +1063,39 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) decode_kernel(const Launc
     }
 }
 
+// Exhaustive check of the packed int8 f/g against the scalar kernels: every
+// (a, b) pair in [-127, 127]^2, in every byte position, next to
+// pseudo-random neighbours, under all 16 partial-sum patterns.
+__global__ void selftest_kernel(unsigned long long* bad) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= 255 * 255) return;
+    const int a = t / 255 - 127, b = t % 255 - 127;
+    unsigned long long nbad = 0;
+    uint32_t h = 0x9e3779b9u * uint32_t(t + 1);
+    for (int pos = 0; pos < 4; ++pos) {
+        uint32_t wa = 0, wb = 0;
+        int8_t va[4], vb[4];
+        for (int j = 0; j < 4; ++j) {
+            h ^= h << 13;
+            h ^= h >> 17;
+            h ^= h << 5;
+            va[j] = int8_t(j == pos ? a : int(h % 255u) - 127);
+            vb[j] = int8_t(j == pos ? b : int((h >> 8) % 255u) - 127);
+            wa |= uint32_t(uint8_t(va[j])) << (8 * j);
+            wb |= uint32_t(uint8_t(vb[j])) << (8 * j);
+        }
+        const uint32_t fo = f_swar(wa, wb);
+        for (int j = 0; j < 4; ++j)
+            nbad += int8_t(fo >> (8 * j)) != Arith<int8_t>::f(va[j], vb[j]);
+        for (uint32_t s4 = 0; s4 < 16; ++s4) {
+            const uint32_t go = g_swar(wa, wb, s4);
+            for (int j = 0; j < 4; ++j)
+                nbad += int8_t(go >> (8 * j)) != Arith<int8_t>::g(va[j], vb[j], (s4 >> j) & 1u);
+        }
+    }
+    if (nbad) atomicAdd(bad, nbad);
+}
+
 template <typename R, bool LIST>
 cudaError_t launch(const LaunchParams& p, int grid, cudaStream_t s) {
     const int smem = p.smem_per_warp * kWarpsPerBlock;
@@ -1066,6 +1137,18 @@ int occupancy_sc(int precision, int smem) {
 }
 int occupancy_list(int precision, int smem) {
     return precision == 0 ? occupancy<float, true>(smem) : occupancy<int8_t, true>(smem);
+}
+
+cudaError_t kernel_selftest(unsigned long long* mismatches) {
+    unsigned long long* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, sizeof(unsigned long long));
+    if (e != cudaSuccess) return e;
+    cudaMemset(d, 0, sizeof(unsigned long long));
+    selftest_kernel<<<(255 * 255 + 255) / 256, 256>>>(d);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpy(mismatches, d, sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    return e;
 }
 
 } // namespace plb
