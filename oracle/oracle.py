@@ -28,9 +28,15 @@ PRECISIONS = {"f32": 0, "i8": 1}
 _u8p = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
 
 
+_BUILT = False
+
+
 def build_oracle(force: bool = False) -> str:
-    if force or not os.path.exists(ORACLE_SO):
+    """make keeps it incremental: a no-op when the .so is up to date."""
+    global _BUILT
+    if force or not _BUILT or not os.path.exists(ORACLE_SO):
         subprocess.check_call(["make", "-s", "-C", HERE, "oracle"])
+        _BUILT = True
     return ORACLE_SO
 
 

@@ -423,6 +423,26 @@ int orc_tree(const uint8_t* frozen, int n, const int32_t* pruning, int32_t* out,
     return cnt;
 }
 
+void orc_kernels_f32(float a, float b, float* out) {
+    out[0] = fk_f32(a, b);
+    out[1] = gk_f32(a, b, 0);
+    out[2] = gk_f32(a, b, 1);
+    out[3] = sat_add_f32(a, b);
+    out[4] = (float)hard_f32(a);
+}
+
+void orc_kernels_i8(int a, int b, int* out) {
+    out[0] = fk_i8((int8_t)a, (int8_t)b);
+    out[1] = gk_i8((int8_t)a, (int8_t)b, 0);
+    out[2] = gk_i8((int8_t)a, (int8_t)b, 1);
+    out[3] = sat_add_i8((int8_t)a, (int8_t)b);
+    out[4] = hard_i8((int8_t)a);
+}
+
+void orc_two_smallest_f32(const float* v, int n, int* i1, int* i2) {
+    two_smallest_f32(v, n, i1, i2);
+}
+
 uint64_t orc_crc(int width, uint64_t poly, int reflect, uint64_t init,
                  uint64_t xorout, const uint8_t* bits, int64_t len) {
     orc_code c;

@@ -46,14 +46,15 @@ _LIB = None
 
 
 def lib_path() -> str:
-    return _build.LIB
+    # PLB_LIB: an alternative in-tree build of the same library (tuning runs)
+    return os.environ.get("PLB_LIB") or _build.LIB
 
 
 def lib():
     global _LIB
     if _LIB is not None:
         return _LIB
-    path = _build.LIB
+    path = lib_path()
     if not os.path.exists(path):
         raise ImportError(f"native library {path} is missing: run __graft_entry__.build()")
     L = C.CDLL(path)

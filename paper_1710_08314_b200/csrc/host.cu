@@ -390,7 +390,7 @@ namespace {
 
 int target_warps_per_sm() {
     const char* e = std::getenv("PLB_TARGET_WARPS");
-    return e ? std::max(1, std::atoi(e)) : 24;
+    return e ? std::max(1, std::atoi(e)) : 32;
 }
 
 // Pick where the depth segments live: the most shared-memory-resident
@@ -403,6 +403,7 @@ RungCfg plan_rung(const pl_handle& h, int l, bool list) {
     if (forced) cands.push_back(std::atoi(forced));
     else
         for (int s = h.nmax; s >= 8; s >>= 1) cands.push_back(s);
+    if (cands.empty()) cands.push_back(h.nmax); // tiny codes: everything in shared memory
     RungCfg best;
     best.l = l;
     for (int seg : cands) {

@@ -1044,8 +1044,12 @@ __device__ void sc_frame(const LaunchParams& P, const DevCode& C, unsigned char*
     __syncwarp();
 }
 
+#ifndef PLB_MINBLOCKS
+#define PLB_MINBLOCKS 8
+#endif
+
 template <typename R, bool LIST>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32) decode_kernel(const LaunchParams P) {
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, PLB_MINBLOCKS) decode_kernel(const LaunchParams P) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t gw = int64_t(blockIdx.x) * kWarpsPerBlock + wib;

@@ -114,6 +114,105 @@ def test_cfg2_like_fa(P, gpu, oracle_lib):
         assert got["esc"].max() >= 2
 
 
+GOLD = __import__("os").path.join(__import__("os").path.dirname(__file__), "golden")
+
+
+def _gold_files():
+    import glob
+    import os
+
+    return sorted(glob.glob(os.path.join(GOLD, "decode_*.npz")))
+
+
+@pytest.mark.parametrize("path", _gold_files(), ids=lambda p: p.split("decode_")[-1][:-4])
+def test_gpu_matches_reference_golden(P, gpu, path):
+    """GPU outputs == the UNMODIFIED reference's outputs stored in the golden
+    fixtures (no oracle in between)."""
+    z = np.load(path)
+    n, k, crc = int(z["n"]), int(z["k"]), str(z["crc"]) or None
+    c = [int(x) for x in z["pruning"]]
+    pr = P.PruningConfig(bool(c[0]), bool(c[1]), bool(c[2]), bool(c[3]), c[4], c[5])
+    code = P.make_code(n, k, z["frozen"], crc)
+    x = gpu.from_numpy(np.ascontiguousarray(z["llr"])).cuda()
+    for j in range(int(z["runs"])):
+        kind, l = str(z[f"r{j}_kind"]), int(z[f"r{j}_l"])
+        dec = P.FrameDecoder(code, kind, l, str(z["precision"]), pr)
+        o = dec.decode_batch(x, codeword=True)
+        gpu.cuda.synchronize()
+        pb, cb = (code.payload_size + 7) // 8, (n + 7) // 8
+        tag = f"{path} {kind} L={l}"
+        assert np.array_equal(o["payload"].cpu().numpy()[:, :pb], z[f"r{j}_payload"]), tag
+        assert np.array_equal(o["codeword"].cpu().numpy()[:, :cb], z[f"r{j}_codeword"]), tag
+        assert np.array_equal(o["crc_ok"].cpu().numpy(), z[f"r{j}_crc_ok"]), tag
+        assert np.array_equal(o["esc"].cpu().numpy(), z[f"r{j}_esc"]), tag
+        assert np.array_equal(o["metric"].cpu().numpy(), z[f"r{j}_metric"].astype(np.float32)), tag
+
+
+def _b(s):
+    return np.array([c == "1" for c in s], np.uint8)
+
+
+def test_gpu_pinned_list_cases(P, gpu):
+    """test_list.cpp:78-193 pinned single-node decodes through the GPU."""
+    none = P.PruningConfig.none()
+    r = P.FrameDecoder(P.make_code(2, 1, _b("10")), "scl", 1, "f32", none).decode([-2.0, 5.0])
+    assert r.metric == 2.0 and r.codeword.tolist() == [0, 0]
+    r = P.FrameDecoder(P.make_code(2, 1, _b("01")), "scl", 2, "f32", none).decode([3.0, 3.0])
+    assert r.metric == 0.0 and r.payload.tolist() == [0]
+    r = P.FrameDecoder(P.make_code(8, 4, _b("11110000")), "sscl", 1, "f32").decode(
+        [1, -2, 3, -4, 100, 100, 100, 100])
+    assert r.metric == 6.0
+    r = P.FrameDecoder(P.make_code(4, 1, _b("1110")), "sscl", 2, "f32").decode([1, 1, 1, -5])
+    assert r.metric == 3.0 and r.codeword.tolist() == [1, 1, 1, 1] and r.payload.tolist() == [1]
+    r = P.FrameDecoder(P.make_code(4, 4, _b("0000")), "sscl", 1, "f32").decode([9, -8, 1, -2])
+    assert r.codeword.tolist() == [0, 1, 0, 1] and r.metric == 0.0
+    spc = P.FrameDecoder(P.make_code(4, 3, _b("1000")), "sscl", 2, "f32")
+    r = spc.decode([1, 5, -6, -7])
+    assert r.codeword.tolist() == [0, 0, 1, 1] and r.metric == 0.0
+    r = spc.decode([1, 5, -6, 7])
+    assert r.codeword.tolist() == [1, 0, 1, 0] and r.metric == 1.0
+    r = P.FrameDecoder(P.make_code(2, 2, _b("00")), "scl", 2, "f32", none).decode([0.0, 0.0])
+    assert r.metric == 0.0 and r.payload.tolist() == [0, 0] and r.codeword.tolist() == [0, 0]
+
+
+def test_gpu_ml_on_tiny_code(P, gpu):
+    """test_list.cpp:291-319 / acceptance criterion 2: a wide list reaches the
+    maximum-likelihood codeword of an (8,4) code."""
+    import itertools
+
+    fz = P.construct_frozen(8, 4, 0.5)
+    code = P.make_code(8, 4, fz)
+    book = []
+    u = np.zeros(8, np.uint8)
+    for bits in itertools.product([0, 1], repeat=4):
+        u[:] = 0
+        u[code.info_pos] = bits
+        x = u.copy()
+        inc = 1
+        while inc < 8:  # x = u * F^{(x)3} and back: systematic codeword via two transforms
+            for i in range(8):
+                if i & inc == 0:
+                    x[i] ^= x[i + inc]
+            inc <<= 1
+        x[fz == 1] = 0
+        inc = 1
+        while inc < 8:
+            for i in range(8):
+                if i & inc == 0:
+                    x[i] ^= x[i + inc]
+            inc <<= 1
+        book.append(x.copy())
+    rng = np.random.default_rng(303)
+    llr = rng.integers(-9, 10, (300, 8)).astype(np.float32)
+    for l in (8, 16):
+        dec = P.FrameDecoder(code, "scl", l, "f32", P.PruningConfig.none())
+        o = dec.decode_batch(gpu.from_numpy(llr).cuda(), codeword=True)
+        met = o["metric"].cpu().numpy()
+        for f in range(300):
+            best = min(float(np.abs(llr[f][(x != (llr[f] < 0))]).sum()) for x in book)
+            assert met[f] == best
+
+
 def test_cfg4_like_l32(P, gpu, oracle_lib):
     code = _code(P, 2048, 1024, "32-GZIP")
     _, llr = P.channel(code, 1.5, 42, 0, 24, "f32")
