@@ -132,11 +132,12 @@ def run_reference(args):
     dt = (time.perf_counter() - t0) / args.steps
     gbps = code.k * nf / dt / 1e9
     out = {
-        "impl": "reference", "metric": "decoded info throughput", "value": gbps, "unit": "Gb/s",
+        "impl": "reference", "metric": METRIC, "value": gbps, "unit": "Gb/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype_of(wl),
         "data": "synthetic (reference FrameRng/encode_systematic/transmit, seed 42)",
-        "config": {**wl.describe(), "frames_per_step": nf},
+        "config": common_config(wl, args.frames or wl.frames, ws),
+        "reference_sample_frames_per_step": nf,
         "cpu_baseline": {"value": gbps, "unit": "Gb/s", "cores": nthr, "kind": "reference",
                          "sample": f"{nf} frames of {wl.name} per step, FrameDecoder<R> per thread"},
         "e2e": {"value": gbps, "unit": "Gb/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -147,6 +148,17 @@ def run_reference(args):
 
 def dtype_of(wl):
     return "int8" if wl.precision == "i8" else "f32"
+
+
+METRIC = "decoded info throughput (Gb/s) N=2048 K=1723"
+
+
+def common_config(wl, frames_per_gpu, ws):
+    """The config both arms report (the driver compares like with like)."""
+    return {**wl.describe(), "frames_per_gpu": frames_per_gpu,
+            "global_frames": frames_per_gpu * ws, "parallelism": f"frame-range shards x{ws}",
+            "l2": "inputs larger than L2 (%.0f MB per GPU per step)"
+                  % (frames_per_gpu * wl.n * (4 if wl.precision == "f32" else 1) / 1e6)}
 
 
 def main():
@@ -166,7 +178,9 @@ def main():
     wl = WORKLOADS[args.workload]
     F = args.frames or wl.frames
     code = wl.code()
-    frame0 = rank * F  # weak scaling: each rank decodes its own global frame range
+    from paper_1710_08314_b200.shard import frame_range
+
+    frame0, _ = frame_range(rank, ws, F)  # weak scaling: each rank its own global frame range
     if args.device_channel:
         info_d, llr_d = P.channel_device(code, wl.ebn0_db, 42, frame0, F, wl.precision, wl.scale, local)
         torch.cuda.synchronize()
@@ -222,10 +236,13 @@ def main():
     value = code.k * total_frames * args.steps / elapsed / 1e9
 
     # ---- FER / escalation of the batch (sanity of the decode itself)
+    from paper_1710_08314_b200.shard import Counters, all_reduce_counters
+
     pay = out["payload"].cpu().numpy()
-    bits = np.unpackbits(pay, axis=1)[:, : code.k]
-    frame_err = (bits != info).any(1)
     esc = out["esc"].cpu().numpy()
+    counts = Counters()
+    counts.add_batch(np.unpackbits(pay, axis=1), info, esc)
+    counts = all_reduce_counters(counts, device=f"cuda:{local}" if ws > 1 else None)
 
     # ---- end to end through the public API with host buffers (pl_decode_host)
     e2e_steps = args.e2e_steps or max(3, min(args.steps, 10))
@@ -264,15 +281,14 @@ def main():
     all_kernel_s = sum(sum(v) for v in kernel_ms.values()) / 1e3
 
     result = {
-        "metric": "decoded info throughput (Gb/s) N=2048 K=1723",
+        "metric": METRIC,
         "value": value, "unit": "Gb/s", "n_gpus": ws, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": dtype_of(wl),
         "data": "synthetic: BPSK-AWGN frames keyed by (seed 42, global frame index), FrameRng semantics",
-        "config": {**wl.describe(), "frames_per_gpu": F, "global_frames": total_frames,
-                   "parallelism": f"frame-range shards x{ws}",
-                   "l2": "inputs larger than L2 (%.0f MB per GPU per step)" % (h2d / 1e6)},
-        "fer": float(frame_err.mean()), "esc_mean": float(esc.mean()),
+        "config": common_config(wl, F, ws),
+        "fer": counts.fer(), "ber": counts.ber(code.k), "frame_errors": counts.frame_errors,
+        "esc_mean": counts.esc_sum / max(counts.frames, 1),
         "gpu_launches": int(launches),
         "kernel_ms": {f"{k[0]}_L{k[1]}": float(np.mean(v)) for k, v in kernel_ms.items()},
         "kernel_share_of_step": all_kernel_s / (elapsed if ws == 1 else elapsed),
