@@ -413,7 +413,7 @@ RungCfg plan_rung(const pl_handle& h, int l, bool list) {
         c.smem_per_warp = int(plb::smem_bytes_per_warp(h.nmax, l, h.esz, seg));
         c.gscratch_per_warp = plb::gscratch_bytes_per_warp(h.nmax, l, h.esz, seg);
         const int smem = c.smem_per_warp * plb::kWarpsPerBlock;
-        const int nb = list ? plb::occupancy_list(h.dec.precision, smem)
+        const int nb = list ? plb::occupancy_list(h.dec.precision, l, smem)
                             : plb::occupancy_sc(h.dec.precision, smem);
         if (nb <= 0) continue;
         c.grid = nb * h.sms;

@@ -278,6 +278,7 @@ __host__ __device__ inline LayoutQ layout_query(int n, int l, int esz, int segma
     off = align16(off + 4 * l * (q.rw | 1));
     int goff = 0;
     const int stages = ilog2(n);
+    #pragma unroll 1
     for (int d = 1; d <= stages; ++d) {
         const int seg = n >> d;
         const int bytes = align16(l * seg * esz);
@@ -343,30 +344,31 @@ struct Ctx {
 };
 
 // ---- f / g over all alive paths ----------------------------------------
-template <typename R, int G, bool IS_G>
+// One body for F and G (is_g is warp-uniform), two vector widths per type
+// (G = 1 for narrow nodes, G = 16 bytes otherwise): the decode loop's hot
+// code must stay inside the instruction cache.
+template <typename R, int G>
 __device__ __forceinline__ void fg_item(const R* in, R* out, const uint32_t* prow, int h,
-                                        int c, int lb) {
+                                        int c, int lb, bool is_g) {
     using A = Arith<R>;
     const Vec<R, G> a = vld<R, G>(in + c * G);
     const Vec<R, G> b = vld<R, G>(in + h + c * G);
     Vec<R, G> o;
+    const int pos = lb + c * G;
+    const uint32_t bits = is_g ? prow[pos >> 5] >> (pos & 31) : 0u;
     if constexpr (A::kFixed && G >= 4) {
         constexpr int W = G / 4;
         const uint32_t* aw = reinterpret_cast<const uint32_t*>(&a.raw);
         const uint32_t* bw = reinterpret_cast<const uint32_t*>(&b.raw);
         uint32_t* ow = reinterpret_cast<uint32_t*>(&o.raw);
-        if constexpr (IS_G) {
-            const int pos = lb + c * G;
-            const uint32_t bits = prow[pos >> 5] >> (pos & 31);
+        if (is_g) {
 #pragma unroll
             for (int w = 0; w < W; ++w) ow[w] = g_swar(aw[w], bw[w], (bits >> (4 * w)) & 15u);
         } else {
 #pragma unroll
             for (int w = 0; w < W; ++w) ow[w] = f_swar(aw[w], bw[w]);
         }
-    } else if constexpr (IS_G) {
-        const int pos = lb + c * G;
-        const uint32_t bits = prow[pos >> 5] >> (pos & 31);
+    } else if (is_g) {
 #pragma unroll
         for (int i = 0; i < G; ++i) o.v[i] = A::g(a.v[i], b.v[i], (bits >> i) & 1u);
     } else {
@@ -376,48 +378,31 @@ __device__ __forceinline__ void fg_item(const R* in, R* out, const uint32_t* pro
     vst<R, G>(out + c * G, o);
 }
 
-template <typename R, int G, bool IS_G>
-__device__ void fg_run(Ctx<R>& cx, int d, int h, int lb, int na) {
+template <typename R, int G>
+__device__ __forceinline__ void fg_run(Ctx<R>& cx, int d, int h, int lb, int na, bool is_g) {
     const int cp = h / G; // items per path, power of two
     const int lg = __ffs(cp) - 1;
     R* const outp = cx.pool(d + 1);
-    if (cp >= 32) {
-        for (int r = 0; r < na; ++r) {
-            const int p = cx.fx->alive_list[r];
-            const R* in = cx.llr(p, d);
-            R* out = outp + r * h;
-            const uint32_t* prow = cx.row(p);
-#pragma unroll 2
-            for (int c = cx.lane; c < cp; c += 32) fg_item<R, G, IS_G>(in, out, prow, h, c, lb);
-        }
-    } else {
-        const int total = na << lg;
-        for (int t = cx.lane; t < total; t += 32) {
-            const int r = t >> lg;
-            const int p = cx.fx->alive_list[r];
-            fg_item<R, G, IS_G>(cx.llr(p, d), outp + r * h, cx.row(p), h, t & (cp - 1), lb);
-        }
+    R* const inp = d == 0 ? const_cast<R*>(cx.chan) : cx.pool(d);
+    const int seg = cx.n >> d;
+    const int total = na << lg;
+    #pragma unroll 1
+    for (int t = cx.lane; t < total; t += 32) {
+        const int r = t >> lg;
+        const int p = cx.fx->alive_list[r];
+        const R* in = d == 0 ? inp : inp + int(cx.fx->bufidx[p * 16 + d]) * seg;
+        fg_item<R, G>(in, outp + r * h, cx.row(p), h, t & (cp - 1), lb, is_g);
     }
 }
 
-template <typename R, bool IS_G>
-__device__ void op_fg(Ctx<R>& cx, int d, int m, int lb, int na) {
+template <typename R>
+__device__ void op_fg(Ctx<R>& cx, int d, int m, int lb, int na, bool is_g) {
     constexpr int VE = 16 / int(sizeof(R));
     const int h = m >> 1;
-    const int G = h < VE ? h : VE;
     // the child segment of the path of rank r goes to buffer r (see header)
     if (cx.is_alive()) cx.fx->bufidx[cx.lane * 16 + d + 1] = uint8_t(cx.myrank);
-    switch (G) {
-    case 1: fg_run<R, 1, IS_G>(cx, d, h, lb, na); break;
-    case 2: fg_run<R, 2, IS_G>(cx, d, h, lb, na); break;
-    case 4: fg_run<R, 4, IS_G>(cx, d, h, lb, na); break;
-    default:
-        if constexpr (VE >= 8) {
-            if (G == 8) fg_run<R, 8, IS_G>(cx, d, h, lb, na);
-            else fg_run<R, 16, IS_G>(cx, d, h, lb, na);
-        }
-        break;
-    }
+    if (h >= VE) fg_run<R, VE>(cx, d, h, lb, na, is_g);
+    else fg_run<R, 1>(cx, d, h, lb, na, is_g);
     __syncwarp();
 }
 
@@ -428,6 +413,7 @@ __device__ void op_h(Ctx<R>& cx, int m, int lb, int na) {
     if (h >= 32) {
         const int W = h >> 5, lg = __ffs(W) - 1;
         const int total = na << lg;
+        #pragma unroll 1
         for (int t = cx.lane; t < total; t += 32) {
             uint32_t* w = cx.row(cx.fx->alive_list[t >> lg]) + (lb >> 5) + (t & (W - 1));
             w[0] ^= w[W];
@@ -444,6 +430,7 @@ __device__ void op_h(Ctx<R>& cx, int m, int lb, int na) {
 // write `bit` over the span [lb, lb+m) of a psum row (whole warp)
 __device__ __forceinline__ void span_fill_warp(uint32_t* row, int lb, int m, int bit, int lane) {
     if (m >= 32) {
+        #pragma unroll 1
         for (int w = lane; w < (m >> 5); w += 32) row[(lb >> 5) + w] = bit ? FULL : 0u;
     } else if (lane == 0) {
         const uint32_t mk = ((1u << m) - 1u) << (lb & 31);
@@ -469,6 +456,7 @@ __device__ void rep_fold(Ctx<R>& cx, int d, int m, int na) {
     if (m <= 32) {
         const int lgm = __ffs(m) - 1;
         const int per = 32 >> lgm;
+        #pragma unroll 1
         for (int r0 = 0; r0 < na; r0 += per) {
             const int r = r0 + (cx.lane >> lgm), i = cx.lane & (m - 1);
             const bool ok = r < na;
@@ -480,14 +468,18 @@ __device__ void rep_fold(Ctx<R>& cx, int d, int m, int na) {
             if (ok && i == 0) cx.fx->st_a1[r] = mbits<M>(v);
         }
     } else {
+        #pragma unroll 1
         for (int r = 0; r < na; ++r) {
             const R* L = cx.llr(cx.fx->alive_list[r], d);
             R* S = cx.pool(d + 1) + r * (m >> 1);
             const int h = m >> 1;
+            #pragma unroll 1
             for (int i = cx.lane; i < h; i += 32) S[i] = A::store(A::sat(A::val(L[i]), A::val(L[i + h])));
             __syncwarp();
+            #pragma unroll 1
             for (int len = h; len > 32; len >>= 1) {
                 const int hh = len >> 1;
+                #pragma unroll 1
                 for (int i = cx.lane; i < hh; i += 32) S[i] = A::store(A::sat(A::val(S[i]), A::val(S[i + hh])));
                 __syncwarp();
             }
@@ -525,11 +517,8 @@ __device__ void fork_apply(Ctx<R>& cx, const typename Arith<R>::M (&cm)[CPL],
         key[k] = i < ncand ? A::make_key(cm[k], i) : A::kKeyMax;
     }
     if constexpr (CPL == 1) {
-        if (ncand <= 2) key[0] = bitonic_lanes<K, 2>(key[0], lane);
-        else if (ncand <= 4) key[0] = bitonic_lanes<K, 4>(key[0], lane);
-        else if (ncand <= 8) key[0] = bitonic_lanes<K, 8>(key[0], lane);
-        else if (ncand <= 16) key[0] = bitonic_lanes<K, 16>(key[0], lane);
-        else key[0] = bitonic_lanes<K, 32>(key[0], lane);
+        // one 32-wide network for every candidate count keeps the code small
+        key[0] = bitonic_lanes<K, 32>(key[0], lane);
     } else {
         bitonic_regs<K, CPL>(key, lane);
     }
@@ -569,12 +558,14 @@ __device__ void fork_apply(Ctx<R>& cx, const typename Arith<R>::M (&cm)[CPL],
         // ... and the decided partial sums incl. the node span (which holds
         // the source's hard decisions for R1/SPC)
         const int nw = min(cx.rw, (lb + m + 31) >> 5);
+        #pragma unroll 1
         for (unsigned mm = dupm; mm; mm &= mm - 1) {
             const int dl = __ffs(mm) - 1;
             const int s = __shfl_sync(FULL, src, dl);
             const int t = __shfl_sync(FULL, tgt, dl);
             const uint32_t* sr = cx.row(s);
             uint32_t* tr = cx.row(t);
+            #pragma unroll 1
             for (int w = lane; w < nw; w += 32) tr[w] = sr[w];
         }
         __syncwarp();
@@ -587,6 +578,7 @@ __device__ void fork_apply(Ctx<R>& cx, const typename Arith<R>::M (&cm)[CPL],
         if (m < 32) {
             if (kept) span_fill_lane(cx.row(tgt), lb, m, ca);
         } else {
+            #pragma unroll 1
             for (int r = 0; r < keep; ++r) {
                 const int t = __shfl_sync(FULL, tgt, r);
                 const int bit = __shfl_sync(FULL, ca, r);
@@ -619,15 +611,18 @@ __device__ void list_frozen(Ctx<R>& cx, int d, int m, int lb, int na) {
     M pen = M(0);
     if (A::kFixed && m >= 32) {
         // saturating sums of non-negative terms are order-free in int8
+        #pragma unroll 1
         for (int r = 0; r < na; ++r) {
             const R* L = cx.llr(cx.fx->alive_list[r], d);
             int s = 0;
+            #pragma unroll 1
             for (int i = cx.lane; i < m; i += 32) s += max(0, -int(A::val(L[i])));
             s = int(__reduce_add_sync(FULL, unsigned(s)));
             if (cx.lane == r) pen = M(min(s, 127));
         }
     } else if (cx.lane < na) {
         const R* L = cx.llr(cx.fx->alive_list[cx.lane], d);
+        #pragma unroll 1
         for (int i = 0; i < m; ++i) {
             const M v = A::val(L[i]);
             if (v < M(0)) pen = A::sat(pen, -v); // sequential: float order matters
@@ -637,34 +632,13 @@ __device__ void list_frozen(Ctx<R>& cx, int d, int m, int lb, int na) {
     if (cx.is_alive()) cx.metric = A::sat(cx.metric, pr);
     if (m >= 32) {
         const int W = m >> 5;
+        #pragma unroll 1
         for (int t = cx.lane; t < na * W; t += 32)
             cx.row(cx.fx->alive_list[t / W])[(lb >> 5) + (t % W)] = 0u;
     } else if (cx.lane < na) {
         span_fill_lane(cx.row(cx.fx->alive_list[cx.lane]), lb, m, 0);
     }
     __syncwarp();
-    cx.normalize();
-}
-
-// information leaf (list_decoder.hpp:240-252)
-template <typename R, int CPL>
-__device__ void list_info(Ctx<R>& cx, int d, int lb, int na) {
-    using A = Arith<R>;
-    using M = typename A::M;
-    M cm[CPL];
-    int cs[CPL], cax[CPL];
-#pragma unroll
-    for (int k = 0; k < CPL; ++k) {
-        const int i = cx.lane + 32 * k, r = min(i >> 1, na - 1), j = i & 1;
-        const int p = cx.fx->alive_list[r];
-        const M v = A::val(cx.llr(p, d)[0]);
-        const M base = __shfl_sync(FULL, cx.metric, p);
-        const bool hb = v < M(0);
-        cm[k] = A::sat(base, (j == 0) == hb ? A::mag(v) : M(0));
-        cs[k] = p;
-        cax[k] = pack_aux(j, -1);
-    }
-    fork_apply<R, CPL>(cx, cm, cs, cax, 2 * na, AK_BIT, lb, 1);
     cx.normalize();
 }
 
@@ -690,6 +664,7 @@ __device__ void r1spc_stats(Ctx<R>& cx, int d, int m, int lb, int na) {
     K k1 = A::kKeyMax, k2 = A::kKeyMax;
     uint32_t acc = 0;
     int par = 0;
+    #pragma unroll 1
     for (int k = 0; k < E; ++k) {
         const int i = l0 + (k << lglp);
         const M v = ok ? A::val(L[i]) : M(0);
@@ -732,77 +707,20 @@ __device__ void r1spc_stats(Ctx<R>& cx, int d, int m, int lb, int na) {
     __syncwarp();
 }
 
-// rate-1 node (list_decoder.hpp:254-274): 4 candidates per path
-template <typename R, int CPL>
-__device__ void list_r1_cands(Ctx<R>& cx, int lb, int m, int na) {
+// repetition node (list_decoder.hpp:276-305): after the fold, pen_w = the
+// sum of the magnitudes that disagree with the fold's decision, sequential
+// in index order (float order matters; int8 is order-free) -> st_a2, st_w.
+template <typename R>
+__device__ void rep_pen(Ctx<R>& cx, int d, int m, int na) {
     using A = Arith<R>;
     using M = typename A::M;
-    M cm[CPL];
-    int cs[CPL], cax[CPL];
-#pragma unroll
-    for (int k = 0; k < CPL; ++k) {
-        const int i = cx.lane + 32 * k, r = min(i >> 2, na - 1), j = i & 3;
-        const M base = base_of(cx, r);
-        const int i1 = cx.fx->st_i1[r], i2 = cx.fx->st_i2[r];
-        const M a1 = mfrom<M>(cx.fx->st_a1[r]), a2 = mfrom<M>(cx.fx->st_a2[r]);
-        cs[k] = cx.fx->alive_list[r];
-        if (j == 0) {
-            cm[k] = base;
-            cax[k] = pack_aux(-1, -1);
-        } else if (j == 1) {
-            cm[k] = A::sat(base, a1);
-            cax[k] = pack_aux(i1, -1);
-        } else if (j == 2) {
-            cm[k] = A::sat(base, a2);
-            cax[k] = pack_aux(i2, -1);
-        } else {
-            cm[k] = A::sat(base, A::sat(a1, a2));
-            cax[k] = pack_aux(i1, i2);
-        }
-    }
-    fork_apply<R, CPL>(cx, cm, cs, cax, 4 * na, AK_FLIPS, lb, m);
-}
-
-// single-parity node (list_decoder.hpp:307-333): 2 candidates per path
-template <typename R, int CPL>
-__device__ void list_spc_cands(Ctx<R>& cx, int lb, int m, int na) {
-    using A = Arith<R>;
-    using M = typename A::M;
-    M cm[CPL];
-    int cs[CPL], cax[CPL];
-#pragma unroll
-    for (int k = 0; k < CPL; ++k) {
-        const int i = cx.lane + 32 * k, r = min(i >> 1, na - 1), j = i & 1;
-        const M base = base_of(cx, r);
-        const int i1 = cx.fx->st_i1[r], i2 = cx.fx->st_i2[r];
-        const M a1 = mfrom<M>(cx.fx->st_a1[r]), a2 = mfrom<M>(cx.fx->st_a2[r]);
-        cs[k] = cx.fx->alive_list[r];
-        if (cx.fx->st_w[r]) { // parity broken: restore it through i1 or i2
-            cm[k] = A::sat(base, j == 0 ? a1 : a2);
-            cax[k] = pack_aux(j == 0 ? i1 : i2, -1);
-        } else if (j == 0) {
-            cm[k] = base;
-            cax[k] = pack_aux(-1, -1);
-        } else {
-            cm[k] = A::sat(base, A::sat(a1, a2));
-            cax[k] = pack_aux(i1, i2);
-        }
-    }
-    fork_apply<R, CPL>(cx, cm, cs, cax, 2 * na, AK_FLIPS, lb, m);
-}
-
-// repetition node (list_decoder.hpp:276-305): 2 candidates per path
-template <typename R, int CPL>
-__device__ void list_rep_cands(Ctx<R>& cx, int d, int lb, int m, int na) {
-    using A = Arith<R>;
-    using M = typename A::M;
-    // pen_w: sum of the magnitudes that disagree with the fold's decision,
-    // sequential in index order (float order matters; int8 is order-free)
     if (A::kFixed && m >= 32) {
+        #pragma unroll 1
         for (int r = 0; r < na; ++r) {
             const R* L = cx.llr(cx.fx->alive_list[r], d);
             const bool w = mfrom<M>(cx.fx->st_a1[r]) < M(0);
             int s = 0;
+            #pragma unroll 1
             for (int i = cx.lane; i < m; i += 32) {
                 const int v = int(A::val(L[i]));
                 if (w ? (v > 0) : (v < 0)) s += abs(v);
@@ -817,6 +735,7 @@ __device__ void list_rep_cands(Ctx<R>& cx, int d, int lb, int m, int na) {
         const R* L = cx.llr(cx.fx->alive_list[cx.lane], d);
         const bool w = mfrom<M>(cx.fx->st_a1[cx.lane]) < M(0);
         M pen = M(0);
+        #pragma unroll 1
         for (int i = 0; i < m; ++i) {
             const M v = A::val(L[i]);
             if (w ? (v > M(0)) : (v < M(0))) pen = A::sat(pen, A::mag(v));
@@ -825,31 +744,63 @@ __device__ void list_rep_cands(Ctx<R>& cx, int d, int lb, int m, int na) {
         cx.fx->st_a2[cx.lane] = mbits<M>(pen);
     }
     __syncwarp();
-    M cm[CPL];
-    int cs[CPL], cax[CPL];
+}
+
+// A forking node: per-path statistics, candidates in emission order
+// (ascending slot, then candidate number, list_decoder.hpp:240-333), one
+// shared fork_apply, normalisation.  C = candidates per lane, fixed per
+// kernel instantiation (4L <= 32C).
+template <typename R, int C>
+__device__ void list_fork_node(Ctx<R>& cx, int code, int d, int m, int lb, int na) {
+    using A = Arith<R>;
+    using M = typename A::M;
+    if (code == OP_R1 || code == OP_SPC) {
+        r1spc_stats(cx, d, m, lb, na);
+    } else if (code == OP_REP) {
+        rep_fold(cx, d, m, na);
+        rep_pen(cx, d, m, na);
+    }
+    const int lgb = code == OP_R1 ? 2 : 1; // candidates per path: 4 or 2
+    M cm[C];
+    int cs[C], cax[C];
 #pragma unroll
-    for (int k = 0; k < CPL; ++k) {
-        const int i = cx.lane + 32 * k, r = min(i >> 1, na - 1), j = i & 1;
-        const M base = base_of(cx, r);
-        const int w = cx.fx->st_w[r];
-        const M pen_w = mfrom<M>(cx.fx->st_a2[r]);
-        const M s = mfrom<M>(cx.fx->st_a1[r]);
-        cs[k] = cx.fx->alive_list[r];
-        if (j == 0) {
-            cm[k] = A::sat(base, pen_w);
-            cax[k] = pack_aux(w, -1);
+    for (int k = 0; k < C; ++k) {
+        const int i = cx.lane + 32 * k, r = min(i >> lgb, na - 1), j = i & ((1 << lgb) - 1);
+        const int p = cx.fx->alive_list[r];
+        const M base = __shfl_sync(FULL, cx.metric, p);
+        cs[k] = p;
+        if (code == OP_INFO) { // list_decoder.hpp:240-252
+            const M v = A::val(cx.llr(p, d)[0]);
+            cm[k] = A::sat(base, (j == 0) == (v < M(0)) ? A::mag(v) : M(0));
+            cax[k] = pack_aux(j, -1);
+        } else if (code == OP_REP) { // :276-305, preferred bit first
+            const int w = cx.fx->st_w[r];
+            const M pen_w = mfrom<M>(cx.fx->st_a2[r]);
+            cm[k] = j == 0 ? A::sat(base, pen_w)
+                           : A::sat(base, A::sat(pen_w, A::mag(mfrom<M>(cx.fx->st_a1[r]))));
+            cax[k] = pack_aux(w ^ j, -1);
         } else {
-            cm[k] = A::sat(base, A::sat(pen_w, A::mag(s)));
-            cax[k] = pack_aux(w ^ 1, -1);
+            const int i1 = cx.fx->st_i1[r], i2 = cx.fx->st_i2[r];
+            const M a1 = mfrom<M>(cx.fx->st_a1[r]), a2 = mfrom<M>(cx.fx->st_a2[r]);
+            // R1 (:254-274): none, i1, i2, i1&i2.  SPC (:307-333): broken
+            // parity -> i1, i2; intact -> none, i1&i2.
+            const int jj = code == OP_R1 ? j : (cx.fx->st_w[r] ? j + 1 : j * 3);
+            cm[k] = jj == 0 ? base : jj == 1 ? A::sat(base, a1) : jj == 2 ? A::sat(base, a2)
+                                                                 : A::sat(base, A::sat(a1, a2));
+            cax[k] = jj == 0 ? pack_aux(-1, -1) : jj == 1 ? pack_aux(i1, -1)
+                                                : jj == 2 ? pack_aux(i2, -1) : pack_aux(i1, i2);
         }
     }
-    fork_apply<R, CPL>(cx, cm, cs, cax, 2 * na, AK_BCAST, lb, m);
+    const int kind = code == OP_INFO ? AK_BIT : code == OP_REP ? AK_BCAST : AK_FLIPS;
+    fork_apply<R, C>(cx, cm, cs, cax, na << lgb, kind, lb, code == OP_INFO ? 1 : m);
+    cx.normalize();
 }
 
 // ---- CRC syndrome of a decided codeword row ----------------
 __device__ uint64_t row_syndrome(const DevCode& C, const uint32_t* row, int lane) {
     uint64_t syn = 0;
     const int nbytes = (C.n + 7) >> 3;
+    #pragma unroll 1
     for (int j = lane; j < nbytes; j += 32) {
         const uint32_t byte = (row[j >> 2] >> ((j & 3) * 8)) & 0xffu;
         syn ^= __ldg(C.crc_tab + (size_t(j) << 8) + byte);
@@ -864,6 +815,7 @@ __device__ void write_outputs(const LaunchParams& P, const DevCode& C, const uin
                               int frame, int lane) {
     uint8_t* pay = P.payload + int64_t(frame) * P.payload_stride;
     const int pb = (C.psize + 7) >> 3;
+    #pragma unroll 1
     for (int q = lane; q < pb; q += 32) {
         uint32_t byte = 0;
 #pragma unroll
@@ -879,6 +831,7 @@ __device__ void write_outputs(const LaunchParams& P, const DevCode& C, const uin
     if (P.codeword) {
         uint8_t* cw = P.codeword + int64_t(frame) * P.codeword_stride;
         const int cb = (C.n + 7) >> 3;
+        #pragma unroll 1
         for (int q = lane; q < cb; q += 32) {
             uint32_t byte = 0;
 #pragma unroll
@@ -918,7 +871,7 @@ __device__ __forceinline__ long long claim(const LaunchParams& P, int lane) {
 }
 
 // ---- one frame, list decoding at list size P.l --------------------------
-template <typename R>
+template <typename R, int CW>
 __device__ void list_frame(const LaunchParams& P, const DevCode& C, unsigned char* sm,
                            unsigned char* gs, int frame, int lane) {
     using A = Arith<R>;
@@ -927,40 +880,15 @@ __device__ void list_frame(const LaunchParams& P, const DevCode& C, unsigned cha
     setup_ctx(cx, P, C, sm, gs, frame, lane, P.l);
     const uint32_t* sched = C.sched_list;
     const int nops = C.nops_list;
+    #pragma unroll 1
     for (int oi = 0; oi < nops; ++oi) {
         const uint32_t op = __ldg(sched + oi);
         const int code = op_code(op), d = op_depth(op), m = 1 << op_logm(op), lb = op_lb(op);
         const int na = __popc(cx.alive);
-        switch (code) {
-        case OP_F: op_fg<R, false>(cx, d, m, lb, na); break;
-        case OP_G: op_fg<R, true>(cx, d, m, lb, na); break;
-        case OP_H: op_h(cx, m, lb, na); break;
-        case OP_FROZEN: list_frozen(cx, d, m, lb, na); break;
-        case OP_INFO:
-            if (2 * na <= 32) list_info<R, 1>(cx, d, lb, na);
-            else list_info<R, 2>(cx, d, lb, na);
-            break;
-        case OP_R1:
-            r1spc_stats(cx, d, m, lb, na);
-            if (4 * na <= 32) list_r1_cands<R, 1>(cx, lb, m, na);
-            else if (4 * na <= 64) list_r1_cands<R, 2>(cx, lb, m, na);
-            else list_r1_cands<R, 4>(cx, lb, m, na);
-            cx.normalize();
-            break;
-        case OP_SPC:
-            r1spc_stats(cx, d, m, lb, na);
-            if (2 * na <= 32) list_spc_cands<R, 1>(cx, lb, m, na);
-            else list_spc_cands<R, 2>(cx, lb, m, na);
-            cx.normalize();
-            break;
-        case OP_REP:
-            rep_fold(cx, d, m, na);
-            if (2 * na <= 32) list_rep_cands<R, 1>(cx, d, lb, m, na);
-            else list_rep_cands<R, 2>(cx, d, lb, m, na);
-            cx.normalize();
-            break;
-        default: break;
-        }
+        if (code <= OP_G) op_fg(cx, d, m, lb, na, code == OP_G);
+        else if (code == OP_H) op_h(cx, m, lb, na);
+        else if (code == OP_FROZEN) list_frozen(cx, d, m, lb, na);
+        else list_fork_node<R, CW>(cx, code, d, m, lb, na);
     }
     // finish (list_decoder.hpp:457-502): stable order by (metric, slot)
     using K = typename A::Key;
@@ -975,6 +903,7 @@ __device__ void list_frame(const LaunchParams& P, const DevCode& C, unsigned cha
             crc_ok = 1;
         } else if (P.select_by_crc) {
             unsigned passm = 0;
+            #pragma unroll 1
             for (unsigned mm = cx.alive & ~(1u << pick); mm; mm &= mm - 1) {
                 const int s = __ffs(mm) - 1;
                 if (row_syndrome(C, cx.row(s), lane) == 0) passm |= 1u << s;
@@ -1010,12 +939,13 @@ __device__ void sc_frame(const LaunchParams& P, const DevCode& C, unsigned char*
     uint32_t* row = cx.row(0);
     const uint32_t* sched = C.sched_sc;
     const int nops = C.nops_sc;
+    #pragma unroll 1
     for (int oi = 0; oi < nops; ++oi) {
         const uint32_t op = __ldg(sched + oi);
         const int code = op_code(op), d = op_depth(op), m = 1 << op_logm(op), lb = op_lb(op);
         switch (code) {
-        case OP_F: op_fg<R, false>(cx, d, m, lb, 1); break;
-        case OP_G: op_fg<R, true>(cx, d, m, lb, 1); break;
+        case OP_F:
+        case OP_G: op_fg(cx, d, m, lb, 1, code == OP_G); break;
         case OP_H: op_h(cx, m, lb, 1); break;
         case OP_FROZEN: span_fill_warp(row, lb, m, 0, lane); __syncwarp(); break;
         case OP_INFO:
@@ -1048,7 +978,9 @@ __device__ void sc_frame(const LaunchParams& P, const DevCode& C, unsigned char*
 #define PLB_MINBLOCKS 8
 #endif
 
-template <typename R, bool LIST>
+// CW = 0: SC pass; CW = 1/2/4: list pass with CW candidates per lane
+// (L <= 8 / 16 / 32).
+template <typename R, int CW>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, PLB_MINBLOCKS) decode_kernel(const LaunchParams P) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -1062,7 +994,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PLB_MINBLOCKS) decode_ker
         const int frame = P.frame_list ? P.frame_list[idx] : int(idx);
         const int cid = P.code_id ? P.code_id[frame] : 0;
         const DevCode C = P.codes[cid];
-        if constexpr (LIST) list_frame<R>(P, C, sm, gs, frame, lane);
+        if constexpr (CW > 0) list_frame<R, CW>(P, C, sm, gs, frame, lane);
         else sc_frame<R>(P, C, sm, gs, frame, lane);
     }
 }
@@ -1100,19 +1032,31 @@ __global__ void selftest_kernel(unsigned long long* bad) {
     if (nbad) atomicAdd(bad, nbad);
 }
 
-template <typename R, bool LIST>
-cudaError_t launch(const LaunchParams& p, int grid, cudaStream_t s) {
+template <typename R>
+void (*kernel_for(int cw))(LaunchParams) {
+    switch (cw) {
+    case 0: return decode_kernel<R, 0>;
+    case 1: return decode_kernel<R, 1>;
+    case 2: return decode_kernel<R, 2>;
+    default: return decode_kernel<R, 4>;
+    }
+}
+
+int cw_of(int l, bool list) { return !list ? 0 : l <= 8 ? 1 : l <= 16 ? 2 : 4; }
+
+template <typename R>
+cudaError_t launch(const LaunchParams& p, int cw, int grid, cudaStream_t s) {
     const int smem = p.smem_per_warp * kWarpsPerBlock;
-    auto kern = decode_kernel<R, LIST>;
+    auto kern = kernel_for<R>(cw);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     kern<<<grid, kWarpsPerBlock * 32, smem, s>>>(p);
     return cudaGetLastError();
 }
 
-template <typename R, bool LIST>
-int occupancy(int smem) {
-    auto kern = decode_kernel<R, LIST>;
+template <typename R>
+int occupancy(int cw, int smem) {
+    auto kern = kernel_for<R>(cw);
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
         return 0;
     int nb = 0;
@@ -1131,16 +1075,18 @@ int64_t gscratch_bytes_per_warp(int nmax, int l, int elem_bytes, int seg_smem_ma
 }
 
 cudaError_t launch_sc(const LaunchParams& p, int precision, int grid, cudaStream_t s) {
-    return precision == 0 ? launch<float, false>(p, grid, s) : launch<int8_t, false>(p, grid, s);
+    return precision == 0 ? launch<float>(p, 0, grid, s) : launch<int8_t>(p, 0, grid, s);
 }
 cudaError_t launch_list(const LaunchParams& p, int precision, int grid, cudaStream_t s) {
-    return precision == 0 ? launch<float, true>(p, grid, s) : launch<int8_t, true>(p, grid, s);
+    const int cw = cw_of(p.l, true);
+    return precision == 0 ? launch<float>(p, cw, grid, s) : launch<int8_t>(p, cw, grid, s);
 }
 int occupancy_sc(int precision, int smem) {
-    return precision == 0 ? occupancy<float, false>(smem) : occupancy<int8_t, false>(smem);
+    return precision == 0 ? occupancy<float>(0, smem) : occupancy<int8_t>(0, smem);
 }
-int occupancy_list(int precision, int smem) {
-    return precision == 0 ? occupancy<float, true>(smem) : occupancy<int8_t, true>(smem);
+int occupancy_list(int precision, int l, int smem) {
+    const int cw = cw_of(l, true);
+    return precision == 0 ? occupancy<float>(cw, smem) : occupancy<int8_t>(cw, smem);
 }
 
 cudaError_t kernel_selftest(unsigned long long* mismatches) {

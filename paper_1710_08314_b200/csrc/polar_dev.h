@@ -88,7 +88,7 @@ cudaError_t launch_sc(const LaunchParams& p, int precision, int grid, cudaStream
 cudaError_t launch_list(const LaunchParams& p, int precision, int grid, cudaStream_t s);
 // Max resident blocks per SM for a kernel at the given dynamic smem.
 int occupancy_sc(int precision, int smem_bytes);
-int occupancy_list(int precision, int smem_bytes);
+int occupancy_list(int precision, int l, int smem_bytes);
 // Exhaustive device check of the packed int8 f/g against the scalar kernels.
 cudaError_t kernel_selftest(unsigned long long* mismatches);
 
