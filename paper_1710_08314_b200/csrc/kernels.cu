@@ -248,6 +248,7 @@ struct alignas(16) Fixed {
     uint8_t bufidx[32 * 16]; // [slot][depth] -> buffer index in the depth pool
     uint8_t alive_list[32];  // rank -> slot, ascending
     uint8_t freetab[32];     // k -> k-th free slot, ascending
+    uint8_t dsrc[32], dtgt[32]; // k-th duplicate of a fork: source, target
     uint32_t met_s[32];      // metric by slot (fork hand-over)
     int32_t st_i1[32], st_i2[32], st_w[32]; // per-rank node statistics
     uint32_t st_a1[32], st_a2[32];
@@ -268,14 +269,17 @@ __host__ __device__ inline int align16(int v) { return (v + 15) & ~15; }
 struct LayoutQ {
     int32_t rw, psum_off, smem_total, gmem_total, pool_off, pool_in_smem;
 };
+// Word stride between the psum rows of two slots: 16-byte aligned with a
+// 4-bank skew for n >= 128 (vector copies, and the same word of different
+// slots falls into different banks), odd below.
+__host__ __device__ inline int row_stride(int rw) { return rw >= 4 ? rw + 4 : (rw | 1); }
+
 __host__ __device__ inline LayoutQ layout_query(int n, int l, int esz, int segmax, int want_d) {
     LayoutQ q{};
     int off = int(sizeof(Fixed));
     q.rw = n >= 32 ? n / 32 : 1;
     q.psum_off = off;
-    // rows at an odd word stride: the same word of different slots' rows
-    // falls into different banks
-    off = align16(off + 4 * l * (q.rw | 1));
+    off = align16(off + 4 * l * row_stride(q.rw));
     int goff = 0;
     const int stages = ilog2(n);
     #pragma unroll 1
@@ -322,7 +326,7 @@ struct Ctx {
         if (d == 0) return const_cast<R*>(chan);
         return pool(d) + int(fx->bufidx[p * 16 + d]) * (n >> d);
     }
-    __device__ __forceinline__ uint32_t* row(int p) const { return ps + p * (rw | 1); }
+    __device__ __forceinline__ uint32_t* row(int p) const { return ps + p * row_stride(rw); }
     __device__ __forceinline__ bool is_alive() const { return (alive >> lane) & 1u; }
 
     __device__ void set_alive(unsigned a) {
@@ -517,8 +521,9 @@ __device__ void fork_apply(Ctx<R>& cx, const typename Arith<R>::M (&cm)[CPL],
         key[k] = i < ncand ? A::make_key(cm[k], i) : A::kKeyMax;
     }
     if constexpr (CPL == 1) {
-        // one 32-wide network for every candidate count keeps the code small
-        key[0] = bitonic_lanes<K, 32>(key[0], lane);
+        // two network widths: 2 candidates/path forks at L <= 8 need 16
+        if (ncand <= 16) key[0] = bitonic_lanes<K, 16>(key[0], lane);
+        else key[0] = bitonic_lanes<K, 32>(key[0], lane);
     } else {
         bitonic_regs<K, CPL>(key, lane);
     }
@@ -550,23 +555,33 @@ __device__ void fork_apply(Ctx<R>& cx, const typename Arith<R>::M (&cm)[CPL],
         if ((freem >> lane) & 1u) cx.fx->freetab[__popc(freem & lanemask_lt())] = uint8_t(lane);
         __syncwarp();
         if (dup) {
-            tgt = cx.fx->freetab[__popc(dupm & lanemask_lt())];
+            const int k = __popc(dupm & lanemask_lt());
+            tgt = cx.fx->freetab[k];
+            cx.fx->dsrc[k] = uint8_t(src);
+            cx.fx->dtgt[k] = uint8_t(tgt);
             // 3. duplicate: the LLR pointer row ...
             *reinterpret_cast<uint4*>(cx.fx->bufidx + tgt * 16) =
                 *reinterpret_cast<const uint4*>(cx.fx->bufidx + src * 16);
         }
+        __syncwarp();
         // ... and the decided partial sums incl. the node span (which holds
-        // the source's hard decisions for R1/SPC)
+        // the source's hard decisions for R1/SPC); words past the decided
+        // prefix are don't-care, so whole 16-byte chunks are copied, all
+        // duplicates at once
         const int nw = min(cx.rw, (lb + m + 31) >> 5);
-        #pragma unroll 1
-        for (unsigned mm = dupm; mm; mm &= mm - 1) {
-            const int dl = __ffs(mm) - 1;
-            const int s = __shfl_sync(FULL, src, dl);
-            const int t = __shfl_sync(FULL, tgt, dl);
-            const uint32_t* sr = cx.row(s);
-            uint32_t* tr = cx.row(t);
+        const int nd = __popc(dupm);
+        if (cx.rw >= 4) {
+            const int n4 = (nw + 3) >> 2;
+            const int lg = ilog2(n4);
             #pragma unroll 1
-            for (int w = lane; w < nw; w += 32) tr[w] = sr[w];
+            for (int t = lane; t < (nd << lg); t += 32) {
+                const int k = t >> lg, q = t & ((1 << lg) - 1);
+                if (q < n4)
+                    reinterpret_cast<uint4*>(cx.row(cx.fx->dtgt[k]))[q] =
+                        reinterpret_cast<const uint4*>(cx.row(cx.fx->dsrc[k]))[q];
+            }
+        } else if (lane < nd) {
+            for (int w = 0; w < cx.rw; ++w) cx.row(cx.fx->dtgt[lane])[w] = cx.row(cx.fx->dsrc[lane])[w];
         }
         __syncwarp();
     }
@@ -651,51 +666,67 @@ __device__ void r1spc_stats(Ctx<R>& cx, int d, int m, int lb, int na) {
     using M = typename A::M;
     using K = typename A::Key;
     // One pass over all paths: lp lanes per path (na is a power of two, C22),
-    // lane l0 of a group takes values l0, l0+lp, l0+2lp, ... of its path.
+    // lane l0 of a group takes the E = m/lp consecutive values
+    // [l0*E, (l0+1)*E) of its path (vector loads), builds their hard bits
+    // locally and ORs them into the path's (cleared) psum span.
     const int lp = min(m, 32 / na);
     const int lglp = __ffs(lp) - 1;
     const int E = m >> lglp;
     const int r = cx.lane >> lglp, l0 = cx.lane & (lp - 1);
     const bool ok = r < na;
     const int p = cx.fx->alive_list[ok ? r : 0];
-    const R* L = cx.llr(p, d);
+    const int i0 = l0 * E;
+    const R* L = cx.llr(p, d) + i0;
     uint32_t* span = cx.row(p) + (lb >> 5);
-    const uint32_t gmask = lp >= 32 ? FULL : ((1u << lp) - 1u);
+    const int base = m < 32 ? (lb & 31) : 0; // span bit of value 0 within span[0]
+    if (ok && l0 == 0) {
+        if (m >= 32) {
+            #pragma unroll 1
+            for (int w = 0; w < (m >> 5); ++w) span[w] = 0u;
+        } else {
+            *span &= ~(((1u << m) - 1u) << base);
+        }
+    }
+    __syncwarp();
     K k1 = A::kKeyMax, k2 = A::kKeyMax;
     uint32_t acc = 0;
     int par = 0;
-    #pragma unroll 1
-    for (int k = 0; k < E; ++k) {
-        const int i = l0 + (k << lglp);
-        const M v = ok ? A::val(L[i]) : M(0);
-        const unsigned hb = __ballot_sync(FULL, ok && v < M(0));
-        // this group's lp hard bits = span bits [k*lp, (k+1)*lp)
-        const uint32_t gb = (hb >> (cx.lane & ~(lp - 1))) & gmask;
-        par ^= __popc(gb);
-        acc |= gb << ((k << lglp) & 31);
-        if (m >= 32 && (((k + 1) << lglp) & 31) == 0) {
-            if (ok && l0 == 0) span[(k << lglp) >> 5] = acc;
-            acc = 0;
-        }
-        if (ok) {
-            const K kv = A::make_key(A::mag(v), i);
-            if (kv < k1) {
-                k2 = k1;
-                k1 = kv;
-            } else if (kv < k2) {
-                k2 = kv;
+    if (ok) {
+        #pragma unroll 1
+        for (int k = 0; k < E; k += 4) {
+            M v[4];
+            if (E >= 4) {
+                const Vec<R, 4> q = vld<R, 4>(L + k);
+                #pragma unroll
+                for (int j = 0; j < 4; ++j) v[j] = A::val(q.v[j]);
+            } else {
+                #pragma unroll
+                for (int j = 0; j < 4; ++j) v[j] = j < E ? A::val(L[j]) : M(0);
+            }
+            #pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (j < E) {
+                    acc |= uint32_t(v[j] < M(0)) << ((k + j) & 31);
+                    const K kv = A::make_key(A::mag(v[j]), i0 + k + j);
+                    const K n1 = kmin(k1, kv);
+                    k2 = kmin(k2, kmax(k1, kv));
+                    k1 = n1;
+                }
+            }
+            if (((k + 4) & 31) == 0 || k + 4 >= E) {
+                const int pos = base + i0 + (k & ~31);
+                if (acc) atomicOr(span + (pos >> 5), acc << (pos & 31));
+                par ^= __popc(acc);
+                acc = 0;
             }
         }
-    }
-    if (m < 32 && ok && l0 == 0) {
-        const uint32_t mk = ((1u << m) - 1u) << (lb & 31);
-        *span = (*span & ~mk) | (acc << (lb & 31));
     }
     for (int off = 1; off < lp; off <<= 1) {
         const K o1 = shfl_xor_k(k1, off), o2 = shfl_xor_k(k2, off);
         const K n1 = kmin(k1, o1);
         k2 = kmin(kmax(k1, o1), kmin(k2, o2));
         k1 = n1;
+        par ^= __shfl_xor_sync(FULL, par, off);
     }
     if (ok && l0 == 0) {
         cx.fx->st_i1[r] = A::key_idx(k1);
