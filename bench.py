@@ -6,6 +6,8 @@ GA frozen set @4.5 dB, CA-SCL L=8 with R0/R1/REP_8-/SPC4 pruning, int8 LLRs
 (x4, saturated to +-127) from BPSK-AWGN at 3.5 dB, 262 144 frames per GPU.
 One step = one decode of that batch (inputs resident in HBM for `value`;
 host buffers with the copies inside the timed region for `e2e`).
+`--workload` selects the other BASELINE configs (cfg0, cfg2_{2.5,3.5,4.5},
+cfg3 mixed-MCS, cfg4_L{8,16,32}).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg1]
   python bench.py --impl reference ...   # the reference's own CPU decoder
@@ -25,6 +27,8 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+METRIC = "decoded info throughput (Gb/s) N=2048 K=1723"
+
 
 def parse():
     ap = argparse.ArgumentParser()
@@ -38,16 +42,12 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=16384)
     ap.add_argument("--ref-sample", type=int, default=16384)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--device-channel", action="store_true",
-                    help="generate LLRs on the GPU (Philox) instead of the host FrameRng")
     return ap.parse_args()
 
 
 def dist_env():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
+    return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
+            int(os.environ.get("LOCAL_RANK", "0")))
 
 
 def sample_clocks_start(gpu_index: int):
@@ -102,13 +102,50 @@ def measured_peaks():
         return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
+def dtype_of(wl):
+    return "int8" if wl.precision == "i8" else "f32"
+
+
+def common_config(wl, frames_per_gpu, ws):
+    """The config both arms report (the driver compares like with like)."""
+    esz = 4 if wl.precision == "f32" else 1
+    return {**wl.describe(), "frames_per_gpu": frames_per_gpu,
+            "global_frames": frames_per_gpu * ws, "parallelism": f"frame-range shards x{ws}",
+            "l2": "inputs larger than L2 (%.0f MB per GPU per step)" % (frames_per_gpu * wl.n * esz / 1e6)}
+
+
+def reference_decode(O, codes, cid, llr, wl, nthr):
+    """The compiled reference FrameDecoder<R> over a batch (per code for
+    mixed batches); returns payload/crc_ok/esc/metric arrays and the seconds
+    spent decoding."""
+    nf = llr.shape[0]
+    pb = max((c.payload_size + 7) // 8 for c in codes)
+    out = {"payload": np.zeros((nf, pb), np.uint8), "crc_ok": np.zeros(nf, np.uint8),
+           "esc": np.zeros(nf, np.uint8), "metric": np.zeros(nf, np.float64)}
+    secs = 0.0
+    groups = [(0, np.arange(nf))] if cid is None else [(i, np.flatnonzero(cid == i)) for i in range(len(codes))]
+    for i, rows in groups:
+        if rows.size == 0:
+            continue
+        c = codes[i]
+        ref = O.Reference(c.n, c.k, c.frozen, c.crc.raw() if c.crc else "", wl.kind, wl.l,
+                          wl.precision, wl.pruning.as_tuple())
+        x = np.ascontiguousarray(llr[rows, : c.n])
+        t0 = time.perf_counter()
+        r = ref.decode(x, nthr)
+        secs += time.perf_counter() - t0
+        out["payload"][rows, : r.payload.shape[1]] = r.payload
+        out["crc_ok"][rows], out["esc"][rows], out["metric"][rows] = r.crc_ok, r.esc, r.metric
+    return out, secs
+
+
 def run_reference(args):
     """The reference's own CPU decoder (oracle/_ref: FrameDecoder<R> compiled
     from /root/reference/proj), all host threads, bounded sample per step."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
-    from paper_1710_08314_b200.workload import WORKLOADS
+    from paper_1710_08314_b200.workload import WORKLOADS, make_batch
     wl = WORKLOADS[args.workload]
     try:
         from oracle import oracle as O
@@ -116,26 +153,21 @@ def run_reference(args):
     except Exception as e:  # noqa: BLE001
         print(json.dumps({"impl": "reference", "unavailable": f"oracle/_ref not loadable: {e}"}))
         return 0
-    import paper_1710_08314_b200 as P
-    code = wl.code()
     nthr = os.cpu_count() or 1
     nf = args.ref_sample
-    _, llr = O.ref_channel(code.n, code.k, code.frozen, wl.crc, wl.ebn0_db, 42, 0, nf,
-                           wl.precision, wl.scale, nthr)
-    ref = O.Reference(code.n, code.k, code.frozen, wl.crc, wl.kind, wl.l, wl.precision,
-                      wl.pruning.as_tuple())
-    for _ in range(args.warmup):
-        ref.decode(llr[: max(nthr, nf // 8)], nthr)
-    t0 = time.perf_counter()
+    codes, cid, info, ks, llr = make_batch(wl, 0, nf, nthreads=nthr)
+    w = max(nthr, nf // 8)
+    reference_decode(O, codes, cid[:w] if cid is not None else None, llr[:w], wl, nthr)  # warm-up
+    secs = 0.0
     for _ in range(args.steps):
-        ref.decode(llr, nthr)
-    dt = (time.perf_counter() - t0) / args.steps
-    gbps = code.k * nf / dt / 1e9
+        secs += reference_decode(O, codes, cid, llr, wl, nthr)[1]
+    dt = secs / args.steps
+    gbps = float(ks.sum()) / dt / 1e9
     out = {
         "impl": "reference", "metric": METRIC, "value": gbps, "unit": "Gb/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype_of(wl),
-        "data": "synthetic (reference FrameRng/encode_systematic/transmit, seed 42)",
+        "data": "synthetic: BPSK-AWGN frames keyed by (seed 42, global frame index), FrameRng semantics",
         "config": common_config(wl, args.frames or wl.frames, ws),
         "reference_sample_frames_per_step": nf,
         "cpu_baseline": {"value": gbps, "unit": "Gb/s", "cores": nthr, "kind": "reference",
@@ -144,21 +176,6 @@ def run_reference(args):
     }
     print(json.dumps(out))
     return 0
-
-
-def dtype_of(wl):
-    return "int8" if wl.precision == "i8" else "f32"
-
-
-METRIC = "decoded info throughput (Gb/s) N=2048 K=1723"
-
-
-def common_config(wl, frames_per_gpu, ws):
-    """The config both arms report (the driver compares like with like)."""
-    return {**wl.describe(), "frames_per_gpu": frames_per_gpu,
-            "global_frames": frames_per_gpu * ws, "parallelism": f"frame-range shards x{ws}",
-            "l2": "inputs larger than L2 (%.0f MB per GPU per step)"
-                  % (frames_per_gpu * wl.n * (4 if wl.precision == "f32" else 1) / 1e6)}
 
 
 def main():
@@ -173,27 +190,22 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     torch.cuda.set_device(local)
     import paper_1710_08314_b200 as P
-    from paper_1710_08314_b200.workload import WORKLOADS, schedule_work
+    from paper_1710_08314_b200.shard import Counters, all_reduce_counters, frame_range
+    from paper_1710_08314_b200.workload import WORKLOADS, make_batch, schedule_work
 
     wl = WORKLOADS[args.workload]
     F = args.frames or wl.frames
-    code = wl.code()
-    from paper_1710_08314_b200.shard import frame_range
-
     frame0, _ = frame_range(rank, ws, F)  # weak scaling: each rank its own global frame range
-    if args.device_channel:
-        info_d, llr_d = P.channel_device(code, wl.ebn0_db, 42, frame0, F, wl.precision, wl.scale, local)
-        torch.cuda.synchronize()
-        llr_h = llr_d.cpu().pin_memory()
-        info = info_d.cpu().numpy()
-    else:
-        info, llr_np = P.channel(code, wl.ebn0_db, 42, frame0, F, wl.precision, wl.scale,
-                                 max(1, (os.cpu_count() or 1) // ws))
-        llr_h = torch.from_numpy(llr_np).pin_memory()
-        llr_d = llr_h.cuda(local)
-    dec = P.FrameDecoder(code, wl.kind, wl.l, wl.precision, wl.pruning, device=local)
+    codes, cid, info, ks, llr_np = make_batch(wl, frame0, F,
+                                              nthreads=max(1, (os.cpu_count() or 1) // ws))
+    llr_h = torch.from_numpy(llr_np).pin_memory()
+    llr_d = llr_h.cuda(local)
+    cid_h = torch.from_numpy(cid).pin_memory() if cid is not None else None
+    cid_d = cid_h.cuda(local) if cid is not None else None
+    dec = P.FrameDecoder(codes, wl.kind, wl.l, wl.precision, wl.pruning, device=local)
     out = dec.alloc_outputs(F)
     stream = torch.cuda.current_stream(local)
+    bits_per_step = float(ks.sum())
 
     def barrier():
         if ws > 1:
@@ -206,8 +218,9 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    for _ in range(max(args.warmup, 3) if args.warmup >= 0 else 3):
-        dec.decode_batch(llr_d, out=out)
+    warmup = max(args.warmup, 3)
+    for _ in range(warmup):
+        dec.decode_batch(llr_d, code_id=cid_d, out=out)
     torch.cuda.synchronize()
 
     # ---- device-resident throughput (value), with live per-kernel timing
@@ -221,7 +234,7 @@ def main():
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     for _ in range(args.steps):
-        dec.decode_batch(llr_d, out=out)
+        dec.decode_batch(llr_d, code_id=cid_d, out=out)
         launches += dec.last_launches()
         for kd, l, ms in dec.last_kernel_ms():
             kernel_ms.setdefault((kd, l), []).append(ms)
@@ -232,16 +245,13 @@ def main():
     dec.profile(False)
     elapsed = max_over_ranks(ev0.elapsed_time(ev1) / 1e3)
     ms_per_step = elapsed / args.steps * 1e3
-    total_frames = F * ws
-    value = code.k * total_frames * args.steps / elapsed / 1e9
+    value = bits_per_step * ws * args.steps / elapsed / 1e9
 
-    # ---- FER / escalation of the batch (sanity of the decode itself)
-    from paper_1710_08314_b200.shard import Counters, all_reduce_counters
-
+    # ---- error counts of the batch, reduced over ranks (sim.cpp:66-71)
     pay = out["payload"].cpu().numpy()
     esc = out["esc"].cpu().numpy()
     counts = Counters()
-    counts.add_batch(np.unpackbits(pay, axis=1), info, esc)
+    counts.add_batch(np.unpackbits(pay, axis=1), info, esc, ks if cid is not None else None)
     counts = all_reduce_counters(counts, device=f"cuda:{local}" if ws > 1 else None)
 
     # ---- end to end through the public API with host buffers (pl_decode_host)
@@ -253,27 +263,30 @@ def main():
         "esc": torch.empty(F, dtype=torch.uint8).pin_memory(),
         "metric": torch.empty(F, dtype=torch.float32).pin_memory(),
     }
-    dec.decode_host_into(llr_h, host_out)
+    dec.decode_host_into(llr_h, host_out, cid_h)
     barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        dec.decode_host_into(llr_h, host_out)
+        dec.decode_host_into(llr_h, host_out, cid_h)
     e2e_s = max_over_ranks(time.perf_counter() - t0)
-    e2e_value = code.k * total_frames * e2e_steps / e2e_s / 1e9
-    h2d = F * code.n * (4 if wl.precision == "f32" else 1)
+    e2e_value = bits_per_step * ws * e2e_steps / e2e_s / 1e9
+    esz = 4 if wl.precision == "f32" else 1
+    h2d = F * dec.llr_stride * esz + (F * 4 if cid is not None else 0)
     d2h = F * (dec.payload_stride + 1 + 1 + 4)
 
     # ---- roofline of the dominant kernel (live CUDA-event durations)
     peaks, peak_src = measured_peaks()
-    dom = max(kernel_ms.items(), key=lambda kv: sum(kv[1]))
-    (dkind, dl), dms = dom
+    (dkind, dl), dms = max(kernel_ms.items(), key=lambda kv: sum(kv[1]))
     per_launch_s = float(np.mean(dms)) / 1e3
-    n_launch_frames = F if (dkind == "list" and wl.kind in ("ca_sscl", "sscl", "scl")) or dkind == "sc" \
-        else int((esc >= dl).sum())
-    esz = 4 if wl.precision == "f32" else 1
-    bytes_per_frame = code.n * esz + dec.payload_stride + 1 + 1 + 4
+    one_pass = dkind == "sc" or wl.kind in ("ca_sscl", "sscl", "scl")
+    n_launch_frames = F if one_pass else int((esc >= dl).sum())
+    # algorithmic bytes / element-ops per frame, averaged over the batch's codes
+    freq = np.bincount(cid, minlength=len(codes)) / F if cid is not None else np.ones(1)
+    bytes_per_frame = float(sum(f * (c.n * esz + (c.payload_size + 7) // 8 + 6)
+                                for f, c in zip(freq, codes)))
+    ops_per_frame = float(sum(f * schedule_work(c, wl.kind, dl, wl.pruning, sc=(dkind == "sc"))
+                              for f, c in zip(freq, codes)))
     achieved_gbs = bytes_per_frame * n_launch_frames / per_launch_s / 1e9
-    ops_per_frame = schedule_work(code, wl.kind, dl, wl.pruning, sc=(dkind == "sc"))
     sm_count = torch.cuda.get_device_properties(local).multi_processor_count
     clk = (peaks.get("sm_max_mhz") or 1965.0) * 1e6
     lane_peak = sm_count * 128 * clk
@@ -283,15 +296,15 @@ def main():
     result = {
         "metric": METRIC,
         "value": value, "unit": "Gb/s", "n_gpus": ws, "steps": args.steps,
-        "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
+        "warmup": warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": dtype_of(wl),
         "data": "synthetic: BPSK-AWGN frames keyed by (seed 42, global frame index), FrameRng semantics",
         "config": common_config(wl, F, ws),
-        "fer": counts.fer(), "ber": counts.ber(code.k), "frame_errors": counts.frame_errors,
+        "fer": counts.fer(), "frame_errors": counts.frame_errors, "bit_errors": counts.bit_errors,
         "esc_mean": counts.esc_sum / max(counts.frames, 1),
         "gpu_launches": int(launches),
         "kernel_ms": {f"{k[0]}_L{k[1]}": float(np.mean(v)) for k, v in kernel_ms.items()},
-        "kernel_share_of_step": all_kernel_s / (elapsed if ws == 1 else elapsed),
+        "kernel_share_of_step": all_kernel_s / elapsed if ws == 1 else None,
         "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peaks["hbm_gbs"],
                      "unit": "GB/s", "frac": achieved_gbs / peaks["hbm_gbs"], "traffic": None,
                      "kernel": f"decode_kernel<{dtype_of(wl)}, {dkind}> L={dl}",
@@ -311,17 +324,13 @@ def main():
             from oracle import oracle as O
             nthr = os.cpu_count() or 1
             S = min(args.cpu_sample, F)
-            ref = O.Reference(code.n, code.k, code.frozen, wl.crc, wl.kind, wl.l, wl.precision,
-                              wl.pruning.as_tuple())
-            sample = llr_h[:S].numpy()
-            t0 = time.perf_counter()
-            r = ref.decode(sample, nthr)
-            dt = time.perf_counter() - t0
-            cpu_gbps = code.k * S / dt / 1e9
-            pb = (code.payload_size + 7) // 8
-            mism = ((pay[:S, :pb] != r.payload).any(1) | (out["crc_ok"].cpu().numpy()[:S] != r.crc_ok)
-                    | (esc[:S] != r.esc)
-                    | (out["metric"].cpu().numpy()[:S] != r.metric.astype(np.float32)))
+            r, dt = reference_decode(O, codes, cid[:S] if cid is not None else None,
+                                     llr_np[:S], wl, nthr)
+            cpu_gbps = float(ks[:S].sum()) / dt / 1e9
+            pb = r["payload"].shape[1]
+            mism = ((pay[:S, :pb] != r["payload"]).any(1) | (out["crc_ok"].cpu().numpy()[:S] != r["crc_ok"])
+                    | (esc[:S] != r["esc"])
+                    | (out["metric"].cpu().numpy()[:S] != r["metric"].astype(np.float32)))
             result["cpu_baseline"] = {
                 "value": cpu_gbps, "unit": "Gb/s", "cores": nthr, "kind": "reference",
                 "sample": f"first {S} frames of the step's batch, FrameDecoder<R> per thread "

@@ -42,6 +42,15 @@ int pl_channel_generate(const pl_code* code, double ebn0_db, uint64_t seed, uint
                         int64_t nframes, int32_t precision, float scale, uint8_t* info_out,
                         void* llr_out, int32_t nthreads);
 
+/* Same for an explicit list of global frame indices (mixed-code batches:
+ * the frames of one code are scattered through the batch).  Frame i of the
+ * output is keyed by frame_ids[i]; llr_stride / info_stride are the output
+ * row strides (values / bytes), so rows can land in a wider batch. */
+int pl_channel_generate_frames(const pl_code* code, double ebn0_db, uint64_t seed,
+                               const uint64_t* frame_ids, int64_t nframes, int32_t precision,
+                               float scale, uint8_t* info_out, int64_t info_stride,
+                               void* llr_out, int64_t llr_stride, int32_t nthreads);
+
 /* Device channel for large Monte-Carlo runs: statistically equivalent
  * (Philox4x32-10 keyed by (seed, frame), Box-Muller), NOT bit-identical to
  * the host generator.  info_out (k bytes per frame, nullable) and llr_out

@@ -18,7 +18,7 @@ EXPORTS = (
     "pl_codeword_stride", "pl_decode", "pl_decode_host", "pl_last_launches", "pl_crc_parse",
     "pl_crc_compute", "pl_tree_build", "pl_construct_frozen_bhat", "pl_construct_frozen_ga",
     "pl_channel_generate", "pl_channel_generate_device", "pl_profile", "pl_last_kernel_ms",
-    "pl_kernel_selftest",
+    "pl_kernel_selftest", "pl_channel_generate_frames",
 )
 
 
@@ -81,6 +81,8 @@ def lib():
     L.pl_last_kernel_ms.argtypes = [vp, vp, vp, vp, i32]
     L.pl_last_kernel_ms.restype = i32
     L.pl_kernel_selftest.argtypes = [i32, vp]
+    L.pl_channel_generate_frames.argtypes = [vp, C.c_double, u64, vp, i64, i32, C.c_float, vp, i64,
+                                             vp, i64, i32]
     _LIB = L
     return L
 

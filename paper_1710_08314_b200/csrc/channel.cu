@@ -167,10 +167,39 @@ private:
 
 } // namespace plb
 
+namespace plb {
+// frame i of the output is keyed by ids ? ids[i] : frame0 + i
+static int channel_core(const pl_code* code, double ebn0_db, uint64_t seed, uint64_t frame0,
+                        const uint64_t* ids, int64_t nframes, int32_t precision, float scale,
+                        uint8_t* info_out, int64_t info_stride, void* llr_out,
+                        int64_t llr_stride, int32_t nthreads);
+} // namespace plb
+
 extern "C" int pl_channel_generate(const pl_code* code, double ebn0_db, uint64_t seed,
                                    uint64_t frame0, int64_t nframes, int32_t precision,
                                    float scale, uint8_t* info_out, void* llr_out,
                                    int32_t nthreads) {
+    if (!code) return PL_ERR_ARG;
+    return plb::channel_core(code, ebn0_db, seed, frame0, nullptr, nframes, precision, scale,
+                             info_out, code->k, llr_out, code->n, nthreads);
+}
+
+extern "C" int pl_channel_generate_frames(const pl_code* code, double ebn0_db, uint64_t seed,
+                                          const uint64_t* frame_ids, int64_t nframes,
+                                          int32_t precision, float scale, uint8_t* info_out,
+                                          int64_t info_stride, void* llr_out, int64_t llr_stride,
+                                          int32_t nthreads) {
+    if (!code || (!frame_ids && nframes > 0) || llr_stride < code->n ||
+        (info_out && info_stride < code->k))
+        return PL_ERR_ARG;
+    return plb::channel_core(code, ebn0_db, seed, 0, frame_ids, nframes, precision, scale,
+                             info_out, info_stride, llr_out, llr_stride, nthreads);
+}
+
+static int plb::channel_core(const pl_code* code, double ebn0_db, uint64_t seed, uint64_t frame0,
+                             const uint64_t* ids, int64_t nframes, int32_t precision, float scale,
+                             uint8_t* info_out, int64_t info_stride, void* llr_out,
+                             int64_t llr_stride, int32_t nthreads) {
     using namespace plb;
     if (!code || !code->frozen || !llr_out || nframes < 0 || !pow2(code->n) || code->k < 1)
         return PL_ERR_ARG;
@@ -207,13 +236,13 @@ extern "C" int pl_channel_generate(const pl_code* code, double ebn0_db, uint64_t
         std::vector<uint64_t> u(static_cast<size_t>(nw));
         std::vector<uint8_t> info(static_cast<size_t>(k));
         for (int64_t f = a; f < b; ++f) {
-            FrameRng rng(seed, frame0 + uint64_t(f));
+            FrameRng rng(seed, ids ? ids[f] : frame0 + uint64_t(f));
             uint64_t crcv = c0;
             for (int i = 0; i < k; ++i) {
                 info[size_t(i)] = rng.coin() ? 1 : 0;
                 if (w && info[size_t(i)]) crcv ^= col[size_t(i)];
             }
-            if (info_out) std::memcpy(info_out + f * k, info.data(), size_t(k));
+            if (info_out) std::memcpy(info_out + f * info_stride, info.data(), size_t(k));
             std::fill(u.begin(), u.end(), 0);
             auto setbit = [&](int pos) { u[size_t(pos >> 6)] |= 1ull << (63 - (pos & 63)); };
             for (int j = 0; j < k; ++j)
@@ -229,10 +258,11 @@ extern "C" int pl_channel_generate(const pl_code* code, double ebn0_db, uint64_t
                 const double y = s + sigma * rng.gaussian();
                 const float v = float(demap * y);
                 if (precision == PL_F32) {
-                    static_cast<float*>(llr_out)[f * n + i] = v;
+                    static_cast<float*>(llr_out)[f * llr_stride + i] = v;
                 } else {
                     const float q = std::round(v * qs);
-                    static_cast<int8_t*>(llr_out)[f * n + i] = int8_t(std::clamp(q, -127.0f, 127.0f));
+                    static_cast<int8_t*>(llr_out)[f * llr_stride + i] =
+                        int8_t(std::clamp(q, -127.0f, 127.0f));
                 }
             }
         }

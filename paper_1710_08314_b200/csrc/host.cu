@@ -221,8 +221,24 @@ void emit_list(const std::vector<Node>& t, int ni, std::vector<uint32_t>& s) {
     }
 }
 
+// a subtree of size <= 32 as one register-level SC op + its frozen mask
+void emit_scsub(int depth, int m, int lb, const uint8_t* frozen, std::vector<uint32_t>& s) {
+    uint32_t mask = 0;
+    for (int i = 0; i < m; ++i)
+        if (frozen[lb + i]) mask |= 1u << i;
+    s.push_back(plb::op_pack(plb::OP_SCSUB, depth, ilog2i(m), lb));
+    s.push_back(mask);
+}
+
 // unabridged recursion of sc_decoder.hpp:99-112
 void emit_sc_subtree(int depth, int m, int base, int frozen_at, std::vector<uint32_t>& s) {
+    if (m <= plb::kScSubMax && m >= 2) {
+        uint32_t mask = 0;
+        if (frozen_at >= 0) mask = 1u << (frozen_at - base);
+        s.push_back(plb::op_pack(plb::OP_SCSUB, depth, ilog2i(m), base));
+        s.push_back(mask);
+        return;
+    }
     if (m == 1) {
         s.push_back(plb::op_pack(base == frozen_at ? plb::OP_FROZEN : plb::OP_INFO, depth, 0, base));
         return;
@@ -235,22 +251,41 @@ void emit_sc_subtree(int depth, int m, int base, int frozen_at, std::vector<uint
     s.push_back(plb::op_pack(plb::OP_H, depth, lg, base));
 }
 
-// SC schedule: the walk of sc_decoder.hpp:58-94
-void emit_sc(const std::vector<Node>& t, int ni, std::vector<uint32_t>& s) {
+// SC schedule: the walk of sc_decoder.hpp:58-94.  Branch subtrees of size
+// <= 32 become one OP_SCSUB (unpruned SC recursion; the R0 / REP shortcuts
+// inside them decide identically, the reference's own SSC == SC property,
+// test_sc.cpp:39-74).
+void emit_sc(const std::vector<Node>& t, int ni, std::vector<uint32_t>& s,
+             const uint8_t* frozen) {
     const Node& nd = t[size_t(ni)];
     const int lg = ilog2i(nd.size);
+    if (nd.kind == NK_BRANCH && nd.size <= plb::kScSubMax) {
+        emit_scsub(nd.depth, nd.size, nd.lb, frozen, s);
+        return;
+    }
     switch (nd.kind) {
     case NK_BRANCH:
         s.push_back(plb::op_pack(plb::OP_F, nd.depth, lg, nd.lb));
-        emit_sc(t, nd.left, s);
+        emit_sc(t, nd.left, s, frozen);
         s.push_back(plb::op_pack(plb::OP_G, nd.depth, lg, nd.lb));
-        emit_sc(t, nd.right, s);
+        emit_sc(t, nd.right, s, frozen);
         s.push_back(plb::op_pack(plb::OP_H, nd.depth, lg, nd.lb));
         break;
     case NK_FROZEN:
     case NK_R0: s.push_back(plb::op_pack(plb::OP_FROZEN, nd.depth, lg, nd.lb)); break;
     case NK_INFO: s.push_back(plb::op_pack(plb::OP_INFO, nd.depth, lg, nd.lb)); break;
-    case NK_R1: emit_sc_subtree(nd.depth, nd.size, nd.lb, -1, s); break;
+    case NK_R1: {
+        // Rate-1 shortcut: f keeps the sign product with magnitude min(|a|,|b|)
+        // and, given the left child's hard decisions, g adds magnitudes, so
+        // with no zero input LLR no zero ever appears and the unabridged
+        // recursion returns exactly hard(L).  Zero inputs run the recursion.
+        s.push_back(plb::op_pack(plb::OP_R1SC, nd.depth, lg, nd.lb));
+        const size_t at = s.size();
+        s.push_back(0);
+        emit_sc_subtree(nd.depth, nd.size, nd.lb, -1, s);
+        s[at] = uint32_t(s.size() - at - 1);
+        break;
+    }
     case NK_SPC: emit_sc_subtree(nd.depth, nd.size, nd.lb, nd.lb, s); break;
     case NK_REP: s.push_back(plb::op_pack(plb::OP_REP, nd.depth, lg, nd.lb)); break;
     }
@@ -302,7 +337,7 @@ HostCode make_host_code(const pl_code& c, const pl_decoder& dec) {
     tree.reserve(size_t(2 * c.n));
     build_tree(tree, h.frozen.data(), 0, c.n, 0, pc);
     emit_list(tree, 0, h.sched_list);
-    emit_sc(tree, 0, h.sched_sc);
+    emit_sc(tree, 0, h.sched_sc, h.frozen.data());
 
     if (crc) {
         // affine map: crc(m) = c0 ^ XOR_i m_i col_i over the K message bits;
@@ -788,8 +823,10 @@ int pl_decode_host(pl_handle* h, const void* llr, const int32_t* code_id, int64_
                 ck(cudaEventCreateWithFlags(&h->ev_d2h[i], cudaEventDisableTiming), "event");
             }
         }
+        // >= 8 chunks so the copies of one chunk overlap the decode of another
         const char* cs = std::getenv("PLB_HOST_CHUNK");
-        const int64_t chunk = cs ? std::max<int64_t>(1, std::atoll(cs)) : 65536;
+        const int64_t chunk = cs ? std::max<int64_t>(1, std::atoll(cs))
+                                 : std::clamp<int64_t>((nframes + 7) / 8, 2048, 65536);
         const int64_t in_bytes = h->nmax * int64_t(h->esz);
         // per frame output record: payload | codeword | crc | esc | metric
         const int64_t ob_pay = h->pstride, ob_cw = codeword ? h->cstride : 0;

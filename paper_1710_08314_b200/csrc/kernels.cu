@@ -253,6 +253,7 @@ struct alignas(16) Fixed {
     int32_t st_i1[32], st_i2[32], st_w[32]; // per-rank node statistics
     uint32_t st_a1[32], st_a2[32];
     uint64_t pool[16];       // generic address of each depth pool
+    uint32_t scv[6 * 32];    // OP_SCSUB: per-level LLRs of the subtree, [level][lane]
 };
 static_assert(sizeof(Fixed) % 16 == 0, "fixed area alignment");
 
@@ -959,6 +960,62 @@ __device__ void list_frame(const LaunchParams& P, const DevCode& C, unsigned cha
     __syncwarp();
 }
 
+// SC over a whole subtree of size m <= 32 (OP_SCSUB): lane i owns position
+// lb + i; the LLRs of the node on the current root-to-leaf path at level k
+// live in scv[k][lane] (a level-k node covering [p, p+s) keeps its values in
+// lanes [p, p+s)), partial sums in one register bit per lane.  Visits the
+// leaves in order exactly like sc_decoder.hpp:58-112: G into the right child
+// whose subtree starts at leaf j, F down to the leaf, the hard (or frozen)
+// decision, then the h combines of every node that leaf completes.
+template <typename R>
+__device__ void sc_sub(Ctx<R>& cx, int d, int m, int lb, uint32_t fmask) {
+    using A = Arith<R>;
+    using M = typename A::M;
+    const int lane = cx.lane;
+    const int lgm = __ffs(m) - 1;
+    M* V = reinterpret_cast<M*>(cx.fx->scv);
+    V[lane] = lane < m ? A::val(cx.llr(0, d)[lane]) : M(0);
+    __syncwarp();
+    uint32_t x = 0;
+    #pragma unroll 1
+    for (int j = 0; j < m; ++j) {
+        int k0 = 0;
+        if (j > 0) {
+            const int kk = lgm - __ffs(j); // parent level of the right child starting at j
+            const int h = 1 << (__ffs(j) - 1);
+            const M vk = V[kk * 32 + lane];
+            const M a = __shfl_up_sync(FULL, vk, h);
+            const uint32_t xb = __shfl_up_sync(FULL, x, h);
+            if (lane >= j && lane < j + h)
+                V[(kk + 1) * 32 + lane] = M(A::g(R(a), R(vk), xb));
+            __syncwarp();
+            k0 = kk + 1;
+        }
+        #pragma unroll 1
+        for (int k = k0; k < lgm; ++k) {
+            const int s = m >> k, h = s >> 1, p = j & ~(s - 1);
+            const M vk = V[k * 32 + lane];
+            const M b = __shfl_down_sync(FULL, vk, h);
+            if (lane >= p && lane < p + h) V[(k + 1) * 32 + lane] = M(A::f(R(vk), R(b)));
+            __syncwarp();
+        }
+        if (lane == j) x = ((fmask >> j) & 1u) ? 0u : uint32_t(V[lgm * 32 + j] < M(0));
+        #pragma unroll 1
+        for (int s = 2; s <= m && ((j + 1) & (s - 1)) == 0; s <<= 1) {
+            const int h = s >> 1;
+            const uint32_t o = __shfl_down_sync(FULL, x, h);
+            if (lane >= j + 1 - s && lane < j + 1 - h) x ^= o;
+        }
+    }
+    const uint32_t bits = __ballot_sync(FULL, lane < m && x);
+    if (lane == 0) {
+        const uint32_t mk = m >= 32 ? FULL : ((1u << m) - 1u);
+        uint32_t* w = cx.row(0) + (lb >> 5);
+        *w = (*w & ~(mk << (lb & 31))) | ((bits & mk) << (lb & 31));
+    }
+    __syncwarp();
+}
+
 // ---- one frame, successive cancellation (sc_decoder.hpp:37-125) ---------
 template <typename R>
 __device__ void sc_frame(const LaunchParams& P, const DevCode& C, unsigned char* sm,
@@ -988,6 +1045,31 @@ __device__ void sc_frame(const LaunchParams& P, const DevCode& C, unsigned char*
             const int bit = mfrom<M>(cx.fx->st_a1[0]) < M(0);
             span_fill_warp(row, lb, m, bit, lane);
             __syncwarp();
+            break;
+        }
+        case OP_SCSUB: sc_sub(cx, d, m, lb, __ldg(sched + ++oi)); break;
+        case OP_R1SC: {
+            const int skip = int(__ldg(sched + ++oi));
+            const R* L = cx.llr(0, d);
+            bool zero = false;
+            #pragma unroll 1
+            for (int i = lane; i < m; i += 32) zero |= A::val(L[i]) == M(0);
+            if (__any_sync(FULL, zero)) break; // run the expanded recursion
+            if (m >= 32) {
+                #pragma unroll 1
+                for (int w = 0; w < (m >> 5); ++w) {
+                    const uint32_t hb = __ballot_sync(FULL, A::val(L[(w << 5) + lane]) < M(0));
+                    if (lane == 0) row[(lb >> 5) + w] = hb;
+                }
+            } else {
+                const uint32_t hb = __ballot_sync(FULL, lane < m && A::val(L[lane]) < M(0));
+                if (lane == 0) {
+                    const uint32_t mk = ((1u << m) - 1u) << (lb & 31);
+                    row[lb >> 5] = (row[lb >> 5] & ~mk) | ((hb << (lb & 31)) & mk);
+                }
+            }
+            __syncwarp();
+            oi += skip;
             break;
         }
         default: break;

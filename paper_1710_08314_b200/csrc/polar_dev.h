@@ -25,7 +25,14 @@ enum Op : uint32_t {
     OP_R1 = 5,     // rate-1 node (list only; SC schedules expand it)
     OP_REP = 6,    // repetition node
     OP_SPC = 7,    // single-parity node (list only; SC schedules expand it)
+    OP_SCSUB = 8,  // SC only: a whole subtree of size <= 32 decoded in one op by
+                   // unabridged SC recursion; the next schedule word is its
+                   // frozen mask (bit i = position lb+i frozen)
+    OP_R1SC = 9,   // SC only: rate-1 node.  Next word = length of the expanded
+                   // recursion that follows; when no input LLR is zero the
+                   // recursion's result is the hard decision and it is skipped
 };
+constexpr int kScSubMax = 32;
 
 __host__ __device__ inline uint32_t op_pack(uint32_t op, int depth, int logm, int lb) {
     return op | (uint32_t(depth) << 4) | (uint32_t(logm) << 8) | (uint32_t(lb) << 12);

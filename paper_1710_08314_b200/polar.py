@@ -262,6 +262,23 @@ def channel(code: PolarCode, ebn0_db: float, seed: int, frame0: int, nframes: in
     return info, llr
 
 
+def channel_frames(code: PolarCode, ebn0_db: float, seed: int, frame_ids, llr_out, info_out=None,
+                   precision: str = "f32", scale: float = 0.0, nthreads: int = 0):
+    """Frames keyed by explicit global indices, written into rows of wider
+    batch buffers (mixed-code batches): llr_out[i, :n], info_out[i, :k]."""
+    ids = np.ascontiguousarray(frame_ids, np.uint64)
+    assert llr_out.flags.c_contiguous and llr_out.shape[0] == ids.size
+    c = code.to_c()
+    rc = L.lib().pl_channel_generate_frames(
+        C.byref(c), ebn0_db, seed, ids.ctypes.data_as(C.c_void_p), ids.size,
+        int(Precision[precision]), scale,
+        info_out.ctypes.data_as(C.c_void_p) if info_out is not None else None,
+        info_out.shape[1] if info_out is not None else 0,
+        llr_out.ctypes.data_as(C.c_void_p), llr_out.shape[1], nthreads)
+    if rc:
+        _raise(rc, "channel generation failed")
+
+
 @dataclass
 class DecodeResult:
     """decode_result.hpp:7-14 (payload/codeword as 0/1 numpy arrays)."""

@@ -38,11 +38,14 @@ class Counters:
     frame_errors: int = 0
     esc_sum: int = 0
 
-    def add_batch(self, payload_bits: np.ndarray, info: np.ndarray, esc: np.ndarray):
+    def add_batch(self, payload_bits: np.ndarray, info: np.ndarray, esc: np.ndarray, ks=None):
         """run_frame's counting (sim.cpp:66-71): bit errors on the first K
-        payload bits, a frame error if any."""
+        payload bits, a frame error if any (ks: per-frame K of a mixed batch)."""
         k = info.shape[1]
-        be = (payload_bits[:, :k] != info).sum(1)
+        diff = payload_bits[:, :k] != info
+        if ks is not None:
+            diff &= np.arange(k)[None, :] < np.asarray(ks)[:, None]
+        be = diff.sum(1)
         self.frames += int(info.shape[0])
         self.bit_errors += int(be.sum())
         self.frame_errors += int((be > 0).sum())

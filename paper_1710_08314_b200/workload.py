@@ -61,6 +61,82 @@ def pruning_string(p: P.PruningConfig) -> str:
     return ",".join(parts) or "none"
 
 
+@dataclass
+class MixedWorkload:
+    """configs[3]: N in {128..1024} x R in {1/3,1/2,2/3,5/6}, K = floor(N R),
+    CRC-11 (0x621) or CRC-24 (0xB2B117) (non-reflected, zero init/xorout,
+    SURVEY §B), per-code GA frozen sets at the operating point; the infeasible
+    (128, 5/6, CRC-24) pair (K + 24 > 128) is dropped: 31 codes.  Each frame's
+    code is a seeded draw keyed by its global index."""
+    name: str = "cfg3_mixed_mcs_ca_scl_L8_f32"
+    kind: str = "ca_sscl"
+    l: int = 8
+    precision: str = "f32"
+    pruning: P.PruningConfig = P.PruningConfig()
+    ebn0_db: float = 3.0
+    frames: int = 524288
+    scale: float = 0.0
+    design_db: float = 3.0
+    n: int = 1024  # the widest code (LLR row stride)
+
+    def code_list(self):
+        out = []
+        for n in (128, 256, 512, 1024):
+            for num, den in ((1, 3), (1, 2), (2, 3), (5, 6)):
+                k = n * num // den
+                for crc in ("11:621:0:0:0", "24:b2b117:0:0:0"):
+                    w = P.CrcSpec.parse(crc).width
+                    if k + w > n:
+                        continue
+                    fz = P.construct_frozen_ga(n, k + w, self.design_db, k / n)
+                    out.append(P.make_code(n, k, fz, crc))
+        return out
+
+    def code_ids(self, frame0: int, nframes: int, ncodes: int, seed: int = 42):
+        idx = np.arange(frame0, frame0 + nframes, dtype=np.uint64)
+        h = (idx * np.uint64(0x9E3779B97F4A7C15)) ^ np.uint64(seed)
+        h ^= h >> np.uint64(31)
+        h *= np.uint64(0xBF58476D1CE4E5B9)
+        h ^= h >> np.uint64(29)
+        return (h % np.uint64(ncodes)).astype(np.int32)
+
+    def describe(self) -> dict:
+        return {"workload": self.name, "N": "128..1024", "K": "floor(N*R)", "crc": "CRC-11/CRC-24",
+                "decoder": self.kind, "L": self.l, "llr": self.precision,
+                "pruning": pruning_string(self.pruning), "ebn0_db": self.ebn0_db,
+                "frames_per_gpu": self.frames, "frozen": f"ga@{self.design_db}dB per code",
+                "codes": 31}
+
+
+def make_batch(wl, frame0: int, nframes: int, seed: int = 42, nthreads: int = 0):
+    """Host inputs for a bench step: (codes, code_id or None, info (F, kmax),
+    k per frame, llr (F, stride)), frames keyed by global index."""
+    dt = np.float32 if wl.precision == "f32" else np.int8
+    if isinstance(wl, MixedWorkload):
+        codes = wl.code_list()
+        cid = wl.code_ids(frame0, nframes, len(codes), seed)
+        nmax = max(c.n for c in codes)
+        kmax = max(c.k for c in codes)
+        llr = np.zeros((nframes, nmax), dt)
+        info = np.zeros((nframes, kmax), np.uint8)
+        ks = np.zeros(nframes, np.int32)
+        for i, c in enumerate(codes):
+            rows = np.flatnonzero(cid == i)
+            if rows.size == 0:
+                continue
+            tl = np.zeros((rows.size, nmax), dt)
+            ti = np.zeros((rows.size, kmax), np.uint8)
+            P.channel_frames(c, wl.ebn0_db, seed, rows.astype(np.uint64) + np.uint64(frame0), tl, ti,
+                             wl.precision, wl.scale, nthreads)
+            llr[rows] = tl
+            info[rows] = ti
+            ks[rows] = c.k
+        return codes, cid, info, ks, llr
+    code = wl.code()
+    info, llr = P.channel(code, wl.ebn0_db, seed, frame0, nframes, wl.precision, wl.scale, nthreads)
+    return [code], None, info, np.full(nframes, code.k, np.int32), llr
+
+
 WORKLOADS = {
     # configs[0]: CA-SCL L=4, float, 4.5 dB, 65 536 frames
     "cfg0": Workload("cfg0_ca_scl_L4_f32", 2048, 1723, "32-GZIP", "ca_sscl", 4, "f32",
@@ -75,6 +151,16 @@ WORKLOADS = {
                          P.PruningConfig(), 3.5, 1048576),
     "cfg2_4.5": Workload("cfg2_fa_scl_L32_f32@4.5dB", 2048, 1723, "32-GZIP", "fa_sscl", 32, "f32",
                          P.PruningConfig(), 4.5, 1048576),
+    # configs[3]: mixed MCS, CA-SCL L=8, float, 3 dB, 524 288 frames
+    "cfg3": MixedWorkload(),
+    # configs[4]: N=2048, K=1024 + CRC-32, CA-SCL L in {8,16,32}; one SNR
+    # point per bench step (the 1..4 dB sweep runs through sweep.py)
+    "cfg4_L8": Workload("cfg4_ca_scl_L8_f32@2.5dB", 2048, 1024, "32-GZIP", "ca_sscl", 8, "f32",
+                        P.PruningConfig(), 2.5, 65536, design_db=2.5),
+    "cfg4_L16": Workload("cfg4_ca_scl_L16_f32@2.5dB", 2048, 1024, "32-GZIP", "ca_sscl", 16, "f32",
+                         P.PruningConfig(), 2.5, 65536, design_db=2.5),
+    "cfg4_L32": Workload("cfg4_ca_scl_L32_f32@2.5dB", 2048, 1024, "32-GZIP", "ca_sscl", 32, "f32",
+                         P.PruningConfig(), 2.5, 32768, design_db=2.5),
 }
 
 

@@ -213,6 +213,46 @@ def test_gpu_ml_on_tiny_code(P, gpu):
             assert met[f] == best
 
 
+def test_cfg3_mixed_codes_one_batch(P, gpu, oracle_lib):
+    """Mixed-MCS: 31 codes (N 128..1024, CRC-11/24) in one batch with a
+    per-frame code id; every frame equals the oracle of its own code."""
+    from paper_1710_08314_b200.workload import MixedWorkload, make_batch
+
+    wl = MixedWorkload()
+    codes, cid, info, ks, llr = make_batch(wl, 0, 1024)
+    assert len(codes) == 31 and len(set(cid.tolist())) == 31
+    dec = P.FrameDecoder(codes, "ca_sscl", 8, "f32", P.PruningConfig())
+    o = dec.decode_batch(gpu.from_numpy(llr).cuda(), code_id=gpu.from_numpy(cid).cuda(), codeword=True)
+    gpu.cuda.synchronize()
+    got = {k: v.cpu().numpy() for k, v in o.items() if v is not None}
+    for i, c in enumerate(codes):
+        rows = np.flatnonzero(cid == i)
+        ref = _oracle(c, "ca_sscl", 8, "f32", P.PruningConfig()).decode(np.ascontiguousarray(llr[rows, :c.n]))
+        pb, cb = (c.payload_size + 7) // 8, (c.n + 7) // 8
+        assert np.array_equal(got["payload"][rows, :pb], ref.payload), c.n
+        assert np.array_equal(got["codeword"][rows, :cb], ref.codeword), c.n
+        assert np.array_equal(got["crc_ok"][rows], ref.crc_ok), c.n
+        assert np.array_equal(got["metric"][rows], ref.metric.astype(np.float32)), c.n
+
+
+def test_decode_host_matches_device_path(P, gpu):
+    """pl_decode_host (pageable and pinned buffers, chunked) == pl_decode."""
+    import os
+
+    code = _code(P, 1024, 480, "32-GZIP")
+    _, llr = P.channel(code, 2.0, 9, 0, 3000, "i8", 4.0)
+    dec = P.FrameDecoder(code, "fa_sscl", 16, "i8", P.PruningConfig(rep_max=8))
+    o = dec.decode_batch(gpu.from_numpy(llr).cuda())
+    gpu.cuda.synchronize()
+    os.environ["PLB_HOST_CHUNK"] = "700"
+    try:
+        h = dec.decode_host(llr)
+    finally:
+        del os.environ["PLB_HOST_CHUNK"]
+    for k in ("payload", "crc_ok", "esc", "metric"):
+        assert np.array_equal(h[k], o[k].cpu().numpy()), k
+
+
 def test_cfg4_like_l32(P, gpu, oracle_lib):
     code = _code(P, 2048, 1024, "32-GZIP")
     _, llr = P.channel(code, 1.5, 42, 0, 24, "f32")

@@ -162,6 +162,31 @@ def test_host_channel_is_the_reference_channel(P):
     assert np.array_equal(info8, z["info8"]) and np.array_equal(llr8, z["llr8"])
 
 
+def test_frame_keyed_channel_matches_range_channel(P):
+    """pl_channel_generate_frames with explicit global indices == the range
+    form; rows land in a wider batch."""
+    code = P.make_code(256, 100, P.construct_frozen(256, 116, 0.5), "16-CCITT")
+    info, llr = P.channel(code, 2.0, 5, 40, 12, "f32")
+    ids = np.arange(40, 52)[::-1].copy()
+    wl = np.zeros((12, 300), np.float32)
+    wi = np.zeros((12, 130), np.uint8)
+    P.polar.channel_frames(code, 2.0, 5, ids, wl, wi, "f32")
+    assert np.array_equal(wl[:, :256], llr[::-1]) and np.array_equal(wi[:, :100], info[::-1])
+    assert not wl[:, 256:].any() and not wi[:, 100:].any()
+
+
+def test_mixed_mcs_workload_codes(P):
+    from paper_1710_08314_b200.workload import MixedWorkload
+
+    wl = MixedWorkload()
+    codes = wl.code_list()
+    assert len(codes) == 31  # (128, 5/6, CRC-24) is infeasible
+    assert {c.n for c in codes} == {128, 256, 512, 1024}
+    cid = wl.code_ids(0, 100000, 31)
+    counts = np.bincount(cid, minlength=31)
+    assert counts.min() > 0.8 * 100000 / 31 and np.array_equal(cid, wl.code_ids(0, 100000, 31))
+
+
 def test_channel_codewords_are_systematic_and_crc_valid(P):
     code = P.make_code(256, 100, P.construct_frozen(256, 116, 0.5), "16-CCITT")
     info, llr = P.channel(code, 30.0, 1, 0, 16, "f32")  # noiseless limit
