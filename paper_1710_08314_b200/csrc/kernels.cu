@@ -183,38 +183,42 @@ __device__ __forceinline__ K bitonic_lanes(K key, int lane) {
     return key;
 }
 
-// 32*C keys at sorted position s = k*32 + lane (register k of lane).
-template <typename K, int C>
-__device__ __forceinline__ void bitonic_regs(K (&key)[C], int lane) {
-    constexpr int NT = 32 * C;
+// The 32 smallest of two ascending 32-key lane sequences, ascending: the
+// element-wise min of a and reversed b is a bitonic sequence holding exactly
+// those 32 keys; one bitonic merge sorts it.
+template <typename K>
+__device__ __forceinline__ K merge_top32(K a, K b, int lane) {
+    K c = kmin(a, __shfl_sync(FULL, b, 31 - lane));
 #pragma unroll
-    for (int size = 2; size <= NT; size <<= 1) {
-#pragma unroll
-        for (int j = size >> 1; j > 0; j >>= 1) {
-            if (j >= 32) {
-                const int jr = j >> 5;
-#pragma unroll
-                for (int k = 0; k < C; ++k) {
-                    const int kp = k ^ jr;
-                    if (kp > k) {
-                        const bool asc = ((k * 32 + lane) & size) == 0;
-                        const K a = key[k], b = key[kp];
-                        const K lo = kmin(a, b), hi = kmax(a, b);
-                        key[k] = asc ? lo : hi;
-                        key[kp] = asc ? hi : lo;
-                    }
-                }
-            } else {
-#pragma unroll
-                for (int k = 0; k < C; ++k) {
-                    const K o = shfl_xor_k(key[k], j);
-                    const bool asc = ((k * 32 + lane) & size) == 0;
-                    const bool lower = (lane & j) == 0;
-                    key[k] = (lower == asc) ? kmin(key[k], o) : kmax(key[k], o);
-                }
-            }
-        }
+    for (int j = 16; j > 0; j >>= 1) {
+        const K o = shfl_xor_k(c, j);
+        c = (lane & j) == 0 ? kmin(c, o) : kmax(c, o);
     }
+    return c;
+}
+template <>
+__device__ __forceinline__ uint64_t merge_top32<uint64_t>(uint64_t a, uint64_t b, int lane) {
+    const uint64_t br = (uint64_t(__shfl_sync(FULL, uint32_t(b >> 32), 31 - lane)) << 32) |
+                        __shfl_sync(FULL, uint32_t(b), 31 - lane);
+    uint64_t c = kmin(a, br);
+#pragma unroll
+    for (int j = 16; j > 0; j >>= 1) {
+        const uint64_t o = shfl_xor_k(c, j);
+        c = (lane & j) == 0 ? kmin(c, o) : kmax(c, o);
+    }
+    return c;
+}
+
+// The 32 smallest of 32*C keys (register k of each lane), ascending in
+// register 0: sort each register across the lanes, then merge pairwise.
+template <typename K, int C>
+__device__ __forceinline__ void top32_regs(K (&key)[C], int lane) {
+#pragma unroll
+    for (int k = 0; k < C; ++k) key[k] = bitonic_lanes<K, 32>(key[k], lane);
+#pragma unroll
+    for (int w = 1; w < C; w <<= 1)
+#pragma unroll
+        for (int k = 0; k + w < C; k += 2 * w) key[k] = merge_top32(key[k], key[k + w], lane);
 }
 
 // ---- vector access of G consecutive values ----------------------------
@@ -526,7 +530,8 @@ __device__ void fork_apply(Ctx<R>& cx, const typename Arith<R>::M (&cm)[CPL],
         if (ncand <= 16) key[0] = bitonic_lanes<K, 16>(key[0], lane);
         else key[0] = bitonic_lanes<K, 32>(key[0], lane);
     } else {
-        bitonic_regs<K, CPL>(key, lane);
+        // only the best keep <= 32 are needed, in order
+        top32_regs<K, CPL>(key, lane);
     }
     const int keep = min(cx.l, ncand);
     const bool kept = lane < keep;
