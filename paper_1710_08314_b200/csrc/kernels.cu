@@ -979,38 +979,69 @@ __device__ void sc_sub(Ctx<R>& cx, int d, int m, int lb, uint32_t fmask) {
     const int lane = cx.lane;
     const int lgm = __ffs(m) - 1;
     M* V = reinterpret_cast<M*>(cx.fx->scv);
-    V[lane] = lane < m ? A::val(cx.llr(0, d)[lane]) : M(0);
+    const M v0 = lane < m ? A::val(cx.llr(0, d)[lane]) : M(0);
+    V[lane] = v0;
     __syncwarp();
     uint32_t x = 0;
+    int j = 0, k = 0; // next leaf; level of the node entered at leaf j
+    M vk = v0;        // V[k][lane]
     #pragma unroll 1
-    for (int j = 0; j < m; ++j) {
-        int k0 = 0;
-        if (j > 0) {
-            const int kk = lgm - __ffs(j); // parent level of the right child starting at j
-            const int h = 1 << (__ffs(j) - 1);
-            const M vk = V[kk * 32 + lane];
-            const M a = __shfl_up_sync(FULL, vk, h);
-            const uint32_t xb = __shfl_up_sync(FULL, x, h);
-            if (lane >= j && lane < j + h)
-                V[(kk + 1) * 32 + lane] = M(A::g(R(a), R(vk), xb));
-            __syncwarp();
-            k0 = kk + 1;
-        }
+    while (true) {
+        // Descend from the node at level k covering [j, j + s).  Two exact
+        // sub-node shortcuts: all frozen -> codeword 0; all information with
+        // no zero input -> hard decisions (see the rate-1 argument in
+        // host.cu emit_sc); otherwise F into the left child.
+        int last, done; // last leaf and size of the node just completed
         #pragma unroll 1
-        for (int k = k0; k < lgm; ++k) {
-            const int s = m >> k, h = s >> 1, p = j & ~(s - 1);
-            const M vk = V[k * 32 + lane];
+        while (true) {
+            const int s = m >> k;
+            const uint32_t mk = s >= 32 ? FULL : ((1u << s) - 1u);
+            const uint32_t fm = (fmask >> j) & mk;
+            const bool mine = lane >= j && lane < j + s;
+            done = s;
+            last = j + s - 1;
+            if (fm == mk) {
+                if (mine) x = 0u;
+                break;
+            }
+            if (fm == 0u && !__any_sync(FULL, mine && vk == M(0))) {
+                if (mine) x = uint32_t(vk < M(0)); // the node's codeword
+                break;
+            }
+            // (s == 1 is always one of the two cases above or a zero-LLR info
+            // leaf, whose hard decision is 0)
+            if (s == 1) {
+                if (mine) x = 0u;
+                break;
+            }
+            const int h = s >> 1;
             const M b = __shfl_down_sync(FULL, vk, h);
-            if (lane >= p && lane < p + h) V[(k + 1) * 32 + lane] = M(A::f(R(vk), R(b)));
+            const M fv = M(A::f(R(vk), R(b)));
+            if (lane >= j && lane < j + h) V[(k + 1) * 32 + lane] = fv;
+            vk = fv;
+            ++k;
             __syncwarp();
         }
-        if (lane == j) x = ((fmask >> j) & 1u) ? 0u : uint32_t(V[lgm * 32 + j] < M(0));
+        // h combines of every enclosing node completed by leaf `last`
         #pragma unroll 1
-        for (int s = 2; s <= m && ((j + 1) & (s - 1)) == 0; s <<= 1) {
+        for (int s = 2 * done; s <= m && ((last + 1) & (s - 1)) == 0; s <<= 1) {
             const int h = s >> 1;
             const uint32_t o = __shfl_down_sync(FULL, x, h);
-            if (lane >= j + 1 - s && lane < j + 1 - h) x ^= o;
+            if (lane >= last + 1 - s && lane < last + 1 - h) x ^= o;
         }
+        j = last + 1;
+        if (j >= m) break;
+        // G into the right child that starts at leaf j
+        const int kk = lgm - __ffs(j);
+        const int h = 1 << (__ffs(j) - 1);
+        const M pv = V[kk * 32 + lane];
+        const M a = __shfl_up_sync(FULL, pv, h);
+        const uint32_t xb = __shfl_up_sync(FULL, x, h);
+        const M gv = M(A::g(R(a), R(pv), xb));
+        if (lane >= j && lane < j + h) V[(kk + 1) * 32 + lane] = gv;
+        vk = gv;
+        k = kk + 1;
+        __syncwarp();
     }
     const uint32_t bits = __ballot_sync(FULL, lane < m && x);
     if (lane == 0) {

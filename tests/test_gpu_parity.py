@@ -80,6 +80,24 @@ def test_rough_llrs_all_kinds(P, gpu, oracle_lib, n, k, crc, prec):
 
 
 @pytest.mark.parametrize("prec", ["f32", "i8"])
+def test_sc_rung_shortcuts_adversarial(P, gpu, oracle_lib, prec):
+    """The SC rung's exact shortcuts (rate-1 hard decision unless an input is
+    zero, all-frozen sub-nodes, in-lane subtree recursion) under LLRs full of
+    zeros, ties and saturation, on large codes of several rates."""
+    rng = np.random.default_rng(4242 + (prec == "i8"))
+    for n, k, crc in [(1024, 300, "16-CCITT"), (2048, 1723, "32-GZIP"), (2048, 600, "8")]:
+        code = _code(P, n, k, crc)
+        llr = rough_llrs(rng, n, 40, prec)
+        for kind in ("sc", "ssc", "fa_sscl"):
+            check_parity(P, gpu, code, kind, 4, prec, P.PruningConfig(), llr, "sc-rough")
+        # sparse zeros in otherwise clean frames exercise the zero fallback
+        _, clean = P.channel(code, 3.0, 11, 0, 40, prec, 4.0 if prec == "i8" else 0.0)
+        clean = clean.copy()
+        clean[rng.random(clean.shape) < 0.01] = 0
+        check_parity(P, gpu, code, "ssc", 1, prec, P.PruningConfig(), clean, "sc-zeros")
+
+
+@pytest.mark.parametrize("prec", ["f32", "i8"])
 def test_awgn_mid_codes(P, gpu, oracle_lib, prec):
     rng_seed = 7
     for n, k, crc, snr in [(256, 100, "16-CCITT", 2.0), (1024, 480, "32-GZIP", 2.0)]:
