@@ -578,7 +578,7 @@ __device__ void fork_apply(Ctx<R>& cx, const typename Arith<R>::M (&cm)[CPL],
         const int nd = __popc(dupm);
         if (cx.rw >= 4) {
             const int n4 = (nw + 3) >> 2;
-            const int lg = ilog2(n4);
+            const int lg = n4 > 1 ? 32 - __clz(n4 - 1) : 0; // ceil(log2(n4))
             #pragma unroll 1
             for (int t = lane; t < (nd << lg); t += 32) {
                 const int k = t >> lg, q = t & ((1 << lg) - 1);
