@@ -681,6 +681,32 @@ __device__ void r1spc_stats(Ctx<R>& cx, int d, int m, int lb, int na) {
     const int r = cx.lane >> lglp, l0 = cx.lane & (lp - 1);
     const bool ok = r < na;
     const int p = cx.fx->alive_list[ok ? r : 0];
+    if (E == 1) {
+        // one value per lane (lp == m): every path's hard bits in one ballot
+        const M v = ok ? A::val(cx.llr(p, d)[l0]) : M(0);
+        const unsigned hb = __ballot_sync(FULL, ok && v < M(0));
+        const uint32_t mk = m >= 32 ? FULL : ((1u << m) - 1u);
+        const uint32_t gb = (hb >> (cx.lane & ~(lp - 1))) & mk;
+        K k1 = ok ? A::make_key(A::mag(v), l0) : A::kKeyMax, k2 = A::kKeyMax;
+        for (int off = 1; off < lp; off <<= 1) {
+            const K o1 = shfl_xor_k(k1, off), o2 = shfl_xor_k(k2, off);
+            const K n1 = kmin(k1, o1);
+            k2 = kmin(kmax(k1, o1), kmin(k2, o2));
+            k1 = n1;
+        }
+        if (ok && l0 == 0) {
+            uint32_t* w = cx.row(p) + (lb >> 5);
+            const int sh = lb & 31;
+            *w = (*w & ~(mk << sh)) | (gb << sh);
+            cx.fx->st_i1[r] = A::key_idx(k1);
+            cx.fx->st_i2[r] = A::key_idx(k2);
+            cx.fx->st_a1[r] = mbits<M>(A::key_val(k1));
+            cx.fx->st_a2[r] = mbits<M>(A::key_val(k2));
+            cx.fx->st_w[r] = __popc(gb) & 1;
+        }
+        __syncwarp();
+        return;
+    }
     const int i0 = l0 * E;
     const R* L = cx.llr(p, d) + i0;
     uint32_t* span = cx.row(p) + (lb >> 5);
