@@ -372,6 +372,7 @@ struct RungCfg {
     int smem_per_warp = 0;
     int64_t gscratch_per_warp = 0;
     int grid = 0;
+    int wpb = plb::kMaxWarpsPerBlock;
 };
 
 } // namespace
@@ -441,19 +442,28 @@ RungCfg plan_rung(const pl_handle& h, int l, bool list) {
     if (cands.empty()) cands.push_back(h.nmax); // tiny codes: everything in shared memory
     RungCfg best;
     best.l = l;
-    for (int seg : cands) {
-        RungCfg c;
-        c.l = l;
-        c.seg_max = seg;
-        c.smem_per_warp = int(plb::smem_bytes_per_warp(h.nmax, l, h.esz, seg));
-        c.gscratch_per_warp = plb::gscratch_bytes_per_warp(h.nmax, l, h.esz, seg);
-        const int smem = c.smem_per_warp * plb::kWarpsPerBlock;
-        const int nb = list ? plb::occupancy_list(h.dec.precision, l, smem)
-                            : plb::occupancy_sc(h.dec.precision, smem);
-        if (nb <= 0) continue;
-        c.grid = nb * h.sms;
-        if (c.grid > best.grid) best = c;
-        if (nb * plb::kWarpsPerBlock >= target) break;
+    int best_warps = 0;
+    // 4-warp blocks first; 2 / 1 when a warp's area is too big (large N x L)
+    for (int wpb = plb::kMaxWarpsPerBlock; wpb >= 1; wpb >>= 1) {
+        for (int seg : cands) {
+            RungCfg c;
+            c.l = l;
+            c.seg_max = seg;
+            c.wpb = wpb;
+            c.smem_per_warp = int(plb::smem_bytes_per_warp(h.nmax, l, h.esz, seg));
+            c.gscratch_per_warp = plb::gscratch_bytes_per_warp(h.nmax, l, h.esz, seg);
+            const int smem = c.smem_per_warp * wpb;
+            const int nb = list ? plb::occupancy_list(h.dec.precision, l, smem, wpb)
+                                : plb::occupancy_sc(h.dec.precision, smem, wpb);
+            if (nb <= 0) continue;
+            c.grid = nb * h.sms;
+            if (nb * wpb > best_warps) {
+                best = c;
+                best_warps = nb * wpb;
+            }
+            if (nb * wpb >= target) break;
+        }
+        if (best_warps >= target) break;
     }
     if (best.grid <= 0) throw ConfigError("no launch configuration fits this code / list size on the device");
     return best;
@@ -517,6 +527,7 @@ void run_decode(pl_handle& h, const void* llr, const int32_t* code_id, int64_t n
         p.smem_per_warp = rc.smem_per_warp;
         p.gscratch_per_warp = rc.gscratch_per_warp;
         p.esc_level = rc.l;
+        p.wpb = rc.wpb;
         if (h.profiling) {
             while (h.prof_ev.size() < size_t(2 * (slot + 1))) {
                 cudaEvent_t ev;
@@ -705,7 +716,7 @@ int pl_create(const pl_code* codes, int32_t ncodes, const pl_decoder* dec, int32
             h->rungs.push_back(plan_rung(*h, l, true));
         int64_t gs = 0;
         auto acc = [&](const RungCfg& r) {
-            gs = std::max<int64_t>(gs, int64_t(r.grid) * plb::kWarpsPerBlock * r.gscratch_per_warp);
+            gs = std::max<int64_t>(gs, int64_t(r.grid) * r.wpb * r.gscratch_per_warp);
         };
         if (h->sc_cfg.grid) acc(h->sc_cfg);
         for (const auto& r : h->rungs) acc(r);

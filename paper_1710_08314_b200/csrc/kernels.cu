@@ -1156,10 +1156,10 @@ __device__ void sc_frame(const LaunchParams& P, const DevCode& C, unsigned char*
 // CW = 0: SC pass; CW = 1/2/4: list pass with CW candidates per lane
 // (L <= 8 / 16 / 32).
 template <typename R, int CW>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, PLB_MINBLOCKS) decode_kernel(const LaunchParams P) {
+__global__ void __launch_bounds__(kMaxWarpsPerBlock * 32, PLB_MINBLOCKS) decode_kernel(const LaunchParams P) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int64_t gw = int64_t(blockIdx.x) * kWarpsPerBlock + wib;
+    const int64_t gw = int64_t(blockIdx.x) * (blockDim.x >> 5) + wib;
     unsigned char* sm = smem_raw + wib * P.smem_per_warp;
     unsigned char* gs = static_cast<unsigned char*>(P.gscratch) + gw * P.gscratch_per_warp;
     const long long count = P.frame_list ? (long long)(*P.frame_count) : (long long)P.nframes;
@@ -1221,22 +1221,26 @@ int cw_of(int l, bool list) { return !list ? 0 : l <= 8 ? 1 : l <= 16 ? 2 : 4; }
 
 template <typename R>
 cudaError_t launch(const LaunchParams& p, int cw, int grid, cudaStream_t s) {
-    const int smem = p.smem_per_warp * kWarpsPerBlock;
+    const int smem = p.smem_per_warp * p.wpb;
     auto kern = kernel_for<R>(cw);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    kern<<<grid, kWarpsPerBlock * 32, smem, s>>>(p);
+    kern<<<grid, p.wpb * 32, smem, s>>>(p);
     return cudaGetLastError();
 }
 
 template <typename R>
-int occupancy(int cw, int smem) {
+int occupancy(int cw, int smem, int wpb) {
     auto kern = kernel_for<R>(cw);
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
+        cudaGetLastError();
         return 0;
+    }
     int nb = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kWarpsPerBlock * 32, smem) != cudaSuccess)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, wpb * 32, smem) != cudaSuccess) {
+        cudaGetLastError();
         return 0;
+    }
     return nb;
 }
 
@@ -1256,12 +1260,12 @@ cudaError_t launch_list(const LaunchParams& p, int precision, int grid, cudaStre
     const int cw = cw_of(p.l, true);
     return precision == 0 ? launch<float>(p, cw, grid, s) : launch<int8_t>(p, cw, grid, s);
 }
-int occupancy_sc(int precision, int smem) {
-    return precision == 0 ? occupancy<float>(0, smem) : occupancy<int8_t>(0, smem);
+int occupancy_sc(int precision, int smem, int wpb) {
+    return precision == 0 ? occupancy<float>(0, smem, wpb) : occupancy<int8_t>(0, smem, wpb);
 }
-int occupancy_list(int precision, int l, int smem) {
+int occupancy_list(int precision, int l, int smem, int wpb) {
     const int cw = cw_of(l, true);
-    return precision == 0 ? occupancy<float>(cw, smem) : occupancy<int8_t>(cw, smem);
+    return precision == 0 ? occupancy<float>(cw, smem, wpb) : occupancy<int8_t>(cw, smem, wpb);
 }
 
 cudaError_t kernel_selftest(unsigned long long* mismatches) {

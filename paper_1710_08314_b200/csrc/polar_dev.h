@@ -82,9 +82,10 @@ struct LaunchParams {
     int32_t nmax;              // largest n over the codes
     int32_t smem_per_warp;     // bytes
     int32_t esc_level;         // value written to esc[] by this pass
+    int32_t wpb;               // warps per block (1, 2 or 4)
 };
 
-constexpr int kWarpsPerBlock = 4;
+constexpr int kMaxWarpsPerBlock = 4; // a block is 1, 2 or 4 independent warps
 
 // Bytes of shared memory / global scratch one warp needs for a pass.
 int64_t smem_bytes_per_warp(int nmax, int l, int elem_bytes, int seg_smem_max);
@@ -94,8 +95,8 @@ int64_t gscratch_bytes_per_warp(int nmax, int l, int elem_bytes, int seg_smem_ma
 cudaError_t launch_sc(const LaunchParams& p, int precision, int grid, cudaStream_t s);
 cudaError_t launch_list(const LaunchParams& p, int precision, int grid, cudaStream_t s);
 // Max resident blocks per SM for a kernel at the given dynamic smem.
-int occupancy_sc(int precision, int smem_bytes);
-int occupancy_list(int precision, int l, int smem_bytes);
+int occupancy_sc(int precision, int smem_bytes, int wpb);
+int occupancy_list(int precision, int l, int smem_bytes, int wpb);
 // Exhaustive device check of the packed int8 f/g against the scalar kernels.
 cudaError_t kernel_selftest(unsigned long long* mismatches);
 
