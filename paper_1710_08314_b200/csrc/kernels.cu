@@ -509,7 +509,7 @@ enum ApplyKind { AK_BIT = 0, AK_BCAST = 1, AK_FLIPS = 2 };
 
 // fork_apply (list_decoder.hpp:339-387) for ncand candidates held as
 // candidate i = lane + 32k in register k.  aux = a | b << 16 (int16 each).
-template <typename R, int CPL>
+template <typename R, int CPL, int MAXW>
 __device__ void fork_apply(Ctx<R>& cx, const typename Arith<R>::M (&cm)[CPL],
                            const int (&csrc)[CPL], const int (&caux)[CPL], int ncand,
                            int kind, int lb, int m) {
@@ -526,9 +526,9 @@ __device__ void fork_apply(Ctx<R>& cx, const typename Arith<R>::M (&cm)[CPL],
         key[k] = i < ncand ? A::make_key(cm[k], i) : A::kKeyMax;
     }
     if constexpr (CPL == 1) {
-        // two network widths: 2 candidates/path forks at L <= 8 need 16
-        if (ncand <= 16) key[0] = bitonic_lanes<K, 16>(key[0], lane);
-        else key[0] = bitonic_lanes<K, 32>(key[0], lane);
+        // two network widths per kernel: MAXW = 4L (<= 32) and MAXW/2
+        if (MAXW > 4 && ncand <= MAXW / 2) key[0] = bitonic_lanes<K, (MAXW > 4 ? MAXW / 2 : 4)>(key[0], lane);
+        else key[0] = bitonic_lanes<K, MAXW>(key[0], lane);
     } else {
         // only the best keep <= 32 are needed, in order
         top32_regs<K, CPL>(key, lane);
@@ -813,7 +813,7 @@ __device__ void rep_pen(Ctx<R>& cx, int d, int m, int na) {
 // (ascending slot, then candidate number, list_decoder.hpp:240-333), one
 // shared fork_apply, normalisation.  C = candidates per lane, fixed per
 // kernel instantiation (4L <= 32C).
-template <typename R, int C>
+template <typename R, int C, int MAXW>
 __device__ void list_fork_node(Ctx<R>& cx, int code, int d, int m, int lb, int na) {
     using A = Arith<R>;
     using M = typename A::M;
@@ -855,7 +855,7 @@ __device__ void list_fork_node(Ctx<R>& cx, int code, int d, int m, int lb, int n
         }
     }
     const int kind = code == OP_INFO ? AK_BIT : code == OP_REP ? AK_BCAST : AK_FLIPS;
-    fork_apply<R, C>(cx, cm, cs, cax, na << lgb, kind, lb, code == OP_INFO ? 1 : m);
+    fork_apply<R, C, MAXW>(cx, cm, cs, cax, na << lgb, kind, lb, code == OP_INFO ? 1 : m);
     cx.normalize();
 }
 
@@ -934,11 +934,17 @@ __device__ __forceinline__ long long claim(const LaunchParams& P, int lane) {
 }
 
 // ---- one frame, list decoding at list size P.l --------------------------
-template <typename R, int CW>
+// Kernel variant KV (1..6) <-> list size 1, 2, 4, 8, 16, 32: candidates per
+// lane CW and the widest ranking network MAXW = min(32, 4L).
+__host__ __device__ constexpr int kv_cw(int kv) { return kv >= 6 ? 4 : kv == 5 ? 2 : 1; }
+__host__ __device__ constexpr int kv_maxw(int kv) { return kv == 1 ? 4 : kv == 2 ? 8 : kv == 3 ? 16 : 32; }
+
+template <typename R, int KV>
 __device__ void list_frame(const LaunchParams& P, const DevCode& C, unsigned char* sm,
                            unsigned char* gs, int frame, int lane) {
     using A = Arith<R>;
     using M = typename A::M;
+    constexpr int CW = kv_cw(KV), MAXW = kv_maxw(KV);
     Ctx<R> cx;
     setup_ctx(cx, P, C, sm, gs, frame, lane, P.l);
     const uint32_t* sched = C.sched_list;
@@ -951,7 +957,7 @@ __device__ void list_frame(const LaunchParams& P, const DevCode& C, unsigned cha
         if (code <= OP_G) op_fg(cx, d, m, lb, na, code == OP_G);
         else if (code == OP_H) op_h(cx, m, lb, na);
         else if (code == OP_FROZEN) list_frozen(cx, d, m, lb, na);
-        else list_fork_node<R, CW>(cx, code, d, m, lb, na);
+        else list_fork_node<R, CW, MAXW>(cx, code, d, m, lb, na);
     }
     // finish (list_decoder.hpp:457-502): stable order by (metric, slot)
     using K = typename A::Key;
@@ -1153,9 +1159,8 @@ __device__ void sc_frame(const LaunchParams& P, const DevCode& C, unsigned char*
 #define PLB_MINBLOCKS 8
 #endif
 
-// CW = 0: SC pass; CW = 1/2/4: list pass with CW candidates per lane
-// (L <= 8 / 16 / 32).
-template <typename R, int CW>
+// KV = 0: SC pass; KV = 1..6: list pass at L = 1, 2, 4, 8, 16, 32.
+template <typename R, int KV>
 __global__ void __launch_bounds__(kMaxWarpsPerBlock * 32, PLB_MINBLOCKS) decode_kernel(const LaunchParams P) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -1169,7 +1174,7 @@ __global__ void __launch_bounds__(kMaxWarpsPerBlock * 32, PLB_MINBLOCKS) decode_
         const int frame = P.frame_list ? P.frame_list[idx] : int(idx);
         const int cid = P.code_id ? P.code_id[frame] : 0;
         const DevCode C = P.codes[cid];
-        if constexpr (CW > 0) list_frame<R, CW>(P, C, sm, gs, frame, lane);
+        if constexpr (KV > 0) list_frame<R, KV>(P, C, sm, gs, frame, lane);
         else sc_frame<R>(P, C, sm, gs, frame, lane);
     }
 }
@@ -1208,16 +1213,25 @@ __global__ void selftest_kernel(unsigned long long* bad) {
 }
 
 template <typename R>
-void (*kernel_for(int cw))(LaunchParams) {
-    switch (cw) {
+void (*kernel_for(int kv))(LaunchParams) {
+    switch (kv) {
     case 0: return decode_kernel<R, 0>;
     case 1: return decode_kernel<R, 1>;
     case 2: return decode_kernel<R, 2>;
-    default: return decode_kernel<R, 4>;
+    case 3: return decode_kernel<R, 3>;
+    case 4: return decode_kernel<R, 4>;
+    case 5: return decode_kernel<R, 5>;
+    default: return decode_kernel<R, 6>;
     }
 }
 
-int cw_of(int l, bool list) { return !list ? 0 : l <= 8 ? 1 : l <= 16 ? 2 : 4; }
+// kernel variant of a pass: 0 = SC, 1..6 = list at L = 1..32
+int cw_of(int l, bool list) {
+    if (!list) return 0;
+    int kv = 1;
+    while ((1 << (kv - 1)) < l && kv < 6) ++kv;
+    return kv;
+}
 
 template <typename R>
 cudaError_t launch(const LaunchParams& p, int cw, int grid, cudaStream_t s) {
