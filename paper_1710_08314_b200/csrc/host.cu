@@ -369,10 +369,12 @@ HostCode make_host_code(const pl_code& c, const pl_decoder& dec) {
 struct RungCfg {
     int l = 1;
     int seg_max = 0;
-    int smem_per_warp = 0;
-    int64_t gscratch_per_warp = 0;
+    int smem_per_frame = 0;
+    int64_t gscratch_per_frame = 0;
     int grid = 0;
     int wpb = plb::kMaxWarpsPerBlock;
+    int fpw = 1; // frames per warp (sub-warp decoding, single-code batches)
+    int64_t gscratch_total() const { return int64_t(grid) * wpb * fpw * gscratch_per_frame; }
 };
 
 } // namespace
@@ -431,37 +433,55 @@ int target_warps_per_sm() {
 
 // Pick where the depth segments live: the most shared-memory-resident
 // layout that still keeps PLB_TARGET_WARPS warps resident per SM, else the
-// layout with the most resident warps.
-RungCfg plan_rung(const pl_handle& h, int l, bool list) {
+// layout with the most resident warps.  Small list sizes on single-code
+// batches decode 2 or 4 frames per warp (one per sub-warp) when that still
+// reaches the target; PLB_FPW forces frames per warp.  Ladder rungs above
+// L = 4 see few frames (the failures of the rung below): one frame per warp
+// spreads them over more warps, which measured faster there.
+RungCfg plan_rung(const pl_handle& h, int l, bool list, bool ladder = false) {
     const char* forced = std::getenv("PLB_SEGMAX");
+    const char* forced_fpw = std::getenv("PLB_FPW");
     const int target = target_warps_per_sm();
     std::vector<int> cands;
     if (forced) cands.push_back(std::atoi(forced));
     else
         for (int s = h.nmax; s >= 8; s >>= 1) cands.push_back(s);
     if (cands.empty()) cands.push_back(h.nmax); // tiny codes: everything in shared memory
+    const int fmax = (list && h.codes.size() == 1 && !(ladder && l > 4)) ? plb::frames_per_warp_max(l) : 1;
+    std::vector<int> fpws;
+    // a list size has kernels for fmax and 1 frames per warp
+    if (forced_fpw) {
+        fpws.push_back(std::atoi(forced_fpw) > 1 ? fmax : 1);
+    } else {
+        fpws.push_back(fmax);
+        if (fmax > 1) fpws.push_back(1);
+    }
     RungCfg best;
     best.l = l;
     int best_warps = 0;
-    // 4-warp blocks first; 2 / 1 when a warp's area is too big (large N x L)
-    for (int wpb = plb::kMaxWarpsPerBlock; wpb >= 1; wpb >>= 1) {
-        for (int seg : cands) {
-            RungCfg c;
-            c.l = l;
-            c.seg_max = seg;
-            c.wpb = wpb;
-            c.smem_per_warp = int(plb::smem_bytes_per_warp(h.nmax, l, h.esz, seg));
-            c.gscratch_per_warp = plb::gscratch_bytes_per_warp(h.nmax, l, h.esz, seg);
-            const int smem = c.smem_per_warp * wpb;
-            const int nb = list ? plb::occupancy_list(h.dec.precision, l, smem, wpb)
-                                : plb::occupancy_sc(h.dec.precision, smem, wpb);
-            if (nb <= 0) continue;
-            c.grid = nb * h.sms;
-            if (nb * wpb > best_warps) {
-                best = c;
-                best_warps = nb * wpb;
+    for (int fpw : fpws) {
+        // 4-warp blocks first; 2 / 1 when a warp's area is too big (large N x L)
+        for (int wpb = plb::kMaxWarpsPerBlock; wpb >= 1; wpb >>= 1) {
+            for (int seg : cands) {
+                RungCfg c;
+                c.l = l;
+                c.seg_max = seg;
+                c.wpb = wpb;
+                c.fpw = fpw;
+                c.smem_per_frame = int(plb::smem_bytes_per_frame(h.nmax, l, h.esz, seg));
+                c.gscratch_per_frame = plb::gscratch_bytes_per_frame(h.nmax, l, h.esz, seg);
+                const int smem = c.smem_per_frame * fpw * wpb;
+                const int nb = list ? plb::occupancy_list(h.dec.precision, l, fpw, smem, wpb)
+                                    : plb::occupancy_sc(h.dec.precision, smem, wpb);
+                if (nb <= 0) continue;
+                c.grid = nb * h.sms;
+                if (nb * wpb > best_warps) {
+                    best = c;
+                    best_warps = nb * wpb;
+                }
+                if (nb * wpb >= target) break;
             }
-            if (nb * wpb >= target) break;
+            if (best_warps >= target) break;
         }
         if (best_warps >= target) break;
     }
@@ -524,10 +544,12 @@ void run_decode(pl_handle& h, const void* llr, const int32_t* code_id, int64_t n
         p.l = rc.l;
         p.select_by_crc = select;
         p.seg_smem_max = rc.seg_max;
-        p.smem_per_warp = rc.smem_per_warp;
-        p.gscratch_per_warp = rc.gscratch_per_warp;
+        p.smem_per_frame = rc.smem_per_frame;
+        p.smem_per_warp = rc.smem_per_frame * rc.fpw;
+        p.gscratch_per_frame = rc.gscratch_per_frame;
         p.esc_level = rc.l;
         p.wpb = rc.wpb;
+        p.fpw = rc.fpw;
         if (h.profiling) {
             while (h.prof_ev.size() < size_t(2 * (slot + 1))) {
                 cudaEvent_t ev;
@@ -711,12 +733,12 @@ int pl_create(const pl_code* codes, int32_t ncodes, const pl_decoder* dec, int32
         // ---- launch plans for every pass this kind can run
         if (!uses_list(kind) || adaptive(kind)) h->sc_cfg = plan_rung(*h, 1, false);
         if (kind == PL_KIND_FA_SSCL)
-            for (int ll = 2; ll <= l; ll *= 2) h->rungs.push_back(plan_rung(*h, ll, true));
+            for (int ll = 2; ll <= l; ll *= 2) h->rungs.push_back(plan_rung(*h, ll, true, true));
         else if (uses_list(kind))
-            h->rungs.push_back(plan_rung(*h, l, true));
+            h->rungs.push_back(plan_rung(*h, l, true, adaptive(kind)));
         int64_t gs = 0;
         auto acc = [&](const RungCfg& r) {
-            gs = std::max<int64_t>(gs, int64_t(r.grid) * r.wpb * r.gscratch_per_warp);
+            gs = std::max<int64_t>(gs, r.gscratch_total());
         };
         if (h->sc_cfg.grid) acc(h->sc_cfg);
         for (const auto& r : h->rungs) acc(r);

@@ -1,13 +1,17 @@
 // sm_100a kernels of the batched polar decoder.
 //
-// Mapping: one warp decodes one frame at a time.  A
+// Mapping: a sub-warp of SW lanes (SW = 32, 16 or 8) decodes
+// one frame at a time, so a warp carries 32/SW frames in lockstep.  A
 // persistent grid of warps claims frames from an atomic counter (frames
-// differ in cost under adaptive decoding).  Inside a warp the lanes are
-// spread over (list path, LLR element) pairs, so a node of width m with A
-// alive paths keeps all 32 lanes busy once A*m/2 >= 32, and every fork /
-// sort / slot-assignment step is warp-synchronous (shuffles, ballots, match,
-// no CTA barrier).  Per-path bookkeeping lives in registers with lane ==
-// slot: lane s holds the path metric of slot s.
+// differ in cost under adaptive decoding).  Inside a sub-warp the lanes are
+// spread over (list path, LLR element) pairs, and every fork / sort /
+// slot-assignment step is sub-warp-synchronous (shuffles, ballots, match, no
+// CTA barrier).  Per-path bookkeeping lives in registers with lane == slot:
+// lane s holds the path metric of slot s.  Frames of one code walk the same
+// op schedule with the same alive count at every op (the alive trace is
+// data-independent), so sub-warps stay in lockstep; SW < 32 is
+// used for small L, where the per-op control work, not the element work,
+// dominates.
 //
 // LLR storage follows the reference's depth-segment stack (sc_decoder.hpp:
 // 18-20, list_decoder.hpp:45) with lazy path copies: every depth d >= 1 has
@@ -18,7 +22,7 @@
 // ever reads the old contents, so the writer of rank r simply takes buffer r:
 // no reference counts, no copy-on-write.  Depth 0 is the channel frame, read
 // in place from HBM.  Small segments live in shared memory, large ones in a
-// per-warp global scratch (L2-resident).  Partial sums are bit-packed, one
+// per-frame global scratch (L2-resident).  Partial sums are bit-packed, one
 // n-bit row per slot, LSB-first within 32-bit words; h is a word XOR.
 //
 // Bit-exactness: f/g/h, the penalty sums (sequential, index
@@ -40,18 +44,6 @@ __device__ __forceinline__ unsigned lanemask_lt() {
     return r;
 }
 
-__device__ __forceinline__ uint32_t shfl_k(uint32_t v, int src) { return __shfl_sync(FULL, v, src); }
-__device__ __forceinline__ uint64_t shfl_k(uint64_t v, int src) {
-    const uint32_t lo = __shfl_sync(FULL, uint32_t(v), src);
-    const uint32_t hi = __shfl_sync(FULL, uint32_t(v >> 32), src);
-    return (uint64_t(hi) << 32) | lo;
-}
-__device__ __forceinline__ uint32_t shfl_xor_k(uint32_t v, int m) { return __shfl_xor_sync(FULL, v, m); }
-__device__ __forceinline__ uint64_t shfl_xor_k(uint64_t v, int m) {
-    const uint32_t lo = __shfl_xor_sync(FULL, uint32_t(v), m);
-    const uint32_t hi = __shfl_xor_sync(FULL, uint32_t(v >> 32), m);
-    return (uint64_t(hi) << 32) | lo;
-}
 template <typename K>
 __device__ __forceinline__ K kmin(K a, K b) { return a < b ? a : b; }
 template <typename K>
@@ -59,6 +51,71 @@ __device__ __forceinline__ K kmax(K a, K b) { return a < b ? b : a; }
 
 __device__ __forceinline__ int pack_aux(int a, int b) {
     return int((uint32_t(a) & 0xffffu) | (uint32_t(b) << 16));
+}
+
+// ---- sub-warp collectives ----------------------------------------------
+// All calls are made by all 32 lanes of the warp (every sub-warp executes
+// the same control flow); results are per sub-warp.
+template <int SW>
+struct Sub {
+    static constexpr unsigned kMask = SW == 32 ? FULL : ((1u << SW) - 1u);
+    int lane; // lane within the sub-warp
+    int base; // first warp lane of the sub-warp
+    int id;   // sub-warp index
+
+    __device__ __forceinline__ unsigned ballot(bool p) const {
+        if constexpr (SW == 32) return __ballot_sync(FULL, p);
+        else return (__ballot_sync(FULL, p) >> base) & kMask;
+    }
+    __device__ __forceinline__ bool any(bool p) const { return ballot(p) != 0u; }
+    __device__ __forceinline__ unsigned lt() const { return lanemask_lt() >> base; }
+    __device__ __forceinline__ uint32_t shfl(uint32_t v, int src) const { return __shfl_sync(FULL, v, src, SW); }
+    __device__ __forceinline__ int shfl(int v, int src) const { return __shfl_sync(FULL, v, src, SW); }
+    __device__ __forceinline__ float shfl(float v, int src) const { return __shfl_sync(FULL, v, src, SW); }
+    __device__ __forceinline__ uint64_t shfl(uint64_t v, int src) const {
+        const uint32_t lo = __shfl_sync(FULL, uint32_t(v), src, SW);
+        const uint32_t hi = __shfl_sync(FULL, uint32_t(v >> 32), src, SW);
+        return (uint64_t(hi) << 32) | lo;
+    }
+    __device__ __forceinline__ unsigned red_or(unsigned v) const {
+        if constexpr (SW == 32) {
+            return __reduce_or_sync(FULL, v);
+        } else {
+#pragma unroll
+            for (int o = SW / 2; o > 0; o >>= 1) v |= __shfl_xor_sync(FULL, v, o);
+            return v;
+        }
+    }
+    __device__ __forceinline__ unsigned red_min(unsigned v) const {
+        if constexpr (SW == 32) {
+            return __reduce_min_sync(FULL, v);
+        } else {
+#pragma unroll
+            for (int o = SW / 2; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(FULL, v, o));
+            return v;
+        }
+    }
+    __device__ __forceinline__ unsigned red_add(unsigned v) const {
+        if constexpr (SW == 32) {
+            return __reduce_add_sync(FULL, v);
+        } else {
+#pragma unroll
+            for (int o = SW / 2; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+            return v;
+        }
+    }
+    // lanes of this sub-warp holding the same v (v < 2^24)
+    __device__ __forceinline__ unsigned match(int v) const {
+        if constexpr (SW == 32) return __match_any_sync(FULL, v);
+        else return (__match_any_sync(FULL, (v << 2) | id) >> base) & kMask;
+    }
+};
+
+__device__ __forceinline__ uint32_t shfl_xor_k(uint32_t v, int m) { return __shfl_xor_sync(FULL, v, m); }
+__device__ __forceinline__ uint64_t shfl_xor_k(uint64_t v, int m) {
+    const uint32_t lo = __shfl_xor_sync(FULL, uint32_t(v), m);
+    const uint32_t hi = __shfl_xor_sync(FULL, uint32_t(v >> 32), m);
+    return (uint64_t(hi) << 32) | lo;
 }
 
 // ---- per-representation arithmetic (llr.hpp:36-69) -------------------
@@ -166,8 +223,8 @@ __device__ __forceinline__ float mfrom<float>(uint32_t b) { return __uint_as_flo
 template <>
 __device__ __forceinline__ int mfrom<int>(uint32_t b) { return int(b); }
 
-// ---- warp bitonic sorts (ascending) -------------------------------------
-// W keys, one per lane, lanes [0, W) sorted.
+// ---- sub-warp bitonic sorts (ascending) ----------------------------------
+// W keys, one per lane, lanes [0, W) of the sub-warp sorted (W <= SW).
 template <typename K, int W>
 __device__ __forceinline__ K bitonic_lanes(K key, int lane) {
 #pragma unroll
@@ -183,42 +240,37 @@ __device__ __forceinline__ K bitonic_lanes(K key, int lane) {
     return key;
 }
 
-// The 32 smallest of two ascending 32-key lane sequences, ascending: the
+// The W smallest of two ascending W-key lane sequences, ascending: the
 // element-wise min of a and reversed b is a bitonic sequence holding exactly
-// those 32 keys; one bitonic merge sorts it.
-template <typename K>
-__device__ __forceinline__ K merge_top32(K a, K b, int lane) {
-    K c = kmin(a, __shfl_sync(FULL, b, 31 - lane));
+// those keys; one bitonic merge sorts it.
+template <typename K, int W>
+__device__ __forceinline__ K merge_top(K a, K b, int lane) {
+    K br;
+    if constexpr (sizeof(K) == 8) {
+        br = (uint64_t(__shfl_sync(FULL, uint32_t(b >> 32), W - 1 - lane, W)) << 32) |
+             __shfl_sync(FULL, uint32_t(b), W - 1 - lane, W);
+    } else {
+        br = __shfl_sync(FULL, b, W - 1 - lane, W);
+    }
+    K c = kmin(a, br);
 #pragma unroll
-    for (int j = 16; j > 0; j >>= 1) {
+    for (int j = W / 2; j > 0; j >>= 1) {
         const K o = shfl_xor_k(c, j);
         c = (lane & j) == 0 ? kmin(c, o) : kmax(c, o);
     }
     return c;
 }
-template <>
-__device__ __forceinline__ uint64_t merge_top32<uint64_t>(uint64_t a, uint64_t b, int lane) {
-    const uint64_t br = (uint64_t(__shfl_sync(FULL, uint32_t(b >> 32), 31 - lane)) << 32) |
-                        __shfl_sync(FULL, uint32_t(b), 31 - lane);
-    uint64_t c = kmin(a, br);
-#pragma unroll
-    for (int j = 16; j > 0; j >>= 1) {
-        const uint64_t o = shfl_xor_k(c, j);
-        c = (lane & j) == 0 ? kmin(c, o) : kmax(c, o);
-    }
-    return c;
-}
 
-// The 32 smallest of 32*C keys (register k of each lane), ascending in
+// The W smallest of W*C keys (register k of each lane), ascending in
 // register 0: sort each register across the lanes, then merge pairwise.
-template <typename K, int C>
-__device__ __forceinline__ void top32_regs(K (&key)[C], int lane) {
+template <typename K, int C, int W>
+__device__ __forceinline__ void top_regs(K (&key)[C], int lane) {
 #pragma unroll
-    for (int k = 0; k < C; ++k) key[k] = bitonic_lanes<K, 32>(key[k], lane);
+    for (int k = 0; k < C; ++k) key[k] = bitonic_lanes<K, W>(key[k], lane);
 #pragma unroll
     for (int w = 1; w < C; w <<= 1)
 #pragma unroll
-        for (int k = 0; k + w < C; k += 2 * w) key[k] = merge_top32(key[k], key[k + w], lane);
+        for (int k = 0; k + w < C; k += 2 * w) key[k] = merge_top<K, W>(key[k], key[k + w], lane);
 }
 
 // ---- vector access of G consecutive values ----------------------------
@@ -247,7 +299,7 @@ __device__ __forceinline__ void vst(R* p, const Vec<R, G>& x) {
     *reinterpret_cast<typename VT<G * sizeof(R)>::T*>(p) = x.raw;
 }
 
-// ---- per-warp shared-memory area ---------------------------------------
+// ---- per-frame shared-memory area ----------------------------------------
 struct alignas(16) Fixed {
     uint8_t bufidx[32 * 16]; // [slot][depth] -> buffer index in the depth pool
     uint8_t alive_list[32];  // rank -> slot, ascending
@@ -268,8 +320,8 @@ __host__ __device__ inline int ilog2(int v) {
 }
 __host__ __device__ inline int align16(int v) { return (v + 15) & ~15; }
 
-// Shared-memory layout of one warp: Fixed | psum rows | depth pools that fit
-// (segment <= segmax values); larger segments go to the warp's global
+// Shared-memory layout of one frame: Fixed | psum rows | depth pools that
+// fit (segment <= segmax values); larger segments go to the frame's global
 // scratch.  want_d selects which depth's pool offset to return.
 struct LayoutQ {
     int32_t rw, psum_off, smem_total, gmem_total, pool_off, pool_in_smem;
@@ -310,19 +362,21 @@ __host__ __device__ inline LayoutQ layout_query(int n, int l, int esz, int segma
     return q;
 }
 
-// ---- warp decode context ----------------------------------------------
-template <typename R>
+// ---- frame decode context (one sub-warp) ---------------------------------
+template <typename R, int SW>
 struct Ctx {
     using A = Arith<R>;
     using M = typename A::M;
 
-    int lane, n, l;
+    Sub<SW> sw;
+    int lane; // == sw.lane
+    int n, l;
     unsigned lmask;
     const R* chan;
     Fixed* fx;
     uint32_t* ps;
     int rw;
-    unsigned alive; // warp-uniform alive-slot mask
+    unsigned alive; // sub-warp-uniform alive-slot mask
     int myrank;     // rank of slot `lane` among the alive slots
     M metric;       // lane s: metric of slot s
 
@@ -336,7 +390,7 @@ struct Ctx {
 
     __device__ void set_alive(unsigned a) {
         alive = a;
-        myrank = __popc(alive & lanemask_lt());
+        myrank = __popc(alive & sw.lt());
         if (is_alive()) fx->alive_list[myrank] = uint8_t(lane);
         __syncwarp();
     }
@@ -346,16 +400,16 @@ struct Ctx {
     __device__ void normalize() {
         if constexpr (A::kFixed) {
             const int v = is_alive() ? int(metric) : 127;
-            const int mn = int(__reduce_min_sync(FULL, unsigned(v)));
+            const int mn = int(sw.red_min(unsigned(v)));
             if (is_alive()) metric -= mn;
         }
     }
 };
 
 // ---- f / g over all alive paths ----------------------------------------
-// One body for F and G (is_g is warp-uniform), two vector widths per type
-// (G = 1 for narrow nodes, G = 16 bytes otherwise): the decode loop's hot
-// code must stay inside the instruction cache.
+// One body for F and G (is_g is uniform), two vector widths per type (G = 1
+// for narrow nodes, G = 16 bytes otherwise): the decode loop's hot code must
+// stay inside the instruction cache.
 template <typename R, int G>
 __device__ __forceinline__ void fg_item(const R* in, R* out, const uint32_t* prow, int h,
                                         int c, int lb, bool is_g) {
@@ -387,8 +441,8 @@ __device__ __forceinline__ void fg_item(const R* in, R* out, const uint32_t* pro
     vst<R, G>(out + c * G, o);
 }
 
-template <typename R, int G>
-__device__ __forceinline__ void fg_run(Ctx<R>& cx, int d, int h, int lb, int na, bool is_g) {
+template <typename R, int SW, int G>
+__device__ __forceinline__ void fg_run(Ctx<R, SW>& cx, int d, int h, int lb, int na, bool is_g) {
     const int cp = h / G; // items per path, power of two
     const int lg = __ffs(cp) - 1;
     R* const outp = cx.pool(d + 1);
@@ -396,7 +450,7 @@ __device__ __forceinline__ void fg_run(Ctx<R>& cx, int d, int h, int lb, int na,
     const int seg = cx.n >> d;
     const int total = na << lg;
     #pragma unroll 1
-    for (int t = cx.lane; t < total; t += 32) {
+    for (int t = cx.lane; t < total; t += SW) {
         const int r = t >> lg;
         const int p = cx.fx->alive_list[r];
         const R* in = d == 0 ? inp : inp + int(cx.fx->bufidx[p * 16 + d]) * seg;
@@ -404,26 +458,26 @@ __device__ __forceinline__ void fg_run(Ctx<R>& cx, int d, int h, int lb, int na,
     }
 }
 
-template <typename R>
-__device__ void op_fg(Ctx<R>& cx, int d, int m, int lb, int na, bool is_g) {
+template <typename R, int SW>
+__device__ void op_fg(Ctx<R, SW>& cx, int d, int m, int lb, int na, bool is_g) {
     constexpr int VE = 16 / int(sizeof(R));
     const int h = m >> 1;
     // the child segment of the path of rank r goes to buffer r (see header)
     if (cx.is_alive()) cx.fx->bufidx[cx.lane * 16 + d + 1] = uint8_t(cx.myrank);
-    if (h >= VE) fg_run<R, VE>(cx, d, h, lb, na, is_g);
-    else fg_run<R, 1>(cx, d, h, lb, na, is_g);
+    if (h >= VE) fg_run<R, SW, VE>(cx, d, h, lb, na, is_g);
+    else fg_run<R, SW, 1>(cx, d, h, lb, na, is_g);
     __syncwarp();
 }
 
 // psums[lb, lb+h) ^= psums[lb+h, lb+2h) for every alive path
-template <typename R>
-__device__ void op_h(Ctx<R>& cx, int m, int lb, int na) {
+template <typename R, int SW>
+__device__ void op_h(Ctx<R, SW>& cx, int m, int lb, int na) {
     const int h = m >> 1;
     if (h >= 32) {
         const int W = h >> 5, lg = __ffs(W) - 1;
         const int total = na << lg;
         #pragma unroll 1
-        for (int t = cx.lane; t < total; t += 32) {
+        for (int t = cx.lane; t < total; t += SW) {
             uint32_t* w = cx.row(cx.fx->alive_list[t >> lg]) + (lb >> 5) + (t & (W - 1));
             w[0] ^= w[W];
         }
@@ -436,11 +490,12 @@ __device__ void op_h(Ctx<R>& cx, int m, int lb, int na) {
     __syncwarp();
 }
 
-// write `bit` over the span [lb, lb+m) of a psum row (whole warp)
-__device__ __forceinline__ void span_fill_warp(uint32_t* row, int lb, int m, int bit, int lane) {
+// write `bit` over the span [lb, lb+m) of a psum row (whole sub-warp)
+template <int SW>
+__device__ __forceinline__ void span_fill(uint32_t* row, int lb, int m, int bit, int lane) {
     if (m >= 32) {
         #pragma unroll 1
-        for (int w = lane; w < (m >> 5); w += 32) row[(lb >> 5) + w] = bit ? FULL : 0u;
+        for (int w = lane; w < (m >> 5); w += SW) row[(lb >> 5) + w] = bit ? FULL : 0u;
     } else if (lane == 0) {
         const uint32_t mk = ((1u << m) - 1u) << (lb & 31);
         uint32_t* w = row + (lb >> 5);
@@ -456,15 +511,15 @@ __device__ __forceinline__ void span_fill_lane(uint32_t* row, int lb, int m, int
 
 // Halving fold of the REP node's LLRs (sc_decoder.hpp:116-125,
 // list_decoder.hpp:282-289) for every alive path; the result of rank r goes
-// to st_a1[r].  For m > 32 the first halvings run in the rank's depth-(d+1)
+// to st_a1[r].  For m > SW the first halvings run in the rank's depth-(d+1)
 // buffer, whose contents are dead at a leaf.
-template <typename R>
-__device__ void rep_fold(Ctx<R>& cx, int d, int m, int na) {
+template <typename R, int SW>
+__device__ void rep_fold(Ctx<R, SW>& cx, int d, int m, int na) {
     using A = Arith<R>;
     using M = typename A::M;
-    if (m <= 32) {
+    if (m <= SW) {
         const int lgm = __ffs(m) - 1;
-        const int per = 32 >> lgm;
+        const int per = SW >> lgm;
         #pragma unroll 1
         for (int r0 = 0; r0 < na; r0 += per) {
             const int r = r0 + (cx.lane >> lgm), i = cx.lane & (m - 1);
@@ -483,18 +538,18 @@ __device__ void rep_fold(Ctx<R>& cx, int d, int m, int na) {
             R* S = cx.pool(d + 1) + r * (m >> 1);
             const int h = m >> 1;
             #pragma unroll 1
-            for (int i = cx.lane; i < h; i += 32) S[i] = A::store(A::sat(A::val(L[i]), A::val(L[i + h])));
+            for (int i = cx.lane; i < h; i += SW) S[i] = A::store(A::sat(A::val(L[i]), A::val(L[i + h])));
             __syncwarp();
             #pragma unroll 1
-            for (int len = h; len > 32; len >>= 1) {
+            for (int len = h; len > SW; len >>= 1) {
                 const int hh = len >> 1;
                 #pragma unroll 1
-                for (int i = cx.lane; i < hh; i += 32) S[i] = A::store(A::sat(A::val(S[i]), A::val(S[i + hh])));
+                for (int i = cx.lane; i < hh; i += SW) S[i] = A::store(A::sat(A::val(S[i]), A::val(S[i + hh])));
                 __syncwarp();
             }
             M v = A::val(S[cx.lane]);
-            for (int off = 16; off >= 1; off >>= 1) {
-                const M o = __shfl_down_sync(FULL, v, off);
+            for (int off = SW / 2; off >= 1; off >>= 1) {
+                const M o = __shfl_down_sync(FULL, v, off, SW);
                 if (cx.lane < off) v = A::sat(v, o);
             }
             if (cx.lane == 0) cx.fx->st_a1[r] = mbits<M>(v);
@@ -508,30 +563,30 @@ __device__ void rep_fold(Ctx<R>& cx, int d, int m, int na) {
 enum ApplyKind { AK_BIT = 0, AK_BCAST = 1, AK_FLIPS = 2 };
 
 // fork_apply (list_decoder.hpp:339-387) for ncand candidates held as
-// candidate i = lane + 32k in register k.  aux = a | b << 16 (int16 each).
-template <typename R, int CPL, int MAXW>
-__device__ void fork_apply(Ctx<R>& cx, const typename Arith<R>::M (&cm)[CPL],
+// candidate i = lane + SW*k in register k.  aux = a | b << 16 (int16 each).
+template <typename R, int SW, int CPL, int MAXW>
+__device__ void fork_apply(Ctx<R, SW>& cx, const typename Arith<R>::M (&cm)[CPL],
                            const int (&csrc)[CPL], const int (&caux)[CPL], int ncand,
                            int kind, int lb, int m) {
     using A = Arith<R>;
     using M = typename A::M;
     using K = typename A::Key;
     const int lane = cx.lane;
-    // 1. stable order by (metric, emission index): a warp bitonic sort of
+    // 1. stable order by (metric, emission index): a sub-warp bitonic sort of
     //    the unique keys leaves the candidate of rank r in lane r (register 0)
     K key[CPL];
 #pragma unroll
     for (int k = 0; k < CPL; ++k) {
-        const int i = lane + 32 * k;
+        const int i = lane + SW * k;
         key[k] = i < ncand ? A::make_key(cm[k], i) : A::kKeyMax;
     }
     if constexpr (CPL == 1) {
-        // two network widths per kernel: MAXW = 4L (<= 32) and MAXW/2
+        // two network widths per kernel: MAXW = min(SW, 4L) and MAXW/2
         if (MAXW > 4 && ncand <= MAXW / 2) key[0] = bitonic_lanes<K, (MAXW > 4 ? MAXW / 2 : 4)>(key[0], lane);
         else key[0] = bitonic_lanes<K, MAXW>(key[0], lane);
     } else {
-        // only the best keep <= 32 are needed, in order
-        top32_regs<K, CPL>(key, lane);
+        // only the best keep <= SW are needed, in order
+        top_regs<K, CPL, SW>(key, lane);
     }
     const int keep = min(cx.l, ncand);
     const bool kept = lane < keep;
@@ -540,9 +595,9 @@ __device__ void fork_apply(Ctx<R>& cx, const typename Arith<R>::M (&cm)[CPL],
     int src = 0, aux = 0;
 #pragma unroll
     for (int k = 0; k < CPL; ++k) {
-        const int s = __shfl_sync(FULL, csrc[k], ci & 31);
-        const int a = __shfl_sync(FULL, caux[k], ci & 31);
-        if ((ci >> 5) == k) {
+        const int s = cx.sw.shfl(csrc[k], ci & (SW - 1));
+        const int a = cx.sw.shfl(caux[k], ci & (SW - 1));
+        if (ci / SW == k) {
             src = s;
             aux = a;
         }
@@ -550,18 +605,18 @@ __device__ void fork_apply(Ctx<R>& cx, const typename Arith<R>::M (&cm)[CPL],
     if (!kept) src = 64 + lane;
     // 2. slot assignment: the first use of a slot stays in place, the others
     //    take the free slots in ascending order, in rank order
-    const unsigned same = __match_any_sync(FULL, src);
+    const unsigned same = cx.sw.match(src);
     const bool first = kept && (__ffs(same) - 1) == lane;
-    const unsigned surv = __reduce_or_sync(FULL, kept ? (1u << src) : 0u);
+    const unsigned surv = cx.sw.red_or(kept ? (1u << src) : 0u);
     const bool dup = kept && !first;
-    const unsigned dupm = __ballot_sync(FULL, dup);
+    const unsigned dupm = cx.sw.ballot(dup);
     int tgt = src;
-    if (dupm) {
+    {
         const unsigned freem = cx.lmask & ~surv;
-        if ((freem >> lane) & 1u) cx.fx->freetab[__popc(freem & lanemask_lt())] = uint8_t(lane);
+        if ((freem >> lane) & 1u) cx.fx->freetab[__popc(freem & cx.sw.lt())] = uint8_t(lane);
         __syncwarp();
         if (dup) {
-            const int k = __popc(dupm & lanemask_lt());
+            const int k = __popc(dupm & cx.sw.lt());
             tgt = cx.fx->freetab[k];
             cx.fx->dsrc[k] = uint8_t(src);
             cx.fx->dtgt[k] = uint8_t(tgt);
@@ -580,7 +635,7 @@ __device__ void fork_apply(Ctx<R>& cx, const typename Arith<R>::M (&cm)[CPL],
             const int n4 = (nw + 3) >> 2;
             const int lg = n4 > 1 ? 32 - __clz(n4 - 1) : 0; // ceil(log2(n4))
             #pragma unroll 1
-            for (int t = lane; t < (nd << lg); t += 32) {
+            for (int t = lane; t < (nd << lg); t += SW) {
                 const int k = t >> lg, q = t & ((1 << lg) - 1);
                 if (q < n4)
                     reinterpret_cast<uint4*>(cx.row(cx.fx->dtgt[k]))[q] =
@@ -601,9 +656,9 @@ __device__ void fork_apply(Ctx<R>& cx, const typename Arith<R>::M (&cm)[CPL],
         } else {
             #pragma unroll 1
             for (int r = 0; r < keep; ++r) {
-                const int t = __shfl_sync(FULL, tgt, r);
-                const int bit = __shfl_sync(FULL, ca, r);
-                span_fill_warp(cx.row(t), lb, m, bit, lane);
+                const int t = cx.sw.shfl(tgt, r);
+                const int bit = cx.sw.shfl(ca, r);
+                span_fill<SW>(cx.row(t), lb, m, bit, lane);
             }
         }
     } else if (kept) {
@@ -612,21 +667,15 @@ __device__ void fork_apply(Ctx<R>& cx, const typename Arith<R>::M (&cm)[CPL],
         if (cb >= 0) tr[(lb + cb) >> 5] ^= 1u << ((lb + cb) & 31);
     }
     if (kept) cx.fx->met_s[tgt] = mbits<M>(cmet);
-    const unsigned nal = __reduce_or_sync(FULL, kept ? (1u << tgt) : 0u);
+    const unsigned nal = cx.sw.red_or(kept ? (1u << tgt) : 0u);
     __syncwarp();
     if ((nal >> lane) & 1u) cx.metric = mfrom<M>(cx.fx->met_s[lane]);
     cx.set_alive(nal);
 }
 
-// base metric of the path at rank r (all lanes participate)
-template <typename R>
-__device__ __forceinline__ typename Arith<R>::M base_of(const Ctx<R>& cx, int r) {
-    return __shfl_sync(FULL, cx.metric, cx.fx->alive_list[r]);
-}
-
 // frozen leaf / rate-0 node (list_decoder.hpp:227-238)
-template <typename R>
-__device__ void list_frozen(Ctx<R>& cx, int d, int m, int lb, int na) {
+template <typename R, int SW>
+__device__ void list_frozen(Ctx<R, SW>& cx, int d, int m, int lb, int na) {
     using A = Arith<R>;
     using M = typename A::M;
     M pen = M(0);
@@ -637,8 +686,8 @@ __device__ void list_frozen(Ctx<R>& cx, int d, int m, int lb, int na) {
             const R* L = cx.llr(cx.fx->alive_list[r], d);
             int s = 0;
             #pragma unroll 1
-            for (int i = cx.lane; i < m; i += 32) s += max(0, -int(A::val(L[i])));
-            s = int(__reduce_add_sync(FULL, unsigned(s)));
+            for (int i = cx.lane; i < m; i += SW) s += max(0, -int(A::val(L[i])));
+            s = int(cx.sw.red_add(unsigned(s)));
             if (cx.lane == r) pen = M(min(s, 127));
         }
     } else if (cx.lane < na) {
@@ -649,12 +698,12 @@ __device__ void list_frozen(Ctx<R>& cx, int d, int m, int lb, int na) {
             if (v < M(0)) pen = A::sat(pen, -v); // sequential: float order matters
         }
     }
-    const M pr = __shfl_sync(FULL, pen, cx.myrank & 31);
+    const M pr = cx.sw.shfl(pen, cx.myrank & (SW - 1));
     if (cx.is_alive()) cx.metric = A::sat(cx.metric, pr);
     if (m >= 32) {
         const int W = m >> 5;
         #pragma unroll 1
-        for (int t = cx.lane; t < na * W; t += 32)
+        for (int t = cx.lane; t < na * W; t += SW)
             cx.row(cx.fx->alive_list[t / W])[(lb >> 5) + (t % W)] = 0u;
     } else if (cx.lane < na) {
         span_fill_lane(cx.row(cx.fx->alive_list[cx.lane]), lb, m, 0);
@@ -666,16 +715,13 @@ __device__ void list_frozen(Ctx<R>& cx, int d, int m, int lb, int na) {
 // Per-path statistics of an R1 / SPC node: hard decisions written into the
 // path's own psum span, the two smallest magnitudes under the (value, index)
 // order (select.hpp:18-68) -> st_i1/st_a1, st_i2/st_a2, parity -> st_w.
-template <typename R>
-__device__ void r1spc_stats(Ctx<R>& cx, int d, int m, int lb, int na) {
+template <typename R, int SW>
+__device__ void r1spc_stats(Ctx<R, SW>& cx, int d, int m, int lb, int na) {
     using A = Arith<R>;
     using M = typename A::M;
     using K = typename A::Key;
-    // One pass over all paths: lp lanes per path (na is a power of two, C22),
-    // lane l0 of a group takes the E = m/lp consecutive values
-    // [l0*E, (l0+1)*E) of its path (vector loads), builds their hard bits
-    // locally and ORs them into the path's (cleared) psum span.
-    const int lp = min(m, 32 / na);
+    // One pass over all paths: lp lanes per path (na is a power of two, C22).
+    const int lp = min(m, SW / na);
     const int lglp = __ffs(lp) - 1;
     const int E = m >> lglp;
     const int r = cx.lane >> lglp, l0 = cx.lane & (lp - 1);
@@ -684,7 +730,7 @@ __device__ void r1spc_stats(Ctx<R>& cx, int d, int m, int lb, int na) {
     if (E == 1) {
         // one value per lane (lp == m): every path's hard bits in one ballot
         const M v = ok ? A::val(cx.llr(p, d)[l0]) : M(0);
-        const unsigned hb = __ballot_sync(FULL, ok && v < M(0));
+        const unsigned hb = cx.sw.ballot(ok && v < M(0));
         const uint32_t mk = m >= 32 ? FULL : ((1u << m) - 1u);
         const uint32_t gb = (hb >> (cx.lane & ~(lp - 1))) & mk;
         K k1 = ok ? A::make_key(A::mag(v), l0) : A::kKeyMax, k2 = A::kKeyMax;
@@ -707,6 +753,9 @@ __device__ void r1spc_stats(Ctx<R>& cx, int d, int m, int lb, int na) {
         __syncwarp();
         return;
     }
+    // lane l0 of a group takes the E = m/lp consecutive values
+    // [l0*E, (l0+1)*E) of its path (vector loads), builds their hard bits
+    // locally and ORs them into the path's (cleared) psum span.
     const int i0 = l0 * E;
     const R* L = cx.llr(p, d) + i0;
     uint32_t* span = cx.row(p) + (lb >> 5);
@@ -773,8 +822,8 @@ __device__ void r1spc_stats(Ctx<R>& cx, int d, int m, int lb, int na) {
 // repetition node (list_decoder.hpp:276-305): after the fold, pen_w = the
 // sum of the magnitudes that disagree with the fold's decision, sequential
 // in index order (float order matters; int8 is order-free) -> st_a2, st_w.
-template <typename R>
-__device__ void rep_pen(Ctx<R>& cx, int d, int m, int na) {
+template <typename R, int SW>
+__device__ void rep_pen(Ctx<R, SW>& cx, int d, int m, int na) {
     using A = Arith<R>;
     using M = typename A::M;
     if (A::kFixed && m >= 32) {
@@ -784,11 +833,11 @@ __device__ void rep_pen(Ctx<R>& cx, int d, int m, int na) {
             const bool w = mfrom<M>(cx.fx->st_a1[r]) < M(0);
             int s = 0;
             #pragma unroll 1
-            for (int i = cx.lane; i < m; i += 32) {
+            for (int i = cx.lane; i < m; i += SW) {
                 const int v = int(A::val(L[i]));
                 if (w ? (v > 0) : (v < 0)) s += abs(v);
             }
-            s = int(__reduce_add_sync(FULL, unsigned(s)));
+            s = int(cx.sw.red_add(unsigned(s)));
             if (cx.lane == 0) {
                 cx.fx->st_w[r] = w;
                 cx.fx->st_a2[r] = mbits<M>(M(min(s, 127)));
@@ -812,9 +861,9 @@ __device__ void rep_pen(Ctx<R>& cx, int d, int m, int na) {
 // A forking node: per-path statistics, candidates in emission order
 // (ascending slot, then candidate number, list_decoder.hpp:240-333), one
 // shared fork_apply, normalisation.  C = candidates per lane, fixed per
-// kernel instantiation (4L <= 32C).
-template <typename R, int C, int MAXW>
-__device__ void list_fork_node(Ctx<R>& cx, int code, int d, int m, int lb, int na) {
+// kernel instantiation (4L <= SW*C).
+template <typename R, int SW, int C, int MAXW>
+__device__ void list_fork_node(Ctx<R, SW>& cx, int code, int d, int m, int lb, int na) {
     using A = Arith<R>;
     using M = typename A::M;
     if (code == OP_R1 || code == OP_SPC) {
@@ -828,9 +877,9 @@ __device__ void list_fork_node(Ctx<R>& cx, int code, int d, int m, int lb, int n
     int cs[C], cax[C];
 #pragma unroll
     for (int k = 0; k < C; ++k) {
-        const int i = cx.lane + 32 * k, r = min(i >> lgb, na - 1), j = i & ((1 << lgb) - 1);
+        const int i = cx.lane + SW * k, r = min(i >> lgb, na - 1), j = i & ((1 << lgb) - 1);
         const int p = cx.fx->alive_list[r];
-        const M base = __shfl_sync(FULL, cx.metric, p);
+        const M base = cx.sw.shfl(cx.metric, p);
         cs[k] = p;
         if (code == OP_INFO) { // list_decoder.hpp:240-252
             const M v = A::val(cx.llr(p, d)[0]);
@@ -855,31 +904,33 @@ __device__ void list_fork_node(Ctx<R>& cx, int code, int d, int m, int lb, int n
         }
     }
     const int kind = code == OP_INFO ? AK_BIT : code == OP_REP ? AK_BCAST : AK_FLIPS;
-    fork_apply<R, C, MAXW>(cx, cm, cs, cax, na << lgb, kind, lb, code == OP_INFO ? 1 : m);
+    fork_apply<R, SW, C, MAXW>(cx, cm, cs, cax, na << lgb, kind, lb, code == OP_INFO ? 1 : m);
     cx.normalize();
 }
 
 // ---- CRC syndrome of a decided codeword row ----------------
+template <int SW>
 __device__ uint64_t row_syndrome(const DevCode& C, const uint32_t* row, int lane) {
     uint64_t syn = 0;
     const int nbytes = (C.n + 7) >> 3;
     #pragma unroll 1
-    for (int j = lane; j < nbytes; j += 32) {
+    for (int j = lane; j < nbytes; j += SW) {
         const uint32_t byte = (row[j >> 2] >> ((j & 3) * 8)) & 0xffu;
         syn ^= __ldg(C.crc_tab + (size_t(j) << 8) + byte);
     }
 #pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) syn ^= shfl_xor_k(syn, off);
+    for (int off = SW / 2; off >= 1; off >>= 1) syn ^= shfl_xor_k(syn, off);
     return syn ^ C.crc_c0;
 }
 
 // payload (MSB-first bytes of the open positions) + optional codeword
+template <int SW>
 __device__ void write_outputs(const LaunchParams& P, const DevCode& C, const uint32_t* row,
                               int frame, int lane) {
     uint8_t* pay = P.payload + int64_t(frame) * P.payload_stride;
     const int pb = (C.psize + 7) >> 3;
     #pragma unroll 1
-    for (int q = lane; q < pb; q += 32) {
+    for (int q = lane; q < pb; q += SW) {
         uint32_t byte = 0;
 #pragma unroll
         for (int b = 0; b < 8; ++b) {
@@ -895,7 +946,7 @@ __device__ void write_outputs(const LaunchParams& P, const DevCode& C, const uin
         uint8_t* cw = P.codeword + int64_t(frame) * P.codeword_stride;
         const int cb = (C.n + 7) >> 3;
         #pragma unroll 1
-        for (int q = lane; q < cb; q += 32) {
+        for (int q = lane; q < cb; q += SW) {
             uint32_t byte = 0;
 #pragma unroll
             for (int b = 0; b < 8; ++b) {
@@ -907,46 +958,48 @@ __device__ void write_outputs(const LaunchParams& P, const DevCode& C, const uin
     }
 }
 
-template <typename R>
-__device__ void setup_ctx(Ctx<R>& cx, const LaunchParams& P, const DevCode& C,
-                          unsigned char* sm, unsigned char* gs, int frame, int lane, int l) {
-    cx.lane = lane;
+template <typename R, int SW>
+__device__ void setup_ctx(Ctx<R, SW>& cx, const LaunchParams& P, const DevCode& C,
+                          unsigned char* sm, unsigned char* gs, int frame, const Sub<SW>& sw,
+                          int l) {
+    cx.sw = sw;
+    cx.lane = sw.lane;
     cx.n = C.n;
     cx.l = l;
     cx.lmask = l >= 32 ? FULL : ((1u << l) - 1u);
     cx.chan = static_cast<const R*>(P.llr) + int64_t(frame) * P.llr_stride;
     cx.fx = reinterpret_cast<Fixed*>(sm);
-    const LayoutQ q = layout_query(C.n, l, int(sizeof(R)), P.seg_smem_max, lane);
-    cx.ps = reinterpret_cast<uint32_t*>(sm + q.psum_off);
-    cx.rw = q.rw;
-    if (lane >= 1 && lane <= C.stages)
-        cx.fx->pool[lane] = reinterpret_cast<uint64_t>((q.pool_in_smem ? sm : gs) + q.pool_off);
-    if (lane == 0) *reinterpret_cast<uint4*>(cx.fx->bufidx) = make_uint4(0, 0, 0, 0);
+    const LayoutQ q0 = layout_query(C.n, l, int(sizeof(R)), P.seg_smem_max, 0);
+    cx.ps = reinterpret_cast<uint32_t*>(sm + q0.psum_off);
+    cx.rw = q0.rw;
+    #pragma unroll 1
+    for (int d = cx.lane + 1; d <= C.stages; d += SW) {
+        const LayoutQ q = layout_query(C.n, l, int(sizeof(R)), P.seg_smem_max, d);
+        cx.fx->pool[d] = reinterpret_cast<uint64_t>((q.pool_in_smem ? sm : gs) + q.pool_off);
+    }
+    if (cx.lane == 0) *reinterpret_cast<uint4*>(cx.fx->bufidx) = make_uint4(0, 0, 0, 0);
     cx.metric = typename Arith<R>::M(0);
     __syncwarp();
     cx.set_alive(1u);
 }
 
-__device__ __forceinline__ long long claim(const LaunchParams& P, int lane) {
-    unsigned long long idx = 0;
-    if (lane == 0) idx = atomicAdd(P.work, 1ull);
-    return (long long)__shfl_sync(FULL, idx, 0);
-}
-
 // ---- one frame, list decoding at list size P.l --------------------------
-// Kernel variant KV (1..6) <-> list size 1, 2, 4, 8, 16, 32: candidates per
-// lane CW and the widest ranking network MAXW = min(32, 4L).
-__host__ __device__ constexpr int kv_cw(int kv) { return kv >= 6 ? 4 : kv == 5 ? 2 : 1; }
-__host__ __device__ constexpr int kv_maxw(int kv) { return kv == 1 ? 4 : kv == 2 ? 8 : kv == 3 ? 16 : 32; }
+// Kernel variant KV (1..6) <-> list size 1, 2, 4, 8, 16, 32 on sub-warps of
+// SW lanes: candidates per lane CW = ceil(4L / SW) and the widest ranking
+// network MAXW = min(SW, 4L).
+__host__ __device__ constexpr int kv_l(int kv) { return 1 << (kv - 1); }
+__host__ __device__ constexpr int kv_cw(int kv, int sw) { return (4 * kv_l(kv) + sw - 1) / sw; }
+__host__ __device__ constexpr int kv_maxw(int kv, int sw) { return 4 * kv_l(kv) < sw ? 4 * kv_l(kv) : sw; }
 
-template <typename R, int KV>
+template <typename R, int KV, int SW>
 __device__ void list_frame(const LaunchParams& P, const DevCode& C, unsigned char* sm,
-                           unsigned char* gs, int frame, int lane) {
+                           unsigned char* gs, int frame, bool active, const Sub<SW>& sw) {
     using A = Arith<R>;
     using M = typename A::M;
-    constexpr int CW = kv_cw(KV), MAXW = kv_maxw(KV);
-    Ctx<R> cx;
-    setup_ctx(cx, P, C, sm, gs, frame, lane, P.l);
+    constexpr int CW = kv_cw(KV, SW), MAXW = kv_maxw(KV, SW);
+    Ctx<R, SW> cx;
+    setup_ctx(cx, P, C, sm, gs, frame, sw, P.l);
+    const int lane = cx.lane;
     const uint32_t* sched = C.sched_list;
     const int nops = C.nops_list;
     #pragma unroll 1
@@ -957,42 +1010,64 @@ __device__ void list_frame(const LaunchParams& P, const DevCode& C, unsigned cha
         if (code <= OP_G) op_fg(cx, d, m, lb, na, code == OP_G);
         else if (code == OP_H) op_h(cx, m, lb, na);
         else if (code == OP_FROZEN) list_frozen(cx, d, m, lb, na);
-        else list_fork_node<R, CW, MAXW>(cx, code, d, m, lb, na);
+        else list_fork_node<R, SW, CW, MAXW>(cx, code, d, m, lb, na);
     }
     // finish (list_decoder.hpp:457-502): stable order by (metric, slot)
     using K = typename A::Key;
     const K okey = cx.is_alive() ? A::make_key(cx.metric, lane) : A::kKeyMax;
     K best = okey;
 #pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) best = kmin(best, shfl_xor_k(best, off));
+    for (int off = SW / 2; off >= 1; off >>= 1) best = kmin(best, shfl_xor_k(best, off));
     int pick = A::key_idx(best);
     int crc_ok = 0;
     if (C.crc_width > 0) {
-        if (row_syndrome(C, cx.row(pick), lane) == 0) {
-            crc_ok = 1;
-        } else if (P.select_by_crc) {
+        if (SW == 32) {
+            if (row_syndrome<SW>(C, cx.row(pick), lane) == 0) {
+                crc_ok = 1;
+            } else if (P.select_by_crc) {
+                unsigned passm = 0;
+                #pragma unroll 1
+                for (unsigned mm = cx.alive & ~(1u << pick); mm; mm &= mm - 1) {
+                    const int s = __ffs(mm) - 1;
+                    if (row_syndrome<SW>(C, cx.row(s), lane) == 0) passm |= 1u << s;
+                }
+                if (passm) {
+                    K bk = ((passm >> lane) & 1u) ? okey : A::kKeyMax;
+#pragma unroll
+                    for (int off = SW / 2; off >= 1; off >>= 1) bk = kmin(bk, shfl_xor_k(bk, off));
+                    pick = A::key_idx(bk);
+                    crc_ok = 1;
+                }
+            }
+        } else {
+            // the sub-warps of a warp hold different frames, so every
+            // collective runs outside data-dependent branches: check every
+            // slot (L <= 8 here), rank the passing ones, then pick as the
+            // reference does
             unsigned passm = 0;
             #pragma unroll 1
-            for (unsigned mm = cx.alive & ~(1u << pick); mm; mm &= mm - 1) {
-                const int s = __ffs(mm) - 1;
-                if (row_syndrome(C, cx.row(s), lane) == 0) passm |= 1u << s;
-            }
-            if (passm) {
-                K bk = ((passm >> lane) & 1u) ? okey : A::kKeyMax;
+            for (int s = 0; s < cx.l; ++s)
+                if (row_syndrome<SW>(C, cx.row(s), lane) == 0 && ((cx.alive >> s) & 1u)) passm |= 1u << s;
+            K bk = ((passm >> lane) & 1u) ? okey : A::kKeyMax;
 #pragma unroll
-                for (int off = 16; off >= 1; off >>= 1) bk = kmin(bk, shfl_xor_k(bk, off));
+            for (int off = SW / 2; off >= 1; off >>= 1) bk = kmin(bk, shfl_xor_k(bk, off));
+            if ((passm >> pick) & 1u) {
+                crc_ok = 1;
+            } else if (P.select_by_crc && passm) {
                 pick = A::key_idx(bk);
                 crc_ok = 1;
             }
         }
     }
-    const M pm = __shfl_sync(FULL, cx.metric, pick);
-    write_outputs(P, C, cx.row(pick), frame, lane);
-    if (lane == 0) {
-        if (P.crc_ok) P.crc_ok[frame] = uint8_t(crc_ok);
-        if (P.esc) P.esc[frame] = uint8_t(P.esc_level);
-        if (P.metric) P.metric[frame] = A::to_float(pm);
-        if (P.fail_list && C.crc_width > 0 && !crc_ok) P.fail_list[atomicAdd(P.fail_count, 1)] = frame;
+    const M pm = cx.sw.shfl(cx.metric, pick);
+    if (active) {
+        write_outputs<SW>(P, C, cx.row(pick), frame, lane);
+        if (lane == 0) {
+            if (P.crc_ok) P.crc_ok[frame] = uint8_t(crc_ok);
+            if (P.esc) P.esc[frame] = uint8_t(P.esc_level);
+            if (P.metric) P.metric[frame] = A::to_float(pm);
+            if (P.fail_list && C.crc_width > 0 && !crc_ok) P.fail_list[atomicAdd(P.fail_count, 1)] = frame;
+        }
     }
     __syncwarp();
 }
@@ -1005,7 +1080,7 @@ __device__ void list_frame(const LaunchParams& P, const DevCode& C, unsigned cha
 // whose subtree starts at leaf j, F down to the leaf, the hard (or frozen)
 // decision, then the h combines of every node that leaf completes.
 template <typename R>
-__device__ void sc_sub(Ctx<R>& cx, int d, int m, int lb, uint32_t fmask) {
+__device__ void sc_sub(Ctx<R, 32>& cx, int d, int m, int lb, uint32_t fmask) {
     using A = Arith<R>;
     using M = typename A::M;
     const int lane = cx.lane;
@@ -1087,11 +1162,12 @@ __device__ void sc_sub(Ctx<R>& cx, int d, int m, int lb, uint32_t fmask) {
 // ---- one frame, successive cancellation (sc_decoder.hpp:37-125) ---------
 template <typename R>
 __device__ void sc_frame(const LaunchParams& P, const DevCode& C, unsigned char* sm,
-                         unsigned char* gs, int frame, int lane) {
+                         unsigned char* gs, int frame, const Sub<32>& sw) {
     using A = Arith<R>;
     using M = typename A::M;
-    Ctx<R> cx;
-    setup_ctx(cx, P, C, sm, gs, frame, lane, 1);
+    Ctx<R, 32> cx;
+    setup_ctx(cx, P, C, sm, gs, frame, sw, 1);
+    const int lane = cx.lane;
     uint32_t* row = cx.row(0);
     const uint32_t* sched = C.sched_sc;
     const int nops = C.nops_sc;
@@ -1103,7 +1179,7 @@ __device__ void sc_frame(const LaunchParams& P, const DevCode& C, unsigned char*
         case OP_F:
         case OP_G: op_fg(cx, d, m, lb, 1, code == OP_G); break;
         case OP_H: op_h(cx, m, lb, 1); break;
-        case OP_FROZEN: span_fill_warp(row, lb, m, 0, lane); __syncwarp(); break;
+        case OP_FROZEN: span_fill<32>(row, lb, m, 0, lane); __syncwarp(); break;
         case OP_INFO:
             if (lane == 0) span_fill_lane(row, lb, 1, A::val(cx.llr(0, d)[0]) < M(0));
             __syncwarp();
@@ -1111,7 +1187,7 @@ __device__ void sc_frame(const LaunchParams& P, const DevCode& C, unsigned char*
         case OP_REP: {
             rep_fold(cx, d, m, 1);
             const int bit = mfrom<M>(cx.fx->st_a1[0]) < M(0);
-            span_fill_warp(row, lb, m, bit, lane);
+            span_fill<32>(row, lb, m, bit, lane);
             __syncwarp();
             break;
         }
@@ -1144,8 +1220,8 @@ __device__ void sc_frame(const LaunchParams& P, const DevCode& C, unsigned char*
         }
     }
     int crc_ok = 0;
-    if (C.crc_width > 0) crc_ok = row_syndrome(C, row, lane) == 0;
-    write_outputs(P, C, row, frame, lane);
+    if (C.crc_width > 0) crc_ok = row_syndrome<32>(C, row, lane) == 0;
+    write_outputs<32>(P, C, row, frame, lane);
     if (lane == 0) {
         if (P.crc_ok) P.crc_ok[frame] = uint8_t(crc_ok);
         if (P.esc) P.esc[frame] = 1;
@@ -1159,23 +1235,34 @@ __device__ void sc_frame(const LaunchParams& P, const DevCode& C, unsigned char*
 #define PLB_MINBLOCKS 8
 #endif
 
-// KV = 0: SC pass; KV = 1..6: list pass at L = 1, 2, 4, 8, 16, 32.
-template <typename R, int KV>
+// KV = 0: SC pass; KV = 1..6: list pass at L = 1, 2, 4, 8, 16, 32.  A warp
+// holds 32/SW frames (SW < 32 only for single-code batches).
+template <typename R, int KV, int SW>
 __global__ void __launch_bounds__(kMaxWarpsPerBlock * 32, PLB_MINBLOCKS) decode_kernel(const LaunchParams P) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    constexpr int FPW = 32 / SW;
+    const int wl = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    Sub<SW> sw;
+    sw.id = wl / SW;
+    sw.base = sw.id * SW;
+    sw.lane = wl - sw.base;
     const int64_t gw = int64_t(blockIdx.x) * (blockDim.x >> 5) + wib;
-    unsigned char* sm = smem_raw + wib * P.smem_per_warp;
-    unsigned char* gs = static_cast<unsigned char*>(P.gscratch) + gw * P.gscratch_per_warp;
+    unsigned char* sm = smem_raw + wib * P.smem_per_warp + sw.id * P.smem_per_frame;
+    unsigned char* gs = static_cast<unsigned char*>(P.gscratch) + (gw * FPW + sw.id) * P.gscratch_per_frame;
     const long long count = P.frame_list ? (long long)(*P.frame_count) : (long long)P.nframes;
     for (;;) {
-        const long long idx = claim(P, lane);
-        if (idx >= count) break;
+        unsigned long long i0 = 0;
+        if (wl == 0) i0 = atomicAdd(P.work, (unsigned long long)FPW);
+        const long long idx0 = (long long)__shfl_sync(FULL, i0, 0);
+        if (idx0 >= count) break;
+        const long long mine = idx0 + sw.id;
+        const bool active = mine < count;
+        const long long idx = active ? mine : idx0; // idle sub-warps shadow frame idx0
         const int frame = P.frame_list ? P.frame_list[idx] : int(idx);
         const int cid = P.code_id ? P.code_id[frame] : 0;
         const DevCode C = P.codes[cid];
-        if constexpr (KV > 0) list_frame<R, KV>(P, C, sm, gs, frame, lane);
-        else sc_frame<R>(P, C, sm, gs, frame, lane);
+        if constexpr (KV > 0) list_frame<R, KV, SW>(P, C, sm, gs, frame, active, sw);
+        else sc_frame<R>(P, C, sm, gs, frame, sw);
     }
 }
 
@@ -1212,21 +1299,23 @@ __global__ void selftest_kernel(unsigned long long* bad) {
     if (nbad) atomicAdd(bad, nbad);
 }
 
+// kernel of a pass: kv = 0 (SC) or 1..6 (list at L = 1..32), frames/warp fpw
 template <typename R>
-void (*kernel_for(int kv))(LaunchParams) {
+void (*kernel_for(int kv, int fpw))(LaunchParams) {
+    if (fpw == 4) return kv == 1 ? decode_kernel<R, 1, 8> : decode_kernel<R, 2, 8>;
+    if (fpw == 2) return kv == 3 ? decode_kernel<R, 3, 16> : decode_kernel<R, 4, 16>;
     switch (kv) {
-    case 0: return decode_kernel<R, 0>;
-    case 1: return decode_kernel<R, 1>;
-    case 2: return decode_kernel<R, 2>;
-    case 3: return decode_kernel<R, 3>;
-    case 4: return decode_kernel<R, 4>;
-    case 5: return decode_kernel<R, 5>;
-    default: return decode_kernel<R, 6>;
+    case 0: return decode_kernel<R, 0, 32>;
+    case 1: return decode_kernel<R, 1, 32>;
+    case 2: return decode_kernel<R, 2, 32>;
+    case 3: return decode_kernel<R, 3, 32>;
+    case 4: return decode_kernel<R, 4, 32>;
+    case 5: return decode_kernel<R, 5, 32>;
+    default: return decode_kernel<R, 6, 32>;
     }
 }
 
-// kernel variant of a pass: 0 = SC, 1..6 = list at L = 1..32
-int cw_of(int l, bool list) {
+int kv_of(int l, bool list) {
     if (!list) return 0;
     int kv = 1;
     while ((1 << (kv - 1)) < l && kv < 6) ++kv;
@@ -1234,9 +1323,9 @@ int cw_of(int l, bool list) {
 }
 
 template <typename R>
-cudaError_t launch(const LaunchParams& p, int cw, int grid, cudaStream_t s) {
+cudaError_t launch(const LaunchParams& p, int kv, int grid, cudaStream_t s) {
     const int smem = p.smem_per_warp * p.wpb;
-    auto kern = kernel_for<R>(cw);
+    auto kern = kernel_for<R>(kv, p.fpw);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     kern<<<grid, p.wpb * 32, smem, s>>>(p);
@@ -1244,8 +1333,8 @@ cudaError_t launch(const LaunchParams& p, int cw, int grid, cudaStream_t s) {
 }
 
 template <typename R>
-int occupancy(int cw, int smem, int wpb) {
-    auto kern = kernel_for<R>(cw);
+int occupancy(int kv, int fpw, int smem, int wpb) {
+    auto kern = kernel_for<R>(kv, fpw);
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
         cudaGetLastError();
         return 0;
@@ -1260,26 +1349,27 @@ int occupancy(int cw, int smem, int wpb) {
 
 } // namespace
 
-int64_t smem_bytes_per_warp(int nmax, int l, int elem_bytes, int seg_smem_max) {
+int64_t smem_bytes_per_frame(int nmax, int l, int elem_bytes, int seg_smem_max) {
     return layout_query(nmax, l, elem_bytes, seg_smem_max, 0).smem_total;
 }
-int64_t gscratch_bytes_per_warp(int nmax, int l, int elem_bytes, int seg_smem_max) {
+int64_t gscratch_bytes_per_frame(int nmax, int l, int elem_bytes, int seg_smem_max) {
     return layout_query(nmax, l, elem_bytes, seg_smem_max, 0).gmem_total;
 }
+int frames_per_warp_max(int l) { return l <= 2 ? 4 : l <= 8 ? 2 : 1; }
 
 cudaError_t launch_sc(const LaunchParams& p, int precision, int grid, cudaStream_t s) {
     return precision == 0 ? launch<float>(p, 0, grid, s) : launch<int8_t>(p, 0, grid, s);
 }
 cudaError_t launch_list(const LaunchParams& p, int precision, int grid, cudaStream_t s) {
-    const int cw = cw_of(p.l, true);
-    return precision == 0 ? launch<float>(p, cw, grid, s) : launch<int8_t>(p, cw, grid, s);
+    const int kv = kv_of(p.l, true);
+    return precision == 0 ? launch<float>(p, kv, grid, s) : launch<int8_t>(p, kv, grid, s);
 }
 int occupancy_sc(int precision, int smem, int wpb) {
-    return precision == 0 ? occupancy<float>(0, smem, wpb) : occupancy<int8_t>(0, smem, wpb);
+    return precision == 0 ? occupancy<float>(0, 1, smem, wpb) : occupancy<int8_t>(0, 1, smem, wpb);
 }
-int occupancy_list(int precision, int l, int smem, int wpb) {
-    const int cw = cw_of(l, true);
-    return precision == 0 ? occupancy<float>(cw, smem, wpb) : occupancy<int8_t>(cw, smem, wpb);
+int occupancy_list(int precision, int l, int fpw, int smem, int wpb) {
+    const int kv = kv_of(l, true);
+    return precision == 0 ? occupancy<float>(kv, fpw, smem, wpb) : occupancy<int8_t>(kv, fpw, smem, wpb);
 }
 
 cudaError_t kernel_selftest(unsigned long long* mismatches) {

@@ -75,28 +75,33 @@ struct LaunchParams {
     uint8_t* esc;              // nullable
     float* metric;             // nullable
     void* gscratch;            // global spill for the large LLR segments
-    int64_t gscratch_per_warp; // bytes
+    int64_t gscratch_per_frame;// bytes per in-flight frame
     int32_t l;                 // list size of this pass (1 for SC)
     int32_t select_by_crc;
     int32_t seg_smem_max;      // segments with more elements live in gscratch
     int32_t nmax;              // largest n over the codes
-    int32_t smem_per_warp;     // bytes
+    int32_t smem_per_warp;     // bytes (= fpw * smem_per_frame)
+    int32_t smem_per_frame;    // bytes
     int32_t esc_level;         // value written to esc[] by this pass
     int32_t wpb;               // warps per block (1, 2 or 4)
+    int32_t fpw;               // frames per warp (1, 2 or 4; >1 needs one code)
 };
 
 constexpr int kMaxWarpsPerBlock = 4; // a block is 1, 2 or 4 independent warps
 
-// Bytes of shared memory / global scratch one warp needs for a pass.
-int64_t smem_bytes_per_warp(int nmax, int l, int elem_bytes, int seg_smem_max);
-int64_t gscratch_bytes_per_warp(int nmax, int l, int elem_bytes, int seg_smem_max);
+// Bytes of shared memory / global scratch one in-flight frame needs.
+int64_t smem_bytes_per_frame(int nmax, int l, int elem_bytes, int seg_smem_max);
+int64_t gscratch_bytes_per_frame(int nmax, int l, int elem_bytes, int seg_smem_max);
+// Frames per warp of the sub-warp kernel of list size l (a list pass runs
+// either that many or 1).
+int frames_per_warp_max(int l);
 
 // Kernel launchers (kernels.cu).  Return cudaError_t of the launch.
 cudaError_t launch_sc(const LaunchParams& p, int precision, int grid, cudaStream_t s);
 cudaError_t launch_list(const LaunchParams& p, int precision, int grid, cudaStream_t s);
 // Max resident blocks per SM for a kernel at the given dynamic smem.
 int occupancy_sc(int precision, int smem_bytes, int wpb);
-int occupancy_list(int precision, int l, int smem_bytes, int wpb);
+int occupancy_list(int precision, int l, int fpw, int smem_bytes, int wpb);
 // Exhaustive device check of the packed int8 f/g against the scalar kernels.
 cudaError_t kernel_selftest(unsigned long long* mismatches);
 
