@@ -451,15 +451,18 @@ RungCfg plan_rung(const pl_handle& h, int l, bool list, bool ladder = false) {
     std::vector<int> fpws;
     // a list size has kernels for fmax and 1 frames per warp
     if (forced_fpw) {
-        fpws.push_back(std::atoi(forced_fpw) > 1 ? fmax : 1);
+        const int f = std::atoi(forced_fpw);
+        fpws.push_back(list && h.codes.size() == 1 && plb::frames_per_warp_ok(l, f) ? f : 1);
     } else {
         fpws.push_back(fmax);
         if (fmax > 1) fpws.push_back(1);
     }
-    RungCfg best;
-    best.l = l;
-    int best_warps = 0;
+    RungCfg pick;
+    pick.l = l;
     for (int fpw : fpws) {
+        RungCfg best;
+        best.l = l;
+        int best_warps = 0;
         // 4-warp blocks first; 2 / 1 when a warp's area is too big (large N x L)
         for (int wpb = plb::kMaxWarpsPerBlock; wpb >= 1; wpb >>= 1) {
             for (int seg : cands) {
@@ -483,10 +486,15 @@ RungCfg plan_rung(const pl_handle& h, int l, bool list, bool ladder = false) {
             }
             if (best_warps >= target) break;
         }
-        if (best_warps >= target) break;
+        // several frames per warp pay off down to half the warp target
+        // (measured: cfg1 at 24 resident 2-frame warps beats 32 1-frame ones)
+        if (best.grid > 0 && (best_warps * 2 >= target || fpw == fpws.back())) {
+            pick = best;
+            break;
+        }
     }
-    if (best.grid <= 0) throw ConfigError("no launch configuration fits this code / list size on the device");
-    return best;
+    if (pick.grid <= 0) throw ConfigError("no launch configuration fits this code / list size on the device");
+    return pick;
 }
 
 void ensure_lists(pl_handle& h, int64_t nframes) {

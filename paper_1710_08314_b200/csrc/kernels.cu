@@ -300,16 +300,23 @@ __device__ __forceinline__ void vst(R* p, const Vec<R, G>& x) {
 }
 
 // ---- per-frame shared-memory area ----------------------------------------
+// (followed by the bufidx rows, [slot][depth] -> buffer index in the depth
+// pool, 16 bytes per slot of the pass's list size)
 struct alignas(16) Fixed {
-    uint8_t bufidx[32 * 16]; // [slot][depth] -> buffer index in the depth pool
     uint8_t alive_list[32];  // rank -> slot, ascending
     uint8_t freetab[32];     // k -> k-th free slot, ascending
     uint8_t dsrc[32], dtgt[32]; // k-th duplicate of a fork: source, target
     uint32_t met_s[32];      // metric by slot (fork hand-over)
-    int32_t st_i1[32], st_i2[32], st_w[32]; // per-rank node statistics
-    uint32_t st_a1[32], st_a2[32];
     uint64_t pool[16];       // generic address of each depth pool
-    uint32_t scv[6 * 32];    // OP_SCSUB: per-level LLRs of the subtree, [level][lane]
+    union {
+        struct {
+            int32_t st_i1[32], st_i2[32], st_w[32]; // per-rank node statistics
+            uint32_t st_a1[32], st_a2[32];
+        };
+        // OP_SCSUB: per-level LLRs of the subtree, [level][lane] (SC pass,
+        // never live together with a node's statistics)
+        uint32_t scv[6 * 32];
+    };
 };
 static_assert(sizeof(Fixed) % 16 == 0, "fixed area alignment");
 
@@ -320,7 +327,7 @@ __host__ __device__ inline int ilog2(int v) {
 }
 __host__ __device__ inline int align16(int v) { return (v + 15) & ~15; }
 
-// Shared-memory layout of one frame: Fixed | psum rows | depth pools that
+// Shared-memory layout of one frame: Fixed | bufidx | psum rows | depth pools that
 // fit (segment <= segmax values); larger segments go to the frame's global
 // scratch.  want_d selects which depth's pool offset to return.
 struct LayoutQ {
@@ -333,7 +340,7 @@ __host__ __device__ inline int row_stride(int rw) { return rw >= 4 ? rw + 4 : (r
 
 __host__ __device__ inline LayoutQ layout_query(int n, int l, int esz, int segmax, int want_d) {
     LayoutQ q{};
-    int off = int(sizeof(Fixed));
+    int off = int(sizeof(Fixed)) + align16(16 * l);
     q.rw = n >= 32 ? n / 32 : 1;
     q.psum_off = off;
     off = align16(off + 4 * l * row_stride(q.rw));
@@ -381,9 +388,10 @@ struct Ctx {
     M metric;       // lane s: metric of slot s
 
     __device__ __forceinline__ R* pool(int d) const { return reinterpret_cast<R*>(fx->pool[d]); }
+    __device__ __forceinline__ uint8_t* bix() const { return reinterpret_cast<uint8_t*>(fx + 1); }
     __device__ __forceinline__ R* llr(int p, int d) const {
         if (d == 0) return const_cast<R*>(chan);
-        return pool(d) + int(fx->bufidx[p * 16 + d]) * (n >> d);
+        return pool(d) + int(bix()[p * 16 + d]) * (n >> d);
     }
     __device__ __forceinline__ uint32_t* row(int p) const { return ps + p * row_stride(rw); }
     __device__ __forceinline__ bool is_alive() const { return (alive >> lane) & 1u; }
@@ -453,7 +461,7 @@ __device__ __forceinline__ void fg_run(Ctx<R, SW>& cx, int d, int h, int lb, int
     for (int t = cx.lane; t < total; t += SW) {
         const int r = t >> lg;
         const int p = cx.fx->alive_list[r];
-        const R* in = d == 0 ? inp : inp + int(cx.fx->bufidx[p * 16 + d]) * seg;
+        const R* in = d == 0 ? inp : inp + int(cx.bix()[p * 16 + d]) * seg;
         fg_item<R, G>(in, outp + r * h, cx.row(p), h, t & (cp - 1), lb, is_g);
     }
 }
@@ -463,7 +471,7 @@ __device__ void op_fg(Ctx<R, SW>& cx, int d, int m, int lb, int na, bool is_g) {
     constexpr int VE = 16 / int(sizeof(R));
     const int h = m >> 1;
     // the child segment of the path of rank r goes to buffer r (see header)
-    if (cx.is_alive()) cx.fx->bufidx[cx.lane * 16 + d + 1] = uint8_t(cx.myrank);
+    if (cx.is_alive()) cx.bix()[cx.lane * 16 + d + 1] = uint8_t(cx.myrank);
     if (h >= VE) fg_run<R, SW, VE>(cx, d, h, lb, na, is_g);
     else fg_run<R, SW, 1>(cx, d, h, lb, na, is_g);
     __syncwarp();
@@ -621,8 +629,8 @@ __device__ void fork_apply(Ctx<R, SW>& cx, const typename Arith<R>::M (&cm)[CPL]
             cx.fx->dsrc[k] = uint8_t(src);
             cx.fx->dtgt[k] = uint8_t(tgt);
             // 3. duplicate: the LLR pointer row ...
-            *reinterpret_cast<uint4*>(cx.fx->bufidx + tgt * 16) =
-                *reinterpret_cast<const uint4*>(cx.fx->bufidx + src * 16);
+            *reinterpret_cast<uint4*>(cx.bix() + tgt * 16) =
+                *reinterpret_cast<const uint4*>(cx.bix() + src * 16);
         }
         __syncwarp();
         // ... and the decided partial sums incl. the node span (which holds
@@ -977,7 +985,7 @@ __device__ void setup_ctx(Ctx<R, SW>& cx, const LaunchParams& P, const DevCode& 
         const LayoutQ q = layout_query(C.n, l, int(sizeof(R)), P.seg_smem_max, d);
         cx.fx->pool[d] = reinterpret_cast<uint64_t>((q.pool_in_smem ? sm : gs) + q.pool_off);
     }
-    if (cx.lane == 0) *reinterpret_cast<uint4*>(cx.fx->bufidx) = make_uint4(0, 0, 0, 0);
+    if (cx.lane == 0) *reinterpret_cast<uint4*>(cx.bix()) = make_uint4(0, 0, 0, 0);
     cx.metric = typename Arith<R>::M(0);
     __syncwarp();
     cx.set_alive(1u);
@@ -1302,6 +1310,7 @@ __global__ void selftest_kernel(unsigned long long* bad) {
 // kernel of a pass: kv = 0 (SC) or 1..6 (list at L = 1..32), frames/warp fpw
 template <typename R>
 void (*kernel_for(int kv, int fpw))(LaunchParams) {
+    // (8-lane sub-warps measured slower than 16-lane ones at L = 4 and 8)
     if (fpw == 4) return kv == 1 ? decode_kernel<R, 1, 8> : decode_kernel<R, 2, 8>;
     if (fpw == 2) return kv == 3 ? decode_kernel<R, 3, 16> : decode_kernel<R, 4, 16>;
     switch (kv) {
@@ -1356,6 +1365,7 @@ int64_t gscratch_bytes_per_frame(int nmax, int l, int elem_bytes, int seg_smem_m
     return layout_query(nmax, l, elem_bytes, seg_smem_max, 0).gmem_total;
 }
 int frames_per_warp_max(int l) { return l <= 2 ? 4 : l <= 8 ? 2 : 1; }
+bool frames_per_warp_ok(int l, int fpw) { return fpw == 1 || fpw == frames_per_warp_max(l); }
 
 cudaError_t launch_sc(const LaunchParams& p, int precision, int grid, cudaStream_t s) {
     return precision == 0 ? launch<float>(p, 0, grid, s) : launch<int8_t>(p, 0, grid, s);

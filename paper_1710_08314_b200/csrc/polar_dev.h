@@ -95,6 +95,7 @@ int64_t gscratch_bytes_per_frame(int nmax, int l, int elem_bytes, int seg_smem_m
 // Frames per warp of the sub-warp kernel of list size l (a list pass runs
 // either that many or 1).
 int frames_per_warp_max(int l);
+bool frames_per_warp_ok(int l, int fpw); // a kernel exists for (l, fpw)
 
 // Kernel launchers (kernels.cu).  Return cudaError_t of the launch.
 cudaError_t launch_sc(const LaunchParams& p, int precision, int grid, cudaStream_t s);
