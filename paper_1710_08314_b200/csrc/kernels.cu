@@ -473,6 +473,7 @@ __device__ void op_fg(Ctx<R, SW>& cx, int d, int m, int lb, int na, bool is_g) {
     // the child segment of the path of rank r goes to buffer r (see header)
     if (cx.is_alive()) cx.bix()[cx.lane * 16 + d + 1] = uint8_t(cx.myrank);
     if (h >= VE) fg_run<R, SW, VE>(cx, d, h, lb, na, is_g);
+    else if (Arith<R>::kFixed && h >= 4) fg_run<R, SW, 4>(cx, d, h, lb, na, is_g); // one SWAR word
     else fg_run<R, SW, 1>(cx, d, h, lb, na, is_g);
     __syncwarp();
 }

@@ -31,6 +31,8 @@ def main():
     ap.add_argument("rep")
     ap.add_argument("--frames", type=int, default=0)
     ap.add_argument("--top", type=int, default=30)
+    ap.add_argument("--src", default="", help="kernels.cu of the profiled revision: "
+                    "also bucket instructions by enclosing function")
     a = ap.parse_args()
     det = list(csv.reader(io.StringIO(ncu(["-i", a.rep, "--page", "details", "--csv"]))))
     hdr = det[0]
@@ -93,6 +95,36 @@ def main():
             continue
         s = text.get(k, "").strip().replace("|", "\\|")[:80]
         print(f"| {k[0]}:{k[1]} | {v[0] / ti * 100:.1f} | {v[1] / ts * 100:.1f} | `{s}` |")
+    if a.src:
+        by_function(agg, ti, ts, a.src)
+
+
+def by_function(agg, ti, ts, path):
+    """Bucket kernels.cu lines by the function whose definition precedes them
+    (inlined helpers count where they are written; intrinsic headers apart)."""
+    import re
+    starts = []
+    for i, line in enumerate(open(path), 1):
+        m = re.match(r"^(?:__device__|__global__|template <.*> __global__)[^(]*?\b(\w+)\(", line)
+        if m:
+            starts.append((i, m.group(1)))
+    fn = collections.defaultdict(lambda: [0.0, 0.0])
+    for k, v in agg.items():
+        if k is None:
+            continue
+        name = k[0]
+        if k[0] == "kernels.cu":
+            name = "(file scope)"
+            for ln, f in starts:
+                if ln <= k[1]:
+                    name = f
+        fn[name][0] += v[0]
+        fn[name][1] += v[1]
+    print("\n## by function (inlined helpers attributed where written)\n")
+    print("| function | inst % | stall % |\n|---|---|---|")
+    for k, v in sorted(fn.items(), key=lambda kv: -kv[1][0]):
+        if v[0] / ti >= 0.002 or v[1] / ts >= 0.002:
+            print(f"| {k} | {v[0] / ti * 100:.1f} | {v[1] / ts * 100:.1f} |")
 
 
 if __name__ == "__main__":
