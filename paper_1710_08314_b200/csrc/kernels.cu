@@ -313,9 +313,10 @@ struct alignas(16) Fixed {
             int32_t st_i1[32], st_i2[32], st_w[32]; // per-rank node statistics
             uint32_t st_a1[32], st_a2[32];
         };
-        // OP_SCSUB: per-level LLRs of the subtree, [level][lane] (SC pass,
+        // OP_SCSUB: per-level LLRs of the subtree, [level][lane], levels
+        // 0..4 (the leaf level of a 32-subtree is never read back; SC pass,
         // never live together with a node's statistics)
-        uint32_t scv[6 * 32];
+        uint32_t scv[5 * 32];
     };
 };
 static_assert(sizeof(Fixed) % 16 == 0, "fixed area alignment");
@@ -1133,7 +1134,7 @@ __device__ void sc_sub(Ctx<R, 32>& cx, int d, int m, int lb, uint32_t fmask) {
             const int h = s >> 1;
             const M b = __shfl_down_sync(FULL, vk, h);
             const M fv = M(A::f(R(vk), R(b)));
-            if (lane >= j && lane < j + h) V[(k + 1) * 32 + lane] = fv;
+            if (lane >= j && lane < j + h && k < 4) V[(k + 1) * 32 + lane] = fv;
             vk = fv;
             ++k;
             __syncwarp();
@@ -1154,7 +1155,7 @@ __device__ void sc_sub(Ctx<R, 32>& cx, int d, int m, int lb, uint32_t fmask) {
         const M a = __shfl_up_sync(FULL, pv, h);
         const uint32_t xb = __shfl_up_sync(FULL, x, h);
         const M gv = M(A::g(R(a), R(pv), xb));
-        if (lane >= j && lane < j + h) V[(kk + 1) * 32 + lane] = gv;
+        if (lane >= j && lane < j + h && kk < 4) V[(kk + 1) * 32 + lane] = gv;
         vk = gv;
         k = kk + 1;
         __syncwarp();
