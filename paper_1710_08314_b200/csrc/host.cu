@@ -200,16 +200,33 @@ int ilog2i(int v) {
     return r;
 }
 
-// list schedule: the walk of list_decoder.hpp:174-224
-void emit_list(const std::vector<Node>& t, int ni, std::vector<uint32_t>& s) {
+// list schedule: the walk of list_decoder.hpp:174-224.  A leaf child of at
+// most fuse_max values replaces its parent's F (G) op: the leaf op computes
+// its LLRs in registers (kOpFused), which skips a round trip through the
+// depth pool and an op.
+void emit_list(const std::vector<Node>& t, int ni, std::vector<uint32_t>& s, int fuse_max) {
     const Node& nd = t[size_t(ni)];
     const int lg = ilog2i(nd.size);
+    auto fusable = [&](int ci) {
+        const Node& c = t[size_t(ci)];
+        return c.kind != NK_BRANCH && c.size <= fuse_max;
+    };
     switch (nd.kind) {
     case NK_BRANCH:
-        s.push_back(plb::op_pack(plb::OP_F, nd.depth, lg, nd.lb));
-        emit_list(t, nd.left, s);
-        s.push_back(plb::op_pack(plb::OP_G, nd.depth, lg, nd.lb));
-        emit_list(t, nd.right, s);
+        if (fusable(nd.left)) {
+            emit_list(t, nd.left, s, fuse_max);
+            s.back() |= plb::kOpFused;
+        } else {
+            s.push_back(plb::op_pack(plb::OP_F, nd.depth, lg, nd.lb));
+            emit_list(t, nd.left, s, fuse_max);
+        }
+        if (fusable(nd.right)) {
+            emit_list(t, nd.right, s, fuse_max);
+            s.back() |= plb::kOpFused | plb::kOpFusedG;
+        } else {
+            s.push_back(plb::op_pack(plb::OP_G, nd.depth, lg, nd.lb));
+            emit_list(t, nd.right, s, fuse_max);
+        }
         s.push_back(plb::op_pack(plb::OP_H, nd.depth, lg, nd.lb));
         break;
     case NK_FROZEN:
@@ -336,7 +353,7 @@ HostCode make_host_code(const pl_code& c, const pl_decoder& dec) {
     std::vector<Node> tree;
     tree.reserve(size_t(2 * c.n));
     build_tree(tree, h.frozen.data(), 0, c.n, 0, pc);
-    emit_list(tree, 0, h.sched_list);
+    emit_list(tree, 0, h.sched_list, dec.precision == PL_I8 ? plb::kFuseMaxI8 : plb::kFuseMaxF32);
     emit_sc(tree, 0, h.sched_sc, h.frozen.data());
 
     if (crc) {

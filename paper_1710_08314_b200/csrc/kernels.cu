@@ -868,19 +868,197 @@ __device__ void rep_pen(Ctx<R, SW>& cx, int d, int m, int na) {
     __syncwarp();
 }
 
+// A leaf of m <= MF values fused with its parent's F or G (kOpFused): lane r
+// < na computes the m LLRs of the path of rank r in registers from the
+// parent segment (depth d-1) and takes the leaf's statistics in-lane, with
+// the same kernels, orders and tie rules as the unfused ops (r1spc_stats,
+// rep_fold/rep_pen, list_frozen; list_decoder.hpp:227-333).  The depth-d
+// segment is never written: nothing reads a leaf's LLRs afterwards.
+template <typename R, int SW>
+__device__ void fused_leaf(Ctx<R, SW>& cx, int code, int d, int m, int lb, int na, bool is_g) {
+    using A = Arith<R>;
+    using M = typename A::M;
+    using K = typename A::Key;
+    constexpr int MF = sizeof(R) == 1 ? kFuseMaxI8 : kFuseMaxF32;
+    const int r = cx.lane;
+    M pen = M(0);
+    if constexpr (A::kFixed) {
+        // int8: the m <= 8 child values packed in one u64 (value i in byte
+        // i), produced by the SWAR f / g, statistics in rolled loops (small
+        // code: the decode loop must stay inside the instruction cache)
+        if (r < na) {
+            const int p = cx.fx->alive_list[r];
+            const R* in = cx.llr(p, d - 1);
+            uint32_t* row = cx.row(p);
+            uint32_t bits = 0;
+            if (is_g) {
+                const int pos = lb - m; // the left sibling's decisions
+                bits = row[pos >> 5] >> (pos & 31);
+            }
+            uint64_t pk = 0;
+            if (m >= 4) {
+                #pragma unroll 1
+                for (int q = 0; q < m; q += 4) {
+                    const uint32_t a4 = *reinterpret_cast<const uint32_t*>(in + q);
+                    const uint32_t b4 = *reinterpret_cast<const uint32_t*>(in + m + q);
+                    const uint32_t c4 = is_g ? g_swar(a4, b4, (bits >> q) & 15u) : f_swar(a4, b4);
+                    pk |= uint64_t(c4) << (8 * q);
+                }
+            } else {
+                #pragma unroll 1
+                for (int i = 0; i < m; ++i) {
+                    const R c = is_g ? A::g(in[i], in[m + i], (bits >> i) & 1u) : A::f(in[i], in[m + i]);
+                    pk |= uint64_t(uint8_t(c)) << (8 * i);
+                }
+            }
+            auto at = [&](int i) { return int(int8_t(uint8_t(pk >> (8 * i)))); };
+            const uint32_t lo = uint32_t(pk), hi = uint32_t(pk >> 32);
+            const uint32_t mk = (1u << m) - 1u;
+            const uint32_t hb = ((((lo >> 7) & 0x01010101u) * 0x01020408u) >> 24 |
+                                 ((((hi >> 7) & 0x01010101u) * 0x01020408u) >> 24) << 4) & mk;
+            uint32_t* w = row + (lb >> 5);
+            const int sh = lb & 31;
+            if (code == OP_FROZEN) {
+                int s = 0; // non-negative terms: the saturating sum is order-free
+                #pragma unroll 1
+                for (int i = 0; i < m; ++i) s += max(0, -at(i));
+                pen = min(s, 127);
+                *w &= ~(mk << sh);
+            } else if (code == OP_INFO) {
+                cx.fx->st_a1[r] = mbits<M>(at(0));
+            } else if (code == OP_REP) {
+                // halving fold: value i of level len/2 = sat(i, i + len/2)
+                uint64_t x = pk;
+                #pragma unroll 1
+                for (int len = m; len > 1; len >>= 1) {
+                    uint64_t y = 0;
+                    #pragma unroll 1
+                    for (int i = 0; i < len / 2; ++i) {
+                        const int s = A::sat(int(int8_t(uint8_t(x >> (8 * i)))),
+                                             int(int8_t(uint8_t(x >> (8 * (i + len / 2))))));
+                        y |= uint64_t(uint8_t(int8_t(s))) << (8 * i);
+                    }
+                    x = y;
+                }
+                const int f0 = int(int8_t(uint8_t(x)));
+                const bool wn = f0 < 0;
+                int s = 0;
+                #pragma unroll 1
+                for (int i = 0; i < m; ++i) {
+                    const int vi = at(i);
+                    if (wn ? (vi > 0) : (vi < 0)) s += abs(vi);
+                }
+                cx.fx->st_w[r] = wn;
+                cx.fx->st_a1[r] = mbits<M>(f0);
+                cx.fx->st_a2[r] = mbits<M>(min(s, 127));
+            } else {
+                K k1 = A::kKeyMax, k2 = A::kKeyMax;
+                #pragma unroll 1
+                for (int i = 0; i < m; ++i) {
+                    const K kv = A::make_key(abs(at(i)), i);
+                    const K n1 = kmin(k1, kv);
+                    k2 = kmin(k2, kmax(k1, kv));
+                    k1 = n1;
+                }
+                *w = (*w & ~(mk << sh)) | (hb << sh);
+                cx.fx->st_i1[r] = A::key_idx(k1);
+                cx.fx->st_i2[r] = A::key_idx(k2);
+                cx.fx->st_a1[r] = mbits<M>(A::key_val(k1));
+                cx.fx->st_a2[r] = mbits<M>(A::key_val(k2));
+                cx.fx->st_w[r] = __popc(hb) & 1;
+            }
+        }
+    } else if (r < na) {
+        const int p = cx.fx->alive_list[r];
+        const R* in = cx.llr(p, d - 1);
+        uint32_t* row = cx.row(p);
+        uint32_t bits = 0;
+        if (is_g) {
+            const int pos = lb - m; // the left sibling's decisions
+            bits = row[pos >> 5] >> (pos & 31);
+        }
+        M v[MF];
+        uint32_t hb = 0;
+#pragma unroll
+        for (int i = 0; i < MF; ++i) {
+            if (i < m) {
+                const R a = in[i], b = in[m + i];
+                v[i] = A::val(is_g ? A::g(a, b, (bits >> i) & 1u) : A::f(a, b));
+                hb |= uint32_t(v[i] < M(0)) << i;
+            }
+        }
+        const uint32_t mk = (1u << m) - 1u;
+        uint32_t* w = row + (lb >> 5);
+        const int sh = lb & 31;
+        if (code == OP_FROZEN) { // list_frozen: sequential penalty, zero span
+#pragma unroll
+            for (int i = 0; i < MF; ++i)
+                if (i < m && v[i] < M(0)) pen = A::sat(pen, -v[i]);
+            *w &= ~(mk << sh);
+        } else if (code == OP_INFO) {
+            cx.fx->st_a1[r] = mbits<M>(v[0]);
+        } else if (code == OP_REP) { // rep_fold (halving) + rep_pen (sequential)
+            M x[MF];
+#pragma unroll
+            for (int i = 0; i < MF; ++i) x[i] = i < m ? v[i] : M(0);
+#pragma unroll
+            for (int len = MF; len > 1; len >>= 1)
+                if (len <= m)
+#pragma unroll
+                    for (int i = 0; i < len / 2; ++i) x[i] = A::sat(x[i], x[i + len / 2]);
+            const bool wn = x[0] < M(0);
+            M pw = M(0);
+#pragma unroll
+            for (int i = 0; i < MF; ++i)
+                if (i < m && (wn ? (v[i] > M(0)) : (v[i] < M(0)))) pw = A::sat(pw, A::mag(v[i]));
+            cx.fx->st_w[r] = wn;
+            cx.fx->st_a1[r] = mbits<M>(x[0]);
+            cx.fx->st_a2[r] = mbits<M>(pw);
+        } else { // R1 / SPC: hard decisions, two smallest (value, index), parity
+            K k1 = A::kKeyMax, k2 = A::kKeyMax;
+#pragma unroll
+            for (int i = 0; i < MF; ++i) {
+                if (i < m) {
+                    const K kv = A::make_key(A::mag(v[i]), i);
+                    const K n1 = kmin(k1, kv);
+                    k2 = kmin(k2, kmax(k1, kv));
+                    k1 = n1;
+                }
+            }
+            *w = (*w & ~(mk << sh)) | (hb << sh);
+            cx.fx->st_i1[r] = A::key_idx(k1);
+            cx.fx->st_i2[r] = A::key_idx(k2);
+            cx.fx->st_a1[r] = mbits<M>(A::key_val(k1));
+            cx.fx->st_a2[r] = mbits<M>(A::key_val(k2));
+            cx.fx->st_w[r] = __popc(hb) & 1;
+        }
+    }
+    __syncwarp();
+    if (code == OP_FROZEN) {
+        const M pr = cx.sw.shfl(pen, cx.myrank & (SW - 1));
+        if (cx.is_alive()) cx.metric = A::sat(cx.metric, pr);
+        cx.normalize();
+    }
+}
+
 // A forking node: per-path statistics, candidates in emission order
 // (ascending slot, then candidate number, list_decoder.hpp:240-333), one
 // shared fork_apply, normalisation.  C = candidates per lane, fixed per
 // kernel instantiation (4L <= SW*C).
 template <typename R, int SW, int C, int MAXW>
-__device__ void list_fork_node(Ctx<R, SW>& cx, int code, int d, int m, int lb, int na) {
+__device__ void list_fork_node(Ctx<R, SW>& cx, int code, int d, int m, int lb, int na, bool fused) {
     using A = Arith<R>;
     using M = typename A::M;
-    if (code == OP_R1 || code == OP_SPC) {
+    if (fused) {
+        // statistics already taken by fused_leaf
+    } else if (code == OP_R1 || code == OP_SPC) {
         r1spc_stats(cx, d, m, lb, na);
     } else if (code == OP_REP) {
         rep_fold(cx, d, m, na);
         rep_pen(cx, d, m, na);
+    } else { // INFO: the leaf LLR of rank r -> st_a1[r]
+        if (cx.lane < na) cx.fx->st_a1[cx.lane] = mbits<M>(A::val(cx.llr(cx.fx->alive_list[cx.lane], d)[0]));
+        __syncwarp();
     }
     const int lgb = code == OP_R1 ? 2 : 1; // candidates per path: 4 or 2
     M cm[C];
@@ -892,7 +1070,7 @@ __device__ void list_fork_node(Ctx<R, SW>& cx, int code, int d, int m, int lb, i
         const M base = cx.sw.shfl(cx.metric, p);
         cs[k] = p;
         if (code == OP_INFO) { // list_decoder.hpp:240-252
-            const M v = A::val(cx.llr(p, d)[0]);
+            const M v = mfrom<M>(cx.fx->st_a1[r]);
             cm[k] = A::sat(base, (j == 0) == (v < M(0)) ? A::mag(v) : M(0));
             cax[k] = pack_aux(j, -1);
         } else if (code == OP_REP) { // :276-305, preferred bit first
@@ -1017,10 +1195,15 @@ __device__ void list_frame(const LaunchParams& P, const DevCode& C, unsigned cha
         const uint32_t op = __ldg(sched + oi);
         const int code = op_code(op), d = op_depth(op), m = 1 << op_logm(op), lb = op_lb(op);
         const int na = __popc(cx.alive);
+        const bool fused = (op & kOpFused) != 0;
+        if (fused) fused_leaf(cx, code, d, m, lb, na, (op & kOpFusedG) != 0);
         if (code <= OP_G) op_fg(cx, d, m, lb, na, code == OP_G);
         else if (code == OP_H) op_h(cx, m, lb, na);
-        else if (code == OP_FROZEN) list_frozen(cx, d, m, lb, na);
-        else list_fork_node<R, SW, CW, MAXW>(cx, code, d, m, lb, na);
+        else if (code == OP_FROZEN) {
+            if (!fused) list_frozen(cx, d, m, lb, na);
+        } else {
+            list_fork_node<R, SW, CW, MAXW>(cx, code, d, m, lb, na, fused);
+        }
     }
     // finish (list_decoder.hpp:457-502): stable order by (metric, slot)
     using K = typename A::Key;

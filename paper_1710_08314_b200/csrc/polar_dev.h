@@ -33,14 +33,21 @@ enum Op : uint32_t {
                    // recursion's result is the hard decision and it is skipped
 };
 constexpr int kScSubMax = 32;
+// largest fused leaf (values held per lane): int8 / float
+constexpr int kFuseMaxI8 = 8, kFuseMaxF32 = 4;
 
+//   bit   28    (list schedules) fused leaf: the leaf's LLRs are not
+//               materialised; the leaf op computes them in registers from
+//               the parent segment (depth - 1) with F, or with G when
+//   bit   29    is set (the F / G op of the parent is then omitted)
+constexpr uint32_t kOpFused = 1u << 28, kOpFusedG = 1u << 29;
 __host__ __device__ inline uint32_t op_pack(uint32_t op, int depth, int logm, int lb) {
     return op | (uint32_t(depth) << 4) | (uint32_t(logm) << 8) | (uint32_t(lb) << 12);
 }
 __host__ __device__ inline int op_code(uint32_t w) { return int(w & 15u); }
 __host__ __device__ inline int op_depth(uint32_t w) { return int((w >> 4) & 15u); }
 __host__ __device__ inline int op_logm(uint32_t w) { return int((w >> 8) & 15u); }
-__host__ __device__ inline int op_lb(uint32_t w) { return int(w >> 12); }
+__host__ __device__ inline int op_lb(uint32_t w) { return int((w >> 12) & 0xffffu); }
 
 // ---- per-code device tables -------------------------------------------
 struct DevCode {
