@@ -264,13 +264,16 @@ __device__ __forceinline__ K merge_top(K a, K b, int lane) {
 // The W smallest of W*C keys (register k of each lane), ascending in
 // register 0: sort each register across the lanes, then merge pairwise.
 template <typename K, int C, int W>
-__device__ __forceinline__ void top_regs(K (&key)[C], int lane) {
+// Registers from nreg on hold only kKeyMax and are skipped (uniform).
+__device__ __forceinline__ void top_regs(K (&key)[C], int lane, int nreg) {
 #pragma unroll
-    for (int k = 0; k < C; ++k) key[k] = bitonic_lanes<K, W>(key[k], lane);
+    for (int k = 0; k < C; ++k)
+        if (k < nreg) key[k] = bitonic_lanes<K, W>(key[k], lane);
 #pragma unroll
     for (int w = 1; w < C; w <<= 1)
 #pragma unroll
-        for (int k = 0; k + w < C; k += 2 * w) key[k] = merge_top<K, W>(key[k], key[k + w], lane);
+        for (int k = 0; k + w < C; k += 2 * w)
+            if (k + w < nreg) key[k] = merge_top<K, W>(key[k], key[k + w], lane);
 }
 
 // ---- vector access of G consecutive values ----------------------------
@@ -596,7 +599,7 @@ __device__ void fork_apply(Ctx<R, SW>& cx, const typename Arith<R>::M (&cm)[CPL]
         else key[0] = bitonic_lanes<K, MAXW>(key[0], lane);
     } else {
         // only the best keep <= SW are needed, in order
-        top_regs<K, CPL, SW>(key, lane);
+        top_regs<K, CPL, SW>(key, lane, (ncand + SW - 1) / SW);
     }
     const int keep = min(cx.l, ncand);
     const bool kept = lane < keep;
