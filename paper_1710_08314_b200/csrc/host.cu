@@ -391,7 +391,10 @@ struct RungCfg {
     int grid = 0;
     int wpb = plb::kMaxWarpsPerBlock;
     int fpw = 1; // frames per warp (sub-warp decoding, single-code batches)
-    int64_t gscratch_total() const { return int64_t(grid) * wpb * fpw * gscratch_per_frame; }
+    int team = 1; // >1: blocks of `team` warps, one frame each
+    int64_t gscratch_total() const {
+        return int64_t(grid) * (team > 1 ? 1 : wpb * fpw) * gscratch_per_frame;
+    }
 };
 
 } // namespace
@@ -455,6 +458,44 @@ int target_warps_per_sm() {
 // reaches the target; PLB_FPW forces frames per warp.  Ladder rungs above
 // L = 4 see few frames (the failures of the rung below): one frame per warp
 // spreads them over more warps, which measured faster there.
+int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : dflt;
+}
+
+// Team mode (opt-in, PLB_TEAM=<warps>): a team of warps per frame, few
+// frames per SM, so the frames' depth pools (L x N values) stay in shared
+// memory and L2 instead of overflowing the L2 into HBM.  Only the element
+// ops (F/G, H) are split over the team; the path bookkeeping stays on warp
+// 0, and with 2-4 frames per SM that serial part dominates: measured 2.4x
+// slower than independent warps at L = 32 float, so it is
+// off by default.  The largest shared-memory share that still keeps
+// PLB_TEAM_BLOCKS frames resident per SM.
+RungCfg plan_team(const pl_handle& h, int l, int team, const std::vector<int>& cands) {
+    const int want = std::max(1, env_int("PLB_TEAM_BLOCKS", 2));
+    RungCfg best;
+    best.l = l;
+    int best_nb = 0;
+    for (int seg : cands) {
+        RungCfg c;
+        c.l = l;
+        c.seg_max = seg;
+        c.wpb = team;
+        c.team = team;
+        c.smem_per_frame = int(plb::smem_bytes_per_frame(h.nmax, l, h.esz, seg));
+        c.gscratch_per_frame = plb::gscratch_bytes_per_frame(h.nmax, l, h.esz, seg);
+        const int nb = plb::occupancy_list(h.dec.precision, l, 1, c.smem_per_frame, team, true);
+        if (nb <= 0) continue;
+        c.grid = nb * h.sms;
+        if (nb >= want) return c;
+        if (nb > best_nb) {
+            best = c;
+            best_nb = nb;
+        }
+    }
+    return best;
+}
+
 RungCfg plan_rung(const pl_handle& h, int l, bool list, bool ladder = false) {
     const char* forced = std::getenv("PLB_SEGMAX");
     const char* forced_fpw = std::getenv("PLB_FPW");
@@ -464,6 +505,15 @@ RungCfg plan_rung(const pl_handle& h, int l, bool list, bool ladder = false) {
     else
         for (int s = h.nmax; s >= 8; s >>= 1) cands.push_back(s);
     if (cands.empty()) cands.push_back(h.nmax); // tiny codes: everything in shared memory
+    if (list) {
+        const int team = std::min(plb::kMaxTeam, env_int("PLB_TEAM", 1));
+        // (team kernels exist for L = 16 and 32)
+        const int team_l = std::max(16, env_int("PLB_TEAM_L", h.dec.precision == PL_F32 ? 16 : 32));
+        if (team > 1 && l >= team_l) {
+            RungCfg t = plan_team(h, l, team, cands);
+            if (t.grid > 0) return t;
+        }
+    }
     const int fmax = (list && h.codes.size() == 1 && !(ladder && l > 4)) ? plb::frames_per_warp_max(l) : 1;
     std::vector<int> fpws;
     // a list size has kernels for fmax and 1 frames per warp
@@ -575,6 +625,7 @@ void run_decode(pl_handle& h, const void* llr, const int32_t* code_id, int64_t n
         p.esc_level = rc.l;
         p.wpb = rc.wpb;
         p.fpw = rc.fpw;
+        p.team = rc.team;
         if (h.profiling) {
             while (h.prof_ev.size() < size_t(2 * (slot + 1))) {
                 cudaEvent_t ev;

@@ -311,6 +311,8 @@ struct alignas(16) Fixed {
     uint8_t dsrc[32], dtgt[32]; // k-th duplicate of a fork: source, target
     uint32_t met_s[32];      // metric by slot (fork hand-over)
     uint64_t pool[16];       // generic address of each depth pool
+    uint32_t alive_w;        // alive-slot mask (read by the helper warps of a team)
+    uint32_t pad_[3];
     union {
         struct {
             int32_t st_i1[32], st_i2[32], st_w[32]; // per-rank node statistics
@@ -390,6 +392,9 @@ struct Ctx {
     unsigned alive; // sub-warp-uniform alive-slot mask
     int myrank;     // rank of slot `lane` among the alive slots
     M metric;       // lane s: metric of slot s
+    // element loops (F/G, H) run over a team of warps when team > 1: thread
+    // tt0 of tstride; otherwise tt0 = lane, tstride = SW
+    int tt0, tstride, team;
 
     __device__ __forceinline__ R* pool(int d) const { return reinterpret_cast<R*>(fx->pool[d]); }
     __device__ __forceinline__ uint8_t* bix() const { return reinterpret_cast<uint8_t*>(fx + 1); }
@@ -404,6 +409,7 @@ struct Ctx {
         alive = a;
         myrank = __popc(alive & sw.lt());
         if (is_alive()) fx->alive_list[myrank] = uint8_t(lane);
+        if (lane == 0) fx->alive_w = a;
         __syncwarp();
     }
 
@@ -462,7 +468,7 @@ __device__ __forceinline__ void fg_run(Ctx<R, SW>& cx, int d, int h, int lb, int
     const int seg = cx.n >> d;
     const int total = na << lg;
     #pragma unroll 1
-    for (int t = cx.lane; t < total; t += SW) {
+    for (int t = cx.tt0; t < total; t += cx.tstride) {
         const int r = t >> lg;
         const int p = cx.fx->alive_list[r];
         const R* in = d == 0 ? inp : inp + int(cx.bix()[p * 16 + d]) * seg;
@@ -471,36 +477,56 @@ __device__ __forceinline__ void fg_run(Ctx<R, SW>& cx, int d, int h, int lb, int
 }
 
 template <typename R, int SW>
-__device__ void op_fg(Ctx<R, SW>& cx, int d, int m, int lb, int na, bool is_g) {
+__device__ __forceinline__ void fg_elems(Ctx<R, SW>& cx, int d, int m, int lb, int na, bool is_g) {
     constexpr int VE = 16 / int(sizeof(R));
     const int h = m >> 1;
-    // the child segment of the path of rank r goes to buffer r (see header)
-    if (cx.is_alive()) cx.bix()[cx.lane * 16 + d + 1] = uint8_t(cx.myrank);
     if (h >= VE) fg_run<R, SW, VE>(cx, d, h, lb, na, is_g);
     else if (Arith<R>::kFixed && h >= 4) fg_run<R, SW, 4>(cx, d, h, lb, na, is_g); // one SWAR word
     else fg_run<R, SW, 1>(cx, d, h, lb, na, is_g);
-    __syncwarp();
+}
+
+// Team barrier around an element op: the control warp's shared-state writes
+// before it, the element results after it (team > 1 only).
+template <typename R, int SW>
+__device__ __forceinline__ void team_sync(const Ctx<R, SW>& cx) {
+    if (cx.team > 1) __syncthreads();
+    else __syncwarp();
+}
+
+template <typename R, int SW>
+__device__ void op_fg(Ctx<R, SW>& cx, int d, int m, int lb, int na, bool is_g) {
+    // the child segment of the path of rank r goes to buffer r (see header)
+    if (cx.is_alive()) cx.bix()[cx.lane * 16 + d + 1] = uint8_t(cx.myrank);
+    if (cx.team > 1) __syncthreads();
+    fg_elems(cx, d, m, lb, na, is_g);
+    team_sync(cx);
 }
 
 // psums[lb, lb+h) ^= psums[lb+h, lb+2h) for every alive path
 template <typename R, int SW>
-__device__ void op_h(Ctx<R, SW>& cx, int m, int lb, int na) {
+__device__ __forceinline__ void h_elems(Ctx<R, SW>& cx, int m, int lb, int na) {
     const int h = m >> 1;
     if (h >= 32) {
         const int W = h >> 5, lg = __ffs(W) - 1;
         const int total = na << lg;
         #pragma unroll 1
-        for (int t = cx.lane; t < total; t += SW) {
+        for (int t = cx.tt0; t < total; t += cx.tstride) {
             uint32_t* w = cx.row(cx.fx->alive_list[t >> lg]) + (lb >> 5) + (t & (W - 1));
             w[0] ^= w[W];
         }
-    } else if (cx.lane < na) {
-        uint32_t* w = cx.row(cx.fx->alive_list[cx.lane]) + (lb >> 5);
+    } else if (cx.tt0 < na) {
+        uint32_t* w = cx.row(cx.fx->alive_list[cx.tt0]) + (lb >> 5);
         const int s = lb & 31;
         const uint32_t mk = (1u << h) - 1u;
         *w ^= ((*w >> (s + h)) & mk) << s;
     }
-    __syncwarp();
+}
+
+template <typename R, int SW>
+__device__ void op_h(Ctx<R, SW>& cx, int m, int lb, int na) {
+    if (cx.team > 1) __syncthreads();
+    h_elems(cx, m, lb, na);
+    team_sync(cx);
 }
 
 // write `bit` over the span [lb, lb+m) of a psum row (whole sub-warp)
@@ -1149,7 +1175,7 @@ __device__ void write_outputs(const LaunchParams& P, const DevCode& C, const uin
     }
 }
 
-template <typename R, int SW>
+template <bool TEAM = false, typename R, int SW>
 __device__ void setup_ctx(Ctx<R, SW>& cx, const LaunchParams& P, const DevCode& C,
                           unsigned char* sm, unsigned char* gs, int frame, const Sub<SW>& sw,
                           int l) {
@@ -1163,6 +1189,10 @@ __device__ void setup_ctx(Ctx<R, SW>& cx, const LaunchParams& P, const DevCode& 
     const LayoutQ q0 = layout_query(C.n, l, int(sizeof(R)), P.seg_smem_max, 0);
     cx.ps = reinterpret_cast<uint32_t*>(sm + q0.psum_off);
     cx.rw = q0.rw;
+    // (constants outside team kernels: the team code folds away)
+    cx.team = TEAM ? P.team : 1;
+    cx.tt0 = cx.lane;
+    cx.tstride = TEAM ? 32 * P.team : SW;
     #pragma unroll 1
     for (int d = cx.lane + 1; d <= C.stages; d += SW) {
         const LayoutQ q = layout_query(C.n, l, int(sizeof(R)), P.seg_smem_max, d);
@@ -1182,14 +1212,14 @@ __host__ __device__ constexpr int kv_l(int kv) { return 1 << (kv - 1); }
 __host__ __device__ constexpr int kv_cw(int kv, int sw) { return (4 * kv_l(kv) + sw - 1) / sw; }
 __host__ __device__ constexpr int kv_maxw(int kv, int sw) { return 4 * kv_l(kv) < sw ? 4 * kv_l(kv) : sw; }
 
-template <typename R, int KV, int SW>
+template <typename R, int KV, int SW, bool TEAM>
 __device__ void list_frame(const LaunchParams& P, const DevCode& C, unsigned char* sm,
                            unsigned char* gs, int frame, bool active, const Sub<SW>& sw) {
     using A = Arith<R>;
     using M = typename A::M;
     constexpr int CW = kv_cw(KV, SW), MAXW = kv_maxw(KV, SW);
     Ctx<R, SW> cx;
-    setup_ctx(cx, P, C, sm, gs, frame, sw, P.l);
+    setup_ctx<TEAM>(cx, P, C, sm, gs, frame, sw, P.l);
     const int lane = cx.lane;
     const uint32_t* sched = C.sched_list;
     const int nops = C.nops_list;
@@ -1427,14 +1457,52 @@ __device__ void sc_frame(const LaunchParams& P, const DevCode& C, unsigned char*
     __syncwarp();
 }
 
+// A helper warp of a team (warps 1..team-1 of a block that decodes one
+// frame, large list sizes): walks the same schedule as the control warp
+// (warp 0, list_frame) and joins only the element ops (F/G, H), between the
+// same two block barriers op_fg / op_h place around them.  All path
+// bookkeeping stays with warp 0; the helpers read the alive list it
+// publishes in shared memory.
+template <typename R>
+__device__ void team_helper(const LaunchParams& P, const DevCode& C, unsigned char* sm,
+                            int frame, int wib) {
+    Ctx<R, 32> cx;
+    cx.lane = threadIdx.x & 31;
+    cx.n = C.n;
+    cx.l = P.l;
+    cx.chan = static_cast<const R*>(P.llr) + int64_t(frame) * P.llr_stride;
+    cx.fx = reinterpret_cast<Fixed*>(sm);
+    const LayoutQ q0 = layout_query(C.n, P.l, int(sizeof(R)), P.seg_smem_max, 0);
+    cx.ps = reinterpret_cast<uint32_t*>(sm + q0.psum_off);
+    cx.rw = q0.rw;
+    cx.team = P.team;
+    cx.tt0 = wib * 32 + cx.lane;
+    cx.tstride = 32 * P.team;
+    const uint32_t* sched = C.sched_list;
+    const int nops = C.nops_list;
+    #pragma unroll 1
+    for (int oi = 0; oi < nops; ++oi) {
+        const uint32_t op = __ldg(sched + oi);
+        const int code = op_code(op);
+        if (code > OP_H) continue; // control ops: warp 0 alone
+        const int d = op_depth(op), m = 1 << op_logm(op), lb = op_lb(op);
+        __syncthreads();
+        const int na = __popc(cx.fx->alive_w);
+        if (code == OP_H) h_elems(cx, m, lb, na);
+        else fg_elems(cx, d, m, lb, na, code == OP_G);
+        __syncthreads();
+    }
+}
+
 #ifndef PLB_MINBLOCKS
 #define PLB_MINBLOCKS 8
 #endif
 
 // KV = 0: SC pass; KV = 1..6: list pass at L = 1, 2, 4, 8, 16, 32.  A warp
 // holds 32/SW frames (SW < 32 only for single-code batches).
-template <typename R, int KV, int SW>
-__global__ void __launch_bounds__(kMaxWarpsPerBlock * 32, PLB_MINBLOCKS) decode_kernel(const LaunchParams P) {
+template <typename R, int KV, int SW, bool TEAM = false>
+__global__ void __launch_bounds__(kMaxTeam * 32, PLB_MINBLOCKS * kMaxWarpsPerBlock / kMaxTeam)
+decode_kernel(const LaunchParams P) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int FPW = 32 / SW;
     const int wl = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -1442,6 +1510,27 @@ __global__ void __launch_bounds__(kMaxWarpsPerBlock * 32, PLB_MINBLOCKS) decode_
     sw.id = wl / SW;
     sw.base = sw.id * SW;
     sw.lane = wl - sw.base;
+    if constexpr (TEAM && KV > 0 && SW == 32) {
+        {
+            // one frame per block: warp 0 controls, the others help
+            __shared__ long long s_claim;
+            const long long count = P.frame_list ? (long long)(*P.frame_count) : (long long)P.nframes;
+            unsigned char* gs = static_cast<unsigned char*>(P.gscratch) + int64_t(blockIdx.x) * P.gscratch_per_frame;
+            for (;;) {
+                if (threadIdx.x == 0) s_claim = (long long)atomicAdd(P.work, 1ull);
+                __syncthreads();
+                const long long idx = s_claim;
+                __syncthreads(); // all read before the next claim overwrites
+                if (idx >= count) break;
+                const int frame = P.frame_list ? P.frame_list[idx] : int(idx);
+                const int cid = P.code_id ? P.code_id[frame] : 0;
+                const DevCode C = P.codes[cid];
+                if (wib == 0) list_frame<R, KV, 32, true>(P, C, smem_raw, gs, frame, true, sw);
+                else team_helper<R>(P, C, smem_raw, frame, wib);
+            }
+            return;
+        }
+    }
     const int64_t gw = int64_t(blockIdx.x) * (blockDim.x >> 5) + wib;
     unsigned char* sm = smem_raw + wib * P.smem_per_warp + sw.id * P.smem_per_frame;
     unsigned char* gs = static_cast<unsigned char*>(P.gscratch) + (gw * FPW + sw.id) * P.gscratch_per_frame;
@@ -1457,7 +1546,7 @@ __global__ void __launch_bounds__(kMaxWarpsPerBlock * 32, PLB_MINBLOCKS) decode_
         const int frame = P.frame_list ? P.frame_list[idx] : int(idx);
         const int cid = P.code_id ? P.code_id[frame] : 0;
         const DevCode C = P.codes[cid];
-        if constexpr (KV > 0) list_frame<R, KV, SW>(P, C, sm, gs, frame, active, sw);
+        if constexpr (KV > 0) list_frame<R, KV, SW, false>(P, C, sm, gs, frame, active, sw);
         else sc_frame<R>(P, C, sm, gs, frame, sw);
     }
 }
@@ -1497,7 +1586,9 @@ __global__ void selftest_kernel(unsigned long long* bad) {
 
 // kernel of a pass: kv = 0 (SC) or 1..6 (list at L = 1..32), frames/warp fpw
 template <typename R>
-void (*kernel_for(int kv, int fpw))(LaunchParams) {
+void (*kernel_for(int kv, int fpw, bool team = false))(LaunchParams) {
+    // team kernels (one frame per block, opt-in) at L = 16 / 32
+    if (team) return kv == 5 ? decode_kernel<R, 5, 32, true> : decode_kernel<R, 6, 32, true>;
     // (8-lane sub-warps measured slower than 16-lane ones at L = 4 and 8)
     if (fpw == 4) return kv == 1 ? decode_kernel<R, 1, 8> : decode_kernel<R, 2, 8>;
     if (fpw == 2) return kv == 3 ? decode_kernel<R, 3, 16> : decode_kernel<R, 4, 16>;
@@ -1521,17 +1612,18 @@ int kv_of(int l, bool list) {
 
 template <typename R>
 cudaError_t launch(const LaunchParams& p, int kv, int grid, cudaStream_t s) {
-    const int smem = p.smem_per_warp * p.wpb;
-    auto kern = kernel_for<R>(kv, p.fpw);
+    const bool team = p.team > 1;
+    const int smem = team ? p.smem_per_frame : p.smem_per_warp * p.wpb;
+    auto kern = kernel_for<R>(kv, p.fpw, team);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    kern<<<grid, p.wpb * 32, smem, s>>>(p);
+    kern<<<grid, (team ? p.team : p.wpb) * 32, smem, s>>>(p);
     return cudaGetLastError();
 }
 
 template <typename R>
-int occupancy(int kv, int fpw, int smem, int wpb) {
-    auto kern = kernel_for<R>(kv, fpw);
+int occupancy(int kv, int fpw, int smem, int wpb, bool team = false) {
+    auto kern = kernel_for<R>(kv, fpw, team);
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
         cudaGetLastError();
         return 0;
@@ -1565,9 +1657,10 @@ cudaError_t launch_list(const LaunchParams& p, int precision, int grid, cudaStre
 int occupancy_sc(int precision, int smem, int wpb) {
     return precision == 0 ? occupancy<float>(0, 1, smem, wpb) : occupancy<int8_t>(0, 1, smem, wpb);
 }
-int occupancy_list(int precision, int l, int fpw, int smem, int wpb) {
+int occupancy_list(int precision, int l, int fpw, int smem, int wpb, bool team) {
     const int kv = kv_of(l, true);
-    return precision == 0 ? occupancy<float>(kv, fpw, smem, wpb) : occupancy<int8_t>(kv, fpw, smem, wpb);
+    return precision == 0 ? occupancy<float>(kv, fpw, smem, wpb, team)
+                          : occupancy<int8_t>(kv, fpw, smem, wpb, team);
 }
 
 cudaError_t kernel_selftest(unsigned long long* mismatches) {

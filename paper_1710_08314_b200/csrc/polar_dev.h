@@ -92,9 +92,12 @@ struct LaunchParams {
     int32_t esc_level;         // value written to esc[] by this pass
     int32_t wpb;               // warps per block (1, 2 or 4)
     int32_t fpw;               // frames per warp (1, 2 or 4; >1 needs one code)
+    int32_t team;              // >1: each block is a team of `team` warps decoding
+                               // one frame (list passes, 32-lane kernels)
 };
 
 constexpr int kMaxWarpsPerBlock = 4; // a block is 1, 2 or 4 independent warps
+constexpr int kMaxTeam = 8;          // ... or a team of up to 8 warps on one frame
 
 // Bytes of shared memory / global scratch one in-flight frame needs.
 int64_t smem_bytes_per_frame(int nmax, int l, int elem_bytes, int seg_smem_max);
@@ -109,7 +112,7 @@ cudaError_t launch_sc(const LaunchParams& p, int precision, int grid, cudaStream
 cudaError_t launch_list(const LaunchParams& p, int precision, int grid, cudaStream_t s);
 // Max resident blocks per SM for a kernel at the given dynamic smem.
 int occupancy_sc(int precision, int smem_bytes, int wpb);
-int occupancy_list(int precision, int l, int fpw, int smem_bytes, int wpb);
+int occupancy_list(int precision, int l, int fpw, int smem_bytes, int wpb, bool team = false);
 // Exhaustive device check of the packed int8 f/g against the scalar kernels.
 cudaError_t kernel_selftest(unsigned long long* mismatches);
 
