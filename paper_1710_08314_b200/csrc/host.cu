@@ -411,22 +411,27 @@ struct pl_handle {
     // device residency
     std::vector<void*> allocs;
     plb::DevCode* d_codes = nullptr;
-    void* d_gscratch = nullptr;
     int64_t gscratch_bytes = 0;
     RungCfg sc_cfg;
     std::vector<RungCfg> rungs; // list rungs in ladder order
-    // per-call control buffers
-    unsigned long long* d_work = nullptr; // one counter per launch
-    int32_t* d_counts = nullptr;          // fail counts per launch
-    int32_t* d_lists[2] = {nullptr, nullptr};
-    int64_t list_cap = 0;
+    // Execution contexts: the scratch and control buffers one decode in
+    // flight needs.  pl_decode uses ex[0]; pl_decode_host alternates ex[0]
+    // and ex[1] on two compute streams, so one chunk's decode can fill the
+    // SMs the previous chunk's tail leaves idle.
+    struct Exec {
+        void* d_gscratch = nullptr;           // global spill of the large depth pools
+        unsigned long long* d_work = nullptr; // one work counter per launch
+        int32_t* d_counts = nullptr;          // fail counts per launch
+        int32_t* d_lists[2] = {nullptr, nullptr};
+        int64_t list_cap = 0;
+    } ex[2];
     int64_t launches = 0;
     // live per-launch timing (pl_profile)
     bool profiling = false;
     std::vector<cudaEvent_t> prof_ev; // 2 per launch slot
     std::vector<int32_t> prof_kind, prof_l;
     // host staging for pl_decode_host
-    cudaStream_t s_compute = nullptr, s_h2d = nullptr, s_d2h = nullptr;
+    cudaStream_t s_comp[2] = {nullptr, nullptr}, s_h2d = nullptr, s_d2h = nullptr;
     int64_t stage_frames = 0;
     void* d_in[2] = {nullptr, nullptr};
     int32_t* d_cid[2] = {nullptr, nullptr};
@@ -564,13 +569,21 @@ RungCfg plan_rung(const pl_handle& h, int l, bool list, bool ladder = false) {
     return pick;
 }
 
-void ensure_lists(pl_handle& h, int64_t nframes) {
-    if (h.list_cap >= nframes && h.d_lists[0]) return;
+void ensure_lists(pl_handle::Exec& x, int64_t nframes) {
+    if (x.list_cap >= nframes && x.d_lists[0]) return;
     for (int i = 0; i < 2; ++i)
-        if (h.d_lists[i]) cudaFree(h.d_lists[i]);
-    h.list_cap = std::max<int64_t>(nframes, 1024);
+        if (x.d_lists[i]) cudaFree(x.d_lists[i]);
+    x.list_cap = std::max<int64_t>(nframes, 1024);
     for (int i = 0; i < 2; ++i)
-        ck(cudaMalloc(&h.d_lists[i], size_t(h.list_cap) * sizeof(int32_t)), "cudaMalloc lists");
+        ck(cudaMalloc(&x.d_lists[i], size_t(x.list_cap) * sizeof(int32_t)), "cudaMalloc lists");
+}
+
+void ensure_exec(pl_handle& h, int e) {
+    pl_handle::Exec& x = h.ex[e];
+    if (x.d_work) return;
+    x.d_gscratch = h.dalloc<void>(size_t(h.gscratch_bytes));
+    x.d_work = h.dalloc<unsigned long long>(16 * sizeof(unsigned long long));
+    x.d_counts = h.dalloc<int32_t>(16 * sizeof(int32_t));
 }
 
 int fail(pl_handle* h, int code, const std::string& msg) {
@@ -581,15 +594,17 @@ int fail(pl_handle* h, int code, const std::string& msg) {
 
 void run_decode(pl_handle& h, const void* llr, const int32_t* code_id, int64_t nframes,
                 uint8_t* payload, uint8_t* codeword, uint8_t* crc_ok, uint8_t* esc,
-                float* metric, cudaStream_t s) {
+                float* metric, cudaStream_t s, int exec = 0) {
     ck(cudaSetDevice(h.device), "cudaSetDevice");
     h.launches = 0;
     if (nframes <= 0) return;
     const int kind = h.dec.kind;
     const bool need_lists = adaptive(kind);
-    if (need_lists) ensure_lists(h, nframes);
-    ck(cudaMemsetAsync(h.d_work, 0, 16 * sizeof(unsigned long long), s), "memset");
-    ck(cudaMemsetAsync(h.d_counts, 0, 16 * sizeof(int32_t), s), "memset");
+    ensure_exec(h, exec);
+    pl_handle::Exec& x = h.ex[exec];
+    if (need_lists) ensure_lists(x, nframes);
+    ck(cudaMemsetAsync(x.d_work, 0, 16 * sizeof(unsigned long long), s), "memset");
+    ck(cudaMemsetAsync(x.d_counts, 0, 16 * sizeof(int32_t), s), "memset");
 
     plb::LaunchParams base{};
     base.codes = h.d_codes;
@@ -604,14 +619,14 @@ void run_decode(pl_handle& h, const void* llr, const int32_t* code_id, int64_t n
     base.crc_ok = crc_ok;
     base.esc = esc;
     base.metric = metric;
-    base.gscratch = h.d_gscratch;
+    base.gscratch = x.d_gscratch;
     base.nmax = h.nmax;
     int slot = 0;
 
     auto run = [&](const RungCfg& rc, bool list, int select, const int32_t* in_list,
                    const int32_t* in_count, int32_t* out_list, int32_t* out_count) {
         plb::LaunchParams p = base;
-        p.work = h.d_work + slot;
+        p.work = x.d_work + slot;
         p.frame_list = in_list;
         p.frame_count = in_count;
         p.fail_list = out_list;
@@ -653,16 +668,16 @@ void run_decode(pl_handle& h, const void* llr, const int32_t* code_id, int64_t n
     case PL_KIND_SSCL: run(h.rungs.back(), true, 0, nullptr, nullptr, nullptr, nullptr); break;
     case PL_KIND_CA_SSCL: run(h.rungs.back(), true, 1, nullptr, nullptr, nullptr, nullptr); break;
     case PL_KIND_PA_SSCL:
-        run(h.sc_cfg, false, 0, nullptr, nullptr, h.d_lists[0], h.d_counts + 0);
-        run(h.rungs.back(), true, 1, h.d_lists[0], h.d_counts + 0, nullptr, nullptr);
+        run(h.sc_cfg, false, 0, nullptr, nullptr, x.d_lists[0], x.d_counts + 0);
+        run(h.rungs.back(), true, 1, x.d_lists[0], x.d_counts + 0, nullptr, nullptr);
         break;
     case PL_KIND_FA_SSCL: {
-        run(h.sc_cfg, false, 0, nullptr, nullptr, h.d_lists[0], h.d_counts + 0);
+        run(h.sc_cfg, false, 0, nullptr, nullptr, x.d_lists[0], x.d_counts + 0);
         int cur = 0;
         for (size_t i = 0; i < h.rungs.size(); ++i) {
             const bool last = i + 1 == h.rungs.size();
-            run(h.rungs[i], true, 1, h.d_lists[cur], h.d_counts + i,
-                last ? nullptr : h.d_lists[cur ^ 1], last ? nullptr : h.d_counts + i + 1);
+            run(h.rungs[i], true, 1, x.d_lists[cur], x.d_counts + i,
+                last ? nullptr : x.d_lists[cur ^ 1], last ? nullptr : x.d_counts + i + 1);
             cur ^= 1;
         }
         break;
@@ -819,9 +834,7 @@ int pl_create(const pl_code* codes, int32_t ncodes, const pl_decoder* dec, int32
         if (h->sc_cfg.grid) acc(h->sc_cfg);
         for (const auto& r : h->rungs) acc(r);
         h->gscratch_bytes = gs;
-        h->d_gscratch = h->dalloc<void>(size_t(gs));
-        h->d_work = h->dalloc<unsigned long long>(16 * sizeof(unsigned long long));
-        h->d_counts = h->dalloc<int32_t>(16 * sizeof(int32_t));
+        ensure_exec(*h, 0);
         *out = h;
         return PL_OK;
     } catch (const ConfigError& e) {
@@ -844,7 +857,9 @@ void pl_destroy(pl_handle* h) {
     cudaSetDevice(h->device);
     for (void* p : h->allocs) cudaFree(p);
     for (int i = 0; i < 2; ++i) {
-        if (h->d_lists[i]) cudaFree(h->d_lists[i]);
+        for (int j = 0; j < 2; ++j)
+            if (h->ex[i].d_lists[j]) cudaFree(h->ex[i].d_lists[j]);
+        if (h->s_comp[i]) cudaStreamDestroy(h->s_comp[i]);
         if (h->d_in[i]) cudaFree(h->d_in[i]);
         if (h->d_cid[i]) cudaFree(h->d_cid[i]);
         if (h->d_out[i]) cudaFree(h->d_out[i]);
@@ -855,7 +870,6 @@ void pl_destroy(pl_handle* h) {
         if (h->ev_d2h[i]) cudaEventDestroy(h->ev_d2h[i]);
     }
     for (cudaEvent_t ev : h->prof_ev) cudaEventDestroy(ev);
-    if (h->s_compute) cudaStreamDestroy(h->s_compute);
     if (h->s_h2d) cudaStreamDestroy(h->s_h2d);
     if (h->s_d2h) cudaStreamDestroy(h->s_d2h);
     delete h;
@@ -922,8 +936,9 @@ int pl_decode_host(pl_handle* h, const void* llr, const int32_t* code_id, int64_
         return fail(h, PL_ERR_ARG, "llr and payload buffers are required");
     try {
         ck(cudaSetDevice(h->device), "cudaSetDevice");
-        if (!h->s_compute) {
-            ck(cudaStreamCreateWithFlags(&h->s_compute, cudaStreamNonBlocking), "stream");
+        if (!h->s_comp[0]) {
+            ck(cudaStreamCreateWithFlags(&h->s_comp[0], cudaStreamNonBlocking), "stream");
+            ck(cudaStreamCreateWithFlags(&h->s_comp[1], cudaStreamNonBlocking), "stream");
             ck(cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking), "stream");
             ck(cudaStreamCreateWithFlags(&h->s_d2h, cudaStreamNonBlocking), "stream");
             for (int i = 0; i < 2; ++i) {
@@ -1000,8 +1015,8 @@ int pl_decode_host(pl_handle* h, const void* llr, const int32_t* code_id, int64_
                                    h->s_h2d),
                    "h2d");
             ck(cudaEventRecord(h->ev_h2d[b], h->s_h2d), "record");
-            ck(cudaStreamWaitEvent(h->s_compute, h->ev_h2d[b], 0), "wait");
-            ck(cudaStreamWaitEvent(h->s_compute, h->ev_d2h[b], 0), "wait");
+            ck(cudaStreamWaitEvent(h->s_comp[b], h->ev_h2d[b], 0), "wait");
+            ck(cudaStreamWaitEvent(h->s_comp[b], h->ev_d2h[b], 0), "wait");
             uint8_t* o = h->d_out[b];
             uint8_t* d_pay = o;
             uint8_t* d_cw = codeword ? o + nf * ob_pay : nullptr;
@@ -1012,9 +1027,9 @@ int pl_decode_host(pl_handle* h, const void* llr, const int32_t* code_id, int64_
             const uintptr_t mis = reinterpret_cast<uintptr_t>(d_met) & 3u;
             if (mis) d_met = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(d_met) + (4 - mis));
             run_decode(*h, h->d_in[b], code_id ? h->d_cid[b] : nullptr, nf, d_pay, d_cw, d_ok, d_esc,
-                       d_met, h->s_compute);
+                       d_met, h->s_comp[b], b);
             launches += h->launches;
-            ck(cudaEventRecord(h->ev_dec[b], h->s_compute), "record");
+            ck(cudaEventRecord(h->ev_dec[b], h->s_comp[b]), "record");
             ck(cudaStreamWaitEvent(h->s_d2h, h->ev_dec[b], 0), "wait");
             auto d2h = [&](void* dst_pinned, uint8_t* dst_stage, const void* srcp, size_t bytes) {
                 void* dst = pin_out ? dst_pinned : static_cast<void*>(dst_stage);
