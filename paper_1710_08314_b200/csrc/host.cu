@@ -424,6 +424,9 @@ struct pl_handle {
         int32_t* d_counts = nullptr;          // fail counts per launch
         int32_t* d_lists[2] = {nullptr, nullptr};
         int64_t list_cap = 0;
+        int32_t* d_hist = nullptr;   // multi-code batches: frames bucketed by code
+        int32_t* d_sorted = nullptr;
+        int64_t sorted_cap = 0;
     } ex[2];
     int64_t launches = 0;
     // live per-launch timing (pl_profile)
@@ -519,12 +522,15 @@ RungCfg plan_rung(const pl_handle& h, int l, bool list, bool ladder = false) {
             if (t.grid > 0) return t;
         }
     }
-    const int fmax = (list && h.codes.size() == 1 && !(ladder && l > 4)) ? plb::frames_per_warp_max(l) : 1;
+    // multi-code batches are bucketed by code before a non-ladder list pass;
+    // ladder rungs get unsorted failure lists
+    const bool multi = h.codes.size() > 1;
+    const int fmax = (list && !(ladder && (l > 4 || multi))) ? plb::frames_per_warp_max(l) : 1;
     std::vector<int> fpws;
     // a list size has kernels for fmax and 1 frames per warp
     if (forced_fpw) {
         const int f = std::atoi(forced_fpw);
-        fpws.push_back(list && h.codes.size() == 1 && plb::frames_per_warp_ok(l, f) ? f : 1);
+        fpws.push_back(fmax > 1 && plb::frames_per_warp_ok(l, f) ? f : 1);
     } else {
         fpws.push_back(fmax);
         if (fmax > 1) fpws.push_back(1);
@@ -665,8 +671,29 @@ void run_decode(pl_handle& h, const void* llr, const int32_t* code_id, int64_t n
     case PL_KIND_SC:
     case PL_KIND_SSC: run(h.sc_cfg, false, 0, nullptr, nullptr, nullptr, nullptr); break;
     case PL_KIND_SCL:
-    case PL_KIND_SSCL: run(h.rungs.back(), true, 0, nullptr, nullptr, nullptr, nullptr); break;
-    case PL_KIND_CA_SSCL: run(h.rungs.back(), true, 1, nullptr, nullptr, nullptr, nullptr); break;
+    case PL_KIND_SSCL:
+    case PL_KIND_CA_SSCL: {
+        const RungCfg& rc = h.rungs.back();
+        const int select = kind == PL_KIND_CA_SSCL ? 1 : 0;
+        if (rc.fpw > 1 && code_id && h.codes.size() > 1) {
+            // sub-warps decode in lockstep only on one code: bucket by code
+            if (x.sorted_cap < nframes) {
+                if (x.d_sorted) cudaFree(x.d_sorted);
+                x.sorted_cap = std::max<int64_t>(nframes, 1024);
+                ck(cudaMalloc(&x.d_sorted, size_t(x.sorted_cap) * sizeof(int32_t)), "cudaMalloc");
+            }
+            if (!x.d_hist)
+                ck(cudaMalloc(&x.d_hist, h.codes.size() * sizeof(int32_t)), "cudaMalloc");
+            ck(plb::bucket_by_code(code_id, nframes, int(h.codes.size()), x.d_hist, x.d_sorted,
+                                   x.d_counts + 15, s),
+               "bucket frames by code");
+            h.launches += 3; // histogram, scan, scatter
+            run(rc, true, select, x.d_sorted, x.d_counts + 15, nullptr, nullptr);
+        } else {
+            run(rc, true, select, nullptr, nullptr, nullptr, nullptr);
+        }
+        break;
+    }
     case PL_KIND_PA_SSCL:
         run(h.sc_cfg, false, 0, nullptr, nullptr, x.d_lists[0], x.d_counts + 0);
         run(h.rungs.back(), true, 1, x.d_lists[0], x.d_counts + 0, nullptr, nullptr);
@@ -859,6 +886,8 @@ void pl_destroy(pl_handle* h) {
     for (int i = 0; i < 2; ++i) {
         for (int j = 0; j < 2; ++j)
             if (h->ex[i].d_lists[j]) cudaFree(h->ex[i].d_lists[j]);
+        if (h->ex[i].d_hist) cudaFree(h->ex[i].d_hist);
+        if (h->ex[i].d_sorted) cudaFree(h->ex[i].d_sorted);
         if (h->s_comp[i]) cudaStreamDestroy(h->s_comp[i]);
         if (h->d_in[i]) cudaFree(h->d_in[i]);
         if (h->d_cid[i]) cudaFree(h->d_cid[i]);

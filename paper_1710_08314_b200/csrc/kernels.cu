@@ -29,6 +29,7 @@
 // order), the halving REP fold, the (value,index) two-smallest order, the
 // stable (metric, emission-index) ranking, the slot assignment and int8
 // normalisation all reproduce list_decoder.hpp / sc_decoder.hpp exactly.
+#include <algorithm>
 #include <cstdint>
 
 #include "polar_dev.h"
@@ -1545,10 +1546,50 @@ decode_kernel(const LaunchParams P) {
         const long long idx = active ? mine : idx0; // idle sub-warps shadow frame idx0
         const int frame = P.frame_list ? P.frame_list[idx] : int(idx);
         const int cid = P.code_id ? P.code_id[frame] : 0;
-        const DevCode C = P.codes[cid];
-        if constexpr (KV > 0) list_frame<R, KV, SW, false>(P, C, sm, gs, frame, active, sw);
-        else sc_frame<R>(P, C, sm, gs, frame, sw);
+        if constexpr (FPW > 1) {
+            // The sub-warps run in lockstep only on one code.  Multi-code
+            // batches arrive bucketed by code (code_bucket), so a warp's
+            // frames straddle two codes only at bucket edges: then the warp
+            // decodes them one after the other, every sub-warp on the same
+            // frame and sub-warp 0 writing.
+            const bool same = __all_sync(FULL, cid == __shfl_sync(FULL, cid, 0));
+            #pragma unroll 1
+            for (int j = 0; j < (same ? 1 : FPW); ++j) {
+                const int fj = same ? frame : __shfl_sync(FULL, frame, j * SW);
+                const int cj = same ? cid : __shfl_sync(FULL, cid, j * SW);
+                const bool aj = same ? active : (__shfl_sync(FULL, int(active), j * SW) && sw.id == 0);
+                list_frame<R, KV, SW, false>(P, P.codes[cj], sm, gs, fj, aj, sw);
+            }
+        } else {
+            const DevCode C = P.codes[cid];
+            if constexpr (KV > 0) list_frame<R, KV, SW, false>(P, C, sm, gs, frame, active, sw);
+            else sc_frame<R>(P, C, sm, gs, frame, sw);
+        }
     }
+}
+
+// Bucket frames by code id (counting sort; order inside a bucket is
+// arbitrary): hist[c] = frames of code c, then exclusive offsets, then each
+// frame takes a slot of its bucket.  Lets multi-code batches use the
+// several-frames-per-warp kernels (lockstep needs one code per warp).
+__global__ void code_hist_kernel(const int32_t* cid, int64_t n, int32_t* hist) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        atomicAdd(hist + cid[i], 1);
+}
+__global__ void code_scan_kernel(int32_t* hist, int ncodes, int32_t* count_out, int64_t n) {
+    if (threadIdx.x == 0) {
+        int32_t acc = 0;
+        for (int c = 0; c < ncodes; ++c) {
+            const int32_t v = hist[c];
+            hist[c] = acc;
+            acc += v;
+        }
+        *count_out = int32_t(n);
+    }
+}
+__global__ void code_scatter_kernel(const int32_t* cid, int64_t n, int32_t* cursor, int32_t* out) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        out[atomicAdd(cursor + cid[i], 1)] = int32_t(i);
 }
 
 // Exhaustive check of the packed int8 f/g against the scalar kernels: every
@@ -1661,6 +1702,17 @@ int occupancy_list(int precision, int l, int fpw, int smem, int wpb, bool team) 
     const int kv = kv_of(l, true);
     return precision == 0 ? occupancy<float>(kv, fpw, smem, wpb, team)
                           : occupancy<int8_t>(kv, fpw, smem, wpb, team);
+}
+
+cudaError_t bucket_by_code(const int32_t* cid, int64_t n, int ncodes, int32_t* hist, int32_t* out,
+                           int32_t* count_out, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(hist, 0, size_t(ncodes) * sizeof(int32_t), s);
+    if (e != cudaSuccess) return e;
+    const int grid = int(std::min<int64_t>((n + 255) / 256, 1184));
+    code_hist_kernel<<<grid, 256, 0, s>>>(cid, n, hist);
+    code_scan_kernel<<<1, 32, 0, s>>>(hist, ncodes, count_out, n);
+    code_scatter_kernel<<<grid, 256, 0, s>>>(cid, n, hist, out);
+    return cudaGetLastError();
 }
 
 cudaError_t kernel_selftest(unsigned long long* mismatches) {

@@ -113,6 +113,10 @@ cudaError_t launch_list(const LaunchParams& p, int precision, int grid, cudaStre
 // Max resident blocks per SM for a kernel at the given dynamic smem.
 int occupancy_sc(int precision, int smem_bytes, int wpb);
 int occupancy_list(int precision, int l, int fpw, int smem_bytes, int wpb, bool team = false);
+// Frame ids [0, n) bucketed by code id into `out` (counting sort, 3 small
+// launches); *count_out = n.  hist: ncodes ints of scratch.
+cudaError_t bucket_by_code(const int32_t* cid, int64_t n, int ncodes, int32_t* hist, int32_t* out,
+                           int32_t* count_out, cudaStream_t s);
 // Exhaustive device check of the packed int8 f/g against the scalar kernels.
 cudaError_t kernel_selftest(unsigned long long* mismatches);
 
