@@ -248,8 +248,9 @@ void emit_scsub(int depth, int m, int lb, const uint8_t* frozen, std::vector<uin
 }
 
 // unabridged recursion of sc_decoder.hpp:99-112
-void emit_sc_subtree(int depth, int m, int base, int frozen_at, std::vector<uint32_t>& s) {
-    if (m <= plb::kScSubMax && m >= 2) {
+void emit_sc_subtree(int depth, int m, int base, int frozen_at, std::vector<uint32_t>& s,
+                     int sub_max) {
+    if (m <= sub_max && m >= 2) {
         uint32_t mask = 0;
         if (frozen_at >= 0) mask = 1u << (frozen_at - base);
         s.push_back(plb::op_pack(plb::OP_SCSUB, depth, ilog2i(m), base));
@@ -262,30 +263,31 @@ void emit_sc_subtree(int depth, int m, int base, int frozen_at, std::vector<uint
     }
     const int lg = ilog2i(m);
     s.push_back(plb::op_pack(plb::OP_F, depth, lg, base));
-    emit_sc_subtree(depth + 1, m / 2, base, frozen_at, s);
+    emit_sc_subtree(depth + 1, m / 2, base, frozen_at, s, sub_max);
     s.push_back(plb::op_pack(plb::OP_G, depth, lg, base));
-    emit_sc_subtree(depth + 1, m / 2, base + m / 2, frozen_at, s);
+    emit_sc_subtree(depth + 1, m / 2, base + m / 2, frozen_at, s, sub_max);
     s.push_back(plb::op_pack(plb::OP_H, depth, lg, base));
 }
 
 // SC schedule: the walk of sc_decoder.hpp:58-94.  Branch subtrees of size
 // <= 32 become one OP_SCSUB (unpruned SC recursion; the R0 / REP shortcuts
 // inside them decide identically, the reference's own SSC == SC property,
-// test_sc.cpp:39-74).
+// test_sc.cpp:39-74).  sub_max = 0: no OP_SCSUB (the frame-per-lane SC
+// kernel walks every op per lane).
 void emit_sc(const std::vector<Node>& t, int ni, std::vector<uint32_t>& s,
-             const uint8_t* frozen) {
+             const uint8_t* frozen, int sub_max = plb::kScSubMax) {
     const Node& nd = t[size_t(ni)];
     const int lg = ilog2i(nd.size);
-    if (nd.kind == NK_BRANCH && nd.size <= plb::kScSubMax) {
+    if (nd.kind == NK_BRANCH && nd.size <= sub_max) {
         emit_scsub(nd.depth, nd.size, nd.lb, frozen, s);
         return;
     }
     switch (nd.kind) {
     case NK_BRANCH:
         s.push_back(plb::op_pack(plb::OP_F, nd.depth, lg, nd.lb));
-        emit_sc(t, nd.left, s, frozen);
+        emit_sc(t, nd.left, s, frozen, sub_max);
         s.push_back(plb::op_pack(plb::OP_G, nd.depth, lg, nd.lb));
-        emit_sc(t, nd.right, s, frozen);
+        emit_sc(t, nd.right, s, frozen, sub_max);
         s.push_back(plb::op_pack(plb::OP_H, nd.depth, lg, nd.lb));
         break;
     case NK_FROZEN:
@@ -299,11 +301,11 @@ void emit_sc(const std::vector<Node>& t, int ni, std::vector<uint32_t>& s,
         s.push_back(plb::op_pack(plb::OP_R1SC, nd.depth, lg, nd.lb));
         const size_t at = s.size();
         s.push_back(0);
-        emit_sc_subtree(nd.depth, nd.size, nd.lb, -1, s);
+        emit_sc_subtree(nd.depth, nd.size, nd.lb, -1, s, sub_max);
         s[at] = uint32_t(s.size() - at - 1);
         break;
     }
-    case NK_SPC: emit_sc_subtree(nd.depth, nd.size, nd.lb, nd.lb, s); break;
+    case NK_SPC: emit_sc_subtree(nd.depth, nd.size, nd.lb, nd.lb, s, sub_max); break;
     case NK_REP: s.push_back(plb::op_pack(plb::OP_REP, nd.depth, lg, nd.lb)); break;
     }
 }
@@ -317,7 +319,7 @@ bool uses_pruning(int k) { return k != PL_KIND_SC && k != PL_KIND_SCL; }
 struct HostCode {
     int n = 0, k = 0, stages = 0, psize = 0, width = 0;
     std::vector<uint8_t> frozen;
-    std::vector<uint32_t> sched_list, sched_sc;
+    std::vector<uint32_t> sched_list, sched_sc, sched_lane;
     std::vector<uint16_t> info_pos;
     std::vector<uint64_t> crc_tab;
     uint64_t crc_c0 = 0;
@@ -355,6 +357,7 @@ HostCode make_host_code(const pl_code& c, const pl_decoder& dec) {
     build_tree(tree, h.frozen.data(), 0, c.n, 0, pc);
     emit_list(tree, 0, h.sched_list, dec.precision == PL_I8 ? plb::kFuseMaxI8 : plb::kFuseMaxF32);
     emit_sc(tree, 0, h.sched_sc, h.frozen.data());
+    emit_sc(tree, 0, h.sched_lane, h.frozen.data(), 0);
 
     if (crc) {
         // affine map: crc(m) = c0 ^ XOR_i m_i col_i over the K message bits;
@@ -392,6 +395,7 @@ struct RungCfg {
     int wpb = plb::kMaxWarpsPerBlock;
     int fpw = 1; // frames per warp (sub-warp decoding, single-code batches)
     int team = 1; // >1: blocks of `team` warps, one frame each
+    bool lanes = false; // frame-per-lane SC kernel (smem / gscratch figures per 32-frame warp)
     int64_t gscratch_total() const {
         return int64_t(grid) * (team > 1 ? 1 : wpb * fpw) * gscratch_per_frame;
     }
@@ -501,6 +505,41 @@ RungCfg plan_team(const pl_handle& h, int l, int team, const std::vector<int>& c
             best_nb = nb;
         }
     }
+    return best;
+}
+
+// The frame-per-lane SC pass: 32 frames per warp; the most shared-memory
+// resident layout that keeps PLB_LANE_WARPS warps per SM.
+RungCfg plan_lanes(const pl_handle& h) {
+    const int target = std::max(1, env_int("PLB_LANE_WARPS", 16));
+    const int forced = env_int("PLB_SEGMAX", 0);
+    std::vector<int> cands;
+    if (forced) cands.push_back(forced);
+    else
+        for (int sg = h.nmax; sg >= 1; sg >>= 1) cands.push_back(sg);
+    RungCfg best;
+    int best_warps = 0;
+    for (int wpb = plb::kMaxWarpsPerBlock; wpb >= 1; wpb >>= 1) {
+        for (int seg : cands) {
+            RungCfg c;
+            c.l = 1;
+            c.lanes = true;
+            c.seg_max = seg;
+            c.wpb = wpb;
+            c.smem_per_frame = int(plb::lane_smem_bytes_per_warp(h.nmax, h.esz, seg));
+            c.gscratch_per_frame = plb::lane_gscratch_bytes_per_warp(h.nmax, h.esz, seg);
+            const int nb = plb::occupancy_sc_lanes(h.dec.precision, c.smem_per_frame * wpb, wpb);
+            if (nb <= 0) continue;
+            c.grid = nb * h.sms;
+            if (nb * wpb > best_warps) {
+                best = c;
+                best_warps = nb * wpb;
+            }
+            if (nb * wpb >= target) break;
+        }
+        if (best_warps >= target) break;
+    }
+    if (best.grid <= 0) throw ConfigError("no launch configuration fits the SC pass on the device");
     return best;
 }
 
@@ -659,47 +698,58 @@ void run_decode(pl_handle& h, const void* llr, const int32_t* code_id, int64_t n
             h.prof_l[size_t(slot)] = rc.l;
             ck(cudaEventRecord(h.prof_ev[size_t(2 * slot)], s), "record");
         }
-        cudaError_t e = list ? plb::launch_list(p, h.dec.precision, rc.grid, s)
-                             : plb::launch_sc(p, h.dec.precision, rc.grid, s);
+        cudaError_t e = list       ? plb::launch_list(p, h.dec.precision, rc.grid, s)
+                        : rc.lanes ? plb::launch_sc_lanes(p, h.dec.precision, rc.grid, s)
+                                   : plb::launch_sc(p, h.dec.precision, rc.grid, s);
         ck(e, list ? "list kernel launch" : "sc kernel launch");
         if (h.profiling) ck(cudaEventRecord(h.prof_ev[size_t(2 * slot + 1)], s), "record");
         ++slot;
         ++h.launches;
     };
 
+    // Kernels that decode several frames in lockstep (sub-warps, the
+    // frame-per-lane SC kernel) need one code per warp: multi-code batches
+    // are bucketed by code first (the frame list of that pass).
+    const int32_t* blist = nullptr;
+    const int32_t* bcount = nullptr;
+    auto bucket = [&](const RungCfg& rc) {
+        blist = nullptr;
+        bcount = nullptr;
+        if (!(code_id && h.codes.size() > 1 && (rc.fpw > 1 || rc.lanes))) return;
+        if (x.sorted_cap < nframes) {
+            if (x.d_sorted) cudaFree(x.d_sorted);
+            x.sorted_cap = std::max<int64_t>(nframes, 1024);
+            ck(cudaMalloc(&x.d_sorted, size_t(x.sorted_cap) * sizeof(int32_t)), "cudaMalloc");
+        }
+        if (!x.d_hist) ck(cudaMalloc(&x.d_hist, h.codes.size() * sizeof(int32_t)), "cudaMalloc");
+        ck(plb::bucket_by_code(code_id, nframes, int(h.codes.size()), x.d_hist, x.d_sorted,
+                               x.d_counts + 15, s),
+           "bucket frames by code");
+        h.launches += 3; // histogram, scan, scatter
+        blist = x.d_sorted;
+        bcount = x.d_counts + 15;
+    };
+
     switch (kind) {
     case PL_KIND_SC:
-    case PL_KIND_SSC: run(h.sc_cfg, false, 0, nullptr, nullptr, nullptr, nullptr); break;
+    case PL_KIND_SSC:
+        bucket(h.sc_cfg);
+        run(h.sc_cfg, false, 0, blist, bcount, nullptr, nullptr);
+        break;
     case PL_KIND_SCL:
     case PL_KIND_SSCL:
-    case PL_KIND_CA_SSCL: {
-        const RungCfg& rc = h.rungs.back();
-        const int select = kind == PL_KIND_CA_SSCL ? 1 : 0;
-        if (rc.fpw > 1 && code_id && h.codes.size() > 1) {
-            // sub-warps decode in lockstep only on one code: bucket by code
-            if (x.sorted_cap < nframes) {
-                if (x.d_sorted) cudaFree(x.d_sorted);
-                x.sorted_cap = std::max<int64_t>(nframes, 1024);
-                ck(cudaMalloc(&x.d_sorted, size_t(x.sorted_cap) * sizeof(int32_t)), "cudaMalloc");
-            }
-            if (!x.d_hist)
-                ck(cudaMalloc(&x.d_hist, h.codes.size() * sizeof(int32_t)), "cudaMalloc");
-            ck(plb::bucket_by_code(code_id, nframes, int(h.codes.size()), x.d_hist, x.d_sorted,
-                                   x.d_counts + 15, s),
-               "bucket frames by code");
-            h.launches += 3; // histogram, scan, scatter
-            run(rc, true, select, x.d_sorted, x.d_counts + 15, nullptr, nullptr);
-        } else {
-            run(rc, true, select, nullptr, nullptr, nullptr, nullptr);
-        }
+    case PL_KIND_CA_SSCL:
+        bucket(h.rungs.back());
+        run(h.rungs.back(), true, kind == PL_KIND_CA_SSCL ? 1 : 0, blist, bcount, nullptr, nullptr);
         break;
-    }
     case PL_KIND_PA_SSCL:
-        run(h.sc_cfg, false, 0, nullptr, nullptr, x.d_lists[0], x.d_counts + 0);
+        bucket(h.sc_cfg);
+        run(h.sc_cfg, false, 0, blist, bcount, x.d_lists[0], x.d_counts + 0);
         run(h.rungs.back(), true, 1, x.d_lists[0], x.d_counts + 0, nullptr, nullptr);
         break;
     case PL_KIND_FA_SSCL: {
-        run(h.sc_cfg, false, 0, nullptr, nullptr, x.d_lists[0], x.d_counts + 0);
+        bucket(h.sc_cfg);
+        run(h.sc_cfg, false, 0, blist, bcount, x.d_lists[0], x.d_counts + 0);
         int cur = 0;
         for (size_t i = 0; i < h.rungs.size(); ++i) {
             const bool last = i + 1 == h.rungs.size();
@@ -838,6 +888,8 @@ int pl_create(const pl_code* codes, int32_t ncodes, const pl_decoder* dec, int32
             };
             d.sched_list = static_cast<const uint32_t*>(up(c.sched_list.data(), c.sched_list.size() * 4));
             d.sched_sc = static_cast<const uint32_t*>(up(c.sched_sc.data(), c.sched_sc.size() * 4));
+            d.sched_lane = static_cast<const uint32_t*>(up(c.sched_lane.data(), c.sched_lane.size() * 4));
+            d.nops_lane = int(c.sched_lane.size());
             d.nops_list = int(c.sched_list.size());
             d.nops_sc = int(c.sched_sc.size());
             d.info_pos = static_cast<const uint16_t*>(up(c.info_pos.data(), c.info_pos.size() * 2));
@@ -849,7 +901,8 @@ int pl_create(const pl_code* codes, int32_t ncodes, const pl_decoder* dec, int32
         ck(cudaMemcpy(h->d_codes, dc.data(), dc.size() * sizeof(plb::DevCode), cudaMemcpyHostToDevice),
            "upload codes");
         // ---- launch plans for every pass this kind can run
-        if (!uses_list(kind) || adaptive(kind)) h->sc_cfg = plan_rung(*h, 1, false);
+        if (!uses_list(kind) || adaptive(kind))
+            h->sc_cfg = env_int("PLB_SC_LANES", 1) ? plan_lanes(*h) : plan_rung(*h, 1, false);
         if (kind == PL_KIND_FA_SSCL)
             for (int ll = 2; ll <= l; ll *= 2) h->rungs.push_back(plan_rung(*h, ll, true, true));
         else if (uses_list(kind))

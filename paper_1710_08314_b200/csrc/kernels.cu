@@ -429,15 +429,12 @@ struct Ctx {
 // One body for F and G (is_g is uniform), two vector widths per type (G = 1
 // for narrow nodes, G = 16 bytes otherwise): the decode loop's hot code must
 // stay inside the instruction cache.
+// o = f(a, b) or g(a, b, bits) on G values (bits: partial sum i in bit i)
 template <typename R, int G>
-__device__ __forceinline__ void fg_item(const R* in, R* out, const uint32_t* prow, int h,
-                                        int c, int lb, bool is_g) {
+__device__ __forceinline__ Vec<R, G> fg_compute(const Vec<R, G>& a, const Vec<R, G>& b, uint32_t bits,
+                                                bool is_g) {
     using A = Arith<R>;
-    const Vec<R, G> a = vld<R, G>(in + c * G);
-    const Vec<R, G> b = vld<R, G>(in + h + c * G);
     Vec<R, G> o;
-    const int pos = lb + c * G;
-    const uint32_t bits = is_g ? prow[pos >> 5] >> (pos & 31) : 0u;
     if constexpr (A::kFixed && G >= 4) {
         constexpr int W = G / 4;
         const uint32_t* aw = reinterpret_cast<const uint32_t*>(&a.raw);
@@ -457,7 +454,17 @@ __device__ __forceinline__ void fg_item(const R* in, R* out, const uint32_t* pro
 #pragma unroll
         for (int i = 0; i < G; ++i) o.v[i] = A::f(a.v[i], b.v[i]);
     }
-    vst<R, G>(out + c * G, o);
+    return o;
+}
+
+template <typename R, int G>
+__device__ __forceinline__ void fg_item(const R* in, R* out, const uint32_t* prow, int h,
+                                        int c, int lb, bool is_g) {
+    const Vec<R, G> a = vld<R, G>(in + c * G);
+    const Vec<R, G> b = vld<R, G>(in + h + c * G);
+    const int pos = lb + c * G;
+    const uint32_t bits = is_g ? prow[pos >> 5] >> (pos & 31) : 0u;
+    vst<R, G>(out + c * G, fg_compute<R, G>(a, b, bits, is_g));
 }
 
 template <typename R, int SW, int G>
@@ -1592,6 +1599,380 @@ __global__ void code_scatter_kernel(const int32_t* cid, int64_t n, int32_t* curs
         out[atomicAdd(cursor + cid[i], 1)] = int32_t(i);
 }
 
+// ==== frame-per-lane SC kernel (SC / SSC and the first pass of PA / FA) ====
+// A warp decodes 32 frames, one per lane, in lockstep over the SC schedule
+// of their (common) code: the op sequence of SC decoding is data-independent
+// except for the rate-1 shortcut, which the warp takes only when no lane has
+// a zero input (the expanded recursion is exact for every lane, so running
+// it for all is correct).  One warp instruction then advances 32 frames, and
+// the small nodes that cost the warp-per-frame kernel a whole warp step per
+// value are plain per-lane loops.  Per-warp storage, lane-interleaved so
+// every access is conflict-free / coalesced:
+//   * partial sums: word w of lane l at ps[w * 32 + l] (shared memory);
+//   * depth-d LLR segment (n >> d values per frame): chunks of
+//     V = min(VE, n >> d) values, chunk c of lane l at ((c * 32) + l) * V
+//     (VE = 16 bytes of values); small segments in shared memory, large ones
+//     in the warp's global scratch;
+//   * depth 0 is the channel, read in place (frame-major).
+struct LaneQ {
+    int32_t rw, psum_off, smem_total, gmem_total, pool_off, pool_in_smem;
+};
+__host__ __device__ inline LaneQ lane_layout(int n, int esz, int segmax, int want_d) {
+    LaneQ q{};
+    int off = 16 * 8; // pool pointer table
+    q.rw = n >= 32 ? n / 32 : 1;
+    q.psum_off = off;
+    off += 4 * q.rw * 32;
+    int goff = 0;
+    const int stages = ilog2(n);
+    #pragma unroll 1
+    for (int d = 1; d <= stages; ++d) {
+        const int bytes = align16((n >> d) * 32 * esz);
+        if ((n >> d) <= segmax) {
+            if (d == want_d) {
+                q.pool_off = off;
+                q.pool_in_smem = 1;
+            }
+            off += bytes;
+        } else {
+            if (d == want_d) {
+                q.pool_off = goff;
+                q.pool_in_smem = 0;
+            }
+            goff += bytes;
+        }
+    }
+    q.smem_total = off;
+    q.gmem_total = goff;
+    return q;
+}
+
+template <typename R>
+struct LaneCtx {
+    static constexpr int VE = 16 / int(sizeof(R));
+    int lane, n;
+    const R* chan;      // this lane's frame
+    uint32_t* ps;       // this lane's psum words, stride 32
+    const uint64_t* pt; // pool pointer table
+    __device__ __forceinline__ R* pool(int d) const { return reinterpret_cast<R*>(pt[d]); }
+    // first value of chunk c at depth d (chunk = min(VE, n >> d) values)
+    __device__ __forceinline__ const R* chunk(int d, int c) const {
+        const int v = min(VE, n >> d);
+        return d == 0 ? chan + c * v : pool(d) + (c * 32 + lane) * v;
+    }
+    __device__ __forceinline__ uint32_t& word(int w) const { return ps[w * 32]; }
+    __device__ void fill(int lb, int m, int bit) const {
+        if (m >= 32) {
+            #pragma unroll 1
+            for (int w = 0; w < (m >> 5); ++w) word((lb >> 5) + w) = bit ? FULL : 0u;
+        } else {
+            const uint32_t mk = ((1u << m) - 1u) << (lb & 31);
+            uint32_t& x = word(lb >> 5);
+            x = bit ? (x | mk) : (x & ~mk);
+        }
+    }
+};
+
+// sign bits of the G values of a vector (value i -> bit i)
+template <typename R, int G>
+__device__ __forceinline__ uint32_t vec_signs(const Vec<R, G>& x) {
+    uint32_t s = 0;
+    if constexpr (sizeof(R) == 1 && G >= 4) {
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(&x.raw);
+#pragma unroll
+        for (int k = 0; k < G / 4; ++k)
+            s |= ((((w[k] >> 7) & 0x01010101u) * 0x01020408u) >> 24) << (4 * k);
+    } else {
+#pragma unroll
+        for (int i = 0; i < G; ++i) s |= uint32_t(Arith<R>::val(x.v[i]) < typename Arith<R>::M(0)) << i;
+    }
+    return s;
+}
+template <typename R, int G>
+__device__ __forceinline__ bool vec_has_zero(const Vec<R, G>& x) {
+    bool z = false;
+#pragma unroll
+    for (int i = 0; i < G; ++i) z |= Arith<R>::val(x.v[i]) == typename Arith<R>::M(0);
+    return z;
+}
+
+// U chunks per iteration: 2U loads in flight per lane (the pools of the
+// upper depths live in global memory), U * VE <= 32 partial-sum bits
+template <typename R, int U>
+__device__ __forceinline__ void lane_fg_chunks(const LaneCtx<R>& c, int d, int nc, int lb, bool is_g,
+                                               R* out) {
+    constexpr int VE = LaneCtx<R>::VE;
+    #pragma unroll 1
+    for (int k = 0; k < nc; k += U) {
+        Vec<R, VE> a[U], b[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            a[u] = vld<R, VE>(c.chunk(d, k + u));
+            b[u] = vld<R, VE>(c.chunk(d, k + u + nc));
+        }
+        const int pos = lb + k * VE;
+        const uint32_t bits = is_g ? c.word(pos >> 5) >> (pos & 31) : 0u;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            vst<R, VE>(out + ((k + u) * 32 + c.lane) * VE, fg_compute<R, VE>(a[u], b[u], bits >> (u * VE), is_g));
+    }
+}
+
+template <typename R>
+__device__ void lane_fg(const LaneCtx<R>& c, int d, int m, int lb, bool is_g) {
+    using A = Arith<R>;
+    constexpr int VE = LaneCtx<R>::VE;
+    constexpr int U = 32 / VE < 4 ? 32 / VE : 4;
+    const int h = m >> 1;
+    R* const out = c.pool(d + 1);
+    if (h >= VE) {
+        const int nc = h / VE;
+        if (nc >= U) lane_fg_chunks<R, U>(c, d, nc, lb, is_g, out);
+        else lane_fg_chunks<R, 1>(c, d, nc, lb, is_g, out);
+    } else {
+        // the parent's m <= VE values are one contiguous chunk
+        const R* p = c.chunk(d, 0);
+        R* q = out + c.lane * h;
+        const uint32_t bits = is_g ? c.word(lb >> 5) >> (lb & 31) : 0u;
+        #pragma unroll 1
+        for (int j = 0; j < h; ++j) q[j] = is_g ? A::g(p[j], p[h + j], (bits >> j) & 1u) : A::f(p[j], p[h + j]);
+    }
+}
+
+template <typename R>
+__device__ void lane_h(const LaneCtx<R>& c, int m, int lb) {
+    const int h = m >> 1;
+    if (h >= 32) {
+        #pragma unroll 1
+        for (int w = 0; w < (h >> 5); ++w) c.word((lb >> 5) + w) ^= c.word(((lb + h) >> 5) + w);
+    } else {
+        uint32_t& x = c.word(lb >> 5);
+        const int s = lb & 31;
+        const uint32_t mk = (1u << h) - 1u;
+        x ^= ((x >> (s + h)) & mk) << s;
+    }
+}
+
+// repetition node (sc_decoder.hpp:114-125): halving fold, bit = fold < 0.
+// Chunk pairs are added elementwise first (into the dead depth-(d+1)
+// segment), then the last chunk is folded in registers: the same additions
+// in the same order as the reference's halving loop.
+template <typename R>
+__device__ int lane_rep(const LaneCtx<R>& c, int d, int m) {
+    using A = Arith<R>;
+    using M = typename A::M;
+    constexpr int VE = LaneCtx<R>::VE;
+    Vec<R, VE> x;
+    int len = m;
+    if (m > VE) {
+        R* S = c.pool(d + 1) + c.lane * VE; // chunk k at S + k * 32 * VE
+        int nc = m / VE;
+        const R* src0 = nullptr;
+        #pragma unroll 1
+        for (int first = 1; nc > 1; first = 0) {
+            const int hc = nc >> 1;
+            #pragma unroll 1
+            for (int k = 0; k < hc; ++k) {
+                const Vec<R, VE> a = first ? vld<R, VE>(c.chunk(d, k)) : vld<R, VE>(S + k * 32 * VE);
+                const Vec<R, VE> b = first ? vld<R, VE>(c.chunk(d, k + hc)) : vld<R, VE>(S + (k + hc) * 32 * VE);
+                vst<R, VE>(S + k * 32 * VE, fg_compute<R, VE>(a, b, 0u, true)); // g with u = 0: sat(a + b)
+            }
+            nc = hc;
+        }
+        (void)src0;
+        x = vld<R, VE>(S);
+        len = VE;
+    } else {
+        const R* p = c.chunk(d, 0);
+#pragma unroll
+        for (int i = 0; i < VE; ++i) x.v[i] = i < m ? p[i] : R(0);
+    }
+    M v[VE];
+#pragma unroll
+    for (int i = 0; i < VE; ++i) v[i] = A::val(x.v[i]);
+#pragma unroll
+    for (int s = VE; s > 1; s >>= 1)
+        if (s <= len)
+#pragma unroll
+            for (int i = 0; i < s / 2; ++i) v[i] = A::sat(v[i], v[i + s / 2]);
+    return v[0] < M(0);
+}
+
+// rate-1 shortcut: true when this lane's m values hold no zero
+template <typename R>
+__device__ bool lane_r1_nozero(const LaneCtx<R>& c, int d, int m) {
+    constexpr int VE = LaneCtx<R>::VE;
+    bool zero = false;
+    if (m >= VE) {
+        #pragma unroll 1
+        for (int k = 0; k < m / VE; ++k) zero |= vec_has_zero<R, VE>(vld<R, VE>(c.chunk(d, k)));
+    } else {
+        const R* p = c.chunk(d, 0);
+        #pragma unroll 1
+        for (int i = 0; i < m; ++i) zero |= Arith<R>::val(p[i]) == typename Arith<R>::M(0);
+    }
+    return !zero;
+}
+template <typename R>
+__device__ void lane_r1_hard(const LaneCtx<R>& c, int d, int m, int lb) {
+    using A = Arith<R>;
+    constexpr int VE = LaneCtx<R>::VE;
+    if (m >= VE) {
+        uint32_t acc = 0;
+        #pragma unroll 1
+        for (int k = 0; k < m / VE; ++k) {
+            const int pos = k * VE; // bit of the node
+            acc |= vec_signs<R, VE>(vld<R, VE>(c.chunk(d, k))) << (pos & 31);
+            if (((pos + VE) & 31) == 0 || pos + VE >= m) {
+                if (m >= 32) {
+                    c.word((lb + (pos & ~31)) >> 5) = acc;
+                } else {
+                    const uint32_t mk = ((1u << m) - 1u) << (lb & 31);
+                    uint32_t& x = c.word(lb >> 5);
+                    x = (x & ~mk) | ((acc << (lb & 31)) & mk);
+                }
+                acc = 0;
+            }
+        }
+    } else {
+        const R* p = c.chunk(d, 0);
+        uint32_t acc = 0;
+        #pragma unroll 1
+        for (int i = 0; i < m; ++i) acc |= uint32_t(A::val(p[i]) < typename A::M(0)) << i;
+        const uint32_t mk = ((1u << m) - 1u) << (lb & 31);
+        uint32_t& x = c.word(lb >> 5);
+        x = (x & ~mk) | ((acc << (lb & 31)) & mk);
+    }
+}
+
+template <typename R>
+__device__ void lane_frame(const LaunchParams& P, const DevCode& C, unsigned char* sm,
+                           unsigned char* gs, int frame, bool active, int lane) {
+    using A = Arith<R>;
+    using M = typename A::M;
+    LaneCtx<R> c;
+    c.lane = lane;
+    c.n = C.n;
+    c.chan = static_cast<const R*>(P.llr) + int64_t(frame) * P.llr_stride;
+    const LaneQ q0 = lane_layout(C.n, int(sizeof(R)), P.seg_smem_max, 0);
+    c.ps = reinterpret_cast<uint32_t*>(sm + q0.psum_off) + lane;
+    uint64_t* pt = reinterpret_cast<uint64_t*>(sm);
+    c.pt = pt;
+    __syncwarp();
+    if (lane >= 1 && lane <= C.stages) {
+        const LaneQ q = lane_layout(C.n, int(sizeof(R)), P.seg_smem_max, lane);
+        pt[lane] = reinterpret_cast<uint64_t>((q.pool_in_smem ? sm : gs) + q.pool_off);
+    }
+    __syncwarp();
+    const uint32_t* sched = C.sched_lane;
+    const int nops = C.nops_lane;
+    #pragma unroll 1
+    for (int oi = 0; oi < nops; ++oi) {
+        const uint32_t op = __ldg(sched + oi);
+        const int code = op_code(op), d = op_depth(op), m = 1 << op_logm(op), lb = op_lb(op);
+        switch (code) {
+        case OP_F:
+        case OP_G: lane_fg(c, d, m, lb, code == OP_G); break;
+        case OP_H: lane_h(c, m, lb); break;
+        case OP_FROZEN: c.fill(lb, m, 0); break;
+        case OP_INFO: c.fill(lb, 1, A::val(*c.chunk(d, 0)) < M(0)); break;
+        case OP_REP: c.fill(lb, m, lane_rep(c, d, m)); break;
+        case OP_R1SC: {
+            const int skip = int(__ldg(sched + ++oi));
+            if (__all_sync(FULL, lane_r1_nozero(c, d, m))) {
+                lane_r1_hard(c, d, m, lb);
+                oi += skip;
+            } // else: every lane runs the expanded recursion that follows
+            break;
+        }
+        default: break;
+        }
+    }
+    // finish: CRC syndrome, payload, codeword, status (per lane)
+    int crc_ok = 0;
+    if (C.crc_width > 0) {
+        uint64_t syn = C.crc_c0;
+        const int nbytes = (C.n + 7) >> 3;
+        #pragma unroll 1
+        for (int j = 0; j < nbytes; ++j) {
+            const uint32_t byte = (c.word(j >> 2) >> ((j & 3) * 8)) & 0xffu;
+            syn ^= __ldg(C.crc_tab + (size_t(j) << 8) + byte);
+        }
+        crc_ok = syn == 0;
+    }
+    if (active) {
+        uint8_t* pay = P.payload + int64_t(frame) * P.payload_stride;
+        const int pb = (C.psize + 7) >> 3;
+        #pragma unroll 1
+        for (int qb = 0; qb < pb; ++qb) {
+            uint32_t byte = 0;
+            #pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                const int j = 8 * qb + b;
+                if (j < C.psize) {
+                    const int pos = __ldg(C.info_pos + j);
+                    byte |= ((c.word(pos >> 5) >> (pos & 31)) & 1u) << (7 - b);
+                }
+            }
+            pay[qb] = uint8_t(byte);
+        }
+        if (P.codeword) {
+            uint8_t* cw = P.codeword + int64_t(frame) * P.codeword_stride;
+            const int cb = (C.n + 7) >> 3;
+            #pragma unroll 1
+            for (int qb = 0; qb < cb; ++qb) {
+                const uint32_t bits = (c.word(qb >> 2) >> ((qb & 3) * 8)) & 0xffu;
+                const uint32_t byte = __brev(bits) >> 24;
+                cw[qb] = uint8_t(C.n >= 8 ? byte : (byte & (0xffu << (8 - C.n))));
+            }
+        }
+        if (P.crc_ok) P.crc_ok[frame] = uint8_t(crc_ok);
+        if (P.esc) P.esc[frame] = 1;
+        if (P.metric) P.metric[frame] = 0.0f; // DecodeResult default (decode_result.hpp:12)
+    }
+    // failed frames -> the next rung's list (warp-aggregated append)
+    if (P.fail_list && C.crc_width > 0) {
+        const bool f = active && !crc_ok;
+        const unsigned fm = __ballot_sync(FULL, f);
+        int base = 0;
+        if (lane == 0 && fm) base = atomicAdd(P.fail_count, __popc(fm));
+        base = __shfl_sync(FULL, base, 0);
+        if (f) P.fail_list[base + __popc(fm & lanemask_lt())] = frame;
+    }
+    __syncwarp();
+}
+
+template <typename R>
+__global__ void __launch_bounds__(128, 8) sc_lanes_kernel(const LaunchParams P) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    unsigned char* sm = smem_raw + wib * P.smem_per_warp;
+    const int64_t gw = int64_t(blockIdx.x) * (blockDim.x >> 5) + wib;
+    // (for this kernel gscratch_per_frame is the scratch of one 32-frame warp)
+    unsigned char* gs = static_cast<unsigned char*>(P.gscratch) + gw * P.gscratch_per_frame;
+    const long long count = P.frame_list ? (long long)(*P.frame_count) : (long long)P.nframes;
+    for (;;) {
+        unsigned long long i0 = 0;
+        if (lane == 0) i0 = atomicAdd(P.work, 32ull);
+        const long long idx0 = (long long)__shfl_sync(FULL, i0, 0);
+        if (idx0 >= count) break;
+        const long long mine = idx0 + lane;
+        const bool active = mine < count;
+        const long long idx = active ? mine : idx0; // idle lanes shadow frame idx0
+        const int frame = P.frame_list ? P.frame_list[idx] : int(idx);
+        const int cid = P.code_id ? P.code_id[frame] : 0;
+        // lockstep needs one code: one pass per distinct code of the warp
+        // (multi-code batches arrive bucketed by code, so usually one)
+        unsigned pending = FULL;
+        while (pending) {
+            const int cc = __shfl_sync(FULL, cid, __ffs(pending) - 1);
+            const unsigned grp = __ballot_sync(FULL, cid == cc) & pending;
+            pending &= ~grp;
+            lane_frame<R>(P, P.codes[cc], sm, gs, frame, active && ((grp >> lane) & 1u), lane);
+        }
+    }
+}
+
 // Exhaustive check of the packed int8 f/g against the scalar kernels: every
 // (a, b) pair in [-127, 127]^2, in every byte position, next to
 // pseudo-random neighbours, under all 16 partial-sum patterns.
@@ -1697,6 +2078,34 @@ cudaError_t launch_list(const LaunchParams& p, int precision, int grid, cudaStre
 }
 int occupancy_sc(int precision, int smem, int wpb) {
     return precision == 0 ? occupancy<float>(0, 1, smem, wpb) : occupancy<int8_t>(0, 1, smem, wpb);
+}
+
+int64_t lane_smem_bytes_per_warp(int nmax, int elem_bytes, int seg_smem_max) {
+    return lane_layout(nmax, elem_bytes, seg_smem_max, 0).smem_total;
+}
+int64_t lane_gscratch_bytes_per_warp(int nmax, int elem_bytes, int seg_smem_max) {
+    return lane_layout(nmax, elem_bytes, seg_smem_max, 0).gmem_total;
+}
+cudaError_t launch_sc_lanes(const LaunchParams& p, int precision, int grid, cudaStream_t s) {
+    const int smem = p.smem_per_warp * p.wpb;
+    void (*kern)(LaunchParams) = precision == 0 ? sc_lanes_kernel<float> : sc_lanes_kernel<int8_t>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, p.wpb * 32, smem, s>>>(p);
+    return cudaGetLastError();
+}
+int occupancy_sc_lanes(int precision, int smem, int wpb) {
+    void (*kern)(LaunchParams) = precision == 0 ? sc_lanes_kernel<float> : sc_lanes_kernel<int8_t>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, wpb * 32, smem) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return nb;
 }
 int occupancy_list(int precision, int l, int fpw, int smem, int wpb, bool team) {
     const int kv = kv_of(l, true);

@@ -54,7 +54,8 @@ struct DevCode {
     int32_t n, stages, k, psize, crc_width, pad;
     const uint32_t* sched_list; // list-decoder schedule (pruned or full tree)
     const uint32_t* sched_sc;   // SC-rung schedule (R1/SPC expanded)
-    int32_t nops_list, nops_sc;
+    const uint32_t* sched_lane; // the same without OP_SCSUB (frame-per-lane SC kernel)
+    int32_t nops_list, nops_sc, nops_lane, pad2;
     const uint16_t* info_pos;   // psize open positions, ascending
     // CRC as an affine map over the decided codeword:
     // syndrome = crc_c0 ^ XOR_j crc_tab[j][byte_j(codeword)], zero <=> pass.
@@ -113,6 +114,13 @@ cudaError_t launch_list(const LaunchParams& p, int precision, int grid, cudaStre
 // Max resident blocks per SM for a kernel at the given dynamic smem.
 int occupancy_sc(int precision, int smem_bytes, int wpb);
 int occupancy_list(int precision, int l, int fpw, int smem_bytes, int wpb, bool team = false);
+// Frame-per-lane SC kernel (32 frames per warp; SC / SSC and the first pass
+// of PA / FA).  For it LaunchParams.smem_per_warp / gscratch_per_frame are
+// the shared / global bytes of one 32-frame warp.
+int64_t lane_smem_bytes_per_warp(int nmax, int elem_bytes, int seg_smem_max);
+int64_t lane_gscratch_bytes_per_warp(int nmax, int elem_bytes, int seg_smem_max);
+cudaError_t launch_sc_lanes(const LaunchParams& p, int precision, int grid, cudaStream_t s);
+int occupancy_sc_lanes(int precision, int smem_bytes, int wpb);
 // Frame ids [0, n) bucketed by code id into `out` (counting sort, 3 small
 // launches); *count_out = n.  hist: ncodes ints of scratch.
 cudaError_t bucket_by_code(const int32_t* cid, int64_t n, int ncodes, int32_t* hist, int32_t* out,
