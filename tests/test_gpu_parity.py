@@ -239,18 +239,23 @@ def test_cfg3_mixed_codes_one_batch(P, gpu, oracle_lib):
     wl = MixedWorkload()
     codes, cid, info, ks, llr = make_batch(wl, 0, 1024)
     assert len(codes) == 31 and len(set(cid.tolist())) == 31
-    dec = P.FrameDecoder(codes, "ca_sscl", 8, "f32", P.PruningConfig())
-    o = dec.decode_batch(gpu.from_numpy(llr).cuda(), code_id=gpu.from_numpy(cid).cuda(), codeword=True)
-    gpu.cuda.synchronize()
-    got = {k: v.cpu().numpy() for k, v in o.items() if v is not None}
-    for i, c in enumerate(codes):
-        rows = np.flatnonzero(cid == i)
-        ref = _oracle(c, "ca_sscl", 8, "f32", P.PruningConfig()).decode(np.ascontiguousarray(llr[rows, :c.n]))
-        pb, cb = (c.payload_size + 7) // 8, (c.n + 7) // 8
-        assert np.array_equal(got["payload"][rows, :pb], ref.payload), c.n
-        assert np.array_equal(got["codeword"][rows, :cb], ref.codeword), c.n
-        assert np.array_equal(got["crc_ok"][rows], ref.crc_ok), c.n
-        assert np.array_equal(got["metric"][rows], ref.metric.astype(np.float32)), c.n
+    # CA at L=8 and SSCL at L=2 run several frames per warp (frames bucketed
+    # by code); SSC and FA's first pass run the frame-per-lane SC kernel
+    for kind, l in [("ca_sscl", 8), ("sscl", 2), ("ssc", 1), ("fa_sscl", 8)]:
+        dec = P.FrameDecoder(codes, kind, l, "f32", P.PruningConfig())
+        o = dec.decode_batch(gpu.from_numpy(llr).cuda(), code_id=gpu.from_numpy(cid).cuda(), codeword=True)
+        gpu.cuda.synchronize()
+        got = {k: v.cpu().numpy() for k, v in o.items() if v is not None}
+        for i, c in enumerate(codes):
+            rows = np.flatnonzero(cid == i)
+            ref = _oracle(c, kind, l, "f32", P.PruningConfig()).decode(np.ascontiguousarray(llr[rows, :c.n]))
+            pb, cb = (c.payload_size + 7) // 8, (c.n + 7) // 8
+            tag = (kind, l, c.n)
+            assert np.array_equal(got["payload"][rows, :pb], ref.payload), tag
+            assert np.array_equal(got["codeword"][rows, :cb], ref.codeword), tag
+            assert np.array_equal(got["crc_ok"][rows], ref.crc_ok), tag
+            assert np.array_equal(got["esc"][rows], ref.esc), tag
+            assert np.array_equal(got["metric"][rows], ref.metric.astype(np.float32)), tag
 
 
 def test_decode_host_matches_device_path(P, gpu):
