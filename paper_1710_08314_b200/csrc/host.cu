@@ -642,6 +642,8 @@ void run_decode(pl_handle& h, const void* llr, const int32_t* code_id, int64_t n
                 float* metric, cudaStream_t s, int exec = 0) {
     ck(cudaSetDevice(h.device), "cudaSetDevice");
     h.launches = 0;
+    h.prof_kind.clear(); // timed decode launches of this call (pl_last_kernel_ms)
+    h.prof_l.clear();
     if (nframes <= 0) return;
     const int kind = h.dec.kind;
     const bool need_lists = adaptive(kind);
@@ -980,7 +982,9 @@ int pl_profile(pl_handle* h, int32_t enable) {
 
 int32_t pl_last_kernel_ms(pl_handle* h, float* ms, int32_t* kind, int32_t* l, int32_t max) {
     if (!h || !h->profiling) return 0;
-    const int32_t n = int32_t(std::min<int64_t>(h->launches, max));
+    // decode kernels only (the bucketing kernels are counted in launches
+    // but not timed)
+    const int32_t n = int32_t(std::min<int64_t>(int64_t(h->prof_kind.size()), max));
     for (int32_t i = 0; i < n; ++i) {
         float t = 0.f;
         if (cudaEventSynchronize(h->prof_ev[size_t(2 * i + 1)]) != cudaSuccess ||
