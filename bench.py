@@ -310,6 +310,8 @@ def main():
         "config": common_config(wl, F, ws),
         "fer": counts.fer(), "frame_errors": counts.frame_errors, "bit_errors": counts.bit_errors,
         "esc_mean": counts.esc_sum / max(counts.frames, 1),
+        # frames per final list size (rank 0's batch): the work each rung sees
+        "esc_hist": {int(v): int(c) for v, c in zip(*np.unique(esc, return_counts=True))},
         "gpu_launches": int(launches),
         "kernel_ms": {f"{k[0]}_L{k[1]}": float(np.mean(v)) for k, v in kernel_ms.items()},
         "kernel_share_of_step": all_kernel_s / elapsed if ws == 1 else None,

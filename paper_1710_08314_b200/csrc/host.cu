@@ -467,9 +467,10 @@ int target_warps_per_sm() {
 // layout that still keeps PLB_TARGET_WARPS warps resident per SM, else the
 // layout with the most resident warps.  Small list sizes on single-code
 // batches decode 2 or 4 frames per warp (one per sub-warp) when that still
-// reaches the target; PLB_FPW forces frames per warp.  Ladder rungs above
-// L = 4 see few frames (the failures of the rung below): one frame per warp
-// spreads them over more warps, which measured faster there.
+// reaches the target; PLB_FPW forces frames per warp.  Ladder rungs (FA)
+// use 2 frames per warp up to L = 8 (measured: FA@3.5 dB L=8 rung 19.9 ->
+// 18.7 ms, @2.5 dB 178 -> 164 ms, @4.5 dB 0.72 -> 0.87 ms with its few
+// frames); multi-code ladder rungs get unsorted failure lists: 1 per warp.
 int env_int(const char* name, int dflt) {
     const char* e = std::getenv(name);
     return e ? std::atoi(e) : dflt;
@@ -564,7 +565,7 @@ RungCfg plan_rung(const pl_handle& h, int l, bool list, bool ladder = false) {
     // multi-code batches are bucketed by code before a non-ladder list pass;
     // ladder rungs get unsorted failure lists
     const bool multi = h.codes.size() > 1;
-    const int fmax = (list && !(ladder && (l > 4 || multi))) ? plb::frames_per_warp_max(l) : 1;
+    const int fmax = (list && !(ladder && (l > 8 || multi))) ? plb::frames_per_warp_max(l) : 1;
     std::vector<int> fpws;
     // a list size has kernels for fmax and 1 frames per warp
     if (forced_fpw) {
