@@ -1767,7 +1767,6 @@ __device__ int lane_rep(const LaneCtx<R>& c, int d, int m) {
     if (m > VE) {
         R* S = c.pool(d + 1) + c.lane * VE; // chunk k at S + k * 32 * VE
         int nc = m / VE;
-        const R* src0 = nullptr;
         #pragma unroll 1
         for (int first = 1; nc > 1; first = 0) {
             const int hc = nc >> 1;
@@ -1779,7 +1778,6 @@ __device__ int lane_rep(const LaneCtx<R>& c, int d, int m) {
             }
             nc = hc;
         }
-        (void)src0;
         x = vld<R, VE>(S);
         len = VE;
     } else {

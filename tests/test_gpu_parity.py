@@ -298,3 +298,22 @@ def test_cfg4_like_l32(P, gpu, oracle_lib):
     code = _code(P, 2048, 1024, "32-GZIP")
     _, llr = P.channel(code, 1.5, 42, 0, 24, "f32")
     check_parity(P, gpu, code, "ca_sscl", 32, "f32", P.PruningConfig(), llr, "cfg4")
+
+
+@pytest.mark.parametrize("prec", ["f32", "i8"])
+def test_alternate_kernels(P, gpu, oracle_lib, prec, monkeypatch):
+    """The opt-in / fallback launch paths stay bit-exact: team mode (a block
+    of warps per frame at L = 16/32, PLB_TEAM), the warp-per-frame SC kernel
+    (PLB_SC_LANES=0) and one frame per warp at small L (PLB_FPW=1)."""
+    code = _code(P, 1024, 480, "32-GZIP")
+    _, llr = P.channel(code, 2.0, 5, 0, 96, prec, 4.0 if prec == "i8" else 0.0)
+    pr = P.PruningConfig(rep_max=8) if prec == "i8" else P.PruningConfig()
+    for env, cases in [({"PLB_TEAM": "4", "PLB_TEAM_L": "16"}, [("ca_sscl", 16), ("ca_sscl", 32)]),
+                       ({"PLB_SC_LANES": "0"}, [("ssc", 1), ("fa_sscl", 8)]),
+                       ({"PLB_FPW": "1"}, [("ca_sscl", 4), ("sscl", 2)])]:
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        for kind, l in cases:
+            check_parity(P, gpu, code, kind, l, prec, pr, llr, f"env={env}")
+        for k in env:
+            monkeypatch.delenv(k)
