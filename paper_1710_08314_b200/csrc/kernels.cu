@@ -1505,11 +1505,19 @@ __device__ void team_helper(const LaunchParams& P, const DevCode& C, unsigned ch
 #ifndef PLB_MINBLOCKS
 #define PLB_MINBLOCKS 8
 #endif
+// register budget of the L = 32 kernels, whose occupancy shared memory
+// limits anyway (minimum resident 256-thread blocks: 2 -> up to 128
+// registers; measured cfg4 L=32 1.17 -> 1.24 Gb/s.  L = 16 is register-
+// limited and keeps 64: 3.15 vs 2.79 Gb/s with 128)
+#ifndef PLB_MINBLOCKS_BIGL
+#define PLB_MINBLOCKS_BIGL 2
+#endif
 
 // KV = 0: SC pass; KV = 1..6: list pass at L = 1, 2, 4, 8, 16, 32.  A warp
 // holds 32/SW frames (SW < 32 only for single-code batches).
 template <typename R, int KV, int SW, bool TEAM = false>
-__global__ void __launch_bounds__(kMaxTeam * 32, PLB_MINBLOCKS * kMaxWarpsPerBlock / kMaxTeam)
+__global__ void __launch_bounds__(kMaxTeam * 32, KV >= 6 ? PLB_MINBLOCKS_BIGL
+                                                         : PLB_MINBLOCKS * kMaxWarpsPerBlock / kMaxTeam)
 decode_kernel(const LaunchParams P) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int FPW = 32 / SW;
