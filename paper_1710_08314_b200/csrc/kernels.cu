@@ -948,60 +948,58 @@ __device__ void fused_leaf(Ctx<R, SW>& cx, int code, int d, int m, int lb, int n
                     pk |= uint64_t(uint8_t(c)) << (8 * i);
                 }
             }
-            auto at = [&](int i) { return int(int8_t(uint8_t(pk >> (8 * i)))); };
+            // statistics on the packed bytes (values past m are 0): byte
+            // magnitudes by VABSDIFF4, sums by VABSDIFF4.ACC (SAD), the two
+            // smallest (|v|, index) keys as 16-bit lanes through VIMNMX.U16x2
             const uint32_t lo = uint32_t(pk), hi = uint32_t(pk >> 32);
             const uint32_t mk = (1u << m) - 1u;
             const uint32_t hb = ((((lo >> 7) & 0x01010101u) * 0x01020408u) >> 24 |
                                  ((((hi >> 7) & 0x01010101u) * 0x01020408u) >> 24) << 4) & mk;
+            const uint32_t alo = __vabsdiffu4(lo ^ 0x80808080u, 0x80808080u);
+            const uint32_t ahi = __vabsdiffu4(hi ^ 0x80808080u, 0x80808080u);
+            const uint32_t nlo = prmt(lo, 0, 0xba98), nhi = prmt(hi, 0, 0xba98); // 0xff: negative
             uint32_t* w = row + (lb >> 5);
             const int sh = lb & 31;
             if (code == OP_FROZEN) {
-                int s = 0; // non-negative terms: the saturating sum is order-free
-                #pragma unroll 1
-                for (int i = 0; i < m; ++i) s += max(0, -at(i));
+                // non-negative terms: the saturating sum is order-free
+                const int s = int(__vsadu4(alo & nlo, 0u) + __vsadu4(ahi & nhi, 0u));
                 pen = min(s, 127);
                 *w &= ~(mk << sh);
             } else if (code == OP_INFO) {
-                cx.fx->st_a1[r] = mbits<M>(at(0));
+                cx.fx->st_a1[r] = mbits<M>(int(int8_t(uint8_t(lo))));
             } else if (code == OP_REP) {
-                // halving fold: value i of level len/2 = sat(i, i + len/2)
-                uint64_t x = pk;
+                // halving fold: value i of level len/2 = sat(i + i + len/2)
+                uint32_t x = m == 8 ? g_swar(lo, hi, 0u) : lo;
                 #pragma unroll 1
-                for (int len = m; len > 1; len >>= 1) {
-                    uint64_t y = 0;
-                    #pragma unroll 1
-                    for (int i = 0; i < len / 2; ++i) {
-                        const int s = A::sat(int(int8_t(uint8_t(x >> (8 * i)))),
-                                             int(int8_t(uint8_t(x >> (8 * (i + len / 2))))));
-                        y |= uint64_t(uint8_t(int8_t(s))) << (8 * i);
-                    }
-                    x = y;
-                }
+                for (int len = m == 8 ? 4 : m; len > 1; len >>= 1) x = g_swar(x, x >> (4 * len), 0u);
                 const int f0 = int(int8_t(uint8_t(x)));
                 const bool wn = f0 < 0;
-                int s = 0;
-                #pragma unroll 1
-                for (int i = 0; i < m; ++i) {
-                    const int vi = at(i);
-                    if (wn ? (vi > 0) : (vi < 0)) s += abs(vi);
-                }
+                // magnitudes of the values that disagree with the fold
+                const int s = int(__vsadu4(alo & (wn ? ~nlo : nlo), 0u) + __vsadu4(ahi & (wn ? ~nhi : nhi), 0u));
                 cx.fx->st_w[r] = wn;
                 cx.fx->st_a1[r] = mbits<M>(f0);
                 cx.fx->st_a2[r] = mbits<M>(min(s, 127));
             } else {
-                K k1 = A::kKeyMax, k2 = A::kKeyMax;
-                #pragma unroll 1
-                for (int i = 0; i < m; ++i) {
-                    const K kv = A::make_key(abs(at(i)), i);
-                    const K n1 = kmin(k1, kv);
-                    k2 = kmin(k2, kmax(k1, kv));
-                    k1 = n1;
-                }
+                // keys (|v| << 3 | i), two per word; values past m -> 0xffff
+                uint32_t k0 = prmt(alo, 0, 0x4140) * 8u + 0x00010000u;
+                uint32_t k1 = prmt(alo, 0, 0x4342) * 8u + 0x00030002u;
+                uint32_t k2 = prmt(ahi, 0, 0x4140) * 8u + 0x00050004u;
+                uint32_t k3 = prmt(ahi, 0, 0x4342) * 8u + 0x00070006u;
+                if (m < 2) k0 |= 0xffff0000u;
+                if (m < 4) k1 = FULL;
+                if (m < 8) k2 = k3 = FULL;
+                const uint32_t mn01 = __vminu2(k0, k1), mx01 = __vmaxu2(k0, k1);
+                const uint32_t mn23 = __vminu2(k2, k3), mx23 = __vmaxu2(k2, k3);
+                const uint32_t a = __vminu2(mn01, mn23);                                   // per lane: smallest
+                const uint32_t b = __vminu2(__vmaxu2(mn01, mn23), __vminu2(mx01, mx23));  // second
+                const uint32_t alo16 = a & 0xffffu, ahi16 = a >> 16;
+                const uint32_t e1 = min(alo16, ahi16);
+                const uint32_t e2 = min(max(alo16, ahi16), min(b & 0xffffu, b >> 16));
                 *w = (*w & ~(mk << sh)) | (hb << sh);
-                cx.fx->st_i1[r] = A::key_idx(k1);
-                cx.fx->st_i2[r] = A::key_idx(k2);
-                cx.fx->st_a1[r] = mbits<M>(A::key_val(k1));
-                cx.fx->st_a2[r] = mbits<M>(A::key_val(k2));
+                cx.fx->st_i1[r] = int(e1 & 7u);
+                cx.fx->st_i2[r] = int(e2 & 7u);
+                cx.fx->st_a1[r] = mbits<M>(int(e1 >> 3));
+                cx.fx->st_a2[r] = mbits<M>(int(e2 >> 3));
                 cx.fx->st_w[r] = __popc(hb) & 1;
             }
         }
