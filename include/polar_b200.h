@@ -105,6 +105,7 @@ void pl_destroy(pl_handle* h);
 int64_t pl_llr_stride(const pl_handle* h);      /* max n over codes */
 int64_t pl_payload_stride(const pl_handle* h);  /* max ceil((k+c)/8) */
 int64_t pl_codeword_stride(const pl_handle* h); /* max ceil(n/8) */
+int32_t pl_precision(const pl_handle* h);       /* PL_F32 / PL_I8, -1 for NULL */
 
 /* Decode nframes frames resident in device memory.
  *   llr      frame-major, pl_llr_stride elements per frame (float or int8)

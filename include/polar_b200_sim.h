@@ -59,6 +59,47 @@ int pl_channel_generate_device(const pl_code* code, double ebn0_db, uint64_t see
                                uint64_t frame0, int64_t nframes, int32_t precision,
                                float scale, uint8_t* info_out, void* llr_out, void* stream);
 
+/* ---- Monte-Carlo point (run_point, sim.cpp:76-135; SimConfig sim.hpp:14-29,
+ * PointStats sim.hpp:31-42).  Frames [frame0, frame0 + max_frames) keyed by
+ * (seed, global frame index) are generated, decoded with the handle's
+ * decoder and compared with their information bits on the device (an
+ * error-count kernel after each decode); the stop rule is evaluated at the
+ * reference's 1024-frame batch boundaries, so with the host channel the
+ * counts equal run_montecarlo's exactly, for any chunking.  frame0 lets
+ * ranks of a multi-GPU run take disjoint frame ranges (sum the counts). */
+enum { PL_CHANNEL_HOST = 0, PL_CHANNEL_DEVICE = 1 };
+
+typedef struct pl_sim_config {
+    double ebn0_db;
+    uint64_t seed;         /* sim.hpp:27 default 42 */
+    uint64_t frame0;       /* first global frame index of this run */
+    uint64_t max_frames;   /* 0 = unbounded (needs max_fe) */
+    uint64_t max_fe;       /* 0 = run to max_frames */
+    float quant_scale;     /* 0 = per-precision default (channel.hpp:94-100) */
+    int32_t channel;       /* PL_CHANNEL_HOST (FrameRng-exact) or PL_CHANNEL_DEVICE */
+    int32_t host_threads;  /* host channel generator threads (0 = all cores) */
+    int32_t pad;
+    int64_t chunk_frames;  /* frames per device batch, rounded up to 1024 (0 = auto) */
+} pl_sim_config;
+
+typedef struct pl_point_stats {
+    double ebn0_db;
+    uint64_t frames, bit_errors, frame_errors, esc_sum;
+    double ber, fer;
+    double ti_mbps;      /* info bits over summed decode-kernel time (GPU throughput) */
+    double lat_avg_us;   /* mean decode time of a device batch (every frame of a batch
+                            completes within it) */
+    double lat_worst_us; /* longest batch */
+    double esc_mean;
+} pl_point_stats;
+
+/* One Eb/N0 point.  `code` must be the handle's (single) code. */
+int pl_sim_point(pl_handle* h, const pl_code* code, const pl_sim_config* cfg,
+                 pl_point_stats* out);
+/* The reference's CSV data row (format_csv_row, report.cpp:40-50), no newline;
+ * returns the row length (the row is truncated to len - 1 bytes). */
+int32_t pl_format_csv_row(const pl_point_stats* p, char* buf, int32_t len);
+
 #ifdef __cplusplus
 }
 #endif

@@ -41,11 +41,12 @@ def build_oracle(force: bool = False) -> str:
 
 
 def build_ref(force: bool = False) -> str | None:
-    """Compile oracle/_ref when the reference sources are present."""
-    if os.path.exists(REF_SO) and not force:
-        return REF_SO
+    """Compile oracle/_ref when the reference sources are present (make keeps
+    it current); elsewhere (the GPU box) use the prebuilt library."""
     if not os.path.isdir(REF_SRC):
-        return None
+        return REF_SO if os.path.exists(REF_SO) else None
+    if force and os.path.exists(REF_SO):
+        os.remove(REF_SO)
     subprocess.check_call(["make", "-s", "-C", HERE, "ref"])
     return REF_SO
 
@@ -273,3 +274,36 @@ def ref_channel(n, k, frozen, crc_spec, ebn0_db, seed, frame0, nframes, precisio
     if rc:
         raise ValueError(err.value.decode())
     return info, llr
+
+
+def ref_montecarlo(n, k, frozen, crc_spec, kind, l, precision, pruning, ebn0_min, ebn0_max,
+                   ebn0_step, max_frames, max_fe, seed=42, quant_scale=0.0, workers=8):
+    """The reference's run_montecarlo (sim.cpp:148-174), timing off: per
+    point (ebn0, frames, bit_errors, frame_errors, ber, fer, esc_mean)."""
+    lib = Reference.lib()
+    lib.polref_montecarlo.argtypes = (
+        [C.c_int, C.c_int, C.c_void_p, C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_float]
+        + [C.c_int] * 6 + [C.c_double] * 3 + [C.c_uint64] * 3
+        + [C.c_int, C.c_int, C.c_void_p, C.c_char_p, C.c_int])
+    fz = np.ascontiguousarray(frozen, np.uint8)
+    out = np.zeros((64, 7), np.float64)
+    err = C.create_string_buffer(512)
+    npts = lib.polref_montecarlo(n, k, _ptr(fz), (crc_spec or "").encode(), KINDS[kind], l,
+                                 PRECISIONS[precision], quant_scale, *_pruning_tuple(pruning),
+                                 ebn0_min, ebn0_max, ebn0_step, max_frames, max_fe, seed, workers,
+                                 64, _ptr(out), err, 512)
+    if npts < 0:
+        raise ValueError(err.value.decode())
+    return out[:npts]
+
+
+def ref_format_csv_row(vals):
+    """The reference's format_csv_row (report.cpp:40-50) for (ebn0, frames,
+    bit_errors, frame_errors, ber, fer, ti_mbps, lat_avg_us, lat_worst_us,
+    esc_mean)."""
+    lib = Reference.lib()
+    lib.polref_format_csv_row.argtypes = [C.c_void_p, C.c_char_p, C.c_int]
+    v = np.ascontiguousarray(vals, np.float64)
+    buf = C.create_string_buffer(512)
+    lib.polref_format_csv_row(_ptr(v), buf, 512)
+    return buf.value.decode()

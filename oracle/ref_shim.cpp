@@ -17,6 +17,9 @@
 //   polref_channel                -> run_frame's input side: FrameRng,
 //                                    random_payload, encode_systematic,
 //                                    transmit (sim.cpp:45-51, channel.hpp)
+//   polref_montecarlo             -> run_montecarlo (sim.cpp:148-174),
+//                                    timing off: the error counts of a sweep
+//   polref_format_csv_row         -> format_csv_row (report.cpp:40-50)
 //
 // Payload and codeword outputs are packed MSB-first, the BitVector byte
 // convention (bit_vector.hpp:11-14, 57-59).
@@ -36,6 +39,8 @@
 #include "polar/decoders.hpp"
 #include "polar/errors.hpp"
 #include "polar/prune_tree.hpp"
+#include "polar/report.hpp"
+#include "polar/sim.hpp"
 
 using namespace polar;
 
@@ -302,6 +307,68 @@ int polref_channel(int n, int k, const std::uint8_t* frozen, const char* crc_spe
         set_err(err, errlen, e.what());
         return 1;
     }
+}
+
+// out: 7 doubles per point (ebn0, frames, bit_errors, frame_errors, ber,
+// fer, esc_mean); returns the number of points or -1
+int polref_montecarlo(int n, int k, const std::uint8_t* frozen, const char* crc_spec, int kind,
+                      int l, int precision, float quant_scale, int r0, int r1, int rep, int spc,
+                      int rep_max, int spc_max, double ebn0_min, double ebn0_max, double ebn0_step,
+                      std::uint64_t max_frames, std::uint64_t max_fe, std::uint64_t seed,
+                      int workers, int max_points, double* out, char* err, int errlen) {
+    try {
+        SimConfig cfg;
+        cfg.code = make_code(n, k, mask_from_bytes(frozen, n), crc_opt(crc_spec));
+        cfg.decoder = DecoderKind(kind);
+        cfg.list_size = l;
+        cfg.precision = precision == 0 ? Precision::f32 : precision == 1 ? Precision::q8 : Precision::q16;
+        cfg.quant_scale = quant_scale;
+        cfg.pruning = PruningConfig{r0 != 0, r1 != 0, rep != 0, spc != 0, rep_max, spc_max};
+        cfg.ebn0_min = ebn0_min;
+        cfg.ebn0_max = ebn0_max;
+        cfg.ebn0_step = ebn0_step;
+        cfg.max_frames = max_frames;
+        cfg.max_fe = max_fe;
+        cfg.seed = seed;
+        cfg.workers = workers;
+        cfg.timing = false;
+        const SimStats st = run_montecarlo(cfg);
+        int i = 0;
+        for (const auto& p : st.points) {
+            if (i >= max_points) break;
+            double* o = out + 7 * i++;
+            o[0] = p.ebn0_db;
+            o[1] = double(p.frames);
+            o[2] = double(p.bit_errors);
+            o[3] = double(p.frame_errors);
+            o[4] = p.ber;
+            o[5] = p.fer;
+            o[6] = p.esc_mean;
+        }
+        return i;
+    } catch (const std::exception& e) {
+        set_err(err, errlen, e.what());
+        return -1;
+    }
+}
+
+// v: ebn0, frames, bit_errors, frame_errors, ber, fer, ti_mbps, lat_avg_us,
+// lat_worst_us, esc_mean
+int polref_format_csv_row(const double* v, char* buf, int len) {
+    PointStats p;
+    p.ebn0_db = v[0];
+    p.frames = std::uint64_t(v[1]);
+    p.bit_errors = std::uint64_t(v[2]);
+    p.frame_errors = std::uint64_t(v[3]);
+    p.ber = v[4];
+    p.fer = v[5];
+    p.ti_mbps = v[6];
+    p.lat_avg_us = v[7];
+    p.lat_worst_us = v[8];
+    p.esc_mean = v[9];
+    const std::string row = format_csv_row(p);
+    std::snprintf(buf, std::size_t(len), "%s", row.c_str());
+    return int(row.size());
 }
 
 } // extern "C"

@@ -15,7 +15,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libpolar_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["host.cu", "kernels.cu", "channel.cu"]
+SOURCES = ["host.cu", "kernels.cu", "channel.cu", "sim.cu"]
 HEADERS = ["polar_dev.h", "channel.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

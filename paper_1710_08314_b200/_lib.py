@@ -11,6 +11,7 @@ import os
 from . import _build
 
 PL_OK, PL_ERR_CONFIG, PL_ERR_PARSE, PL_ERR_CUDA, PL_ERR_ARG = 0, 1, 2, 3, 4
+PL_CHANNEL_HOST, PL_CHANNEL_DEVICE = 0, 1
 
 # every symbol the two public headers declare
 EXPORTS = (
@@ -18,7 +19,8 @@ EXPORTS = (
     "pl_codeword_stride", "pl_decode", "pl_decode_host", "pl_last_launches", "pl_crc_parse",
     "pl_crc_compute", "pl_tree_build", "pl_construct_frozen_bhat", "pl_construct_frozen_ga",
     "pl_channel_generate", "pl_channel_generate_device", "pl_profile", "pl_last_kernel_ms",
-    "pl_kernel_selftest", "pl_channel_generate_frames",
+    "pl_kernel_selftest", "pl_channel_generate_frames", "pl_precision", "pl_sim_point",
+    "pl_format_csv_row",
 )
 
 
@@ -35,6 +37,20 @@ class pl_code(C.Structure):
 class pl_pruning(C.Structure):
     _fields_ = [("rate_zero", C.c_int32), ("rate_one", C.c_int32), ("repetition", C.c_int32),
                 ("single_parity", C.c_int32), ("rep_max", C.c_int32), ("spc_max", C.c_int32)]
+
+
+class pl_sim_config(C.Structure):
+    _fields_ = [("ebn0_db", C.c_double), ("seed", C.c_uint64), ("frame0", C.c_uint64),
+                ("max_frames", C.c_uint64), ("max_fe", C.c_uint64), ("quant_scale", C.c_float),
+                ("channel", C.c_int32), ("host_threads", C.c_int32), ("pad", C.c_int32),
+                ("chunk_frames", C.c_int64)]
+
+
+class pl_point_stats(C.Structure):
+    _fields_ = [("ebn0_db", C.c_double), ("frames", C.c_uint64), ("bit_errors", C.c_uint64),
+                ("frame_errors", C.c_uint64), ("esc_sum", C.c_uint64), ("ber", C.c_double),
+                ("fer", C.c_double), ("ti_mbps", C.c_double), ("lat_avg_us", C.c_double),
+                ("lat_worst_us", C.c_double), ("esc_mean", C.c_double)]
 
 
 class pl_decoder(C.Structure):
@@ -83,6 +99,11 @@ def lib():
     L.pl_kernel_selftest.argtypes = [i32, vp]
     L.pl_channel_generate_frames.argtypes = [vp, C.c_double, u64, vp, i64, i32, C.c_float, vp, i64,
                                              vp, i64, i32]
+    L.pl_precision.argtypes = [vp]
+    L.pl_precision.restype = i32
+    L.pl_sim_point.argtypes = [vp, vp, vp, vp]
+    L.pl_format_csv_row.argtypes = [vp, C.c_char_p, i32]
+    L.pl_format_csv_row.restype = i32
     _LIB = L
     return L
 

@@ -963,6 +963,7 @@ void pl_destroy(pl_handle* h) {
 int64_t pl_llr_stride(const pl_handle* h) { return h ? h->nmax : 0; }
 int64_t pl_payload_stride(const pl_handle* h) { return h ? h->pstride : 0; }
 int64_t pl_codeword_stride(const pl_handle* h) { return h ? h->cstride : 0; }
+int32_t pl_precision(const pl_handle* h) { return h ? h->dec.precision : -1; }
 int64_t pl_last_launches(const pl_handle* h) { return h ? h->launches : 0; }
 
 int pl_kernel_selftest(int32_t device, uint64_t* mismatches) {

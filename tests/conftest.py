@@ -34,6 +34,18 @@ def oracle_lib():
 
 
 @pytest.fixture(scope="session")
+def ref_lib():
+    """The compiled, unmodified reference (oracle/_ref), or skip."""
+    from oracle import oracle
+
+    try:
+        oracle.Reference.lib()
+    except Exception as e:  # noqa: BLE001
+        pytest.skip(f"reference not available: {e}")
+    return oracle
+
+
+@pytest.fixture(scope="session")
 def gpu():
     import torch
 
