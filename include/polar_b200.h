@@ -54,9 +54,11 @@ extern "C" {
 #define PL_KIND_PA_SSCL 5
 #define PL_KIND_FA_SSCL 6
 
-/* LLR representation (llr.hpp:12-33): float32 or int8 saturated to +-127 */
+/* LLR representation (llr.hpp:12-33): float32, int8 saturated to +-127 or
+ * int16 saturated to +-32767 */
 #define PL_F32 0
 #define PL_I8 1
+#define PL_I16 2
 
 typedef struct pl_crc {
     int32_t width; /* 0 = code without CRC; else 1..64 */
@@ -82,7 +84,7 @@ typedef struct pl_pruning { /* PruningConfig, prune_tree.hpp:25-34 */
 typedef struct pl_decoder {
     int32_t kind;      /* PL_KIND_* */
     int32_t l;         /* list size (Lmax for PA/FA); power of two <= 32 */
-    int32_t precision; /* PL_F32 / PL_I8 */
+    int32_t precision; /* PL_F32 / PL_I8 / PL_I16 */
     pl_pruning pruning;
 } pl_decoder;
 
@@ -105,7 +107,7 @@ void pl_destroy(pl_handle* h);
 int64_t pl_llr_stride(const pl_handle* h);      /* max n over codes */
 int64_t pl_payload_stride(const pl_handle* h);  /* max ceil((k+c)/8) */
 int64_t pl_codeword_stride(const pl_handle* h); /* max ceil(n/8) */
-int32_t pl_precision(const pl_handle* h);       /* PL_F32 / PL_I8, -1 for NULL */
+int32_t pl_precision(const pl_handle* h);       /* PL_F32 / PL_I8 / PL_I16, -1 for NULL */
 
 /* Decode nframes frames resident in device memory.
  *   llr      frame-major, pl_llr_stride elements per frame (float or int8)

@@ -23,7 +23,7 @@ REF_SO = os.path.join(HERE, "_ref", "libpolar_ref.so")
 REF_SRC = "/root/reference/proj"
 
 KINDS = {"sc": 0, "ssc": 1, "scl": 2, "sscl": 3, "ca_sscl": 4, "pa_sscl": 5, "fa_sscl": 6}
-PRECISIONS = {"f32": 0, "i8": 1}
+PRECISIONS = {"f32": 0, "i8": 1, "i16": 2}
 
 _u8p = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
 
@@ -265,7 +265,7 @@ def ref_channel(n, k, frozen, crc_spec, ebn0_db, seed, frame0, nframes, precisio
     lib = Reference.lib()
     fz = np.ascontiguousarray(frozen, np.uint8)
     info = np.zeros((nframes, k), np.uint8)
-    dt = np.float32 if precision == "f32" else np.int8
+    dt = {"f32": np.float32, "i8": np.int8, "i16": np.int16}[precision]
     llr = np.zeros((nframes, n), dt)
     err = C.create_string_buffer(256)
     rc = lib.polref_channel(n, k, _ptr(fz), (crc_spec or "").encode(), ebn0_db, seed, frame0,

@@ -203,7 +203,7 @@ static int plb::channel_core(const pl_code* code, double ebn0_db, uint64_t seed,
     using namespace plb;
     if (!code || !code->frozen || !llr_out || nframes < 0 || !pow2(code->n) || code->k < 1)
         return PL_ERR_ARG;
-    if (precision != PL_F32 && precision != PL_I8) return PL_ERR_CONFIG;
+    if (precision != PL_F32 && precision != PL_I8 && precision != PL_I16) return PL_ERR_CONFIG;
     const int n = code->n, k = code->k, w = code->crc.width;
     std::vector<int> info_pos;
     for (int i = 0; i < n; ++i)
@@ -231,7 +231,8 @@ static int plb::channel_core(const pl_code* code, double ebn0_db, uint64_t seed,
     const double sigma2 = 1.0 / (2.0 * rate * std::pow(10.0, ebn0_db / 10.0));
     const double sigma = std::sqrt(sigma2);
     const double demap = 2.0 / sigma2;
-    const float qs = scale > 0 ? scale : (precision == PL_I8 ? 8.0f : 1.0f);
+    // default_quant_scale (channel.hpp:94-100)
+    const float qs = scale > 0 ? scale : (precision == PL_I8 ? 8.0f : precision == PL_I16 ? 64.0f : 1.0f);
     auto work = [&](int64_t a, int64_t b) {
         std::vector<uint64_t> u(static_cast<size_t>(nw));
         std::vector<uint8_t> info(static_cast<size_t>(k));
@@ -259,10 +260,14 @@ static int plb::channel_core(const pl_code* code, double ebn0_db, uint64_t seed,
                 const float v = float(demap * y);
                 if (precision == PL_F32) {
                     static_cast<float*>(llr_out)[f * llr_stride + i] = v;
-                } else {
+                } else if (precision == PL_I8) {
                     const float q = std::round(v * qs);
                     static_cast<int8_t*>(llr_out)[f * llr_stride + i] =
                         int8_t(std::clamp(q, -127.0f, 127.0f));
+                } else {
+                    const float q = std::round(v * qs);
+                    static_cast<int16_t*>(llr_out)[f * llr_stride + i] =
+                        int16_t(std::clamp(q, -32767.0f, 32767.0f));
                 }
             }
         }
@@ -361,9 +366,12 @@ __global__ void chan_kernel(const ChanParams P) {
             const float v = P.demap * y;
             if (P.precision == PL_F32) {
                 static_cast<float*>(P.llr_out)[f * P.n + i] = v;
-            } else {
+            } else if (P.precision == PL_I8) {
                 const float q = fminf(fmaxf(roundf(v * P.qs), -127.0f), 127.0f);
                 static_cast<int8_t*>(P.llr_out)[f * P.n + i] = int8_t(q);
+            } else {
+                const float q = fminf(fmaxf(roundf(v * P.qs), -32767.0f), 32767.0f);
+                static_cast<int16_t*>(P.llr_out)[f * P.n + i] = int16_t(q);
             }
         }
         __syncwarp();
@@ -380,7 +388,7 @@ extern "C" int pl_channel_generate_device(const pl_code* code, double ebn0_db, u
     using namespace plb;
     if (!code || !code->frozen || !llr_out || nframes < 0 || !pow2(code->n) || code->k < 1)
         return PL_ERR_ARG;
-    if (precision != PL_F32 && precision != PL_I8) return PL_ERR_CONFIG;
+    if (precision != PL_F32 && precision != PL_I8 && precision != PL_I16) return PL_ERR_CONFIG;
     if (nframes == 0) return PL_OK;
     const int n = code->n, k = code->k, w = code->crc.width;
     std::vector<int32_t> info_pos;
@@ -422,7 +430,7 @@ extern "C" int pl_channel_generate_device(const pl_code* code, double ebn0_db, u
     const double sigma2 = 1.0 / (2.0 * (double(k) / n) * std::pow(10.0, ebn0_db / 10.0));
     P.sigma = float(std::sqrt(sigma2));
     P.demap = float(2.0 / sigma2);
-    P.qs = scale > 0 ? scale : (precision == PL_I8 ? 8.0f : 1.0f);
+    P.qs = scale > 0 ? scale : (precision == PL_I8 ? 8.0f : precision == PL_I16 ? 64.0f : 1.0f);
     P.precision = precision;
     P.seed = seed;
     P.frame0 = frame0;

@@ -847,9 +847,9 @@ int pl_create(const pl_code* codes, int32_t ncodes, const pl_decoder* dec, int32
         h->dec = *dec;
         const int kind = dec->kind;
         if (kind < PL_KIND_SC || kind > PL_KIND_FA_SSCL) throw ConfigError("unknown decoder kind");
-        if (dec->precision != PL_F32 && dec->precision != PL_I8)
-            throw ConfigError("precision must be PL_F32 or PL_I8");
-        h->esz = dec->precision == PL_F32 ? 4 : 1;
+        if (dec->precision != PL_F32 && dec->precision != PL_I8 && dec->precision != PL_I16)
+            throw ConfigError("precision must be PL_F32, PL_I8 or PL_I16");
+        h->esz = dec->precision == PL_F32 ? 4 : dec->precision == PL_I16 ? 2 : 1;
         // FrameDecoder validation (decoders.hpp:40-55)
         const int l = uses_list(kind) ? dec->l : 1;
         h->dec.l = l;

@@ -130,6 +130,7 @@ struct Arith<float> {
     using M = float;      // path-metric type
     using Key = uint64_t; // float bits << 32 | index  (value >= +0)
     static constexpr bool kFixed = false;
+    static constexpr int kMax = 0; // (fixed point only: no saturation)
     static constexpr Key kKeyMax = ~0ull;
     __device__ static M sat(M a, M b) { return a + b; }
     // |v| as a non-negative float: abs_llr(-0.0f) is -0.0f in the reference,
@@ -158,6 +159,7 @@ struct Arith<int8_t> {
     using M = int;
     using Key = uint32_t; // value (0..127) << 16 | index
     static constexpr bool kFixed = true;
+    static constexpr int kMax = 127; // symmetric range (llr.hpp:29-33)
     static constexpr Key kKeyMax = ~0u;
     __device__ static M sat(M a, M b) { return max(-127, min(127, a + b)); }
     __device__ static M mag(int v) { return abs(v); }
@@ -174,6 +176,32 @@ struct Arith<int8_t> {
         return int8_t(max(-127, min(127, v)));
     }
     __device__ static int8_t store(M v) { return int8_t(v); }
+    __device__ static float to_float(M v) { return float(v); }
+};
+
+// int16 (llr.hpp:22-26): the int8 rules on [-32767, 32767], scalar f / g
+template <>
+struct Arith<int16_t> {
+    using M = int;
+    using Key = uint32_t; // value (0..32767) << 16 | index
+    static constexpr bool kFixed = true;
+    static constexpr int kMax = 32767;
+    static constexpr Key kKeyMax = ~0u;
+    __device__ static M sat(M a, M b) { return max(-kMax, min(kMax, a + b)); }
+    __device__ static M mag(int v) { return abs(v); }
+    __device__ static Key make_key(M v, int idx) { return (uint32_t(v) << 16) | uint32_t(idx); }
+    __device__ static int key_idx(Key k) { return int(k & 0xffffu); }
+    __device__ static M key_val(Key k) { return int(k >> 16); }
+    __device__ static M val(int16_t v) { return int(v); }
+    __device__ static int16_t f(int16_t a, int16_t b) {
+        const int m = min(abs(int(a)), abs(int(b)));
+        return int16_t(((a ^ b) < 0) ? -m : m);
+    }
+    __device__ static int16_t g(int16_t a, int16_t b, uint32_t s) {
+        const int v = s ? int(b) - int(a) : int(a) + int(b);
+        return int16_t(max(-kMax, min(kMax, v)));
+    }
+    __device__ static int16_t store(M v) { return int16_t(v); }
     __device__ static float to_float(M v) { return float(v); }
 };
 
@@ -418,7 +446,7 @@ struct Ctx {
     // (list_decoder.hpp:447-455).
     __device__ void normalize() {
         if constexpr (A::kFixed) {
-            const int v = is_alive() ? int(metric) : 127;
+            const int v = is_alive() ? int(metric) : A::kMax;
             const int mn = int(sw.red_min(unsigned(v)));
             if (is_alive()) metric -= mn;
         }
@@ -435,7 +463,7 @@ __device__ __forceinline__ Vec<R, G> fg_compute(const Vec<R, G>& a, const Vec<R,
                                                 bool is_g) {
     using A = Arith<R>;
     Vec<R, G> o;
-    if constexpr (A::kFixed && G >= 4) {
+    if constexpr (sizeof(R) == 1 && G >= 4) {
         constexpr int W = G / 4;
         const uint32_t* aw = reinterpret_cast<const uint32_t*>(&a.raw);
         const uint32_t* bw = reinterpret_cast<const uint32_t*>(&b.raw);
@@ -489,7 +517,7 @@ __device__ __forceinline__ void fg_elems(Ctx<R, SW>& cx, int d, int m, int lb, i
     constexpr int VE = 16 / int(sizeof(R));
     const int h = m >> 1;
     if (h >= VE) fg_run<R, SW, VE>(cx, d, h, lb, na, is_g);
-    else if (Arith<R>::kFixed && h >= 4) fg_run<R, SW, 4>(cx, d, h, lb, na, is_g); // one SWAR word
+    else if (sizeof(R) == 1 && h >= 4) fg_run<R, SW, 4>(cx, d, h, lb, na, is_g); // one SWAR word
     else fg_run<R, SW, 1>(cx, d, h, lb, na, is_g);
 }
 
@@ -735,7 +763,7 @@ __device__ void list_frozen(Ctx<R, SW>& cx, int d, int m, int lb, int na) {
             #pragma unroll 1
             for (int i = cx.lane; i < m; i += SW) s += max(0, -int(A::val(L[i])));
             s = int(cx.sw.red_add(unsigned(s)));
-            if (cx.lane == r) pen = M(min(s, 127));
+            if (cx.lane == r) pen = M(min(s, A::kMax));
         }
     } else if (cx.lane < na) {
         const R* L = cx.llr(cx.fx->alive_list[cx.lane], d);
@@ -887,7 +915,7 @@ __device__ void rep_pen(Ctx<R, SW>& cx, int d, int m, int na) {
             s = int(cx.sw.red_add(unsigned(s)));
             if (cx.lane == 0) {
                 cx.fx->st_w[r] = w;
-                cx.fx->st_a2[r] = mbits<M>(M(min(s, 127)));
+                cx.fx->st_a2[r] = mbits<M>(M(min(s, A::kMax)));
             }
         }
     } else if (cx.lane < na) {
@@ -919,7 +947,7 @@ __device__ void fused_leaf(Ctx<R, SW>& cx, int code, int d, int m, int lb, int n
     constexpr int MF = sizeof(R) == 1 ? kFuseMaxI8 : kFuseMaxF32;
     const int r = cx.lane;
     M pen = M(0);
-    if constexpr (A::kFixed) {
+    if constexpr (sizeof(R) == 1) {
         // int8: the m <= 8 child values packed in one u64 (value i in byte
         // i), produced by the SWAR f / g, statistics in rolled loops (small
         // code: the decode loop must stay inside the instruction cache)
@@ -2073,15 +2101,22 @@ int64_t gscratch_bytes_per_frame(int nmax, int l, int elem_bytes, int seg_smem_m
 int frames_per_warp_max(int l) { return l <= 2 ? 4 : l <= 8 ? 2 : 1; }
 bool frames_per_warp_ok(int l, int fpw) { return fpw == 1 || fpw == frames_per_warp_max(l); }
 
+// precision: 0 float, 1 int8, 2 int16 (PL_F32 / PL_I8 / PL_I16)
 cudaError_t launch_sc(const LaunchParams& p, int precision, int grid, cudaStream_t s) {
-    return precision == 0 ? launch<float>(p, 0, grid, s) : launch<int8_t>(p, 0, grid, s);
+    return precision == 0   ? launch<float>(p, 0, grid, s)
+           : precision == 1 ? launch<int8_t>(p, 0, grid, s)
+                            : launch<int16_t>(p, 0, grid, s);
 }
 cudaError_t launch_list(const LaunchParams& p, int precision, int grid, cudaStream_t s) {
     const int kv = kv_of(p.l, true);
-    return precision == 0 ? launch<float>(p, kv, grid, s) : launch<int8_t>(p, kv, grid, s);
+    return precision == 0   ? launch<float>(p, kv, grid, s)
+           : precision == 1 ? launch<int8_t>(p, kv, grid, s)
+                            : launch<int16_t>(p, kv, grid, s);
 }
 int occupancy_sc(int precision, int smem, int wpb) {
-    return precision == 0 ? occupancy<float>(0, 1, smem, wpb) : occupancy<int8_t>(0, 1, smem, wpb);
+    return precision == 0   ? occupancy<float>(0, 1, smem, wpb)
+           : precision == 1 ? occupancy<int8_t>(0, 1, smem, wpb)
+                            : occupancy<int16_t>(0, 1, smem, wpb);
 }
 
 int64_t lane_smem_bytes_per_warp(int nmax, int elem_bytes, int seg_smem_max) {
@@ -2092,14 +2127,18 @@ int64_t lane_gscratch_bytes_per_warp(int nmax, int elem_bytes, int seg_smem_max)
 }
 cudaError_t launch_sc_lanes(const LaunchParams& p, int precision, int grid, cudaStream_t s) {
     const int smem = p.smem_per_warp * p.wpb;
-    void (*kern)(LaunchParams) = precision == 0 ? sc_lanes_kernel<float> : sc_lanes_kernel<int8_t>;
+    void (*kern)(LaunchParams) = precision == 0   ? sc_lanes_kernel<float>
+                                 : precision == 1 ? sc_lanes_kernel<int8_t>
+                                                  : sc_lanes_kernel<int16_t>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     kern<<<grid, p.wpb * 32, smem, s>>>(p);
     return cudaGetLastError();
 }
 int occupancy_sc_lanes(int precision, int smem, int wpb) {
-    void (*kern)(LaunchParams) = precision == 0 ? sc_lanes_kernel<float> : sc_lanes_kernel<int8_t>;
+    void (*kern)(LaunchParams) = precision == 0   ? sc_lanes_kernel<float>
+                                 : precision == 1 ? sc_lanes_kernel<int8_t>
+                                                  : sc_lanes_kernel<int16_t>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
         cudaGetLastError();
         return 0;
@@ -2113,8 +2152,9 @@ int occupancy_sc_lanes(int precision, int smem, int wpb) {
 }
 int occupancy_list(int precision, int l, int fpw, int smem, int wpb, bool team) {
     const int kv = kv_of(l, true);
-    return precision == 0 ? occupancy<float>(kv, fpw, smem, wpb, team)
-                          : occupancy<int8_t>(kv, fpw, smem, wpb, team);
+    return precision == 0   ? occupancy<float>(kv, fpw, smem, wpb, team)
+           : precision == 1 ? occupancy<int8_t>(kv, fpw, smem, wpb, team)
+                            : occupancy<int16_t>(kv, fpw, smem, wpb, team);
 }
 
 cudaError_t bucket_by_code(const int32_t* cid, int64_t n, int ncodes, int32_t* hist, int32_t* out,

@@ -139,7 +139,7 @@ int pl_sim_point(pl_handle* h, const pl_code* code, const pl_sim_config* cfg, pl
     const int64_t pstride = pl_payload_stride(h);
     if (pl_llr_stride(h) != n) return PL_ERR_ARG; // the handle's own (single) code
     const int32_t prec = pl_precision(h);
-    const int64_t esz = prec == PL_I8 ? 1 : 4;
+    const int64_t esz = prec == PL_I8 ? 1 : prec == PL_I16 ? 2 : 4;
     const uint64_t max_frames = cfg->max_frames ? cfg->max_frames : ~0ull;
     int64_t chunk = cfg->chunk_frames > 0 ? cfg->chunk_frames : (int64_t(1) << 18);
     chunk = (chunk + kBatch - 1) / kBatch * kBatch;

@@ -84,6 +84,10 @@ class DecoderKind(enum.IntEnum):
 class Precision(enum.IntEnum):
     f32 = 0
     i8 = 1
+    i16 = 2
+
+
+_NP_DTYPE = {"f32": np.float32, "i8": np.int8, "i16": np.int16}
 
 
 @dataclass(frozen=True)
@@ -232,7 +236,7 @@ def channel_device(code: PolarCode, ebn0_db: float, seed: int, frame0: int, nfra
     import torch
 
     dev = f"cuda:{device}"
-    dt = torch.float32 if precision == "f32" else torch.int8
+    dt = {"f32": torch.float32, "i8": torch.int8, "i16": torch.int16}[precision]
     llr = torch.empty((nframes, code.n), dtype=dt, device=dev)
     info = torch.empty((nframes, code.k), dtype=torch.uint8, device=dev) if with_info else None
     c = code.to_c()
@@ -250,7 +254,7 @@ def channel(code: PolarCode, ebn0_db: float, seed: int, frame0: int, nframes: in
             precision: str = "f32", scale: float = 0.0, nthreads: int = 0):
     """run_frame's inputs (sim.cpp:48-51), frame-keyed like FrameRng."""
     info = np.zeros((nframes, code.k), np.uint8)
-    dt = np.float32 if precision == "f32" else np.int8
+    dt = _NP_DTYPE[precision]
     llr = np.zeros((nframes, code.n), dt)
     c = code.to_c()
     rc = L.lib().pl_channel_generate(C.byref(c), ebn0_db, seed, frame0, nframes,
@@ -297,7 +301,7 @@ class FrameDecoder:
     """FrameDecoder<R> (decoders.hpp:37-103) on the GPU, over a batch.
 
     ``codes`` is one PolarCode or a list of them (mixed-code batches pick a
-    code per frame with ``code_id``).  ``precision`` is "f32" or "i8".
+    code per frame with ``code_id``).  ``precision`` is "f32", "i8" or "i16".
     """
 
     def __init__(self, codes, kind, l: int = 8, precision: str = "f32",
@@ -333,7 +337,8 @@ class FrameDecoder:
 
     @property
     def llr_dtype(self):
-        return self._torch.float32 if self.precision == Precision.f32 else self._torch.int8
+        t = self._torch
+        return {Precision.f32: t.float32, Precision.i8: t.int8, Precision.i16: t.int16}[self.precision]
 
     def alloc_outputs(self, nframes: int, codeword: bool = False):
         t = self._torch
