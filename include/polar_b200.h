@@ -44,6 +44,7 @@ extern "C" {
 #define PL_ERR_PARSE 2  /* ParseError: malformed CRC spec text */
 #define PL_ERR_CUDA 3   /* device failure (no GPU, launch error, OOM) */
 #define PL_ERR_ARG 4    /* null pointer / bad size passed to the ABI */
+#define PL_ERR_IO 5     /* IoError: filesystem failure (errors.hpp:19-21) */
 
 /* DecoderKind, decoders.hpp:10-18 — same order */
 #define PL_KIND_SC 0
@@ -162,6 +163,14 @@ int pl_crc_compute(const pl_crc* spec, const uint8_t* bits, int64_t len,
  * -1 (bad arguments / buffer too small). */
 int32_t pl_tree_build(const uint8_t* frozen, int32_t n, const pl_pruning* cfg,
                       int32_t* out, int32_t max_nodes);
+
+/* Frozen-set files (load_frozen_file / save_frozen_file, code.cpp:164-194):
+ * "N K" then one line of N characters, '1' = frozen.  Load with
+ * frozen_out = NULL to query n and k; errors are PL_ERR_PARSE / PL_ERR_IO
+ * with the reference's messages (pl_last_error(NULL)). */
+int pl_frozen_file_load(const char* path, int32_t* n, int32_t* k, uint8_t* frozen_out,
+                        int32_t cap);
+int pl_frozen_file_save(const char* path, int32_t n, int32_t k, const uint8_t* frozen);
 
 #ifdef __cplusplus
 }

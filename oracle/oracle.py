@@ -307,3 +307,26 @@ def ref_format_csv_row(vals):
     buf = C.create_string_buffer(512)
     lib.polref_format_csv_row(_ptr(v), buf, 512)
     return buf.value.decode()
+
+
+def ref_frozen_load(path, nmax=1 << 16):
+    """load_frozen_file; returns (n, k, mask) or raises (kind, message)."""
+    lib = Reference.lib()
+    lib.polref_frozen_load.argtypes = [C.c_char_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
+                                       C.c_char_p, C.c_int]
+    n, k = C.c_int(), C.c_int()
+    out = np.zeros(nmax, np.uint8)
+    err = C.create_string_buffer(512)
+    rc = lib.polref_frozen_load(str(path).encode(), C.byref(n), C.byref(k), _ptr(out), nmax, err, 512)
+    if rc:
+        raise RuntimeError(("parse" if rc == 1 else "io"), err.value.decode())
+    return n.value, k.value, out[:n.value]
+
+
+def ref_frozen_save(path, n, k, frozen):
+    lib = Reference.lib()
+    lib.polref_frozen_save.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_void_p, C.c_char_p, C.c_int]
+    fz = np.ascontiguousarray(frozen, np.uint8)
+    err = C.create_string_buffer(512)
+    if lib.polref_frozen_save(str(path).encode(), n, k, _ptr(fz), err, 512):
+        raise RuntimeError("io", err.value.decode())

@@ -20,6 +20,8 @@
 //   polref_montecarlo             -> run_montecarlo (sim.cpp:148-174),
 //                                    timing off: the error counts of a sweep
 //   polref_format_csv_row         -> format_csv_row (report.cpp:40-50)
+//   polref_frozen_load / _save    -> load_frozen_file / save_frozen_file
+//                                    (code.cpp:164-194)
 //
 // Payload and codeword outputs are packed MSB-first, the BitVector byte
 // convention (bit_vector.hpp:11-14, 57-59).
@@ -369,6 +371,35 @@ int polref_format_csv_row(const double* v, char* buf, int len) {
     const std::string row = format_csv_row(p);
     std::snprintf(buf, std::size_t(len), "%s", row.c_str());
     return int(row.size());
+}
+
+// returns 0, 1 (ParseError), 2 (IoError) with the message in err
+int polref_frozen_load(const char* path, int* n, int* k, std::uint8_t* out, int cap, char* err,
+                       int errlen) {
+    try {
+        const FrozenFile f = load_frozen_file(path);
+        *n = f.n;
+        *k = f.k;
+        for (int i = 0; i < f.n && i < cap; ++i) out[i] = f.mask.get(std::size_t(i)) ? 1 : 0;
+        return 0;
+    } catch (const ParseError& e) {
+        set_err(err, errlen, e.what());
+        return 1;
+    } catch (const IoError& e) {
+        set_err(err, errlen, e.what());
+        return 2;
+    }
+}
+
+int polref_frozen_save(const char* path, int n, int k, const std::uint8_t* frozen, char* err,
+                       int errlen) {
+    try {
+        save_frozen_file(path, n, k, mask_from_bytes(frozen, n));
+        return 0;
+    } catch (const std::exception& e) {
+        set_err(err, errlen, e.what());
+        return 2;
+    }
 }
 
 } // extern "C"

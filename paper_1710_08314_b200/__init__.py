@@ -12,6 +12,7 @@ from .polar import (  # noqa: F401
     DecoderKind,
     DeviceError,
     FrameDecoder,
+    IoError,
     ParseError,
     PolarCode,
     Precision,
@@ -20,7 +21,9 @@ from .polar import (  # noqa: F401
     construct_frozen,
     construct_frozen_ga,
     crc_compute,
+    load_frozen_file,
     make_code,
     prune_tree,
+    save_frozen_file,
     unpack_msb,
 )

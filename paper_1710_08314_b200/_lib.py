@@ -10,7 +10,7 @@ import os
 
 from . import _build
 
-PL_OK, PL_ERR_CONFIG, PL_ERR_PARSE, PL_ERR_CUDA, PL_ERR_ARG = 0, 1, 2, 3, 4
+PL_OK, PL_ERR_CONFIG, PL_ERR_PARSE, PL_ERR_CUDA, PL_ERR_ARG, PL_ERR_IO = 0, 1, 2, 3, 4, 5
 PL_CHANNEL_HOST, PL_CHANNEL_DEVICE = 0, 1
 
 # every symbol the two public headers declare
@@ -20,7 +20,7 @@ EXPORTS = (
     "pl_crc_compute", "pl_tree_build", "pl_construct_frozen_bhat", "pl_construct_frozen_ga",
     "pl_channel_generate", "pl_channel_generate_device", "pl_profile", "pl_last_kernel_ms",
     "pl_kernel_selftest", "pl_channel_generate_frames", "pl_precision", "pl_sim_point",
-    "pl_format_csv_row",
+    "pl_format_csv_row", "pl_frozen_file_load", "pl_frozen_file_save",
 )
 
 
@@ -104,6 +104,8 @@ def lib():
     L.pl_sim_point.argtypes = [vp, vp, vp, vp]
     L.pl_format_csv_row.argtypes = [vp, C.c_char_p, i32]
     L.pl_format_csv_row.restype = i32
+    L.pl_frozen_file_load.argtypes = [C.c_char_p, vp, vp, vp, i32]
+    L.pl_frozen_file_save.argtypes = [C.c_char_p, i32, i32, vp]
     _LIB = L
     return L
 

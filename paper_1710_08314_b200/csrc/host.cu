@@ -7,6 +7,8 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <cctype>
+#include <climits>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -797,6 +799,72 @@ int pl_crc_parse(const char* text, pl_crc* out) {
     } catch (const std::exception& e) {
         return fail(nullptr, PL_ERR_PARSE, e.what());
     }
+}
+
+// Frozen-set files in the reference format (code.cpp:164-194): "N K" then
+// one line of N characters, '1' = frozen.  Messages as the reference's
+// ParseError / IoError.
+int pl_frozen_file_load(const char* path, int32_t* n, int32_t* k, uint8_t* frozen_out, int32_t cap) {
+    if (!path || !n || !k) return fail(nullptr, PL_ERR_ARG, "null argument");
+    const std::string p(path);
+    FILE* fp = std::fopen(path, "r");
+    if (!fp) return fail(nullptr, PL_ERR_IO, "cannot open '" + p + "' for reading");
+    std::string text;
+    char buf[4096];
+    size_t got;
+    while ((got = std::fread(buf, 1, sizeof buf, fp)) > 0) text.append(buf, got);
+    std::fclose(fp);
+    // whitespace-separated tokens, as operator>> reads them
+    size_t pos = 0;
+    auto token = [&](std::string& out) {
+        while (pos < text.size() && std::isspace(static_cast<unsigned char>(text[pos]))) ++pos;
+        const size_t b = pos;
+        while (pos < text.size() && !std::isspace(static_cast<unsigned char>(text[pos]))) ++pos;
+        out = text.substr(b, pos - b);
+        return !out.empty();
+    };
+    auto as_int = [](const std::string& t, int32_t& v) {
+        if (t.empty()) return false;
+        char* end = nullptr;
+        const long x = std::strtol(t.c_str(), &end, 10);
+        if (*end || x < INT32_MIN || x > INT32_MAX) return false;
+        v = int32_t(x);
+        return true;
+    };
+    std::string tn, tk, mask;
+    int32_t vn = 0, vk = 0;
+    if (!token(tn) || !as_int(tn, vn) || !token(tk) || !as_int(tk, vk))
+        return fail(nullptr, PL_ERR_PARSE, "frozen file '" + p + "': header must be 'N K'");
+    if (!token(mask)) return fail(nullptr, PL_ERR_PARSE, "frozen file '" + p + "': missing mask line");
+    if (mask.size() != size_t(vn))
+        return fail(nullptr, PL_ERR_PARSE,
+                    "frozen file '" + p + "': mask has " + std::to_string(mask.size()) +
+                        " characters, header says N = " + std::to_string(vn));
+    for (size_t i = 0; i < mask.size(); ++i)
+        if (mask[i] != '0' && mask[i] != '1')
+            return fail(nullptr, PL_ERR_PARSE,
+                        "frozen file '" + p + "': mask character '" + std::string(1, mask[i]) +
+                            "' at position " + std::to_string(i) + " (want 0 or 1)");
+    *n = vn;
+    *k = vk;
+    if (frozen_out) {
+        if (cap < vn) return fail(nullptr, PL_ERR_ARG, "frozen buffer too small");
+        for (int32_t i = 0; i < vn; ++i) frozen_out[i] = mask[size_t(i)] == '1';
+    }
+    return PL_OK;
+}
+
+int pl_frozen_file_save(const char* path, int32_t n, int32_t k, const uint8_t* frozen) {
+    if (!path || (!frozen && n > 0) || n < 0) return fail(nullptr, PL_ERR_ARG, "bad argument");
+    const std::string p(path);
+    FILE* fp = std::fopen(path, "w");
+    if (!fp) return fail(nullptr, PL_ERR_IO, "cannot open '" + p + "' for writing");
+    std::string out = std::to_string(n) + ' ' + std::to_string(k) + '\n';
+    for (int32_t i = 0; i < n; ++i) out += frozen[i] ? '1' : '0';
+    out += '\n';
+    const bool ok = std::fwrite(out.data(), 1, out.size(), fp) == out.size();
+    if (std::fclose(fp) != 0 || !ok) return fail(nullptr, PL_ERR_IO, "failed writing '" + p + "'");
+    return PL_OK;
 }
 
 int pl_crc_compute(const pl_crc* spec, const uint8_t* bits, int64_t len, uint64_t* out) {

@@ -32,6 +32,10 @@ import numpy as np
 from . import _lib as L
 
 
+class IoError(OSError):
+    """errors.hpp:19-21"""
+
+
 class ConfigError(ValueError):
     """Invalid code, decoder or tree parameters (errors.hpp:9-11)."""
 
@@ -51,7 +55,32 @@ def _raise(rc: int, msg: str):
         raise ParseError(msg)
     if rc == L.PL_ERR_ARG:
         raise ValueError(msg)
+    if rc == L.PL_ERR_IO:
+        raise IoError(msg)
     raise DeviceError(msg)
+
+
+def load_frozen_file(path: str):
+    """load_frozen_file (code.cpp:164-185) -> (n, k, frozen mask as uint8)."""
+    n, k = C.c_int32(), C.c_int32()
+    rc = L.lib().pl_frozen_file_load(str(path).encode(), C.byref(n), C.byref(k), None, 0)
+    if rc:
+        _raise(rc, L.last_error(None))
+    out = np.zeros(n.value, np.uint8)
+    rc = L.lib().pl_frozen_file_load(str(path).encode(), C.byref(n), C.byref(k),
+                                     out.ctypes.data_as(C.c_void_p), out.size)
+    if rc:
+        _raise(rc, L.last_error(None))
+    return n.value, k.value, out
+
+
+def save_frozen_file(path: str, n: int, k: int, frozen):
+    """save_frozen_file (code.cpp:187-194)."""
+    fz = (np.ascontiguousarray(frozen).astype(np.uint8) != 0).astype(np.uint8)
+    assert fz.size == n
+    rc = L.lib().pl_frozen_file_save(str(path).encode(), n, k, fz.ctypes.data_as(C.c_void_p))
+    if rc:
+        _raise(rc, L.last_error(None))
 
 
 class DecoderKind(enum.IntEnum):
