@@ -74,7 +74,15 @@ typedef struct pl_code {
     int32_t k;             /* information bits, CRC excluded (code.hpp:31) */
     const uint8_t* frozen; /* n bytes, nonzero = frozen; host memory */
     pl_crc crc;
+    /* PuncturePattern (code.hpp:13-24): n bytes, PL_USE_*; NULL = every
+     * position transmitted.  Only the channel side reads it (rate, demap);
+     * the decoders take whatever LLRs arrive. */
+    const uint8_t* channel_use;
 } pl_code;
+
+#define PL_USE_TRANSMITTED 0
+#define PL_USE_PUNCTURED 1 /* never sent: LLR 0 */
+#define PL_USE_SHORTENED 2 /* known zero: the largest LLR (llr.hpp:105-111) */
 
 typedef struct pl_pruning { /* PruningConfig, prune_tree.hpp:25-34 */
     int32_t rate_zero, rate_one, repetition, single_parity;
@@ -171,6 +179,9 @@ int32_t pl_tree_build(const uint8_t* frozen, int32_t n, const pl_pruning* cfg,
 int pl_frozen_file_load(const char* path, int32_t* n, int32_t* k, uint8_t* frozen_out,
                         int32_t cap);
 int pl_frozen_file_save(const char* path, int32_t n, int32_t k, const uint8_t* frozen);
+/* Puncture files (load_puncture_file, code.cpp:196-221): "N" then N
+ * characters T / P / S -> PL_USE_TRANSMITTED / _PUNCTURED / _SHORTENED. */
+int pl_puncture_file_load(const char* path, int32_t* n, uint8_t* use_out, int32_t cap);
 
 #ifdef __cplusplus
 }

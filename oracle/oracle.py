@@ -178,7 +178,8 @@ class Reference:
                                                     C.c_char_p, C.c_int]
             lib.polref_channel.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_char_p, C.c_double,
                                            C.c_uint64, C.c_uint64, C.c_int64, C.c_int, C.c_float,
-                                           C.c_void_p, C.c_void_p, C.c_int, C.c_char_p, C.c_int]
+                                           C.c_void_p, C.c_void_p, C.c_int, C.c_char_p, C.c_char_p,
+                                           C.c_int]
             cls._lib = lib
         return cls._lib
 
@@ -260,7 +261,7 @@ def ref_construct_frozen(n, reliable, design):
 
 
 def ref_channel(n, k, frozen, crc_spec, ebn0_db, seed, frame0, nframes, precision="f32",
-                scale=0.0, nthreads=8):
+                scale=0.0, nthreads=8, punct=""):
     """run_frame's inputs (sim.cpp:48-51): info bits and channel LLRs."""
     lib = Reference.lib()
     fz = np.ascontiguousarray(frozen, np.uint8)
@@ -270,7 +271,7 @@ def ref_channel(n, k, frozen, crc_spec, ebn0_db, seed, frame0, nframes, precisio
     err = C.create_string_buffer(256)
     rc = lib.polref_channel(n, k, _ptr(fz), (crc_spec or "").encode(), ebn0_db, seed, frame0,
                             nframes, PRECISIONS[precision], scale, _ptr(info), _ptr(llr),
-                            nthreads, err, 256)
+                            nthreads, punct.encode(), err, 256)
     if rc:
         raise ValueError(err.value.decode())
     return info, llr
@@ -330,3 +331,17 @@ def ref_frozen_save(path, n, k, frozen):
     err = C.create_string_buffer(512)
     if lib.polref_frozen_save(str(path).encode(), n, k, _ptr(fz), err, 512):
         raise RuntimeError("io", err.value.decode())
+
+
+def ref_puncture_load(path, nmax=1 << 16):
+    """load_puncture_file -> channel uses (0 T / 1 P / 2 S) or raises (kind, message)."""
+    lib = Reference.lib()
+    lib.polref_puncture_load.argtypes = [C.c_char_p, C.c_void_p, C.c_void_p, C.c_int, C.c_char_p,
+                                         C.c_int]
+    n = C.c_int()
+    out = np.zeros(nmax, np.uint8)
+    err = C.create_string_buffer(512)
+    rc = lib.polref_puncture_load(str(path).encode(), C.byref(n), _ptr(out), nmax, err, 512)
+    if rc:
+        raise RuntimeError(("parse" if rc == 1 else "io"), err.value.decode())
+    return out[:n.value]

@@ -272,13 +272,24 @@ int polref_construct_frozen(int n, int reliable, double design, std::uint8_t* ou
 // run_frame's input side (sim.cpp:48-51) for frames [frame0, frame0+nframes):
 // info bits as 0/1 bytes (k per frame) and channel LLRs in the requested
 // representation (precision 0 f32, 1 int8, 2 int16; scale <= 0 = default).
+// punct: "" or n characters T / P / S (the PuncturePattern of make_code)
 int polref_channel(int n, int k, const std::uint8_t* frozen, const char* crc_spec,
                    double ebn0_db, std::uint64_t seed, std::uint64_t frame0,
                    std::int64_t nframes, int precision, float scale,
-                   std::uint8_t* info_out, void* llr_out, int nthreads, char* err,
-                   int errlen) {
+                   std::uint8_t* info_out, void* llr_out, int nthreads, const char* punct,
+                   char* err, int errlen) {
     try {
-        const PolarCode code = make_code(n, k, mask_from_bytes(frozen, n), crc_opt(crc_spec));
+        std::optional<PuncturePattern> pp;
+        if (punct && *punct) {
+            PuncturePattern p;
+            for (const char* c = punct; *c; ++c) {
+                p.use.push_back(*c == 'T' ? ChannelUse::transmitted
+                                : *c == 'P' ? ChannelUse::punctured : ChannelUse::shortened);
+                p.transmitted += *c == 'T';
+            }
+            pp = std::move(p);
+        }
+        const PolarCode code = make_code(n, k, mask_from_bytes(frozen, n), crc_opt(crc_spec), pp);
         const double sigma2 = awgn_sigma2(code, ebn0_db);
         parallel_frames(nframes, nthreads, [&](std::int64_t a, std::int64_t b) {
             for (std::int64_t f = a; f < b; ++f) {
@@ -397,6 +408,22 @@ int polref_frozen_save(const char* path, int n, int k, const std::uint8_t* froze
         save_frozen_file(path, n, k, mask_from_bytes(frozen, n));
         return 0;
     } catch (const std::exception& e) {
+        set_err(err, errlen, e.what());
+        return 2;
+    }
+}
+
+// load_puncture_file: uses 0 T / 1 P / 2 S; 0, 1 (ParseError), 2 (IoError)
+int polref_puncture_load(const char* path, int* n, std::uint8_t* out, int cap, char* err, int errlen) {
+    try {
+        const PuncturePattern p = load_puncture_file(path);
+        *n = int(p.use.size());
+        for (int i = 0; i < *n && i < cap; ++i) out[i] = std::uint8_t(p.use[std::size_t(i)]);
+        return 0;
+    } catch (const ParseError& e) {
+        set_err(err, errlen, e.what());
+        return 1;
+    } catch (const IoError& e) {
         set_err(err, errlen, e.what());
         return 2;
     }

@@ -18,10 +18,13 @@ from .polar import (  # noqa: F401
     Precision,
     PruningConfig,
     channel,
+    channel_device,
+    channel_frames,
     construct_frozen,
     construct_frozen_ga,
     crc_compute,
     load_frozen_file,
+    load_puncture_file,
     make_code,
     prune_tree,
     save_frozen_file,

@@ -20,7 +20,7 @@ EXPORTS = (
     "pl_crc_compute", "pl_tree_build", "pl_construct_frozen_bhat", "pl_construct_frozen_ga",
     "pl_channel_generate", "pl_channel_generate_device", "pl_profile", "pl_last_kernel_ms",
     "pl_kernel_selftest", "pl_channel_generate_frames", "pl_precision", "pl_sim_point",
-    "pl_format_csv_row", "pl_frozen_file_load", "pl_frozen_file_save",
+    "pl_format_csv_row", "pl_frozen_file_load", "pl_frozen_file_save", "pl_puncture_file_load",
 )
 
 
@@ -31,7 +31,7 @@ class pl_crc(C.Structure):
 
 class pl_code(C.Structure):
     _fields_ = [("n", C.c_int32), ("k", C.c_int32), ("frozen", C.POINTER(C.c_uint8)),
-                ("crc", pl_crc)]
+                ("crc", pl_crc), ("channel_use", C.POINTER(C.c_uint8))]
 
 
 class pl_pruning(C.Structure):
@@ -106,6 +106,7 @@ def lib():
     L.pl_format_csv_row.restype = i32
     L.pl_frozen_file_load.argtypes = [C.c_char_p, vp, vp, vp, i32]
     L.pl_frozen_file_save.argtypes = [C.c_char_p, i32, i32, vp]
+    L.pl_puncture_file_load.argtypes = [C.c_char_p, vp, vp, i32]
     _LIB = L
     return L
 

@@ -227,7 +227,18 @@ static int plb::channel_core(const pl_code* code, double ebn0_db, uint64_t seed,
             msg[size_t(j)] = 0;
         }
     }
-    const double rate = double(k) / double(n);
+    // puncturing (channel.hpp:62-89): the rate counts transmitted uses only
+    const uint8_t* use = code->channel_use;
+    int transmitted = n;
+    if (use) {
+        transmitted = 0;
+        for (int i = 0; i < n; ++i) {
+            if (use[i] > PL_USE_SHORTENED) return PL_ERR_CONFIG;
+            transmitted += use[i] == PL_USE_TRANSMITTED;
+        }
+        if (transmitted < k + w) return PL_ERR_CONFIG;
+    }
+    const double rate = double(k) / double(transmitted);
     const double sigma2 = 1.0 / (2.0 * rate * std::pow(10.0, ebn0_db / 10.0));
     const double sigma = std::sqrt(sigma2);
     const double demap = 2.0 / sigma2;
@@ -254,6 +265,17 @@ static int plb::channel_core(const pl_code* code, double ebn0_db, uint64_t seed,
             for (int j = 0; j < nw; ++j) u[size_t(j)] &= amask[size_t(j)];
             polar_transform_words(u.data(), n);
             for (int i = 0; i < n; ++i) {
+                const int ui = use ? use[i] : PL_USE_TRANSMITTED;
+                if (ui != PL_USE_TRANSMITTED) { // no noise draw (channel.hpp:70-80)
+                    const bool sh = ui == PL_USE_SHORTENED; // known_zero_llr (llr.hpp:105-111)
+                    if (precision == PL_F32)
+                        static_cast<float*>(llr_out)[f * llr_stride + i] = sh ? 1e9f : 0.0f;
+                    else if (precision == PL_I8)
+                        static_cast<int8_t*>(llr_out)[f * llr_stride + i] = int8_t(sh ? 127 : 0);
+                    else
+                        static_cast<int16_t*>(llr_out)[f * llr_stride + i] = int16_t(sh ? 32767 : 0);
+                    continue;
+                }
                 const bool x = (u[size_t(i >> 6)] >> (63 - (i & 63))) & 1;
                 const double s = x ? -1.0 : 1.0;
                 const double y = s + sigma * rng.gaussian();
@@ -292,6 +314,7 @@ namespace {
 struct ChanParams {
     int n, k, w, rw;
     const int32_t* info_pos; // k + w
+    const uint8_t* use;      // n channel uses, nullable
     const uint64_t* col;     // k CRC columns
     uint64_t c0;
     float sigma, demap, qs;
@@ -361,6 +384,14 @@ __global__ void chan_kernel(const ChanParams P) {
         __syncwarp();
         transform_row(row, P.n, P.rw, lane);
         for (int i = lane; i < P.n; i += 32) {
+            const int ui = P.use ? P.use[i] : PL_USE_TRANSMITTED;
+            if (ui != PL_USE_TRANSMITTED) {
+                const bool sh = ui == PL_USE_SHORTENED;
+                if (P.precision == PL_F32) static_cast<float*>(P.llr_out)[f * P.n + i] = sh ? 1e9f : 0.0f;
+                else if (P.precision == PL_I8) static_cast<int8_t*>(P.llr_out)[f * P.n + i] = int8_t(sh ? 127 : 0);
+                else static_cast<int16_t*>(P.llr_out)[f * P.n + i] = int16_t(sh ? 32767 : 0);
+                continue;
+            }
             const bool x = (row[i >> 5] >> (i & 31)) & 1u;
             const float y = (x ? -1.0f : 1.0f) + P.sigma * curand_normal(&st);
             const float v = P.demap * y;
@@ -412,9 +443,24 @@ extern "C" int pl_channel_generate_device(const pl_code* code, double ebn0_db, u
     }
     uint32_t* amask = reinterpret_cast<uint32_t*>(tab.data() + k);
     for (int p : info_pos) amask[p >> 5] |= 1u << (p & 31);
+    const uint8_t* use = code->channel_use;
+    int transmitted = n;
+    if (use) {
+        transmitted = 0;
+        for (int i = 0; i < n; ++i) {
+            if (use[i] > PL_USE_SHORTENED) return PL_ERR_CONFIG;
+            transmitted += use[i] == PL_USE_TRANSMITTED;
+        }
+        if (transmitted < k + w) return PL_ERR_CONFIG;
+    }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     int32_t* d_pos = nullptr;
     uint64_t* d_tab = nullptr;
+    uint8_t* d_use = nullptr;
+    if (use) {
+        if (cudaMallocAsync(&d_use, size_t(n), s) != cudaSuccess) return PL_ERR_CUDA;
+        cudaMemcpyAsync(d_use, use, size_t(n), cudaMemcpyHostToDevice, s);
+    }
     if (cudaMallocAsync(&d_pos, info_pos.size() * 4, s) != cudaSuccess) return PL_ERR_CUDA;
     if (cudaMallocAsync(&d_tab, tab.size() * 8, s) != cudaSuccess) return PL_ERR_CUDA;
     cudaMemcpyAsync(d_pos, info_pos.data(), info_pos.size() * 4, cudaMemcpyHostToDevice, s);
@@ -425,9 +471,10 @@ extern "C" int pl_channel_generate_device(const pl_code* code, double ebn0_db, u
     P.w = w;
     P.rw = rw;
     P.info_pos = d_pos;
+    P.use = d_use;
     P.col = d_tab;
     P.c0 = c0;
-    const double sigma2 = 1.0 / (2.0 * (double(k) / n) * std::pow(10.0, ebn0_db / 10.0));
+    const double sigma2 = 1.0 / (2.0 * (double(k) / transmitted) * std::pow(10.0, ebn0_db / 10.0));
     P.sigma = float(std::sqrt(sigma2));
     P.demap = float(2.0 / sigma2);
     P.qs = scale > 0 ? scale : (precision == PL_I8 ? 8.0f : precision == PL_I16 ? 64.0f : 1.0f);
@@ -446,5 +493,6 @@ extern "C" int pl_channel_generate_device(const pl_code* code, double ebn0_db, u
     const cudaError_t e = cudaGetLastError();
     cudaFreeAsync(d_pos, s);
     cudaFreeAsync(d_tab, s);
+    if (d_use) cudaFreeAsync(d_use, s);
     return e == cudaSuccess ? PL_OK : PL_ERR_CUDA;
 }

@@ -351,6 +351,18 @@ HostCode make_host_code(const pl_code& c, const pl_decoder& dec) {
     h.psize = c.k + h.width;
     for (int i = 0; i < c.n; ++i)
         if (!h.frozen[size_t(i)]) h.info_pos.push_back(uint16_t(i));
+    if (c.channel_use) { // make_code's puncture checks (code.cpp:112-125)
+        int transmitted = 0;
+        for (int i = 0; i < c.n; ++i) {
+            if (c.channel_use[i] > PL_USE_SHORTENED)
+                throw ConfigError("channel use " + std::to_string(int(c.channel_use[i])) +
+                                  " at position " + std::to_string(i) + " (want T, P or S)");
+            transmitted += c.channel_use[i] == PL_USE_TRANSMITTED;
+        }
+        if (transmitted < c.k + h.width)
+            throw ConfigError("puncture pattern transmits only " + std::to_string(transmitted) +
+                              " symbols, fewer than K + CRC bits = " + std::to_string(c.k + h.width));
+    }
 
     static const pl_pruning none{0, 0, 0, 0, 0, 0};
     const pl_pruning& pc = uses_pruning(dec.kind) ? dec.pruning : none;
@@ -850,6 +862,51 @@ int pl_frozen_file_load(const char* path, int32_t* n, int32_t* k, uint8_t* froze
     if (frozen_out) {
         if (cap < vn) return fail(nullptr, PL_ERR_ARG, "frozen buffer too small");
         for (int32_t i = 0; i < vn; ++i) frozen_out[i] = mask[size_t(i)] == '1';
+    }
+    return PL_OK;
+}
+
+// Puncture files (load_puncture_file, code.cpp:196-221): "N" then N
+// characters T / P / S -> PL_USE_*.
+int pl_puncture_file_load(const char* path, int32_t* n, uint8_t* use_out, int32_t cap) {
+    if (!path || !n) return fail(nullptr, PL_ERR_ARG, "null argument");
+    const std::string p(path);
+    FILE* fp = std::fopen(path, "r");
+    if (!fp) return fail(nullptr, PL_ERR_IO, "cannot open '" + p + "' for reading");
+    std::string text;
+    char buf[4096];
+    size_t got;
+    while ((got = std::fread(buf, 1, sizeof buf, fp)) > 0) text.append(buf, got);
+    std::fclose(fp);
+    size_t pos = 0;
+    auto token = [&](std::string& out) {
+        while (pos < text.size() && std::isspace(static_cast<unsigned char>(text[pos]))) ++pos;
+        const size_t b = pos;
+        while (pos < text.size() && !std::isspace(static_cast<unsigned char>(text[pos]))) ++pos;
+        out = text.substr(b, pos - b);
+        return !out.empty();
+    };
+    std::string tn, pat;
+    char* end = nullptr;
+    long vn = 0;
+    if (!token(tn) || (vn = std::strtol(tn.c_str(), &end, 10), *end) || vn < INT32_MIN || vn > INT32_MAX)
+        return fail(nullptr, PL_ERR_PARSE, "puncture file '" + p + "': header must be 'N'");
+    if (!token(pat)) return fail(nullptr, PL_ERR_PARSE, "puncture file '" + p + "': missing pattern line");
+    if (pat.size() != size_t(vn))
+        return fail(nullptr, PL_ERR_PARSE,
+                    "puncture file '" + p + "': pattern has " + std::to_string(pat.size()) +
+                        " characters, header says N = " + std::to_string(vn));
+    for (size_t i = 0; i < pat.size(); ++i)
+        if (pat[i] != 'T' && pat[i] != 'P' && pat[i] != 'S')
+            return fail(nullptr, PL_ERR_PARSE,
+                        "puncture file '" + p + "': pattern character '" + std::string(1, pat[i]) +
+                            "' at position " + std::to_string(i) + " (want T, P or S)");
+    *n = int32_t(vn);
+    if (use_out) {
+        if (cap < vn) return fail(nullptr, PL_ERR_ARG, "pattern buffer too small");
+        for (long i = 0; i < vn; ++i)
+            use_out[i] = pat[size_t(i)] == 'T' ? PL_USE_TRANSMITTED
+                         : pat[size_t(i)] == 'P' ? PL_USE_PUNCTURED : PL_USE_SHORTENED;
     }
     return PL_OK;
 }

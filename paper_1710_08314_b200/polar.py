@@ -200,6 +200,8 @@ class PolarCode:
     frozen: np.ndarray
     crc: CrcSpec | None = None
     info_pos: np.ndarray = field(default=None)
+    # PuncturePattern.use (code.hpp:13-24): 0 T / 1 P / 2 S per position, or None
+    channel_use: np.ndarray | None = None
 
     @property
     def crc_width(self) -> int:
@@ -210,7 +212,9 @@ class PolarCode:
         return self.k + self.crc_width
 
     def rate(self) -> float:
-        return self.k / self.n
+        """code.hpp:40: information bits over transmitted channel uses"""
+        t = self.n if self.channel_use is None else int((self.channel_use == 0).sum())
+        return self.k / t
 
     def to_c(self) -> "L.pl_code":
         c = L.pl_code()
@@ -218,11 +222,15 @@ class PolarCode:
         c.k = self.k
         c.frozen = self.frozen.ctypes.data_as(C.POINTER(C.c_uint8))
         c.crc = self.crc.to_c() if self.crc else L.pl_crc(0, 0, 0, 0, 0)
+        c.channel_use = (self.channel_use.ctypes.data_as(C.POINTER(C.c_uint8))
+                         if self.channel_use is not None else None)
         return c
 
 
-def make_code(n: int, k: int, frozen, crc: CrcSpec | str | None = None) -> PolarCode:
-    """make_code (code.cpp:79-126): validates N, K and the open-position count."""
+def make_code(n: int, k: int, frozen, crc: CrcSpec | str | None = None, punct=None) -> PolarCode:
+    """make_code (code.cpp:79-126): validates N, K, the open-position count and
+    the puncture pattern (``punct``: n channel uses 0 T / 1 P / 2 S, or a
+    "TPS..." string)."""
     if isinstance(crc, str):
         crc = CrcSpec.parse(crc)
     fz = (np.ascontiguousarray(frozen).astype(np.uint8) != 0).astype(np.uint8)
@@ -236,7 +244,33 @@ def make_code(n: int, k: int, frozen, crc: CrcSpec | str | None = None) -> Polar
     open_ = int(n - fz.sum())
     if open_ != k + w:
         raise ConfigError(f"frozen mask leaves {open_} information positions, need K + CRC bits = {k + w}")
-    return PolarCode(n, k, fz, crc, np.flatnonzero(fz == 0).astype(np.int32))
+    use = None
+    if punct is not None:
+        if isinstance(punct, str):
+            punct = ["TPS".index(ch) for ch in punct]
+        use = np.ascontiguousarray(punct, np.uint8)
+        if use.size != n:
+            raise ConfigError(f"puncture pattern has {use.size} entries, code has N = {n}")
+        if use.max(initial=0) > 2:
+            raise ConfigError("channel uses must be 0 (T), 1 (P) or 2 (S)")
+        t = int((use == 0).sum())
+        if t < k + w:
+            raise ConfigError(f"puncture pattern transmits only {t} symbols, fewer than K + CRC bits = {k + w}")
+    return PolarCode(n, k, fz, crc, np.flatnonzero(fz == 0).astype(np.int32), use)
+
+
+def load_puncture_file(path: str) -> np.ndarray:
+    """load_puncture_file (code.cpp:196-221) -> channel uses (0 T / 1 P / 2 S)."""
+    n = C.c_int32()
+    rc = L.lib().pl_puncture_file_load(str(path).encode(), C.byref(n), None, 0)
+    if rc:
+        _raise(rc, L.last_error(None))
+    out = np.zeros(n.value, np.uint8)
+    rc = L.lib().pl_puncture_file_load(str(path).encode(), C.byref(n), out.ctypes.data_as(C.c_void_p),
+                                       out.size)
+    if rc:
+        _raise(rc, L.last_error(None))
+    return out
 
 
 def construct_frozen(n: int, reliable: int, design_erasure: float) -> np.ndarray:
