@@ -27,8 +27,15 @@
 //
 // Bit-exactness: f/g/h, the penalty sums (sequential, index
 // order), the halving REP fold, the (value,index) two-smallest order, the
-// stable (metric, emission-index) ranking, the slot assignment and int8
-// normalisation all reproduce list_decoder.hpp / sc_decoder.hpp exactly.
+// stable (metric, emission-index) ranking, the slot assignment and int8 /
+// int16 normalisation all reproduce list_decoder.hpp / sc_decoder.hpp
+// exactly, for float, int8 and int16 LLRs.
+//
+// Kernel families in this file: decode_kernel<R, KV, SW> (list passes at
+// L = 2^(KV-1) and the warp-per-frame SC pass, KV = 0), its opt-in team
+// variant (a block of warps per frame), sc_lanes_kernel<R> (the default SC
+// pass: one frame per lane), the frame bucketing kernels for multi-code
+// batches, and the int8 SWAR self-test.
 #include <algorithm>
 #include <cstdint>
 
