@@ -103,12 +103,23 @@ def measured_peaks():
 
 
 def dtype_of(wl):
-    return "int8" if wl.precision == "i8" else "f32"
+    return {"i8": "int8", "i16": "int16"}.get(wl.precision, "f32")
+
+
+def measured_traffic(wl, frames):
+    """roofline.traffic: DRAM bytes per launch of this workload's first decode
+    kernel, scaled from one committed ncu capture (profiles/traffic.py)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as fh:
+            t = json.load(fh)[wl.name]
+        return t["dram_bytes_per_frame"] * frames, t["source"]
+    except (OSError, KeyError, ValueError):
+        return None, None
 
 
 def common_config(wl, frames_per_gpu, ws):
     """The config both arms report (the driver compares like with like)."""
-    esz = 4 if wl.precision == "f32" else 1
+    esz = {"f32": 4, "i16": 2}.get(wl.precision, 1)
     return {**wl.describe(), "frames_per_gpu": frames_per_gpu,
             "global_frames": frames_per_gpu * ws, "parallelism": f"frame-range shards x{ws}",
             "l2": "inputs larger than L2 (%.0f MB per GPU per step)" % (frames_per_gpu * wl.n * esz / 1e6)}
@@ -278,7 +289,7 @@ def main():
         dec.decode_host_into(llr_h, host_out, cid_h)
     e2e_s = max_over_ranks(time.perf_counter() - t0)
     e2e_value = bits_per_step * ws * e2e_steps / e2e_s / 1e9
-    esz = 4 if wl.precision == "f32" else 1
+    esz = {"f32": 4, "i16": 2}.get(wl.precision, 1)
     h2d = F * dec.llr_stride * esz + (F * 4 if cid is not None else 0)
     d2h = F * (dec.payload_stride + 1 + 1 + 4)
 
@@ -301,6 +312,7 @@ def main():
     lane_achieved = ops_per_frame * n_launch_frames / per_launch_s
     all_kernel_s = sum(sum(v) for v in kernel_ms.values()) / 1e3
 
+    traffic, traffic_src = measured_traffic(wl, n_launch_frames)
     result = {
         "metric": METRIC,
         "value": value, "unit": "Gb/s", "n_gpus": ws, "steps": args.steps,
@@ -316,7 +328,8 @@ def main():
         "kernel_ms": {f"{k[0]}_L{k[1]}": float(np.mean(v)) for k, v in kernel_ms.items()},
         "kernel_share_of_step": all_kernel_s / elapsed if ws == 1 else None,
         "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peaks["hbm_gbs"],
-                     "unit": "GB/s", "frac": achieved_gbs / peaks["hbm_gbs"], "traffic": None,
+                     "unit": "GB/s", "frac": achieved_gbs / peaks["hbm_gbs"],
+                     "traffic": traffic, "traffic_source": traffic_src,
                      "kernel": f"decode_kernel<{dtype_of(wl)}, {dkind}> L={dl}",
                      "bytes_per_frame": bytes_per_frame, "peak_source": peak_src},
         "roofline_issue": {"bound": "issue", "achieved": lane_achieved / 1e9,
