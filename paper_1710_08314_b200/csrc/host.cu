@@ -780,16 +780,6 @@ void run_decode(pl_handle& h, const void* llr, const int32_t* code_id, int64_t n
     }
 }
 
-bool is_device_ptr(const void* p) {
-    if (!p) return true;
-    cudaPointerAttributes a{};
-    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-        cudaGetLastError();
-        return false;
-    }
-    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
-}
-
 bool is_pinned_host(const void* p) {
     cudaPointerAttributes a{};
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -1167,7 +1157,6 @@ int pl_decode_host(pl_handle* h, const void* llr, const int32_t* code_id, int64_
         const int64_t in_bytes = h->nmax * int64_t(h->esz);
         // per frame output record: payload | codeword | crc | esc | metric
         const int64_t ob_pay = h->pstride, ob_cw = codeword ? h->cstride : 0;
-        const int64_t out_rec = ob_pay + ob_cw + 1 + 1 + 4;
         if (h->stage_frames < chunk) {
             for (int i = 0; i < 2; ++i) {
                 if (h->d_in[i]) cudaFree(h->d_in[i]);
