@@ -172,8 +172,11 @@ def write_report(stream: io.TextIOBase, fmt: str, meta: list[str], stats: list[P
 def _main(argv=None):
     """A sweep from the command line, e.g. BASELINE configs[4]:
 
-        python -m paper_1710_08314_b200.sim --n 2048 --k 1024 --crc 32-GZIP \\
-            --decoder ca_sscl --l 32 --ebn0 1.0 4.0 0.5 --frames 16777216
+        python -m paper_1710_08314_b200.sim 2048:1024:32-GZIP \\
+            --decoder ca_sscl --list-size 32 --ebn0 1.0 4.0 0.5 --frames 16777216
+
+    The code is the first (positional) argument, N:K[:CRC], which keeps the
+    options apart from torchrun's own when launched under it.
 
     Under torchrun each rank takes its frame range of every point and the
     counts are summed with one all-reduce per point (NCCL)."""
@@ -183,12 +186,10 @@ def _main(argv=None):
     import time
 
     ap = argparse.ArgumentParser(description=_main.__doc__)
-    ap.add_argument("--n", type=int, default=2048)
-    ap.add_argument("--k", type=int, default=1024)
-    ap.add_argument("--crc", default="32-GZIP")
+    ap.add_argument("code", nargs="?", default="2048:1024:32-GZIP", help="N:K[:CRC]")
     ap.add_argument("--design", default="ga@2.5", help="ga@<dB> or bhat@<erasure>")
     ap.add_argument("--decoder", default="ca_sscl")
-    ap.add_argument("--l", type=int, default=8)
+    ap.add_argument("--list-size", type=int, default=8)  # (not --l: torchrun abbreviations)
     ap.add_argument("--precision", default="f32")
     ap.add_argument("--ebn0", type=float, nargs=3, default=[1.0, 4.0, 0.5])
     ap.add_argument("--frames", type=int, default=1 << 20)
@@ -206,27 +207,36 @@ def _main(argv=None):
         import torch
         import torch.distributed as dist
 
+        ndev = torch.cuda.device_count()
+        shared = world > ndev  # more ranks than GPUs: exercising the path only
+        local = local % ndev
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        red_dev = "cpu" if shared else f"cuda:{local}"
 
         def reduce(v):
-            t = torch.tensor(v, dtype=torch.int64, device=f"cuda:{local}")
+            t = torch.tensor(v, dtype=torch.int64, device=red_dev)
             dist.all_reduce(t)
             return t.tolist()
+    parts = a.code.split(":", 2)
+    a.n, a.k, a.crc = int(parts[0]), int(parts[1]), (parts[2] if len(parts) > 2 else "")
     w = Pm.CrcSpec.parse(a.crc).width if a.crc else 0
     kind, val = a.design.split("@")
     fz = (Pm.construct_frozen_ga(a.n, a.k + w, float(val), a.k / a.n) if kind == "ga"
           else Pm.construct_frozen(a.n, a.k + w, float(val)))
     code = Pm.make_code(a.n, a.k, fz, a.crc or None)
     pr = PruningConfig(rep_max=8) if a.precision == "i8" else PruningConfig()
-    cfg = SimConfig(code, a.decoder, a.l, a.precision, pruning=pr, ebn0_min=a.ebn0[0],
+    cfg = SimConfig(code, a.decoder, a.list_size, a.precision, pruning=pr, ebn0_min=a.ebn0[0],
                     ebn0_max=a.ebn0[1], ebn0_step=a.ebn0[2], max_frames=a.frames, max_fe=a.max_fe,
                     seed=a.seed, channel=a.channel, device=local)
     t0 = time.time()
     stats = run_montecarlo(cfg, rank, world, reduce)
     if rank == 0:
         meta = [f"code: N={a.n} K={a.k} crc={a.crc} frozen={a.design}",
-                f"decoder: {a.decoder} L={a.l} {a.precision}", f"seed: {a.seed}",
+                f"decoder: {a.decoder} L={a.list_size} {a.precision}", f"seed: {a.seed}",
                 f"channel: {a.channel}", f"gpus: {world}", f"wall_s: {time.time() - t0:.1f}"]
         write_report(sys.stdout, a.format, meta, stats)
 

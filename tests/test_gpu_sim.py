@@ -104,3 +104,30 @@ def P(native):
     import paper_1710_08314_b200 as P
 
     return P
+
+
+def test_sweep_cli_two_ranks_equals_one(tmp_path):
+    """`python -m paper_1710_08314_b200.sim` under torchrun: each rank takes
+    its frame range and the counters are all-reduced; the report equals the
+    single-process one (gloo when the ranks share one GPU)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    args = ["-m", "paper_1710_08314_b200.sim", "256:128:16-CCITT", "--design", "bhat@0.5", "--decoder", "ca_sscl", "--list-size", "4", "--ebn0", "1.0", "2.0", "0.5",
+            "--frames", "24576"]
+    one = subprocess.run([sys.executable, *args], cwd=root, capture_output=True, text=True,
+                         timeout=600)
+    assert one.returncode == 0, one.stderr[-2000:]
+    two = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes", "1",
+                          "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
+                          "--master-port", "29571", *args], cwd=root, capture_output=True,
+                         text=True, timeout=600)
+    assert two.returncode == 0, two.stderr[-2000:]
+
+    def counts(text):
+        rows = [r.split(",") for r in text.splitlines() if r and r[0].isdigit()]
+        return [(r[0], r[1], r[2], r[3], r[9]) for r in rows]  # all but the timing columns
+
+    assert counts(one.stdout) == counts(two.stdout) and len(counts(one.stdout)) == 3
