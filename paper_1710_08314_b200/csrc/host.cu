@@ -803,50 +803,71 @@ int pl_crc_parse(const char* text, pl_crc* out) {
     }
 }
 
+namespace {
+// A text file read whole and split at whitespace, as operator>> reads it.
+struct TextTokens {
+    std::string text;
+    size_t pos = 0;
+    bool load(const char* path) {
+        FILE* fp = std::fopen(path, "r");
+        if (!fp) return false;
+        char buf[4096];
+        size_t got;
+        while ((got = std::fread(buf, 1, sizeof buf, fp)) > 0) text.append(buf, got);
+        std::fclose(fp);
+        return true;
+    }
+    bool next(std::string& out) {
+        while (pos < text.size() && std::isspace(static_cast<unsigned char>(text[pos]))) ++pos;
+        const size_t b = pos;
+        while (pos < text.size() && !std::isspace(static_cast<unsigned char>(text[pos]))) ++pos;
+        out = text.substr(b, pos - b);
+        return !out.empty();
+    }
+    bool next_int(int32_t& v) {
+        std::string t;
+        if (!next(t)) return false;
+        char* end = nullptr;
+        const long x = std::strtol(t.c_str(), &end, 10);
+        if (*end || x < INT32_MIN || x > INT32_MAX) return false;
+        v = int32_t(x);
+        return true;
+    }
+};
+
+// One line of n characters from `alphabet`; value = index in the alphabet.
+// Messages as the reference's ParseError (code.cpp:164-221).
+int read_pattern(TextTokens& tt, const std::string& what, const std::string& path, int32_t n,
+                 const char* alphabet, const char* want, const char* count_word, std::string& out) {
+    if (!tt.next(out))
+        return fail(nullptr, PL_ERR_PARSE, what + " file '" + path + "': missing " + count_word + " line");
+    if (out.size() != size_t(n))
+        return fail(nullptr, PL_ERR_PARSE,
+                    what + " file '" + path + "': " + count_word + " has " + std::to_string(out.size()) +
+                        " characters, header says N = " + std::to_string(n));
+    for (size_t i = 0; i < out.size(); ++i)
+        if (!std::strchr(alphabet, out[i]))
+            return fail(nullptr, PL_ERR_PARSE,
+                        what + " file '" + path + "': " + count_word + " character '" +
+                            std::string(1, out[i]) + "' at position " + std::to_string(i) + " (want " +
+                            want + ")");
+    return PL_OK;
+}
+} // namespace
+
 // Frozen-set files in the reference format (code.cpp:164-194): "N K" then
 // one line of N characters, '1' = frozen.  Messages as the reference's
 // ParseError / IoError.
 int pl_frozen_file_load(const char* path, int32_t* n, int32_t* k, uint8_t* frozen_out, int32_t cap) {
     if (!path || !n || !k) return fail(nullptr, PL_ERR_ARG, "null argument");
     const std::string p(path);
-    FILE* fp = std::fopen(path, "r");
-    if (!fp) return fail(nullptr, PL_ERR_IO, "cannot open '" + p + "' for reading");
-    std::string text;
-    char buf[4096];
-    size_t got;
-    while ((got = std::fread(buf, 1, sizeof buf, fp)) > 0) text.append(buf, got);
-    std::fclose(fp);
-    // whitespace-separated tokens, as operator>> reads them
-    size_t pos = 0;
-    auto token = [&](std::string& out) {
-        while (pos < text.size() && std::isspace(static_cast<unsigned char>(text[pos]))) ++pos;
-        const size_t b = pos;
-        while (pos < text.size() && !std::isspace(static_cast<unsigned char>(text[pos]))) ++pos;
-        out = text.substr(b, pos - b);
-        return !out.empty();
-    };
-    auto as_int = [](const std::string& t, int32_t& v) {
-        if (t.empty()) return false;
-        char* end = nullptr;
-        const long x = std::strtol(t.c_str(), &end, 10);
-        if (*end || x < INT32_MIN || x > INT32_MAX) return false;
-        v = int32_t(x);
-        return true;
-    };
-    std::string tn, tk, mask;
+    TextTokens tt;
+    if (!tt.load(path)) return fail(nullptr, PL_ERR_IO, "cannot open '" + p + "' for reading");
     int32_t vn = 0, vk = 0;
-    if (!token(tn) || !as_int(tn, vn) || !token(tk) || !as_int(tk, vk))
+    if (!tt.next_int(vn) || !tt.next_int(vk))
         return fail(nullptr, PL_ERR_PARSE, "frozen file '" + p + "': header must be 'N K'");
-    if (!token(mask)) return fail(nullptr, PL_ERR_PARSE, "frozen file '" + p + "': missing mask line");
-    if (mask.size() != size_t(vn))
-        return fail(nullptr, PL_ERR_PARSE,
-                    "frozen file '" + p + "': mask has " + std::to_string(mask.size()) +
-                        " characters, header says N = " + std::to_string(vn));
-    for (size_t i = 0; i < mask.size(); ++i)
-        if (mask[i] != '0' && mask[i] != '1')
-            return fail(nullptr, PL_ERR_PARSE,
-                        "frozen file '" + p + "': mask character '" + std::string(1, mask[i]) +
-                            "' at position " + std::to_string(i) + " (want 0 or 1)");
+    std::string mask;
+    if (const int rc = read_pattern(tt, "frozen", p, vn, "01", "0 or 1", "mask", mask)) return rc;
     *n = vn;
     *k = vk;
     if (frozen_out) {
@@ -861,42 +882,17 @@ int pl_frozen_file_load(const char* path, int32_t* n, int32_t* k, uint8_t* froze
 int pl_puncture_file_load(const char* path, int32_t* n, uint8_t* use_out, int32_t cap) {
     if (!path || !n) return fail(nullptr, PL_ERR_ARG, "null argument");
     const std::string p(path);
-    FILE* fp = std::fopen(path, "r");
-    if (!fp) return fail(nullptr, PL_ERR_IO, "cannot open '" + p + "' for reading");
-    std::string text;
-    char buf[4096];
-    size_t got;
-    while ((got = std::fread(buf, 1, sizeof buf, fp)) > 0) text.append(buf, got);
-    std::fclose(fp);
-    size_t pos = 0;
-    auto token = [&](std::string& out) {
-        while (pos < text.size() && std::isspace(static_cast<unsigned char>(text[pos]))) ++pos;
-        const size_t b = pos;
-        while (pos < text.size() && !std::isspace(static_cast<unsigned char>(text[pos]))) ++pos;
-        out = text.substr(b, pos - b);
-        return !out.empty();
-    };
-    std::string tn, pat;
-    char* end = nullptr;
-    long vn = 0;
-    if (!token(tn) || (vn = std::strtol(tn.c_str(), &end, 10), *end) || vn < INT32_MIN || vn > INT32_MAX)
-        return fail(nullptr, PL_ERR_PARSE, "puncture file '" + p + "': header must be 'N'");
-    if (!token(pat)) return fail(nullptr, PL_ERR_PARSE, "puncture file '" + p + "': missing pattern line");
-    if (pat.size() != size_t(vn))
-        return fail(nullptr, PL_ERR_PARSE,
-                    "puncture file '" + p + "': pattern has " + std::to_string(pat.size()) +
-                        " characters, header says N = " + std::to_string(vn));
-    for (size_t i = 0; i < pat.size(); ++i)
-        if (pat[i] != 'T' && pat[i] != 'P' && pat[i] != 'S')
-            return fail(nullptr, PL_ERR_PARSE,
-                        "puncture file '" + p + "': pattern character '" + std::string(1, pat[i]) +
-                            "' at position " + std::to_string(i) + " (want T, P or S)");
-    *n = int32_t(vn);
+    TextTokens tt;
+    if (!tt.load(path)) return fail(nullptr, PL_ERR_IO, "cannot open '" + p + "' for reading");
+    int32_t vn = 0;
+    if (!tt.next_int(vn)) return fail(nullptr, PL_ERR_PARSE, "puncture file '" + p + "': header must be 'N'");
+    std::string pat;
+    if (const int rc = read_pattern(tt, "puncture", p, vn, "TPS", "T, P or S", "pattern", pat)) return rc;
+    *n = vn;
     if (use_out) {
         if (cap < vn) return fail(nullptr, PL_ERR_ARG, "pattern buffer too small");
-        for (long i = 0; i < vn; ++i)
-            use_out[i] = pat[size_t(i)] == 'T' ? PL_USE_TRANSMITTED
-                         : pat[size_t(i)] == 'P' ? PL_USE_PUNCTURED : PL_USE_SHORTENED;
+        for (int32_t i = 0; i < vn; ++i)
+            use_out[i] = uint8_t(std::strchr("TPS", pat[size_t(i)]) - "TPS"); // PL_USE_* order
     }
     return PL_OK;
 }
