@@ -43,7 +43,7 @@ class Workload:
             "decoder": self.kind, "L": self.l, "llr": self.precision,
             "pruning": pruning_string(self.pruning), "ebn0_db": self.ebn0_db,
             "frames_per_gpu": self.frames, "frozen": f"{self.construction}@{self.design_db}dB",
-            **({"quant_scale": self.scale} if self.precision == "i8" else {}),
+            **({"quant_scale": self.scale} if self.precision != "f32" else {}),
         }
 
 
@@ -153,8 +153,14 @@ WORKLOADS = {
                          P.PruningConfig(), 4.5, 1048576),
     # configs[3]: mixed MCS, CA-SCL L=8, float, 3 dB, 524 288 frames
     "cfg3": MixedWorkload(),
+    # the paper's fixed-point FA-SSCL points: same code as
+    # configs[2], L=32 at 4.5 dB, int8 (x4, REP_8-) and int16 (x64)
+    "fa_i8_4.5": Workload("fa_scl_L32_i8@4.5dB", 2048, 1723, "32-GZIP", "fa_sscl", 32, "i8",
+                          P.PruningConfig(rep_max=8), 4.5, 1048576, scale=4.0),
+    "fa_i16_4.5": Workload("fa_scl_L32_i16@4.5dB", 2048, 1723, "32-GZIP", "fa_sscl", 32, "i16",
+                           P.PruningConfig(), 4.5, 1048576),
     # configs[4]: N=2048, K=1024 + CRC-32, CA-SCL L in {8,16,32}; one SNR
-    # point per bench step (the 1..4 dB sweep runs through sweep.py)
+    # point per bench step (the 1..4 dB sweep: python -m paper_1710_08314_b200.sim)
     "cfg4_L8": Workload("cfg4_ca_scl_L8_f32@2.5dB", 2048, 1024, "32-GZIP", "ca_sscl", 8, "f32",
                         P.PruningConfig(), 2.5, 65536, design_db=2.5),
     "cfg4_L16": Workload("cfg4_ca_scl_L16_f32@2.5dB", 2048, 1024, "32-GZIP", "ca_sscl", 16, "f32",
