@@ -346,7 +346,13 @@ def main():
         try:
             from oracle import oracle as O
             nthr = os.cpu_count() or 1
-            S = min(args.cpu_sample, F)
+            # bounded sample: a probe of cpu_sample/4 frames sets the size so
+            # the timed run is ~20 core-seconds of reference decoding
+            S = min(max(args.cpu_sample // 4, 256), F)
+            _, dt0 = reference_decode(O, codes, cid[:S] if cid is not None else None,
+                                      llr_np[:S], wl, nthr)
+            S = int(min(F, max(args.cpu_sample, S * 20.0 / max(dt0 * nthr, 1e-6))))
+            S = max(256, S - S % 256)
             r, dt = reference_decode(O, codes, cid[:S] if cid is not None else None,
                                      llr_np[:S], wl, nthr)
             cpu_gbps = float(ks[:S].sum()) / dt / 1e9

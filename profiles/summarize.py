@@ -61,6 +61,34 @@ def main():
         for w in want:
             if w in names:
                 print(f"- `{w}` = {vals[names.index(w)]} {raw[1][names.index(w)]}")
+        # issue / pipe utilisation and the stall breakdown (cycles per issued
+        # instruction by reason): the issue-bound evidence
+        print("\n## issue, pipes, stalls\n")
+        print("| metric | value |\n|---|---|")
+        for w in ["smsp__issue_active.avg.pct_of_peak_sustained_active",
+                  "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+                  "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+                  "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+                  "sm__inst_executed_pipe_adu.avg.pct_of_peak_sustained_active",
+                  "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+                  "sm__inst_executed_pipe_cbu.avg.pct_of_peak_sustained_active"]:
+            if w in names:
+                print(f"| `{w}` | {vals[names.index(w)]} % |")
+        st = [(n[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")],
+               float(vals[i] or 0)) for i, n in enumerate(names)
+              if n.startswith("smsp__average_warps_issue_stalled_") and n.endswith("_per_issue_active.ratio")]
+        st = [x for x in sorted(st, key=lambda x: -x[1]) if x[1] >= 0.05]
+        if st:
+            print("\nstall cycles per issued instruction: " +
+                  ", ".join(f"{n} {v:.2f}" for n, v in st))
+    mix = list(csv.reader(io.StringIO(ncu(["-i", a.rep, "--page", "raw", "--csv",
+                                            "--print-metric-instances", "details"]))))
+    if len(mix) > 2 and "sass__inst_executed_per_opcode" in mix[0]:
+        v = mix[2][mix[0].index("sass__inst_executed_per_opcode")]
+        tot = float(v.split()[0])
+        parts = [p.strip().rsplit(":", 1) for p in v[v.index("(") + 1:-1].split(";")]
+        print("\nopcode mix (warp-level, % of executed): " +
+              ", ".join(f"{o} {float(c) / tot * 100:.1f}" for o, c in parts[:16]))
     src = list(csv.reader(io.StringIO(ncu(["-i", a.rep, "--page", "source", "--csv",
                                             "--print-source", "cuda,sass"]))))
     agg = collections.defaultdict(lambda: [0.0, 0.0])
