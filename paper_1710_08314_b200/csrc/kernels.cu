@@ -85,14 +85,11 @@ struct Sub {
         const uint32_t hi = __shfl_sync(FULL, uint32_t(v >> 32), src, SW);
         return (uint64_t(hi) << 32) | lo;
     }
+    // OR of slot masks (v < 2^SW): every sub-warp's mask in its own SW-bit
+    // field of one warp-wide redux
     __device__ __forceinline__ unsigned red_or(unsigned v) const {
-        if constexpr (SW == 32) {
-            return __reduce_or_sync(FULL, v);
-        } else {
-#pragma unroll
-            for (int o = SW / 2; o > 0; o >>= 1) v |= __shfl_xor_sync(FULL, v, o);
-            return v;
-        }
+        if constexpr (SW == 32) return __reduce_or_sync(FULL, v);
+        else return (__reduce_or_sync(FULL, v << base) >> base) & kMask;
     }
     __device__ __forceinline__ unsigned red_min(unsigned v) const {
         if constexpr (SW == 32) {
@@ -259,52 +256,84 @@ __device__ __forceinline__ float mfrom<float>(uint32_t b) { return __uint_as_flo
 template <>
 __device__ __forceinline__ int mfrom<int>(uint32_t b) { return int(b); }
 
-// ---- sub-warp bitonic sorts (ascending) ----------------------------------
-// W keys, one per lane, lanes [0, W) of the sub-warp sorted (W <= SW).
+// ---- sub-warp sorting networks (ascending) -------------------------------
+// Every network here uses ascending comparators only: a bitonic merge whose
+// first stage compares mirrored lanes (lane ^ (size-1)) merges two ASCENDING
+// runs, so runs that are already sorted need no direction flips and their
+// phases are skipped.  The candidates of one path are emitted in ascending
+// (metric, index) order for R1, SPC and REP nodes (their penalties are
+// 0 <= a1 <= a2 <= a1+a2 resp. pen_w <= pen_w+|s|, list_decoder.hpp:254-333),
+// which makes each path's 2 or 4 consecutive lanes a sorted run.
+// compare-exchange with lane ^ m: lanes with `bit` clear keep the smaller key
+template <typename K>
+__device__ __forceinline__ K cex(K key, int m, int lane, int bit) {
+    const K o = shfl_xor_k(key, m);
+    return (lane & bit) == 0 ? kmin(key, o) : kmax(key, o);
+}
+
+// W keys, one per lane, made of sorted runs of 2^lgrun lanes (lgrun uniform;
+// 0 = unsorted): lanes [0, W) of each aligned W-lane group sorted ascending.
 template <typename K, int W>
-__device__ __forceinline__ K bitonic_lanes(K key, int lane) {
+__device__ __forceinline__ K sort_runs(K key, int lane, int lgrun) {
 #pragma unroll
     for (int size = 2; size <= W; size <<= 1) {
+        if (size <= (1 << lgrun)) continue;
+        key = cex(key, size - 1, lane, size >> 1);
 #pragma unroll
-        for (int j = size >> 1; j > 0; j >>= 1) {
-            const K o = shfl_xor_k(key, j);
-            const bool asc = (lane & size) == 0;
-            const bool lower = (lane & j) == 0;
-            key = (lower == asc) ? kmin(key, o) : kmax(key, o);
-        }
+        for (int j = size >> 2; j > 0; j >>= 1) key = cex(key, j, lane, j);
     }
     return key;
 }
 
+// The W/2 smallest of 2W keys (two registers, sorted runs of 2^lgrun),
+// ascending in lanes [0, W/2): sort W/2-lane runs in both registers, keep the
+// W/2 smallest of each pair of runs (min against the other register's run
+// reversed: a bitonic sequence), sort those, then the same step across the
+// two halves.  14 compare stages at W = 16 from runs of 4, vs 25 for two full
+// sorts and a merge.
+template <typename K, int W>
+__device__ __forceinline__ K top_half2(K a, K b, int lane, int lgrun) {
+    // both registers through the same stages (one uniform branch per phase,
+    // two independent chains)
+#pragma unroll
+    for (int size = 2; size <= W / 2; size <<= 1) {
+        if (size <= (1 << lgrun)) continue;
+        a = cex(a, size - 1, lane, size >> 1);
+        b = cex(b, size - 1, lane, size >> 1);
+#pragma unroll
+        for (int j = size >> 2; j > 0; j >>= 1) {
+            a = cex(a, j, lane, j);
+            b = cex(b, j, lane, j);
+        }
+    }
+    K c = kmin(a, shfl_xor_k(b, W / 2 - 1));
+#pragma unroll
+    for (int j = W / 4; j > 0; j >>= 1) c = cex(c, j, lane, j);
+    c = cex(c, W - 1, lane, W / 2);
+#pragma unroll
+    for (int j = W / 4; j > 0; j >>= 1) c = cex(c, j, lane, j);
+    return c;
+}
+
 // The W smallest of two ascending W-key lane sequences, ascending: the
 // element-wise min of a and reversed b is a bitonic sequence holding exactly
-// those keys; one bitonic merge sorts it.
+// those keys; half-cleaners sort it.
 template <typename K, int W>
 __device__ __forceinline__ K merge_top(K a, K b, int lane) {
-    K br;
-    if constexpr (sizeof(K) == 8) {
-        br = (uint64_t(__shfl_sync(FULL, uint32_t(b >> 32), W - 1 - lane, W)) << 32) |
-             __shfl_sync(FULL, uint32_t(b), W - 1 - lane, W);
-    } else {
-        br = __shfl_sync(FULL, b, W - 1 - lane, W);
-    }
-    K c = kmin(a, br);
+    K c = kmin(a, shfl_xor_k(b, W - 1));
 #pragma unroll
-    for (int j = W / 2; j > 0; j >>= 1) {
-        const K o = shfl_xor_k(c, j);
-        c = (lane & j) == 0 ? kmin(c, o) : kmax(c, o);
-    }
+    for (int j = W / 2; j > 0; j >>= 1) c = cex(c, j, lane, j);
     return c;
 }
 
 // The W smallest of W*C keys (register k of each lane), ascending in
 // register 0: sort each register across the lanes, then merge pairwise.
-template <typename K, int C, int W>
 // Registers from nreg on hold only kKeyMax and are skipped (uniform).
-__device__ __forceinline__ void top_regs(K (&key)[C], int lane, int nreg) {
+template <typename K, int C, int W>
+__device__ __forceinline__ void top_regs(K (&key)[C], int lane, int nreg, int lgrun) {
 #pragma unroll
     for (int k = 0; k < C; ++k)
-        if (k < nreg) key[k] = bitonic_lanes<K, W>(key[k], lane);
+        if (k < nreg) key[k] = sort_runs<K, W>(key[k], lane, lgrun);
 #pragma unroll
     for (int w = 1; w < C; w <<= 1)
 #pragma unroll
@@ -645,11 +674,14 @@ __device__ void rep_fold(Ctx<R, SW>& cx, int d, int m, int na) {
 enum ApplyKind { AK_BIT = 0, AK_BCAST = 1, AK_FLIPS = 2 };
 
 // fork_apply (list_decoder.hpp:339-387) for ncand candidates held as
-// candidate i = lane + SW*k in register k.  aux = a | b << 16 (int16 each).
+// candidate i = lane + SW*k in register k; candidate i belongs to the path of
+// rank i >> lgb and is that path's candidate number i & (2^lgb - 1) at a node
+// of type `code` (its decision is decoded from the node statistics after the
+// ranking, so only the metrics travel through the sort).
 template <typename R, int SW, int CPL, int MAXW>
 __device__ void fork_apply(Ctx<R, SW>& cx, const typename Arith<R>::M (&cm)[CPL],
                            const int (&csrc)[CPL], const int (&caux)[CPL], int ncand,
-                           int kind, int lb, int m) {
+                           int code, int lgb, int lb, int m, int lgrun) {
     using A = Arith<R>;
     using M = typename A::M;
     using K = typename A::Key;
@@ -664,27 +696,59 @@ __device__ void fork_apply(Ctx<R, SW>& cx, const typename Arith<R>::M (&cm)[CPL]
     }
     if constexpr (CPL == 1) {
         // two network widths per kernel: MAXW = min(SW, 4L) and MAXW/2
-        if (MAXW > 4 && ncand <= MAXW / 2) key[0] = bitonic_lanes<K, (MAXW > 4 ? MAXW / 2 : 4)>(key[0], lane);
-        else key[0] = bitonic_lanes<K, MAXW>(key[0], lane);
+        if (MAXW > 4 && ncand <= MAXW / 2) key[0] = sort_runs<K, (MAXW > 4 ? MAXW / 2 : 4)>(key[0], lane, lgrun);
+        else key[0] = sort_runs<K, MAXW>(key[0], lane, lgrun);
+    } else if constexpr (CPL == 2) {
+        // 4L <= 2 SW: keep = L <= SW/2, so the best SW/2 suffice
+        if (ncand > SW) key[0] = top_half2<K, SW>(key[0], key[1], lane, lgrun);
+        else key[0] = sort_runs<K, SW>(key[0], lane, lgrun);
     } else {
         // only the best keep <= SW are needed, in order
-        top_regs<K, CPL, SW>(key, lane, (ncand + SW - 1) / SW);
+        top_regs<K, CPL, SW>(key, lane, (ncand + SW - 1) / SW, lgrun);
     }
     const int keep = min(cx.l, ncand);
     const bool kept = lane < keep;
     const int ci = kept ? A::key_idx(key[0]) : 0;
     const M cmet = A::key_val(key[0]);
-    int src = 0, aux = 0;
-#pragma unroll
-    for (int k = 0; k < CPL; ++k) {
-        const int s = cx.sw.shfl(csrc[k], ci & (SW - 1));
-        const int a = cx.sw.shfl(caux[k], ci & (SW - 1));
-        if (ci / SW == k) {
-            src = s;
-            aux = a;
+    // the ranked candidate's source path and decision (list_decoder.hpp:
+    // 240-333): ca = the bit (info leaf, REP) or the first flip, cb = the
+    // second flip (R1 / SPC; -1 = none)
+    int src, ca, cb = -1;
+    if constexpr (A::kFixed) {
+        // issue-bound fixed-point kernels: decoded from the node statistics
+        const int cr = ci >> lgb, j = ci & ((1 << lgb) - 1);
+        src = cx.fx->alive_list[cr];
+        if (code == OP_INFO) {
+            ca = j;
+        } else if (code == OP_REP) {
+            ca = cx.fx->st_w[cr] ^ j;
+        } else {
+            // R1: none, i1, i2, i1&i2.  SPC: broken parity -> i1, i2;
+            // intact -> none, i1&i2.
+            const int jj = code == OP_R1 ? j : (cx.fx->st_w[cr] ? j + 1 : j * 3);
+            const int i1 = cx.fx->st_i1[cr], i2 = cx.fx->st_i2[cr];
+            ca = jj == 0 ? -1 : jj == 2 ? i2 : i1;
+            if (jj == 3) cb = i2;
         }
+    } else {
+        // latency-bound float kernels: emitted before the ranking (off its
+        // critical path), fetched from the emitting lane
+        int aux = 0;
+        src = 0;
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) {
+            const int sv = cx.sw.shfl(csrc[k], ci & (SW - 1));
+            const int av = cx.sw.shfl(caux[k], ci & (SW - 1));
+            if (ci / SW == k) {
+                src = sv;
+                aux = av;
+            }
+        }
+        ca = int(int16_t(aux & 0xffff));
+        cb = aux >> 16;
     }
     if (!kept) src = 64 + lane;
+    const int kind = code == OP_INFO ? AK_BIT : code == OP_REP ? AK_BCAST : AK_FLIPS;
     // 2. slot assignment: the first use of a slot stays in place, the others
     //    take the free slots in ascending order, in rank order
     const unsigned same = cx.sw.match(src);
@@ -729,7 +793,6 @@ __device__ void fork_apply(Ctx<R, SW>& cx, const typename Arith<R>::M (&cm)[CPL]
         __syncwarp();
     }
     // 4. apply decisions (list_decoder.hpp:425-445)
-    const int ca = int(int16_t(aux & 0xffff)), cb = aux >> 16;
     if (kind == AK_BIT) {
         if (kept) span_fill_lane(cx.row(tgt), lb, 1, ca);
     } else if (kind == AK_BCAST) {
@@ -1132,37 +1195,56 @@ __device__ void list_fork_node(Ctx<R, SW>& cx, int code, int d, int m, int lb, i
     }
     const int lgb = code == OP_R1 ? 2 : 1; // candidates per path: 4 or 2
     M cm[C];
-    int cs[C], cax[C];
+    int cs[C], cax[C]; // source slot, decision (a | b << 16): float kernels only
+    if constexpr (A::kFixed) {
+        // metrics only (fork_apply decodes the kept candidates' decisions)
 #pragma unroll
-    for (int k = 0; k < C; ++k) {
-        const int i = cx.lane + SW * k, r = min(i >> lgb, na - 1), j = i & ((1 << lgb) - 1);
-        const int p = cx.fx->alive_list[r];
-        const M base = cx.sw.shfl(cx.metric, p);
-        cs[k] = p;
-        if (code == OP_INFO) { // list_decoder.hpp:240-252
-            const M v = mfrom<M>(cx.fx->st_a1[r]);
-            cm[k] = A::sat(base, (j == 0) == (v < M(0)) ? A::mag(v) : M(0));
-            cax[k] = pack_aux(j, -1);
-        } else if (code == OP_REP) { // :276-305, preferred bit first
-            const int w = cx.fx->st_w[r];
-            const M pen_w = mfrom<M>(cx.fx->st_a2[r]);
-            cm[k] = j == 0 ? A::sat(base, pen_w)
-                           : A::sat(base, A::sat(pen_w, A::mag(mfrom<M>(cx.fx->st_a1[r]))));
-            cax[k] = pack_aux(w ^ j, -1);
-        } else {
-            const int i1 = cx.fx->st_i1[r], i2 = cx.fx->st_i2[r];
-            const M a1 = mfrom<M>(cx.fx->st_a1[r]), a2 = mfrom<M>(cx.fx->st_a2[r]);
-            // R1 (:254-274): none, i1, i2, i1&i2.  SPC (:307-333): broken
-            // parity -> i1, i2; intact -> none, i1&i2.
-            const int jj = code == OP_R1 ? j : (cx.fx->st_w[r] ? j + 1 : j * 3);
-            cm[k] = jj == 0 ? base : jj == 1 ? A::sat(base, a1) : jj == 2 ? A::sat(base, a2)
-                                                                 : A::sat(base, A::sat(a1, a2));
-            cax[k] = jj == 0 ? pack_aux(-1, -1) : jj == 1 ? pack_aux(i1, -1)
-                                                : jj == 2 ? pack_aux(i2, -1) : pack_aux(i1, i2);
+        for (int k = 0; k < C; ++k) {
+            const int i = cx.lane + SW * k, r = min(i >> lgb, na - 1), j = i & ((1 << lgb) - 1);
+            const M base = cx.sw.shfl(cx.metric, int(cx.fx->alive_list[r]));
+            const M a1 = mfrom<M>(cx.fx->st_a1[r]);
+            if (code == OP_INFO) { // list_decoder.hpp:240-252
+                cm[k] = A::sat(base, (j == 0) == (a1 < M(0)) ? A::mag(a1) : M(0));
+            } else if (code == OP_REP) { // :276-305, preferred bit first
+                const M pen_w = mfrom<M>(cx.fx->st_a2[r]);
+                cm[k] = A::sat(base, j == 0 ? pen_w : A::sat(pen_w, A::mag(a1)));
+            } else { // R1 :254-274, SPC :307-333 (jj as in fork_apply)
+                const M a2 = mfrom<M>(cx.fx->st_a2[r]);
+                const int jj = code == OP_R1 ? j : (cx.fx->st_w[r] ? j + 1 : j * 3);
+                cm[k] = jj == 0 ? base : A::sat(base, jj == 1 ? a1 : jj == 2 ? a2 : A::sat(a1, a2));
+            }
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < C; ++k) {
+            const int i = cx.lane + SW * k, r = min(i >> lgb, na - 1), j = i & ((1 << lgb) - 1);
+            const int p = cx.fx->alive_list[r];
+            const M base = cx.sw.shfl(cx.metric, p);
+            cs[k] = p;
+            if (code == OP_INFO) { // list_decoder.hpp:240-252
+                const M v = mfrom<M>(cx.fx->st_a1[r]);
+                cm[k] = A::sat(base, (j == 0) == (v < M(0)) ? A::mag(v) : M(0));
+                cax[k] = pack_aux(j, -1);
+            } else if (code == OP_REP) { // :276-305, preferred bit first
+                const int w = cx.fx->st_w[r];
+                const M pen_w = mfrom<M>(cx.fx->st_a2[r]);
+                cm[k] = j == 0 ? A::sat(base, pen_w)
+                               : A::sat(base, A::sat(pen_w, A::mag(mfrom<M>(cx.fx->st_a1[r]))));
+                cax[k] = pack_aux(w ^ j, -1);
+            } else {
+                const int i1 = cx.fx->st_i1[r], i2 = cx.fx->st_i2[r];
+                const M a1 = mfrom<M>(cx.fx->st_a1[r]), a2 = mfrom<M>(cx.fx->st_a2[r]);
+                const int jj = code == OP_R1 ? j : (cx.fx->st_w[r] ? j + 1 : j * 3);
+                cm[k] = jj == 0 ? base : jj == 1 ? A::sat(base, a1) : jj == 2 ? A::sat(base, a2)
+                                                                     : A::sat(base, A::sat(a1, a2));
+                cax[k] = jj == 0 ? pack_aux(-1, -1) : jj == 1 ? pack_aux(i1, -1)
+                                                    : jj == 2 ? pack_aux(i2, -1) : pack_aux(i1, i2);
+            }
         }
     }
-    const int kind = code == OP_INFO ? AK_BIT : code == OP_REP ? AK_BCAST : AK_FLIPS;
-    fork_apply<R, SW, C, MAXW>(cx, cm, cs, cax, na << lgb, kind, lb, code == OP_INFO ? 1 : m);
+    // candidates of one path form a sorted run except at information leaves
+    fork_apply<R, SW, C, MAXW>(cx, cm, cs, cax, na << lgb, code, lgb, lb, code == OP_INFO ? 1 : m,
+                               code == OP_INFO ? 0 : lgb);
     cx.normalize();
 }
 
