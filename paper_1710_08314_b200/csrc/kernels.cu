@@ -815,6 +815,12 @@ __device__ void fork_apply(Ctx<R, SW>& cx, const typename Arith<R>::M (&cm)[CPL]
     const unsigned nal = cx.sw.red_or(kept ? (1u << tgt) : 0u);
     __syncwarp();
     if ((nal >> lane) & 1u) cx.metric = mfrom<M>(cx.fx->met_s[lane]);
+    if constexpr (A::kFixed) {
+        // normalisation (list_decoder.hpp:447-455): the smallest alive metric
+        // is the rank-0 candidate's, no reduction needed
+        const M mn = cx.sw.shfl(cmet, 0);
+        if ((nal >> lane) & 1u) cx.metric -= mn;
+    }
     cx.set_alive(nal);
 }
 
@@ -917,7 +923,40 @@ __device__ void r1spc_stats(Ctx<R, SW>& cx, int d, int m, int lb, int na) {
     K k1 = A::kKeyMax, k2 = A::kKeyMax;
     uint32_t acc = 0;
     int par = 0;
-    if (ok) {
+    bool swar = false;
+    if constexpr (sizeof(R) == 1) swar = E >= 4 && m <= 512;
+    if (ok && swar) {
+        // int8, four values per word: hard bits from the sign bits, |v| by
+        // VABSDIFF4, the two smallest (|v| << 9 | index) keys per 16-bit lane
+        // by VIMNMX.U16x2 (index < 512: the (value, index) order of
+        // select.hpp:18-68 in 16 bits)
+        uint32_t q1 = FULL, q2 = FULL;
+        #pragma unroll 1
+        for (int k = 0; k < E; k += 4) {
+            const uint32_t w = *reinterpret_cast<const uint32_t*>(L + k);
+            acc |= ((((w >> 7) & 0x01010101u) * 0x01020408u) >> 24) << (k & 31);
+            const uint32_t a4 = __vabsdiffu4(w ^ 0x80808080u, 0x80808080u);
+            const uint32_t ix = uint32_t(i0 + k) * 0x00010001u + 0x00010000u;
+            const uint32_t ka = prmt(a4, 0, 0x4140) * 512u + ix;
+            const uint32_t kb = prmt(a4, 0, 0x4342) * 512u + ix + 0x00020002u;
+            uint32_t n1 = __vminu2(q1, ka);
+            q2 = __vminu2(q2, __vmaxu2(q1, ka));
+            q1 = n1;
+            n1 = __vminu2(q1, kb);
+            q2 = __vminu2(q2, __vmaxu2(q1, kb));
+            q1 = n1;
+            if (((k + 4) & 31) == 0 || k + 4 >= E) {
+                const int pos = base + i0 + (k & ~31);
+                if (acc) atomicOr(span + (pos >> 5), acc << (pos & 31));
+                par ^= __popc(acc);
+                acc = 0;
+            }
+        }
+        const uint32_t x = q1 & 0xffffu, y = q1 >> 16;
+        const uint32_t e1 = min(x, y), e2 = min(max(x, y), min(q2 & 0xffffu, q2 >> 16));
+        k1 = K(((e1 >> 9) << 16) | (e1 & 511u));
+        k2 = K(((e2 >> 9) << 16) | (e2 & 511u));
+    } else if (ok) {
         #pragma unroll 1
         for (int k = 0; k < E; k += 4) {
             M v[4];
@@ -1245,7 +1284,6 @@ __device__ void list_fork_node(Ctx<R, SW>& cx, int code, int d, int m, int lb, i
     // candidates of one path form a sorted run except at information leaves
     fork_apply<R, SW, C, MAXW>(cx, cm, cs, cax, na << lgb, code, lgb, lb, code == OP_INFO ? 1 : m,
                                code == OP_INFO ? 0 : lgb);
-    cx.normalize();
 }
 
 // ---- CRC syndrome of a decided codeword row ----------------

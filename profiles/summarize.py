@@ -12,6 +12,9 @@ import collections
 import csv
 import io
 import subprocess
+import sys
+
+csv.field_size_limit(sys.maxsize)
 
 KEYS = [
     "Duration", "Executed Instructions", "Executed Ipc Active", "Issue Slots Busy",
