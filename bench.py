@@ -106,15 +106,22 @@ def dtype_of(wl):
     return {"i8": "int8", "i16": "int16"}.get(wl.precision, "f32")
 
 
-def measured_traffic(wl, frames):
-    """roofline.traffic: DRAM bytes per launch of this workload's first decode
-    kernel, scaled from one committed ncu capture (profiles/traffic.py)."""
+def kernel_counters(wl, key, frames):
+    """ncu counters of this workload's pass kernel `key` (sc_L1 / list_L<l>),
+    per launch of the default batch (profiles/traffic.py, from one committed
+    ncu capture per workload); counts scale with the batch size.  None if
+    absent."""
     try:
         with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as fh:
             t = json.load(fh)[wl.name]
-        return t["dram_bytes_per_frame"] * frames, t["source"]
+        c = dict(t["kernels"][key])
     except (OSError, KeyError, ValueError):
-        return None, None
+        return None
+    s = frames / t["frames"]
+    for k in ("dram_bytes", "dram_read_bytes", "dram_write_bytes", "warp_inst"):
+        c[k] *= s
+    c["source"] = t["source"]
+    return c
 
 
 def common_config(wl, frames_per_gpu, ws):
@@ -312,7 +319,8 @@ def main():
     lane_achieved = ops_per_frame * n_launch_frames / per_launch_s
     all_kernel_s = sum(sum(v) for v in kernel_ms.values()) / 1e3
 
-    traffic, traffic_src = measured_traffic(wl, n_launch_frames)
+    kc = kernel_counters(wl, f"{dkind}_L{dl}", F)
+    issue_peak = sm_count * 4 * clk  # warp-instructions per second (4 schedulers per SM)
     result = {
         "metric": METRIC,
         "value": value, "unit": "Gb/s", "n_gpus": ws, "steps": args.steps,
@@ -329,13 +337,26 @@ def main():
         "kernel_share_of_step": all_kernel_s / elapsed if ws == 1 else None,
         "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peaks["hbm_gbs"],
                      "unit": "GB/s", "frac": achieved_gbs / peaks["hbm_gbs"],
-                     "traffic": traffic, "traffic_source": traffic_src,
+                     "traffic": kc["dram_bytes"] if kc else None,
+                     "traffic_source": kc["source"] if kc else None,
+                     # measured DRAM bytes of the launch / its live duration
+                     "traffic_frac": (kc["dram_bytes"] / per_launch_s / 1e9 / peaks["hbm_gbs"]) if kc else None,
                      "kernel": f"decode_kernel<{dtype_of(wl)}, {dkind}> L={dl}",
                      "bytes_per_frame": bytes_per_frame, "peak_source": peak_src},
-        "roofline_issue": {"bound": "issue", "achieved": lane_achieved / 1e9,
-                           "peak": lane_peak / 1e9, "unit": "Glane-op/s",
-                           "frac": lane_achieved / lane_peak, "ops_per_frame": ops_per_frame,
-                           "note": "element-ops E(tree,L) per SURVEY 8(d) / (SMs*128 lanes*max clock)"},
+        # the binding roofline of this issue-bound path: warp-instructions
+        # issued per second (ncu's instruction count of the same launch / the
+        # live launch time) against 4 per SM per clock, plus ncu's issue-slot
+        # and ALU-pipe utilisation of that launch
+        "roofline_issue": None if kc is None else {
+            "bound": "issue", "achieved": kc["warp_inst"] / per_launch_s / 1e9,
+            "peak": issue_peak / 1e9, "unit": "Gwarp-inst/s",
+            "frac": kc["warp_inst"] / per_launch_s / issue_peak,
+            "warp_inst_per_frame": kc["warp_inst"] / max(n_launch_frames, 1),
+            "ncu_issue_active_pct": kc["issue_active_pct"], "ncu_alu_pipe_pct": kc["alu_pipe_pct"],
+            "ncu_smem_bank_conflict_pct": 100.0 * kc["smem_bank_conflicts"] / max(kc["smem_wavefronts"], 1),
+            "element_ops_per_frame": ops_per_frame,
+            "element_op_frac": lane_achieved / lane_peak,
+            "source": kc["source"]},
         "clocks": clocks,
         "e2e": {"value": e2e_value, "unit": "Gb/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "steps": e2e_steps, "api": "pl_decode_host"},

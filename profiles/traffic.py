@@ -1,38 +1,75 @@
 #!/usr/bin/env python
-"""DRAM traffic per frame of the first decode kernel of each bench workload,
-from one ncu pass per workload:
+"""Per-kernel counters of each bench workload's passes, from one ncu pass per
+workload (`profiles/collect_ncu.sh`, its CSVs kept in `r01_ncu/`):
+DRAM bytes, warp-instructions, issue-slot and ALU-pipe utilisation, shared
+memory wavefronts / bank conflicts, per launch of the workload's default batch
+(the inputs are seeded, so bench.py's launches decode the same frames).
 
-  ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \\
-      -k regex:decode_kernel -c 1 --csv python bench.py --workload W --steps 1 --warmup 0 --no-cpu
+Writes `r01_traffic.json`, which bench.py reads for `roofline.traffic` and
+`roofline_issue` of the dominant kernel.
 
-(`r01_traffic_ncu.log` holds the grepped lines).  Writes `r01_traffic.json`,
-which bench.py reads for `roofline.traffic` (bytes per launch)."""
-import collections
+  python profiles/traffic.py
+"""
+import csv
+import glob
 import json
 import os
+import re
 import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(HERE))
 from paper_1710_08314_b200.workload import WORKLOADS  # noqa: E402
 
-vals = collections.defaultdict(dict)
-for line in open(os.path.join(HERE, "r01_traffic_ncu.log")):
-    w, metric, v = line.split()
-    vals[w][metric] = float(v.strip('"'))
+
+def kernel_key(name):
+    """bench.py's kernel_ms key of a kernel name: sc_L1 / list_L<l>."""
+    if "sc_lanes_kernel" in name:
+        return "sc_L1"
+    m = re.search(r"decode_kernel<[^,]+, (\d+), (\d+), (\d+)>", name)
+    kv = int(m.group(1))
+    return "sc_L1" if kv == 0 else f"list_L{1 << (kv - 1)}"
+
+
 out = {}
-for w, m in vals.items():
-    frames = WORKLOADS[w].frames
-    dram = m["dram__bytes_read.sum"] + m["dram__bytes_write.sum"]
+for path in sorted(glob.glob(os.path.join(HERE, "r01_ncu", "ncu_*.csv"))):
+    w = os.path.basename(path)[4:-4]
+    rows = [r for r in csv.reader(open(path)) if r]
+    hdr = rows[0]
+    ix = {k: hdr.index(k) for k in ("ID", "Kernel Name", "Metric Name", "Metric Value")}
+    launches = {}
+    for r in rows[1:]:
+        lid = int(r[ix["ID"]])
+        d = launches.setdefault(lid, {"kernel": r[ix["Kernel Name"]]})
+        d[r[ix["Metric Name"]]] = float(r[ix["Metric Value"]].replace(",", ""))
+    kernels = {}
+    for lid in sorted(launches):
+        d = launches[lid]
+        key = kernel_key(d["kernel"])
+        if key in kernels:
+            continue  # first launch of each pass kernel
+        kernels[key] = {
+            "kernel": d["kernel"],
+            "dram_bytes": d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"],
+            "dram_read_bytes": d["dram__bytes_read.sum"],
+            "dram_write_bytes": d["dram__bytes_write.sum"],
+            "warp_inst": d["smsp__inst_executed.sum"],
+            "issue_active_pct": d["smsp__issue_active.avg.pct_of_peak_sustained_active"],
+            "alu_pipe_pct": d["sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"],
+            "warps_active_pct": d["sm__warps_active.avg.pct_of_peak_sustained_active"],
+            "smem_wavefronts": d["l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"],
+            "smem_bank_conflicts": d["l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"],
+            "ncu_duration_ns": d["gpu__time_duration.sum"],
+        }
     out[WORKLOADS[w].name] = {
-        "frames_per_launch": frames,
-        "dram_bytes_per_launch": dram,
-        "dram_bytes_per_frame": dram / frames,
-        "dram_read_bytes": m["dram__bytes_read.sum"],
-        "dram_write_bytes": m["dram__bytes_write.sum"],
-        "source": "profiles/r01_traffic_ncu.log (ncu --metrics dram__bytes_read.sum,"
-                  "dram__bytes_write.sum, first decode_kernel launch)",
+        "frames": WORKLOADS[w].frames,
+        "kernels": kernels,
+        "source": f"profiles/r01_ncu/ncu_{w}.csv (profiles/collect_ncu.sh: ncu --metrics, "
+                  "first launch of each pass kernel of the workload's default batch)",
     }
 json.dump(out, open(os.path.join(HERE, "r01_traffic.json"), "w"), indent=1)
-for k, v in out.items():
-    print(f"{k:32s} {v['dram_bytes_per_frame']:10.0f} B/frame")
+for name, v in out.items():
+    for k, d in v["kernels"].items():
+        print(f"{name:32s} {k:9s} {d['dram_bytes'] / 1e9:8.2f} GB  {d['warp_inst'] / 1e9:7.2f} Ginst  "
+              f"issue {d['issue_active_pct']:5.1f}%  alu {d['alu_pipe_pct']:5.1f}%  "
+              f"smem conflicts {d['smem_bank_conflicts'] / max(d['smem_wavefronts'], 1) * 100:4.1f}%")
