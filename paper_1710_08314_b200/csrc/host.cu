@@ -558,6 +558,16 @@ RungCfg plan_lanes(const pl_handle& h) {
     return best;
 }
 
+// Sub-warps of one warp read the same structures of their own frame areas in
+// the same instruction (alive list, buffer indices, node statistics, psum
+// words): with an area stride of a multiple of 128 bytes they hit the same
+// banks.  Strides of 128/fpw (mod 128) spread the frames over the banks.
+int skew_frame_area(int bytes, int fpw) {
+    if (fpw <= 1 || !env_int("PLB_SKEW", 1)) return bytes;
+    const int want = 128 / fpw;
+    return bytes + (want - bytes % 128 + 128) % 128;
+}
+
 RungCfg plan_rung(const pl_handle& h, int l, bool list, bool ladder = false) {
     const char* forced = std::getenv("PLB_SEGMAX");
     const char* forced_fpw = std::getenv("PLB_FPW");
@@ -603,7 +613,7 @@ RungCfg plan_rung(const pl_handle& h, int l, bool list, bool ladder = false) {
                 c.seg_max = seg;
                 c.wpb = wpb;
                 c.fpw = fpw;
-                c.smem_per_frame = int(plb::smem_bytes_per_frame(h.nmax, l, h.esz, seg));
+                c.smem_per_frame = skew_frame_area(int(plb::smem_bytes_per_frame(h.nmax, l, h.esz, seg)), fpw);
                 c.gscratch_per_frame = plb::gscratch_bytes_per_frame(h.nmax, l, h.esz, seg);
                 const int smem = c.smem_per_frame * fpw * wpb;
                 const int nb = list ? plb::occupancy_list(h.dec.precision, l, fpw, smem, wpb)
