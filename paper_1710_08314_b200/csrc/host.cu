@@ -409,6 +409,7 @@ struct RungCfg {
     int wpb = plb::kMaxWarpsPerBlock;
     int fpw = 1; // frames per warp (sub-warp decoding, single-code batches)
     int team = 1; // >1: blocks of `team` warps, one frame each
+    int seg_solo = 0; // solo-mode layout (warp 0 with the whole block's smem), 0 = none
     bool lanes = false; // frame-per-lane SC kernel (smem / gscratch figures per 32-frame warp)
     int64_t gscratch_total() const {
         return int64_t(grid) * (team > 1 ? 1 : wpb * fpw) * gscratch_per_frame;
@@ -636,6 +637,16 @@ RungCfg plan_rung(const pl_handle& h, int l, bool list, bool ladder = false) {
         }
     }
     if (pick.grid <= 0) throw ConfigError("no launch configuration fits this code / list size on the device");
+    // solo mode (passes with at most one frame per block): the most
+    // shared-memory-resident layout in the area of all the block's warps
+    if (pick.wpb > 1 && env_int("PLB_SOLO", 1)) {
+        for (int seg = h.nmax; seg >= 1; seg >>= 1) {
+            if (plb::smem_bytes_per_frame(h.nmax, l, h.esz, seg) <= int64_t(pick.smem_per_frame) * pick.wpb) {
+                pick.seg_solo = seg;
+                break;
+            }
+        }
+    }
     return pick;
 }
 
@@ -713,6 +724,8 @@ void run_decode(pl_handle& h, const void* llr, const int32_t* code_id, int64_t n
         p.wpb = rc.wpb;
         p.fpw = rc.fpw;
         p.team = rc.team;
+        p.seg_solo = rc.seg_solo;
+        p.solo_max = rc.grid * rc.fpw;
         if (h.profiling) {
             while (h.prof_ev.size() < size_t(2 * (slot + 1))) {
                 cudaEvent_t ev;

@@ -1339,7 +1339,7 @@ __device__ void write_outputs(const LaunchParams& P, const DevCode& C, const uin
 template <bool TEAM = false, typename R, int SW>
 __device__ void setup_ctx(Ctx<R, SW>& cx, const LaunchParams& P, const DevCode& C,
                           unsigned char* sm, unsigned char* gs, int frame, const Sub<SW>& sw,
-                          int l) {
+                          int l, int segmax) {
     cx.sw = sw;
     cx.lane = sw.lane;
     cx.n = C.n;
@@ -1347,7 +1347,7 @@ __device__ void setup_ctx(Ctx<R, SW>& cx, const LaunchParams& P, const DevCode& 
     cx.lmask = l >= 32 ? FULL : ((1u << l) - 1u);
     cx.chan = static_cast<const R*>(P.llr) + int64_t(frame) * P.llr_stride;
     cx.fx = reinterpret_cast<Fixed*>(sm);
-    const LayoutQ q0 = layout_query(C.n, l, int(sizeof(R)), P.seg_smem_max, 0);
+    const LayoutQ q0 = layout_query(C.n, l, int(sizeof(R)), segmax, 0);
     cx.ps = reinterpret_cast<uint32_t*>(sm + q0.psum_off);
     cx.rw = q0.rw;
     // (constants outside team kernels: the team code folds away)
@@ -1356,7 +1356,7 @@ __device__ void setup_ctx(Ctx<R, SW>& cx, const LaunchParams& P, const DevCode& 
     cx.tstride = TEAM ? 32 * P.team : SW;
     #pragma unroll 1
     for (int d = cx.lane + 1; d <= C.stages; d += SW) {
-        const LayoutQ q = layout_query(C.n, l, int(sizeof(R)), P.seg_smem_max, d);
+        const LayoutQ q = layout_query(C.n, l, int(sizeof(R)), segmax, d);
         cx.fx->pool[d] = reinterpret_cast<uint64_t>((q.pool_in_smem ? sm : gs) + q.pool_off);
     }
     if (cx.lane == 0) *reinterpret_cast<uint4*>(cx.bix()) = make_uint4(0, 0, 0, 0);
@@ -1375,12 +1375,12 @@ __host__ __device__ constexpr int kv_maxw(int kv, int sw) { return 4 * kv_l(kv) 
 
 template <typename R, int KV, int SW, bool TEAM>
 __device__ void list_frame(const LaunchParams& P, const DevCode& C, unsigned char* sm,
-                           unsigned char* gs, int frame, bool active, const Sub<SW>& sw) {
+                           unsigned char* gs, int frame, bool active, const Sub<SW>& sw, int segmax) {
     using A = Arith<R>;
     using M = typename A::M;
     constexpr int CW = kv_cw(KV, SW), MAXW = kv_maxw(KV, SW);
     Ctx<R, SW> cx;
-    setup_ctx<TEAM>(cx, P, C, sm, gs, frame, sw, P.l);
+    setup_ctx<TEAM>(cx, P, C, sm, gs, frame, sw, P.l, segmax);
     const int lane = cx.lane;
     const uint32_t* sched = C.sched_list;
     const int nops = C.nops_list;
@@ -1553,7 +1553,7 @@ __device__ void sc_frame(const LaunchParams& P, const DevCode& C, unsigned char*
     using A = Arith<R>;
     using M = typename A::M;
     Ctx<R, 32> cx;
-    setup_ctx(cx, P, C, sm, gs, frame, sw, 1);
+    setup_ctx(cx, P, C, sm, gs, frame, sw, 1, P.seg_smem_max);
     const int lane = cx.lane;
     uint32_t* row = cx.row(0);
     const uint32_t* sched = C.sched_sc;
@@ -1694,16 +1694,24 @@ decode_kernel(const LaunchParams P) {
                 const int frame = P.frame_list ? P.frame_list[idx] : int(idx);
                 const int cid = P.code_id ? P.code_id[frame] : 0;
                 const DevCode C = P.codes[cid];
-                if (wib == 0) list_frame<R, KV, 32, true>(P, C, smem_raw, gs, frame, true, sw);
+                if (wib == 0) list_frame<R, KV, 32, true>(P, C, smem_raw, gs, frame, true, sw, P.seg_smem_max);
                 else team_helper<R>(P, C, smem_raw, frame, wib);
             }
             return;
         }
     }
-    const int64_t gw = int64_t(blockIdx.x) * (blockDim.x >> 5) + wib;
-    unsigned char* sm = smem_raw + wib * P.smem_per_warp + sw.id * P.smem_per_frame;
-    unsigned char* gs = static_cast<unsigned char*>(P.gscratch) + (gw * FPW + sw.id) * P.gscratch_per_frame;
     const long long count = P.frame_list ? (long long)(*P.frame_count) : (long long)P.nframes;
+    // Solo mode for passes with few frames (the upper FA rungs: a few
+    // hundred frames or less, where a frame's latency, not the throughput,
+    // sets the pass time): warp 0 of each block decodes with the shared
+    // memory of the whole block, so more depth segments stay out of the L2.
+    const bool solo = P.seg_solo > 0 && count <= P.solo_max;
+    if (solo && wib != 0) return;
+    const int64_t gw = solo ? int64_t(blockIdx.x) : int64_t(blockIdx.x) * (blockDim.x >> 5) + wib;
+    unsigned char* sm = solo ? smem_raw + sw.id * (P.smem_per_warp * P.wpb / FPW)
+                             : smem_raw + wib * P.smem_per_warp + sw.id * P.smem_per_frame;
+    unsigned char* gs = static_cast<unsigned char*>(P.gscratch) + (gw * FPW + sw.id) * P.gscratch_per_frame;
+    const int segmax = solo ? P.seg_solo : P.seg_smem_max;
     for (;;) {
         unsigned long long i0 = 0;
         if (wl == 0) i0 = atomicAdd(P.work, (unsigned long long)FPW);
@@ -1726,11 +1734,11 @@ decode_kernel(const LaunchParams P) {
                 const int fj = same ? frame : __shfl_sync(FULL, frame, j * SW);
                 const int cj = same ? cid : __shfl_sync(FULL, cid, j * SW);
                 const bool aj = same ? active : (__shfl_sync(FULL, int(active), j * SW) && sw.id == 0);
-                list_frame<R, KV, SW, false>(P, P.codes[cj], sm, gs, fj, aj, sw);
+                list_frame<R, KV, SW, false>(P, P.codes[cj], sm, gs, fj, aj, sw, segmax);
             }
         } else {
             const DevCode C = P.codes[cid];
-            if constexpr (KV > 0) list_frame<R, KV, SW, false>(P, C, sm, gs, frame, active, sw);
+            if constexpr (KV > 0) list_frame<R, KV, SW, false>(P, C, sm, gs, frame, active, sw, segmax);
             else sc_frame<R>(P, C, sm, gs, frame, sw);
         }
     }

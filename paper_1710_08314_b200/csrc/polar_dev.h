@@ -95,6 +95,9 @@ struct LaunchParams {
     int32_t fpw;               // frames per warp (1, 2 or 4; >1 needs one code)
     int32_t team;              // >1: each block is a team of `team` warps decoding
                                // one frame (list passes, 32-lane kernels)
+    int32_t seg_solo;          // >0: solo mode when the pass has <= solo_max frames:
+    int32_t solo_max;          // warp 0 of each block decodes with the whole block's
+                               // shared memory (segments <= seg_solo in smem)
 };
 
 constexpr int kMaxWarpsPerBlock = 4; // a block is 1, 2 or 4 independent warps
