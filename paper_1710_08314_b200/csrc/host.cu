@@ -1171,10 +1171,17 @@ int pl_decode_host(pl_handle* h, const void* llr, const int32_t* code_id, int64_
         }
         // ~16 chunks so the copies of one chunk overlap the decode of another
         // and the pipeline fill / drain stays short (measured: cfg1 e2e 16.2 ->
-        // 16.7 Gb/s going from 8 to 16 chunks; float cfg0 best at 8192 frames)
+        // 16.7 Gb/s going from 8 to 16 chunks; float cfg0 best at 8192 frames).
+        // Adaptive kinds on int8 LLRs: ~8 chunks, since every chunk pays the
+        // latency of the upper ladder rungs (a few frames each) and the int8
+        // copies are short (measured FA@4.5 dB int8 e2e 33.1 -> 39.2-40.7
+        // Gb/s; the PCIe-bound float / int16 ladders keep 16: 11.25 vs 11.09,
+        // 21.8 vs 20.9)
         const char* cs = std::getenv("PLB_HOST_CHUNK");
         const int64_t chunk = cs ? std::max<int64_t>(1, std::atoll(cs))
-                                 : std::clamp<int64_t>((nframes + 15) / 16, 8192, 65536);
+                              : adaptive(h->dec.kind) && h->esz == 1
+                                  ? std::clamp<int64_t>((nframes + 7) / 8, 8192, 131072)
+                                                  : std::clamp<int64_t>((nframes + 15) / 16, 8192, 65536);
         const int64_t in_bytes = h->nmax * int64_t(h->esz);
         // per frame output record: payload | codeword | crc | esc | metric
         const int64_t ob_pay = h->pstride, ob_cw = codeword ? h->cstride : 0;
