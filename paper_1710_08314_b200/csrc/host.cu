@@ -525,9 +525,11 @@ RungCfg plan_team(const pl_handle& h, int l, int team, const std::vector<int>& c
 }
 
 // The frame-per-lane SC pass: 32 frames per warp; the most shared-memory
-// resident layout that keeps PLB_LANE_WARPS warps per SM.
+// resident layout that keeps PLB_LANE_WARPS warps per SM (measured best:
+// 16 for float, whose pass is DRAM-bound; 24 for int8 / int16 — FA@4.5 dB
+// int8 SC pass 12.6 -> 10.8 ms, int16 17.8 -> 16.4 ms).
 RungCfg plan_lanes(const pl_handle& h) {
-    const int target = std::max(1, env_int("PLB_LANE_WARPS", 16));
+    const int target = std::max(1, env_int("PLB_LANE_WARPS", h.dec.precision == PL_F32 ? 16 : 24));
     const int forced = env_int("PLB_SEGMAX", 0);
     std::vector<int> cands;
     if (forced) cands.push_back(forced);
