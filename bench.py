@@ -289,15 +289,30 @@ def main():
         "esc": torch.empty(F, dtype=torch.uint8).pin_memory(),
         "metric": torch.empty(F, dtype=torch.float32).pin_memory(),
     }
-    dec.decode_host_into(llr_h, host_out, cid_h)
+    esz = {"f32": 4, "i16": 2}.get(wl.precision, 1)
+    if cid is not None:
+        # mixed codes: packed variable-length frames (pl_decode_host_packed),
+        # each frame's own n LLRs cross the host link
+        ns = np.array([c.n for c in codes])[cid]
+        frames = [llr_np[f, : ns[f]] for f in range(F)]
+        pk, off = dec.pack_frames(frames)
+        del frames
+        pk_h = torch.from_numpy(pk).pin_memory()
+        off_h = torch.from_numpy(off).pin_memory()
+        e2e_call = lambda: dec.decode_host_packed_into(pk_h, off_h, host_out, cid_h)  # noqa: E731
+        h2d = pk.nbytes + off.nbytes + F * 4
+        e2e_api = "pl_decode_host_packed"
+    else:
+        e2e_call = lambda: dec.decode_host_into(llr_h, host_out, cid_h)  # noqa: E731
+        h2d = F * dec.llr_stride * esz
+        e2e_api = "pl_decode_host"
+    e2e_call()
     barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        dec.decode_host_into(llr_h, host_out, cid_h)
+        e2e_call()
     e2e_s = max_over_ranks(time.perf_counter() - t0)
     e2e_value = bits_per_step * ws * e2e_steps / e2e_s / 1e9
-    esz = {"f32": 4, "i16": 2}.get(wl.precision, 1)
-    h2d = F * dec.llr_stride * esz + (F * 4 if cid is not None else 0)
     d2h = F * (dec.payload_stride + 1 + 1 + 4)
 
     # ---- roofline of the dominant kernel (live CUDA-event durations)
@@ -359,7 +374,7 @@ def main():
             "source": kc["source"]},
         "clocks": clocks,
         "e2e": {"value": e2e_value, "unit": "Gb/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "steps": e2e_steps, "api": "pl_decode_host"},
+                "d2h_bytes_per_step": d2h, "steps": e2e_steps, "api": e2e_api},
     }
 
     # ---- CPU baseline: the reference decoder on this box's cores (rank 0, N=1)

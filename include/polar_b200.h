@@ -140,6 +140,24 @@ int pl_decode_host(pl_handle* h, const void* llr, const int32_t* code_id,
                    int64_t nframes, uint8_t* payload, uint8_t* codeword,
                    uint8_t* crc_ok, uint8_t* esc, float* metric);
 
+/* Packed variable-length frames (mixed-code batches without padding every
+ * frame to pl_llr_stride): frame i's n LLRs start at element llr_offset[i]
+ * of llr.  Offsets ascending, frames not overlapping, every frame 16-byte
+ * aligned (offset * sizeof(R) % 16 == 0); PL_ERR_ARG otherwise (host call).
+ * The reference decodes each frame from its own buffer of n LLRs
+ * (FrameDecoder<R>::decode(const R*), decoders.hpp:60): this is that
+ * layout for a batch.
+ *   pl_decode_packed       device buffers (llr, llr_offset), async on stream
+ *   pl_decode_host_packed  host buffers; only each frame's n LLRs cross the
+ *                          host link */
+int pl_decode_packed(pl_handle* h, const void* llr, const int64_t* llr_offset,
+                     const int32_t* code_id, int64_t nframes, uint8_t* payload,
+                     uint8_t* codeword, uint8_t* crc_ok, uint8_t* esc, float* metric,
+                     void* stream);
+int pl_decode_host_packed(pl_handle* h, const void* llr, const int64_t* llr_offset,
+                          const int32_t* code_id, int64_t nframes, uint8_t* payload,
+                          uint8_t* codeword, uint8_t* crc_ok, uint8_t* esc, float* metric);
+
 /* Kernel launches issued by the last pl_decode / pl_decode_host call. */
 int64_t pl_last_launches(const pl_handle* h);
 

@@ -21,6 +21,7 @@ EXPORTS = (
     "pl_channel_generate", "pl_channel_generate_device", "pl_profile", "pl_last_kernel_ms",
     "pl_kernel_selftest", "pl_channel_generate_frames", "pl_precision", "pl_sim_point",
     "pl_format_csv_row", "pl_frozen_file_load", "pl_frozen_file_save", "pl_puncture_file_load",
+    "pl_decode_packed", "pl_decode_host_packed",
 )
 
 
@@ -85,6 +86,8 @@ def lib():
         getattr(L, f).restype = i64
     L.pl_decode.argtypes = [vp, vp, vp, i64, vp, vp, vp, vp, vp, vp]
     L.pl_decode_host.argtypes = [vp, vp, vp, i64, vp, vp, vp, vp, vp]
+    L.pl_decode_packed.argtypes = [vp, vp, vp, vp, i64, vp, vp, vp, vp, vp, vp]
+    L.pl_decode_host_packed.argtypes = [vp, vp, vp, vp, i64, vp, vp, vp, vp, vp]
     L.pl_crc_parse.argtypes = [C.c_char_p, vp]
     L.pl_crc_compute.argtypes = [vp, vp, i64, vp]
     L.pl_tree_build.argtypes = [vp, i32, vp, vp, i32]

@@ -456,7 +456,10 @@ struct pl_handle {
     cudaStream_t s_comp[2] = {nullptr, nullptr}, s_h2d = nullptr, s_d2h = nullptr;
     int64_t stage_frames = 0;
     void* d_in[2] = {nullptr, nullptr};
+    int64_t in_cap = 0; // bytes of each d_in / h_stage_in buffer
     int32_t* d_cid[2] = {nullptr, nullptr};
+    int64_t* d_off[2] = {nullptr, nullptr}; // packed input: chunk-relative frame offsets
+    int64_t* h_stage_off[2] = {nullptr, nullptr};
     uint8_t* d_out[2] = {nullptr, nullptr};
     void* h_stage_in[2] = {nullptr, nullptr};
     uint8_t* h_stage_out[2] = {nullptr, nullptr};
@@ -677,7 +680,7 @@ int fail(pl_handle* h, int code, const std::string& msg) {
 
 void run_decode(pl_handle& h, const void* llr, const int32_t* code_id, int64_t nframes,
                 uint8_t* payload, uint8_t* codeword, uint8_t* crc_ok, uint8_t* esc,
-                float* metric, cudaStream_t s, int exec = 0) {
+                float* metric, cudaStream_t s, int exec = 0, const int64_t* llr_offset = nullptr) {
     ck(cudaSetDevice(h.device), "cudaSetDevice");
     h.launches = 0;
     h.prof_kind.clear(); // timed decode launches of this call (pl_last_kernel_ms)
@@ -695,6 +698,7 @@ void run_decode(pl_handle& h, const void* llr, const int32_t* code_id, int64_t n
     base.codes = h.d_codes;
     base.llr = llr;
     base.llr_stride = h.nmax;
+    base.llr_offset = llr_offset;
     base.code_id = code_id;
     base.nframes = nframes;
     base.payload = payload;
@@ -1083,6 +1087,8 @@ void pl_destroy(pl_handle* h) {
         if (h->s_comp[i]) cudaStreamDestroy(h->s_comp[i]);
         if (h->d_in[i]) cudaFree(h->d_in[i]);
         if (h->d_cid[i]) cudaFree(h->d_cid[i]);
+        if (h->d_off[i]) cudaFree(h->d_off[i]);
+        if (h->h_stage_off[i]) cudaFreeHost(h->h_stage_off[i]);
         if (h->d_out[i]) cudaFree(h->d_out[i]);
         if (h->h_stage_in[i]) cudaFreeHost(h->h_stage_in[i]);
         if (h->h_stage_out[i]) cudaFreeHost(h->h_stage_out[i]);
@@ -1152,12 +1158,67 @@ int pl_decode(pl_handle* h, const void* llr, const int32_t* code_id, int64_t nfr
     }
 }
 
+int pl_decode_packed(pl_handle* h, const void* llr, const int64_t* llr_offset, const int32_t* code_id,
+                     int64_t nframes, uint8_t* payload, uint8_t* codeword, uint8_t* crc_ok, uint8_t* esc,
+                     float* metric, void* stream) {
+    if (!h) return fail(nullptr, PL_ERR_ARG, "null handle");
+    if (nframes < 0 || (nframes > 0 && (!llr || !llr_offset || !payload)))
+        return fail(h, PL_ERR_ARG, "llr, llr_offset and payload buffers are required");
+    if (nframes > INT32_MAX) return fail(h, PL_ERR_ARG, "too many frames in one call");
+    try {
+        run_decode(*h, llr, code_id, nframes, payload, codeword, crc_ok, esc, metric,
+                   static_cast<cudaStream_t>(stream), 0, llr_offset);
+        h->err.clear();
+        return PL_OK;
+    } catch (const std::exception& e) {
+        return fail(h, PL_ERR_CUDA, e.what());
+    }
+}
+
+namespace {
+int decode_host_impl(pl_handle* h, const void* llr, const int64_t* offsets, const int32_t* code_id,
+                     int64_t nframes, uint8_t* payload, uint8_t* codeword, uint8_t* crc_ok,
+                     uint8_t* esc, float* metric);
+}
+
 int pl_decode_host(pl_handle* h, const void* llr, const int32_t* code_id, int64_t nframes,
                    uint8_t* payload, uint8_t* codeword, uint8_t* crc_ok, uint8_t* esc,
                    float* metric) {
+    return decode_host_impl(h, llr, nullptr, code_id, nframes, payload, codeword, crc_ok, esc, metric);
+}
+
+int pl_decode_host_packed(pl_handle* h, const void* llr, const int64_t* llr_offset,
+                          const int32_t* code_id, int64_t nframes, uint8_t* payload,
+                          uint8_t* codeword, uint8_t* crc_ok, uint8_t* esc, float* metric) {
+    if (h && nframes > 0 && !llr_offset) return fail(h, PL_ERR_ARG, "llr_offset is required");
+    return decode_host_impl(h, llr, llr_offset, code_id, nframes, payload, codeword, crc_ok, esc, metric);
+}
+
+} // extern "C"
+
+namespace {
+int decode_host_impl(pl_handle* h, const void* llr, const int64_t* offsets, const int32_t* code_id,
+                     int64_t nframes, uint8_t* payload, uint8_t* codeword, uint8_t* crc_ok,
+                     uint8_t* esc, float* metric) {
     if (!h) return fail(nullptr, PL_ERR_ARG, "null handle");
     if (nframes < 0 || (nframes > 0 && (!llr || !payload)))
         return fail(h, PL_ERR_ARG, "llr and payload buffers are required");
+    // packed frames: ascending, 16-byte aligned offsets (the kernels read
+    // the channel with 16-byte vectors), code ids in range
+    auto frame_n = [&](int64_t f) {
+        const int32_t c = code_id ? code_id[f] : 0;
+        return (c >= 0 && c < int32_t(h->codes.size())) ? h->codes[size_t(c)].n : -1;
+    };
+    if (offsets) {
+        for (int64_t f = 0; f < nframes; ++f) {
+            const int n = frame_n(f);
+            if (n < 0) return fail(h, PL_ERR_ARG, "code id out of range");
+            if (offsets[f] < 0 || (offsets[f] * h->esz) % 16 != 0)
+                return fail(h, PL_ERR_ARG, "packed frame offsets must be non-negative and 16-byte aligned");
+            if (f > 0 && offsets[f] < offsets[f - 1] + frame_n(f - 1))
+                return fail(h, PL_ERR_ARG, "packed frames must be ascending and must not overlap");
+        }
+    }
     try {
         ck(cudaSetDevice(h->device), "cudaSetDevice");
         if (!h->s_comp[0]) {
@@ -1185,29 +1246,55 @@ int pl_decode_host(pl_handle* h, const void* llr, const int32_t* code_id, int64_
                                   ? std::clamp<int64_t>((nframes + 7) / 8, 8192, 131072)
                                                   : std::clamp<int64_t>((nframes + 15) / 16, 8192, 65536);
         const int64_t in_bytes = h->nmax * int64_t(h->esz);
+        const int64_t nchunks = (nframes + chunk - 1) / chunk;
+        // input element range of a chunk (packed: first offset .. end of its
+        // last frame; padded: nf strides)
+        auto in_range = [&](int64_t f0, int64_t nf, int64_t& e0, int64_t& e1) {
+            if (offsets) {
+                e0 = offsets[f0];
+                e1 = offsets[f0 + nf - 1] + frame_n(f0 + nf - 1);
+            } else {
+                e0 = f0 * h->nmax;
+                e1 = (f0 + nf) * h->nmax;
+            }
+        };
+        int64_t need = chunk * in_bytes;
+        if (offsets) {
+            need = 16;
+            for (int64_t c = 0; c < nchunks; ++c) {
+                int64_t e0, e1;
+                in_range(c * chunk, std::min(chunk, nframes - c * chunk), e0, e1);
+                need = std::max(need, (e1 - e0) * int64_t(h->esz));
+            }
+        }
         // per frame output record: payload | codeword | crc | esc | metric
         const int64_t ob_pay = h->pstride, ob_cw = codeword ? h->cstride : 0;
-        if (h->stage_frames < chunk) {
+        if (h->stage_frames < chunk || h->in_cap < need || (offsets && !h->d_off[0])) {
+            const int64_t cap = std::max(need, chunk * in_bytes);
             for (int i = 0; i < 2; ++i) {
                 if (h->d_in[i]) cudaFree(h->d_in[i]);
                 if (h->d_cid[i]) cudaFree(h->d_cid[i]);
+                if (h->d_off[i]) cudaFree(h->d_off[i]);
+                if (h->h_stage_off[i]) cudaFreeHost(h->h_stage_off[i]);
                 if (h->d_out[i]) cudaFree(h->d_out[i]);
                 if (h->h_stage_in[i]) cudaFreeHost(h->h_stage_in[i]);
                 if (h->h_stage_out[i]) cudaFreeHost(h->h_stage_out[i]);
-                ck(cudaMalloc(&h->d_in[i], size_t(chunk * in_bytes)), "cudaMalloc");
+                ck(cudaMalloc(&h->d_in[i], size_t(cap)), "cudaMalloc");
                 ck(cudaMalloc(&h->d_cid[i], size_t(chunk) * 4), "cudaMalloc");
+                ck(cudaMalloc(&h->d_off[i], size_t(chunk) * 8), "cudaMalloc");
+                ck(cudaMallocHost(&h->h_stage_off[i], size_t(chunk) * 8), "cudaMallocHost");
                 ck(cudaMalloc(&h->d_out[i], size_t(chunk * (h->pstride + h->cstride + 6) + 64)), "cudaMalloc");
-                ck(cudaMallocHost(&h->h_stage_in[i], size_t(chunk * in_bytes)), "cudaMallocHost");
+                ck(cudaMallocHost(&h->h_stage_in[i], size_t(cap)), "cudaMallocHost");
                 ck(cudaMallocHost(&h->h_stage_out[i], size_t(chunk * (h->pstride + h->cstride + 6))),
                    "cudaMallocHost");
             }
             h->stage_frames = chunk;
+            h->in_cap = cap;
         }
         const bool pin_in = is_pinned_host(llr);
         const bool pin_out = is_pinned_host(payload) && (!codeword || is_pinned_host(codeword)) &&
                              (!crc_ok || is_pinned_host(crc_ok)) && (!esc || is_pinned_host(esc)) &&
                              (!metric || is_pinned_host(metric));
-        const int64_t nchunks = (nframes + chunk - 1) / chunk;
         int64_t launches = 0;
         std::vector<int64_t> pending(2, -1);
         auto finish_chunk = [&](int64_t c) {
@@ -1234,14 +1321,23 @@ int pl_decode_host(pl_handle* h, const void* llr, const int32_t* code_id, int64_
                 finish_chunk(pending[size_t(b)]);
                 pending[size_t(b)] = -1;
             }
-            const char* src = static_cast<const char*>(llr) + f0 * in_bytes;
+            int64_t e0, e1;
+            in_range(f0, nf, e0, e1);
+            const int64_t nbytes = (e1 - e0) * int64_t(h->esz);
+            const char* src = static_cast<const char*>(llr) + e0 * int64_t(h->esz);
             if (!pin_in) {
-                std::memcpy(h->h_stage_in[b], src, size_t(nf * in_bytes));
+                std::memcpy(h->h_stage_in[b], src, size_t(nbytes));
                 src = static_cast<const char*>(h->h_stage_in[b]);
             }
             ck(cudaStreamWaitEvent(h->s_h2d, h->ev_dec[b], 0), "wait");
-            ck(cudaMemcpyAsync(h->d_in[b], src, size_t(nf * in_bytes), cudaMemcpyHostToDevice, h->s_h2d),
-               "h2d");
+            ck(cudaMemcpyAsync(h->d_in[b], src, size_t(nbytes), cudaMemcpyHostToDevice, h->s_h2d), "h2d");
+            if (offsets) {
+                // chunk-relative offsets (the chunk's input starts at its first frame)
+                for (int64_t i = 0; i < nf; ++i) h->h_stage_off[b][i] = offsets[f0 + i] - e0;
+                ck(cudaMemcpyAsync(h->d_off[b], h->h_stage_off[b], size_t(nf) * 8, cudaMemcpyHostToDevice,
+                                   h->s_h2d),
+                   "h2d");
+            }
             if (code_id)
                 ck(cudaMemcpyAsync(h->d_cid[b], code_id + f0, size_t(nf) * 4, cudaMemcpyHostToDevice,
                                    h->s_h2d),
@@ -1259,7 +1355,7 @@ int pl_decode_host(pl_handle* h, const void* llr, const int32_t* code_id, int64_
             const uintptr_t mis = reinterpret_cast<uintptr_t>(d_met) & 3u;
             if (mis) d_met = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(d_met) + (4 - mis));
             run_decode(*h, h->d_in[b], code_id ? h->d_cid[b] : nullptr, nf, d_pay, d_cw, d_ok, d_esc,
-                       d_met, h->s_comp[b], b);
+                       d_met, h->s_comp[b], b, offsets ? h->d_off[b] : nullptr);
             launches += h->launches;
             ck(cudaEventRecord(h->ev_dec[b], h->s_comp[b]), "record");
             ck(cudaStreamWaitEvent(h->s_d2h, h->ev_dec[b], 0), "wait");
@@ -1291,4 +1387,4 @@ int pl_decode_host(pl_handle* h, const void* llr, const int32_t* code_id, int64_
     }
 }
 
-} // extern "C"
+} // namespace

@@ -367,6 +367,12 @@ __device__ __forceinline__ void vst(R* p, const Vec<R, G>& x) {
     *reinterpret_cast<typename VT<G * sizeof(R)>::T*>(p) = x.raw;
 }
 
+// first channel LLR of a frame: fixed stride, or the packed layout's offset
+template <typename R>
+__device__ __forceinline__ const R* frame_llr(const LaunchParams& P, int frame) {
+    return static_cast<const R*>(P.llr) + (P.llr_offset ? P.llr_offset[frame] : int64_t(frame) * P.llr_stride);
+}
+
 // ---- per-frame shared-memory area ----------------------------------------
 // (followed by the bufidx rows, [slot][depth] -> buffer index in the depth
 // pool, 16 bytes per slot of the pass's list size)
@@ -1345,7 +1351,7 @@ __device__ void setup_ctx(Ctx<R, SW>& cx, const LaunchParams& P, const DevCode& 
     cx.n = C.n;
     cx.l = l;
     cx.lmask = l >= 32 ? FULL : ((1u << l) - 1u);
-    cx.chan = static_cast<const R*>(P.llr) + int64_t(frame) * P.llr_stride;
+    cx.chan = frame_llr<R>(P, frame);
     cx.fx = reinterpret_cast<Fixed*>(sm);
     const LayoutQ q0 = layout_query(C.n, l, int(sizeof(R)), segmax, 0);
     cx.ps = reinterpret_cast<uint32_t*>(sm + q0.psum_off);
@@ -1631,7 +1637,7 @@ __device__ void team_helper(const LaunchParams& P, const DevCode& C, unsigned ch
     cx.lane = threadIdx.x & 31;
     cx.n = C.n;
     cx.l = P.l;
-    cx.chan = static_cast<const R*>(P.llr) + int64_t(frame) * P.llr_stride;
+    cx.chan = frame_llr<R>(P, frame);
     cx.fx = reinterpret_cast<Fixed*>(sm);
     const LayoutQ q0 = layout_query(C.n, P.l, int(sizeof(R)), P.seg_smem_max, 0);
     cx.ps = reinterpret_cast<uint32_t*>(sm + q0.psum_off);
@@ -2020,7 +2026,7 @@ __device__ void lane_frame(const LaunchParams& P, const DevCode& C, unsigned cha
     LaneCtx<R> c;
     c.lane = lane;
     c.n = C.n;
-    c.chan = static_cast<const R*>(P.llr) + int64_t(frame) * P.llr_stride;
+    c.chan = frame_llr<R>(P, frame);
     const LaneQ q0 = lane_layout(C.n, int(sizeof(R)), P.seg_smem_max, 0);
     c.ps = reinterpret_cast<uint32_t*>(sm + q0.psum_off) + lane;
     uint64_t* pt = reinterpret_cast<uint64_t*>(sm);

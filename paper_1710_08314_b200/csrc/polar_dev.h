@@ -68,6 +68,8 @@ struct LaunchParams {
     const DevCode* codes;
     const void* llr;
     int64_t llr_stride;        // elements per frame
+    const int64_t* llr_offset; // nullable: element offset of each frame (packed
+                               // variable-length frames, pl_decode_packed)
     const int32_t* code_id;    // nullable
     const int32_t* frame_list; // nullable: frames [0, nframes) in order
     const int32_t* frame_count;// device count for frame_list (nullable)

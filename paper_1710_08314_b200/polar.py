@@ -432,6 +432,64 @@ class FrameDecoder:
             _raise(rc, L.last_error(self._h))
         return out
 
+    def pack_frames(self, frames, code_id=None):
+        """Variable-length frames (a list of 1-D arrays, frame i of its code's
+        n) -> (packed host buffer, element offsets): each frame starts 16-byte
+        aligned, in order (the layout pl_decode_packed / pl_decode_host_packed
+        take)."""
+        dt = self._torch.empty(0, dtype=self.llr_dtype).numpy().dtype
+        align = 16 // dt.itemsize
+        off = np.zeros(len(frames), np.int64)
+        pos = 0
+        for i, f in enumerate(frames):
+            off[i] = pos
+            pos += -(-len(f) // align) * align
+        buf = np.zeros(max(pos, align), dt)
+        for i, f in enumerate(frames):
+            buf[off[i]: off[i] + len(f)] = f
+        return buf, off
+
+    def decode_packed(self, llr, offsets, code_id=None, out=None, codeword: bool = False, stream=None):
+        """Device-resident packed frames: llr (1-D CUDA tensor), offsets
+        (int64 CUDA tensor, element offset of each frame)."""
+        t = self._torch
+        assert llr.is_cuda and llr.dtype == self.llr_dtype and llr.is_contiguous()
+        assert offsets.is_cuda and offsets.dtype == t.int64
+        nframes = offsets.numel()
+        if out is None:
+            out = self.alloc_outputs(nframes, codeword)
+        ptr = lambda x: C.c_void_p(x.data_ptr()) if x is not None else None
+        if code_id is not None:
+            assert code_id.is_cuda and code_id.dtype == t.int32
+        s = stream if stream is not None else t.cuda.current_stream(self.device)
+        rc = L.lib().pl_decode_packed(self._h, ptr(llr), ptr(offsets), ptr(code_id), nframes,
+                                      ptr(out["payload"]), ptr(out.get("codeword")), ptr(out["crc_ok"]),
+                                      ptr(out["esc"]), ptr(out["metric"]), C.c_void_p(s.cuda_stream))
+        if rc:
+            _raise(rc, L.last_error(self._h))
+        return out
+
+    def decode_host_packed_into(self, llr, offsets, o, code_id=None):
+        """Host packed frames (pl_decode_host_packed): only each frame's own
+        n LLRs cross the host link."""
+        def ptr(x):
+            if x is None:
+                return None
+            if hasattr(x, "data_ptr"):
+                return C.c_void_p(x.data_ptr())
+            return x.ctypes.data_as(C.c_void_p)
+        if not hasattr(offsets, "data_ptr"):
+            offsets = np.ascontiguousarray(offsets, np.int64)
+        nframes = offsets.numel() if hasattr(offsets, "numel") else offsets.size
+        if code_id is not None and not hasattr(code_id, "data_ptr"):
+            code_id = np.ascontiguousarray(code_id, np.int32)
+        rc = L.lib().pl_decode_host_packed(self._h, ptr(llr), ptr(offsets), ptr(code_id), nframes,
+                                           ptr(o["payload"]), ptr(o.get("codeword")), ptr(o["crc_ok"]),
+                                           ptr(o["esc"]), ptr(o["metric"]))
+        if rc:
+            _raise(rc, L.last_error(self._h))
+        return o
+
     def decode_host(self, llr: np.ndarray, code_id: np.ndarray | None = None, codeword: bool = False):
         """Host buffers in, host buffers out (copies overlap decoding)."""
         llr = np.ascontiguousarray(llr)

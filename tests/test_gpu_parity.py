@@ -258,6 +258,59 @@ def test_cfg3_mixed_codes_one_batch(P, gpu, oracle_lib):
             assert np.array_equal(got["metric"][rows], ref.metric.astype(np.float32)), tag
 
 
+def test_packed_frames_match_padded(P, gpu):
+    """Packed variable-length frames (pl_decode_packed, pl_decode_host_packed
+    with several chunks) decode exactly as the padded layout, for the mixed
+    31-code batch in float and a mixed int8 batch; malformed offsets fail
+    with PL_ERR_ARG (ValueError)."""
+    import os
+
+    from paper_1710_08314_b200.workload import MixedWorkload, make_batch
+
+    wl = MixedWorkload()
+    codes, cid, info, ks, llr = make_batch(wl, 0, 1500)
+    cases = [("f32", llr, codes, cid)]
+    # int8: N 16..256, every frame 16-byte aligned as packed
+    c8 = [_code(P, n, max(4, n // 2 - 8), "8") for n in (16, 64, 256)]
+    cid8 = np.random.default_rng(3).integers(0, 3, 900).astype(np.int32)
+    llr8 = np.zeros((900, 256), np.int8)
+    for i, c in enumerate(c8):
+        rows = np.flatnonzero(cid8 == i)
+        _, x = P.channel(c, 2.0, 11, 0, rows.size, "i8", 4.0)
+        llr8[rows, :c.n] = x
+    cases.append(("i8", llr8, c8, cid8))
+    for prec, x, cs, ci in cases:
+        kind, l = ("ca_sscl", 8) if prec == "f32" else ("fa_sscl", 8)
+        dec = P.FrameDecoder(cs, kind, l, prec, P.PruningConfig())
+        ref = dec.decode_batch(gpu.from_numpy(np.ascontiguousarray(x)).cuda(),
+                               code_id=gpu.from_numpy(ci).cuda())
+        gpu.cuda.synchronize()
+        ref = {k: v.cpu().numpy() for k, v in ref.items() if v is not None}
+        buf, off = dec.pack_frames([x[f, :cs[ci[f]].n] for f in range(x.shape[0])])
+        assert buf.size < x.size
+        o = dec.decode_packed(gpu.from_numpy(buf).cuda(), gpu.from_numpy(off).cuda(),
+                              code_id=gpu.from_numpy(ci).cuda())
+        gpu.cuda.synchronize()
+        hout = {k: np.zeros_like(v) for k, v in ref.items()}
+        os.environ["PLB_HOST_CHUNK"] = "256"
+        try:
+            dec.decode_host_packed_into(buf, off, hout, ci)
+        finally:
+            del os.environ["PLB_HOST_CHUNK"]
+        got = {k: o[k].cpu().numpy() for k in ("payload", "crc_ok", "esc", "metric")}
+        for k in ("crc_ok", "esc", "metric"):
+            assert np.array_equal(got[k], ref[k]), (prec, k)
+            assert np.array_equal(hout[k], ref[k]), (prec, k, "host")
+        for i, c in enumerate(cs):  # payload bytes past a code's own size are not written
+            rows, pb = np.flatnonzero(ci == i), (c.payload_size + 7) // 8
+            assert np.array_equal(got["payload"][rows, :pb], ref["payload"][rows, :pb]), (prec, c.n)
+            assert np.array_equal(hout["payload"][rows, :pb], ref["payload"][rows, :pb]), (prec, c.n, "host")
+        with pytest.raises(ValueError, match="packed frame"):
+            bad = off.copy()
+            bad[1] = bad[0] + 1  # overlapping and misaligned
+            dec.decode_host_packed_into(buf, bad, hout, ci)
+
+
 def test_decode_host_matches_device_path(P, gpu):
     """pl_decode_host (pageable and pinned buffers, chunked) == pl_decode."""
     import os
