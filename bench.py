@@ -293,10 +293,7 @@ def main():
     if cid is not None:
         # mixed codes: packed variable-length frames (pl_decode_host_packed),
         # each frame's own n LLRs cross the host link
-        ns = np.array([c.n for c in codes])[cid]
-        frames = [llr_np[f, : ns[f]] for f in range(F)]
-        pk, off = dec.pack_frames(frames)
-        del frames
+        pk, off = dec.pack_batch(llr_np, cid)
         pk_h = torch.from_numpy(pk).pin_memory()
         off_h = torch.from_numpy(off).pin_memory()
         e2e_call = lambda: dec.decode_host_packed_into(pk_h, off_h, host_out, cid_h)  # noqa: E731

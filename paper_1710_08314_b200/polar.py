@@ -449,6 +449,21 @@ class FrameDecoder:
             buf[off[i]: off[i] + len(f)] = f
         return buf, off
 
+    def pack_batch(self, llr: np.ndarray, code_id: np.ndarray):
+        """A padded mixed batch (frames x pl_llr_stride, frame f valid up to
+        its code's n) -> (packed buffer, offsets), vectorised per code length."""
+        dt = self._torch.empty(0, dtype=self.llr_dtype).numpy().dtype
+        align = 16 // dt.itemsize
+        ns = np.array([c.n for c in self.codes], np.int64)[np.asarray(code_id)]
+        sz = -(-ns // align) * align
+        off = np.zeros(ns.size, np.int64)
+        np.cumsum(sz[:-1], out=off[1:])
+        buf = np.zeros(max(int(sz.sum()), align), dt)
+        for n in np.unique(ns):
+            rows = np.flatnonzero(ns == n)
+            buf[(off[rows][:, None] + np.arange(n)).ravel()] = llr[rows, :n].ravel()
+        return buf, off
+
     def decode_packed(self, llr, offsets, code_id=None, out=None, codeword: bool = False, stream=None):
         """Device-resident packed frames: llr (1-D CUDA tensor), offsets
         (int64 CUDA tensor, element offset of each frame)."""

@@ -288,6 +288,8 @@ def test_packed_frames_match_padded(P, gpu):
         ref = {k: v.cpu().numpy() for k, v in ref.items() if v is not None}
         buf, off = dec.pack_frames([x[f, :cs[ci[f]].n] for f in range(x.shape[0])])
         assert buf.size < x.size
+        b2, o2 = dec.pack_batch(x, ci)
+        assert np.array_equal(b2, buf) and np.array_equal(o2, off)
         o = dec.decode_packed(gpu.from_numpy(buf).cuda(), gpu.from_numpy(off).cuda(),
                               code_id=gpu.from_numpy(ci).cuda())
         gpu.cuda.synchronize()
