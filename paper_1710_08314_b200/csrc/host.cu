@@ -323,6 +323,7 @@ struct HostCode {
     std::vector<uint8_t> frozen;
     std::vector<uint32_t> sched_list, sched_sc, sched_lane;
     std::vector<uint16_t> info_pos;
+    std::vector<uint8_t> open_mask; // ceil(n/8): bit i of byte j = position 8j+i is open
     std::vector<uint64_t> crc_tab;
     uint64_t crc_c0 = 0;
 };
@@ -351,6 +352,9 @@ HostCode make_host_code(const pl_code& c, const pl_decoder& dec) {
     h.psize = c.k + h.width;
     for (int i = 0; i < c.n; ++i)
         if (!h.frozen[size_t(i)]) h.info_pos.push_back(uint16_t(i));
+    h.open_mask.assign(size_t((c.n + 7) / 8), 0);
+    for (int i = 0; i < c.n; ++i)
+        if (!h.frozen[size_t(i)]) h.open_mask[size_t(i >> 3)] |= uint8_t(1u << (i & 7));
     if (c.channel_use) { // make_code's puncture checks (code.cpp:112-125)
         int transmitted = 0;
         for (int i = 0; i < c.n; ++i) {
@@ -1016,6 +1020,21 @@ int pl_create(const pl_code* codes, int32_t ncodes, const pl_decoder* dec, int32
         ck(cudaSetDevice(device), "cudaSetDevice");
         ck(cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device), "attr");
         std::vector<plb::DevCode> dc(h->codes.size());
+        // the universal byte-compaction table of the payload gather
+        const uint8_t* comp_tab = nullptr;
+        {
+            std::vector<uint8_t> t(size_t(256) * 256);
+            for (int m = 0; m < 256; ++m)
+                for (int v = 0; v < 256; ++v) {
+                    uint32_t o = 0;
+                    for (int i = 0; i < 8; ++i)
+                        if ((m >> i) & 1) o = (o << 1) | ((v >> i) & 1);
+                    t[size_t(m) * 256 + size_t(v)] = uint8_t(o);
+                }
+            uint8_t* p = h->dalloc<uint8_t>(t.size());
+            ck(cudaMemcpy(p, t.data(), t.size(), cudaMemcpyHostToDevice), "upload");
+            comp_tab = p;
+        }
         for (size_t i = 0; i < h->codes.size(); ++i) {
             const HostCode& c = h->codes[i];
             plb::DevCode& d = dc[i];
@@ -1039,6 +1058,8 @@ int pl_create(const pl_code* codes, int32_t ncodes, const pl_decoder* dec, int32
             d.crc_tab = c.crc_tab.empty() ? nullptr
                                           : static_cast<const uint64_t*>(up(c.crc_tab.data(), c.crc_tab.size() * 8));
             d.crc_c0 = c.crc_c0;
+            d.open_mask = static_cast<const uint8_t*>(up(c.open_mask.data(), c.open_mask.size()));
+            d.comp_tab = comp_tab;
         }
         h->d_codes = h->dalloc<plb::DevCode>(dc.size() * sizeof(plb::DevCode));
         ck(cudaMemcpy(h->d_codes, dc.data(), dc.size() * sizeof(plb::DevCode), cudaMemcpyHostToDevice),

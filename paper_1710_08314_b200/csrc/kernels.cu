@@ -2074,21 +2074,28 @@ __device__ void lane_frame(const LaunchParams& P, const DevCode& C, unsigned cha
         crc_ok = syn == 0;
     }
     if (active) {
+        // payload (extract_payload, prune_tree.hpp:78-105): the open bits of
+        // each codeword byte compacted by table (all-open bytes: a bit
+        // reversal) and streamed out MSB-first
         uint8_t* pay = P.payload + int64_t(frame) * P.payload_stride;
-        const int pb = (C.psize + 7) >> 3;
+        const int cbytes = (C.n + 7) >> 3;
+        uint32_t acc = 0;
+        int nb = 0, qb = 0;
         #pragma unroll 1
-        for (int qb = 0; qb < pb; ++qb) {
-            uint32_t byte = 0;
-            #pragma unroll
-            for (int b = 0; b < 8; ++b) {
-                const int j = 8 * qb + b;
-                if (j < C.psize) {
-                    const int pos = __ldg(C.info_pos + j);
-                    byte |= ((c.word(pos >> 5) >> (pos & 31)) & 1u) << (7 - b);
-                }
+        for (int j = 0; j < cbytes; ++j) {
+            const uint32_t m = __ldg(C.open_mask + j);
+            if (m == 0u) continue; // uniform: one code per warp
+            const uint32_t v = (c.word(j >> 2) >> ((j & 3) * 8)) & 0xffu;
+            const uint32_t bits = m == 0xffu ? __brev(v) >> 24 : uint32_t(__ldg(C.comp_tab + (m << 8) + v));
+            const int k = __popc(m);
+            acc = (acc << k) | bits;
+            nb += k;
+            if (nb >= 8) {
+                nb -= 8;
+                pay[qb++] = uint8_t(acc >> nb);
             }
-            pay[qb] = uint8_t(byte);
         }
+        if (nb > 0) pay[qb] = uint8_t(acc << (8 - nb));
         if (P.codeword) {
             uint8_t* cw = P.codeword + int64_t(frame) * P.codeword_stride;
             const int cb = (C.n + 7) >> 3;

@@ -61,6 +61,12 @@ struct DevCode {
     // syndrome = crc_c0 ^ XOR_j crc_tab[j][byte_j(codeword)], zero <=> pass.
     const uint64_t* crc_tab;    // (n/8) x 256
     uint64_t crc_c0;
+    // payload gather by codeword byte: open_mask[j] = the open positions
+    // among 8j..8j+7 (bit i = position 8j+i); comp_tab[m * 256 + v] = the
+    // bits of v selected by m in ascending position order, first one most
+    // significant (a universal 64 KB table)
+    const uint8_t* open_mask;   // ceil(n/8)
+    const uint8_t* comp_tab;
 };
 
 // ---- launch parameters ------------------------------------------------
