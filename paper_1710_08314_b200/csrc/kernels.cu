@@ -1909,6 +1909,22 @@ __device__ void lane_fg(const LaneCtx<R>& c, int d, int m, int lb, bool is_g) {
         const R* p = c.chunk(d, 0);
         R* q = out + c.lane * h;
         const uint32_t bits = is_g ? c.word(lb >> 5) >> (lb & 31) : 0u;
+        if constexpr (sizeof(R) == 1) {
+            // int8 nodes of 16 / 8 values: SWAR words (the chunk is m-byte aligned)
+            if (h == 8) {
+                const uint4 x = *reinterpret_cast<const uint4*>(p);
+                uint2 o;
+                o.x = is_g ? g_swar(x.x, x.z, bits & 15u) : f_swar(x.x, x.z);
+                o.y = is_g ? g_swar(x.y, x.w, (bits >> 4) & 15u) : f_swar(x.y, x.w);
+                *reinterpret_cast<uint2*>(q) = o;
+                return;
+            }
+            if (h == 4) {
+                const uint2 x = *reinterpret_cast<const uint2*>(p);
+                *reinterpret_cast<uint32_t*>(q) = is_g ? g_swar(x.x, x.y, bits & 15u) : f_swar(x.x, x.y);
+                return;
+            }
+        }
         #pragma unroll 1
         for (int j = 0; j < h; ++j) q[j] = is_g ? A::g(p[j], p[h + j], (bits >> j) & 1u) : A::f(p[j], p[h + j]);
     }
