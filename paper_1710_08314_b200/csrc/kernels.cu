@@ -1835,6 +1835,12 @@ struct LaneCtx {
         const int v = min(VE, n >> d);
         return d == 0 ? chan + c * v : pool(d) + (c * 32 + lane) * v;
     }
+    // chunk k of depth d is at base + k * stride (loop-invariant form of chunk())
+    __device__ __forceinline__ const R* chunk_base(int d, int& stride) const {
+        const int v = min(VE, n >> d);
+        stride = d == 0 ? v : 32 * v;
+        return d == 0 ? chan : pool(d) + lane * v;
+    }
     __device__ __forceinline__ uint32_t& word(int w) const { return ps[w * 32]; }
     __device__ void fill(int lb, int m, int bit) const {
         if (m >= 32) {
@@ -1877,19 +1883,23 @@ template <typename R, int U>
 __device__ __forceinline__ void lane_fg_chunks(const LaneCtx<R>& c, int d, int nc, int lb, bool is_g,
                                                R* out) {
     constexpr int VE = LaneCtx<R>::VE;
+    int cs;
+    const R* in = c.chunk_base(d, cs);
+    const R* in_b = in + nc * cs;
+    R* o = out + c.lane * VE;
     #pragma unroll 1
     for (int k = 0; k < nc; k += U) {
         Vec<R, VE> a[U], b[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            a[u] = vld<R, VE>(c.chunk(d, k + u));
-            b[u] = vld<R, VE>(c.chunk(d, k + u + nc));
+            a[u] = vld<R, VE>(in + (k + u) * cs);
+            b[u] = vld<R, VE>(in_b + (k + u) * cs);
         }
         const int pos = lb + k * VE;
         const uint32_t bits = is_g ? c.word(pos >> 5) >> (pos & 31) : 0u;
 #pragma unroll
         for (int u = 0; u < U; ++u)
-            vst<R, VE>(out + ((k + u) * 32 + c.lane) * VE, fg_compute<R, VE>(a[u], b[u], bits >> (u * VE), is_g));
+            vst<R, VE>(o + (k + u) * 32 * VE, fg_compute<R, VE>(a[u], b[u], bits >> (u * VE), is_g));
     }
 }
 
