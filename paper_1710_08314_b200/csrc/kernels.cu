@@ -1871,10 +1871,19 @@ __device__ __forceinline__ uint32_t vec_signs(const Vec<R, G>& x) {
 }
 template <typename R, int G>
 __device__ __forceinline__ bool vec_has_zero(const Vec<R, G>& x) {
-    bool z = false;
+    if constexpr (sizeof(R) == 1 && G >= 4) {
+        // a zero byte: (w - 0x01..) & ~w & 0x80.. is non-zero exactly then
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(&x.raw);
+        uint32_t z = 0;
 #pragma unroll
-    for (int i = 0; i < G; ++i) z |= Arith<R>::val(x.v[i]) == typename Arith<R>::M(0);
-    return z;
+        for (int k = 0; k < G / 4; ++k) z |= (w[k] - 0x01010101u) & ~w[k] & 0x80808080u;
+        return z != 0u;
+    } else {
+        bool z = false;
+#pragma unroll
+        for (int i = 0; i < G; ++i) z |= Arith<R>::val(x.v[i]) == typename Arith<R>::M(0);
+        return z;
+    }
 }
 
 // U chunks per iteration: 2U loads in flight per lane (the pools of the
@@ -2003,8 +2012,10 @@ __device__ bool lane_r1_nozero(const LaneCtx<R>& c, int d, int m) {
     constexpr int VE = LaneCtx<R>::VE;
     bool zero = false;
     if (m >= VE) {
+        int cs;
+        const R* in = c.chunk_base(d, cs);
         #pragma unroll 1
-        for (int k = 0; k < m / VE; ++k) zero |= vec_has_zero<R, VE>(vld<R, VE>(c.chunk(d, k)));
+        for (int k = 0; k < m / VE; ++k) zero |= vec_has_zero<R, VE>(vld<R, VE>(in + k * cs));
     } else {
         const R* p = c.chunk(d, 0);
         #pragma unroll 1
