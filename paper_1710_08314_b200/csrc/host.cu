@@ -1048,9 +1048,15 @@ int pl_create(const pl_code* codes, int32_t ncodes, const pl_decoder* dec, int32
                 if (bytes) ck(cudaMemcpy(p, src, bytes, cudaMemcpyHostToDevice), "upload");
                 return p;
             };
-            d.sched_list = static_cast<const uint32_t*>(up(c.sched_list.data(), c.sched_list.size() * 4));
-            d.sched_sc = static_cast<const uint32_t*>(up(c.sched_sc.data(), c.sched_sc.size() * 4));
-            d.sched_lane = static_cast<const uint32_t*>(up(c.sched_lane.data(), c.sched_lane.size() * 4));
+            // schedules carry one padding word (kernels may fetch one op ahead)
+            auto up_sched = [&](const std::vector<uint32_t>& v) {
+                std::vector<uint32_t> padded(v);
+                padded.push_back(0u);
+                return static_cast<const uint32_t*>(up(padded.data(), padded.size() * 4));
+            };
+            d.sched_list = up_sched(c.sched_list);
+            d.sched_sc = up_sched(c.sched_sc);
+            d.sched_lane = up_sched(c.sched_lane);
             d.nops_lane = int(c.sched_lane.size());
             d.nops_list = int(c.sched_list.size());
             d.nops_sc = int(c.sched_sc.size());

@@ -1929,7 +1929,13 @@ __device__ void lane_fg(const LaneCtx<R>& c, int d, int m, int lb, bool is_g) {
         R* q = out + c.lane * h;
         const uint32_t bits = is_g ? c.word(lb >> 5) >> (lb & 31) : 0u;
         if constexpr (sizeof(R) == 1) {
-            // int8 nodes of 16 / 8 values: SWAR words (the chunk is m-byte aligned)
+            // int8 nodes of 16 / 8 / 4 values: SWAR words (the chunk is m-byte aligned)
+            if (h == 2) {
+                const uint32_t x = *reinterpret_cast<const uint32_t*>(p);
+                const uint32_t o = is_g ? g_swar(x & 0xffffu, x >> 16, bits & 3u) : f_swar(x & 0xffffu, x >> 16);
+                *reinterpret_cast<uint16_t*>(q) = uint16_t(o);
+                return;
+            }
             if (h == 8) {
                 const uint4 x = *reinterpret_cast<const uint4*>(p);
                 uint2 o;
@@ -2076,9 +2082,13 @@ __device__ void lane_frame(const LaunchParams& P, const DevCode& C, unsigned cha
     __syncwarp();
     const uint32_t* sched = C.sched_lane;
     const int nops = C.nops_lane;
+    // the next schedule word is fetched one op ahead (the schedules carry a
+    // padding word)
+    uint32_t next = __ldg(sched);
     #pragma unroll 1
     for (int oi = 0; oi < nops; ++oi) {
-        const uint32_t op = __ldg(sched + oi);
+        const uint32_t op = next;
+        next = __ldg(sched + oi + 1);
         const int code = op_code(op), d = op_depth(op), m = 1 << op_logm(op), lb = op_lb(op);
         switch (code) {
         case OP_F:
@@ -2088,11 +2098,13 @@ __device__ void lane_frame(const LaunchParams& P, const DevCode& C, unsigned cha
         case OP_INFO: c.fill(lb, 1, A::val(*c.chunk(d, 0)) < M(0)); break;
         case OP_REP: c.fill(lb, m, lane_rep(c, d, m)); break;
         case OP_R1SC: {
-            const int skip = int(__ldg(sched + ++oi));
+            const int skip = int(next); // the word after OP_R1SC
+            ++oi;
             if (__all_sync(FULL, lane_r1_nozero(c, d, m))) {
                 lane_r1_hard(c, d, m, lb);
                 oi += skip;
             } // else: every lane runs the expanded recursion that follows
+            next = __ldg(sched + oi + 1);
             break;
         }
         default: break;
