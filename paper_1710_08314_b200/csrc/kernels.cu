@@ -1983,13 +1983,15 @@ __device__ int lane_rep(const LaneCtx<R>& c, int d, int m) {
     if (m > VE) {
         R* S = c.pool(d + 1) + c.lane * VE; // chunk k at S + k * 32 * VE
         int nc = m / VE;
+        int cs;
+        const R* in = c.chunk_base(d, cs);
         #pragma unroll 1
         for (int first = 1; nc > 1; first = 0) {
             const int hc = nc >> 1;
             #pragma unroll 1
             for (int k = 0; k < hc; ++k) {
-                const Vec<R, VE> a = first ? vld<R, VE>(c.chunk(d, k)) : vld<R, VE>(S + k * 32 * VE);
-                const Vec<R, VE> b = first ? vld<R, VE>(c.chunk(d, k + hc)) : vld<R, VE>(S + (k + hc) * 32 * VE);
+                const Vec<R, VE> a = first ? vld<R, VE>(in + k * cs) : vld<R, VE>(S + k * 32 * VE);
+                const Vec<R, VE> b = first ? vld<R, VE>(in + (k + hc) * cs) : vld<R, VE>(S + (k + hc) * 32 * VE);
                 vst<R, VE>(S + k * 32 * VE, fg_compute<R, VE>(a, b, 0u, true)); // g with u = 0: sat(a + b)
             }
             nc = hc;
@@ -2022,6 +2024,10 @@ __device__ bool lane_r1_nozero(const LaneCtx<R>& c, int d, int m) {
         const R* in = c.chunk_base(d, cs);
         #pragma unroll 1
         for (int k = 0; k < m / VE; ++k) zero |= vec_has_zero<R, VE>(vld<R, VE>(in + k * cs));
+    } else if (sizeof(R) == 1 && m >= 4) { // int8 nodes of 4 / 8 values: whole words
+        const uint32_t* p = reinterpret_cast<const uint32_t*>(c.chunk(d, 0));
+        #pragma unroll 1
+        for (int k = 0; k < (m >> 2); ++k) zero |= ((p[k] - 0x01010101u) & ~p[k] & 0x80808080u) != 0u;
     } else {
         const R* p = c.chunk(d, 0);
         #pragma unroll 1
@@ -2035,10 +2041,12 @@ __device__ void lane_r1_hard(const LaneCtx<R>& c, int d, int m, int lb) {
     constexpr int VE = LaneCtx<R>::VE;
     if (m >= VE) {
         uint32_t acc = 0;
+        int cs;
+        const R* in = c.chunk_base(d, cs);
         #pragma unroll 1
         for (int k = 0; k < m / VE; ++k) {
             const int pos = k * VE; // bit of the node
-            acc |= vec_signs<R, VE>(vld<R, VE>(c.chunk(d, k))) << (pos & 31);
+            acc |= vec_signs<R, VE>(vld<R, VE>(in + k * cs)) << (pos & 31);
             if (((pos + VE) & 31) == 0 || pos + VE >= m) {
                 if (m >= 32) {
                     c.word((lb + (pos & ~31)) >> 5) = acc;
@@ -2053,8 +2061,16 @@ __device__ void lane_r1_hard(const LaneCtx<R>& c, int d, int m, int lb) {
     } else {
         const R* p = c.chunk(d, 0);
         uint32_t acc = 0;
-        #pragma unroll 1
-        for (int i = 0; i < m; ++i) acc |= uint32_t(A::val(p[i]) < typename A::M(0)) << i;
+        if (sizeof(R) == 1 && m >= 4) { // sign bits of whole words
+            #pragma unroll 1
+            for (int k = 0; k < (m >> 2); ++k) {
+                const uint32_t w = reinterpret_cast<const uint32_t*>(p)[k];
+                acc |= ((((w >> 7) & 0x01010101u) * 0x01020408u) >> 24) << (4 * k);
+            }
+        } else {
+            #pragma unroll 1
+            for (int i = 0; i < m; ++i) acc |= uint32_t(A::val(p[i]) < typename A::M(0)) << i;
+        }
         const uint32_t mk = ((1u << m) - 1u) << (lb & 31);
         uint32_t& x = c.word(lb >> 5);
         x = (x & ~mk) | ((acc << (lb & 31)) & mk);
