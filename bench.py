@@ -262,8 +262,11 @@ def main():
     for _ in range(args.steps):
         dec.decode_batch(llr_d, code_id=cid_d, out=out)
         launches += dec.last_launches()
+        per = {}  # launches of one pass (an adaptive rung may issue two) summed
         for kd, l, ms in dec.last_kernel_ms():
-            kernel_ms.setdefault((kd, l), []).append(ms)
+            per[(kd, l)] = per.get((kd, l), 0.0) + ms
+        for k, ms in per.items():
+            kernel_ms.setdefault(k, []).append(ms)
     ev1.record(stream)
     torch.cuda.synchronize()
     barrier()

@@ -437,6 +437,10 @@ struct pl_handle {
     int64_t gscratch_bytes = 0;
     RungCfg sc_cfg;
     std::vector<RungCfg> rungs; // list rungs in ladder order
+    // adaptive rungs planned with several frames per warp also get a
+    // 1-frame-per-warp plan for small passes (lower latency per frame); the
+    // device picks one of the two launches from the pass's frame count
+    std::vector<RungCfg> rungs_small;
     // Execution contexts: the scratch and control buffers one decode in
     // flight needs.  pl_decode uses ex[0]; pl_decode_host alternates ex[0]
     // and ex[1] on two compute streams, so one chunk's decode can fill the
@@ -578,9 +582,9 @@ int skew_frame_area(int bytes, int fpw) {
     return bytes + (want - bytes % 128 + 128) % 128;
 }
 
-RungCfg plan_rung(const pl_handle& h, int l, bool list, bool ladder = false) {
+RungCfg plan_rung(const pl_handle& h, int l, bool list, bool ladder = false, int force_fpw = 0) {
     const char* forced = std::getenv("PLB_SEGMAX");
-    const char* forced_fpw = std::getenv("PLB_FPW");
+    const char* forced_fpw = force_fpw ? "1" : std::getenv("PLB_FPW");
     const int target = target_warps_per_sm();
     std::vector<int> cands;
     if (forced) cands.push_back(std::atoi(forced));
@@ -717,8 +721,11 @@ void run_decode(pl_handle& h, const void* llr, const int32_t* code_id, int64_t n
     int slot = 0;
 
     auto run = [&](const RungCfg& rc, bool list, int select, const int32_t* in_list,
-                   const int32_t* in_count, int32_t* out_list, int32_t* out_count) {
+                   const int32_t* in_count, int32_t* out_list, int32_t* out_count,
+                   int64_t count_lo = -1, int64_t count_hi = INT64_MAX) {
         plb::LaunchParams p = base;
+        p.count_lo = count_lo;
+        p.count_hi = count_hi;
         p.work = x.d_work + slot;
         p.frame_list = in_list;
         p.frame_count = in_count;
@@ -780,6 +787,24 @@ void run_decode(pl_handle& h, const void* llr, const int32_t* code_id, int64_t n
         bcount = x.d_counts + 15;
     };
 
+    // an adaptive rung: with a small-pass plan, two launches with
+    // complementary frame-count ranges.  Measured crossovers (FA@4.5 dB,
+    // N=2048): float passes gain from 32 lanes per frame up to one frame per
+    // resident warp (L=2 rung, 4.5k frames: 0.84 -> 0.63 ms); int8 / int16
+    // only with at most ~8 frames per SM (at 4.5k frames the 8-lane
+    // sub-warps stay faster: 0.42 vs 0.65 ms)
+    auto rung = [&](size_t i, const int32_t* in_list, const int32_t* in_count, int32_t* out_list,
+                    int32_t* out_count) {
+        const RungCfg& sm = h.rungs_small[i];
+        if (sm.grid > 0) {
+            const int64_t t = h.dec.precision == PL_F32 ? int64_t(sm.grid) * sm.wpb : int64_t(h.sms) * 8;
+            run(sm, true, 1, in_list, in_count, out_list, out_count, -1, t);
+            run(h.rungs[i], true, 1, in_list, in_count, out_list, out_count, t, INT64_MAX);
+        } else {
+            run(h.rungs[i], true, 1, in_list, in_count, out_list, out_count);
+        }
+    };
+
     switch (kind) {
     case PL_KIND_SC:
     case PL_KIND_SSC:
@@ -795,7 +820,7 @@ void run_decode(pl_handle& h, const void* llr, const int32_t* code_id, int64_t n
     case PL_KIND_PA_SSCL:
         bucket(h.sc_cfg);
         run(h.sc_cfg, false, 0, blist, bcount, x.d_lists[0], x.d_counts + 0);
-        run(h.rungs.back(), true, 1, x.d_lists[0], x.d_counts + 0, nullptr, nullptr);
+        rung(h.rungs.size() - 1, x.d_lists[0], x.d_counts + 0, nullptr, nullptr);
         break;
     case PL_KIND_FA_SSCL: {
         bucket(h.sc_cfg);
@@ -803,8 +828,8 @@ void run_decode(pl_handle& h, const void* llr, const int32_t* code_id, int64_t n
         int cur = 0;
         for (size_t i = 0; i < h.rungs.size(); ++i) {
             const bool last = i + 1 == h.rungs.size();
-            run(h.rungs[i], true, 1, x.d_lists[cur], x.d_counts + i,
-                last ? nullptr : x.d_lists[cur ^ 1], last ? nullptr : x.d_counts + i + 1);
+            rung(i, x.d_lists[cur], x.d_counts + i, last ? nullptr : x.d_lists[cur ^ 1],
+                 last ? nullptr : x.d_counts + i + 1);
             cur ^= 1;
         }
         break;
@@ -1077,12 +1102,20 @@ int pl_create(const pl_code* codes, int32_t ncodes, const pl_decoder* dec, int32
             for (int ll = 2; ll <= l; ll *= 2) h->rungs.push_back(plan_rung(*h, ll, true, true));
         else if (uses_list(kind))
             h->rungs.push_back(plan_rung(*h, l, true, adaptive(kind)));
+        for (const auto& r : h->rungs) {
+            RungCfg sm;
+            if (adaptive(kind) && r.fpw > 1 && r.team <= 1 && env_int("PLB_SMALL_RUNGS", 1))
+                sm = plan_rung(*h, r.l, true, true, 1);
+            h->rungs_small.push_back(sm);
+        }
         int64_t gs = 0;
         auto acc = [&](const RungCfg& r) {
             gs = std::max<int64_t>(gs, r.gscratch_total());
         };
         if (h->sc_cfg.grid) acc(h->sc_cfg);
         for (const auto& r : h->rungs) acc(r);
+        for (const auto& r : h->rungs_small)
+            if (r.grid) acc(r);
         h->gscratch_bytes = gs;
         ensure_exec(*h, 0);
         *out = h;

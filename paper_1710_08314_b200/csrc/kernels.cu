@@ -1690,6 +1690,7 @@ decode_kernel(const LaunchParams P) {
             // one frame per block: warp 0 controls, the others help
             __shared__ long long s_claim;
             const long long count = P.frame_list ? (long long)(*P.frame_count) : (long long)P.nframes;
+            if (count <= P.count_lo || count > P.count_hi) return;
             unsigned char* gs = static_cast<unsigned char*>(P.gscratch) + int64_t(blockIdx.x) * P.gscratch_per_frame;
             for (;;) {
                 if (threadIdx.x == 0) s_claim = (long long)atomicAdd(P.work, 1ull);
@@ -1707,6 +1708,7 @@ decode_kernel(const LaunchParams P) {
         }
     }
     const long long count = P.frame_list ? (long long)(*P.frame_count) : (long long)P.nframes;
+    if (count <= P.count_lo || count > P.count_hi) return;
     // Solo mode for passes with few frames (the upper FA rungs: a few
     // hundred frames or less, where a frame's latency, not the throughput,
     // sets the pass time): warp 0 of each block decodes with the shared

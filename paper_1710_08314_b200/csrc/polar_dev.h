@@ -103,6 +103,9 @@ struct LaunchParams {
     int32_t fpw;               // frames per warp (1, 2 or 4; >1 needs one code)
     int32_t team;              // >1: each block is a team of `team` warps decoding
                                // one frame (list passes, 32-lane kernels)
+    int64_t count_lo, count_hi;// the launch decodes only if count_lo < frames <= count_hi
+                               // (two launches with complementary ranges pick a
+                               // plan on the device from the pass's frame count)
     int32_t seg_solo;          // >0: solo mode when the pass has <= solo_max frames:
     int32_t solo_max;          // warp 0 of each block decodes with the whole block's
                                // shared memory (segments <= seg_solo in smem)

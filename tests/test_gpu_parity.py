@@ -359,16 +359,19 @@ def test_cfg4_like_l32(P, gpu, oracle_lib):
 def test_alternate_kernels(P, gpu, oracle_lib, prec, monkeypatch):
     """The opt-in / fallback launch paths stay bit-exact: team mode (a block
     of warps per frame at L = 16/32, PLB_TEAM), the warp-per-frame SC kernel
-    (PLB_SC_LANES=0), one frame per warp at small L (PLB_FPW=1), and the
+    (PLB_SC_LANES=0), one frame per warp at small L (PLB_FPW=1), the
     regular layout for small passes (PLB_SOLO=0; by default a pass with at
-    most one frame per block, as here, runs in solo mode)."""
+    most one frame per block, as here, runs in solo mode), and the
+    several-frames-per-warp plan of small adaptive rungs (PLB_SMALL_RUNGS=0;
+    by default a rung with few frames takes the 1-frame-per-warp launch)."""
     code = _code(P, 1024, 480, "32-GZIP")
     _, llr = P.channel(code, 2.0, 5, 0, 96, prec, 4.0 if prec == "i8" else 0.0)
     pr = P.PruningConfig(rep_max=8) if prec == "i8" else P.PruningConfig()
     for env, cases in [({"PLB_TEAM": "4", "PLB_TEAM_L": "16"}, [("ca_sscl", 16), ("ca_sscl", 32)]),
                        ({"PLB_SC_LANES": "0"}, [("ssc", 1), ("fa_sscl", 8)]),
                        ({"PLB_FPW": "1"}, [("ca_sscl", 4), ("sscl", 2)]),
-                       ({"PLB_SOLO": "0"}, [("ca_sscl", 8), ("fa_sscl", 32), ("sscl", 2)])]:
+                       ({"PLB_SOLO": "0"}, [("ca_sscl", 8), ("fa_sscl", 32), ("sscl", 2)]),
+                       ({"PLB_SMALL_RUNGS": "0"}, [("fa_sscl", 8), ("pa_sscl", 4)])]:
         for k, v in env.items():
             monkeypatch.setenv(k, v)
         for kind, l in cases:
