@@ -414,6 +414,7 @@ struct RungCfg {
     int fpw = 1; // frames per warp (sub-warp decoding, single-code batches)
     int team = 1; // >1: blocks of `team` warps, one frame each
     int seg_solo = 0; // solo-mode layout (warp 0 with the whole block's smem), 0 = none
+    int64_t small_max = 0; // small-pass plan of an adaptive rung: used up to this many frames
     bool lanes = false; // frame-per-lane SC kernel (smem / gscratch figures per 32-frame warp)
     int64_t gscratch_total() const {
         return int64_t(grid) * (team > 1 ? 1 : wpb * fpw) * gscratch_per_frame;
@@ -787,17 +788,13 @@ void run_decode(pl_handle& h, const void* llr, const int32_t* code_id, int64_t n
         bcount = x.d_counts + 15;
     };
 
-    // an adaptive rung: with a small-pass plan, two launches with
-    // complementary frame-count ranges.  Measured crossovers (FA@4.5 dB,
-    // N=2048): float passes gain from 32 lanes per frame up to one frame per
-    // resident warp (L=2 rung, 4.5k frames: 0.84 -> 0.63 ms); int8 / int16
-    // only with at most ~8 frames per SM (at 4.5k frames the 8-lane
-    // sub-warps stay faster: 0.42 vs 0.65 ms)
+    // an adaptive rung with a small-pass plan (pl_create): two launches
+    // with complementary frame-count ranges, the device picks
     auto rung = [&](size_t i, const int32_t* in_list, const int32_t* in_count, int32_t* out_list,
                     int32_t* out_count) {
         const RungCfg& sm = h.rungs_small[i];
         if (sm.grid > 0) {
-            const int64_t t = h.dec.precision == PL_F32 ? int64_t(sm.grid) * sm.wpb : int64_t(h.sms) * 8;
+            const int64_t t = sm.small_max;
             run(sm, true, 1, in_list, in_count, out_list, out_count, -1, t);
             run(h.rungs[i], true, 1, in_list, in_count, out_list, out_count, t, INT64_MAX);
         } else {
@@ -1104,8 +1101,26 @@ int pl_create(const pl_code* codes, int32_t ncodes, const pl_decoder* dec, int32
             h->rungs.push_back(plan_rung(*h, l, true, adaptive(kind)));
         for (const auto& r : h->rungs) {
             RungCfg sm;
-            if (adaptive(kind) && r.fpw > 1 && r.team <= 1 && env_int("PLB_SMALL_RUNGS", 1))
-                sm = plan_rung(*h, r.l, true, true, 1);
+            if (adaptive(kind) && r.team <= 1 && env_int("PLB_SMALL_RUNGS", 1)) {
+                if (r.fpw > 1) {
+                    // 32 lanes per frame.  Measured crossovers (FA@4.5 dB, N=2048):
+                    // float gains up to one frame per resident warp (L=2 rung,
+                    // 4.5k frames: 0.84 -> 0.63 ms); int8 / int16 only with at
+                    // most ~8 frames per SM (at 4.5k frames the 8-lane
+                    // sub-warps stay faster: 0.42 vs 0.65 ms)
+                    sm = plan_rung(*h, r.l, true, true, 1);
+                    sm.small_max = h->dec.precision == PL_F32 ? int64_t(sm.grid) * sm.wpb : int64_t(h->sms) * 8;
+                } else if (r.l >= 16) {
+                    // a team of 8 warps per frame (one frame per block, one
+                    // wave): L=32 with 48 frames 1.52 -> 0.79 ms float, 0.76
+                    // -> 0.63 int8; L=16 0.74 -> 0.53 float
+                    std::vector<int> cands;
+                    for (int sg = h->nmax; sg >= 8; sg >>= 1) cands.push_back(sg);
+                    if (cands.empty()) cands.push_back(h->nmax);
+                    sm = plan_team(*h, r.l, plb::kMaxTeam, cands);
+                    sm.small_max = sm.grid;
+                }
+            }
             h->rungs_small.push_back(sm);
         }
         int64_t gs = 0;
