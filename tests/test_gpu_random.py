@@ -45,7 +45,7 @@ def _random_case(P, rng):
     return code, kind, l, prec, pr
 
 
-@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("PLB_RANDOM_CASES", "60"))))
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("PLB_RANDOM_CASES", "200"))))
 def test_random_configuration(P, gpu, oracle_lib, ref_lib, seed):
     rng = np.random.default_rng(9000 + seed)
     code, kind, l, prec, pr = _random_case(P, rng)
