@@ -522,7 +522,7 @@ RungCfg plan_team(const pl_handle& h, int l, int team, const std::vector<int>& c
         c.seg_max = seg;
         c.wpb = team;
         c.team = team;
-        c.smem_per_frame = int(plb::smem_bytes_per_frame(h.nmax, l, h.esz, seg));
+        c.smem_per_frame = int(plb::smem_bytes_per_frame(h.nmax, l, h.esz, seg, 32));
         c.gscratch_per_frame = plb::gscratch_bytes_per_frame(h.nmax, l, h.esz, seg);
         const int nb = plb::occupancy_list(h.dec.precision, l, 1, c.smem_per_frame, team, true);
         if (nb <= 0) continue;
@@ -628,7 +628,7 @@ RungCfg plan_rung(const pl_handle& h, int l, bool list, bool ladder = false, int
                 c.seg_max = seg;
                 c.wpb = wpb;
                 c.fpw = fpw;
-                c.smem_per_frame = skew_frame_area(int(plb::smem_bytes_per_frame(h.nmax, l, h.esz, seg)), fpw);
+                c.smem_per_frame = skew_frame_area(int(plb::smem_bytes_per_frame(h.nmax, l, h.esz, seg, 32 / fpw)), fpw);
                 c.gscratch_per_frame = plb::gscratch_bytes_per_frame(h.nmax, l, h.esz, seg);
                 const int smem = c.smem_per_frame * fpw * wpb;
                 const int nb = list ? plb::occupancy_list(h.dec.precision, l, fpw, smem, wpb)
@@ -655,7 +655,7 @@ RungCfg plan_rung(const pl_handle& h, int l, bool list, bool ladder = false, int
     // shared-memory-resident layout in the area of all the block's warps
     if (pick.wpb > 1 && env_int("PLB_SOLO", 1)) {
         for (int seg = h.nmax; seg >= 1; seg >>= 1) {
-            if (plb::smem_bytes_per_frame(h.nmax, l, h.esz, seg) <= int64_t(pick.smem_per_frame) * pick.wpb) {
+            if (plb::smem_bytes_per_frame(h.nmax, l, h.esz, seg, 32 / pick.fpw) <= int64_t(pick.smem_per_frame) * pick.wpb) {
                 pick.seg_solo = seg;
                 break;
             }

@@ -375,27 +375,37 @@ __device__ __forceinline__ const R* frame_llr(const LaunchParams& P, int frame) 
 
 // ---- per-frame shared-memory area ----------------------------------------
 // (followed by the bufidx rows, [slot][depth] -> buffer index in the depth
-// pool, 16 bytes per slot of the pass's list size)
-struct alignas(16) Fixed {
-    uint8_t alive_list[32];  // rank -> slot, ascending
-    uint8_t freetab[32];     // k -> k-th free slot, ascending
-    uint8_t dsrc[32], dtgt[32]; // k-th duplicate of a fork: source, target
-    uint32_t met_s[32];      // metric by slot (fork hand-over)
+// pool, 16 bytes per slot of the pass's list size).  Arrays indexed by slot
+// or rank hold NS = SW entries (a sub-warp of SW lanes decodes L <= SW
+// paths): the 16-lane kernels (L = 4, 8) use a 592-byte area instead of
+// 1 040, which leaves room for more depth pools in shared memory (cfg1
+// +1.8%).
+template <int NS>
+struct alignas(16) FixedS {
+    uint8_t alive_list[NS];  // rank -> slot, ascending
+    uint8_t freetab[NS];     // k -> k-th free slot, ascending
+    uint8_t dsrc[NS], dtgt[NS]; // k-th duplicate of a fork: source, target
+    uint32_t met_s[NS];      // metric by slot (fork hand-over)
     uint64_t pool[16];       // generic address of each depth pool
     uint32_t alive_w;        // alive-slot mask (read by the helper warps of a team)
     uint32_t pad_[3];
     union {
         struct {
-            int32_t st_i1[32], st_i2[32], st_w[32]; // per-rank node statistics
-            uint32_t st_a1[32], st_a2[32];
+            int32_t st_i1[NS], st_i2[NS], st_w[NS]; // per-rank node statistics
+            uint32_t st_a1[NS], st_a2[NS];
         };
         // OP_SCSUB: per-level LLRs of the subtree, [level][lane], levels
         // 0..4 (the leaf level of a 32-subtree is never read back; SC pass,
-        // never live together with a node's statistics)
-        uint32_t scv[5 * 32];
+        // never live together with a node's statistics; 32-lane kernels)
+        uint32_t scv[5 * (NS == 32 ? 32 : 1)];
     };
 };
-static_assert(sizeof(Fixed) % 16 == 0, "fixed area alignment");
+static_assert(sizeof(FixedS<8>) % 16 == 0 && sizeof(FixedS<16>) % 16 == 0 && sizeof(FixedS<32>) % 16 == 0,
+              "fixed area alignment");
+// bytes of the fixed area of an SW-lane kernel
+__host__ __device__ constexpr int fixed_bytes(int sw) {
+    return sw >= 32 ? int(sizeof(FixedS<32>)) : sw >= 16 ? int(sizeof(FixedS<16>)) : int(sizeof(FixedS<8>));
+}
 
 __host__ __device__ inline int ilog2(int v) {
     int r = 0;
@@ -415,9 +425,9 @@ struct LayoutQ {
 // slots falls into different banks), odd below.
 __host__ __device__ inline int row_stride(int rw) { return rw >= 4 ? rw + 4 : (rw | 1); }
 
-__host__ __device__ inline LayoutQ layout_query(int n, int l, int esz, int segmax, int want_d) {
+__host__ __device__ inline LayoutQ layout_query(int n, int l, int esz, int segmax, int want_d, int sw) {
     LayoutQ q{};
-    int off = int(sizeof(Fixed)) + align16(16 * l);
+    int off = fixed_bytes(sw) + align16(16 * l);
     q.rw = n >= 32 ? n / 32 : 1;
     q.psum_off = off;
     off = align16(off + 4 * l * row_stride(q.rw));
@@ -457,7 +467,7 @@ struct Ctx {
     int n, l;
     unsigned lmask;
     const R* chan;
-    Fixed* fx;
+    FixedS<SW>* fx;
     uint32_t* ps;
     int rw;
     unsigned alive; // sub-warp-uniform alive-slot mask
@@ -1352,8 +1362,8 @@ __device__ void setup_ctx(Ctx<R, SW>& cx, const LaunchParams& P, const DevCode& 
     cx.l = l;
     cx.lmask = l >= 32 ? FULL : ((1u << l) - 1u);
     cx.chan = frame_llr<R>(P, frame);
-    cx.fx = reinterpret_cast<Fixed*>(sm);
-    const LayoutQ q0 = layout_query(C.n, l, int(sizeof(R)), segmax, 0);
+    cx.fx = reinterpret_cast<FixedS<SW>*>(sm);
+    const LayoutQ q0 = layout_query(C.n, l, int(sizeof(R)), segmax, 0, SW);
     cx.ps = reinterpret_cast<uint32_t*>(sm + q0.psum_off);
     cx.rw = q0.rw;
     // (constants outside team kernels: the team code folds away)
@@ -1362,7 +1372,7 @@ __device__ void setup_ctx(Ctx<R, SW>& cx, const LaunchParams& P, const DevCode& 
     cx.tstride = TEAM ? 32 * P.team : SW;
     #pragma unroll 1
     for (int d = cx.lane + 1; d <= C.stages; d += SW) {
-        const LayoutQ q = layout_query(C.n, l, int(sizeof(R)), segmax, d);
+        const LayoutQ q = layout_query(C.n, l, int(sizeof(R)), segmax, d, SW);
         cx.fx->pool[d] = reinterpret_cast<uint64_t>((q.pool_in_smem ? sm : gs) + q.pool_off);
     }
     if (cx.lane == 0) *reinterpret_cast<uint4*>(cx.bix()) = make_uint4(0, 0, 0, 0);
@@ -1638,8 +1648,8 @@ __device__ void team_helper(const LaunchParams& P, const DevCode& C, unsigned ch
     cx.n = C.n;
     cx.l = P.l;
     cx.chan = frame_llr<R>(P, frame);
-    cx.fx = reinterpret_cast<Fixed*>(sm);
-    const LayoutQ q0 = layout_query(C.n, P.l, int(sizeof(R)), P.seg_smem_max, 0);
+    cx.fx = reinterpret_cast<FixedS<32>*>(sm);
+    const LayoutQ q0 = layout_query(C.n, P.l, int(sizeof(R)), P.seg_smem_max, 0, 32);
     cx.ps = reinterpret_cast<uint32_t*>(sm + q0.psum_off);
     cx.rw = q0.rw;
     cx.team = P.team;
@@ -2307,11 +2317,11 @@ int occupancy(int kv, int fpw, int smem, int wpb, bool team = false) {
 
 } // namespace
 
-int64_t smem_bytes_per_frame(int nmax, int l, int elem_bytes, int seg_smem_max) {
-    return layout_query(nmax, l, elem_bytes, seg_smem_max, 0).smem_total;
+int64_t smem_bytes_per_frame(int nmax, int l, int elem_bytes, int seg_smem_max, int sw) {
+    return layout_query(nmax, l, elem_bytes, seg_smem_max, 0, sw).smem_total;
 }
 int64_t gscratch_bytes_per_frame(int nmax, int l, int elem_bytes, int seg_smem_max) {
-    return layout_query(nmax, l, elem_bytes, seg_smem_max, 0).gmem_total;
+    return layout_query(nmax, l, elem_bytes, seg_smem_max, 0, 32).gmem_total;
 }
 int frames_per_warp_max(int l) { return l <= 2 ? 4 : l <= 8 ? 2 : 1; }
 bool frames_per_warp_ok(int l, int fpw) { return fpw == 1 || fpw == frames_per_warp_max(l); }

@@ -115,7 +115,8 @@ constexpr int kMaxWarpsPerBlock = 4; // a block is 1, 2 or 4 independent warps
 constexpr int kMaxTeam = 8;          // ... or a team of up to 8 warps on one frame
 
 // Bytes of shared memory / global scratch one in-flight frame needs.
-int64_t smem_bytes_per_frame(int nmax, int l, int elem_bytes, int seg_smem_max);
+// sw: lanes per frame of the kernel (32 / frames per warp; team and SC kernels 32)
+int64_t smem_bytes_per_frame(int nmax, int l, int elem_bytes, int seg_smem_max, int sw);
 int64_t gscratch_bytes_per_frame(int nmax, int l, int elem_bytes, int seg_smem_max);
 // Frames per warp of the sub-warp kernel of list size l (a list pass runs
 // either that many or 1).
