@@ -720,7 +720,50 @@ __device__ void fork_apply(Ctx<R, SW>& cx, const typename Arith<R>::M (&cm)[CPL]
         else key[0] = sort_runs<K, SW>(key[0], lane, lgrun);
     } else {
         // only the best keep <= SW are needed, in order
-        top_regs<K, CPL, SW>(key, lane, (ncand + SW - 1) / SW, lgrun);
+        int nreg = (ncand + SW - 1) / SW;
+        if constexpr (!A::kFixed && SW == 32) {
+            // L = 32 float, all paths alive: every path's smallest candidate
+            // (the head of its sorted run) has a metric <= T = the largest of
+            // them, so >= L candidates do and none with a larger metric can
+            // be kept.  Survivors (99% of the 128-candidate R1 forks keep <= 64,
+            // measured at cfg4) are compacted in emission order into two
+            // registers through the node-statistics area (the float path
+            // carries its decisions in registers, the statistics are spent):
+            // cfg4 L=32 +5% (the 64-candidate REP / SPC forks: -1%, not done).
+            if (ncand > 2 * SW && __popc(cx.alive) == cx.l && lgrun > 0) {
+                uint32_t hb = 0;
+#pragma unroll
+                for (int k = 0; k < CPL; ++k)
+                    if ((lane & ((1 << lgrun) - 1)) == 0 && lane + SW * k < ncand)
+                        hb = max(hb, uint32_t(key[k] >> 32));
+                const uint32_t t = __reduce_max_sync(FULL, hb);
+                unsigned bal[CPL];
+                int cnt = 0;
+#pragma unroll
+                for (int k = 0; k < CPL; ++k) {
+                    bal[k] = __ballot_sync(FULL, lane + SW * k < ncand && uint32_t(key[k] >> 32) <= t);
+                    cnt += __popc(bal[k]);
+                }
+                if (cnt <= 2 * SW) {
+                    K* stage = reinterpret_cast<K*>(cx.fx->st_i1);
+                    int base = 0;
+#pragma unroll
+                    for (int k = 0; k < CPL; ++k) {
+                        if ((bal[k] >> lane) & 1u) stage[base + __popc(bal[k] & lanemask_lt())] = key[k];
+                        base += __popc(bal[k]);
+                    }
+                    __syncwarp();
+                    key[0] = lane < cnt ? stage[lane] : A::kKeyMax;
+                    key[1] = lane + SW < cnt ? stage[SW + lane] : A::kKeyMax;
+#pragma unroll
+                    for (int k = 2; k < CPL; ++k) key[k] = A::kKeyMax;
+                    __syncwarp();
+                    nreg = cnt > SW ? 2 : 1;
+                    lgrun = 0;
+                }
+            }
+        }
+        top_regs<K, CPL, SW>(key, lane, nreg, lgrun);
     }
     const int keep = min(cx.l, ncand);
     const bool kept = lane < keep;
