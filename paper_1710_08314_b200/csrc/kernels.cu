@@ -1439,7 +1439,7 @@ __device__ void list_frame(const LaunchParams& P, const DevCode& C, unsigned cha
     using M = typename A::M;
     constexpr int CW = kv_cw(KV, SW), MAXW = kv_maxw(KV, SW);
     Ctx<R, SW> cx;
-    setup_ctx<TEAM>(cx, P, C, sm, gs, frame, sw, P.l, segmax);
+    setup_ctx<TEAM>(cx, P, C, sm, gs, frame, sw, kv_l(KV), segmax); // P.l == kv_l(KV)
     const int lane = cx.lane;
     const uint32_t* sched = C.sched_list;
     const int nops = C.nops_list;
