@@ -60,6 +60,38 @@ def _raise(rc: int, msg: str):
     raise DeviceError(msg)
 
 
+def pack_frames(frames, dtype):
+    """Packed layout of variable-length frames (pl_decode_packed): frame i
+    at element offset off[i], ascending, each 16-byte aligned."""
+    dt = np.dtype(dtype)
+    align = 16 // dt.itemsize
+    off = np.zeros(len(frames), np.int64)
+    pos = 0
+    for i, f in enumerate(frames):
+        off[i] = pos
+        pos += -(-len(f) // align) * align
+    buf = np.zeros(max(pos, align), dt)
+    for i, f in enumerate(frames):
+        buf[off[i]: off[i] + len(f)] = f
+    return buf, off
+
+
+def pack_batch(llr: np.ndarray, ns: np.ndarray):
+    """pack_frames of a padded batch (frame f: llr[f, :ns[f]]), vectorised
+    per frame length."""
+    align = 16 // llr.dtype.itemsize
+    ns = np.asarray(ns, np.int64)
+    sz = -(-ns // align) * align
+    off = np.zeros(ns.size, np.int64)
+    if ns.size > 1:
+        np.cumsum(sz[:-1], out=off[1:])
+    buf = np.zeros(max(int(sz.sum()), align), llr.dtype)
+    for n in np.unique(ns):
+        rows = np.flatnonzero(ns == n)
+        buf[(off[rows][:, None] + np.arange(n)).ravel()] = llr[rows, :n].ravel()
+    return buf, off
+
+
 def load_frozen_file(path: str):
     """load_frozen_file (code.cpp:164-185) -> (n, k, frozen mask as uint8)."""
     n, k = C.c_int32(), C.c_int32()
@@ -437,32 +469,12 @@ class FrameDecoder:
         n) -> (packed host buffer, element offsets): each frame starts 16-byte
         aligned, in order (the layout pl_decode_packed / pl_decode_host_packed
         take)."""
-        dt = self._torch.empty(0, dtype=self.llr_dtype).numpy().dtype
-        align = 16 // dt.itemsize
-        off = np.zeros(len(frames), np.int64)
-        pos = 0
-        for i, f in enumerate(frames):
-            off[i] = pos
-            pos += -(-len(f) // align) * align
-        buf = np.zeros(max(pos, align), dt)
-        for i, f in enumerate(frames):
-            buf[off[i]: off[i] + len(f)] = f
-        return buf, off
+        return pack_frames(frames, self._torch.empty(0, dtype=self.llr_dtype).numpy().dtype)
 
     def pack_batch(self, llr: np.ndarray, code_id: np.ndarray):
         """A padded mixed batch (frames x pl_llr_stride, frame f valid up to
         its code's n) -> (packed buffer, offsets), vectorised per code length."""
-        dt = self._torch.empty(0, dtype=self.llr_dtype).numpy().dtype
-        align = 16 // dt.itemsize
-        ns = np.array([c.n for c in self.codes], np.int64)[np.asarray(code_id)]
-        sz = -(-ns // align) * align
-        off = np.zeros(ns.size, np.int64)
-        np.cumsum(sz[:-1], out=off[1:])
-        buf = np.zeros(max(int(sz.sum()), align), dt)
-        for n in np.unique(ns):
-            rows = np.flatnonzero(ns == n)
-            buf[(off[rows][:, None] + np.arange(n)).ravel()] = llr[rows, :n].ravel()
-        return buf, off
+        return pack_batch(llr, np.array([c.n for c in self.codes], np.int64)[np.asarray(code_id)])
 
     def decode_packed(self, llr, offsets, code_id=None, out=None, codeword: bool = False, stream=None):
         """Device-resident packed frames: llr (1-D CUDA tensor), offsets

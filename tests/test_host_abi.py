@@ -244,3 +244,22 @@ def test_no_cpu_fallback(P):
     code = P.make_code(16, 8, P.construct_frozen(16, 8, 0.5))
     with pytest.raises(P.DeviceError):
         P.FrameDecoder(code, "sscl", 4)
+
+
+def test_packed_layout():
+    """pack_frames / pack_batch (the pl_decode_packed layout): ascending,
+    16-byte aligned offsets, each frame's values in place, both agree."""
+    import numpy as np
+
+    from paper_1710_08314_b200.polar import pack_batch, pack_frames
+
+    rng = np.random.default_rng(5)
+    for dt in (np.float32, np.int8, np.int16):
+        ns = rng.choice([8, 16, 128, 256, 1024], 300)
+        llr = rng.integers(-100, 100, (300, 1024)).astype(dt)
+        buf, off = pack_frames([llr[f, :ns[f]] for f in range(300)], dt)
+        b2, o2 = pack_batch(llr, ns)
+        assert np.array_equal(buf, b2) and np.array_equal(off, o2)
+        assert (off * np.dtype(dt).itemsize % 16 == 0).all() and (np.diff(off) >= ns[:-1]).all()
+        for f in range(300):
+            assert np.array_equal(buf[off[f]: off[f] + ns[f]], llr[f, :ns[f]])
