@@ -1310,7 +1310,8 @@ int decode_host_impl(pl_handle* h, const void* llr, const int64_t* offsets, cons
         // ~20 chunks so the copies of one chunk overlap the decode of another
         // and the pipeline fill / drain stays short (measured: cfg1 e2e 16.2 ->
         // 16.7 Gb/s going from 8 to 16 chunks, 18.50 -> 18.61 at ~21; float
-        // cfg0 best at 8192 frames).
+        // cfg0 best at 8192 frames).  Multi-code batches keep 16: every chunk
+        // also buckets its frames by code (cfg3 e2e 5.6 at 16, 5.2 at 20).
         // Adaptive kinds on int8 LLRs: ~8 chunks, since every chunk pays the
         // latency of the upper ladder rungs (a few frames each) and the int8
         // copies are short (measured FA@4.5 dB int8 e2e 33.1 -> 39.2-40.7
@@ -1320,6 +1321,7 @@ int decode_host_impl(pl_handle* h, const void* llr, const int64_t* offsets, cons
         const int64_t chunk = cs ? std::max<int64_t>(1, std::atoll(cs))
                               : adaptive(h->dec.kind) && h->esz == 1
                                   ? std::clamp<int64_t>((nframes + 7) / 8, 8192, 131072)
+                              : h->codes.size() > 1 ? std::clamp<int64_t>((nframes + 15) / 16, 8192, 65536)
                                                   : std::clamp<int64_t>((nframes + 19) / 20, 8192, 65536);
         const int64_t in_bytes = h->nmax * int64_t(h->esz);
         const int64_t nchunks = (nframes + chunk - 1) / chunk;
