@@ -7,16 +7,25 @@ GA frozen set @4.5 dB, CA-SCL L=8 with R0/R1/REP_8-/SPC4 pruning, int8 LLRs
 One step = one decode of that batch (inputs resident in HBM for `value`;
 host buffers with the copies inside the timed region for `e2e`).
 `--workload` selects the other BASELINE configs (cfg0, cfg2_{2.5,3.5,4.5},
-cfg3 mixed-MCS, cfg4_L{8,16,32}).
+cfg3 mixed-MCS, cfg4_L{8,16,32}); `--extra` appends a `workloads` block with
+the same measurements of further configs (default: cfg0 and the paper's
+FA-SCL points cfg2 @ 4.5 / 3.5 dB).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg1]
   python bench.py --impl reference ...   # the reference's own CPU decoder
+
+Multi-GPU: `--gpus N` without a torchrun environment relaunches itself
+under torch.distributed.run with N local ranks, one GPU each (NCCL); rank r
+decodes global frames [r*F, (r+1)*F) (weak scaling, shard.frame_range) and
+the only collectives are one 4 x i64 counter SUM per workload and the
+max-over-ranks of the timed region (sim.cpp:84-109, test_sim.cpp:37-66).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import tempfile
@@ -28,6 +37,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "decoded info throughput (Gb/s) N=2048 K=1723"
+DATA = "synthetic: BPSK-AWGN frames keyed by (seed 42, global frame index), FrameRng semantics"
+EXTRA_DEFAULT = "cfg0,cfg2_4.5,cfg2_3.5"
+# ncu counters of the current kernels (profiles/traffic.py); the newest round's file wins
+COUNTERS_FILES = [os.path.join(ROOT, "profiles", f) for f in ("r02_traffic.json", "r01_traffic.json")]
 
 
 def parse():
@@ -37,17 +50,42 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="cfg1")
+    ap.add_argument("--extra", default=EXTRA_DEFAULT,
+                    help="comma-separated further workloads for the `workloads` block, or 'none'")
+    ap.add_argument("--extra-steps", type=int, default=5)
     ap.add_argument("--frames", type=int, default=0, help="override frames per GPU")
     ap.add_argument("--e2e-steps", type=int, default=0)
     ap.add_argument("--cpu-sample", type=int, default=16384)
     ap.add_argument("--ref-sample", type=int, default=16384)
+    ap.add_argument("--parity-sample", type=int, default=4096)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--allow-shared", action="store_true",
+                    help="let more ranks than GPUs share devices over gloo (a path exercise, "
+                         "not a scaling number)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="the multi-rank plumbing only (launch, frame ranges, input generation, "
+                         "counter reduction) with no decode; runs without a GPU")
     return ap.parse_args()
 
 
 def dist_env():
     return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
             int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def relaunch(args) -> int:
+    """`--gpus N` outside torchrun: re-exec under torch.distributed.run with
+    N local ranks on 127.0.0.1 (rank 0 prints the JSON line)."""
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__), *sys.argv[1:]]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.call(cmd, env=env)
 
 
 def sample_clocks_start(gpu_index: int):
@@ -106,38 +144,57 @@ def dtype_of(wl):
     return {"i8": "int8", "i16": "int16"}.get(wl.precision, "f32")
 
 
-def kernel_counters(wl, key, frames):
-    """ncu counters of this workload's pass kernel `key` (sc_L1 / list_L<l>),
-    per launch of the default batch (profiles/traffic.py, from one committed
-    ncu capture per workload); counts scale with the batch size.  None if
-    absent."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as fh:
-            t = json.load(fh)[wl.name]
-        c = dict(t["kernels"][key])
-    except (OSError, KeyError, ValueError):
-        return None
-    s = frames / t["frames"]
-    for k in ("dram_bytes", "dram_read_bytes", "dram_write_bytes", "warp_inst"):
-        c[k] *= s
-    c["source"] = t["source"]
-    return c
+def esize(wl):
+    return {"f32": 4, "i16": 2}.get(wl.precision, 1)
+
+
+def ncu_counters(wl):
+    """ncu counters of this workload's pass kernels (profiles/traffic.py,
+    one committed ncu capture per workload of its default batch): {key:
+    counters}, the capture's frame count; None if absent."""
+    for path in COUNTERS_FILES:
+        try:
+            with open(path) as fh:
+                t = json.load(fh)[wl.name]
+            t["source"] = f"{os.path.relpath(path, ROOT)}: {t['source']}"
+            return t
+        except (OSError, KeyError, ValueError):
+            continue
+    return None
 
 
 def common_config(wl, frames_per_gpu, ws):
     """The config both arms report (the driver compares like with like)."""
-    esz = {"f32": 4, "i16": 2}.get(wl.precision, 1)
     return {**wl.describe(), "frames_per_gpu": frames_per_gpu,
             "global_frames": frames_per_gpu * ws, "parallelism": f"frame-range shards x{ws}",
-            "l2": "inputs larger than L2 (%.0f MB per GPU per step)" % (frames_per_gpu * wl.n * esz / 1e6)}
+            "l2": "inputs larger than L2 (%.0f MB per GPU per step)" % (frames_per_gpu * wl.n * esize(wl) / 1e6)}
 
+
+def mapped_native_libs():
+    """The in-tree / oracle .so files this process has mapped."""
+    out = set()
+    try:
+        with open("/proc/self/maps") as fh:
+            for line in fh:
+                p = line.split()[-1] if line.split() else ""
+                if p.endswith(".so") and (p.startswith(ROOT) or "/_ref/" in p):
+                    out.add(os.path.relpath(p, ROOT))
+    except OSError:
+        pass
+    return sorted(out)
+
+
+# --------------------------------------------------------------------------
+# the reference's own CPU decoder (checker / baseline; oracle/_ref only)
 
 def reference_decode(O, codes, cid, llr, wl, nthr):
     """The compiled reference FrameDecoder<R> over a batch (per code for
-    mixed batches); returns payload/crc_ok/esc/metric arrays and the seconds
-    spent decoding."""
+    mixed batches); `codes` = [(n, k, crc text, frozen mask)]. Returns
+    payload/crc_ok/esc/metric arrays and the seconds spent decoding."""
     nf = llr.shape[0]
-    pb = max((c.payload_size + 7) // 8 for c in codes)
+    from paper_1710_08314_b200.workload import crc_width
+
+    pb = max((k + crc_width(c) + 7) // 8 for _, k, c, _ in codes)
     out = {"payload": np.zeros((nf, pb), np.uint8), "crc_ok": np.zeros(nf, np.uint8),
            "esc": np.zeros(nf, np.uint8), "metric": np.zeros(nf, np.float64)}
     secs = 0.0
@@ -145,10 +202,9 @@ def reference_decode(O, codes, cid, llr, wl, nthr):
     for i, rows in groups:
         if rows.size == 0:
             continue
-        c = codes[i]
-        ref = O.Reference(c.n, c.k, c.frozen, c.crc.raw() if c.crc else "", wl.kind, wl.l,
-                          wl.precision, wl.pruning.as_tuple())
-        x = np.ascontiguousarray(llr[rows, : c.n])
+        n, k, crc, fz = codes[i]
+        ref = O.Reference(n, k, fz, crc, wl.kind, wl.l, wl.precision, wl.pruning.as_tuple())
+        x = np.ascontiguousarray(llr[rows, :n])
         t0 = time.perf_counter()
         r = ref.decode(x, nthr)
         secs += time.perf_counter() - t0
@@ -157,14 +213,48 @@ def reference_decode(O, codes, cid, llr, wl, nthr):
     return out, secs
 
 
+def reference_inputs(O, wl, frame0, nframes, nthr):
+    """Codes and inputs built by the reference alone: frozen masks from the
+    committed frozen files (load_frozen_file, code.cpp:164-185) and frames
+    from FrameRng / random_payload / encode_systematic / transmit
+    (channel.hpp:17-89) -- byte-identical to the product arm's host channel
+    (tests/test_oracle.py)."""
+    from paper_1710_08314_b200.workload import MixedWorkload
+
+    codes = []
+    for n, k, crc, path in wl.code_specs():
+        n2, _, fz = O.ref_frozen_load(path)
+        assert n2 == n, path
+        codes.append((n, k, crc, fz))
+    if isinstance(wl, MixedWorkload):
+        cid = wl.code_ids(frame0, nframes, len(codes))
+        nmax = max(c[0] for c in codes)
+        dt = {"f32": np.float32, "i8": np.int8, "i16": np.int16}[wl.precision]
+        llr = np.zeros((nframes, nmax), dt)
+        ks = np.zeros(nframes, np.int64)
+        for i, (n, k, crc, fz) in enumerate(codes):
+            rows = np.flatnonzero(cid == i)
+            if rows.size:
+                _, x = O.ref_channel_ids(n, k, fz, crc, wl.ebn0_db, 42,
+                                         rows.astype(np.uint64) + np.uint64(frame0),
+                                         wl.precision, wl.scale, nthr)
+                llr[rows, :n] = x
+                ks[rows] = k
+        return codes, cid, ks, llr
+    n, k, crc, fz = codes[0]
+    _, llr = O.ref_channel(n, k, fz, crc, wl.ebn0_db, 42, frame0, nframes, wl.precision,
+                           wl.scale, nthr)
+    return codes, None, np.full(nframes, k, np.int64), llr
+
+
 def run_reference(args):
     """The reference's own CPU decoder (oracle/_ref: FrameDecoder<R> compiled
-    from /root/reference/proj), all host threads, bounded sample per step."""
+    from /root/reference/proj), all host threads, bounded sample per step.
+    Nothing of this repo's product library is loaded in this process."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
-    from paper_1710_08314_b200.workload import WORKLOADS, make_batch
-    wl = WORKLOADS[args.workload]
+    from paper_1710_08314_b200.workload import WORKLOADS
     try:
         from oracle import oracle as O
         O.Reference.lib()
@@ -172,53 +262,128 @@ def run_reference(args):
         print(json.dumps({"impl": "reference", "unavailable": f"oracle/_ref not loadable: {e}"}))
         return 0
     nthr = os.cpu_count() or 1
+
+    def one(wl, nf, steps):
+        codes, cid, ks, llr = reference_inputs(O, wl, 0, nf, nthr)
+        w = max(nthr, nf // 8)
+        reference_decode(O, codes, cid[:w] if cid is not None else None, llr[:w], wl, nthr)  # warm-up
+        secs = 0.0
+        for _ in range(steps):
+            secs += reference_decode(O, codes, cid, llr, wl, nthr)[1]
+        dt = secs / steps
+        return float(ks.sum()) / dt / 1e9, dt
+
+    wl = WORKLOADS[args.workload]
     nf = args.ref_sample
-    codes, cid, info, ks, llr = make_batch(wl, 0, nf, nthreads=nthr)
-    w = max(nthr, nf // 8)
-    reference_decode(O, codes, cid[:w] if cid is not None else None, llr[:w], wl, nthr)  # warm-up
-    secs = 0.0
-    for _ in range(args.steps):
-        secs += reference_decode(O, codes, cid, llr, wl, nthr)[1]
-    dt = secs / args.steps
-    gbps = float(ks.sum()) / dt / 1e9
+    gbps, dt = one(wl, nf, args.steps)
     out = {
         "impl": "reference", "metric": METRIC, "value": gbps, "unit": "Gb/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype_of(wl),
-        "data": "synthetic: BPSK-AWGN frames keyed by (seed 42, global frame index), FrameRng semantics",
-        "config": common_config(wl, args.frames or wl.frames, ws),
+        "data": DATA, "config": common_config(wl, args.frames or wl.frames, ws),
         "reference_sample_frames_per_step": nf,
         "cpu_baseline": {"value": gbps, "unit": "Gb/s", "cores": nthr, "kind": "reference",
                          "sample": f"{nf} frames of {wl.name} per step, FrameDecoder<R> per thread"},
         "e2e": {"value": gbps, "unit": "Gb/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    extras = [] if args.extra in ("", "none") else [w for w in args.extra.split(",") if w != args.workload]
+    if extras:
+        out["workloads"] = []
+        for name in extras:
+            w2 = WORKLOADS[name]
+            g2, dt2 = one(w2, args.parity_sample, 2)
+            out["workloads"].append({"workload": name, "config": w2.describe(), "value": g2,
+                                     "unit": "Gb/s", "ms_per_step": dt2 * 1e3,
+                                     "sample_frames_per_step": args.parity_sample, "cores": nthr})
+    out["native_so_loaded"] = mapped_native_libs()
     print(json.dumps(out))
     return 0
 
 
-def main():
-    args = parse()
-    if args.impl == "reference":
-        return run_reference(args)
-    ws, rank, local = dist_env()
-    import torch
+# --------------------------------------------------------------------------
+# the multi-rank plumbing without a decode (CPU test of the N>1 path)
+
+def run_dry(args):
+    ws, rank, _ = dist_env()
     import torch.distributed as dist
+    from paper_1710_08314_b200.shard import frame_range
+    from paper_1710_08314_b200.workload import WORKLOADS, make_batch
 
-    ndev = torch.cuda.device_count()
-    shared = ws > ndev  # more ranks than GPUs: only for exercising the path
     if ws > 1:
-        if shared:
-            dist.init_process_group("gloo")
-        else:
-            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    local = local % ndev
-    torch.cuda.set_device(local)
-    import paper_1710_08314_b200 as P
-    from paper_1710_08314_b200.shard import Counters, all_reduce_counters, frame_range
-    from paper_1710_08314_b200.workload import WORKLOADS, make_batch, schedule_work
-
+        dist.init_process_group("gloo")
+    import torch
     wl = WORKLOADS[args.workload]
     F = args.frames or wl.frames
+    frame0, frame1 = frame_range(rank, ws, F)
+    _, _, info, ks, llr = make_batch(wl, frame0, F, nthreads=1)
+    v = np.array([F, int(info.sum()), int((llr < 0).sum()),
+                  int(llr.view(np.uint8).astype(np.int64).sum())], np.int64)
+    if ws > 1:
+        t = torch.from_numpy(v)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        v = t.numpy()
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": ws, "config": common_config(wl, F, ws),
+                          "frames": int(v[0]), "info_ones": int(v[1]), "llr_negative": int(v[2]),
+                          "llr_byte_sum": int(v[3])}))
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+# --------------------------------------------------------------------------
+# the B200 arm
+
+class Ranks:
+    """Process group plumbing: barrier and max-over-ranks (device-timed)."""
+
+    def __init__(self, args):
+        import torch
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.ws, self.rank, local = dist_env()
+        ndev = torch.cuda.device_count()
+        if ndev == 0:
+            raise SystemExit("bench.py: no CUDA device (the decoder has no CPU path)")
+        self.shared = self.ws > ndev
+        if self.shared and not args.allow_shared:
+            raise SystemExit(f"bench.py: {self.ws} ranks but only {ndev} GPU(s); one rank per GPU "
+                             "(pass --allow-shared to exercise the path on shared devices)")
+        if self.ws > 1:
+            if self.shared:
+                dist.init_process_group("gloo")
+            else:
+                dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        self.local = local % ndev
+        torch.cuda.set_device(self.local)
+        self.red_dev = "cpu" if self.shared else f"cuda:{self.local}"
+
+    def barrier(self):
+        if self.ws > 1:
+            self.dist.barrier()
+
+    def max(self, x):
+        if self.ws == 1:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64, device=self.red_dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+
+def measure(wl, F, steps, warmup, e2e_steps, R: Ranks, peaks, peak_src):
+    """One workload: device-resident throughput with live per-kernel CUDA-event
+    timing, error counters reduced over ranks, e2e through the host API, and
+    per-kernel roofline fractions.  Returns (line fields, host state kept for
+    the parity / CPU-baseline leg)."""
+    import torch
+
+    import paper_1710_08314_b200 as P
+    from paper_1710_08314_b200.shard import Counters, all_reduce_counters, frame_range
+    from paper_1710_08314_b200.workload import make_batch, schedule_work
+
+    ws, rank, local = R.ws, R.rank, R.local
     frame0, _ = frame_range(rank, ws, F)  # weak scaling: each rank its own global frame range
     codes, cid, info, ks, llr_np = make_batch(wl, frame0, F,
                                               nthreads=max(1, (os.cpu_count() or 1) // ws))
@@ -231,20 +396,6 @@ def main():
     stream = torch.cuda.current_stream(local)
     bits_per_step = float(ks.sum())
 
-    def barrier():
-        if ws > 1:
-            dist.barrier()
-
-    red_dev = "cpu" if shared else f"cuda:{local}"
-
-    def max_over_ranks(x):
-        if ws == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=red_dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
-    warmup = max(args.warmup, 3)
     for _ in range(warmup):
         dec.decode_batch(llr_d, code_id=cid_d, out=out)
     torch.cuda.synchronize()
@@ -254,12 +405,12 @@ def main():
     kernel_ms = {}
     launches = 0
     clk_p, clk_f = sample_clocks_start(local)
-    barrier()
+    R.barrier()
     torch.cuda.synchronize()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
-    for _ in range(args.steps):
+    for _ in range(steps):
         dec.decode_batch(llr_d, code_id=cid_d, out=out)
         launches += dec.last_launches()
         per = {}  # launches of one pass (an adaptive rung may issue two) summed
@@ -269,22 +420,23 @@ def main():
             kernel_ms.setdefault(k, []).append(ms)
     ev1.record(stream)
     torch.cuda.synchronize()
-    barrier()
+    R.barrier()
     clocks = sample_clocks_stop(clk_p, clk_f)
     dec.profile(False)
-    elapsed = max_over_ranks(ev0.elapsed_time(ev1) / 1e3)
-    ms_per_step = elapsed / args.steps * 1e3
-    value = bits_per_step * ws * args.steps / elapsed / 1e9
+    elapsed = R.max(ev0.elapsed_time(ev1) / 1e3)
+    ms_per_step = elapsed / steps * 1e3
+    value = bits_per_step * ws * steps / elapsed / 1e9
 
     # ---- error counts of the batch, reduced over ranks (sim.cpp:66-71)
     pay = out["payload"].cpu().numpy()
     esc = out["esc"].cpu().numpy()
+    crc_ok = out["crc_ok"].cpu().numpy()
+    metric = out["metric"].cpu().numpy()
     counts = Counters()
     counts.add_batch(np.unpackbits(pay, axis=1), info, esc, ks if cid is not None else None)
-    counts = all_reduce_counters(counts, device=red_dev if ws > 1 else None)
+    counts = all_reduce_counters(counts, device=R.red_dev if ws > 1 else None)
 
     # ---- end to end through the public API with host buffers (pl_decode_host)
-    e2e_steps = args.e2e_steps or max(3, min(args.steps, 10))
     host_out = {
         "payload": torch.empty((F, dec.payload_stride), dtype=torch.uint8).pin_memory(),
         "codeword": None,
@@ -292,7 +444,7 @@ def main():
         "esc": torch.empty(F, dtype=torch.uint8).pin_memory(),
         "metric": torch.empty(F, dtype=torch.float32).pin_memory(),
     }
-    esz = {"f32": 4, "i16": 2}.get(wl.precision, 1)
+    esz = esize(wl)
     if cid is not None:
         # mixed codes: packed variable-length frames (pl_decode_host_packed),
         # each frame's own n LLRs cross the host link
@@ -307,111 +459,194 @@ def main():
         h2d = F * dec.llr_stride * esz
         e2e_api = "pl_decode_host"
     e2e_call()
-    barrier()
+    R.barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         e2e_call()
-    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    e2e_s = R.max(time.perf_counter() - t0)
     e2e_value = bits_per_step * ws * e2e_steps / e2e_s / 1e9
     d2h = F * (dec.payload_stride + 1 + 1 + 4)
+    e2e_same = bool((host_out["payload"].numpy() == pay).all() and (host_out["esc"].numpy() == esc).all())
 
-    # ---- roofline of the dominant kernel (live CUDA-event durations)
-    peaks, peak_src = measured_peaks()
-    (dkind, dl), dms = max(kernel_ms.items(), key=lambda kv: sum(kv[1]))
-    per_launch_s = float(np.mean(dms)) / 1e3
-    one_pass = dkind == "sc" or wl.kind in ("ca_sscl", "sscl", "scl")
-    n_launch_frames = F if one_pass else int((esc >= dl).sum())
-    # algorithmic bytes / element-ops per frame, averaged over the batch's codes
+    # ---- per-kernel roofline fractions (live CUDA-event durations)
     freq = np.bincount(cid, minlength=len(codes)) / F if cid is not None else np.ones(1)
     bytes_per_frame = float(sum(f * (c.n * esz + (c.payload_size + 7) // 8 + 6)
                                 for f, c in zip(freq, codes)))
-    ops_per_frame = float(sum(f * schedule_work(c, wl.kind, dl, wl.pruning, sc=(dkind == "sc"))
-                              for f, c in zip(freq, codes)))
-    achieved_gbs = bytes_per_frame * n_launch_frames / per_launch_s / 1e9
     sm_count = torch.cuda.get_device_properties(local).multi_processor_count
     clk = (peaks.get("sm_max_mhz") or 1965.0) * 1e6
-    lane_peak = sm_count * 128 * clk
-    lane_achieved = ops_per_frame * n_launch_frames / per_launch_s
-    all_kernel_s = sum(sum(v) for v in kernel_ms.values()) / 1e3
-
-    kc = kernel_counters(wl, f"{dkind}_L{dl}", F)
+    lane_peak = sm_count * 128 * clk  # one element-op per lane per clock
     issue_peak = sm_count * 4 * clk  # warp-instructions per second (4 schedulers per SM)
-    result = {
-        "metric": METRIC,
-        "value": value, "unit": "Gb/s", "n_gpus": ws, "steps": args.steps,
-        "warmup": warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": dtype_of(wl),
-        "data": "synthetic: BPSK-AWGN frames keyed by (seed 42, global frame index), FrameRng semantics",
-        "config": common_config(wl, F, ws),
-        "fer": counts.fer(), "frame_errors": counts.frame_errors, "bit_errors": counts.bit_errors,
-        "esc_mean": counts.esc_sum / max(counts.frames, 1),
+    hbm_peak = peaks["hbm_gbs"]
+    nc = ncu_counters(wl)
+    kernels = {}
+    for (kd, l), v in sorted(kernel_ms.items(), key=lambda kv: -sum(kv[1])):
+        s = float(np.mean(v)) / 1e3
+        one_pass = kd == "sc" or wl.kind in ("ca_sscl", "sscl", "scl")
+        nfr = F if one_pass else int((esc >= l).sum())
+        ops = float(sum(f * schedule_work(c, wl.kind, l, wl.pruning, sc=(kd == "sc"))
+                        for f, c in zip(freq, codes)))
+        e = {"ms": s * 1e3, "share_of_step": s * 1e3 / ms_per_step, "frames": nfr,
+             "hbm_achieved_gbs": bytes_per_frame * nfr / s / 1e9,
+             "hbm_frac": bytes_per_frame * nfr / s / 1e9 / hbm_peak,
+             "element_ops_per_frame": ops, "element_op_frac": ops * nfr / s / lane_peak}
+        c = (nc or {}).get("kernels", {}).get(f"{kd}_L{l}")
+        if c:
+            sc = F / nc["frames"]  # the capture decoded the default batch of the same seed
+            e.update({
+                "issue_frac": c["warp_inst"] * sc / s / issue_peak,
+                "warp_inst_per_frame": c["warp_inst"] * sc / max(nfr, 1),
+                "dram_bytes_per_frame": c["dram_bytes"] * sc / max(nfr, 1),
+                "dram_frac": c["dram_bytes"] * sc / s / 1e9 / hbm_peak,
+                "ncu_issue_active_pct": c["issue_active_pct"], "ncu_alu_pipe_pct": c["alu_pipe_pct"],
+                "ncu_smem_bank_conflict_pct": 100.0 * c["smem_bank_conflicts"] / max(c["smem_wavefronts"], 1),
+                "kernel": c["kernel"]})
+        kernels[f"{kd}_L{l}"] = e
+    all_kernel_s = sum(sum(v) for v in kernel_ms.values()) / 1e3 / steps
+
+    # the dominant kernel's roofline: the binding unit of the launch (issue
+    # slots for the ALU-bound list kernels, HBM for a DRAM-bound pass)
+    dkey = next(iter(kernels))
+    d = kernels[dkey]
+    per_launch_s = d["ms"] / 1e3
+    if "issue_frac" in d and d["issue_frac"] >= d.get("dram_frac", 0.0):
+        roof = {"bound": "issue", "achieved": d["issue_frac"] * issue_peak / 1e9,
+                "peak": issue_peak / 1e9, "unit": "Gwarp-inst/s", "frac": d["issue_frac"]}
+    else:
+        roof = {"bound": "hbm", "achieved": d["hbm_achieved_gbs"], "peak": hbm_peak,
+                "unit": "GB/s", "frac": d["hbm_frac"]}
+    roof.update({
+        "kernel": d.get("kernel", dkey), "key": dkey,
+        "traffic": d["dram_bytes_per_frame"] * d["frames"] if "dram_bytes_per_frame" in d else None,
+        "traffic_frac": d.get("dram_frac"),
+        "algorithmic_bytes_per_frame": bytes_per_frame,
+        "hbm_algorithmic": {"achieved": d["hbm_achieved_gbs"], "peak": hbm_peak, "unit": "GB/s",
+                            "frac": d["hbm_frac"], "peak_source": peak_src},
+        "element_op_frac": d["element_op_frac"], "element_ops_per_frame": d["element_ops_per_frame"],
+        "launch_ms": per_launch_s * 1e3,
+        "counters_source": (nc or {}).get("source"),
+    })
+    fields = {
+        "value": value, "unit": "Gb/s", "ms_per_step": ms_per_step, "steps": steps,
+        "warmup": warmup, "dtype": dtype_of(wl), "config": common_config(wl, F, ws),
+        "fer": counts.fer(), "frames_counted": counts.frames, "frame_errors": counts.frame_errors,
+        "bit_errors": counts.bit_errors, "esc_mean": counts.esc_sum / max(counts.frames, 1),
         # frames per final list size (rank 0's batch): the work each rung sees
         "esc_hist": {int(v): int(c) for v, c in zip(*np.unique(esc, return_counts=True))},
         "gpu_launches": int(launches),
-        "kernel_ms": {f"{k[0]}_L{k[1]}": float(np.mean(v)) for k, v in kernel_ms.items()},
-        "kernel_share_of_step": all_kernel_s / elapsed if ws == 1 else None,
-        "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peaks["hbm_gbs"],
-                     "unit": "GB/s", "frac": achieved_gbs / peaks["hbm_gbs"],
-                     "traffic": kc["dram_bytes"] if kc else None,
-                     "traffic_source": kc["source"] if kc else None,
-                     # measured DRAM bytes of the launch / its live duration
-                     "traffic_frac": (kc["dram_bytes"] / per_launch_s / 1e9 / peaks["hbm_gbs"]) if kc else None,
-                     "kernel": f"decode_kernel<{dtype_of(wl)}, {dkind}> L={dl}",
-                     "bytes_per_frame": bytes_per_frame, "peak_source": peak_src},
-        # the binding roofline of this issue-bound path: warp-instructions
-        # issued per second (ncu's instruction count of the same launch / the
-        # live launch time) against 4 per SM per clock, plus ncu's issue-slot
-        # and ALU-pipe utilisation of that launch
-        "roofline_issue": None if kc is None else {
-            "bound": "issue", "achieved": kc["warp_inst"] / per_launch_s / 1e9,
-            "peak": issue_peak / 1e9, "unit": "Gwarp-inst/s",
-            "frac": kc["warp_inst"] / per_launch_s / issue_peak,
-            "warp_inst_per_frame": kc["warp_inst"] / max(n_launch_frames, 1),
-            "ncu_issue_active_pct": kc["issue_active_pct"], "ncu_alu_pipe_pct": kc["alu_pipe_pct"],
-            "ncu_smem_bank_conflict_pct": 100.0 * kc["smem_bank_conflicts"] / max(kc["smem_wavefronts"], 1),
-            "element_ops_per_frame": ops_per_frame,
-            "element_op_frac": lane_achieved / lane_peak,
-            "source": kc["source"]},
+        "kernels": kernels,
+        "kernel_share_of_step": all_kernel_s * 1e3 / ms_per_step,
+        "roofline": roof,
         "clocks": clocks,
         "e2e": {"value": e2e_value, "unit": "Gb/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "steps": e2e_steps, "api": e2e_api},
+                "d2h_bytes_per_step": d2h, "steps": e2e_steps, "api": e2e_api,
+                "outputs_equal_device_path": e2e_same},
     }
+    state = {"codes": codes, "cid": cid, "ks": ks, "llr": llr_np, "payload": pay, "esc": esc,
+             "crc_ok": crc_ok, "metric": metric}
+    del llr_d, llr_h, out, host_out, dec
+    torch.cuda.empty_cache()
+    return fields, state
 
-    # ---- CPU baseline: the reference decoder on this box's cores (rank 0, N=1)
-    if rank == 0 and ws == 1 and not args.no_cpu:
+
+def parity_and_cpu(wl, st, S, nthr, time_it):
+    """The compiled reference on the first S frames of the step's batch
+    (identical LLR bytes): per-frame parity of payload, crc_ok, escalation
+    and metric; the reference's decode time when `time_it`."""
+    from oracle import oracle as O
+
+    codes = [(c.n, c.k, c.crc.raw() if c.crc else "", c.frozen) for c in st["codes"]]
+    cid = st["cid"][:S] if st["cid"] is not None else None
+    r, dt = reference_decode(O, codes, cid, st["llr"][:S], wl, nthr)
+    pb = r["payload"].shape[1]
+    mism = ((st["payload"][:S, :pb] != r["payload"]).any(1) | (st["crc_ok"][:S] != r["crc_ok"])
+            | (st["esc"][:S] != r["esc"]) | (st["metric"][:S] != r["metric"].astype(np.float32)))
+    par = {"frames": int(S), "mismatching_frames": int(mism.sum()),
+           "fields": "payload, crc_ok, esc, metric (bit-exact)", "against": "oracle/_ref"}
+    cpu = None
+    if time_it:
+        cpu = {"value": float(st["ks"][:S].sum()) / dt / 1e9, "unit": "Gb/s", "cores": nthr,
+               "kind": "reference",
+               "sample": f"first {S} frames of the step's batch, FrameDecoder<R> per thread "
+                         f"({dt:.1f} s wall, {dt * nthr:.0f} core-s)"}
+    return par, cpu, dt
+
+
+def main():
+    args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args)
+    if args.impl == "reference":
+        return run_reference(args)
+    if args.dry_run:
+        return run_dry(args)
+    from paper_1710_08314_b200.workload import WORKLOADS
+
+    R = Ranks(args)
+    ws, rank = R.ws, R.rank
+    peaks, peak_src = measured_peaks()
+    wl = WORKLOADS[args.workload]
+    F = args.frames or wl.frames
+    warmup = max(args.warmup, 3)
+    e2e_steps = args.e2e_steps or max(3, min(args.steps, 10))
+    fields, st = measure(wl, F, args.steps, warmup, e2e_steps, R, peaks, peak_src)
+    result = {"metric": METRIC, **fields, "n_gpus": ws, "higher_is_better": True,
+              "scaling": "weak", "vs_baseline": None, "data": DATA}
+
+    # ---- CPU baseline + parity: the reference decoder on this box's cores
+    nthr = os.cpu_count() or 1
+    if rank == 0 and not args.no_cpu:
         try:
-            from oracle import oracle as O
-            nthr = os.cpu_count() or 1
-            # bounded sample: a probe of cpu_sample/4 frames sets the size so
-            # the timed run is ~20 core-seconds of reference decoding
-            S = min(max(args.cpu_sample // 4, 256), F)
-            _, dt0 = reference_decode(O, codes, cid[:S] if cid is not None else None,
-                                      llr_np[:S], wl, nthr)
-            S = int(min(F, max(args.cpu_sample, S * 20.0 / max(dt0 * nthr, 1e-6))))
-            S = max(256, S - S % 256)
-            r, dt = reference_decode(O, codes, cid[:S] if cid is not None else None,
-                                     llr_np[:S], wl, nthr)
-            cpu_gbps = float(ks[:S].sum()) / dt / 1e9
-            pb = r["payload"].shape[1]
-            mism = ((pay[:S, :pb] != r["payload"]).any(1) | (out["crc_ok"].cpu().numpy()[:S] != r["crc_ok"])
-                    | (esc[:S] != r["esc"])
-                    | (out["metric"].cpu().numpy()[:S] != r["metric"].astype(np.float32)))
-            result["cpu_baseline"] = {
-                "value": cpu_gbps, "unit": "Gb/s", "cores": nthr, "kind": "reference",
-                "sample": f"first {S} frames of the step's batch, FrameDecoder<R> per thread "
-                          f"({dt:.1f} s wall, {dt * nthr:.0f} core-s)"}
-            result["parity_vs_reference"] = {"frames": int(S), "mismatching_frames": int(mism.sum()),
-                                             "fields": "payload, crc_ok, esc, metric"}
+            from oracle import oracle as O  # noqa: F401
+            if ws == 1:
+                # bounded sample: a probe of cpu_sample/4 frames sets the size so
+                # the timed run is ~20 core-seconds of reference decoding
+                S = min(max(args.cpu_sample // 4, 256), F)
+                _, _, dt0 = parity_and_cpu(wl, st, S, nthr, False)
+                S = int(min(F, max(args.cpu_sample, S * 20.0 / max(dt0 * nthr, 1e-6))))
+                S = max(256, S - S % 256)
+            else:
+                S = min(args.parity_sample, F)
+            par, cpu, _ = parity_and_cpu(wl, st, S, nthr, ws == 1)
+            result["parity_vs_reference"] = par
+            if cpu:
+                result["cpu_baseline"] = cpu
         except Exception as e:  # noqa: BLE001
             result["cpu_baseline"] = {"value": None, "unit": "Gb/s", "cores": 0, "kind": "reference",
                                       "sample": f"unavailable: {e}"}
-    if shared:
-        result["note"] = f"{ws} ranks shared {ndev} GPU(s): path exercise only, not a scaling number"
+    del st
+
+    # ---- further BASELINE configs, same measurements (driver-run evidence)
+    extras = [] if args.extra in ("", "none") else [w for w in args.extra.split(",") if w != args.workload]
+    if extras:
+        result["workloads"] = []
+        for name in extras:
+            w2 = WORKLOADS[name]
+            f2, st2 = measure(w2, w2.frames, args.extra_steps, warmup, 3, R, peaks, peak_src)
+            f2 = {"workload": name, **f2}
+            if rank == 0 and not args.no_cpu:
+                try:
+                    S = min(args.parity_sample, w2.frames)
+                    par, cpu, _ = parity_and_cpu(w2, st2, S, nthr, ws == 1)
+                    f2["parity_vs_reference"] = par
+                    if cpu:
+                        f2["cpu_baseline"] = cpu
+                except Exception as e:  # noqa: BLE001
+                    f2["parity_vs_reference"] = {"unavailable": str(e)}
+            del st2
+            result["workloads"].append(f2)
+    if R.shared:
+        result["note"] = f"{ws} ranks shared {torch_device_count()} GPU(s): path exercise only, not a scaling number"
+    result["native_so_loaded"] = mapped_native_libs()
     if rank == 0:
         print(json.dumps(result))
     if ws > 1:
-        dist.destroy_process_group()
+        R.dist.destroy_process_group()
     return 0
+
+
+def torch_device_count():
+    import torch
+    return torch.cuda.device_count()
 
 
 if __name__ == "__main__":

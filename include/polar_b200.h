@@ -26,7 +26,10 @@
  * Plain pointers and sizes only.  Device pointers are CUDA global-memory
  * pointers; `stream` is a cudaStream_t passed as void*.  A handle is not
  * thread-safe (the reference's FrameDecoder is not either);
- * use one handle per host thread / stream.  There is no CPU fallback: every
+ * use one handle per host thread.  Calls on one handle may use different
+ * streams: each decode waits (cudaStreamWaitEvent) for the previous decode
+ * that used the same scratch, so they serialise on the device instead of
+ * racing.  Decodes that should overlap need one handle each.  There is no CPU fallback: every
  * decode runs the sm_100a kernels or fails with PL_ERR_CUDA.
  */
 #ifndef POLAR_B200_H

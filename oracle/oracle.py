@@ -51,6 +51,19 @@ def build_ref(force: bool = False) -> str | None:
     return REF_SO
 
 
+ADAPTER_BIN = os.path.join(HERE, "_ref", "check_adapter")
+
+
+def build_adapter() -> str | None:
+    """oracle/_ref/check_adapter (integration/check_adapter.cpp: the
+    reference's FrameDecoder<R> and the GpuFrameDecoder<R> adapter in one
+    binary) when the reference sources are present; else the prebuilt one."""
+    if not os.path.isdir(REF_SRC):
+        return ADAPTER_BIN if os.path.exists(ADAPTER_BIN) else None
+    subprocess.check_call(["make", "-s", "-C", HERE, "adapter"])
+    return ADAPTER_BIN
+
+
 def _ptr(a):
     return None if a is None else a.ctypes.data_as(C.c_void_p)
 
@@ -180,6 +193,11 @@ class Reference:
                                            C.c_uint64, C.c_uint64, C.c_int64, C.c_int, C.c_float,
                                            C.c_void_p, C.c_void_p, C.c_int, C.c_char_p, C.c_char_p,
                                            C.c_int]
+            lib.polref_channel_ids.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_char_p,
+                                               C.c_double, C.c_uint64, C.c_uint64, C.c_void_p,
+                                               C.c_int64, C.c_int, C.c_float, C.c_void_p,
+                                               C.c_void_p, C.c_int, C.c_char_p, C.c_char_p,
+                                               C.c_int]
             cls._lib = lib
         return cls._lib
 
@@ -272,6 +290,24 @@ def ref_channel(n, k, frozen, crc_spec, ebn0_db, seed, frame0, nframes, precisio
     rc = lib.polref_channel(n, k, _ptr(fz), (crc_spec or "").encode(), ebn0_db, seed, frame0,
                             nframes, PRECISIONS[precision], scale, _ptr(info), _ptr(llr),
                             nthreads, punct.encode(), err, 256)
+    if rc:
+        raise ValueError(err.value.decode())
+    return info, llr
+
+
+def ref_channel_ids(n, k, frozen, crc_spec, ebn0_db, seed, ids, precision="f32", scale=0.0,
+                    nthreads=8):
+    """ref_channel over explicit global frame indices (mixed-code batches)."""
+    lib = Reference.lib()
+    fz = np.ascontiguousarray(frozen, np.uint8)
+    ids = np.ascontiguousarray(ids, np.uint64)
+    info = np.zeros((ids.size, k), np.uint8)
+    dt = {"f32": np.float32, "i8": np.int8, "i16": np.int16}[precision]
+    llr = np.zeros((ids.size, n), dt)
+    err = C.create_string_buffer(256)
+    rc = lib.polref_channel_ids(n, k, _ptr(fz), (crc_spec or "").encode(), ebn0_db, seed, 0,
+                                _ptr(ids), ids.size, PRECISIONS[precision], scale, _ptr(info),
+                                _ptr(llr), nthreads, b"", err, 256)
     if rc:
         raise ValueError(err.value.decode())
     return info, llr

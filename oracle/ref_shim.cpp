@@ -273,11 +273,27 @@ int polref_construct_frozen(int n, int reliable, double design, std::uint8_t* ou
 // info bits as 0/1 bytes (k per frame) and channel LLRs in the requested
 // representation (precision 0 f32, 1 int8, 2 int16; scale <= 0 = default).
 // punct: "" or n characters T / P / S (the PuncturePattern of make_code)
+int polref_channel_ids(int n, int k, const std::uint8_t* frozen, const char* crc_spec,
+                       double ebn0_db, std::uint64_t seed, std::uint64_t frame0,
+                       const std::uint64_t* ids, std::int64_t nframes, int precision,
+                       float scale, std::uint8_t* info_out, void* llr_out, int nthreads,
+                       const char* punct, char* err, int errlen);
+
 int polref_channel(int n, int k, const std::uint8_t* frozen, const char* crc_spec,
                    double ebn0_db, std::uint64_t seed, std::uint64_t frame0,
                    std::int64_t nframes, int precision, float scale,
                    std::uint8_t* info_out, void* llr_out, int nthreads, const char* punct,
                    char* err, int errlen) {
+    return polref_channel_ids(n, k, frozen, crc_spec, ebn0_db, seed, frame0, nullptr, nframes,
+                              precision, scale, info_out, llr_out, nthreads, punct, err, errlen);
+}
+
+// frame f of the batch is global frame ids[f] (ids == nullptr: frame0 + f)
+int polref_channel_ids(int n, int k, const std::uint8_t* frozen, const char* crc_spec,
+                       double ebn0_db, std::uint64_t seed, std::uint64_t frame0,
+                       const std::uint64_t* ids, std::int64_t nframes, int precision,
+                       float scale, std::uint8_t* info_out, void* llr_out, int nthreads,
+                       const char* punct, char* err, int errlen) {
     try {
         std::optional<PuncturePattern> pp;
         if (punct && *punct) {
@@ -293,7 +309,7 @@ int polref_channel(int n, int k, const std::uint8_t* frozen, const char* crc_spe
         const double sigma2 = awgn_sigma2(code, ebn0_db);
         parallel_frames(nframes, nthreads, [&](std::int64_t a, std::int64_t b) {
             for (std::int64_t f = a; f < b; ++f) {
-                FrameRng rng(seed, frame0 + std::uint64_t(f));
+                FrameRng rng(seed, ids ? ids[f] : frame0 + std::uint64_t(f));
                 const BitVector info = random_payload(rng, std::size_t(k));
                 const BitVector x = encode_systematic(code, info);
                 if (info_out)

@@ -455,6 +455,11 @@ struct pl_handle {
         int32_t* d_hist = nullptr;   // multi-code batches: frames bucketed by code
         int32_t* d_sorted = nullptr;
         int64_t sorted_cap = 0;
+        // end of the last decode issued on this context, whatever its stream:
+        // the next user waits on it, so pl_decode / pl_decode_host /
+        // pl_sim_point on different streams never overlap on the scratch
+        cudaEvent_t done = nullptr;
+        bool issued = false;
     } ex[2];
     int64_t launches = 0;
     // live per-launch timing (pl_profile)
@@ -679,6 +684,7 @@ void ensure_exec(pl_handle& h, int e) {
     x.d_gscratch = h.dalloc<void>(size_t(h.gscratch_bytes));
     x.d_work = h.dalloc<unsigned long long>(16 * sizeof(unsigned long long));
     x.d_counts = h.dalloc<int32_t>(16 * sizeof(int32_t));
+    ck(cudaEventCreateWithFlags(&x.done, cudaEventDisableTiming), "event");
 }
 
 int fail(pl_handle* h, int code, const std::string& msg) {
@@ -699,6 +705,7 @@ void run_decode(pl_handle& h, const void* llr, const int32_t* code_id, int64_t n
     const bool need_lists = adaptive(kind);
     ensure_exec(h, exec);
     pl_handle::Exec& x = h.ex[exec];
+    if (x.issued) ck(cudaStreamWaitEvent(s, x.done, 0), "wait");
     if (need_lists) ensure_lists(x, nframes);
     ck(cudaMemsetAsync(x.d_work, 0, 16 * sizeof(unsigned long long), s), "memset");
     ck(cudaMemsetAsync(x.d_counts, 0, 16 * sizeof(int32_t), s), "memset");
@@ -833,6 +840,8 @@ void run_decode(pl_handle& h, const void* llr, const int32_t* code_id, int64_t n
     }
     default: throw ConfigError("unhandled decoder variant");
     }
+    ck(cudaEventRecord(x.done, s), "record");
+    x.issued = true;
 }
 
 bool is_pinned_host(const void* p) {
@@ -1159,6 +1168,7 @@ void pl_destroy(pl_handle* h) {
             if (h->ex[i].d_lists[j]) cudaFree(h->ex[i].d_lists[j]);
         if (h->ex[i].d_hist) cudaFree(h->ex[i].d_hist);
         if (h->ex[i].d_sorted) cudaFree(h->ex[i].d_sorted);
+        if (h->ex[i].done) cudaEventDestroy(h->ex[i].done);
         if (h->s_comp[i]) cudaStreamDestroy(h->s_comp[i]);
         if (h->d_in[i]) cudaFree(h->d_in[i]);
         if (h->d_cid[i]) cudaFree(h->d_cid[i]);

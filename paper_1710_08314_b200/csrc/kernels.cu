@@ -2277,7 +2277,11 @@ __global__ void __launch_bounds__(128, 8) sc_lanes_kernel(const LaunchParams P) 
             const int cc = __shfl_sync(FULL, cid, __ffs(pending) - 1);
             const unsigned grp = __ballot_sync(FULL, cid == cc) & pending;
             pending &= ~grp;
-            lane_frame<R>(P, P.codes[cc], sm, gs, frame, active && ((grp >> lane) & 1u), lane);
+            // lanes outside the group shadow a member's frame: packed frames of
+            // another code may be shorter than this code's n (no reads past them)
+            const bool in_grp = (grp >> lane) & 1u;
+            const int fr = __shfl_sync(FULL, frame, __ffs(grp) - 1);
+            lane_frame<R>(P, P.codes[cc], sm, gs, in_grp ? frame : fr, active && in_grp, lane);
         }
     }
 }

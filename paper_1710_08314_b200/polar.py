@@ -496,6 +496,35 @@ class FrameDecoder:
             _raise(rc, L.last_error(self._h))
         return out
 
+    def _check_host_buffers(self, llr, o, nframes, code_id=None):
+        """The C side reads nframes * stride LLRs and writes nframes rows of
+        each output: reject buffers of the wrong type, layout or size."""
+        t = self._torch
+        want_np = _NP_DTYPE[self.precision.name]
+        if hasattr(llr, "data_ptr"):
+            if llr.dtype != self.llr_dtype or not llr.is_contiguous() or llr.is_cuda:
+                raise ValueError(f"llr must be a contiguous CPU {self.llr_dtype} tensor")
+        elif not (isinstance(llr, np.ndarray) and llr.dtype == want_np and llr.flags.c_contiguous):
+            raise ValueError(f"llr must be a C-contiguous {np.dtype(want_np).name} array")
+        need = {"payload": nframes * self.payload_stride, "crc_ok": nframes, "esc": nframes,
+                "metric": nframes}
+        if o.get("codeword") is not None:
+            need["codeword"] = nframes * self.codeword_stride
+        for key, n in need.items():
+            x = o.get(key)
+            if x is None:
+                continue
+            nbytes = x.numel() * x.element_size() if hasattr(x, "numel") else x.nbytes
+            esz = 4 if key == "metric" else 1
+            contig = x.is_contiguous() if hasattr(x, "is_contiguous") else x.flags.c_contiguous
+            if nbytes < n * esz or not contig:
+                raise ValueError(f"output '{key}' must be contiguous with room for {nframes} frames")
+        if code_id is not None:
+            ok = (code_id.dtype == t.int32 and code_id.numel() >= nframes and code_id.is_contiguous()
+                  if hasattr(code_id, "data_ptr") else code_id.size >= nframes)
+            if not ok:
+                raise ValueError("code_id must hold one int32 per frame")
+
     def decode_host_packed_into(self, llr, offsets, o, code_id=None):
         """Host packed frames (pl_decode_host_packed): only each frame's own
         n LLRs cross the host link."""
@@ -510,6 +539,7 @@ class FrameDecoder:
         nframes = offsets.numel() if hasattr(offsets, "numel") else offsets.size
         if code_id is not None and not hasattr(code_id, "data_ptr"):
             code_id = np.ascontiguousarray(code_id, np.int32)
+        self._check_host_buffers(llr, o, nframes, code_id)
         rc = L.lib().pl_decode_host_packed(self._h, ptr(llr), ptr(offsets), ptr(code_id), nframes,
                                            ptr(o["payload"]), ptr(o.get("codeword")), ptr(o["crc_ok"]),
                                            ptr(o["esc"]), ptr(o["metric"]))
@@ -519,7 +549,10 @@ class FrameDecoder:
 
     def decode_host(self, llr: np.ndarray, code_id: np.ndarray | None = None, codeword: bool = False):
         """Host buffers in, host buffers out (copies overlap decoding)."""
-        llr = np.ascontiguousarray(llr)
+        llr = np.ascontiguousarray(llr, _NP_DTYPE[self.precision.name])
+        if llr.size % self.llr_stride:
+            raise ValueError(f"llr holds {llr.size} values, not a multiple of the frame stride "
+                             f"{self.llr_stride}")
         nframes = llr.size // self.llr_stride
         o = {
             "payload": np.zeros((nframes, self.payload_stride), np.uint8),
@@ -539,9 +572,14 @@ class FrameDecoder:
             if hasattr(x, "data_ptr"):
                 return C.c_void_p(x.data_ptr())
             return x.ctypes.data_as(C.c_void_p)
-        nframes = (llr.numel() if hasattr(llr, "numel") else llr.size) // self.llr_stride
+        size = llr.numel() if hasattr(llr, "numel") else llr.size
+        if size % self.llr_stride:
+            raise ValueError(f"llr holds {size} values, not a multiple of the frame stride "
+                             f"{self.llr_stride}")
+        nframes = size // self.llr_stride
         if code_id is not None and not hasattr(code_id, "data_ptr"):
             code_id = np.ascontiguousarray(code_id, np.int32)
+        self._check_host_buffers(llr, o, nframes, code_id)
         rc = L.lib().pl_decode_host(self._h, ptr(llr), ptr(code_id), nframes, ptr(o["payload"]),
                                     ptr(o.get("codeword")), ptr(o["crc_ok"]), ptr(o["esc"]),
                                     ptr(o["metric"]))

@@ -3,11 +3,29 @@ roofline.  Harness code: nothing here is on the decode path.
 """
 from __future__ import annotations
 
+import os
+import re
 from dataclasses import dataclass
 
 import numpy as np
 
 from . import polar as P
+
+# GA frozen sets of every workload code in the reference's frozen-file format
+# (load_frozen_file, code.cpp:164-185), so the reference arm of bench.py
+# builds its codes without this package's library (oracle/frozen/make_frozen.py)
+FROZEN_DIR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                          "oracle", "frozen")
+
+
+def crc_width(crc: str) -> int:
+    """Width of a CRC spec text ("32-GZIP", "11:621:0:0:0", ...) without the
+    library (crc.cpp:42-84: presets and raw specs both lead with the width)."""
+    return int(re.match(r"\d+", crc).group(0)) if crc else 0
+
+
+def frozen_file(n: int, k: int, crc: str, design_db: float, construction: str = "ga") -> str:
+    return os.path.join(FROZEN_DIR, f"{construction}_n{n}_k{k}_c{crc_width(crc)}_d{design_db:g}.frozen")
 
 # op codes of the device schedule (csrc/polar_dev.h)
 OP_F, OP_G, OP_H, OP_FROZEN, OP_INFO, OP_R1, OP_REP, OP_SPC = range(8)
@@ -28,6 +46,11 @@ class Workload:
     scale: float = 0.0
     design_db: float = 4.5
     construction: str = "ga"
+
+    def code_specs(self):
+        """[(n, k, crc text, frozen file)] without the library."""
+        return [(self.n, self.k, self.crc, frozen_file(self.n, self.k, self.crc, self.design_db,
+                                                       self.construction))]
 
     def code(self) -> P.PolarCode:
         w = P.CrcSpec.parse(self.crc).width if self.crc else 0
@@ -79,17 +102,23 @@ class MixedWorkload:
     design_db: float = 3.0
     n: int = 1024  # the widest code (LLR row stride)
 
-    def code_list(self):
+    def code_specs(self):
+        """[(n, k, crc text, frozen file)] of the 31 codes, without the library."""
         out = []
         for n in (128, 256, 512, 1024):
             for num, den in ((1, 3), (1, 2), (2, 3), (5, 6)):
                 k = n * num // den
                 for crc in ("11:621:0:0:0", "24:b2b117:0:0:0"):
-                    w = P.CrcSpec.parse(crc).width
-                    if k + w > n:
+                    if k + crc_width(crc) > n:
                         continue
-                    fz = P.construct_frozen_ga(n, k + w, self.design_db, k / n)
-                    out.append(P.make_code(n, k, fz, crc))
+                    out.append((n, k, crc, frozen_file(n, k, crc, self.design_db)))
+        return out
+
+    def code_list(self):
+        out = []
+        for n, k, crc, _ in self.code_specs():
+            fz = P.construct_frozen_ga(n, k + crc_width(crc), self.design_db, k / n)
+            out.append(P.make_code(n, k, fz, crc))
         return out
 
     def code_ids(self, frame0: int, nframes: int, ncodes: int, seed: int = 42):

@@ -1,5 +1,7 @@
 """The C ABI is consumable from plain C and C++ exactly as INTEGRATION.md
-shows: compile a translation unit against include/ and link the library."""
+shows: compile a translation unit against include/ and link the library;
+and the reference-side adapter (integration/gpu_frame_decoder.hpp, compiled
+against the reference's own headers) decodes like FrameDecoder<R>."""
 import os
 import shutil
 import subprocess
@@ -50,3 +52,22 @@ def test_c_consumer_compiles_links_and_runs(native, tmp_path):
     out = subprocess.run([str(exe)], capture_output=True, text=True)
     assert out.returncode == 0, (out.returncode, out.stderr)
     assert out.stdout.strip() == "ok"
+
+
+@pytest.mark.gpu
+def test_reference_side_adapter_matches_frame_decoder(native, gpu):
+    """oracle/_ref/check_adapter: GpuFrameDecoder<R> and
+    the reference's FrameDecoder<R> (decoders.hpp:60-85) in one binary, on
+    frames from the reference's own channel: payload, codeword, crc_ok,
+    escalation level and metric of every frame equal, decode() too, and the
+    same ConfigError messages (cfg1-, cfg0- and cfg2-like codes, int16 FA,
+    PA, SSC)."""
+    from oracle import oracle
+
+    exe = oracle.build_adapter()
+    if exe is None:
+        pytest.fail("oracle/_ref/check_adapter was not built (build() builds it with /root/reference)")
+    r = subprocess.run([exe, ROOT], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "adapter ok" in r.stdout
