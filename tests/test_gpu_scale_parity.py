@@ -56,8 +56,12 @@ def _compare(got, ref, codes, cid, label):
     nf = ref["esc"].size
     bad = {}
     for key in ("payload", "codeword"):
-        w = ref[key].shape[1]
-        bad[key] = (got[key][:, :w] != ref[key]).any(1)
+        # each frame's own bytes (mixed batches: rows are as wide as the widest code)
+        bad[key] = np.zeros(nf, bool)
+        for i, c in enumerate(codes):
+            rows = np.arange(nf) if cid is None else np.flatnonzero(cid == i)
+            w = (c.payload_size if key == "payload" else c.n) + 7 >> 3
+            bad[key][rows] = (got[key][rows, :w] != ref[key][rows, :w]).any(1)
     bad["crc_ok"] = got["crc_ok"] != ref["crc_ok"]
     bad["esc"] = got["esc"] != ref["esc"]
     bad["metric"] = got["metric"] != ref["metric"].astype(np.float32)
