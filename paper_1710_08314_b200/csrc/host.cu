@@ -430,6 +430,7 @@ struct pl_handle {
     int nmax = 0;
     int64_t pstride = 0, cstride = 0;
     int esz = 4;
+    int sc_keep = 0; // L2 hint split of the frame-per-lane SC pass (LaunchParams::sc_keep)
     int sms = 0;
     std::string err;
     // device residency
@@ -469,15 +470,19 @@ struct pl_handle {
     // host staging for pl_decode_host
     cudaStream_t s_comp[2] = {nullptr, nullptr}, s_h2d = nullptr, s_d2h = nullptr;
     int64_t stage_frames = 0;
-    void* d_in[2] = {nullptr, nullptr};
+    // a ring of kStage chunk buffers: the H2D copy of chunk c waits only for
+    // the decode of chunk c - kStage, so the copy engine keeps streaming while
+    // two chunks decode (2 buffers: cfg3 e2e lost ~0.4 ms per chunk)
+    static constexpr int kStage = 4;
+    void* d_in[kStage] = {};
     int64_t in_cap = 0; // bytes of each d_in / h_stage_in buffer
-    int32_t* d_cid[2] = {nullptr, nullptr};
-    int64_t* d_off[2] = {nullptr, nullptr}; // packed input: chunk-relative frame offsets
-    int64_t* h_stage_off[2] = {nullptr, nullptr};
-    uint8_t* d_out[2] = {nullptr, nullptr};
-    void* h_stage_in[2] = {nullptr, nullptr};
-    uint8_t* h_stage_out[2] = {nullptr, nullptr};
-    cudaEvent_t ev_h2d[2]{}, ev_dec[2]{}, ev_d2h[2]{};
+    int32_t* d_cid[kStage] = {};
+    int64_t* d_off[kStage] = {}; // packed input: chunk-relative frame offsets
+    int64_t* h_stage_off[kStage] = {};
+    uint8_t* d_out[kStage] = {};
+    void* h_stage_in[kStage] = {};
+    uint8_t* h_stage_out[kStage] = {};
+    cudaEvent_t ev_h2d[kStage]{}, ev_dec[kStage]{}, ev_d2h[kStage]{};
 
     template <class T>
     T* dalloc(size_t bytes) {
@@ -750,6 +755,7 @@ void run_decode(pl_handle& h, const void* llr, const int32_t* code_id, int64_t n
         p.fpw = rc.fpw;
         p.team = rc.team;
         p.seg_solo = rc.seg_solo;
+        p.sc_keep = rc.lanes ? h.sc_keep : 0;
         p.solo_max = rc.grid * rc.fpw;
         if (h.profiling) {
             while (h.prof_ev.size() < size_t(2 * (slot + 1))) {
@@ -1104,6 +1110,11 @@ int pl_create(const pl_code* codes, int32_t ncodes, const pl_decoder* dec, int32
         // ---- launch plans for every pass this kind can run
         if (!uses_list(kind) || adaptive(kind))
             h->sc_cfg = env_int("PLB_SC_LANES", 1) ? plan_lanes(*h) : plan_rung(*h, 1, false);
+            // L2 hints of the frame-per-lane pass: segments <= 256 values kept
+            // (evict_last), larger ones and the channel streamed (evict_first).
+            // FA@4.5 dB float SC pass 23.1 -> 21.7 ms per 2^20 frames; int8 is
+            // slower with hints (9.4 -> 9.9 ms), so only float takes them
+            h->sc_keep = env_int("PLB_SC_KEEP", h->dec.precision == PL_F32 ? 256 : 0);
         if (kind == PL_KIND_FA_SSCL)
             for (int ll = 2; ll <= l; ll *= 2) h->rungs.push_back(plan_rung(*h, ll, true, true));
         else if (uses_list(kind))
@@ -1170,6 +1181,8 @@ void pl_destroy(pl_handle* h) {
         if (h->ex[i].d_sorted) cudaFree(h->ex[i].d_sorted);
         if (h->ex[i].done) cudaEventDestroy(h->ex[i].done);
         if (h->s_comp[i]) cudaStreamDestroy(h->s_comp[i]);
+    }
+    for (int i = 0; i < pl_handle::kStage; ++i) {
         if (h->d_in[i]) cudaFree(h->d_in[i]);
         if (h->d_cid[i]) cudaFree(h->d_cid[i]);
         if (h->d_off[i]) cudaFree(h->d_off[i]);
@@ -1311,7 +1324,7 @@ int decode_host_impl(pl_handle* h, const void* llr, const int64_t* offsets, cons
             ck(cudaStreamCreateWithFlags(&h->s_comp[1], cudaStreamNonBlocking), "stream");
             ck(cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking), "stream");
             ck(cudaStreamCreateWithFlags(&h->s_d2h, cudaStreamNonBlocking), "stream");
-            for (int i = 0; i < 2; ++i) {
+            for (int i = 0; i < pl_handle::kStage; ++i) {
                 ck(cudaEventCreateWithFlags(&h->ev_h2d[i], cudaEventDisableTiming), "event");
                 ck(cudaEventCreateWithFlags(&h->ev_dec[i], cudaEventDisableTiming), "event");
                 ck(cudaEventCreateWithFlags(&h->ev_d2h[i], cudaEventDisableTiming), "event");
@@ -1359,7 +1372,7 @@ int decode_host_impl(pl_handle* h, const void* llr, const int64_t* offsets, cons
         const int64_t ob_pay = h->pstride, ob_cw = codeword ? h->cstride : 0;
         if (h->stage_frames < chunk || h->in_cap < need || (offsets && !h->d_off[0])) {
             const int64_t cap = std::max(need, chunk * in_bytes);
-            for (int i = 0; i < 2; ++i) {
+            for (int i = 0; i < pl_handle::kStage; ++i) {
                 if (h->d_in[i]) cudaFree(h->d_in[i]);
                 if (h->d_cid[i]) cudaFree(h->d_cid[i]);
                 if (h->d_off[i]) cudaFree(h->d_off[i]);
@@ -1384,10 +1397,10 @@ int decode_host_impl(pl_handle* h, const void* llr, const int64_t* offsets, cons
                              (!crc_ok || is_pinned_host(crc_ok)) && (!esc || is_pinned_host(esc)) &&
                              (!metric || is_pinned_host(metric));
         int64_t launches = 0;
-        std::vector<int64_t> pending(2, -1);
+        std::vector<int64_t> pending(pl_handle::kStage, -1);
         auto finish_chunk = [&](int64_t c) {
             // unpack a chunk that went through the host staging buffer
-            const int b = int(c & 1);
+            const int b = int(c % pl_handle::kStage);
             ck(cudaEventSynchronize(h->ev_d2h[b]), "sync");
             if (pin_out) return;
             const int64_t f0 = c * chunk, nf = std::min(chunk, nframes - f0);
@@ -1403,7 +1416,8 @@ int decode_host_impl(pl_handle* h, const void* llr, const int64_t* offsets, cons
             if (metric) std::memcpy(metric + f0, o, size_t(nf) * 4);
         };
         for (int64_t c = 0; c < nchunks; ++c) {
-            const int b = int(c & 1);
+            const int b = int(c % pl_handle::kStage); // staging buffer
+            const int e = int(c & 1);                 // execution context + compute stream
             const int64_t f0 = c * chunk, nf = std::min(chunk, nframes - f0);
             if (pending[size_t(b)] >= 0) {
                 finish_chunk(pending[size_t(b)]);
@@ -1431,8 +1445,8 @@ int decode_host_impl(pl_handle* h, const void* llr, const int64_t* offsets, cons
                                    h->s_h2d),
                    "h2d");
             ck(cudaEventRecord(h->ev_h2d[b], h->s_h2d), "record");
-            ck(cudaStreamWaitEvent(h->s_comp[b], h->ev_h2d[b], 0), "wait");
-            ck(cudaStreamWaitEvent(h->s_comp[b], h->ev_d2h[b], 0), "wait");
+            ck(cudaStreamWaitEvent(h->s_comp[e], h->ev_h2d[b], 0), "wait");
+            ck(cudaStreamWaitEvent(h->s_comp[e], h->ev_d2h[b], 0), "wait");
             uint8_t* o = h->d_out[b];
             uint8_t* d_pay = o;
             uint8_t* d_cw = codeword ? o + nf * ob_pay : nullptr;
@@ -1443,9 +1457,9 @@ int decode_host_impl(pl_handle* h, const void* llr, const int64_t* offsets, cons
             const uintptr_t mis = reinterpret_cast<uintptr_t>(d_met) & 3u;
             if (mis) d_met = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(d_met) + (4 - mis));
             run_decode(*h, h->d_in[b], code_id ? h->d_cid[b] : nullptr, nf, d_pay, d_cw, d_ok, d_esc,
-                       d_met, h->s_comp[b], b, offsets ? h->d_off[b] : nullptr);
+                       d_met, h->s_comp[e], e, offsets ? h->d_off[b] : nullptr);
             launches += h->launches;
-            ck(cudaEventRecord(h->ev_dec[b], h->s_comp[b]), "record");
+            ck(cudaEventRecord(h->ev_dec[b], h->s_comp[e]), "record");
             ck(cudaStreamWaitEvent(h->s_d2h, h->ev_dec[b], 0), "wait");
             auto d2h = [&](void* dst_pinned, uint8_t* dst_stage, const void* srcp, size_t bytes) {
                 void* dst = pin_out ? dst_pinned : static_cast<void*>(dst_stage);
@@ -1464,7 +1478,7 @@ int decode_host_impl(pl_handle* h, const void* llr, const int64_t* offsets, cons
             ck(cudaEventRecord(h->ev_d2h[b], h->s_d2h), "record");
             pending[size_t(b)] = c;
         }
-        for (int b = 0; b < 2; ++b)
+        for (int b = 0; b < pl_handle::kStage; ++b)
             if (pending[size_t(b)] >= 0) finish_chunk(pending[size_t(b)]);
         // finish in chunk order is not required: chunks write disjoint ranges
         h->launches = launches;

@@ -367,6 +367,31 @@ __device__ __forceinline__ void vst(R* p, const Vec<R, G>& x) {
     *reinterpret_cast<typename VT<G * sizeof(R)>::T*>(p) = x.raw;
 }
 
+// L2 eviction-priority hints of the frame-per-lane SC pass (global memory only)
+__device__ __forceinline__ uint64_t l2_policy(bool keep) {
+    uint64_t p;
+    if (keep) asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    else asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+template <typename R, int G>
+__device__ __forceinline__ Vec<R, G> vld_hint(const R* ptr, uint64_t pol) {
+    static_assert(G * sizeof(R) == 16, "16-byte vectors");
+    Vec<R, G> x;
+    uint4 v;
+    asm volatile("ld.global.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(ptr), "l"(pol));
+    x.raw = *reinterpret_cast<const typename VT<16>::T*>(&v);
+    return x;
+}
+template <typename R, int G>
+__device__ __forceinline__ void vst_hint(R* ptr, const Vec<R, G>& x, uint64_t pol) {
+    static_assert(G * sizeof(R) == 16, "16-byte vectors");
+    const uint4 v = *reinterpret_cast<const uint4*>(&x.raw);
+    asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;"
+                 :: "l"(ptr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol) : "memory");
+}
+
 // first channel LLR of a frame: fixed stride, or the packed layout's offset
 template <typename R>
 __device__ __forceinline__ const R* frame_llr(const LaunchParams& P, int frame) {
@@ -1890,6 +1915,7 @@ template <typename R>
 struct LaneCtx {
     static constexpr int VE = 16 / int(sizeof(R));
     int lane, n;
+    int segmax, keep; // depth segments > segmax values live in global scratch
     const R* chan;      // this lane's frame
     uint32_t* ps;       // this lane's psum words, stride 32
     const uint64_t* pt; // pool pointer table
@@ -1951,10 +1977,12 @@ __device__ __forceinline__ bool vec_has_zero(const Vec<R, G>& x) {
 }
 
 // U chunks per iteration: 2U loads in flight per lane (the pools of the
-// upper depths live in global memory), U * VE <= 32 partial-sum bits
-template <typename R, int U>
+// upper depths live in global memory), U * VE <= 32 partial-sum bits.
+// HIN / HOUT: the input / output depth is in global memory and takes an L2
+// eviction hint (pin / pout).
+template <typename R, int U, bool HIN, bool HOUT>
 __device__ __forceinline__ void lane_fg_chunks(const LaneCtx<R>& c, int d, int nc, int lb, bool is_g,
-                                               R* out) {
+                                               R* out, uint64_t pin, uint64_t pout) {
     constexpr int VE = LaneCtx<R>::VE;
     int cs;
     const R* in = c.chunk_base(d, cs);
@@ -1965,14 +1993,36 @@ __device__ __forceinline__ void lane_fg_chunks(const LaneCtx<R>& c, int d, int n
         Vec<R, VE> a[U], b[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            a[u] = vld<R, VE>(in + (k + u) * cs);
-            b[u] = vld<R, VE>(in_b + (k + u) * cs);
+            if constexpr (HIN) {
+                a[u] = vld_hint<R, VE>(in + (k + u) * cs, pin);
+                b[u] = vld_hint<R, VE>(in_b + (k + u) * cs, pin);
+            } else {
+                a[u] = vld<R, VE>(in + (k + u) * cs);
+                b[u] = vld<R, VE>(in_b + (k + u) * cs);
+            }
         }
         const int pos = lb + k * VE;
         const uint32_t bits = is_g ? c.word(pos >> 5) >> (pos & 31) : 0u;
 #pragma unroll
-        for (int u = 0; u < U; ++u)
-            vst<R, VE>(o + (k + u) * 32 * VE, fg_compute<R, VE>(a[u], b[u], bits >> (u * VE), is_g));
+        for (int u = 0; u < U; ++u) {
+            const Vec<R, VE> r = fg_compute<R, VE>(a[u], b[u], bits >> (u * VE), is_g);
+            if constexpr (HOUT) vst_hint<R, VE>(o + (k + u) * 32 * VE, r, pout);
+            else vst<R, VE>(o + (k + u) * 32 * VE, r);
+        }
+    }
+}
+template <typename R, int U>
+__device__ __forceinline__ void lane_fg_chunks_any(const LaneCtx<R>& c, int d, int nc, int lb, bool is_g,
+                                                   R* out) {
+    // hints only on global depths (the channel is depth 0); uniform per op
+    const bool gin = c.keep > 0 && (d == 0 || (c.n >> d) > c.segmax);
+    const bool gout = c.keep > 0 && (c.n >> (d + 1)) > c.segmax;
+    if (gin) {
+        const uint64_t pin = l2_policy(d > 0 && (c.n >> d) <= c.keep);
+        if (gout) lane_fg_chunks<R, U, true, true>(c, d, nc, lb, is_g, out, pin, l2_policy((c.n >> (d + 1)) <= c.keep));
+        else lane_fg_chunks<R, U, true, false>(c, d, nc, lb, is_g, out, pin, 0);
+    } else {
+        lane_fg_chunks<R, U, false, false>(c, d, nc, lb, is_g, out, 0, 0);
     }
 }
 
@@ -1985,8 +2035,8 @@ __device__ void lane_fg(const LaneCtx<R>& c, int d, int m, int lb, bool is_g) {
     R* const out = c.pool(d + 1);
     if (h >= VE) {
         const int nc = h / VE;
-        if (nc >= U) lane_fg_chunks<R, U>(c, d, nc, lb, is_g, out);
-        else lane_fg_chunks<R, 1>(c, d, nc, lb, is_g, out);
+        if (nc >= U) lane_fg_chunks_any<R, U>(c, d, nc, lb, is_g, out);
+        else lane_fg_chunks_any<R, 1>(c, d, nc, lb, is_g, out);
     } else {
         // the parent's m <= VE values are one contiguous chunk
         const R* p = c.chunk(d, 0);
@@ -2149,6 +2199,8 @@ __device__ void lane_frame(const LaunchParams& P, const DevCode& C, unsigned cha
     LaneCtx<R> c;
     c.lane = lane;
     c.n = C.n;
+    c.segmax = P.seg_smem_max;
+    c.keep = P.sc_keep;
     c.chan = frame_llr<R>(P, frame);
     const LaneQ q0 = lane_layout(C.n, int(sizeof(R)), P.seg_smem_max, 0);
     c.ps = reinterpret_cast<uint32_t*>(sm + q0.psum_off) + lane;

@@ -109,6 +109,9 @@ struct LaunchParams {
     int32_t seg_solo;          // >0: solo mode when the pass has <= solo_max frames:
     int32_t solo_max;          // warp 0 of each block decodes with the whole block's
                                // shared memory (segments <= seg_solo in smem)
+    int32_t sc_keep;           // frame-per-lane SC pass: global depth segments of <= sc_keep
+                               // values are loaded / stored L2::evict_last, larger ones
+                               // (and the channel) evict_first; 0 = no cache hints
 };
 
 constexpr int kMaxWarpsPerBlock = 4; // a block is 1, 2 or 4 independent warps
