@@ -431,6 +431,7 @@ struct pl_handle {
     int64_t pstride = 0, cstride = 0;
     int esz = 4;
     int sc_keep = 0; // L2 hint split of the frame-per-lane SC pass (LaunchParams::sc_keep)
+    int sc_discard = 0; // LaunchParams::sc_discard
     int sms = 0;
     std::string err;
     // device residency
@@ -756,6 +757,7 @@ void run_decode(pl_handle& h, const void* llr, const int32_t* code_id, int64_t n
         p.team = rc.team;
         p.seg_solo = rc.seg_solo;
         p.sc_keep = rc.lanes ? h.sc_keep : 0;
+        p.sc_discard = rc.lanes ? h.sc_discard : 0;
         p.solo_max = rc.grid * rc.fpw;
         if (h.profiling) {
             while (h.prof_ev.size() < size_t(2 * (slot + 1))) {
@@ -1115,6 +1117,9 @@ int pl_create(const pl_code* codes, int32_t ncodes, const pl_decoder* dec, int32
             // FA@4.5 dB float SC pass 23.1 -> 21.7 ms per 2^20 frames; int8 is
             // slower with hints (9.4 -> 9.9 ms), so only float takes them
             h->sc_keep = env_int("PLB_SC_KEEP", h->dec.precision == PL_F32 ? 256 : 0);
+            // ... and dead global segments dropped from the L2 after their
+            // last read (float: SC pass 21.9 -> 20.7 ms)
+            h->sc_discard = env_int("PLB_SC_DISCARD", h->dec.precision == PL_F32 ? 1 : 0);
         if (kind == PL_KIND_FA_SSCL)
             for (int ll = 2; ll <= l; ll *= 2) h->rungs.push_back(plan_rung(*h, ll, true, true));
         else if (uses_list(kind))

@@ -1916,6 +1916,7 @@ struct LaneCtx {
     static constexpr int VE = 16 / int(sizeof(R));
     int lane, n;
     int segmax, keep; // depth segments > segmax values live in global scratch
+    bool discard;     // drop dead global segments from the L2 (LaunchParams::sc_discard)
     const R* chan;      // this lane's frame
     uint32_t* ps;       // this lane's psum words, stride 32
     const uint64_t* pt; // pool pointer table
@@ -1980,9 +1981,12 @@ __device__ __forceinline__ bool vec_has_zero(const Vec<R, G>& x) {
 // upper depths live in global memory), U * VE <= 32 partial-sum bits.
 // HIN / HOUT: the input / output depth is in global memory and takes an L2
 // eviction hint (pin / pout).
+// disc: the input segment is a global depth pool read for the last time (a G
+// op): its L2 lines are dropped without write-back once consumed
+// (discard.global.L2), so dead LLRs of 32-frame warps never reach DRAM.
 template <typename R, int U, bool HIN, bool HOUT>
 __device__ __forceinline__ void lane_fg_chunks(const LaneCtx<R>& c, int d, int nc, int lb, bool is_g,
-                                               R* out, uint64_t pin, uint64_t pout) {
+                                               R* out, uint64_t pin, uint64_t pout, bool disc) {
     constexpr int VE = LaneCtx<R>::VE;
     int cs;
     const R* in = c.chunk_base(d, cs);
@@ -2009,20 +2013,38 @@ __device__ __forceinline__ void lane_fg_chunks(const LaneCtx<R>& c, int d, int n
             if constexpr (HOUT) vst_hint<R, VE>(o + (k + u) * 32 * VE, r, pout);
             else vst<R, VE>(o + (k + u) * 32 * VE, r);
         }
+        // (the values were consumed above by every lane of the warp; chunk
+        // rows are 512-byte aligned, lanes 0 / 8 / 16 / 24 start its lines)
+        if (disc && (c.lane & 7) == 0) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                asm volatile("discard.global.L2 [%0], 128;" :: "l"(in + (k + u) * cs) : "memory");
+                asm volatile("discard.global.L2 [%0], 128;" :: "l"(in_b + (k + u) * cs) : "memory");
+            }
+        }
     }
 }
 template <typename R, int U>
 __device__ __forceinline__ void lane_fg_chunks_any(const LaneCtx<R>& c, int d, int nc, int lb, bool is_g,
                                                    R* out) {
+    if constexpr (sizeof(R) != 4) {
+        // fixed point: no hint / discard code at all (the int16 pass lost 10%
+        // to the larger loop even with the hints switched off)
+        lane_fg_chunks<R, U, false, false>(c, d, nc, lb, is_g, out, 0, 0, false);
+        return;
+    }
     // hints only on global depths (the channel is depth 0); uniform per op
     const bool gin = c.keep > 0 && (d == 0 || (c.n >> d) > c.segmax);
     const bool gout = c.keep > 0 && (c.n >> (d + 1)) > c.segmax;
+    const bool disc = c.discard && is_g && d > 0 && (c.n >> d) > c.segmax;
     if (gin) {
         const uint64_t pin = l2_policy(d > 0 && (c.n >> d) <= c.keep);
-        if (gout) lane_fg_chunks<R, U, true, true>(c, d, nc, lb, is_g, out, pin, l2_policy((c.n >> (d + 1)) <= c.keep));
-        else lane_fg_chunks<R, U, true, false>(c, d, nc, lb, is_g, out, pin, 0);
+        if (gout)
+            lane_fg_chunks<R, U, true, true>(c, d, nc, lb, is_g, out, pin,
+                                             l2_policy((c.n >> (d + 1)) <= c.keep), disc);
+        else lane_fg_chunks<R, U, true, false>(c, d, nc, lb, is_g, out, pin, 0, disc);
     } else {
-        lane_fg_chunks<R, U, false, false>(c, d, nc, lb, is_g, out, 0, 0);
+        lane_fg_chunks<R, U, false, false>(c, d, nc, lb, is_g, out, 0, 0, disc);
     }
 }
 
@@ -2201,6 +2223,7 @@ __device__ void lane_frame(const LaunchParams& P, const DevCode& C, unsigned cha
     c.n = C.n;
     c.segmax = P.seg_smem_max;
     c.keep = P.sc_keep;
+    c.discard = P.sc_discard != 0;
     c.chan = frame_llr<R>(P, frame);
     const LaneQ q0 = lane_layout(C.n, int(sizeof(R)), P.seg_smem_max, 0);
     c.ps = reinterpret_cast<uint32_t*>(sm + q0.psum_off) + lane;

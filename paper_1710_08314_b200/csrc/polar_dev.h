@@ -112,6 +112,8 @@ struct LaunchParams {
     int32_t sc_keep;           // frame-per-lane SC pass: global depth segments of <= sc_keep
                                // values are loaded / stored L2::evict_last, larger ones
                                // (and the channel) evict_first; 0 = no cache hints
+    int32_t sc_discard;        // frame-per-lane SC pass: discard.global.L2 the lines of a
+                               // global depth segment after its last read (G op)
 };
 
 constexpr int kMaxWarpsPerBlock = 4; // a block is 1, 2 or 4 independent warps

@@ -1,14 +1,14 @@
 #!/usr/bin/env python
 """Per-kernel counters of each bench workload's passes, from one ncu pass per
-workload (`profiles/collect_ncu.sh`, its CSVs kept in `r01_ncu/`):
+workload (`profiles/collect_ncu.sh`, its CSVs kept in `<round>_ncu/`):
 DRAM bytes, warp-instructions, issue-slot and ALU-pipe utilisation, shared
 memory wavefronts / bank conflicts, per launch of the workload's default batch
 (the inputs are seeded, so bench.py's launches decode the same frames).
 
-Writes `r01_traffic.json`, which bench.py reads for `roofline.traffic` and
-`roofline_issue` of the dominant kernel.
+Writes `<round>_traffic.json`, which bench.py reads for the per-kernel
+issue / DRAM fractions and `roofline.traffic` of the dominant kernel.
 
-  python profiles/traffic.py
+  python profiles/traffic.py [round]     (default r02: profiles/r02_ncu/ -> r02_traffic.json)
 """
 import csv
 import glob
@@ -31,10 +31,12 @@ def kernel_key(name):
     return "sc_L1" if kv == 0 else f"list_L{1 << (kv - 1)}"
 
 
+RND = sys.argv[1] if len(sys.argv) > 1 else "r02"
 out = {}
-for path in sorted(glob.glob(os.path.join(HERE, "r01_ncu", "ncu_*.csv"))):
+for path in sorted(glob.glob(os.path.join(HERE, f"{RND}_ncu", "ncu_*.csv"))):
     w = os.path.basename(path)[4:-4]
     rows = [r for r in csv.reader(open(path)) if r]
+    rows = rows[next(i for i, r in enumerate(rows) if r[0] == "ID"):]  # skip ==PROF== notes
     hdr = rows[0]
     ix = {k: hdr.index(k) for k in ("ID", "Kernel Name", "Metric Name", "Metric Value")}
     launches = {}
@@ -68,10 +70,10 @@ for path in sorted(glob.glob(os.path.join(HERE, "r01_ncu", "ncu_*.csv"))):
     out[WORKLOADS[w].name] = {
         "frames": WORKLOADS[w].frames,
         "kernels": kernels,
-        "source": f"profiles/r01_ncu/ncu_{w}.csv (profiles/collect_ncu.sh: ncu --metrics, "
+        "source": f"profiles/{RND}_ncu/ncu_{w}.csv (profiles/collect_ncu.sh: ncu --metrics, "
                   "the decoding launch of each pass kernel of the workload's default batch)",
     }
-json.dump(out, open(os.path.join(HERE, "r01_traffic.json"), "w"), indent=1)
+json.dump(out, open(os.path.join(HERE, f"{RND}_traffic.json"), "w"), indent=1)
 for name, v in out.items():
     for k, d in v["kernels"].items():
         print(f"{name:32s} {k:9s} {d['dram_bytes'] / 1e9:8.2f} GB  {d['warp_inst'] / 1e9:7.2f} Ginst  "
