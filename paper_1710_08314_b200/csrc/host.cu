@@ -432,6 +432,7 @@ struct pl_handle {
     int esz = 4;
     int sc_keep = 0; // L2 hint split of the frame-per-lane SC pass (LaunchParams::sc_keep)
     int sc_discard = 0; // LaunchParams::sc_discard
+    int list_discard = 0; // LaunchParams::list_discard
     int sms = 0;
     std::string err;
     // device residency
@@ -758,6 +759,7 @@ void run_decode(pl_handle& h, const void* llr, const int32_t* code_id, int64_t n
         p.seg_solo = rc.seg_solo;
         p.sc_keep = rc.lanes ? h.sc_keep : 0;
         p.sc_discard = rc.lanes ? h.sc_discard : 0;
+        p.list_discard = rc.lanes ? 0 : h.list_discard;
         p.solo_max = rc.grid * rc.fpw;
         if (h.profiling) {
             while (h.prof_ev.size() < size_t(2 * (slot + 1))) {
@@ -1120,6 +1122,7 @@ int pl_create(const pl_code* codes, int32_t ncodes, const pl_decoder* dec, int32
             // ... and dead global segments dropped from the L2 after their
             // last read (float: SC pass 21.9 -> 20.7 ms)
             h->sc_discard = env_int("PLB_SC_DISCARD", h->dec.precision == PL_F32 ? 1 : 0);
+            h->list_discard = env_int("PLB_LIST_DISCARD", h->dec.precision == PL_F32 ? 1 : 0);
         if (kind == PL_KIND_FA_SSCL)
             for (int ll = 2; ll <= l; ll *= 2) h->rungs.push_back(plan_rung(*h, ll, true, true));
         else if (uses_list(kind))

@@ -473,7 +473,9 @@ __host__ __device__ inline LayoutQ layout_query(int n, int l, int esz, int segma
                 q.pool_off = goff;
                 q.pool_in_smem = 0;
             }
-            goff += bytes;
+            // whole 128-byte L2 lines per global pool (discard.global.L2 of a
+            // dead pool must not touch a neighbour's)
+            goff += (bytes + 127) & ~127;
         }
     }
     q.smem_total = off;
@@ -501,6 +503,7 @@ struct Ctx {
     // element loops (F/G, H) run over a team of warps when team > 1: thread
     // tt0 of tstride; otherwise tt0 = lane, tstride = SW
     int tt0, tstride, team;
+    bool discard; // float: discard.global.L2 dead global depth pools (LaunchParams::list_discard)
 
     __device__ __forceinline__ R* pool(int d) const { return reinterpret_cast<R*>(fx->pool[d]); }
     __device__ __forceinline__ uint8_t* bix() const { return reinterpret_cast<uint8_t*>(fx + 1); }
@@ -596,10 +599,54 @@ __device__ __forceinline__ void fg_run(Ctx<R, SW>& cx, int d, int h, int lb, int
     }
 }
 
-template <typename R, int SW>
+// U items per lane in flight (all loads issued before the first compute):
+// the L = 32 float kernel waits on L2 / DRAM for its depth pools, and one
+// item per trip leaves a single load pair in flight per lane
+template <typename R, int SW, int G, int U>
+__device__ __forceinline__ void fg_run_batched(Ctx<R, SW>& cx, int d, int h, int lb, int na, bool is_g) {
+    const int cp = h / G;
+    const int lg = __ffs(cp) - 1;
+    R* const outp = cx.pool(d + 1);
+    R* const inp = d == 0 ? cx.channel() : cx.pool(d);
+    const int seg = cx.n >> d;
+    const int total = na << lg;
+    #pragma unroll 1
+    for (int t0 = cx.tt0; t0 < total; t0 += U * cx.tstride) {
+        Vec<R, G> a[U], b[U];
+        uint32_t bits[U];
+        int ro[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int t = t0 + u * cx.tstride;
+            const int tt = t < total ? t : t0; // tail: re-read item t0, store nothing
+            const int r = tt >> lg, c = tt & (cp - 1);
+            const int p = cx.fx->alive_list[r];
+            const R* in = d == 0 ? inp : inp + int(cx.bix()[p * 16 + d]) * seg;
+            a[u] = vld<R, G>(in + c * G);
+            b[u] = vld<R, G>(in + h + c * G);
+            const int pos = lb + c * G;
+            bits[u] = is_g ? cx.row(p)[pos >> 5] >> (pos & 31) : 0u;
+            ro[u] = t < total ? r * h + c * G : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (ro[u] >= 0) vst<R, G>(outp + ro[u], fg_compute<R, G>(a[u], b[u], bits[u], is_g));
+    }
+}
+
+#ifndef PLB_FG_UNROLL
+#define PLB_FG_UNROLL 2
+#endif
+template <int UB = 1, typename R, int SW>
 __device__ __forceinline__ void fg_elems(Ctx<R, SW>& cx, int d, int m, int lb, int na, bool is_g) {
     constexpr int VE = 16 / int(sizeof(R));
     const int h = m >> 1;
+    if constexpr (UB > 1) {
+        if (h >= VE) {
+            fg_run_batched<R, SW, VE, UB>(cx, d, h, lb, na, is_g);
+            return;
+        }
+    }
     if (h >= VE) fg_run<R, SW, VE>(cx, d, h, lb, na, is_g);
     else if (sizeof(R) == 1 && h >= 4) fg_run<R, SW, 4>(cx, d, h, lb, na, is_g); // one SWAR word
     else fg_run<R, SW, 1>(cx, d, h, lb, na, is_g);
@@ -613,13 +660,27 @@ __device__ __forceinline__ void team_sync(const Ctx<R, SW>& cx) {
     else __syncwarp();
 }
 
-template <typename R, int SW>
+template <int UB = 1, typename R, int SW>
 __device__ void op_fg(Ctx<R, SW>& cx, int d, int m, int lb, int na, bool is_g) {
     // the child segment of the path of rank r goes to buffer r (see header)
     if (cx.is_alive()) cx.bix()[cx.lane * 16 + d + 1] = uint8_t(cx.myrank);
     if (cx.team > 1) __syncthreads();
-    fg_elems(cx, d, m, lb, na, is_g);
+    fg_elems<UB>(cx, d, m, lb, na, is_g);
     team_sync(cx);
+    if constexpr (sizeof(R) == 4 && SW == 32) {
+        // after a G op the depth-d pool is dead (its next use is a write by
+        // the parent's next op): drop its L2 lines without write-back when
+        // it lives in global scratch, so dead LLRs never reach DRAM (the
+        // float list passes write 2x what they read).  Float 32-lane kernels
+        // (L >= 16) only: cfg4 L=32 / 16 +1.5%, L = 4 / 8 unchanged
+        if (is_g && d > 0 && cx.discard && __isGlobal(cx.pool(d))) {
+            const char* base = reinterpret_cast<const char*>(cx.pool(d));
+            const int lines = (cx.l * (cx.n >> d) * int(sizeof(R))) >> 7;
+            #pragma unroll 1
+            for (int i = cx.lane; i < lines; i += SW)
+                asm volatile("discard.global.L2 [%0], 128;" :: "l"(base + (size_t(i) << 7)) : "memory");
+        }
+    }
 }
 
 // psums[lb, lb+h) ^= psums[lb+h, lb+2h) for every alive path
@@ -1436,6 +1497,7 @@ __device__ void setup_ctx(Ctx<R, SW>& cx, const LaunchParams& P, const DevCode& 
     cx.n = C.n;
     cx.l = l;
     cx.lmask = l >= 32 ? FULL : ((1u << l) - 1u);
+    if constexpr (sizeof(R) == 4 && SW == 32) cx.discard = P.list_discard != 0;
     cx.chan = frame_llr<R>(P, frame);
     cx.fx = reinterpret_cast<FixedS<SW>*>(sm);
     if constexpr (sizeof(R) == 4)
@@ -1484,7 +1546,7 @@ __device__ void list_frame(const LaunchParams& P, const DevCode& C, unsigned cha
         const int na = __popc(cx.alive);
         const bool fused = (op & kOpFused) != 0;
         if (fused) fused_leaf(cx, code, d, m, lb, na, (op & kOpFusedG) != 0);
-        if (code <= OP_G) op_fg(cx, d, m, lb, na, code == OP_G);
+        if (code <= OP_G) op_fg<(sizeof(R) == 4 && KV >= 6) ? PLB_FG_UNROLL : 1>(cx, d, m, lb, na, code == OP_G);
         else if (code == OP_H) op_h(cx, m, lb, na);
         else if (code == OP_FROZEN) {
             if (!fused) list_frozen(cx, d, m, lb, na);

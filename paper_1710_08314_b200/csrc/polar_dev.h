@@ -114,6 +114,8 @@ struct LaunchParams {
                                // (and the channel) evict_first; 0 = no cache hints
     int32_t sc_discard;        // frame-per-lane SC pass: discard.global.L2 the lines of a
                                // global depth segment after its last read (G op)
+    int32_t list_discard;      // float list passes: the same for a frame's global depth
+                               // pool after a G op
 };
 
 constexpr int kMaxWarpsPerBlock = 4; // a block is 1, 2 or 4 independent warps
