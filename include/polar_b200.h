@@ -164,6 +164,15 @@ int pl_decode_host_packed(pl_handle* h, const void* llr, const int64_t* llr_offs
 /* Kernel launches issued by the last pl_decode / pl_decode_host call. */
 int64_t pl_last_launches(const pl_handle* h);
 
+/* Per-frame decode latency (the reference's run_frame timing, sim.cpp:54-61:
+ * lat_sum / lat_worst over decode() calls).  With a device buffer set,
+ * every later pl_decode / pl_decode_packed on the handle writes lat_ns[f] =
+ * device time (ns, %globaltimer) from the start of frame f's decode to its
+ * final output, summed over the passes it runs through (SC, then each rung
+ * of an adaptive ladder); NULL switches it off.  The buffer must hold one
+ * uint32 per frame of each call. */
+int pl_frame_latency(pl_handle* h, uint32_t* lat_ns);
+
 /* Live kernel timing: with profiling enabled every launch of pl_decode is
  * bracketed by CUDA events on its stream; pl_last_kernel_ms waits for them
  * and writes the duration (ms) of each launch of the last pl_decode call and

@@ -87,9 +87,10 @@ typedef struct pl_point_stats {
     uint64_t frames, bit_errors, frame_errors, esc_sum;
     double ber, fer;
     double ti_mbps;      /* info bits over summed decode-kernel time (GPU throughput) */
-    double lat_avg_us;   /* mean decode time of a device batch (every frame of a batch
-                            completes within it) */
-    double lat_worst_us; /* longest batch */
+    double lat_avg_us;   /* mean per-frame decode time on the device (pl_frame_latency:
+                            from the start of a frame's decode to its final output,
+                            summed over its passes), as run_frame times decode() */
+    double lat_worst_us; /* largest per-frame decode time */
     double esc_mean;
 } pl_point_stats;
 

@@ -430,6 +430,7 @@ struct pl_handle {
     int nmax = 0;
     int64_t pstride = 0, cstride = 0;
     int esz = 4;
+    uint32_t* lat_ns = nullptr; // pl_frame_latency: per-frame decode time of pl_decode(_packed)
     int sc_keep = 0; // L2 hint split of the frame-per-lane SC pass (LaunchParams::sc_keep)
     int sc_discard = 0; // LaunchParams::sc_discard
     int list_discard = 0; // LaunchParams::list_discard
@@ -702,7 +703,8 @@ int fail(pl_handle* h, int code, const std::string& msg) {
 
 void run_decode(pl_handle& h, const void* llr, const int32_t* code_id, int64_t nframes,
                 uint8_t* payload, uint8_t* codeword, uint8_t* crc_ok, uint8_t* esc,
-                float* metric, cudaStream_t s, int exec = 0, const int64_t* llr_offset = nullptr) {
+                float* metric, cudaStream_t s, int exec = 0, const int64_t* llr_offset = nullptr,
+                uint32_t* lat_ns = nullptr) {
     ck(cudaSetDevice(h.device), "cudaSetDevice");
     h.launches = 0;
     h.prof_kind.clear(); // timed decode launches of this call (pl_last_kernel_ms)
@@ -731,6 +733,8 @@ void run_decode(pl_handle& h, const void* llr, const int32_t* code_id, int64_t n
     base.crc_ok = crc_ok;
     base.esc = esc;
     base.metric = metric;
+    base.lat_ns = lat_ns;
+    if (lat_ns) ck(cudaMemsetAsync(lat_ns, 0, size_t(nframes) * sizeof(uint32_t), s), "memset");
     base.gscratch = x.d_gscratch;
     base.nmax = h.nmax;
     int slot = 0;
@@ -1214,6 +1218,12 @@ int64_t pl_codeword_stride(const pl_handle* h) { return h ? h->cstride : 0; }
 int32_t pl_precision(const pl_handle* h) { return h ? h->dec.precision : -1; }
 int64_t pl_last_launches(const pl_handle* h) { return h ? h->launches : 0; }
 
+int pl_frame_latency(pl_handle* h, uint32_t* lat_ns) {
+    if (!h) return fail(nullptr, PL_ERR_ARG, "null handle");
+    h->lat_ns = lat_ns;
+    return PL_OK;
+}
+
 int pl_kernel_selftest(int32_t device, uint64_t* mismatches) {
     if (!mismatches) return fail(nullptr, PL_ERR_ARG, "null argument");
     if (cudaSetDevice(device) != cudaSuccess) return fail(nullptr, PL_ERR_CUDA, "no such CUDA device");
@@ -1256,7 +1266,7 @@ int pl_decode(pl_handle* h, const void* llr, const int32_t* code_id, int64_t nfr
     if (nframes > INT32_MAX) return fail(h, PL_ERR_ARG, "too many frames in one call");
     try {
         run_decode(*h, llr, code_id, nframes, payload, codeword, crc_ok, esc, metric,
-                   static_cast<cudaStream_t>(stream));
+                   static_cast<cudaStream_t>(stream), 0, nullptr, h->lat_ns);
         h->err.clear();
         return PL_OK;
     } catch (const std::exception& e) {
@@ -1273,7 +1283,7 @@ int pl_decode_packed(pl_handle* h, const void* llr, const int64_t* llr_offset, c
     if (nframes > INT32_MAX) return fail(h, PL_ERR_ARG, "too many frames in one call");
     try {
         run_decode(*h, llr, code_id, nframes, payload, codeword, crc_ok, esc, metric,
-                   static_cast<cudaStream_t>(stream), 0, llr_offset);
+                   static_cast<cudaStream_t>(stream), 0, llr_offset, h->lat_ns);
         h->err.clear();
         return PL_OK;
     } catch (const std::exception& e) {

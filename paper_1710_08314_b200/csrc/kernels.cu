@@ -392,6 +392,13 @@ __device__ __forceinline__ void vst_hint(R* ptr, const Vec<R, G>& x, uint64_t po
                  :: "l"(ptr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol) : "memory");
 }
 
+// per-frame decode time (LaunchParams::lat_ns): the device's global timer
+__device__ __forceinline__ uint64_t gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 // first channel LLR of a frame: fixed stride, or the packed layout's offset
 template <typename R>
 __device__ __forceinline__ const R* frame_llr(const LaunchParams& P, int frame) {
@@ -636,6 +643,9 @@ __device__ __forceinline__ void fg_run_batched(Ctx<R, SW>& cx, int d, int h, int
 
 #ifndef PLB_FG_UNROLL
 #define PLB_FG_UNROLL 2
+#endif
+#ifndef PLB_FG_UNROLL_MINKV
+#define PLB_FG_UNROLL_MINKV 6
 #endif
 template <int UB = 1, typename R, int SW>
 __device__ __forceinline__ void fg_elems(Ctx<R, SW>& cx, int d, int m, int lb, int na, bool is_g) {
@@ -1534,6 +1544,9 @@ __device__ void list_frame(const LaunchParams& P, const DevCode& C, unsigned cha
     using A = Arith<R>;
     using M = typename A::M;
     constexpr int CW = kv_cw(KV, SW), MAXW = kv_maxw(KV, SW);
+    // (the start time goes to memory, not a register live across the op loop:
+    // lat = end - start in wrapping 32-bit ns)
+    if (P.lat_ns && active && sw.lane == 0) P.lat_ns[frame] -= uint32_t(gtimer());
     Ctx<R, SW> cx;
     setup_ctx<TEAM>(cx, P, C, sm, gs, frame, sw, kv_l(KV), segmax); // P.l == kv_l(KV)
     const int lane = cx.lane;
@@ -1546,7 +1559,7 @@ __device__ void list_frame(const LaunchParams& P, const DevCode& C, unsigned cha
         const int na = __popc(cx.alive);
         const bool fused = (op & kOpFused) != 0;
         if (fused) fused_leaf(cx, code, d, m, lb, na, (op & kOpFusedG) != 0);
-        if (code <= OP_G) op_fg<(sizeof(R) == 4 && KV >= 6) ? PLB_FG_UNROLL : 1>(cx, d, m, lb, na, code == OP_G);
+        if (code <= OP_G) op_fg<(sizeof(R) == 4 && KV >= PLB_FG_UNROLL_MINKV) ? PLB_FG_UNROLL : 1>(cx, d, m, lb, na, code == OP_G);
         else if (code == OP_H) op_h(cx, m, lb, na);
         else if (code == OP_FROZEN) {
             if (!fused) list_frozen(cx, d, m, lb, na);
@@ -1609,6 +1622,7 @@ __device__ void list_frame(const LaunchParams& P, const DevCode& C, unsigned cha
             if (P.esc) P.esc[frame] = uint8_t(P.esc_level);
             if (P.metric) P.metric[frame] = A::to_float(pm);
             if (P.fail_list && C.crc_width > 0 && !crc_ok) P.fail_list[atomicAdd(P.fail_count, 1)] = frame;
+            if (P.lat_ns) P.lat_ns[frame] += uint32_t(gtimer());
         }
     }
     __syncwarp();
@@ -1707,6 +1721,7 @@ __device__ void sc_frame(const LaunchParams& P, const DevCode& C, unsigned char*
                          unsigned char* gs, int frame, const Sub<32>& sw) {
     using A = Arith<R>;
     using M = typename A::M;
+    if (P.lat_ns && sw.lane == 0) P.lat_ns[frame] -= uint32_t(gtimer());
     Ctx<R, 32> cx;
     setup_ctx(cx, P, C, sm, gs, frame, sw, 1, P.seg_smem_max);
     const int lane = cx.lane;
@@ -1769,6 +1784,7 @@ __device__ void sc_frame(const LaunchParams& P, const DevCode& C, unsigned char*
         if (P.esc) P.esc[frame] = 1;
         if (P.metric) P.metric[frame] = 0.0f; // DecodeResult default (decode_result.hpp:12)
         if (P.fail_list && C.crc_width > 0 && !crc_ok) P.fail_list[atomicAdd(P.fail_count, 1)] = frame;
+        if (P.lat_ns) P.lat_ns[frame] += uint32_t(gtimer());
     }
     __syncwarp();
 }
@@ -2280,6 +2296,7 @@ __device__ void lane_frame(const LaunchParams& P, const DevCode& C, unsigned cha
                            unsigned char* gs, int frame, bool active, int lane) {
     using A = Arith<R>;
     using M = typename A::M;
+    if (P.lat_ns && active) P.lat_ns[frame] -= uint32_t(gtimer());
     LaneCtx<R> c;
     c.lane = lane;
     c.n = C.n;
@@ -2375,6 +2392,7 @@ __device__ void lane_frame(const LaunchParams& P, const DevCode& C, unsigned cha
         if (P.crc_ok) P.crc_ok[frame] = uint8_t(crc_ok);
         if (P.esc) P.esc[frame] = 1;
         if (P.metric) P.metric[frame] = 0.0f; // DecodeResult default (decode_result.hpp:12)
+        if (P.lat_ns) P.lat_ns[frame] += uint32_t(gtimer());
     }
     // failed frames -> the next rung's list (warp-aggregated append)
     if (P.fail_list && C.crc_width > 0) {

@@ -116,6 +116,8 @@ struct LaunchParams {
                                // global depth segment after its last read (G op)
     int32_t list_discard;      // float list passes: the same for a frame's global depth
                                // pool after a G op
+    uint32_t* lat_ns;          // nullable: per-frame device decode time, ns, summed over
+                               // the passes the frame runs through (pl_frame_latency)
 };
 
 constexpr int kMaxWarpsPerBlock = 4; // a block is 1, 2 or 4 independent warps

@@ -26,7 +26,8 @@ constexpr int64_t kBatch = 1024; // sim.cpp:18
 __global__ void count_errors_kernel(const uint8_t* payload, int64_t pstride, const uint8_t* info,
                                     int k, const uint8_t* esc, int64_t nframes,
                                     unsigned long long* batch_be, unsigned int* batch_fe,
-                                    unsigned long long* batch_esc) {
+                                    unsigned long long* batch_esc, const uint32_t* lat,
+                                    unsigned long long* batch_lsum, unsigned int* batch_lmax) {
     const int lane = threadIdx.x & 31;
     const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
     for (int64_t f = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); f < nframes;
@@ -55,6 +56,10 @@ __global__ void count_errors_kernel(const uint8_t* payload, int64_t pstride, con
                 atomicAdd(batch_fe + b, 1u);
             }
             atomicAdd(batch_esc + b, (unsigned long long)(esc ? esc[f] : 1));
+            if (lat) {
+                atomicAdd(batch_lsum + b, (unsigned long long)lat[f]);
+                atomicMax(batch_lmax + b, lat[f]);
+            }
         }
     }
 }
@@ -107,10 +112,11 @@ struct HostBuf {
 
 struct SimBuffers {
     int device = -1;
-    DevBuf d_llr, d_info, d_pay, d_esc, d_be, d_fe, d_es;
+    DevBuf d_llr, d_info, d_pay, d_esc, d_be, d_fe, d_es, d_lat, d_ls, d_lm;
     HostBuf h_llr, h_info;
     void reset() {
-        for (DevBuf* b : {&d_llr, &d_info, &d_pay, &d_esc, &d_be, &d_fe, &d_es}) b->release();
+        for (DevBuf* b : {&d_llr, &d_info, &d_pay, &d_esc, &d_be, &d_fe, &d_es, &d_lat, &d_ls, &d_lm})
+            b->release();
         h_llr.release();
         h_info.release();
     }
@@ -154,16 +160,20 @@ int pl_sim_point(pl_handle* h, const pl_code* code, const pl_sim_config* cfg, pl
     }
     DevBuf &d_llr = g_buf.d_llr, &d_info = g_buf.d_info, &d_pay = g_buf.d_pay, &d_esc = g_buf.d_esc;
     DevBuf &d_be = g_buf.d_be, &d_fe = g_buf.d_fe, &d_es = g_buf.d_es;
+    DevBuf &d_lat = g_buf.d_lat, &d_ls = g_buf.d_ls, &d_lm = g_buf.d_lm;
     HostBuf &h_llr = g_buf.h_llr, &h_info = g_buf.h_info;
     cudaStream_t s = nullptr;
     EventPair ev;
     std::vector<unsigned long long> be(static_cast<size_t>(nb)), es(static_cast<size_t>(nb));
-    std::vector<unsigned int> fe(static_cast<size_t>(nb));
+    std::vector<unsigned int> fe(static_cast<size_t>(nb)), lm(static_cast<size_t>(nb));
+    std::vector<unsigned long long> ls(static_cast<size_t>(nb));
     auto ck = [](cudaError_t e) { return e == cudaSuccess; };
     if (!ck(d_llr.alloc(size_t(chunk * n * esz))) || !ck(d_info.alloc(size_t(chunk * k))) ||
         !ck(d_pay.alloc(size_t(chunk * pstride))) || !ck(d_esc.alloc(size_t(chunk))) ||
         !ck(d_be.alloc(size_t(nb) * 8)) || !ck(d_fe.alloc(size_t(nb) * 4)) ||
-        !ck(d_es.alloc(size_t(nb) * 8)) || !ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)) ||
+        !ck(d_es.alloc(size_t(nb) * 8)) || !ck(d_lat.alloc(size_t(chunk) * 4)) ||
+        !ck(d_ls.alloc(size_t(nb) * 8)) || !ck(d_lm.alloc(size_t(nb) * 4)) ||
+        !ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)) ||
         !ck(cudaEventCreate(&ev.a)) || !ck(cudaEventCreate(&ev.b))) {
         if (s) cudaStreamDestroy(s);
         return PL_ERR_CUDA;
@@ -174,9 +184,11 @@ int pl_sim_point(pl_handle* h, const pl_code* code, const pl_sim_config* cfg, pl
         return PL_ERR_CUDA;
     }
 
-    uint64_t done = 0, decoded = 0, tot_be = 0, tot_fe = 0, tot_es = 0;
-    double dec_us = 0, worst_us = 0;
-    int64_t nchunks = 0;
+    uint64_t done = 0, decoded = 0, tot_be = 0, tot_fe = 0, tot_es = 0, lat_sum = 0;
+    uint32_t lat_worst = 0;
+    double dec_us = 0;
+    // per-frame decode time (pl_frame_latency) over the frames that count
+    pl_frame_latency(h, d_lat.get<uint32_t>());
     int rc = PL_OK;
     bool stop = false;
     while (!stop && done < max_frames) {
@@ -200,6 +212,8 @@ int pl_sim_point(pl_handle* h, const pl_code* code, const pl_sim_config* cfg, pl
         cudaMemsetAsync(d_be.p, 0, size_t(nbc) * 8, s);
         cudaMemsetAsync(d_fe.p, 0, size_t(nbc) * 4, s);
         cudaMemsetAsync(d_es.p, 0, size_t(nbc) * 8, s);
+        cudaMemsetAsync(d_ls.p, 0, size_t(nbc) * 8, s);
+        cudaMemsetAsync(d_lm.p, 0, size_t(nbc) * 4, s);
         cudaEventRecord(ev.a, s);
         rc = pl_decode(h, d_llr.p, nullptr, nf, d_pay.get<uint8_t>(), nullptr, nullptr,
                        d_esc.get<uint8_t>(), nullptr, s);
@@ -207,11 +221,15 @@ int pl_sim_point(pl_handle* h, const pl_code* code, const pl_sim_config* cfg, pl
         cudaEventRecord(ev.b, s);
         count_errors_kernel<<<1184, 256, 0, s>>>(d_pay.get<uint8_t>(), pstride, d_info.get<uint8_t>(), k,
                                                   d_esc.get<uint8_t>(), nf, d_be.get<unsigned long long>(),
-                                                  d_fe.get<unsigned int>(), d_es.get<unsigned long long>());
+                                                  d_fe.get<unsigned int>(), d_es.get<unsigned long long>(),
+                                                  d_lat.get<uint32_t>(), d_ls.get<unsigned long long>(),
+                                                  d_lm.get<unsigned int>());
         if (!ck(cudaGetLastError()) ||
             !ck(cudaMemcpyAsync(be.data(), d_be.p, size_t(nbc) * 8, cudaMemcpyDeviceToHost, s)) ||
             !ck(cudaMemcpyAsync(fe.data(), d_fe.p, size_t(nbc) * 4, cudaMemcpyDeviceToHost, s)) ||
             !ck(cudaMemcpyAsync(es.data(), d_es.p, size_t(nbc) * 8, cudaMemcpyDeviceToHost, s)) ||
+            !ck(cudaMemcpyAsync(ls.data(), d_ls.p, size_t(nbc) * 8, cudaMemcpyDeviceToHost, s)) ||
+            !ck(cudaMemcpyAsync(lm.data(), d_lm.p, size_t(nbc) * 4, cudaMemcpyDeviceToHost, s)) ||
             !ck(cudaStreamSynchronize(s))) {
             rc = PL_ERR_CUDA;
             break;
@@ -219,9 +237,7 @@ int pl_sim_point(pl_handle* h, const pl_code* code, const pl_sim_config* cfg, pl
         float ms = 0.f;
         cudaEventElapsedTime(&ms, ev.a, ev.b);
         dec_us += 1e3 * double(ms);
-        worst_us = std::max(worst_us, 1e3 * double(ms));
         decoded += uint64_t(nf);
-        ++nchunks;
         // the reference's batch loop (sim.cpp:91-115), one 1024-frame batch
         // at a time
         for (int64_t b = 0; b < nbc; ++b) {
@@ -229,6 +245,8 @@ int pl_sim_point(pl_handle* h, const pl_code* code, const pl_sim_config* cfg, pl
             tot_be += be[size_t(b)];
             tot_fe += fe[size_t(b)];
             tot_es += es[size_t(b)];
+            lat_sum += ls[size_t(b)];
+            lat_worst = std::max(lat_worst, lm[size_t(b)]);
             done += uint64_t(bf);
             if (cfg->max_fe && tot_fe >= cfg->max_fe) {
                 stop = true;
@@ -236,6 +254,7 @@ int pl_sim_point(pl_handle* h, const pl_code* code, const pl_sim_config* cfg, pl
             }
         }
     }
+    pl_frame_latency(h, nullptr);
     cudaStreamDestroy(s);
     if (rc != PL_OK) return rc;
 
@@ -251,8 +270,11 @@ int pl_sim_point(pl_handle* h, const pl_code* code, const pl_sim_config* cfg, pl
     p.esc_mean = done ? double(tot_es) / double(done) : 0;
     if (dec_us > 0) {
         p.ti_mbps = double(k) * double(decoded) / dec_us; // bits per µs = Mb/s
-        p.lat_avg_us = dec_us / double(nchunks);
-        p.lat_worst_us = worst_us;
+    }
+    if (done) {
+        // per frame, as run_frame times each decode() (sim.cpp:54-61, 131-134)
+        p.lat_avg_us = double(lat_sum) * 1e-3 / double(done);
+        p.lat_worst_us = double(lat_worst) * 1e-3;
     }
     *out = p;
     return PL_OK;

@@ -587,6 +587,17 @@ class FrameDecoder:
             _raise(rc, L.last_error(self._h))
         return o
 
+    def frame_latency(self, lat_ns=None):
+        """pl_frame_latency: later decode_batch / decode_packed calls write
+        each frame's device decode time in ns into ``lat_ns`` (a CUDA int32
+        tensor, one entry per frame); None switches it off."""
+        if lat_ns is not None:
+            assert lat_ns.is_cuda and lat_ns.dtype == self._torch.int32 and lat_ns.is_contiguous()
+        self._lat = lat_ns  # keep the buffer alive while the library holds it
+        rc = L.lib().pl_frame_latency(self._h, C.c_void_p(lat_ns.data_ptr()) if lat_ns is not None else None)
+        if rc:
+            _raise(rc, L.last_error(self._h))
+
     def last_launches(self) -> int:
         return int(L.lib().pl_last_launches(self._h))
 

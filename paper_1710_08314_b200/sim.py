@@ -116,8 +116,10 @@ def run_point(dec: FrameDecoder, cfg: SimConfig, ebn0_db: float, frame0: int = 0
 
 
 def run_montecarlo(cfg: SimConfig, rank: int = 0, world: int = 1, reduce=None) -> list[PointStats]:
-    """The sweep.  ``reduce(list_of_ints) -> list_of_ints`` sums counters over
-    ranks (e.g. a torch.distributed all-reduce) when world > 1."""
+    """The sweep.  ``reduce(list_of_ints, op="sum"|"max") -> list_of_ints``
+    combines counters over ranks (e.g. a torch.distributed all-reduce) when
+    world > 1: the error counts and the per-frame latency sum add up, the
+    worst per-frame latency is the maximum."""
     _validate(cfg)
     if world > 1 and (cfg.max_fe or not cfg.max_frames):
         raise ConfigError("multi-rank sweeps need a fixed frame count (max_fe = 0)")
@@ -129,8 +131,11 @@ def run_montecarlo(cfg: SimConfig, rank: int = 0, world: int = 1, reduce=None) -
             a = cfg.max_frames * rank // world
             b = cfg.max_frames * (rank + 1) // world
             p = run_point(dec, cfg, e, cfg.frame0 + a, b - a)
-            tot = reduce([p.frames, p.bit_errors, p.frame_errors, p.esc_sum])
-            p.frames, p.bit_errors, p.frame_errors, p.esc_sum = (int(x) for x in tot)
+            lat_ns = int(round(p.lat_avg_us * 1e3 * p.frames))
+            tot = reduce([p.frames, p.bit_errors, p.frame_errors, p.esc_sum, lat_ns])
+            p.frames, p.bit_errors, p.frame_errors, p.esc_sum = (int(x) for x in tot[:4])
+            p.lat_avg_us = int(tot[4]) * 1e-3 / p.frames if p.frames else 0.0
+            p.lat_worst_us = int(reduce([int(round(p.lat_worst_us * 1e3))], op="max")[0]) * 1e-3
             kf = cfg.code.k * p.frames
             p.ber = p.bit_errors / kf if p.frames else 0.0
             p.fer = p.frame_errors / p.frames if p.frames else 0.0
@@ -217,9 +222,9 @@ def _main(argv=None):
             dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
         red_dev = "cpu" if shared else f"cuda:{local}"
 
-        def reduce(v):
+        def reduce(v, op="sum"):
             t = torch.tensor(v, dtype=torch.int64, device=red_dev)
-            dist.all_reduce(t)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
             return t.tolist()
     parts = a.code.split(":", 2)
     a.n, a.k, a.crc = int(parts[0]), int(parts[1]), (parts[2] if len(parts) > 2 else "")

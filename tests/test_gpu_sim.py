@@ -92,7 +92,7 @@ def test_sharded_point_equals_single(P, S):
     whole = S.run_montecarlo(cfg)[0]
     parts = []
     for r in range(3):
-        parts.append(S.run_montecarlo(cfg, rank=r, world=3, reduce=lambda v, r=r: v)[0])
+        parts.append(S.run_montecarlo(cfg, rank=r, world=3, reduce=lambda v, op="sum", r=r: v)[0])
     assert sum(p.frames for p in parts) == whole.frames
     assert sum(p.bit_errors for p in parts) == whole.bit_errors
     assert sum(p.frame_errors for p in parts) == whole.frame_errors
@@ -131,3 +131,31 @@ def test_sweep_cli_two_ranks_equals_one(tmp_path):
         return [(r[0], r[1], r[2], r[3], r[9]) for r in rows]  # all but the timing columns
 
     assert counts(one.stdout) == counts(two.stdout) and len(counts(one.stdout)) == 3
+
+
+def test_frame_latency(P, S, gpu):
+    """pl_frame_latency: per-frame device decode time (the reference times
+    every decode() call, sim.cpp:54-61).  Every frame gets a positive time;
+    frames that climbed the FA ladder took longer than SC-only ones; the
+    Monte-Carlo point reports the per-frame mean and worst."""
+    code = _code(P, 1024, 480, "32-GZIP")
+    _, llr = P.channel(code, 2.0, 5, 0, 4096, "f32")
+    dec = P.FrameDecoder(code, "fa_sscl", 16, "f32")
+    lat = gpu.zeros(4096, dtype=gpu.int32, device="cuda")
+    dec.frame_latency(lat)
+    out = dec.decode_batch(gpu.from_numpy(llr).cuda())
+    gpu.cuda.synchronize()
+    t = lat.cpu().numpy().astype(np.int64)
+    esc = out["esc"].cpu().numpy()
+    assert (t > 0).all()
+    assert (esc > 1).any() and (esc == 1).any()
+    assert t[esc > 1].mean() > t[esc == 1].mean()
+    dec.frame_latency(None)
+    lat.zero_()
+    dec.decode_batch(gpu.from_numpy(llr).cuda())
+    gpu.cuda.synchronize()
+    assert int(lat.abs().sum()) == 0
+    cfg = S.SimConfig(code, "fa_sscl", 16, "f32", ebn0_min=2.0, ebn0_max=2.0, max_frames=8192,
+                      max_fe=0, channel="device")
+    p = S.run_montecarlo(cfg)[0]
+    assert 0 < p.lat_avg_us <= p.lat_worst_us
