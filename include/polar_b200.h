@@ -73,7 +73,7 @@ typedef struct pl_crc {
 } pl_crc;
 
 typedef struct pl_code {
-    int32_t n;             /* block length, power of two, 2..16384 */
+    int32_t n;             /* block length, power of two, 2..32768 */
     int32_t k;             /* information bits, CRC excluded (code.hpp:31) */
     const uint8_t* frozen; /* n bytes, nonzero = frozen; host memory */
     pl_crc crc;

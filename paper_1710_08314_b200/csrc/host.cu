@@ -331,7 +331,8 @@ struct HostCode {
 HostCode make_host_code(const pl_code& c, const pl_decoder& dec) {
     if (c.n < 2 || (c.n & (c.n - 1)) != 0)
         throw ConfigError("N must be a power of two >= 2 (got " + std::to_string(c.n) + ")");
-    if (c.n > 16384) throw ConfigError("N > 16384 is not supported by the GPU decoder");
+    // schedule words hold log2(m) and the depth in 4 bits each (polar_dev.h)
+    if (c.n > 32768) throw ConfigError("N > 32768 is not supported by the GPU decoder");
     if (c.k < 1) throw ConfigError("K must be at least 1 (got " + std::to_string(c.k) + ")");
     if (!c.frozen) throw ConfigError("frozen mask is null");
     HostCode h;

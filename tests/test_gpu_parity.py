@@ -333,17 +333,18 @@ def test_decode_host_matches_device_path(P, gpu):
 
 def test_edge_codes(P, gpu, oracle_lib):
     """Rate-1 and rate-1/N codes, the smallest N, and the largest N = 16384
-    at L = 32 (the per-warp area forces 1-warp blocks)."""
+    and 32768 at L = 32 (the per-warp area forces 1-warp blocks)."""
     rng = np.random.default_rng(99)
     cases = [
         (P.make_code(64, 56, np.zeros(64, np.uint8), "8"), ["ssc", "sscl", "fa_sscl"]),  # no frozen bit
         (P.make_code(64, 1, np.r_[np.ones(63, np.uint8), 0]), ["sc", "ssc", "scl", "sscl"]),  # repetition code
         (P.make_code(2, 1, np.array([1, 0], np.uint8)), ["sc", "ssc", "scl", "sscl"]),
         (_code(P, 16384, 8000, "32-GZIP"), ["ssc", "fa_sscl"]),
+        (_code(P, 32768, 20000, "32-GZIP"), ["ssc", "fa_sscl"]),
     ]
     for code, kinds in cases:
         for prec in ("f32", "i8"):
-            llr = rough_llrs(rng, code.n, 6 if code.n > 4096 else 24, prec)
+            llr = rough_llrs(rng, code.n, (3 if code.n > 16384 else 6) if code.n > 4096 else 24, prec)
             for kind in kinds:
                 l = 32 if code.n > 4096 else 8
                 check_parity(P, gpu, code, kind, l, prec, P.PruningConfig(), llr, "edge")
