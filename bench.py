@@ -388,6 +388,7 @@ def measure(wl, F, steps, warmup, e2e_steps, R: Ranks, peaks, peak_src):
     codes, cid, info, ks, llr_np = make_batch(wl, frame0, F,
                                               nthreads=max(1, (os.cpu_count() or 1) // ws))
     llr_h = torch.from_numpy(llr_np).pin_memory()
+    llr_np = llr_h.numpy()  # one host copy (the pinned one): N ranks x 8.6 GB for cfg2
     llr_d = llr_h.cuda(local)
     cid_h = torch.from_numpy(cid).pin_memory() if cid is not None else None
     cid_d = cid_h.cuda(local) if cid is not None else None

@@ -1219,6 +1219,13 @@ int64_t pl_codeword_stride(const pl_handle* h) { return h ? h->cstride : 0; }
 int32_t pl_precision(const pl_handle* h) { return h ? h->dec.precision : -1; }
 int64_t pl_last_launches(const pl_handle* h) { return h ? h->launches : 0; }
 
+#ifdef PLB_OPTIME
+// profiling build only: cycles and counts per list-op kind of frame 0
+int pl_debug_optime(unsigned long long* out, int reset) {
+    return plb::read_optime(out, reset != 0) == cudaSuccess ? PL_OK : PL_ERR_CUDA;
+}
+#endif
+
 int pl_frame_latency(pl_handle* h, uint32_t* lat_ns) {
     if (!h) return fail(nullptr, PL_ERR_ARG, "null handle");
     h->lat_ns = lat_ns;

@@ -392,6 +392,10 @@ __device__ __forceinline__ void vst_hint(R* ptr, const Vec<R, G>& x, uint64_t po
                  :: "l"(ptr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol) : "memory");
 }
 
+#ifdef PLB_OPTIME
+__device__ unsigned long long g_optime[64]; // profiling build: cycles / count per op kind
+#endif
+
 // per-frame decode time (LaunchParams::lat_ns): the device's global timer
 __device__ __forceinline__ uint64_t gtimer() {
     uint64_t t;
@@ -1554,6 +1558,9 @@ __device__ void list_frame(const LaunchParams& P, const DevCode& C, unsigned cha
     const int nops = C.nops_list;
     #pragma unroll 1
     for (int oi = 0; oi < nops; ++oi) {
+#ifdef PLB_OPTIME
+        const long long ot0 = clock64();
+#endif
         const uint32_t op = __ldg(sched + oi);
         const int code = op_code(op), d = op_depth(op), m = 1 << op_logm(op), lb = op_lb(op);
         const int na = __popc(cx.alive);
@@ -1566,6 +1573,15 @@ __device__ void list_frame(const LaunchParams& P, const DevCode& C, unsigned cha
         } else {
             list_fork_node<R, SW, CW, MAXW>(cx, code, d, m, lb, na, fused);
         }
+#ifdef PLB_OPTIME
+        // (profiling build only) cycles per op kind of the first frame
+        __syncwarp();
+        if (frame == 0 && lane == 0) {
+            const int slot = code * 2 + (fused ? 1 : 0);
+            atomicAdd(&g_optime[slot], (unsigned long long)(clock64() - ot0));
+            atomicAdd(&g_optime[32 + slot], 1ull);
+        }
+#endif
     }
     // finish (list_decoder.hpp:457-502): stable order by (metric, slot)
     using K = typename A::Key;
@@ -2603,6 +2619,17 @@ cudaError_t bucket_by_code(const int32_t* cid, int64_t n, int ncodes, int32_t* h
     code_scatter_kernel<<<grid, 256, 0, s>>>(cid, n, hist, out);
     return cudaGetLastError();
 }
+
+#ifdef PLB_OPTIME
+cudaError_t read_optime(unsigned long long* out, bool reset) {
+    cudaError_t e = cudaMemcpyFromSymbol(out, g_optime, sizeof(g_optime));
+    if (e == cudaSuccess && reset) {
+        static const unsigned long long z[64] = {};
+        e = cudaMemcpyToSymbol(g_optime, z, sizeof(z));
+    }
+    return e;
+}
+#endif
 
 cudaError_t kernel_selftest(unsigned long long* mismatches) {
     unsigned long long* d = nullptr;

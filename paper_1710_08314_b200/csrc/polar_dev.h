@@ -151,5 +151,8 @@ cudaError_t bucket_by_code(const int32_t* cid, int64_t n, int ncodes, int32_t* h
                            int32_t* count_out, cudaStream_t s);
 // Exhaustive device check of the packed int8 f/g against the scalar kernels.
 cudaError_t kernel_selftest(unsigned long long* mismatches);
+#ifdef PLB_OPTIME
+cudaError_t read_optime(unsigned long long* out, bool reset); // profiling build only
+#endif
 
 } // namespace plb
