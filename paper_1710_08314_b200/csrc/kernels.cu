@@ -747,7 +747,17 @@ __device__ __forceinline__ void span_fill_lane(uint32_t* row, int lb, int m, int
 // list_decoder.hpp:282-289) for every alive path; the result of rank r goes
 // to st_a1[r].  For m > SW the first halvings run in the rank's depth-(d+1)
 // buffer, whose contents are dead at a leaf.
-template <typename R, int SW>
+#ifndef PLB_BIG_VF
+#define PLB_BIG_VF 1 // float L = 32 kernel: vectors per trip in the per-path leaf loops
+                     // (2 / 4: 111 / 126 registers, cfg4 L=32 -8% / -10%)
+#endif
+#ifndef PLB_BIG_R1
+#define PLB_BIG_R1 1
+#endif
+#ifndef PLB_BIG_PEN
+#define PLB_BIG_PEN 1
+#endif
+template <bool BIG = false, typename R, int SW>
 __device__ void rep_fold(Ctx<R, SW>& cx, int d, int m, int na) {
     using A = Arith<R>;
     using M = typename A::M;
@@ -765,6 +775,36 @@ __device__ void rep_fold(Ctx<R, SW>& cx, int d, int m, int na) {
             }
             if (ok && i == 0) cx.fx->st_a1[r] = mbits<M>(v);
         }
+    } else if constexpr (sizeof(R) == 4 && BIG) {
+        // float, m > SW: one halving level at a time for all paths together
+        // (level len: S[i] = S[i] + S[i + len/2], i < len/2 — the same sums
+        // as the per-path loop below, in the same tree), so a level costs one
+        // round trip to the depth-(d+1) buffers instead of one per path
+        const int h = m >> 1;
+        R* const S0 = cx.pool(d + 1);
+        {
+            const int q = h >> 2, lgq = __ffs(q) - 1; // float4 items per path
+            #pragma unroll 1
+            for (int t = cx.lane; t < (na << lgq); t += SW) {
+                const int r = t >> lgq, c = (t & (q - 1)) << 2;
+                const R* L = cx.llr(cx.fx->alive_list[r], d);
+                const Vec<R, 4> a = vld<R, 4>(L + c), b = vld<R, 4>(L + h + c);
+                vst<R, 4>(S0 + r * h + c, fg_compute<R, 4>(a, b, 0u, true)); // g with u = 0: a + b
+            }
+            __syncwarp();
+        }
+        #pragma unroll 1
+        for (int len = h; len > 1; len >>= 1) {
+            const int hh = len >> 1, lgh = __ffs(hh) - 1;
+            #pragma unroll 1
+            for (int t = cx.lane; t < (na << lgh); t += SW) {
+                R* S = S0 + (t >> lgh) * h;
+                const int i = t & (hh - 1);
+                S[i] = A::store(A::sat(A::val(S[i]), A::val(S[i + hh])));
+            }
+            __syncwarp();
+        }
+        if (cx.lane < na) cx.fx->st_a1[cx.lane] = mbits<M>(A::val(S0[cx.lane * h]));
     } else {
         #pragma unroll 1
         for (int r = 0; r < na; ++r) {
@@ -991,7 +1031,7 @@ __device__ void fork_apply(Ctx<R, SW>& cx, const typename Arith<R>::M (&cm)[CPL]
 }
 
 // frozen leaf / rate-0 node (list_decoder.hpp:227-238)
-template <typename R, int SW>
+template <bool BIG = false, typename R, int SW>
 __device__ void list_frozen(Ctx<R, SW>& cx, int d, int m, int lb, int na) {
     using A = Arith<R>;
     using M = typename A::M;
@@ -1009,12 +1049,35 @@ __device__ void list_frozen(Ctx<R, SW>& cx, int d, int m, int lb, int na) {
         }
     } else if (cx.lane < na) {
         const R* L = cx.llr(cx.fx->alive_list[cx.lane], d);
+        if constexpr (sizeof(R) == 4 && BIG && PLB_BIG_PEN) {
+            if (m >= 8) {
+                // float: PLB_BIG_VF vectors in flight per trip; the penalty
+                // is still summed one value at a time in index order
+                #pragma unroll 1
+                for (int i = 0; i < m; i += 4 * PLB_BIG_VF) {
+                    Vec<R, 4> q[PLB_BIG_VF];
+#pragma unroll
+                    for (int u = 0; u < PLB_BIG_VF; ++u)
+                        if (i + 4 * u < m) q[u] = vld<R, 4>(L + i + 4 * u);
+#pragma unroll
+                    for (int u = 0; u < PLB_BIG_VF; ++u)
+                        if (i + 4 * u < m)
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                const M v = A::val(q[u].v[j]);
+                                if (v < M(0)) pen = A::sat(pen, -v);
+                            }
+                }
+                goto frozen_pen_done;
+            }
+        }
         #pragma unroll 1
         for (int i = 0; i < m; ++i) {
             const M v = A::val(L[i]);
             if (v < M(0)) pen = A::sat(pen, -v); // sequential: float order matters
         }
     }
+frozen_pen_done:
     const M pr = cx.sw.shfl(pen, cx.myrank & (SW - 1));
     if (cx.is_alive()) cx.metric = A::sat(cx.metric, pr);
     if (m >= 32) {
@@ -1032,7 +1095,7 @@ __device__ void list_frozen(Ctx<R, SW>& cx, int d, int m, int lb, int na) {
 // Per-path statistics of an R1 / SPC node: hard decisions written into the
 // path's own psum span, the two smallest magnitudes under the (value, index)
 // order (select.hpp:18-68) -> st_i1/st_a1, st_i2/st_a2, parity -> st_w.
-template <typename R, int SW>
+template <bool BIG = false, typename R, int SW>
 __device__ void r1spc_stats(Ctx<R, SW>& cx, int d, int m, int lb, int na) {
     using A = Arith<R>;
     using M = typename A::M;
@@ -1122,6 +1185,32 @@ __device__ void r1spc_stats(Ctx<R, SW>& cx, int d, int m, int lb, int na) {
         const uint32_t e1 = min(x, y), e2 = min(max(x, y), min(q2 & 0xffffu, q2 >> 16));
         k1 = K(((e1 >> 9) << 16) | (e1 & 511u));
         k2 = K(((e2 >> 9) << 16) | (e2 & 511u));
+    } else if (sizeof(R) == 4 && BIG && PLB_BIG_R1 && ok && E >= 4 * PLB_BIG_VF) {
+        // float L = 32 kernel: PLB_BIG_VF vectors in flight per trip, keys in
+        // index order
+        #pragma unroll 1
+        for (int k = 0; k < E; k += 4 * PLB_BIG_VF) {
+            Vec<R, 4> q[PLB_BIG_VF];
+#pragma unroll
+            for (int u = 0; u < PLB_BIG_VF; ++u) q[u] = vld<R, 4>(L + k + 4 * u);
+#pragma unroll
+            for (int u = 0; u < PLB_BIG_VF; ++u)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const M v = A::val(q[u].v[j]);
+                    acc |= uint32_t(v < M(0)) << ((k + 4 * u + j) & 31);
+                    const K kv = A::make_key(A::mag(v), i0 + k + 4 * u + j);
+                    const K n1 = kmin(k1, kv);
+                    k2 = kmin(k2, kmax(k1, kv));
+                    k1 = n1;
+                }
+            if (((k + 4 * PLB_BIG_VF) & 31) == 0 || k + 4 * PLB_BIG_VF >= E) {
+                const int pos = base + i0 + (k & ~31);
+                if (acc) atomicOr(span + (pos >> 5), acc << (pos & 31));
+                par ^= __popc(acc);
+                acc = 0;
+            }
+        }
     } else if (ok) {
         #pragma unroll 1
         for (int k = 0; k < E; k += 4) {
@@ -1172,7 +1261,7 @@ __device__ void r1spc_stats(Ctx<R, SW>& cx, int d, int m, int lb, int na) {
 // repetition node (list_decoder.hpp:276-305): after the fold, pen_w = the
 // sum of the magnitudes that disagree with the fold's decision, sequential
 // in index order (float order matters; int8 is order-free) -> st_a2, st_w.
-template <typename R, int SW>
+template <bool BIG = false, typename R, int SW>
 __device__ void rep_pen(Ctx<R, SW>& cx, int d, int m, int na) {
     using A = Arith<R>;
     using M = typename A::M;
@@ -1197,10 +1286,29 @@ __device__ void rep_pen(Ctx<R, SW>& cx, int d, int m, int na) {
         const R* L = cx.llr(cx.fx->alive_list[cx.lane], d);
         const bool w = mfrom<M>(cx.fx->st_a1[cx.lane]) < M(0);
         M pen = M(0);
-        #pragma unroll 1
-        for (int i = 0; i < m; ++i) {
-            const M v = A::val(L[i]);
-            if (w ? (v > M(0)) : (v < M(0))) pen = A::sat(pen, A::mag(v));
+        if (sizeof(R) == 4 && BIG && PLB_BIG_PEN && m >= 8) {
+            // float: PLB_BIG_VF vectors in flight per trip, summed in index order
+            #pragma unroll 1
+            for (int i = 0; i < m; i += 4 * PLB_BIG_VF) {
+                Vec<R, 4> q[PLB_BIG_VF];
+#pragma unroll
+                for (int u = 0; u < PLB_BIG_VF; ++u)
+                    if (i + 4 * u < m) q[u] = vld<R, 4>(L + i + 4 * u);
+#pragma unroll
+                for (int u = 0; u < PLB_BIG_VF; ++u)
+                    if (i + 4 * u < m)
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const M v = A::val(q[u].v[j]);
+                            if (w ? (v > M(0)) : (v < M(0))) pen = A::sat(pen, A::mag(v));
+                        }
+            }
+        } else {
+            #pragma unroll 1
+            for (int i = 0; i < m; ++i) {
+                const M v = A::val(L[i]);
+                if (w ? (v > M(0)) : (v < M(0))) pen = A::sat(pen, A::mag(v));
+            }
         }
         cx.fx->st_w[cx.lane] = w;
         cx.fx->st_a2[cx.lane] = mbits<M>(pen);
@@ -1383,17 +1491,17 @@ __device__ void fused_leaf(Ctx<R, SW>& cx, int code, int d, int m, int lb, int n
 // (ascending slot, then candidate number, list_decoder.hpp:240-333), one
 // shared fork_apply, normalisation.  C = candidates per lane, fixed per
 // kernel instantiation (4L <= SW*C).
-template <typename R, int SW, int C, int MAXW>
+template <typename R, int SW, int C, int MAXW, bool BIG = false>
 __device__ void list_fork_node(Ctx<R, SW>& cx, int code, int d, int m, int lb, int na, bool fused) {
     using A = Arith<R>;
     using M = typename A::M;
     if (fused) {
         // statistics already taken by fused_leaf
     } else if (code == OP_R1 || code == OP_SPC) {
-        r1spc_stats(cx, d, m, lb, na);
+        r1spc_stats<BIG>(cx, d, m, lb, na);
     } else if (code == OP_REP) {
-        rep_fold(cx, d, m, na);
-        rep_pen(cx, d, m, na);
+        rep_fold<BIG>(cx, d, m, na);
+        rep_pen<BIG>(cx, d, m, na);
     } else { // INFO: the leaf LLR of rank r -> st_a1[r]
         if (cx.lane < na) cx.fx->st_a1[cx.lane] = mbits<M>(A::val(cx.llr(cx.fx->alive_list[cx.lane], d)[0]));
         __syncwarp();
@@ -1569,9 +1677,9 @@ __device__ void list_frame(const LaunchParams& P, const DevCode& C, unsigned cha
         if (code <= OP_G) op_fg<(sizeof(R) == 4 && KV >= PLB_FG_UNROLL_MINKV) ? PLB_FG_UNROLL : 1>(cx, d, m, lb, na, code == OP_G);
         else if (code == OP_H) op_h(cx, m, lb, na);
         else if (code == OP_FROZEN) {
-            if (!fused) list_frozen(cx, d, m, lb, na);
+            if (!fused) list_frozen<(sizeof(R) == 4 && KV >= 6)>(cx, d, m, lb, na);
         } else {
-            list_fork_node<R, SW, CW, MAXW>(cx, code, d, m, lb, na, fused);
+            list_fork_node<R, SW, CW, MAXW, (sizeof(R) == 4 && KV >= 6)>(cx, code, d, m, lb, na, fused);
         }
 #ifdef PLB_OPTIME
         // (profiling build only) cycles per op kind of the first frame
@@ -2249,7 +2357,20 @@ template <typename R>
 __device__ bool lane_r1_nozero(const LaneCtx<R>& c, int d, int m) {
     constexpr int VE = LaneCtx<R>::VE;
     bool zero = false;
-    if (m >= VE) {
+    if (sizeof(R) == 4 && m >= 8 * VE) {
+        // float: 8 chunks (32 values) in flight per trip (the large rate-1
+        // nodes read global depth pools)
+        int cs;
+        const R* in = c.chunk_base(d, cs);
+        #pragma unroll 1
+        for (int k = 0; k < m / VE; k += 8) {
+            Vec<R, VE> q[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) q[u] = vld<R, VE>(in + (k + u) * cs);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) zero |= vec_has_zero<R, VE>(q[u]);
+        }
+    } else if (m >= VE) {
         int cs;
         const R* in = c.chunk_base(d, cs);
         #pragma unroll 1
@@ -2269,7 +2390,21 @@ template <typename R>
 __device__ void lane_r1_hard(const LaneCtx<R>& c, int d, int m, int lb) {
     using A = Arith<R>;
     constexpr int VE = LaneCtx<R>::VE;
-    if (m >= VE) {
+    if (sizeof(R) == 4 && m >= 32) {
+        // float: a 32-bit partial-sum word (8 chunks) per trip, its loads in flight together
+        int cs;
+        const R* in = c.chunk_base(d, cs);
+        #pragma unroll 1
+        for (int k = 0; k < m / VE; k += 8) {
+            Vec<R, VE> q[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) q[u] = vld<R, VE>(in + (k + u) * cs);
+            uint32_t acc = 0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc |= vec_signs<R, VE>(q[u]) << (u * VE);
+            c.word((lb + k * VE) >> 5) = acc;
+        }
+    } else if (m >= VE) {
         uint32_t acc = 0;
         int cs;
         const R* in = c.chunk_base(d, cs);
