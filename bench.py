@@ -8,8 +8,8 @@ One step = one decode of that batch (inputs resident in HBM for `value`;
 host buffers with the copies inside the timed region for `e2e`).
 `--workload` selects the other BASELINE configs (cfg0, cfg2_{2.5,3.5,4.5},
 cfg3 mixed-MCS, cfg4_L{8,16,32}); `--extra` appends a `workloads` block with
-the same measurements of further configs (default: cfg0 and the paper's
-FA-SCL points cfg2 @ 4.5 / 3.5 dB).
+the same measurements of further configs (default: every other workload at
+N = 1; cfg0 and the paper's FA-SCL points cfg2 @ 4.5 / 3.5 dB at N > 1).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg1]
   python bench.py --impl reference ...   # the reference's own CPU decoder
@@ -38,7 +38,11 @@ sys.path.insert(0, ROOT)
 
 METRIC = "decoded info throughput (Gb/s) N=2048 K=1723"
 DATA = "synthetic: BPSK-AWGN frames keyed by (seed 42, global frame index), FrameRng semantics"
-EXTRA_DEFAULT = "cfg0,cfg2_4.5,cfg2_3.5"
+# further workloads of the default run: every other BASELINE config at N = 1;
+# at N > 1 (the driver's scaling run) the paper's FA points and cfg0, whose
+# inputs every rank generates on its share of the host cores
+EXTRA_DEFAULT = "cfg0,cfg2_4.5,cfg2_3.5,cfg2_2.5,cfg3,cfg4_L8,cfg4_L16,cfg4_L32,fa_i8_4.5,fa_i16_4.5"
+EXTRA_DEFAULT_MULTI = "cfg0,cfg2_4.5,cfg2_3.5"
 # ncu counters of the current kernels (profiles/traffic.py); the newest round's file wins
 COUNTERS_FILES = [os.path.join(ROOT, "profiles", f) for f in ("r02_traffic.json", "r01_traffic.json")]
 
@@ -50,8 +54,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="cfg1")
-    ap.add_argument("--extra", default=EXTRA_DEFAULT,
-                    help="comma-separated further workloads for the `workloads` block, or 'none'")
+    ap.add_argument("--extra", default=None,
+                    help="comma-separated further workloads for the `workloads` block, or 'none' "
+                         f"(default: {EXTRA_DEFAULT} at N=1, {EXTRA_DEFAULT_MULTI} at N>1)")
     ap.add_argument("--extra-steps", type=int, default=5)
     ap.add_argument("--frames", type=int, default=0, help="override frames per GPU")
     ap.add_argument("--e2e-steps", type=int, default=0)
@@ -286,7 +291,7 @@ def run_reference(args):
                          "sample": f"{nf} frames of {wl.name} per step, FrameDecoder<R> per thread"},
         "e2e": {"value": gbps, "unit": "Gb/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    extras = [] if args.extra in ("", "none") else [w for w in args.extra.split(",") if w != args.workload]
+    extras = extra_list(args, ws)
     if extras:
         out["workloads"] = []
         for name in extras:
@@ -372,7 +377,7 @@ class Ranks:
         return float(t.item())
 
 
-def measure(wl, F, steps, warmup, e2e_steps, R: Ranks, peaks, peak_src):
+def measure(wl, F, steps, warmup, e2e_steps, R: Ranks, peaks, peak_src, min_timed_s=0.0):
     """One workload: device-resident throughput with live per-kernel CUDA-event
     timing, error counters reduced over ranks, e2e through the host API, and
     per-kernel roofline fractions.  Returns (line fields, host state kept for
@@ -397,9 +402,15 @@ def measure(wl, F, steps, warmup, e2e_steps, R: Ranks, peaks, peak_src):
     stream = torch.cuda.current_stream(local)
     bits_per_step = float(ks.sum())
 
+    t_w = time.perf_counter()
     for _ in range(warmup):
         dec.decode_batch(llr_d, code_id=cid_d, out=out)
     torch.cuda.synchronize()
+    if min_timed_s > 0:
+        # short steps: enough of them for the clock sampler (100 ms period) to
+        # see the timed region; the same count on every rank
+        per = (time.perf_counter() - t_w) / max(warmup, 1)
+        steps = int(R.max(float(max(steps, min(200, int(min_timed_s / max(per, 1e-6)) + 1)))))
 
     # ---- device-resident throughput (value), with live per-kernel timing
     dec.profile(True)
@@ -572,6 +583,11 @@ def parity_and_cpu(wl, st, S, nthr, time_it):
     return par, cpu, dt
 
 
+def extra_list(args, ws):
+    ex = args.extra if args.extra is not None else (EXTRA_DEFAULT if ws == 1 else EXTRA_DEFAULT_MULTI)
+    return [] if ex in ("", "none") else [w for w in ex.split(",") if w != args.workload]
+
+
 def main():
     args = parse()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
@@ -617,12 +633,13 @@ def main():
     del st
 
     # ---- further BASELINE configs, same measurements (driver-run evidence)
-    extras = [] if args.extra in ("", "none") else [w for w in args.extra.split(",") if w != args.workload]
+    extras = extra_list(args, ws)
     if extras:
         result["workloads"] = []
         for name in extras:
             w2 = WORKLOADS[name]
-            f2, st2 = measure(w2, w2.frames, args.extra_steps, warmup, 3, R, peaks, peak_src)
+            f2, st2 = measure(w2, w2.frames, args.extra_steps, warmup, 3, R, peaks, peak_src,
+                              min_timed_s=0.4)
             f2 = {"workload": name, **f2}
             if rank == 0 and not args.no_cpu:
                 try:
