@@ -173,6 +173,12 @@ int64_t pl_last_launches(const pl_handle* h);
  * uint32 per frame of each call. */
 int pl_frame_latency(pl_handle* h, uint32_t* lat_ns);
 
+/* Frames per chunk of pl_decode_host / pl_decode_host_packed (copies of one
+ * chunk overlap the decode of others); 0 = automatic (~20 chunks per call,
+ * 16 for multi-code handles, 8 for adaptive int8).  Default at pl_create:
+ * $PLB_HOST_CHUNK or 0. */
+int pl_set_host_chunk(pl_handle* h, int64_t frames);
+
 /* Live kernel timing: with profiling enabled every launch of pl_decode is
  * bracketed by CUDA events on its stream; pl_last_kernel_ms waits for them
  * and writes the duration (ms) of each launch of the last pl_decode call and

@@ -432,6 +432,7 @@ struct pl_handle {
     int64_t pstride = 0, cstride = 0;
     int esz = 4;
     uint32_t* lat_ns = nullptr; // pl_frame_latency: per-frame decode time of pl_decode(_packed)
+    int64_t host_chunk = 0;     // frames per chunk of pl_decode_host (0 = automatic)
     int sc_keep = 0; // L2 hint split of the frame-per-lane SC pass (LaunchParams::sc_keep)
     int sc_discard = 0; // LaunchParams::sc_discard
     int list_discard = 0; // LaunchParams::list_discard
@@ -1128,6 +1129,7 @@ int pl_create(const pl_code* codes, int32_t ncodes, const pl_decoder* dec, int32
             // last read (float: SC pass 21.9 -> 20.7 ms)
             h->sc_discard = env_int("PLB_SC_DISCARD", h->dec.precision == PL_F32 ? 1 : 0);
             h->list_discard = env_int("PLB_LIST_DISCARD", h->dec.precision == PL_F32 ? 1 : 0);
+            h->host_chunk = env_int("PLB_HOST_CHUNK", 0);
         if (kind == PL_KIND_FA_SSCL)
             for (int ll = 2; ll <= l; ll *= 2) h->rungs.push_back(plan_rung(*h, ll, true, true));
         else if (uses_list(kind))
@@ -1225,6 +1227,13 @@ int pl_debug_optime(unsigned long long* out, int reset) {
     return plb::read_optime(out, reset != 0) == cudaSuccess ? PL_OK : PL_ERR_CUDA;
 }
 #endif
+
+int pl_set_host_chunk(pl_handle* h, int64_t frames) {
+    if (!h) return fail(nullptr, PL_ERR_ARG, "null handle");
+    if (frames < 0) return fail(h, PL_ERR_ARG, "chunk size must be >= 0");
+    h->host_chunk = frames;
+    return PL_OK;
+}
 
 int pl_frame_latency(pl_handle* h, uint32_t* lat_ns) {
     if (!h) return fail(nullptr, PL_ERR_ARG, "null handle");
@@ -1366,8 +1375,7 @@ int decode_host_impl(pl_handle* h, const void* llr, const int64_t* offsets, cons
         // copies are short (measured FA@4.5 dB int8 e2e 33.1 -> 39.2-40.7
         // Gb/s; the PCIe-bound float / int16 ladders keep 16: 11.25 vs 11.09,
         // 21.8 vs 20.9)
-        const char* cs = std::getenv("PLB_HOST_CHUNK");
-        const int64_t chunk = cs ? std::max<int64_t>(1, std::atoll(cs))
+        const int64_t chunk = h->host_chunk > 0 ? h->host_chunk
                               : adaptive(h->dec.kind) && h->esz == 1
                                   ? std::clamp<int64_t>((nframes + 7) / 8, 8192, 131072)
                               : h->codes.size() > 1 ? std::clamp<int64_t>((nframes + 15) / 16, 8192, 65536)

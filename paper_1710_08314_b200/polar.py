@@ -587,6 +587,13 @@ class FrameDecoder:
             _raise(rc, L.last_error(self._h))
         return o
 
+    def set_host_chunk(self, frames: int = 0):
+        """pl_set_host_chunk: frames per chunk of the host-buffer decodes
+        (0 = automatic)."""
+        rc = L.lib().pl_set_host_chunk(self._h, int(frames))
+        if rc:
+            _raise(rc, L.last_error(self._h))
+
     def frame_latency(self, lat_ns=None):
         """pl_frame_latency: later decode_batch / decode_packed calls write
         each frame's device decode time in ns into ``lat_ns`` (a CUDA int32

@@ -100,3 +100,28 @@ def test_two_ranks_on_one_gpu_count_like_one_process(gpu):
     for k in ("frames_counted", "frame_errors", "bit_errors", "esc_mean"):
         assert two[k] == one[k], k
     assert "note" in two
+
+
+def test_extra_workload_defaults():
+    """The default run covers every other workload at N=1 and the FA points +
+    cfg0 at N>1; 'none' and explicit lists are honoured; the main workload
+    is never repeated."""
+    sys.path.insert(0, ROOT)
+    import argparse
+
+    import bench
+    from paper_1710_08314_b200.workload import WORKLOADS
+
+    a = argparse.Namespace(extra=None, workload="cfg1")
+    one = bench.extra_list(a, 1)
+    assert set(one) == set(WORKLOADS) - {"cfg1"}
+    assert bench.extra_list(a, 8) == ["cfg0", "cfg2_4.5", "cfg2_3.5"]
+    assert bench.extra_list(argparse.Namespace(extra="none", workload="cfg1"), 1) == []
+    assert bench.extra_list(argparse.Namespace(extra="cfg1,cfg3", workload="cfg1"), 1) == ["cfg3"]
+
+
+def test_crc_width_without_library():
+    from paper_1710_08314_b200.workload import crc_width
+
+    assert crc_width("32-GZIP") == 32 and crc_width("11:621:0:0:0") == 11
+    assert crc_width("24:b2b117:0:0:0") == 24 and crc_width("") == 0 and crc_width("8") == 8

@@ -294,11 +294,9 @@ def test_packed_frames_match_padded(P, gpu):
                               code_id=gpu.from_numpy(ci).cuda())
         gpu.cuda.synchronize()
         hout = {k: np.zeros_like(v) for k, v in ref.items()}
-        os.environ["PLB_HOST_CHUNK"] = "256"
-        try:
-            dec.decode_host_packed_into(buf, off, hout, ci)
-        finally:
-            del os.environ["PLB_HOST_CHUNK"]
+        dec.set_host_chunk(256)  # several chunks
+        dec.decode_host_packed_into(buf, off, hout, ci)
+        dec.set_host_chunk(0)
         got = {k: o[k].cpu().numpy() for k in ("payload", "crc_ok", "esc", "metric")}
         for k in ("crc_ok", "esc", "metric"):
             assert np.array_equal(got[k], ref[k]), (prec, k)
@@ -322,11 +320,8 @@ def test_decode_host_matches_device_path(P, gpu):
     dec = P.FrameDecoder(code, "fa_sscl", 16, "i8", P.PruningConfig(rep_max=8))
     o = dec.decode_batch(gpu.from_numpy(llr).cuda())
     gpu.cuda.synchronize()
-    os.environ["PLB_HOST_CHUNK"] = "700"
-    try:
-        h = dec.decode_host(llr)
-    finally:
-        del os.environ["PLB_HOST_CHUNK"]
+    dec.set_host_chunk(700)
+    h = dec.decode_host(llr)
     for k in ("payload", "crc_ok", "esc", "metric"):
         assert np.array_equal(h[k], o[k].cpu().numpy()), k
 
