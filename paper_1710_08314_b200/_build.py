@@ -16,7 +16,7 @@ LIB = os.path.join(PKG, "libpolar_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 SOURCES = ["host.cu", "kernels.cu", "channel.cu", "sim.cu"]
-HEADERS = ["polar_dev.h", "channel.h"]
+HEADERS = ["polar_dev.h", "channel.h", "primitives.cuh", "lanes.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-cudart", "static",

@@ -31,11 +31,13 @@
 // int16 normalisation all reproduce list_decoder.hpp / sc_decoder.hpp
 // exactly, for float, int8 and int16 LLRs.
 //
-// Kernel families in this file: decode_kernel<R, KV, SW> (list passes at
-// L = 2^(KV-1) and the warp-per-frame SC pass, KV = 0), its opt-in team
-// variant (a block of warps per frame), sc_lanes_kernel<R> (the default SC
-// pass: one frame per lane), the frame bucketing kernels for multi-code
-// batches, and the int8 SWAR self-test.
+// Kernel families in this translation unit: decode_kernel<R, KV, SW> (list
+// passes at L = 2^(KV-1) and the warp-per-frame SC pass, KV = 0), its
+// opt-in team variant (a block of warps per frame), sc_lanes_kernel<R> (the
+// default SC pass: one frame per lane, lanes.cuh), the frame bucketing
+// kernels for multi-code batches, and the int8 SWAR self-test.  The device
+// primitives they share (sub-warp collectives, Arith, SWAR f/g, sorting
+// networks, vector access, L2 policies) are in primitives.cuh.
 #include <algorithm>
 #include <cstdint>
 
@@ -44,370 +46,7 @@
 namespace plb {
 namespace {
 
-constexpr unsigned FULL = 0xffffffffu;
-
-__device__ __forceinline__ unsigned lanemask_lt() {
-    unsigned r;
-    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
-    return r;
-}
-
-template <typename K>
-__device__ __forceinline__ K kmin(K a, K b) { return a < b ? a : b; }
-template <typename K>
-__device__ __forceinline__ K kmax(K a, K b) { return a < b ? b : a; }
-
-__device__ __forceinline__ int pack_aux(int a, int b) {
-    return int((uint32_t(a) & 0xffffu) | (uint32_t(b) << 16));
-}
-
-// ---- sub-warp collectives ----------------------------------------------
-// All calls are made by all 32 lanes of the warp (every sub-warp executes
-// the same control flow); results are per sub-warp.
-template <int SW>
-struct Sub {
-    static constexpr unsigned kMask = SW == 32 ? FULL : ((1u << SW) - 1u);
-    int lane; // lane within the sub-warp
-    int base; // first warp lane of the sub-warp
-    int id;   // sub-warp index
-
-    __device__ __forceinline__ unsigned ballot(bool p) const {
-        if constexpr (SW == 32) return __ballot_sync(FULL, p);
-        else return (__ballot_sync(FULL, p) >> base) & kMask;
-    }
-    __device__ __forceinline__ bool any(bool p) const { return ballot(p) != 0u; }
-    __device__ __forceinline__ unsigned lt() const { return lanemask_lt() >> base; }
-    __device__ __forceinline__ uint32_t shfl(uint32_t v, int src) const { return __shfl_sync(FULL, v, src, SW); }
-    __device__ __forceinline__ int shfl(int v, int src) const { return __shfl_sync(FULL, v, src, SW); }
-    __device__ __forceinline__ float shfl(float v, int src) const { return __shfl_sync(FULL, v, src, SW); }
-    __device__ __forceinline__ uint64_t shfl(uint64_t v, int src) const {
-        const uint32_t lo = __shfl_sync(FULL, uint32_t(v), src, SW);
-        const uint32_t hi = __shfl_sync(FULL, uint32_t(v >> 32), src, SW);
-        return (uint64_t(hi) << 32) | lo;
-    }
-    // OR of slot masks (v < 2^SW): every sub-warp's mask in its own SW-bit
-    // field of one warp-wide redux
-    __device__ __forceinline__ unsigned red_or(unsigned v) const {
-        if constexpr (SW == 32) return __reduce_or_sync(FULL, v);
-        else return (__reduce_or_sync(FULL, v << base) >> base) & kMask;
-    }
-    __device__ __forceinline__ unsigned red_min(unsigned v) const {
-        if constexpr (SW == 32) {
-            return __reduce_min_sync(FULL, v);
-        } else {
-#pragma unroll
-            for (int o = SW / 2; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(FULL, v, o));
-            return v;
-        }
-    }
-    __device__ __forceinline__ unsigned red_add(unsigned v) const {
-        if constexpr (SW == 32) {
-            return __reduce_add_sync(FULL, v);
-        } else {
-#pragma unroll
-            for (int o = SW / 2; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-            return v;
-        }
-    }
-    // lanes of this sub-warp holding the same v (v < 2^24)
-    __device__ __forceinline__ unsigned match(int v) const {
-        if constexpr (SW == 32) return __match_any_sync(FULL, v);
-        else return (__match_any_sync(FULL, (v << 2) | id) >> base) & kMask;
-    }
-};
-
-__device__ __forceinline__ uint32_t shfl_xor_k(uint32_t v, int m) { return __shfl_xor_sync(FULL, v, m); }
-__device__ __forceinline__ uint64_t shfl_xor_k(uint64_t v, int m) {
-    const uint32_t lo = __shfl_xor_sync(FULL, uint32_t(v), m);
-    const uint32_t hi = __shfl_xor_sync(FULL, uint32_t(v >> 32), m);
-    return (uint64_t(hi) << 32) | lo;
-}
-
-// ---- per-representation arithmetic (llr.hpp:36-69) -------------------
-// Key: a totally ordered (value, index) pair in one integer, used for the
-// stable candidate ranking and for the two-smallest selection.
-template <typename R>
-struct Arith;
-
-template <>
-struct Arith<float> {
-    using M = float;      // path-metric type
-    using Key = uint64_t; // float bits << 32 | index  (value >= +0)
-    static constexpr bool kFixed = false;
-    static constexpr int kMax = 0; // (fixed point only: no saturation)
-    static constexpr Key kKeyMax = ~0ull;
-    __device__ static M sat(M a, M b) { return a + b; }
-    // |v| as a non-negative float: abs_llr(-0.0f) is -0.0f in the reference,
-    // but every use of a magnitude is an add to a non-negative metric or a
-    // (value, index) comparison, where +-0 behave identically.
-    __device__ static M mag(float v) { return fabsf(v); }
-    __device__ static Key make_key(M v, int idx) { return (uint64_t(__float_as_uint(v)) << 32) | uint32_t(idx); }
-    __device__ static int key_idx(Key k) { return int(uint32_t(k)); }
-    __device__ static M key_val(Key k) { return __uint_as_float(uint32_t(k >> 32)); }
-    __device__ static M val(float v) { return v; }
-    __device__ static float f(float a, float b) {
-        // min-sum (llr.hpp:55-59).  The sign comes from the sign bits, which
-        // differs from `(a<0) != (b<0)` only when an operand is -0.0, and
-        // then the magnitude is 0: the result is a zero either way.
-        const float m = fminf(fabsf(a), fabsf(b));
-        return __uint_as_float(__float_as_uint(m) |
-                               ((__float_as_uint(a) ^ __float_as_uint(b)) & 0x80000000u));
-    }
-    __device__ static float g(float a, float b, uint32_t s) { return s ? b - a : a + b; }
-    __device__ static float store(M v) { return v; }
-    __device__ static float to_float(M v) { return v; }
-};
-
-template <>
-struct Arith<int8_t> {
-    using M = int;
-    using Key = uint32_t; // value (0..127) << 16 | index
-    static constexpr bool kFixed = true;
-    static constexpr int kMax = 127; // symmetric range (llr.hpp:29-33)
-    static constexpr Key kKeyMax = ~0u;
-    __device__ static M sat(M a, M b) { return max(-127, min(127, a + b)); }
-    __device__ static M mag(int v) { return abs(v); }
-    __device__ static Key make_key(M v, int idx) { return (uint32_t(v) << 16) | uint32_t(idx); }
-    __device__ static int key_idx(Key k) { return int(k & 0xffffu); }
-    __device__ static M key_val(Key k) { return int(k >> 16); }
-    __device__ static M val(int8_t v) { return int(v); }
-    __device__ static int8_t f(int8_t a, int8_t b) {
-        const int m = min(abs(int(a)), abs(int(b)));
-        return int8_t(((a ^ b) < 0) ? -m : m);
-    }
-    __device__ static int8_t g(int8_t a, int8_t b, uint32_t s) {
-        const int v = s ? int(b) - int(a) : int(a) + int(b);
-        return int8_t(max(-127, min(127, v)));
-    }
-    __device__ static int8_t store(M v) { return int8_t(v); }
-    __device__ static float to_float(M v) { return float(v); }
-};
-
-// int16 (llr.hpp:22-26): the int8 rules on [-32767, 32767], scalar f / g
-template <>
-struct Arith<int16_t> {
-    using M = int;
-    using Key = uint32_t; // value (0..32767) << 16 | index
-    static constexpr bool kFixed = true;
-    static constexpr int kMax = 32767;
-    static constexpr Key kKeyMax = ~0u;
-    __device__ static M sat(M a, M b) { return max(-kMax, min(kMax, a + b)); }
-    __device__ static M mag(int v) { return abs(v); }
-    __device__ static Key make_key(M v, int idx) { return (uint32_t(v) << 16) | uint32_t(idx); }
-    __device__ static int key_idx(Key k) { return int(k & 0xffffu); }
-    __device__ static M key_val(Key k) { return int(k >> 16); }
-    __device__ static M val(int16_t v) { return int(v); }
-    __device__ static int16_t f(int16_t a, int16_t b) {
-        const int m = min(abs(int(a)), abs(int(b)));
-        return int16_t(((a ^ b) < 0) ? -m : m);
-    }
-    __device__ static int16_t g(int16_t a, int16_t b, uint32_t s) {
-        const int v = s ? int(b) - int(a) : int(a) + int(b);
-        return int16_t(max(-kMax, min(kMax, v)));
-    }
-    __device__ static int16_t store(M v) { return int16_t(v); }
-    __device__ static float to_float(M v) { return float(v); }
-};
-
-// ---- int8 f / g on four packed values (SWAR) ---------------------------
-// Bit-exact with Arith<int8_t>::f / ::g for operands in [-127, 127]; checked
-// exhaustively by pl_kernel_selftest.
-// f: |x| = absdiff_u8(x ^ 0x80, 0x80); min(p, q) = (p + q - |p - q|) / 2
-// (bytes <= 127: no carries); the result is negated (two's complement, no
-// carry for m >= 1) where the operand signs differ and m != 0.
-// PRMT with the selector's sign-replicate bit (__byte_perm masks it away)
-__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
-    uint32_t d;
-    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
-    return d;
-}
-__device__ __forceinline__ uint32_t f_swar(uint32_t a, uint32_t b) {
-    const uint32_t aa = __vabsdiffu4(a ^ 0x80808080u, 0x80808080u);
-    const uint32_t ab = __vabsdiffu4(b ^ 0x80808080u, 0x80808080u);
-    const uint32_t m = (((aa + ab) - __vabsdiffu4(aa, ab)) >> 1) & 0x7f7f7f7fu;
-    const uint32_t sp = (a ^ b) & (m + 0x7f7f7f7fu) & 0x80808080u;
-    return (m ^ prmt(sp, 0, 0xba98)) + (sp >> 7);
-}
-// g in two 16x2 halves: sign-extend, b + (s ? -a : a), clamp to [-127, 127]
-// (the reference clamps to the symmetric range, llr.hpp:61-69), repack.
-// s4 = the four partial-sum bits, element i in bit i.
-__device__ __forceinline__ uint32_t g_swar(uint32_t a, uint32_t b, uint32_t s4) {
-    const uint32_t al = prmt(a, 0, 0x9180), ah = prmt(a, 0, 0xb3a2);
-    const uint32_t bl = prmt(b, 0, 0x9180), bh = prmt(b, 0, 0xb3a2);
-    const uint32_t t = ((s4 * 0x00204081u) & 0x01010101u) << 7; // bit 7 of byte i = s_i
-    const uint32_t ml = prmt(t, 0, 0x9988), mh = prmt(t, 0, 0xbbaa);
-    uint32_t vl = __vadd2(__vadd2(al ^ ml, bl), ml & 0x00010001u);
-    uint32_t vh = __vadd2(__vadd2(ah ^ mh, bh), mh & 0x00010001u);
-    vl = __vmins2(__vmaxs2(vl, 0xff81ff81u), 0x007f007fu);
-    vh = __vmins2(__vmaxs2(vh, 0xff81ff81u), 0x007f007fu);
-    return __byte_perm(vl, vh, 0x6420);
-}
-
-template <typename M>
-__device__ __forceinline__ uint32_t mbits(M v);
-template <>
-__device__ __forceinline__ uint32_t mbits<float>(float v) { return __float_as_uint(v); }
-template <>
-__device__ __forceinline__ uint32_t mbits<int>(int v) { return uint32_t(v); }
-template <typename M>
-__device__ __forceinline__ M mfrom(uint32_t b);
-template <>
-__device__ __forceinline__ float mfrom<float>(uint32_t b) { return __uint_as_float(b); }
-template <>
-__device__ __forceinline__ int mfrom<int>(uint32_t b) { return int(b); }
-
-// ---- sub-warp sorting networks (ascending) -------------------------------
-// Every network here uses ascending comparators only: a bitonic merge whose
-// first stage compares mirrored lanes (lane ^ (size-1)) merges two ASCENDING
-// runs, so runs that are already sorted need no direction flips and their
-// phases are skipped.  The candidates of one path are emitted in ascending
-// (metric, index) order for R1, SPC and REP nodes (their penalties are
-// 0 <= a1 <= a2 <= a1+a2 resp. pen_w <= pen_w+|s|, list_decoder.hpp:254-333),
-// which makes each path's 2 or 4 consecutive lanes a sorted run.
-// compare-exchange with lane ^ m: lanes with `bit` clear keep the smaller key
-template <typename K>
-__device__ __forceinline__ K cex(K key, int m, int lane, int bit) {
-    const K o = shfl_xor_k(key, m);
-    return (lane & bit) == 0 ? kmin(key, o) : kmax(key, o);
-}
-
-// W keys, one per lane, made of sorted runs of 2^lgrun lanes (lgrun uniform;
-// 0 = unsorted): lanes [0, W) of each aligned W-lane group sorted ascending.
-template <typename K, int W>
-__device__ __forceinline__ K sort_runs(K key, int lane, int lgrun) {
-#pragma unroll
-    for (int size = 2; size <= W; size <<= 1) {
-        if (size <= (1 << lgrun)) continue;
-        key = cex(key, size - 1, lane, size >> 1);
-#pragma unroll
-        for (int j = size >> 2; j > 0; j >>= 1) key = cex(key, j, lane, j);
-    }
-    return key;
-}
-
-// The W/2 smallest of 2W keys (two registers, sorted runs of 2^lgrun),
-// ascending in lanes [0, W/2): sort W/2-lane runs in both registers, keep the
-// W/2 smallest of each pair of runs (min against the other register's run
-// reversed: a bitonic sequence), sort those, then the same step across the
-// two halves.  14 compare stages at W = 16 from runs of 4, vs 25 for two full
-// sorts and a merge.
-template <typename K, int W>
-__device__ __forceinline__ K top_half2(K a, K b, int lane, int lgrun) {
-    // both registers through the same stages (one uniform branch per phase,
-    // two independent chains)
-#pragma unroll
-    for (int size = 2; size <= W / 2; size <<= 1) {
-        if (size <= (1 << lgrun)) continue;
-        a = cex(a, size - 1, lane, size >> 1);
-        b = cex(b, size - 1, lane, size >> 1);
-#pragma unroll
-        for (int j = size >> 2; j > 0; j >>= 1) {
-            a = cex(a, j, lane, j);
-            b = cex(b, j, lane, j);
-        }
-    }
-    K c = kmin(a, shfl_xor_k(b, W / 2 - 1));
-#pragma unroll
-    for (int j = W / 4; j > 0; j >>= 1) c = cex(c, j, lane, j);
-    c = cex(c, W - 1, lane, W / 2);
-#pragma unroll
-    for (int j = W / 4; j > 0; j >>= 1) c = cex(c, j, lane, j);
-    return c;
-}
-
-// The W smallest of two ascending W-key lane sequences, ascending: the
-// element-wise min of a and reversed b is a bitonic sequence holding exactly
-// those keys; half-cleaners sort it.
-template <typename K, int W>
-__device__ __forceinline__ K merge_top(K a, K b, int lane) {
-    K c = kmin(a, shfl_xor_k(b, W - 1));
-#pragma unroll
-    for (int j = W / 2; j > 0; j >>= 1) c = cex(c, j, lane, j);
-    return c;
-}
-
-// The W smallest of W*C keys (register k of each lane), ascending in
-// register 0: sort each register across the lanes, then merge pairwise.
-// Registers from nreg on hold only kKeyMax and are skipped (uniform).
-template <typename K, int C, int W>
-__device__ __forceinline__ void top_regs(K (&key)[C], int lane, int nreg, int lgrun) {
-#pragma unroll
-    for (int k = 0; k < C; ++k)
-        if (k < nreg) key[k] = sort_runs<K, W>(key[k], lane, lgrun);
-#pragma unroll
-    for (int w = 1; w < C; w <<= 1)
-#pragma unroll
-        for (int k = 0; k + w < C; k += 2 * w)
-            if (k + w < nreg) key[k] = merge_top<K, W>(key[k], key[k + w], lane);
-}
-
-// ---- vector access of G consecutive values ----------------------------
-template <int B>
-struct VT;
-template <> struct VT<1> { using T = uint8_t; };
-template <> struct VT<2> { using T = uint16_t; };
-template <> struct VT<4> { using T = uint32_t; };
-template <> struct VT<8> { using T = uint2; };
-template <> struct VT<16> { using T = uint4; };
-
-template <typename R, int G>
-union Vec {
-    typename VT<G * sizeof(R)>::T raw;
-    R v[G];
-};
-
-template <typename R, int G>
-__device__ __forceinline__ Vec<R, G> vld(const R* p) {
-    Vec<R, G> x;
-    x.raw = *reinterpret_cast<const typename VT<G * sizeof(R)>::T*>(p);
-    return x;
-}
-template <typename R, int G>
-__device__ __forceinline__ void vst(R* p, const Vec<R, G>& x) {
-    *reinterpret_cast<typename VT<G * sizeof(R)>::T*>(p) = x.raw;
-}
-
-// L2 eviction-priority hints of the frame-per-lane SC pass (global memory only)
-__device__ __forceinline__ uint64_t l2_policy(bool keep) {
-    uint64_t p;
-    if (keep) asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-    else asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-template <typename R, int G>
-__device__ __forceinline__ Vec<R, G> vld_hint(const R* ptr, uint64_t pol) {
-    static_assert(G * sizeof(R) == 16, "16-byte vectors");
-    Vec<R, G> x;
-    uint4 v;
-    asm volatile("ld.global.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(ptr), "l"(pol));
-    x.raw = *reinterpret_cast<const typename VT<16>::T*>(&v);
-    return x;
-}
-template <typename R, int G>
-__device__ __forceinline__ void vst_hint(R* ptr, const Vec<R, G>& x, uint64_t pol) {
-    static_assert(G * sizeof(R) == 16, "16-byte vectors");
-    const uint4 v = *reinterpret_cast<const uint4*>(&x.raw);
-    asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;"
-                 :: "l"(ptr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol) : "memory");
-}
-
-#ifdef PLB_OPTIME
-__device__ unsigned long long g_optime[64]; // profiling build: cycles / count per op kind
-#endif
-
-// per-frame decode time (LaunchParams::lat_ns): the device's global timer
-__device__ __forceinline__ uint64_t gtimer() {
-    uint64_t t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-
-// first channel LLR of a frame: fixed stride, or the packed layout's offset
-template <typename R>
-__device__ __forceinline__ const R* frame_llr(const LaunchParams& P, int frame) {
-    return static_cast<const R*>(P.llr) + (P.llr_offset ? P.llr_offset[frame] : int64_t(frame) * P.llr_stride);
-}
+#include "primitives.cuh"
 
 // ---- per-frame shared-memory area ----------------------------------------
 // (followed by the bufidx rows, [slot][depth] -> buffer index in the depth
@@ -2065,532 +1704,7 @@ __global__ void code_scatter_kernel(const int32_t* cid, int64_t n, int32_t* curs
         out[atomicAdd(cursor + cid[i], 1)] = int32_t(i);
 }
 
-// ==== frame-per-lane SC kernel (SC / SSC and the first pass of PA / FA) ====
-// A warp decodes 32 frames, one per lane, in lockstep over the SC schedule
-// of their (common) code: the op sequence of SC decoding is data-independent
-// except for the rate-1 shortcut, which the warp takes only when no lane has
-// a zero input (the expanded recursion is exact for every lane, so running
-// it for all is correct).  One warp instruction then advances 32 frames, and
-// the small nodes that cost the warp-per-frame kernel a whole warp step per
-// value are plain per-lane loops.  Per-warp storage, lane-interleaved so
-// every access is conflict-free / coalesced:
-//   * partial sums: word w of lane l at ps[w * 32 + l] (shared memory);
-//   * depth-d LLR segment (n >> d values per frame): chunks of
-//     V = min(VE, n >> d) values, chunk c of lane l at ((c * 32) + l) * V
-//     (VE = 16 bytes of values); small segments in shared memory, large ones
-//     in the warp's global scratch;
-//   * depth 0 is the channel, read in place (frame-major).
-struct LaneQ {
-    int32_t rw, psum_off, smem_total, gmem_total, pool_off, pool_in_smem;
-};
-__host__ __device__ inline LaneQ lane_layout(int n, int esz, int segmax, int want_d) {
-    LaneQ q{};
-    int off = 16 * 8; // pool pointer table
-    q.rw = n >= 32 ? n / 32 : 1;
-    q.psum_off = off;
-    off += 4 * q.rw * 32;
-    int goff = 0;
-    const int stages = ilog2(n);
-    #pragma unroll 1
-    for (int d = 1; d <= stages; ++d) {
-        const int bytes = align16((n >> d) * 32 * esz);
-        if ((n >> d) <= segmax) {
-            if (d == want_d) {
-                q.pool_off = off;
-                q.pool_in_smem = 1;
-            }
-            off += bytes;
-        } else {
-            if (d == want_d) {
-                q.pool_off = goff;
-                q.pool_in_smem = 0;
-            }
-            goff += bytes;
-        }
-    }
-    q.smem_total = off;
-    q.gmem_total = goff;
-    return q;
-}
-
-template <typename R>
-struct LaneCtx {
-    static constexpr int VE = 16 / int(sizeof(R));
-    int lane, n;
-    int segmax, keep; // depth segments > segmax values live in global scratch
-    bool discard;     // drop dead global segments from the L2 (LaunchParams::sc_discard)
-    const R* chan;      // this lane's frame
-    uint32_t* ps;       // this lane's psum words, stride 32
-    const uint64_t* pt; // pool pointer table
-    __device__ __forceinline__ R* pool(int d) const { return reinterpret_cast<R*>(pt[d]); }
-    // first value of chunk c at depth d (chunk = min(VE, n >> d) values)
-    __device__ __forceinline__ const R* chunk(int d, int c) const {
-        const int v = min(VE, n >> d);
-        return d == 0 ? chan + c * v : pool(d) + (c * 32 + lane) * v;
-    }
-    // chunk k of depth d is at base + k * stride (loop-invariant form of chunk())
-    __device__ __forceinline__ const R* chunk_base(int d, int& stride) const {
-        const int v = min(VE, n >> d);
-        stride = d == 0 ? v : 32 * v;
-        return d == 0 ? chan : pool(d) + lane * v;
-    }
-    __device__ __forceinline__ uint32_t& word(int w) const { return ps[w * 32]; }
-    __device__ void fill(int lb, int m, int bit) const {
-        if (m >= 32) {
-            #pragma unroll 1
-            for (int w = 0; w < (m >> 5); ++w) word((lb >> 5) + w) = bit ? FULL : 0u;
-        } else {
-            const uint32_t mk = ((1u << m) - 1u) << (lb & 31);
-            uint32_t& x = word(lb >> 5);
-            x = bit ? (x | mk) : (x & ~mk);
-        }
-    }
-};
-
-// sign bits of the G values of a vector (value i -> bit i)
-template <typename R, int G>
-__device__ __forceinline__ uint32_t vec_signs(const Vec<R, G>& x) {
-    uint32_t s = 0;
-    if constexpr (sizeof(R) == 1 && G >= 4) {
-        const uint32_t* w = reinterpret_cast<const uint32_t*>(&x.raw);
-#pragma unroll
-        for (int k = 0; k < G / 4; ++k)
-            s |= ((((w[k] >> 7) & 0x01010101u) * 0x01020408u) >> 24) << (4 * k);
-    } else {
-#pragma unroll
-        for (int i = 0; i < G; ++i) s |= uint32_t(Arith<R>::val(x.v[i]) < typename Arith<R>::M(0)) << i;
-    }
-    return s;
-}
-template <typename R, int G>
-__device__ __forceinline__ bool vec_has_zero(const Vec<R, G>& x) {
-    if constexpr (sizeof(R) == 1 && G >= 4) {
-        // a zero byte: (w - 0x01..) & ~w & 0x80.. is non-zero exactly then
-        const uint32_t* w = reinterpret_cast<const uint32_t*>(&x.raw);
-        uint32_t z = 0;
-#pragma unroll
-        for (int k = 0; k < G / 4; ++k) z |= (w[k] - 0x01010101u) & ~w[k] & 0x80808080u;
-        return z != 0u;
-    } else {
-        bool z = false;
-#pragma unroll
-        for (int i = 0; i < G; ++i) z |= Arith<R>::val(x.v[i]) == typename Arith<R>::M(0);
-        return z;
-    }
-}
-
-// U chunks per iteration: 2U loads in flight per lane (the pools of the
-// upper depths live in global memory), U * VE <= 32 partial-sum bits.
-// HIN / HOUT: the input / output depth is in global memory and takes an L2
-// eviction hint (pin / pout).
-// disc: the input segment is a global depth pool read for the last time (a G
-// op): its L2 lines are dropped without write-back once consumed
-// (discard.global.L2), so dead LLRs of 32-frame warps never reach DRAM.
-template <typename R, int U, bool HIN, bool HOUT>
-__device__ __forceinline__ void lane_fg_chunks(const LaneCtx<R>& c, int d, int nc, int lb, bool is_g,
-                                               R* out, uint64_t pin, uint64_t pout, bool disc) {
-    constexpr int VE = LaneCtx<R>::VE;
-    int cs;
-    const R* in = c.chunk_base(d, cs);
-    const R* in_b = in + nc * cs;
-    R* o = out + c.lane * VE;
-    #pragma unroll 1
-    for (int k = 0; k < nc; k += U) {
-        Vec<R, VE> a[U], b[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            if constexpr (HIN) {
-                a[u] = vld_hint<R, VE>(in + (k + u) * cs, pin);
-                b[u] = vld_hint<R, VE>(in_b + (k + u) * cs, pin);
-            } else {
-                a[u] = vld<R, VE>(in + (k + u) * cs);
-                b[u] = vld<R, VE>(in_b + (k + u) * cs);
-            }
-        }
-        const int pos = lb + k * VE;
-        const uint32_t bits = is_g ? c.word(pos >> 5) >> (pos & 31) : 0u;
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const Vec<R, VE> r = fg_compute<R, VE>(a[u], b[u], bits >> (u * VE), is_g);
-            if constexpr (HOUT) vst_hint<R, VE>(o + (k + u) * 32 * VE, r, pout);
-            else vst<R, VE>(o + (k + u) * 32 * VE, r);
-        }
-        // (the values were consumed above by every lane of the warp; chunk
-        // rows are 512-byte aligned, lanes 0 / 8 / 16 / 24 start its lines)
-        if (disc && (c.lane & 7) == 0) {
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                asm volatile("discard.global.L2 [%0], 128;" :: "l"(in + (k + u) * cs) : "memory");
-                asm volatile("discard.global.L2 [%0], 128;" :: "l"(in_b + (k + u) * cs) : "memory");
-            }
-        }
-    }
-}
-template <typename R, int U>
-__device__ __forceinline__ void lane_fg_chunks_any(const LaneCtx<R>& c, int d, int nc, int lb, bool is_g,
-                                                   R* out) {
-    if constexpr (sizeof(R) != 4) {
-        // fixed point: no hint / discard code at all (the int16 pass lost 10%
-        // to the larger loop even with the hints switched off)
-        lane_fg_chunks<R, U, false, false>(c, d, nc, lb, is_g, out, 0, 0, false);
-        return;
-    }
-    // hints only on global depths (the channel is depth 0); uniform per op
-    const bool gin = c.keep > 0 && (d == 0 || (c.n >> d) > c.segmax);
-    const bool gout = c.keep > 0 && (c.n >> (d + 1)) > c.segmax;
-    const bool disc = c.discard && is_g && d > 0 && (c.n >> d) > c.segmax;
-    if (gin) {
-        const uint64_t pin = l2_policy(d > 0 && (c.n >> d) <= c.keep);
-        if (gout)
-            lane_fg_chunks<R, U, true, true>(c, d, nc, lb, is_g, out, pin,
-                                             l2_policy((c.n >> (d + 1)) <= c.keep), disc);
-        else lane_fg_chunks<R, U, true, false>(c, d, nc, lb, is_g, out, pin, 0, disc);
-    } else {
-        lane_fg_chunks<R, U, false, false>(c, d, nc, lb, is_g, out, 0, 0, disc);
-    }
-}
-
-template <typename R>
-__device__ void lane_fg(const LaneCtx<R>& c, int d, int m, int lb, bool is_g) {
-    using A = Arith<R>;
-    constexpr int VE = LaneCtx<R>::VE;
-    constexpr int U = 32 / VE < 4 ? 32 / VE : 4;
-    const int h = m >> 1;
-    R* const out = c.pool(d + 1);
-    if (h >= VE) {
-        const int nc = h / VE;
-        if (nc >= U) lane_fg_chunks_any<R, U>(c, d, nc, lb, is_g, out);
-        else lane_fg_chunks_any<R, 1>(c, d, nc, lb, is_g, out);
-    } else {
-        // the parent's m <= VE values are one contiguous chunk
-        const R* p = c.chunk(d, 0);
-        R* q = out + c.lane * h;
-        const uint32_t bits = is_g ? c.word(lb >> 5) >> (lb & 31) : 0u;
-        if constexpr (sizeof(R) == 1) {
-            // int8 nodes of 16 / 8 / 4 values: SWAR words (the chunk is m-byte aligned)
-            if (h == 2) {
-                const uint32_t x = *reinterpret_cast<const uint32_t*>(p);
-                const uint32_t o = is_g ? g_swar(x & 0xffffu, x >> 16, bits & 3u) : f_swar(x & 0xffffu, x >> 16);
-                *reinterpret_cast<uint16_t*>(q) = uint16_t(o);
-                return;
-            }
-            if (h == 8) {
-                const uint4 x = *reinterpret_cast<const uint4*>(p);
-                uint2 o;
-                o.x = is_g ? g_swar(x.x, x.z, bits & 15u) : f_swar(x.x, x.z);
-                o.y = is_g ? g_swar(x.y, x.w, (bits >> 4) & 15u) : f_swar(x.y, x.w);
-                *reinterpret_cast<uint2*>(q) = o;
-                return;
-            }
-            if (h == 4) {
-                const uint2 x = *reinterpret_cast<const uint2*>(p);
-                *reinterpret_cast<uint32_t*>(q) = is_g ? g_swar(x.x, x.y, bits & 15u) : f_swar(x.x, x.y);
-                return;
-            }
-        }
-        #pragma unroll 1
-        for (int j = 0; j < h; ++j) q[j] = is_g ? A::g(p[j], p[h + j], (bits >> j) & 1u) : A::f(p[j], p[h + j]);
-    }
-}
-
-template <typename R>
-__device__ void lane_h(const LaneCtx<R>& c, int m, int lb) {
-    const int h = m >> 1;
-    if (h >= 32) {
-        #pragma unroll 1
-        for (int w = 0; w < (h >> 5); ++w) c.word((lb >> 5) + w) ^= c.word(((lb + h) >> 5) + w);
-    } else {
-        uint32_t& x = c.word(lb >> 5);
-        const int s = lb & 31;
-        const uint32_t mk = (1u << h) - 1u;
-        x ^= ((x >> (s + h)) & mk) << s;
-    }
-}
-
-// repetition node (sc_decoder.hpp:114-125): halving fold, bit = fold < 0.
-// Chunk pairs are added elementwise first (into the dead depth-(d+1)
-// segment), then the last chunk is folded in registers: the same additions
-// in the same order as the reference's halving loop.
-template <typename R>
-__device__ int lane_rep(const LaneCtx<R>& c, int d, int m) {
-    using A = Arith<R>;
-    using M = typename A::M;
-    constexpr int VE = LaneCtx<R>::VE;
-    Vec<R, VE> x;
-    int len = m;
-    if (m > VE) {
-        R* S = c.pool(d + 1) + c.lane * VE; // chunk k at S + k * 32 * VE
-        int nc = m / VE;
-        int cs;
-        const R* in = c.chunk_base(d, cs);
-        #pragma unroll 1
-        for (int first = 1; nc > 1; first = 0) {
-            const int hc = nc >> 1;
-            #pragma unroll 1
-            for (int k = 0; k < hc; ++k) {
-                const Vec<R, VE> a = first ? vld<R, VE>(in + k * cs) : vld<R, VE>(S + k * 32 * VE);
-                const Vec<R, VE> b = first ? vld<R, VE>(in + (k + hc) * cs) : vld<R, VE>(S + (k + hc) * 32 * VE);
-                vst<R, VE>(S + k * 32 * VE, fg_compute<R, VE>(a, b, 0u, true)); // g with u = 0: sat(a + b)
-            }
-            nc = hc;
-        }
-        x = vld<R, VE>(S);
-        len = VE;
-    } else {
-        const R* p = c.chunk(d, 0);
-#pragma unroll
-        for (int i = 0; i < VE; ++i) x.v[i] = i < m ? p[i] : R(0);
-    }
-    M v[VE];
-#pragma unroll
-    for (int i = 0; i < VE; ++i) v[i] = A::val(x.v[i]);
-#pragma unroll
-    for (int s = VE; s > 1; s >>= 1)
-        if (s <= len)
-#pragma unroll
-            for (int i = 0; i < s / 2; ++i) v[i] = A::sat(v[i], v[i + s / 2]);
-    return v[0] < M(0);
-}
-
-// rate-1 shortcut: true when this lane's m values hold no zero
-template <typename R>
-__device__ bool lane_r1_nozero(const LaneCtx<R>& c, int d, int m) {
-    constexpr int VE = LaneCtx<R>::VE;
-    bool zero = false;
-    if (sizeof(R) == 4 && m >= 8 * VE) {
-        // float: 8 chunks (32 values) in flight per trip (the large rate-1
-        // nodes read global depth pools)
-        int cs;
-        const R* in = c.chunk_base(d, cs);
-        #pragma unroll 1
-        for (int k = 0; k < m / VE; k += 8) {
-            Vec<R, VE> q[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) q[u] = vld<R, VE>(in + (k + u) * cs);
-#pragma unroll
-            for (int u = 0; u < 8; ++u) zero |= vec_has_zero<R, VE>(q[u]);
-        }
-    } else if (m >= VE) {
-        int cs;
-        const R* in = c.chunk_base(d, cs);
-        #pragma unroll 1
-        for (int k = 0; k < m / VE; ++k) zero |= vec_has_zero<R, VE>(vld<R, VE>(in + k * cs));
-    } else if (sizeof(R) == 1 && m >= 4) { // int8 nodes of 4 / 8 values: whole words
-        const uint32_t* p = reinterpret_cast<const uint32_t*>(c.chunk(d, 0));
-        #pragma unroll 1
-        for (int k = 0; k < (m >> 2); ++k) zero |= ((p[k] - 0x01010101u) & ~p[k] & 0x80808080u) != 0u;
-    } else {
-        const R* p = c.chunk(d, 0);
-        #pragma unroll 1
-        for (int i = 0; i < m; ++i) zero |= Arith<R>::val(p[i]) == typename Arith<R>::M(0);
-    }
-    return !zero;
-}
-template <typename R>
-__device__ void lane_r1_hard(const LaneCtx<R>& c, int d, int m, int lb) {
-    using A = Arith<R>;
-    constexpr int VE = LaneCtx<R>::VE;
-    if (sizeof(R) == 4 && m >= 32) {
-        // float: a 32-bit partial-sum word (8 chunks) per trip, its loads in flight together
-        int cs;
-        const R* in = c.chunk_base(d, cs);
-        #pragma unroll 1
-        for (int k = 0; k < m / VE; k += 8) {
-            Vec<R, VE> q[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) q[u] = vld<R, VE>(in + (k + u) * cs);
-            uint32_t acc = 0;
-#pragma unroll
-            for (int u = 0; u < 8; ++u) acc |= vec_signs<R, VE>(q[u]) << (u * VE);
-            c.word((lb + k * VE) >> 5) = acc;
-        }
-    } else if (m >= VE) {
-        uint32_t acc = 0;
-        int cs;
-        const R* in = c.chunk_base(d, cs);
-        #pragma unroll 1
-        for (int k = 0; k < m / VE; ++k) {
-            const int pos = k * VE; // bit of the node
-            acc |= vec_signs<R, VE>(vld<R, VE>(in + k * cs)) << (pos & 31);
-            if (((pos + VE) & 31) == 0 || pos + VE >= m) {
-                if (m >= 32) {
-                    c.word((lb + (pos & ~31)) >> 5) = acc;
-                } else {
-                    const uint32_t mk = ((1u << m) - 1u) << (lb & 31);
-                    uint32_t& x = c.word(lb >> 5);
-                    x = (x & ~mk) | ((acc << (lb & 31)) & mk);
-                }
-                acc = 0;
-            }
-        }
-    } else {
-        const R* p = c.chunk(d, 0);
-        uint32_t acc = 0;
-        if (sizeof(R) == 1 && m >= 4) { // sign bits of whole words
-            #pragma unroll 1
-            for (int k = 0; k < (m >> 2); ++k) {
-                const uint32_t w = reinterpret_cast<const uint32_t*>(p)[k];
-                acc |= ((((w >> 7) & 0x01010101u) * 0x01020408u) >> 24) << (4 * k);
-            }
-        } else {
-            #pragma unroll 1
-            for (int i = 0; i < m; ++i) acc |= uint32_t(A::val(p[i]) < typename A::M(0)) << i;
-        }
-        const uint32_t mk = ((1u << m) - 1u) << (lb & 31);
-        uint32_t& x = c.word(lb >> 5);
-        x = (x & ~mk) | ((acc << (lb & 31)) & mk);
-    }
-}
-
-template <typename R>
-__device__ void lane_frame(const LaunchParams& P, const DevCode& C, unsigned char* sm,
-                           unsigned char* gs, int frame, bool active, int lane) {
-    using A = Arith<R>;
-    using M = typename A::M;
-    if (P.lat_ns && active) P.lat_ns[frame] -= uint32_t(gtimer());
-    LaneCtx<R> c;
-    c.lane = lane;
-    c.n = C.n;
-    c.segmax = P.seg_smem_max;
-    c.keep = P.sc_keep;
-    c.discard = P.sc_discard != 0;
-    c.chan = frame_llr<R>(P, frame);
-    const LaneQ q0 = lane_layout(C.n, int(sizeof(R)), P.seg_smem_max, 0);
-    c.ps = reinterpret_cast<uint32_t*>(sm + q0.psum_off) + lane;
-    uint64_t* pt = reinterpret_cast<uint64_t*>(sm);
-    c.pt = pt;
-    __syncwarp();
-    if (lane >= 1 && lane <= C.stages) {
-        const LaneQ q = lane_layout(C.n, int(sizeof(R)), P.seg_smem_max, lane);
-        pt[lane] = reinterpret_cast<uint64_t>((q.pool_in_smem ? sm : gs) + q.pool_off);
-    }
-    __syncwarp();
-    const uint32_t* sched = C.sched_lane;
-    const int nops = C.nops_lane;
-    // the next schedule word is fetched one op ahead (the schedules carry a
-    // padding word)
-    uint32_t next = __ldg(sched);
-    #pragma unroll 1
-    for (int oi = 0; oi < nops; ++oi) {
-        const uint32_t op = next;
-        next = __ldg(sched + oi + 1);
-        const int code = op_code(op), d = op_depth(op), m = 1 << op_logm(op), lb = op_lb(op);
-        switch (code) {
-        case OP_F:
-        case OP_G: lane_fg(c, d, m, lb, code == OP_G); break;
-        case OP_H: lane_h(c, m, lb); break;
-        case OP_FROZEN: c.fill(lb, m, 0); break;
-        case OP_INFO: c.fill(lb, 1, A::val(*c.chunk(d, 0)) < M(0)); break;
-        case OP_REP: c.fill(lb, m, lane_rep(c, d, m)); break;
-        case OP_R1SC: {
-            const int skip = int(next); // the word after OP_R1SC
-            ++oi;
-            if (__all_sync(FULL, lane_r1_nozero(c, d, m))) {
-                lane_r1_hard(c, d, m, lb);
-                oi += skip;
-            } // else: every lane runs the expanded recursion that follows
-            next = __ldg(sched + oi + 1);
-            break;
-        }
-        default: break;
-        }
-    }
-    // finish: CRC syndrome, payload, codeword, status (per lane)
-    int crc_ok = 0;
-    if (C.crc_width > 0) {
-        uint64_t syn = C.crc_c0;
-        const int nbytes = (C.n + 7) >> 3;
-        #pragma unroll 1
-        for (int j = 0; j < nbytes; ++j) {
-            const uint32_t byte = (c.word(j >> 2) >> ((j & 3) * 8)) & 0xffu;
-            syn ^= __ldg(C.crc_tab + (size_t(j) << 8) + byte);
-        }
-        crc_ok = syn == 0;
-    }
-    if (active) {
-        // payload (extract_payload, prune_tree.hpp:78-105): the open bits of
-        // each codeword byte compacted by table (all-open bytes: a bit
-        // reversal) and streamed out MSB-first
-        uint8_t* pay = P.payload + int64_t(frame) * P.payload_stride;
-        const int cbytes = (C.n + 7) >> 3;
-        uint32_t acc = 0;
-        int nb = 0, qb = 0;
-        #pragma unroll 1
-        for (int j = 0; j < cbytes; ++j) {
-            const uint32_t m = __ldg(C.open_mask + j);
-            if (m == 0u) continue; // uniform: one code per warp
-            const uint32_t v = (c.word(j >> 2) >> ((j & 3) * 8)) & 0xffu;
-            const uint32_t bits = m == 0xffu ? __brev(v) >> 24 : uint32_t(__ldg(C.comp_tab + (m << 8) + v));
-            const int k = __popc(m);
-            acc = (acc << k) | bits;
-            nb += k;
-            if (nb >= 8) {
-                nb -= 8;
-                pay[qb++] = uint8_t(acc >> nb);
-            }
-        }
-        if (nb > 0) pay[qb] = uint8_t(acc << (8 - nb));
-        if (P.codeword) {
-            uint8_t* cw = P.codeword + int64_t(frame) * P.codeword_stride;
-            const int cb = (C.n + 7) >> 3;
-            #pragma unroll 1
-            for (int qb = 0; qb < cb; ++qb) {
-                const uint32_t bits = (c.word(qb >> 2) >> ((qb & 3) * 8)) & 0xffu;
-                const uint32_t byte = __brev(bits) >> 24;
-                cw[qb] = uint8_t(C.n >= 8 ? byte : (byte & (0xffu << (8 - C.n))));
-            }
-        }
-        if (P.crc_ok) P.crc_ok[frame] = uint8_t(crc_ok);
-        if (P.esc) P.esc[frame] = 1;
-        if (P.metric) P.metric[frame] = 0.0f; // DecodeResult default (decode_result.hpp:12)
-        if (P.lat_ns) P.lat_ns[frame] += uint32_t(gtimer());
-    }
-    // failed frames -> the next rung's list (warp-aggregated append)
-    if (P.fail_list && C.crc_width > 0) {
-        const bool f = active && !crc_ok;
-        const unsigned fm = __ballot_sync(FULL, f);
-        int base = 0;
-        if (lane == 0 && fm) base = atomicAdd(P.fail_count, __popc(fm));
-        base = __shfl_sync(FULL, base, 0);
-        if (f) P.fail_list[base + __popc(fm & lanemask_lt())] = frame;
-    }
-    __syncwarp();
-}
-
-template <typename R>
-__global__ void __launch_bounds__(128, 8) sc_lanes_kernel(const LaunchParams P) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    unsigned char* sm = smem_raw + wib * P.smem_per_warp;
-    const int64_t gw = int64_t(blockIdx.x) * (blockDim.x >> 5) + wib;
-    // (for this kernel gscratch_per_frame is the scratch of one 32-frame warp)
-    unsigned char* gs = static_cast<unsigned char*>(P.gscratch) + gw * P.gscratch_per_frame;
-    const long long count = P.frame_list ? (long long)(*P.frame_count) : (long long)P.nframes;
-    for (;;) {
-        unsigned long long i0 = 0;
-        if (lane == 0) i0 = atomicAdd(P.work, 32ull);
-        const long long idx0 = (long long)__shfl_sync(FULL, i0, 0);
-        if (idx0 >= count) break;
-        const long long mine = idx0 + lane;
-        const bool active = mine < count;
-        const long long idx = active ? mine : idx0; // idle lanes shadow frame idx0
-        const int frame = P.frame_list ? P.frame_list[idx] : int(idx);
-        const int cid = P.code_id ? P.code_id[frame] : 0;
-        // lockstep needs one code: one pass per distinct code of the warp
-        // (multi-code batches arrive bucketed by code, so usually one)
-        unsigned pending = FULL;
-        while (pending) {
-            const int cc = __shfl_sync(FULL, cid, __ffs(pending) - 1);
-            const unsigned grp = __ballot_sync(FULL, cid == cc) & pending;
-            pending &= ~grp;
-            // lanes outside the group shadow a member's frame: packed frames of
-            // another code may be shorter than this code's n (no reads past them)
-            const bool in_grp = (grp >> lane) & 1u;
-            const int fr = __shfl_sync(FULL, frame, __ffs(grp) - 1);
-            lane_frame<R>(P, P.codes[cc], sm, gs, in_grp ? frame : fr, active && in_grp, lane);
-        }
-    }
-}
+#include "lanes.cuh"
 
 // Exhaustive check of the packed int8 f/g against the scalar kernels: every
 // (a, b) pair in [-127, 127]^2, in every byte position, next to

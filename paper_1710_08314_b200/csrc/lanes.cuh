@@ -1,0 +1,532 @@
+// The frame-per-lane SC kernel (SC / SSC and the first pass of PA / FA):
+// 32 frames per warp, one per lane, in lockstep over the SC schedule.
+//
+// A fragment of kernels.cu: included inside namespace plb::{anonymous} after
+// the list decoder (it shares Arith, Vec, fg_compute and the schedules).
+#pragma once
+// ==== frame-per-lane SC kernel (SC / SSC and the first pass of PA / FA) ====
+// A warp decodes 32 frames, one per lane, in lockstep over the SC schedule
+// of their (common) code: the op sequence of SC decoding is data-independent
+// except for the rate-1 shortcut, which the warp takes only when no lane has
+// a zero input (the expanded recursion is exact for every lane, so running
+// it for all is correct).  One warp instruction then advances 32 frames, and
+// the small nodes that cost the warp-per-frame kernel a whole warp step per
+// value are plain per-lane loops.  Per-warp storage, lane-interleaved so
+// every access is conflict-free / coalesced:
+//   * partial sums: word w of lane l at ps[w * 32 + l] (shared memory);
+//   * depth-d LLR segment (n >> d values per frame): chunks of
+//     V = min(VE, n >> d) values, chunk c of lane l at ((c * 32) + l) * V
+//     (VE = 16 bytes of values); small segments in shared memory, large ones
+//     in the warp's global scratch;
+//   * depth 0 is the channel, read in place (frame-major).
+struct LaneQ {
+    int32_t rw, psum_off, smem_total, gmem_total, pool_off, pool_in_smem;
+};
+__host__ __device__ inline LaneQ lane_layout(int n, int esz, int segmax, int want_d) {
+    LaneQ q{};
+    int off = 16 * 8; // pool pointer table
+    q.rw = n >= 32 ? n / 32 : 1;
+    q.psum_off = off;
+    off += 4 * q.rw * 32;
+    int goff = 0;
+    const int stages = ilog2(n);
+    #pragma unroll 1
+    for (int d = 1; d <= stages; ++d) {
+        const int bytes = align16((n >> d) * 32 * esz);
+        if ((n >> d) <= segmax) {
+            if (d == want_d) {
+                q.pool_off = off;
+                q.pool_in_smem = 1;
+            }
+            off += bytes;
+        } else {
+            if (d == want_d) {
+                q.pool_off = goff;
+                q.pool_in_smem = 0;
+            }
+            goff += bytes;
+        }
+    }
+    q.smem_total = off;
+    q.gmem_total = goff;
+    return q;
+}
+
+template <typename R>
+struct LaneCtx {
+    static constexpr int VE = 16 / int(sizeof(R));
+    int lane, n;
+    int segmax, keep; // depth segments > segmax values live in global scratch
+    bool discard;     // drop dead global segments from the L2 (LaunchParams::sc_discard)
+    const R* chan;      // this lane's frame
+    uint32_t* ps;       // this lane's psum words, stride 32
+    const uint64_t* pt; // pool pointer table
+    __device__ __forceinline__ R* pool(int d) const { return reinterpret_cast<R*>(pt[d]); }
+    // first value of chunk c at depth d (chunk = min(VE, n >> d) values)
+    __device__ __forceinline__ const R* chunk(int d, int c) const {
+        const int v = min(VE, n >> d);
+        return d == 0 ? chan + c * v : pool(d) + (c * 32 + lane) * v;
+    }
+    // chunk k of depth d is at base + k * stride (loop-invariant form of chunk())
+    __device__ __forceinline__ const R* chunk_base(int d, int& stride) const {
+        const int v = min(VE, n >> d);
+        stride = d == 0 ? v : 32 * v;
+        return d == 0 ? chan : pool(d) + lane * v;
+    }
+    __device__ __forceinline__ uint32_t& word(int w) const { return ps[w * 32]; }
+    __device__ void fill(int lb, int m, int bit) const {
+        if (m >= 32) {
+            #pragma unroll 1
+            for (int w = 0; w < (m >> 5); ++w) word((lb >> 5) + w) = bit ? FULL : 0u;
+        } else {
+            const uint32_t mk = ((1u << m) - 1u) << (lb & 31);
+            uint32_t& x = word(lb >> 5);
+            x = bit ? (x | mk) : (x & ~mk);
+        }
+    }
+};
+
+// sign bits of the G values of a vector (value i -> bit i)
+template <typename R, int G>
+__device__ __forceinline__ uint32_t vec_signs(const Vec<R, G>& x) {
+    uint32_t s = 0;
+    if constexpr (sizeof(R) == 1 && G >= 4) {
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(&x.raw);
+#pragma unroll
+        for (int k = 0; k < G / 4; ++k)
+            s |= ((((w[k] >> 7) & 0x01010101u) * 0x01020408u) >> 24) << (4 * k);
+    } else {
+#pragma unroll
+        for (int i = 0; i < G; ++i) s |= uint32_t(Arith<R>::val(x.v[i]) < typename Arith<R>::M(0)) << i;
+    }
+    return s;
+}
+template <typename R, int G>
+__device__ __forceinline__ bool vec_has_zero(const Vec<R, G>& x) {
+    if constexpr (sizeof(R) == 1 && G >= 4) {
+        // a zero byte: (w - 0x01..) & ~w & 0x80.. is non-zero exactly then
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(&x.raw);
+        uint32_t z = 0;
+#pragma unroll
+        for (int k = 0; k < G / 4; ++k) z |= (w[k] - 0x01010101u) & ~w[k] & 0x80808080u;
+        return z != 0u;
+    } else {
+        bool z = false;
+#pragma unroll
+        for (int i = 0; i < G; ++i) z |= Arith<R>::val(x.v[i]) == typename Arith<R>::M(0);
+        return z;
+    }
+}
+
+// U chunks per iteration: 2U loads in flight per lane (the pools of the
+// upper depths live in global memory), U * VE <= 32 partial-sum bits.
+// HIN / HOUT: the input / output depth is in global memory and takes an L2
+// eviction hint (pin / pout).
+// disc: the input segment is a global depth pool read for the last time (a G
+// op): its L2 lines are dropped without write-back once consumed
+// (discard.global.L2), so dead LLRs of 32-frame warps never reach DRAM.
+template <typename R, int U, bool HIN, bool HOUT>
+__device__ __forceinline__ void lane_fg_chunks(const LaneCtx<R>& c, int d, int nc, int lb, bool is_g,
+                                               R* out, uint64_t pin, uint64_t pout, bool disc) {
+    constexpr int VE = LaneCtx<R>::VE;
+    int cs;
+    const R* in = c.chunk_base(d, cs);
+    const R* in_b = in + nc * cs;
+    R* o = out + c.lane * VE;
+    #pragma unroll 1
+    for (int k = 0; k < nc; k += U) {
+        Vec<R, VE> a[U], b[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if constexpr (HIN) {
+                a[u] = vld_hint<R, VE>(in + (k + u) * cs, pin);
+                b[u] = vld_hint<R, VE>(in_b + (k + u) * cs, pin);
+            } else {
+                a[u] = vld<R, VE>(in + (k + u) * cs);
+                b[u] = vld<R, VE>(in_b + (k + u) * cs);
+            }
+        }
+        const int pos = lb + k * VE;
+        const uint32_t bits = is_g ? c.word(pos >> 5) >> (pos & 31) : 0u;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const Vec<R, VE> r = fg_compute<R, VE>(a[u], b[u], bits >> (u * VE), is_g);
+            if constexpr (HOUT) vst_hint<R, VE>(o + (k + u) * 32 * VE, r, pout);
+            else vst<R, VE>(o + (k + u) * 32 * VE, r);
+        }
+        // (the values were consumed above by every lane of the warp; chunk
+        // rows are 512-byte aligned, lanes 0 / 8 / 16 / 24 start its lines)
+        if (disc && (c.lane & 7) == 0) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                asm volatile("discard.global.L2 [%0], 128;" :: "l"(in + (k + u) * cs) : "memory");
+                asm volatile("discard.global.L2 [%0], 128;" :: "l"(in_b + (k + u) * cs) : "memory");
+            }
+        }
+    }
+}
+template <typename R, int U>
+__device__ __forceinline__ void lane_fg_chunks_any(const LaneCtx<R>& c, int d, int nc, int lb, bool is_g,
+                                                   R* out) {
+    if constexpr (sizeof(R) != 4) {
+        // fixed point: no hint / discard code at all (the int16 pass lost 10%
+        // to the larger loop even with the hints switched off)
+        lane_fg_chunks<R, U, false, false>(c, d, nc, lb, is_g, out, 0, 0, false);
+        return;
+    }
+    // hints only on global depths (the channel is depth 0); uniform per op
+    const bool gin = c.keep > 0 && (d == 0 || (c.n >> d) > c.segmax);
+    const bool gout = c.keep > 0 && (c.n >> (d + 1)) > c.segmax;
+    const bool disc = c.discard && is_g && d > 0 && (c.n >> d) > c.segmax;
+    if (gin) {
+        const uint64_t pin = l2_policy(d > 0 && (c.n >> d) <= c.keep);
+        if (gout)
+            lane_fg_chunks<R, U, true, true>(c, d, nc, lb, is_g, out, pin,
+                                             l2_policy((c.n >> (d + 1)) <= c.keep), disc);
+        else lane_fg_chunks<R, U, true, false>(c, d, nc, lb, is_g, out, pin, 0, disc);
+    } else {
+        lane_fg_chunks<R, U, false, false>(c, d, nc, lb, is_g, out, 0, 0, disc);
+    }
+}
+
+template <typename R>
+__device__ void lane_fg(const LaneCtx<R>& c, int d, int m, int lb, bool is_g) {
+    using A = Arith<R>;
+    constexpr int VE = LaneCtx<R>::VE;
+    constexpr int U = 32 / VE < 4 ? 32 / VE : 4;
+    const int h = m >> 1;
+    R* const out = c.pool(d + 1);
+    if (h >= VE) {
+        const int nc = h / VE;
+        if (nc >= U) lane_fg_chunks_any<R, U>(c, d, nc, lb, is_g, out);
+        else lane_fg_chunks_any<R, 1>(c, d, nc, lb, is_g, out);
+    } else {
+        // the parent's m <= VE values are one contiguous chunk
+        const R* p = c.chunk(d, 0);
+        R* q = out + c.lane * h;
+        const uint32_t bits = is_g ? c.word(lb >> 5) >> (lb & 31) : 0u;
+        if constexpr (sizeof(R) == 1) {
+            // int8 nodes of 16 / 8 / 4 values: SWAR words (the chunk is m-byte aligned)
+            if (h == 2) {
+                const uint32_t x = *reinterpret_cast<const uint32_t*>(p);
+                const uint32_t o = is_g ? g_swar(x & 0xffffu, x >> 16, bits & 3u) : f_swar(x & 0xffffu, x >> 16);
+                *reinterpret_cast<uint16_t*>(q) = uint16_t(o);
+                return;
+            }
+            if (h == 8) {
+                const uint4 x = *reinterpret_cast<const uint4*>(p);
+                uint2 o;
+                o.x = is_g ? g_swar(x.x, x.z, bits & 15u) : f_swar(x.x, x.z);
+                o.y = is_g ? g_swar(x.y, x.w, (bits >> 4) & 15u) : f_swar(x.y, x.w);
+                *reinterpret_cast<uint2*>(q) = o;
+                return;
+            }
+            if (h == 4) {
+                const uint2 x = *reinterpret_cast<const uint2*>(p);
+                *reinterpret_cast<uint32_t*>(q) = is_g ? g_swar(x.x, x.y, bits & 15u) : f_swar(x.x, x.y);
+                return;
+            }
+        }
+        #pragma unroll 1
+        for (int j = 0; j < h; ++j) q[j] = is_g ? A::g(p[j], p[h + j], (bits >> j) & 1u) : A::f(p[j], p[h + j]);
+    }
+}
+
+template <typename R>
+__device__ void lane_h(const LaneCtx<R>& c, int m, int lb) {
+    const int h = m >> 1;
+    if (h >= 32) {
+        #pragma unroll 1
+        for (int w = 0; w < (h >> 5); ++w) c.word((lb >> 5) + w) ^= c.word(((lb + h) >> 5) + w);
+    } else {
+        uint32_t& x = c.word(lb >> 5);
+        const int s = lb & 31;
+        const uint32_t mk = (1u << h) - 1u;
+        x ^= ((x >> (s + h)) & mk) << s;
+    }
+}
+
+// repetition node (sc_decoder.hpp:114-125): halving fold, bit = fold < 0.
+// Chunk pairs are added elementwise first (into the dead depth-(d+1)
+// segment), then the last chunk is folded in registers: the same additions
+// in the same order as the reference's halving loop.
+template <typename R>
+__device__ int lane_rep(const LaneCtx<R>& c, int d, int m) {
+    using A = Arith<R>;
+    using M = typename A::M;
+    constexpr int VE = LaneCtx<R>::VE;
+    Vec<R, VE> x;
+    int len = m;
+    if (m > VE) {
+        R* S = c.pool(d + 1) + c.lane * VE; // chunk k at S + k * 32 * VE
+        int nc = m / VE;
+        int cs;
+        const R* in = c.chunk_base(d, cs);
+        #pragma unroll 1
+        for (int first = 1; nc > 1; first = 0) {
+            const int hc = nc >> 1;
+            #pragma unroll 1
+            for (int k = 0; k < hc; ++k) {
+                const Vec<R, VE> a = first ? vld<R, VE>(in + k * cs) : vld<R, VE>(S + k * 32 * VE);
+                const Vec<R, VE> b = first ? vld<R, VE>(in + (k + hc) * cs) : vld<R, VE>(S + (k + hc) * 32 * VE);
+                vst<R, VE>(S + k * 32 * VE, fg_compute<R, VE>(a, b, 0u, true)); // g with u = 0: sat(a + b)
+            }
+            nc = hc;
+        }
+        x = vld<R, VE>(S);
+        len = VE;
+    } else {
+        const R* p = c.chunk(d, 0);
+#pragma unroll
+        for (int i = 0; i < VE; ++i) x.v[i] = i < m ? p[i] : R(0);
+    }
+    M v[VE];
+#pragma unroll
+    for (int i = 0; i < VE; ++i) v[i] = A::val(x.v[i]);
+#pragma unroll
+    for (int s = VE; s > 1; s >>= 1)
+        if (s <= len)
+#pragma unroll
+            for (int i = 0; i < s / 2; ++i) v[i] = A::sat(v[i], v[i + s / 2]);
+    return v[0] < M(0);
+}
+
+// rate-1 shortcut: true when this lane's m values hold no zero
+template <typename R>
+__device__ bool lane_r1_nozero(const LaneCtx<R>& c, int d, int m) {
+    constexpr int VE = LaneCtx<R>::VE;
+    bool zero = false;
+    if (sizeof(R) == 4 && m >= 8 * VE) {
+        // float: 8 chunks (32 values) in flight per trip (the large rate-1
+        // nodes read global depth pools)
+        int cs;
+        const R* in = c.chunk_base(d, cs);
+        #pragma unroll 1
+        for (int k = 0; k < m / VE; k += 8) {
+            Vec<R, VE> q[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) q[u] = vld<R, VE>(in + (k + u) * cs);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) zero |= vec_has_zero<R, VE>(q[u]);
+        }
+    } else if (m >= VE) {
+        int cs;
+        const R* in = c.chunk_base(d, cs);
+        #pragma unroll 1
+        for (int k = 0; k < m / VE; ++k) zero |= vec_has_zero<R, VE>(vld<R, VE>(in + k * cs));
+    } else if (sizeof(R) == 1 && m >= 4) { // int8 nodes of 4 / 8 values: whole words
+        const uint32_t* p = reinterpret_cast<const uint32_t*>(c.chunk(d, 0));
+        #pragma unroll 1
+        for (int k = 0; k < (m >> 2); ++k) zero |= ((p[k] - 0x01010101u) & ~p[k] & 0x80808080u) != 0u;
+    } else {
+        const R* p = c.chunk(d, 0);
+        #pragma unroll 1
+        for (int i = 0; i < m; ++i) zero |= Arith<R>::val(p[i]) == typename Arith<R>::M(0);
+    }
+    return !zero;
+}
+template <typename R>
+__device__ void lane_r1_hard(const LaneCtx<R>& c, int d, int m, int lb) {
+    using A = Arith<R>;
+    constexpr int VE = LaneCtx<R>::VE;
+    if (sizeof(R) == 4 && m >= 32) {
+        // float: a 32-bit partial-sum word (8 chunks) per trip, its loads in flight together
+        int cs;
+        const R* in = c.chunk_base(d, cs);
+        #pragma unroll 1
+        for (int k = 0; k < m / VE; k += 8) {
+            Vec<R, VE> q[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) q[u] = vld<R, VE>(in + (k + u) * cs);
+            uint32_t acc = 0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc |= vec_signs<R, VE>(q[u]) << (u * VE);
+            c.word((lb + k * VE) >> 5) = acc;
+        }
+    } else if (m >= VE) {
+        uint32_t acc = 0;
+        int cs;
+        const R* in = c.chunk_base(d, cs);
+        #pragma unroll 1
+        for (int k = 0; k < m / VE; ++k) {
+            const int pos = k * VE; // bit of the node
+            acc |= vec_signs<R, VE>(vld<R, VE>(in + k * cs)) << (pos & 31);
+            if (((pos + VE) & 31) == 0 || pos + VE >= m) {
+                if (m >= 32) {
+                    c.word((lb + (pos & ~31)) >> 5) = acc;
+                } else {
+                    const uint32_t mk = ((1u << m) - 1u) << (lb & 31);
+                    uint32_t& x = c.word(lb >> 5);
+                    x = (x & ~mk) | ((acc << (lb & 31)) & mk);
+                }
+                acc = 0;
+            }
+        }
+    } else {
+        const R* p = c.chunk(d, 0);
+        uint32_t acc = 0;
+        if (sizeof(R) == 1 && m >= 4) { // sign bits of whole words
+            #pragma unroll 1
+            for (int k = 0; k < (m >> 2); ++k) {
+                const uint32_t w = reinterpret_cast<const uint32_t*>(p)[k];
+                acc |= ((((w >> 7) & 0x01010101u) * 0x01020408u) >> 24) << (4 * k);
+            }
+        } else {
+            #pragma unroll 1
+            for (int i = 0; i < m; ++i) acc |= uint32_t(A::val(p[i]) < typename A::M(0)) << i;
+        }
+        const uint32_t mk = ((1u << m) - 1u) << (lb & 31);
+        uint32_t& x = c.word(lb >> 5);
+        x = (x & ~mk) | ((acc << (lb & 31)) & mk);
+    }
+}
+
+template <typename R>
+__device__ void lane_frame(const LaunchParams& P, const DevCode& C, unsigned char* sm,
+                           unsigned char* gs, int frame, bool active, int lane) {
+    using A = Arith<R>;
+    using M = typename A::M;
+    if (P.lat_ns && active) P.lat_ns[frame] -= uint32_t(gtimer());
+    LaneCtx<R> c;
+    c.lane = lane;
+    c.n = C.n;
+    c.segmax = P.seg_smem_max;
+    c.keep = P.sc_keep;
+    c.discard = P.sc_discard != 0;
+    c.chan = frame_llr<R>(P, frame);
+    const LaneQ q0 = lane_layout(C.n, int(sizeof(R)), P.seg_smem_max, 0);
+    c.ps = reinterpret_cast<uint32_t*>(sm + q0.psum_off) + lane;
+    uint64_t* pt = reinterpret_cast<uint64_t*>(sm);
+    c.pt = pt;
+    __syncwarp();
+    if (lane >= 1 && lane <= C.stages) {
+        const LaneQ q = lane_layout(C.n, int(sizeof(R)), P.seg_smem_max, lane);
+        pt[lane] = reinterpret_cast<uint64_t>((q.pool_in_smem ? sm : gs) + q.pool_off);
+    }
+    __syncwarp();
+    const uint32_t* sched = C.sched_lane;
+    const int nops = C.nops_lane;
+    // the next schedule word is fetched one op ahead (the schedules carry a
+    // padding word)
+    uint32_t next = __ldg(sched);
+    #pragma unroll 1
+    for (int oi = 0; oi < nops; ++oi) {
+        const uint32_t op = next;
+        next = __ldg(sched + oi + 1);
+        const int code = op_code(op), d = op_depth(op), m = 1 << op_logm(op), lb = op_lb(op);
+        switch (code) {
+        case OP_F:
+        case OP_G: lane_fg(c, d, m, lb, code == OP_G); break;
+        case OP_H: lane_h(c, m, lb); break;
+        case OP_FROZEN: c.fill(lb, m, 0); break;
+        case OP_INFO: c.fill(lb, 1, A::val(*c.chunk(d, 0)) < M(0)); break;
+        case OP_REP: c.fill(lb, m, lane_rep(c, d, m)); break;
+        case OP_R1SC: {
+            const int skip = int(next); // the word after OP_R1SC
+            ++oi;
+            if (__all_sync(FULL, lane_r1_nozero(c, d, m))) {
+                lane_r1_hard(c, d, m, lb);
+                oi += skip;
+            } // else: every lane runs the expanded recursion that follows
+            next = __ldg(sched + oi + 1);
+            break;
+        }
+        default: break;
+        }
+    }
+    // finish: CRC syndrome, payload, codeword, status (per lane)
+    int crc_ok = 0;
+    if (C.crc_width > 0) {
+        uint64_t syn = C.crc_c0;
+        const int nbytes = (C.n + 7) >> 3;
+        #pragma unroll 1
+        for (int j = 0; j < nbytes; ++j) {
+            const uint32_t byte = (c.word(j >> 2) >> ((j & 3) * 8)) & 0xffu;
+            syn ^= __ldg(C.crc_tab + (size_t(j) << 8) + byte);
+        }
+        crc_ok = syn == 0;
+    }
+    if (active) {
+        // payload (extract_payload, prune_tree.hpp:78-105): the open bits of
+        // each codeword byte compacted by table (all-open bytes: a bit
+        // reversal) and streamed out MSB-first
+        uint8_t* pay = P.payload + int64_t(frame) * P.payload_stride;
+        const int cbytes = (C.n + 7) >> 3;
+        uint32_t acc = 0;
+        int nb = 0, qb = 0;
+        #pragma unroll 1
+        for (int j = 0; j < cbytes; ++j) {
+            const uint32_t m = __ldg(C.open_mask + j);
+            if (m == 0u) continue; // uniform: one code per warp
+            const uint32_t v = (c.word(j >> 2) >> ((j & 3) * 8)) & 0xffu;
+            const uint32_t bits = m == 0xffu ? __brev(v) >> 24 : uint32_t(__ldg(C.comp_tab + (m << 8) + v));
+            const int k = __popc(m);
+            acc = (acc << k) | bits;
+            nb += k;
+            if (nb >= 8) {
+                nb -= 8;
+                pay[qb++] = uint8_t(acc >> nb);
+            }
+        }
+        if (nb > 0) pay[qb] = uint8_t(acc << (8 - nb));
+        if (P.codeword) {
+            uint8_t* cw = P.codeword + int64_t(frame) * P.codeword_stride;
+            const int cb = (C.n + 7) >> 3;
+            #pragma unroll 1
+            for (int qb = 0; qb < cb; ++qb) {
+                const uint32_t bits = (c.word(qb >> 2) >> ((qb & 3) * 8)) & 0xffu;
+                const uint32_t byte = __brev(bits) >> 24;
+                cw[qb] = uint8_t(C.n >= 8 ? byte : (byte & (0xffu << (8 - C.n))));
+            }
+        }
+        if (P.crc_ok) P.crc_ok[frame] = uint8_t(crc_ok);
+        if (P.esc) P.esc[frame] = 1;
+        if (P.metric) P.metric[frame] = 0.0f; // DecodeResult default (decode_result.hpp:12)
+        if (P.lat_ns) P.lat_ns[frame] += uint32_t(gtimer());
+    }
+    // failed frames -> the next rung's list (warp-aggregated append)
+    if (P.fail_list && C.crc_width > 0) {
+        const bool f = active && !crc_ok;
+        const unsigned fm = __ballot_sync(FULL, f);
+        int base = 0;
+        if (lane == 0 && fm) base = atomicAdd(P.fail_count, __popc(fm));
+        base = __shfl_sync(FULL, base, 0);
+        if (f) P.fail_list[base + __popc(fm & lanemask_lt())] = frame;
+    }
+    __syncwarp();
+}
+
+template <typename R>
+__global__ void __launch_bounds__(128, 8) sc_lanes_kernel(const LaunchParams P) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    unsigned char* sm = smem_raw + wib * P.smem_per_warp;
+    const int64_t gw = int64_t(blockIdx.x) * (blockDim.x >> 5) + wib;
+    // (for this kernel gscratch_per_frame is the scratch of one 32-frame warp)
+    unsigned char* gs = static_cast<unsigned char*>(P.gscratch) + gw * P.gscratch_per_frame;
+    const long long count = P.frame_list ? (long long)(*P.frame_count) : (long long)P.nframes;
+    for (;;) {
+        unsigned long long i0 = 0;
+        if (lane == 0) i0 = atomicAdd(P.work, 32ull);
+        const long long idx0 = (long long)__shfl_sync(FULL, i0, 0);
+        if (idx0 >= count) break;
+        const long long mine = idx0 + lane;
+        const bool active = mine < count;
+        const long long idx = active ? mine : idx0; // idle lanes shadow frame idx0
+        const int frame = P.frame_list ? P.frame_list[idx] : int(idx);
+        const int cid = P.code_id ? P.code_id[frame] : 0;
+        // lockstep needs one code: one pass per distinct code of the warp
+        // (multi-code batches arrive bucketed by code, so usually one)
+        unsigned pending = FULL;
+        while (pending) {
+            const int cc = __shfl_sync(FULL, cid, __ffs(pending) - 1);
+            const unsigned grp = __ballot_sync(FULL, cid == cc) & pending;
+            pending &= ~grp;
+            // lanes outside the group shadow a member's frame: packed frames of
+            // another code may be shorter than this code's n (no reads past them)
+            const bool in_grp = (grp >> lane) & 1u;
+            const int fr = __shfl_sync(FULL, frame, __ffs(grp) - 1);
+            lane_frame<R>(P, P.codes[cc], sm, gs, in_grp ? frame : fr, active && in_grp, lane);
+        }
+    }
+}
