@@ -439,6 +439,16 @@ def measure(wl, F, steps, warmup, e2e_steps, R: Ranks, peaks, peak_src, min_time
     ms_per_step = elapsed / steps * 1e3
     value = bits_per_step * ws * steps / elapsed / 1e9
 
+    # ---- per-frame device decode latency (pl_frame_latency; the reference
+    # times every decode() call, sim.cpp:54-61), one extra untimed decode
+    lat = torch.zeros(F, dtype=torch.int32, device=f"cuda:{local}")
+    dec.frame_latency(lat)
+    dec.decode_batch(llr_d, code_id=cid_d, out=out)
+    torch.cuda.synchronize()
+    dec.frame_latency(None)
+    lat_us = lat.cpu().numpy().astype(np.float64) / 1e3
+    del lat
+
     # ---- error counts of the batch, reduced over ranks (sim.cpp:66-71)
     pay = out["payload"].cpu().numpy()
     esc = out["esc"].cpu().numpy()
@@ -545,6 +555,10 @@ def measure(wl, F, steps, warmup, e2e_steps, R: Ranks, peaks, peak_src, min_time
         # frames per final list size (rank 0's batch): the work each rung sees
         "esc_hist": {int(v): int(c) for v, c in zip(*np.unique(esc, return_counts=True))},
         "gpu_launches": int(launches),
+        # rank 0's batch: device time from a frame's first to its last pass
+        # output, summed over its passes (a batch of F frames in flight)
+        "frame_latency_us": {"mean": float(lat_us.mean()), "p50": float(np.percentile(lat_us, 50)),
+                             "p99": float(np.percentile(lat_us, 99)), "max": float(lat_us.max())},
         "kernels": kernels,
         "kernel_share_of_step": all_kernel_s * 1e3 / ms_per_step,
         "roofline": roof,
