@@ -488,7 +488,8 @@ def measure(wl, F, steps, warmup, e2e_steps, R: Ranks, peaks, peak_src, min_time
     e2e_s = R.max(time.perf_counter() - t0)
     e2e_value = bits_per_step * ws * e2e_steps / e2e_s / 1e9
     d2h = F * (dec.payload_stride + 1 + 1 + 4)
-    e2e_same = bool((host_out["payload"].numpy() == pay).all() and (host_out["esc"].numpy() == esc).all())
+    e2e_same = bool(payload_rows_equal(host_out["payload"].numpy(), pay, codes, cid)
+                    and (host_out["esc"].numpy() == esc).all())
 
     # ---- per-kernel roofline fractions (live CUDA-event durations)
     freq = np.bincount(cid, minlength=len(codes)) / F if cid is not None else np.ones(1)
@@ -574,6 +575,18 @@ def measure(wl, F, steps, warmup, e2e_steps, R: Ranks, peaks, peak_src, min_time
     return fields, state
 
 
+def payload_rows_equal(a, b, codes, cid):
+    """Every frame's own payload bytes equal (mixed batches: rows are as wide
+    as the widest code, the bytes past a frame's payload are not written)."""
+    n = a.shape[0]
+    for i, c in enumerate(codes):
+        rows = np.arange(n) if cid is None else np.flatnonzero(cid[:n] == i)
+        w = (c.payload_size + 7) // 8
+        if not np.array_equal(a[rows, :w], b[rows, :w]):
+            return False
+    return True
+
+
 def parity_and_cpu(wl, st, S, nthr, time_it):
     """The compiled reference on the first S frames of the step's batch
     (identical LLR bytes): per-frame parity of payload, crc_ok, escalation
@@ -583,9 +596,14 @@ def parity_and_cpu(wl, st, S, nthr, time_it):
     codes = [(c.n, c.k, c.crc.raw() if c.crc else "", c.frozen) for c in st["codes"]]
     cid = st["cid"][:S] if st["cid"] is not None else None
     r, dt = reference_decode(O, codes, cid, st["llr"][:S], wl, nthr)
-    pb = r["payload"].shape[1]
-    mism = ((st["payload"][:S, :pb] != r["payload"]).any(1) | (st["crc_ok"][:S] != r["crc_ok"])
-            | (st["esc"][:S] != r["esc"]) | (st["metric"][:S] != r["metric"].astype(np.float32)))
+    # each frame's own payload bytes (mixed batches: rows are as wide as the widest code)
+    bad_pay = np.zeros(S, bool)
+    for i, c in enumerate(st["codes"]):
+        rows = np.arange(S) if cid is None else np.flatnonzero(cid == i)
+        w = (c.payload_size + 7) // 8
+        bad_pay[rows] = (st["payload"][rows, :w] != r["payload"][rows, :w]).any(1)
+    mism = (bad_pay | (st["crc_ok"][:S] != r["crc_ok"]) | (st["esc"][:S] != r["esc"])
+            | (st["metric"][:S] != r["metric"].astype(np.float32)))
     par = {"frames": int(S), "mismatching_frames": int(mism.sum()),
            "fields": "payload, crc_ok, esc, metric (bit-exact)", "against": "oracle/_ref"}
     cpu = None
