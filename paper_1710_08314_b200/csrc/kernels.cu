@@ -688,35 +688,32 @@ __device__ void list_frozen(Ctx<R, SW>& cx, int d, int m, int lb, int na) {
         }
     } else if (cx.lane < na) {
         const R* L = cx.llr(cx.fx->alive_list[cx.lane], d);
-        if constexpr (sizeof(R) == 4 && BIG && PLB_BIG_PEN) {
-            if (m >= 8) {
-                // float: PLB_BIG_VF vectors in flight per trip; the penalty
-                // is still summed one value at a time in index order
-                #pragma unroll 1
-                for (int i = 0; i < m; i += 4 * PLB_BIG_VF) {
-                    Vec<R, 4> q[PLB_BIG_VF];
+        if (sizeof(R) == 4 && BIG && PLB_BIG_PEN && m >= 8) {
+            // float: PLB_BIG_VF vectors in flight per trip; the penalty
+            // is still summed one value at a time in index order
+            #pragma unroll 1
+            for (int i = 0; i < m; i += 4 * PLB_BIG_VF) {
+                Vec<R, 4> q[PLB_BIG_VF];
 #pragma unroll
-                    for (int u = 0; u < PLB_BIG_VF; ++u)
-                        if (i + 4 * u < m) q[u] = vld<R, 4>(L + i + 4 * u);
+                for (int u = 0; u < PLB_BIG_VF; ++u)
+                    if (i + 4 * u < m) q[u] = vld<R, 4>(L + i + 4 * u);
 #pragma unroll
-                    for (int u = 0; u < PLB_BIG_VF; ++u)
-                        if (i + 4 * u < m)
+                for (int u = 0; u < PLB_BIG_VF; ++u)
+                    if (i + 4 * u < m)
 #pragma unroll
-                            for (int j = 0; j < 4; ++j) {
-                                const M v = A::val(q[u].v[j]);
-                                if (v < M(0)) pen = A::sat(pen, -v);
-                            }
-                }
-                goto frozen_pen_done;
+                        for (int j = 0; j < 4; ++j) {
+                            const M v = A::val(q[u].v[j]);
+                            if (v < M(0)) pen = A::sat(pen, -v);
+                        }
+            }
+        } else {
+            #pragma unroll 1
+            for (int i = 0; i < m; ++i) {
+                const M v = A::val(L[i]);
+                if (v < M(0)) pen = A::sat(pen, -v); // sequential: float order matters
             }
         }
-        #pragma unroll 1
-        for (int i = 0; i < m; ++i) {
-            const M v = A::val(L[i]);
-            if (v < M(0)) pen = A::sat(pen, -v); // sequential: float order matters
-        }
     }
-frozen_pen_done:
     const M pr = cx.sw.shfl(pen, cx.myrank & (SW - 1));
     if (cx.is_alive()) cx.metric = A::sat(cx.metric, pr);
     if (m >= 32) {
