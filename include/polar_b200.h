@@ -173,6 +173,15 @@ int64_t pl_last_launches(const pl_handle* h);
  * uint32 per frame of each call. */
 int pl_frame_latency(pl_handle* h, uint32_t* lat_ns);
 
+/* The final list of each frame, as ListDecoder<R>::alive_count / is_alive /
+ * metric_of expose it (list_decoder.hpp:91-93): with device buffers set, every
+ * later pl_decode / pl_decode_packed writes alive[f] = alive-slot mask of
+ * frame f's last list pass (bit s = logical slot s, the reference's slot
+ * numbering) and metric[f * L + s] = the metric of slot s (L = the handle's
+ * list size; dead slots hold stale values, as in the reference).  Passes
+ * without a list (SC) leave them untouched; NULL, NULL switches it off. */
+int pl_list_paths(pl_handle* h, uint32_t* alive, float* metric);
+
 /* Frames per chunk of pl_decode_host / pl_decode_host_packed (copies of one
  * chunk overlap the decode of others); 0 = automatic (~20 chunks per call,
  * 16 for multi-code handles, 8 for adaptive int8).  Default at pl_create:

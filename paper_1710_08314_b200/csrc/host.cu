@@ -432,6 +432,8 @@ struct pl_handle {
     int64_t pstride = 0, cstride = 0;
     int esz = 4;
     uint32_t* lat_ns = nullptr; // pl_frame_latency: per-frame decode time of pl_decode(_packed)
+    uint32_t* path_alive = nullptr; // pl_list_paths: the final list of every frame
+    float* path_metric = nullptr;
     int64_t host_chunk = 0;     // frames per chunk of pl_decode_host (0 = automatic)
     int sc_keep = 0; // L2 hint split of the frame-per-lane SC pass (LaunchParams::sc_keep)
     int sc_discard = 0; // LaunchParams::sc_discard
@@ -706,7 +708,7 @@ int fail(pl_handle* h, int code, const std::string& msg) {
 void run_decode(pl_handle& h, const void* llr, const int32_t* code_id, int64_t nframes,
                 uint8_t* payload, uint8_t* codeword, uint8_t* crc_ok, uint8_t* esc,
                 float* metric, cudaStream_t s, int exec = 0, const int64_t* llr_offset = nullptr,
-                uint32_t* lat_ns = nullptr) {
+                uint32_t* lat_ns = nullptr, bool paths = false) {
     ck(cudaSetDevice(h.device), "cudaSetDevice");
     h.launches = 0;
     h.prof_kind.clear(); // timed decode launches of this call (pl_last_kernel_ms)
@@ -736,6 +738,9 @@ void run_decode(pl_handle& h, const void* llr, const int32_t* code_id, int64_t n
     base.esc = esc;
     base.metric = metric;
     base.lat_ns = lat_ns;
+    base.path_alive = paths ? h.path_alive : nullptr;
+    base.path_metric = paths ? h.path_metric : nullptr;
+    base.path_stride = h.dec.l;
     if (lat_ns) ck(cudaMemsetAsync(lat_ns, 0, size_t(nframes) * sizeof(uint32_t), s), "memset");
     base.gscratch = x.d_gscratch;
     base.nmax = h.nmax;
@@ -1228,6 +1233,15 @@ int pl_debug_optime(unsigned long long* out, int reset) {
 }
 #endif
 
+int pl_list_paths(pl_handle* h, uint32_t* alive, float* metric) {
+    if (!h) return fail(nullptr, PL_ERR_ARG, "null handle");
+    if ((alive == nullptr) != (metric == nullptr))
+        return fail(h, PL_ERR_ARG, "alive and metric buffers are set together");
+    h->path_alive = alive;
+    h->path_metric = metric;
+    return PL_OK;
+}
+
 int pl_set_host_chunk(pl_handle* h, int64_t frames) {
     if (!h) return fail(nullptr, PL_ERR_ARG, "null handle");
     if (frames < 0) return fail(h, PL_ERR_ARG, "chunk size must be >= 0");
@@ -1283,7 +1297,7 @@ int pl_decode(pl_handle* h, const void* llr, const int32_t* code_id, int64_t nfr
     if (nframes > INT32_MAX) return fail(h, PL_ERR_ARG, "too many frames in one call");
     try {
         run_decode(*h, llr, code_id, nframes, payload, codeword, crc_ok, esc, metric,
-                   static_cast<cudaStream_t>(stream), 0, nullptr, h->lat_ns);
+                   static_cast<cudaStream_t>(stream), 0, nullptr, h->lat_ns, true);
         h->err.clear();
         return PL_OK;
     } catch (const std::exception& e) {
@@ -1300,7 +1314,7 @@ int pl_decode_packed(pl_handle* h, const void* llr, const int64_t* llr_offset, c
     if (nframes > INT32_MAX) return fail(h, PL_ERR_ARG, "too many frames in one call");
     try {
         run_decode(*h, llr, code_id, nframes, payload, codeword, crc_ok, esc, metric,
-                   static_cast<cudaStream_t>(stream), 0, llr_offset, h->lat_ns);
+                   static_cast<cudaStream_t>(stream), 0, llr_offset, h->lat_ns, true);
         h->err.clear();
         return PL_OK;
     } catch (const std::exception& e) {

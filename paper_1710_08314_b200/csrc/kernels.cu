@@ -1377,6 +1377,12 @@ __device__ void list_frame(const LaunchParams& P, const DevCode& C, unsigned cha
     const M pm = cx.sw.shfl(cx.metric, pick);
     if (active) {
         write_outputs<SW>(P, C, cx.row(pick), frame, lane);
+        if (P.path_alive) {
+            // ListDecoder<R>::alive / metric_of (list_decoder.hpp:91-93): the
+            // final list, logical slot s in lane s
+            if (lane < cx.l) P.path_metric[int64_t(frame) * P.path_stride + lane] = A::to_float(cx.metric);
+            if (lane == 0) P.path_alive[frame] = cx.alive;
+        }
         if (lane == 0) {
             if (P.crc_ok) P.crc_ok[frame] = uint8_t(crc_ok);
             if (P.esc) P.esc[frame] = uint8_t(P.esc_level);

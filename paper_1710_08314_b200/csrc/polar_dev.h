@@ -118,6 +118,9 @@ struct LaunchParams {
                                // pool after a G op
     uint32_t* lat_ns;          // nullable: per-frame device decode time, ns, summed over
                                // the passes the frame runs through (pl_frame_latency)
+    uint32_t* path_alive;      // nullable (pl_list_paths): alive-slot mask of the final list
+    float* path_metric;        // ... and the metric of every slot, path_stride per frame
+    int32_t path_stride;
 };
 
 constexpr int kMaxWarpsPerBlock = 4; // a block is 1, 2 or 4 independent warps

@@ -587,6 +587,21 @@ class FrameDecoder:
             _raise(rc, L.last_error(self._h))
         return o
 
+    def list_paths(self, alive=None, metric=None):
+        """pl_list_paths: later decode_batch / decode_packed calls write each
+        frame's final list — ``alive`` (CUDA int32, one mask per frame, bit s
+        = slot s) and ``metric`` (CUDA float32, frames x L) — as the
+        reference's ListDecoder alive/metric_of expose it; None switches it off."""
+        t = self._torch
+        if alive is not None:
+            assert alive.is_cuda and alive.dtype == t.int32 and alive.is_contiguous()
+            assert metric.is_cuda and metric.dtype == t.float32 and metric.is_contiguous()
+        self._paths = (alive, metric)  # keep the buffers alive while the library holds them
+        ptr = lambda x: C.c_void_p(x.data_ptr()) if x is not None else None  # noqa: E731
+        rc = L.lib().pl_list_paths(self._h, ptr(alive), ptr(metric))
+        if rc:
+            _raise(rc, L.last_error(self._h))
+
     def set_host_chunk(self, frames: int = 0):
         """pl_set_host_chunk: frames per chunk of the host-buffer decodes
         (0 = automatic)."""
