@@ -8,6 +8,7 @@ from __future__ import annotations
 
 import os
 import subprocess
+import tempfile
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
@@ -46,9 +47,10 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
         return LIB
     objs = []
     procs = []
-    tag = "" if out is None else "_" + os.path.basename(out).replace(".so", "")
+    # variant builds (``out``) keep their objects out of the source tree
+    objdir = CSRC if out is None else tempfile.mkdtemp(prefix="plb_build_")
     for src in SOURCES:
-        obj = os.path.join(CSRC, src.replace(".cu", f"{tag}.o"))
+        obj = os.path.join(objdir, src.replace(".cu", ".o"))
         cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src),
                "-o", obj]
         if verbose:
