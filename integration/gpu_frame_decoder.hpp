@@ -24,9 +24,12 @@ namespace polar {
 template <class R>
 class GpuFrameDecoder {
 public:
+    // (layout: FrameDecoder's PsumLayout; copy and shared are decision-
+    // identical in the reference, the GPU decoder has one layout)
     GpuFrameDecoder(const PolarCode& code, const PruningConfig& pruning, DecoderKind kind, int l,
-                    int device = 0)
+                    PsumLayout layout = PsumLayout::copy, int device = 0)
         : code_(&code) {
+        (void)layout;
         mask_.resize(std::size_t(code.n));
         for (int i = 0; i < code.n; ++i) mask_[std::size_t(i)] = code.frozen.get(std::size_t(i));
         pl_code c{code.n, code.k, mask_.data(), {0, 0, 0, 0, 0}, nullptr};

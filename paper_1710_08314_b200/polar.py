@@ -400,8 +400,15 @@ class FrameDecoder:
     """
 
     def __init__(self, codes, kind, l: int = 8, precision: str = "f32",
-                 pruning: PruningConfig = PruningConfig(), device: int = 0):
+                 pruning: PruningConfig = PruningConfig(), device: int = 0,
+                 psum_layout: str = "copy"):
         import torch  # device memory and streams only
+
+        # PsumLayout (list_decoder.hpp:22): "copy" and "shared" are
+        # decision-identical in the reference (test_list.cpp:253-289); the GPU
+        # decoder has one layout (lazy pointer rows), so both are accepted
+        if psum_layout not in ("copy", "shared"):
+            raise ConfigError(f"unknown partial-sum layout {psum_layout!r}")
 
         self._torch = torch
         if isinstance(codes, PolarCode):

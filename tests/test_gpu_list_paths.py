@@ -53,3 +53,18 @@ def test_final_list_matches_reference(P, gpu, ref_lib, prec, kind):
             for s in range(l):
                 if ra[s]:
                     assert m[f, s] == np.float32(rm[s]), (l, f, s, m[f, s], rm[s])
+
+
+def test_psum_layouts_accepted(P, gpu):
+    """FrameDecoder's PsumLayout (list_decoder.hpp:22): copy and shared are
+    decision-identical in the reference; both are accepted, same outputs."""
+    code = _code(P, 256, 100, "16-CCITT")
+    _, llr = P.channel(code, 1.5, 5, 0, 32, "f32")
+    x = gpu.from_numpy(llr).cuda()
+    a = P.FrameDecoder(code, "ca_sscl", 8, "f32", psum_layout="copy").decode_batch(x)
+    b = P.FrameDecoder(code, "ca_sscl", 8, "f32", psum_layout="shared").decode_batch(x)
+    gpu.cuda.synchronize()
+    for k in ("payload", "crc_ok", "esc", "metric"):
+        assert gpu.equal(a[k], b[k]), k
+    with pytest.raises(P.ConfigError):
+        P.FrameDecoder(code, "ca_sscl", 8, "f32", psum_layout="banked")
