@@ -215,6 +215,13 @@ __device__ __forceinline__ Vec<R, G> fg_compute(const Vec<R, G>& a, const Vec<R,
     } else if (is_g) {
 #pragma unroll
         for (int i = 0; i < G; ++i) o.v[i] = A::g(a.v[i], b.v[i], (bits >> i) & 1u);
+    } else if constexpr (sizeof(R) == 2 && G >= 2) {
+        // int16 f: two values per 32-bit word
+        const uint32_t* aw = reinterpret_cast<const uint32_t*>(&a.raw);
+        const uint32_t* bw = reinterpret_cast<const uint32_t*>(&b.raw);
+        uint32_t* ow = reinterpret_cast<uint32_t*>(&o.raw);
+#pragma unroll
+        for (int w = 0; w < G / 2; ++w) ow[w] = f_swar16(aw[w], bw[w]);
     } else {
 #pragma unroll
         for (int i = 0; i < G; ++i) o.v[i] = A::f(a.v[i], b.v[i]);
@@ -1712,6 +1719,31 @@ __global__ void code_scatter_kernel(const int32_t* cid, int64_t n, int32_t* curs
 // Exhaustive check of the packed int8 f/g against the scalar kernels: every
 // (a, b) pair in [-127, 127]^2, in every byte position, next to
 // pseudo-random neighbours, under all 16 partial-sum patterns.
+// int16 f on packed pairs against the scalar kernel: every a in
+// [-32767, 32767] against 512 pseudo-random b (incl. 0, +-1, +-32767), in
+// both 16-bit lanes, with swapped operands in the other lane.
+__global__ void selftest16_kernel(unsigned long long* bad) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= 65535) return;
+    using A = Arith<int16_t>;
+    const int a = t - 32767;
+    unsigned long long nbad = 0;
+    uint32_t h = 0x9e3779b9u * uint32_t(t + 1);
+    for (int j = 0; j < 512; ++j) {
+        h ^= h << 13;
+        h ^= h >> 17;
+        h ^= h << 5;
+        const int b = j < 5 ? (j == 0 ? 0 : j == 1 ? 1 : j == 2 ? -1 : j == 3 ? 32767 : -32767)
+                            : int(h % 65535u) - 32767;
+        const uint32_t x = uint32_t(uint16_t(int16_t(a))) | (uint32_t(uint16_t(int16_t(b))) << 16);
+        const uint32_t y = uint32_t(uint16_t(int16_t(b))) | (uint32_t(uint16_t(int16_t(a))) << 16);
+        const uint32_t r = f_swar16(x, y);
+        nbad += int16_t(r & 0xffffu) != A::f(int16_t(a), int16_t(b));
+        nbad += int16_t(r >> 16) != A::f(int16_t(b), int16_t(a));
+    }
+    if (nbad) atomicAdd(bad, nbad);
+}
+
 __global__ void selftest_kernel(unsigned long long* bad) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= 255 * 255) return;
@@ -1889,6 +1921,7 @@ cudaError_t kernel_selftest(unsigned long long* mismatches) {
     if (e != cudaSuccess) return e;
     cudaMemset(d, 0, sizeof(unsigned long long));
     selftest_kernel<<<(255 * 255 + 255) / 256, 256>>>(d);
+    selftest16_kernel<<<(65535 + 255) / 256, 256>>>(d);
     e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaMemcpy(mismatches, d, sizeof(unsigned long long), cudaMemcpyDeviceToHost);
     cudaFree(d);

@@ -204,6 +204,20 @@ __device__ __forceinline__ uint32_t g_swar(uint32_t a, uint32_t b, uint32_t s4) 
     return __byte_perm(vl, vh, 0x6420);
 }
 
+// int16 f on two packed values (16x2 SIMD): |x| = max(x, ~x + 1) per lane
+// (VIADDMNMX.S16x2), the smaller magnitude by VIMNMX.U16x2, negated
+// (two's complement per lane, no carry across lanes) where the operand
+// signs differ.  Bit-exact with Arith<int16_t>::f for operands in
+// [-32767, 32767] (pl_kernel_selftest); 10 instructions per 2 values
+// instead of 19.
+__device__ __forceinline__ uint32_t f_swar16(uint32_t a, uint32_t b) {
+    const uint32_t aa = __vmaxs2(a, __vadd2(~a, 0x00010001u));
+    const uint32_t ab = __vmaxs2(b, __vadd2(~b, 0x00010001u));
+    const uint32_t m = __vminu2(aa, ab);
+    const uint32_t mk = prmt((a ^ b) & 0x80008000u, 0, 0xBB99); // sign -> 0xffff per lane
+    return __vadd2(m ^ mk, mk & 0x00010001u);
+}
+
 template <typename M>
 __device__ __forceinline__ uint32_t mbits(M v);
 template <>
