@@ -4,6 +4,7 @@
 // A fragment of kernels.cu: included inside namespace plb::{anonymous} after
 // the list decoder (it shares Arith, Vec, fg_compute and the schedules).
 #pragma once
+
 // ==== frame-per-lane SC kernel (SC / SSC and the first pass of PA / FA) ====
 // A warp decodes 32 frames, one per lane, in lockstep over the SC schedule
 // of their (common) code: the op sequence of SC decoding is data-independent
@@ -296,18 +297,19 @@ template <typename R>
 __device__ bool lane_r1_nozero(const LaneCtx<R>& c, int d, int m) {
     constexpr int VE = LaneCtx<R>::VE;
     bool zero = false;
-    if (sizeof(R) == 4 && m >= 8 * VE) {
-        // float: 8 chunks (32 values) in flight per trip (the large rate-1
-        // nodes read global depth pools)
+    constexpr int NB = sizeof(R) == 4 ? 8 : 4; // chunks per trip (32 / 64 / 32 values)
+    if (m >= NB * VE) {
+        // NB chunks in flight per trip (the large rate-1 nodes read global
+        // depth pools)
         int cs;
         const R* in = c.chunk_base(d, cs);
         #pragma unroll 1
-        for (int k = 0; k < m / VE; k += 8) {
-            Vec<R, VE> q[8];
+        for (int k = 0; k < m / VE; k += NB) {
+            Vec<R, VE> q[NB];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) q[u] = vld<R, VE>(in + (k + u) * cs);
+            for (int u = 0; u < NB; ++u) q[u] = vld<R, VE>(in + (k + u) * cs);
 #pragma unroll
-            for (int u = 0; u < 8; ++u) zero |= vec_has_zero<R, VE>(q[u]);
+            for (int u = 0; u < NB; ++u) zero |= vec_has_zero<R, VE>(q[u]);
         }
     } else if (m >= VE) {
         int cs;
@@ -329,19 +331,24 @@ template <typename R>
 __device__ void lane_r1_hard(const LaneCtx<R>& c, int d, int m, int lb) {
     using A = Arith<R>;
     constexpr int VE = LaneCtx<R>::VE;
-    if (sizeof(R) == 4 && m >= 32) {
-        // float: a 32-bit partial-sum word (8 chunks) per trip, its loads in flight together
+    constexpr int NB = sizeof(R) == 4 ? 8 : 4; // chunks per trip: whole partial-sum words
+    if (m >= NB * VE) {
+        // NB chunks' loads in flight together, then their words
         int cs;
         const R* in = c.chunk_base(d, cs);
         #pragma unroll 1
-        for (int k = 0; k < m / VE; k += 8) {
-            Vec<R, VE> q[8];
+        for (int k = 0; k < m / VE; k += NB) {
+            Vec<R, VE> q[NB];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) q[u] = vld<R, VE>(in + (k + u) * cs);
-            uint32_t acc = 0;
+            for (int u = 0; u < NB; ++u) q[u] = vld<R, VE>(in + (k + u) * cs);
 #pragma unroll
-            for (int u = 0; u < 8; ++u) acc |= vec_signs<R, VE>(q[u]) << (u * VE);
-            c.word((lb + k * VE) >> 5) = acc;
+            for (int w = 0; w < NB * VE / 32; ++w) {
+                uint32_t acc = 0;
+#pragma unroll
+                for (int u = w * 32 / VE; u < (w + 1) * 32 / VE; ++u)
+                    acc |= vec_signs<R, VE>(q[u]) << ((u * VE) & 31);
+                c.word(((lb + k * VE) >> 5) + w) = acc;
+            }
         }
     } else if (m >= VE) {
         uint32_t acc = 0;
