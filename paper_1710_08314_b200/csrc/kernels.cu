@@ -393,17 +393,22 @@ __device__ __forceinline__ void span_fill_lane(uint32_t* row, int lb, int m, int
 // list_decoder.hpp:282-289) for every alive path; the result of rank r goes
 // to st_a1[r].  For m > SW the first halvings run in the rank's depth-(d+1)
 // buffer, whose contents are dead at a leaf.
-#ifndef PLB_BIG_VF
-#define PLB_BIG_VF 1 // float L = 32 kernel: vectors per trip in the per-path leaf loops
-                     // (2 / 4: 111 / 126 registers, cfg4 L=32 -8% / -10%)
+#ifndef PLB_VLEAF_MINKV
+#define PLB_VLEAF_MINKV 2 // float list kernels (KV >= this: L >= 2) with the batched leaf loops
+                          // (cfg4 L=8 +6%, cfg0 / cfg3 +1%, L=2 rungs +0.6%;
+                          // `profiles/r02_sweep_big_leaf.log`)
 #endif
-#ifndef PLB_BIG_R1
-#define PLB_BIG_R1 1
+#ifndef PLB_VLEAF_VF
+#define PLB_VLEAF_VF 1 // float list kernels: vectors per trip in the per-path leaf loops
+                       // (2 / 4 in the L = 32 kernel: 111 / 126 registers, cfg4 L=32 -8% / -10%)
 #endif
-#ifndef PLB_BIG_PEN
-#define PLB_BIG_PEN 1
+#ifndef PLB_VLEAF_R1
+#define PLB_VLEAF_R1 1
 #endif
-template <bool BIG = false, typename R, int SW>
+#ifndef PLB_VLEAF_PEN
+#define PLB_VLEAF_PEN 1
+#endif
+template <bool VLEAF = false, typename R, int SW>
 __device__ void rep_fold(Ctx<R, SW>& cx, int d, int m, int na) {
     using A = Arith<R>;
     using M = typename A::M;
@@ -421,7 +426,7 @@ __device__ void rep_fold(Ctx<R, SW>& cx, int d, int m, int na) {
             }
             if (ok && i == 0) cx.fx->st_a1[r] = mbits<M>(v);
         }
-    } else if constexpr (sizeof(R) == 4 && BIG) {
+    } else if constexpr (sizeof(R) == 4 && VLEAF) {
         // float, m > SW: one halving level at a time for all paths together
         // (level len: S[i] = S[i] + S[i + len/2], i < len/2 — the same sums
         // as the per-path loop below, in the same tree), so a level costs one
@@ -677,7 +682,7 @@ __device__ void fork_apply(Ctx<R, SW>& cx, const typename Arith<R>::M (&cm)[CPL]
 }
 
 // frozen leaf / rate-0 node (list_decoder.hpp:227-238)
-template <bool BIG = false, typename R, int SW>
+template <bool VLEAF = false, typename R, int SW>
 __device__ void list_frozen(Ctx<R, SW>& cx, int d, int m, int lb, int na) {
     using A = Arith<R>;
     using M = typename A::M;
@@ -695,17 +700,17 @@ __device__ void list_frozen(Ctx<R, SW>& cx, int d, int m, int lb, int na) {
         }
     } else if (cx.lane < na) {
         const R* L = cx.llr(cx.fx->alive_list[cx.lane], d);
-        if (sizeof(R) == 4 && BIG && PLB_BIG_PEN && m >= 8) {
-            // float: PLB_BIG_VF vectors in flight per trip; the penalty
+        if (sizeof(R) == 4 && VLEAF && PLB_VLEAF_PEN && m >= 8) {
+            // float: PLB_VLEAF_VF vectors in flight per trip; the penalty
             // is still summed one value at a time in index order
             #pragma unroll 1
-            for (int i = 0; i < m; i += 4 * PLB_BIG_VF) {
-                Vec<R, 4> q[PLB_BIG_VF];
+            for (int i = 0; i < m; i += 4 * PLB_VLEAF_VF) {
+                Vec<R, 4> q[PLB_VLEAF_VF];
 #pragma unroll
-                for (int u = 0; u < PLB_BIG_VF; ++u)
+                for (int u = 0; u < PLB_VLEAF_VF; ++u)
                     if (i + 4 * u < m) q[u] = vld<R, 4>(L + i + 4 * u);
 #pragma unroll
-                for (int u = 0; u < PLB_BIG_VF; ++u)
+                for (int u = 0; u < PLB_VLEAF_VF; ++u)
                     if (i + 4 * u < m)
 #pragma unroll
                         for (int j = 0; j < 4; ++j) {
@@ -738,7 +743,7 @@ __device__ void list_frozen(Ctx<R, SW>& cx, int d, int m, int lb, int na) {
 // Per-path statistics of an R1 / SPC node: hard decisions written into the
 // path's own psum span, the two smallest magnitudes under the (value, index)
 // order (select.hpp:18-68) -> st_i1/st_a1, st_i2/st_a2, parity -> st_w.
-template <bool BIG = false, typename R, int SW>
+template <bool VLEAF = false, typename R, int SW>
 __device__ void r1spc_stats(Ctx<R, SW>& cx, int d, int m, int lb, int na) {
     using A = Arith<R>;
     using M = typename A::M;
@@ -828,16 +833,15 @@ __device__ void r1spc_stats(Ctx<R, SW>& cx, int d, int m, int lb, int na) {
         const uint32_t e1 = min(x, y), e2 = min(max(x, y), min(q2 & 0xffffu, q2 >> 16));
         k1 = K(((e1 >> 9) << 16) | (e1 & 511u));
         k2 = K(((e2 >> 9) << 16) | (e2 & 511u));
-    } else if (sizeof(R) == 4 && BIG && PLB_BIG_R1 && ok && E >= 4 * PLB_BIG_VF) {
-        // float L = 32 kernel: PLB_BIG_VF vectors in flight per trip, keys in
-        // index order
+    } else if (sizeof(R) == 4 && VLEAF && PLB_VLEAF_R1 && ok && E >= 4 * PLB_VLEAF_VF) {
+        // float (VLEAF): PLB_VLEAF_VF vectors per trip, keys in index order
         #pragma unroll 1
-        for (int k = 0; k < E; k += 4 * PLB_BIG_VF) {
-            Vec<R, 4> q[PLB_BIG_VF];
+        for (int k = 0; k < E; k += 4 * PLB_VLEAF_VF) {
+            Vec<R, 4> q[PLB_VLEAF_VF];
 #pragma unroll
-            for (int u = 0; u < PLB_BIG_VF; ++u) q[u] = vld<R, 4>(L + k + 4 * u);
+            for (int u = 0; u < PLB_VLEAF_VF; ++u) q[u] = vld<R, 4>(L + k + 4 * u);
 #pragma unroll
-            for (int u = 0; u < PLB_BIG_VF; ++u)
+            for (int u = 0; u < PLB_VLEAF_VF; ++u)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     const M v = A::val(q[u].v[j]);
@@ -847,7 +851,7 @@ __device__ void r1spc_stats(Ctx<R, SW>& cx, int d, int m, int lb, int na) {
                     k2 = kmin(k2, kmax(k1, kv));
                     k1 = n1;
                 }
-            if (((k + 4 * PLB_BIG_VF) & 31) == 0 || k + 4 * PLB_BIG_VF >= E) {
+            if (((k + 4 * PLB_VLEAF_VF) & 31) == 0 || k + 4 * PLB_VLEAF_VF >= E) {
                 const int pos = base + i0 + (k & ~31);
                 if (acc) atomicOr(span + (pos >> 5), acc << (pos & 31));
                 par ^= __popc(acc);
@@ -904,7 +908,7 @@ __device__ void r1spc_stats(Ctx<R, SW>& cx, int d, int m, int lb, int na) {
 // repetition node (list_decoder.hpp:276-305): after the fold, pen_w = the
 // sum of the magnitudes that disagree with the fold's decision, sequential
 // in index order (float order matters; int8 is order-free) -> st_a2, st_w.
-template <bool BIG = false, typename R, int SW>
+template <bool VLEAF = false, typename R, int SW>
 __device__ void rep_pen(Ctx<R, SW>& cx, int d, int m, int na) {
     using A = Arith<R>;
     using M = typename A::M;
@@ -929,16 +933,16 @@ __device__ void rep_pen(Ctx<R, SW>& cx, int d, int m, int na) {
         const R* L = cx.llr(cx.fx->alive_list[cx.lane], d);
         const bool w = mfrom<M>(cx.fx->st_a1[cx.lane]) < M(0);
         M pen = M(0);
-        if (sizeof(R) == 4 && BIG && PLB_BIG_PEN && m >= 8) {
-            // float: PLB_BIG_VF vectors in flight per trip, summed in index order
+        if (sizeof(R) == 4 && VLEAF && PLB_VLEAF_PEN && m >= 8) {
+            // float: PLB_VLEAF_VF vectors in flight per trip, summed in index order
             #pragma unroll 1
-            for (int i = 0; i < m; i += 4 * PLB_BIG_VF) {
-                Vec<R, 4> q[PLB_BIG_VF];
+            for (int i = 0; i < m; i += 4 * PLB_VLEAF_VF) {
+                Vec<R, 4> q[PLB_VLEAF_VF];
 #pragma unroll
-                for (int u = 0; u < PLB_BIG_VF; ++u)
+                for (int u = 0; u < PLB_VLEAF_VF; ++u)
                     if (i + 4 * u < m) q[u] = vld<R, 4>(L + i + 4 * u);
 #pragma unroll
-                for (int u = 0; u < PLB_BIG_VF; ++u)
+                for (int u = 0; u < PLB_VLEAF_VF; ++u)
                     if (i + 4 * u < m)
 #pragma unroll
                         for (int j = 0; j < 4; ++j) {
@@ -1134,17 +1138,17 @@ __device__ void fused_leaf(Ctx<R, SW>& cx, int code, int d, int m, int lb, int n
 // (ascending slot, then candidate number, list_decoder.hpp:240-333), one
 // shared fork_apply, normalisation.  C = candidates per lane, fixed per
 // kernel instantiation (4L <= SW*C).
-template <typename R, int SW, int C, int MAXW, bool BIG = false>
+template <typename R, int SW, int C, int MAXW, bool VLEAF = false>
 __device__ void list_fork_node(Ctx<R, SW>& cx, int code, int d, int m, int lb, int na, bool fused) {
     using A = Arith<R>;
     using M = typename A::M;
     if (fused) {
         // statistics already taken by fused_leaf
     } else if (code == OP_R1 || code == OP_SPC) {
-        r1spc_stats<BIG>(cx, d, m, lb, na);
+        r1spc_stats<VLEAF>(cx, d, m, lb, na);
     } else if (code == OP_REP) {
-        rep_fold<BIG>(cx, d, m, na);
-        rep_pen<BIG>(cx, d, m, na);
+        rep_fold<VLEAF>(cx, d, m, na);
+        rep_pen<VLEAF>(cx, d, m, na);
     } else { // INFO: the leaf LLR of rank r -> st_a1[r]
         if (cx.lane < na) cx.fx->st_a1[cx.lane] = mbits<M>(A::val(cx.llr(cx.fx->alive_list[cx.lane], d)[0]));
         __syncwarp();
@@ -1320,9 +1324,9 @@ __device__ void list_frame(const LaunchParams& P, const DevCode& C, unsigned cha
         if (code <= OP_G) op_fg<(sizeof(R) == 4 && KV >= PLB_FG_UNROLL_MINKV) ? PLB_FG_UNROLL : 1>(cx, d, m, lb, na, code == OP_G);
         else if (code == OP_H) op_h(cx, m, lb, na);
         else if (code == OP_FROZEN) {
-            if (!fused) list_frozen<(sizeof(R) == 4 && KV >= 6)>(cx, d, m, lb, na);
+            if (!fused) list_frozen<(sizeof(R) == 4 && KV >= PLB_VLEAF_MINKV)>(cx, d, m, lb, na);
         } else {
-            list_fork_node<R, SW, CW, MAXW, (sizeof(R) == 4 && KV >= 6)>(cx, code, d, m, lb, na, fused);
+            list_fork_node<R, SW, CW, MAXW, (sizeof(R) == 4 && KV >= PLB_VLEAF_MINKV)>(cx, code, d, m, lb, na, fused);
         }
 #ifdef PLB_OPTIME
         // (profiling build only) cycles per op kind of the first frame
