@@ -254,7 +254,7 @@ void emit_sc_subtree(int depth, int m, int base, int frozen_at, std::vector<uint
                      int sub_max) {
     if (m <= sub_max && m >= 2) {
         uint32_t mask = 0;
-        if (frozen_at >= 0) mask = 1u << (frozen_at - base);
+        if (frozen_at >= base && frozen_at < base + m) mask = 1u << (frozen_at - base);
         s.push_back(plb::op_pack(plb::OP_SCSUB, depth, ilog2i(m), base));
         s.push_back(mask);
         return;
@@ -277,19 +277,21 @@ void emit_sc_subtree(int depth, int m, int base, int frozen_at, std::vector<uint
 // test_sc.cpp:39-74).  sub_max = 0: no OP_SCSUB (the frame-per-lane SC
 // kernel walks every op per lane).
 void emit_sc(const std::vector<Node>& t, int ni, std::vector<uint32_t>& s,
-             const uint8_t* frozen, int sub_max = plb::kScSubMax) {
+             const uint8_t* frozen, int sub_max = plb::kScSubMax, bool lane = false) {
     const Node& nd = t[size_t(ni)];
     const int lg = ilog2i(nd.size);
-    if (nd.kind == NK_BRANCH && nd.size <= sub_max) {
+    // (lane schedules: a small rate-1 node is a subtree op with no frozen
+    // position; the op takes the hard-decision shortcut itself)
+    if ((nd.kind == NK_BRANCH || (lane && nd.kind == NK_R1)) && nd.size <= sub_max && nd.size >= 2) {
         emit_scsub(nd.depth, nd.size, nd.lb, frozen, s);
         return;
     }
     switch (nd.kind) {
     case NK_BRANCH:
         s.push_back(plb::op_pack(plb::OP_F, nd.depth, lg, nd.lb));
-        emit_sc(t, nd.left, s, frozen, sub_max);
+        emit_sc(t, nd.left, s, frozen, sub_max, lane);
         s.push_back(plb::op_pack(plb::OP_G, nd.depth, lg, nd.lb));
-        emit_sc(t, nd.right, s, frozen, sub_max);
+        emit_sc(t, nd.right, s, frozen, sub_max, lane);
         s.push_back(plb::op_pack(plb::OP_H, nd.depth, lg, nd.lb));
         break;
     case NK_FROZEN:
@@ -376,7 +378,11 @@ HostCode make_host_code(const pl_code& c, const pl_decoder& dec) {
     build_tree(tree, h.frozen.data(), 0, c.n, 0, pc);
     emit_list(tree, 0, h.sched_list, dec.precision == PL_I8 ? plb::kFuseMaxI8 : plb::kFuseMaxF32);
     emit_sc(tree, 0, h.sched_sc, h.frozen.data());
-    emit_sc(tree, 0, h.sched_lane, h.frozen.data(), 0);
+    // frame-per-lane SC kernel: subtrees of <= PLB_LANE_SUB values (default and
+    // maximum 16) are decoded in registers (OP_SCSUB), everything else op by op
+    const char* ls = std::getenv("PLB_LANE_SUB");
+    const int lane_sub = ls ? std::min(16, std::max(0, std::atoi(ls))) : 16;
+    emit_sc(tree, 0, h.sched_lane, h.frozen.data(), lane_sub, true);
 
     if (crc) {
         // affine map: crc(m) = c0 ^ XOR_i m_i col_i over the K message bits;

@@ -388,6 +388,101 @@ __device__ void lane_r1_hard(const LaneCtx<R>& c, int d, int m, int lb) {
     }
 }
 
+// ---- in-register subtrees (OP_SCSUB of the lane schedule) ----------------
+// A subtree of M <= kLaneSubMax values is decoded by the unabridged SC
+// recursion of sc_decoder.hpp:99-112 on registers: the lane loads its M
+// LLRs once, every f / g level is straight-line code on values of the
+// metric type (no depth-pool round trips, no per-op dispatch), and the
+// node's partial sums (after its H steps) come back as M bits.  `mask`
+// (uniform: one code per warp) marks the frozen positions.  R0 / REP / SPC /
+// R1 sub-nodes decide exactly as their pruned forms do (sc_decoder.hpp:
+// 80-94: rate-1 and single-parity run this very recursion; the repetition
+// fold is the frozen descent's g chain; rate-0 leaves are all 0).
+template <typename R>
+__device__ __forceinline__ typename Arith<R>::M f_val(typename Arith<R>::M a, typename Arith<R>::M b) {
+    if constexpr (sizeof(R) == 4) {
+        return Arith<float>::f(a, b);
+    } else {
+        const int m = min(abs(a), abs(b));
+        return ((a ^ b) < 0) ? -m : m;
+    }
+}
+template <typename R>
+__device__ __forceinline__ typename Arith<R>::M g_val(typename Arith<R>::M a, typename Arith<R>::M b,
+                                                      uint32_t s) {
+    if constexpr (sizeof(R) == 4) {
+        return Arith<float>::g(a, b, s);
+    } else {
+        const int v = s ? b - a : a + b;
+        return max(-Arith<R>::kMax, min(Arith<R>::kMax, v));
+    }
+}
+template <typename R, int M>
+__device__ __forceinline__ uint32_t sc_regs(const typename Arith<R>::M (&x)[M], uint32_t mask) {
+    using MM = typename Arith<R>::M;
+    if constexpr (M == 1) {
+        return uint32_t(x[0] < MM(0)) & ~mask & 1u;
+    } else {
+        constexpr int H = M / 2;
+        constexpr uint32_t ones = (1u << H) - 1u;
+        MM t[H];
+        uint32_t ul = 0;
+        // an all-frozen left half decides 0 without its f values (uniform)
+        if (M < 4 || (mask & ones) != ones) {
+#pragma unroll
+            for (int i = 0; i < H; ++i) t[i] = f_val<R>(x[i], x[i + H]);
+            ul = sc_regs<R, H>(t, mask & ones);
+        }
+#pragma unroll
+        for (int i = 0; i < H; ++i) t[i] = g_val<R>(x[i], x[i + H], (ul >> i) & 1u);
+        const uint32_t ur = sc_regs<R, H>(t, mask >> H);
+        return (ul ^ ur) | (ur << H);
+    }
+}
+constexpr int kLaneSubMax = 16;
+
+template <typename R, int M>
+__device__ __forceinline__ void lane_sub(const LaneCtx<R>& c, int d, int lb, uint32_t mask) {
+    using A = Arith<R>;
+    using MM = typename A::M;
+    constexpr int VE = LaneCtx<R>::VE;
+    MM x[M];
+    if constexpr (M >= VE) {
+        int cs;
+        const R* in = c.chunk_base(d, cs);
+#pragma unroll
+        for (int k = 0; k < M / VE; ++k) {
+            const Vec<R, VE> q = vld<R, VE>(in + k * cs);
+#pragma unroll
+            for (int i = 0; i < VE; ++i) x[k * VE + i] = A::val(q.v[i]);
+        }
+    } else {
+        const Vec<R, M> q = vld<R, M>(c.chunk(d, 0));
+#pragma unroll
+        for (int i = 0; i < M; ++i) x[i] = A::val(q.v[i]);
+    }
+    uint32_t bits;
+    bool hard = false;
+    if (mask == 0u) {
+        // rate-1 shortcut (uniform): no zero input in any lane -> hard decisions
+        bool nz = true;
+#pragma unroll
+        for (int i = 0; i < M; ++i) nz &= x[i] != MM(0);
+        hard = __all_sync(FULL, nz);
+    }
+    if (hard) {
+        bits = 0;
+#pragma unroll
+        for (int i = 0; i < M; ++i) bits |= uint32_t(x[i] < MM(0)) << i;
+    } else {
+        bits = sc_regs<R, M>(x, mask);
+    }
+    constexpr uint32_t mk0 = M >= 32 ? FULL : ((1u << M) - 1u);
+    uint32_t& w = c.word(lb >> 5);
+    const int s = lb & 31;
+    w = (w & ~(mk0 << s)) | (bits << s);
+}
+
 template <typename R>
 __device__ void lane_frame(const LaunchParams& P, const DevCode& C, unsigned char* sm,
                            unsigned char* gs, int frame, bool active, int lane) {
@@ -428,6 +523,18 @@ __device__ void lane_frame(const LaunchParams& P, const DevCode& C, unsigned cha
         case OP_FROZEN: c.fill(lb, m, 0); break;
         case OP_INFO: c.fill(lb, 1, A::val(*c.chunk(d, 0)) < M(0)); break;
         case OP_REP: c.fill(lb, m, lane_rep(c, d, m)); break;
+        case OP_SCSUB: {
+            const uint32_t mask = next; // the word after OP_SCSUB
+            ++oi;
+            next = __ldg(sched + oi + 1);
+            switch (m) {
+            case 2: lane_sub<R, 2>(c, d, lb, mask); break;
+            case 4: lane_sub<R, 4>(c, d, lb, mask); break;
+            case 8: lane_sub<R, 8>(c, d, lb, mask); break;
+            default: lane_sub<R, 16>(c, d, lb, mask); break;
+            }
+            break;
+        }
         case OP_R1SC: {
             const int skip = int(next); // the word after OP_R1SC
             ++oi;
