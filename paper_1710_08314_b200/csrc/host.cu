@@ -314,6 +314,61 @@ void emit_sc(const std::vector<Node>& t, int ni, std::vector<uint32_t>& s,
     }
 }
 
+// Lane schedules: an F / G op whose next ops are F ops (the left descent
+// below its child) takes up to jmax of them along: the op computes its own
+// output chunk group and the F levels below it in registers and stores every
+// level, so the chained F ops never read their input segment back
+// (kOpChainShift bits of the op word = the number of chained F ops, which are
+// dropped from the schedule).  Level j's segment must still hold whole
+// 16-byte chunks: (m / 2) >> J >= ve values.  R1SC skip lengths are
+// recomputed for the shortened expansions.
+void fuse_lane_chains(const std::vector<uint32_t>& in, size_t lo, size_t hi,
+                      std::vector<uint32_t>& out, int ve, int jmax, int jmax0, bool gr1) {
+    size_t i = lo;
+    while (i < hi) {
+        const uint32_t w = in[i];
+        const int code = plb::op_code(w);
+        if (gr1 && code == plb::OP_G && i + 2 < hi && plb::op_code(in[i + 1]) == plb::OP_R1SC &&
+            plb::op_depth(in[i + 1]) == plb::op_depth(w) + 1 && (1 << plb::op_logm(w)) >= 64) {
+            // G + rate-1 child: OP_GR1, count, then the plain G and the
+            // expanded recursion of the child (taken when a g value is zero)
+            out.push_back((w & ~15u) | plb::OP_GR1);
+            const size_t at = out.size();
+            out.push_back(0);
+            out.push_back(w);
+            const size_t len = in[i + 2];
+            fuse_lane_chains(in, i + 3, i + 3 + len, out, ve, jmax, jmax0, gr1);
+            out[at] = uint32_t(out.size() - at - 1);
+            i += 3 + len;
+        } else if (code == plb::OP_SCSUB) {
+            out.push_back(w);
+            out.push_back(in[i + 1]);
+            i += 2;
+        } else if (code == plb::OP_R1SC) {
+            out.push_back(w);
+            const size_t at = out.size();
+            out.push_back(0);
+            const size_t len = in[i + 1];
+            fuse_lane_chains(in, i + 2, i + 2 + len, out, ve, jmax, jmax0, gr1);
+            out[at] = uint32_t(out.size() - at - 1);
+            i += 2 + len;
+        } else if (code == plb::OP_F || code == plb::OP_G) {
+            const int h = (1 << plb::op_logm(w)) >> 1;
+            int j = 0;
+            const int jm = plb::op_depth(w) == 0 ? jmax0 : jmax;
+            while (j < jm && i + 1 + size_t(j) < hi && plb::op_code(in[i + 1 + size_t(j)]) == plb::OP_F &&
+                   plb::op_depth(in[i + 1 + size_t(j)]) == plb::op_depth(w) + 1 + j &&
+                   (h >> (j + 1)) >= ve)
+                ++j;
+            out.push_back(w | (uint32_t(j) << plb::kOpChainShift));
+            i += 1 + size_t(j);
+        } else {
+            out.push_back(w);
+            ++i;
+        }
+    }
+}
+
 bool uses_list(int k) { return k != PL_KIND_SC && k != PL_KIND_SSC; }
 bool uses_crc(int k) { return k == PL_KIND_CA_SSCL || k == PL_KIND_PA_SSCL || k == PL_KIND_FA_SSCL; }
 bool adaptive(int k) { return k == PL_KIND_PA_SSCL || k == PL_KIND_FA_SSCL; }
@@ -383,6 +438,24 @@ HostCode make_host_code(const pl_code& c, const pl_decoder& dec) {
     const char* ls = std::getenv("PLB_LANE_SUB");
     const int lane_sub = ls ? std::min(16, std::max(0, std::atoi(ls))) : 16;
     emit_sc(tree, 0, h.sched_lane, h.frozen.data(), lane_sub, true);
+    {
+        // chained F levels (PLB_LANE_CHAIN, at most 1; 0 = one op per level)
+        const char* lc = std::getenv("PLB_LANE_CHAIN");
+        const int jdef = dec.precision == PL_F32 ? 1 : 0; // float only (lanes.cuh lane_fg)
+        const int jmax = dec.precision != PL_F32 ? 0 : lc ? std::min(1, std::max(0, std::atoi(lc))) : jdef;
+        const char* lc0 = std::getenv("PLB_LANE_CHAIN0"); // ... of the ops on the channel
+        const int jmax0 = dec.precision != PL_F32 ? 0 : lc0 ? std::min(1, std::max(0, std::atoi(lc0))) : 0;
+        // G ops with a rate-1 child: decided in registers (float; zero LLRs are
+        // common in fixed point, where the plain ops would run as well)
+        const bool gr1 = dec.precision == PL_F32 && !(std::getenv("PLB_LANE_GR1") && std::atoi(std::getenv("PLB_LANE_GR1")) == 0);
+        if (jmax > 0 || jmax0 > 0 || gr1) {
+            std::vector<uint32_t> fused;
+            fused.reserve(h.sched_lane.size());
+            const int ve = dec.precision == PL_F32 ? 4 : dec.precision == PL_I8 ? 16 : 8;
+            fuse_lane_chains(h.sched_lane, 0, h.sched_lane.size(), fused, ve, jmax, jmax0, gr1);
+            h.sched_lane.swap(fused);
+        }
+    }
 
     if (crc) {
         // affine map: crc(m) = c0 ^ XOR_i m_i col_i over the K message bits;
@@ -441,7 +514,7 @@ struct pl_handle {
     uint32_t* path_alive = nullptr; // pl_list_paths: the final list of every frame
     float* path_metric = nullptr;
     int64_t host_chunk = 0;     // frames per chunk of pl_decode_host (0 = automatic)
-    int sc_keep = 0; // L2 hint split of the frame-per-lane SC pass (LaunchParams::sc_keep)
+    int sc_keep = 0, sc_keep_hi = 0; // L2 hint split of the frame-per-lane SC pass (LaunchParams::sc_keep)
     int sc_discard = 0; // LaunchParams::sc_discard
     int list_discard = 0; // LaunchParams::list_discard
     int sms = 0;
@@ -775,6 +848,7 @@ void run_decode(pl_handle& h, const void* llr, const int32_t* code_id, int64_t n
         p.team = rc.team;
         p.seg_solo = rc.seg_solo;
         p.sc_keep = rc.lanes ? h.sc_keep : 0;
+        p.sc_keep_hi = rc.lanes ? h.sc_keep_hi : 0;
         p.sc_discard = rc.lanes ? h.sc_discard : 0;
         p.list_discard = rc.lanes ? 0 : h.list_discard;
         p.solo_max = rc.grid * rc.fpw;
@@ -1135,7 +1209,10 @@ int pl_create(const pl_code* codes, int32_t ncodes, const pl_decoder* dec, int32
             // (evict_last), larger ones and the channel streamed (evict_first).
             // FA@4.5 dB float SC pass 23.1 -> 21.7 ms per 2^20 frames; int8 is
             // slower with hints (9.4 -> 9.9 ms), so only float takes them
-            h->sc_keep = env_int("PLB_SC_KEEP", h->dec.precision == PL_F32 ? 256 : 0);
+            // Three classes (round 2, with the GR1 / chained ops): <= 64 values
+            // evict_last, <= 256 evict_normal: 15.65 -> 15.4 ms
+            h->sc_keep = env_int("PLB_SC_KEEP", h->dec.precision == PL_F32 ? 64 : 0);
+            h->sc_keep_hi = env_int("PLB_SC_KEEP_HI", h->dec.precision == PL_F32 ? 256 : 0);
             // ... and dead global segments dropped from the L2 after their
             // last read (float: SC pass 21.9 -> 20.7 ms)
             h->sc_discard = env_int("PLB_SC_DISCARD", h->dec.precision == PL_F32 ? 1 : 0);

@@ -57,7 +57,7 @@ template <typename R>
 struct LaneCtx {
     static constexpr int VE = 16 / int(sizeof(R));
     int lane, n;
-    int segmax, keep; // depth segments > segmax values live in global scratch
+    int segmax, keep, keep_hi; // depth segments > segmax values live in global scratch
     bool discard;     // drop dead global segments from the L2 (LaunchParams::sc_discard)
     const R* chan;      // this lane's frame
     uint32_t* ps;       // this lane's psum words, stride 32
@@ -75,6 +75,13 @@ struct LaneCtx {
         return d == 0 ? chan : pool(d) + lane * v;
     }
     __device__ __forceinline__ uint32_t& word(int w) const { return ps[w * 32]; }
+    // L2 eviction class of depth d's global segment: <= keep values
+    // evict_last, <= keep_hi evict_normal, larger ones and the channel
+    // evict_first
+    __device__ __forceinline__ uint64_t policy(int d) const {
+        const int seg = n >> d;
+        return l2_policy(d == 0 ? 0 : seg <= keep ? 2 : seg <= keep_hi ? 1 : 0);
+    }
     __device__ void fill(int lb, int m, int bit) const {
         if (m >= 32) {
             #pragma unroll 1
@@ -180,18 +187,110 @@ __device__ __forceinline__ void lane_fg_chunks_any(const LaneCtx<R>& c, int d, i
     const bool gout = c.keep > 0 && (c.n >> (d + 1)) > c.segmax;
     const bool disc = c.discard && is_g && d > 0 && (c.n >> d) > c.segmax;
     if (gin) {
-        const uint64_t pin = l2_policy(d > 0 && (c.n >> d) <= c.keep);
+        const uint64_t pin = c.policy(d);
         if (gout)
             lane_fg_chunks<R, U, true, true>(c, d, nc, lb, is_g, out, pin,
-                                             l2_policy((c.n >> (d + 1)) <= c.keep), disc);
+                                             c.policy(d + 1), disc);
         else lane_fg_chunks<R, U, true, false>(c, d, nc, lb, is_g, out, pin, 0, disc);
     } else {
         lane_fg_chunks<R, U, false, false>(c, d, nc, lb, is_g, out, 0, 0, disc);
     }
 }
 
+// A chained op (host.cu fuse_lane_chains): the F / G op at depth d and the
+// J F ops below it in one sweep.  Output chunk group k of the deepest level
+// needs the 2^J depth-(d+1) chunks k + t * q (q = nc >> J), i.e. 2 * 2^J
+// input chunks; every level is stored (the G ops of the levels read them
+// later), none is read back.  HINT: float only, L2 eviction hints on the
+// global levels as in lane_fg_chunks.
+template <typename R, int J, int U, bool HINT>
+__device__ __forceinline__ void lane_fg_chain(const LaneCtx<R>& c, int d, int nc, int lb, bool is_g) {
+    constexpr int VE = LaneCtx<R>::VE;
+    constexpr int T = 1 << J;
+    int cs;
+    const R* in = c.chunk_base(d, cs);
+    const R* in_b = in + nc * cs;
+    const int q = nc >> J;
+    R* o[J + 1];
+    bool og[J + 1];
+    uint64_t pol[J + 1];
+#pragma unroll
+    for (int j = 0; j <= J; ++j) {
+        o[j] = c.pool(d + 1 + j) + c.lane * VE;
+        og[j] = HINT && c.keep > 0 && (c.n >> (d + 1 + j)) > c.segmax;
+        pol[j] = 0;
+        if constexpr (HINT)
+            if (og[j]) pol[j] = c.policy(d + 1 + j);
+    }
+    const bool gin = HINT && c.keep > 0 && (d == 0 || (c.n >> d) > c.segmax);
+    uint64_t pin = 0;
+    if constexpr (HINT)
+        if (gin) pin = c.policy(d);
+    const bool disc = HINT && c.discard && is_g && d > 0 && (c.n >> d) > c.segmax;
+    #pragma unroll 1
+    for (int k = 0; k < q; k += U) {
+        Vec<R, VE> a[U][T], b[U][T];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int t = 0; t < T; ++t) {
+                const int ci = k + u + t * q;
+                if (HINT && gin) {
+                    a[u][t] = vld_hint<R, VE>(in + ci * cs, pin);
+                    b[u][t] = vld_hint<R, VE>(in_b + ci * cs, pin);
+                } else {
+                    a[u][t] = vld<R, VE>(in + ci * cs);
+                    b[u][t] = vld<R, VE>(in_b + ci * cs);
+                }
+            }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+#pragma unroll
+            for (int t = 0; t < T; ++t) {
+                const int ci = k + u + t * q;
+                const int pos = lb + ci * VE;
+                const uint32_t bits = is_g ? c.word(pos >> 5) >> (pos & 31) : 0u;
+                a[u][t] = fg_compute<R, VE>(a[u][t], b[u][t], bits, is_g);
+                if (HINT && og[0]) vst_hint<R, VE>(o[0] + ci * 32 * VE, a[u][t], pol[0]);
+                else vst<R, VE>(o[0] + ci * 32 * VE, a[u][t]);
+            }
+#pragma unroll
+            for (int j = 1; j <= J; ++j) {
+#pragma unroll
+                for (int t = 0; t < (T >> j); ++t) {
+                    const int ci = k + u + t * q;
+                    a[u][t] = fg_compute<R, VE>(a[u][t], a[u][t + (T >> j)], 0u, false);
+                    if (HINT && og[j]) vst_hint<R, VE>(o[j] + ci * 32 * VE, a[u][t], pol[j]);
+                    else vst<R, VE>(o[j] + ci * 32 * VE, a[u][t]);
+                }
+            }
+        }
+        if (HINT && disc && (c.lane & 7) == 0) {
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int t = 0; t < T; ++t) {
+                    const int ci = k + u + t * q;
+                    asm volatile("discard.global.L2 [%0], 128;" :: "l"(in + ci * cs) : "memory");
+                    asm volatile("discard.global.L2 [%0], 128;" :: "l"(in_b + ci * cs) : "memory");
+                }
+        }
+    }
+}
+
 template <typename R>
-__device__ void lane_fg(const LaneCtx<R>& c, int d, int m, int lb, bool is_g) {
+__device__ void lane_fg(const LaneCtx<R>& c, int d, int m, int lb, bool is_g, int chain) {
+    if constexpr (sizeof(R) == 4) if (chain) {
+        // (float only: the fixed-point passes measured 5-25% slower with
+        // chained levels, host.cu emits none for them)
+        constexpr bool HINT = true;
+        const int nc = (m >> 1) / LaneCtx<R>::VE;
+        // one chained level: 4 * U loads in flight per lane
+        if (nc >= 8) lane_fg_chain<R, 1, 4, HINT>(c, d, nc, lb, is_g);
+        else if (nc >= 4) lane_fg_chain<R, 1, 2, HINT>(c, d, nc, lb, is_g);
+        else lane_fg_chain<R, 1, 1, HINT>(c, d, nc, lb, is_g);
+        return;
+    }
     using A = Arith<R>;
     constexpr int VE = LaneCtx<R>::VE;
     constexpr int U = 32 / VE < 4 ? 32 / VE : 4;
@@ -388,6 +487,59 @@ __device__ void lane_r1_hard(const LaneCtx<R>& c, int d, int m, int lb) {
     }
 }
 
+// OP_GR1 (float): the G op at depth d whose child [lb + m/2, lb + m) is a
+// rate-1 node.  The g values stay in registers: their signs go to the
+// partial sums (rewritten by the expanded recursion if that runs) and the
+// result says whether this lane saw no zero.  The input segment is neither
+// stored to depth d + 1 nor dropped here (the plain G op still needs it when
+// some lane has a zero).
+template <typename R>
+__device__ bool lane_gr1(const LaneCtx<R>& c, int d, int m, int lb) {
+    constexpr int VE = LaneCtx<R>::VE;
+    constexpr int NB = 32 / VE; // chunks per partial-sum word
+    const int h = m >> 1, nc = h / VE;
+    int cs;
+    const R* in = c.chunk_base(d, cs);
+    const R* in_b = in + nc * cs;
+    const bool gin = c.keep > 0 && (d == 0 || (c.n >> d) > c.segmax);
+    const uint64_t pin = gin ? c.policy(d) : 0;
+    bool zero = false;
+    #pragma unroll 1
+    for (int k = 0; k < nc; k += NB) {
+        Vec<R, VE> a[NB], b[NB];
+#pragma unroll
+        for (int u = 0; u < NB; ++u) {
+            if (gin) {
+                a[u] = vld_hint<R, VE>(in + (k + u) * cs, pin);
+                b[u] = vld_hint<R, VE>(in_b + (k + u) * cs, pin);
+            } else {
+                a[u] = vld<R, VE>(in + (k + u) * cs);
+                b[u] = vld<R, VE>(in_b + (k + u) * cs);
+            }
+        }
+        const uint32_t bits = c.word((lb + k * VE) >> 5);
+        uint32_t acc = 0;
+#pragma unroll
+        for (int u = 0; u < NB; ++u) {
+            const Vec<R, VE> r = fg_compute<R, VE>(a[u], b[u], bits >> (u * VE), true);
+            zero |= vec_has_zero<R, VE>(r);
+            acc |= vec_signs<R, VE>(r) << (u * VE);
+        }
+        c.word((lb + h + k * VE) >> 5) = acc;
+    }
+    return !zero;
+}
+// the input segment of a taken OP_GR1 is dead: drop its lines from the L2
+template <typename R>
+__device__ void lane_discard_seg(const LaneCtx<R>& c, int d, int m) {
+    constexpr int VE = LaneCtx<R>::VE;
+    if (!(c.discard && d > 0 && (c.n >> d) > c.segmax) || (c.lane & 7) != 0) return;
+    int cs;
+    const R* in = c.chunk_base(d, cs);
+    #pragma unroll 1
+    for (int k = 0; k < m / VE; ++k) asm volatile("discard.global.L2 [%0], 128;" :: "l"(in + k * cs) : "memory");
+}
+
 // ---- in-register subtrees (OP_SCSUB of the lane schedule) ----------------
 // A subtree of M <= kLaneSubMax values is decoded by the unabridged SC
 // recursion of sc_decoder.hpp:99-112 on registers: the lane loads its M
@@ -494,6 +646,7 @@ __device__ void lane_frame(const LaunchParams& P, const DevCode& C, unsigned cha
     c.n = C.n;
     c.segmax = P.seg_smem_max;
     c.keep = P.sc_keep;
+    c.keep_hi = P.sc_keep_hi;
     c.discard = P.sc_discard != 0;
     c.chan = frame_llr<R>(P, frame);
     const LaneQ q0 = lane_layout(C.n, int(sizeof(R)), P.seg_smem_max, 0);
@@ -518,7 +671,7 @@ __device__ void lane_frame(const LaunchParams& P, const DevCode& C, unsigned cha
         const int code = op_code(op), d = op_depth(op), m = 1 << op_logm(op), lb = op_lb(op);
         switch (code) {
         case OP_F:
-        case OP_G: lane_fg(c, d, m, lb, code == OP_G); break;
+        case OP_G: lane_fg(c, d, m, lb, code == OP_G, int(op >> kOpChainShift) & 3); break;
         case OP_H: lane_h(c, m, lb); break;
         case OP_FROZEN: c.fill(lb, m, 0); break;
         case OP_INFO: c.fill(lb, 1, A::val(*c.chunk(d, 0)) < M(0)); break;
@@ -533,6 +686,18 @@ __device__ void lane_frame(const LaunchParams& P, const DevCode& C, unsigned cha
             case 8: lane_sub<R, 8>(c, d, lb, mask); break;
             default: lane_sub<R, 16>(c, d, lb, mask); break;
             }
+            break;
+        }
+        case OP_GR1: {
+            const int skip = int(next); // the word after OP_GR1
+            ++oi;
+            if constexpr (sizeof(R) == 4) {
+                if (__all_sync(FULL, lane_gr1(c, d, m, lb))) {
+                    lane_discard_seg(c, d, m);
+                    oi += skip;
+                } // else: the plain G op and the expanded recursion follow
+            }
+            next = __ldg(sched + oi + 1);
             break;
         }
         case OP_R1SC: {
@@ -610,8 +775,10 @@ __device__ void lane_frame(const LaunchParams& P, const DevCode& C, unsigned cha
     __syncwarp();
 }
 
+// resident blocks the register budget allows: float runs 16 warps per SM
+// (DRAM-bound), the fixed-point passes 24 (host.cu plan_lanes)
 template <typename R>
-__global__ void __launch_bounds__(128, 8) sc_lanes_kernel(const LaunchParams P) {
+__global__ void __launch_bounds__(128, sizeof(R) == 4 ? 4 : 6) sc_lanes_kernel(const LaunchParams P) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     unsigned char* sm = smem_raw + wib * P.smem_per_warp;

@@ -31,6 +31,11 @@ enum Op : uint32_t {
     OP_R1SC = 9,   // SC only: rate-1 node.  Next word = length of the expanded
                    // recursion that follows; when no input LLR is zero the
                    // recursion's result is the hard decision and it is skipped
+    OP_GR1 = 10,   // lane schedules, float: a G op whose child is a rate-1 node.
+                   // The g values are formed in registers; when none of them is
+                   // zero (in any lane) their signs are the node's decisions and
+                   // the next word's count of ops (the plain G op and the
+                   // expanded recursion) is skipped; nothing is stored
 };
 constexpr int kScSubMax = 32;
 // largest fused leaf (values held per lane): int8 / float
@@ -41,6 +46,9 @@ constexpr int kFuseMaxI8 = 8, kFuseMaxF32 = 4;
 //               the parent segment (depth - 1) with F, or with G when
 //   bit   29    is set (the F / G op of the parent is then omitted)
 constexpr uint32_t kOpFused = 1u << 28, kOpFusedG = 1u << 29;
+//   bits 28..29 (lane schedules) F / G: number of chained F ops this op
+//               computes along with its own level (host.cu fuse_lane_chains)
+constexpr int kOpChainShift = 28;
 __host__ __device__ inline uint32_t op_pack(uint32_t op, int depth, int logm, int lb) {
     return op | (uint32_t(depth) << 4) | (uint32_t(logm) << 8) | (uint32_t(lb) << 12);
 }
@@ -112,6 +120,7 @@ struct LaunchParams {
     int32_t sc_keep;           // frame-per-lane SC pass: global depth segments of <= sc_keep
                                // values are loaded / stored L2::evict_last, larger ones
                                // (and the channel) evict_first; 0 = no cache hints
+    int32_t sc_keep_hi;        // ... segments of <= sc_keep_hi values (> sc_keep) evict_normal
     int32_t sc_discard;        // frame-per-lane SC pass: discard.global.L2 the lines of a
                                // global depth segment after its last read (G op)
     int32_t list_discard;      // float list passes: the same for a frame's global depth

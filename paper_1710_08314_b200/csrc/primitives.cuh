@@ -343,9 +343,10 @@ __device__ __forceinline__ void vst(R* p, const Vec<R, G>& x) {
 }
 
 // L2 eviction-priority hints of the frame-per-lane SC pass (global memory only)
-__device__ __forceinline__ uint64_t l2_policy(bool keep) {
+__device__ __forceinline__ uint64_t l2_policy(int cls) { // 2 evict_last, 1 evict_normal, 0 evict_first
     uint64_t p;
-    if (keep) asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    if (cls == 2) asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    else if (cls == 1) asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
     else asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
