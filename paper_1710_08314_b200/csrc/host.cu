@@ -529,6 +529,14 @@ struct pl_handle {
     // 1-frame-per-warp plan for small passes (lower latency per frame); the
     // device picks one of the two launches from the pass's frame count
     std::vector<RungCfg> rungs_small;
+    // FA ladder, speculative tail: when at most spec_max frames reach the
+    // third-last rung, the last three rungs decode them side by side on
+    // three streams into a staging area and a commit kernel keeps, per
+    // frame, the first list size whose CRC passed (decoders.hpp:70-82 is a
+    // sequence of independent decodes, so the results are the same): the
+    // tail costs one frame latency instead of three.
+    std::vector<RungCfg> spec; // plans of the last three rungs, grid <= spec_max blocks
+    int spec_max = 0;          // 0 = off
     // Execution contexts: the scratch and control buffers one decode in
     // flight needs.  pl_decode uses ex[0]; pl_decode_host alternates ex[0]
     // and ex[1] on two compute streams, so one chunk's decode can fill the
@@ -547,6 +555,14 @@ struct pl_handle {
         // pl_sim_point on different streams never overlap on the scratch
         cudaEvent_t done = nullptr;
         bool issued = false;
+        // speculative tail of the FA ladder (pl_handle::spec)
+        cudaStream_t s_spec[2] = {nullptr, nullptr};
+        cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
+        void* spec_scratch[3] = {nullptr, nullptr, nullptr};
+        uint8_t* st_payload = nullptr;
+        uint8_t* st_codeword = nullptr;
+        uint8_t* st_crc = nullptr;
+        float* st_metric = nullptr;
     } ex[2];
     int64_t launches = 0;
     // live per-launch timing (pl_profile)
@@ -786,8 +802,9 @@ int fail(pl_handle* h, int code, const std::string& msg) {
 
 void run_decode(pl_handle& h, const void* llr, const int32_t* code_id, int64_t nframes,
                 uint8_t* payload, uint8_t* codeword, uint8_t* crc_ok, uint8_t* esc,
-                float* metric, cudaStream_t s, int exec = 0, const int64_t* llr_offset = nullptr,
+                float* metric, cudaStream_t s0, int exec = 0, const int64_t* llr_offset = nullptr,
                 uint32_t* lat_ns = nullptr, bool paths = false) {
+    cudaStream_t s = s0;
     ck(cudaSetDevice(h.device), "cudaSetDevice");
     h.launches = 0;
     h.prof_kind.clear(); // timed decode launches of this call (pl_last_kernel_ms)
@@ -825,10 +842,24 @@ void run_decode(pl_handle& h, const void* llr, const int32_t* code_id, int64_t n
     base.nmax = h.nmax;
     int slot = 0;
 
+    // (spec_j >= 0: speculative rung j of the ladder's tail, on its own
+    // stream and scratch, outputs staged by list position)
     auto run = [&](const RungCfg& rc, bool list, int select, const int32_t* in_list,
                    const int32_t* in_count, int32_t* out_list, int32_t* out_count,
-                   int64_t count_lo = -1, int64_t count_hi = INT64_MAX) {
+                   int64_t count_lo = -1, int64_t count_hi = INT64_MAX, int spec_j = -1) {
         plb::LaunchParams p = base;
+        cudaStream_t s = s0;
+        if (spec_j >= 0) {
+            if (spec_j > 0) s = x.s_spec[spec_j - 1];
+            const int64_t o = int64_t(spec_j) * h.spec_max;
+            p.gscratch = x.spec_scratch[spec_j];
+            p.payload = x.st_payload + o * h.pstride;
+            p.codeword = codeword ? x.st_codeword + o * h.cstride : nullptr;
+            p.crc_ok = x.st_crc + o;
+            p.metric = x.st_metric + o;
+            p.esc = nullptr;
+            p.out_by_idx = 1;
+        }
         p.count_lo = count_lo;
         p.count_hi = count_hi;
         p.work = x.d_work + slot;
@@ -898,16 +929,67 @@ void run_decode(pl_handle& h, const void* llr, const int32_t* code_id, int64_t n
 
     // an adaptive rung with a small-pass plan (pl_create): two launches
     // with complementary frame-count ranges, the device picks
+    // (lo: the pass runs only with more than lo frames; fewer went to the
+    // speculative tail)
     auto rung = [&](size_t i, const int32_t* in_list, const int32_t* in_count, int32_t* out_list,
-                    int32_t* out_count) {
+                    int32_t* out_count, int64_t lo = -1) {
         const RungCfg& sm = h.rungs_small[i];
         if (sm.grid > 0) {
             const int64_t t = sm.small_max;
-            run(sm, true, 1, in_list, in_count, out_list, out_count, -1, t);
-            run(h.rungs[i], true, 1, in_list, in_count, out_list, out_count, t, INT64_MAX);
+            if (t > lo) run(sm, true, 1, in_list, in_count, out_list, out_count, lo, t);
+            run(h.rungs[i], true, 1, in_list, in_count, out_list, out_count, std::max(t, lo), INT64_MAX);
         } else {
-            run(h.rungs[i], true, 1, in_list, in_count, out_list, out_count);
+            run(h.rungs[i], true, 1, in_list, in_count, out_list, out_count, lo, INT64_MAX);
         }
+    };
+    // the speculative tail: rungs [first, first + 3) side by side on the
+    // frames of in_list when there are at most spec_max of them
+    auto spec_tail = [&](size_t first, const int32_t* in_list, const int32_t* in_count) {
+        if (!x.s_spec[0]) {
+            for (int j = 0; j < 2; ++j) {
+                ck(cudaStreamCreateWithFlags(&x.s_spec[j], cudaStreamNonBlocking), "stream");
+                ck(cudaEventCreateWithFlags(&x.ev_join[j], cudaEventDisableTiming), "event");
+            }
+            ck(cudaEventCreateWithFlags(&x.ev_fork, cudaEventDisableTiming), "event");
+            for (int j = 0; j < 3; ++j)
+                x.spec_scratch[j] = h.dalloc<void>(size_t(h.spec[size_t(j)].gscratch_total()));
+            const size_t cap = size_t(3) * size_t(h.spec_max);
+            x.st_payload = h.dalloc<uint8_t>(cap * size_t(h.pstride));
+            x.st_codeword = h.dalloc<uint8_t>(cap * size_t(h.cstride));
+            x.st_crc = h.dalloc<uint8_t>(cap);
+            x.st_metric = h.dalloc<float>(cap * sizeof(float));
+        }
+        ck(cudaEventRecord(x.ev_fork, s0), "record");
+        for (int j = 0; j < 3; ++j) {
+            if (j > 0) ck(cudaStreamWaitEvent(x.s_spec[j - 1], x.ev_fork, 0), "wait");
+            run(h.spec[size_t(j)], true, 1, in_list, in_count, nullptr, nullptr, -1, h.spec_max, j);
+            if (j > 0) {
+                ck(cudaEventRecord(x.ev_join[j - 1], x.s_spec[j - 1]), "record");
+                ck(cudaStreamWaitEvent(s0, x.ev_join[j - 1], 0), "wait");
+            }
+        }
+        plb::CommitParams cp{};
+        cp.codes = h.d_codes;
+        cp.code_id = code_id;
+        cp.list = in_list;
+        cp.count = in_count;
+        cp.count_hi = h.spec_max;
+        cp.nst = 3;
+        cp.cap = h.spec_max;
+        for (int j = 0; j < 3; ++j) cp.levels[j] = h.spec[size_t(j)].l;
+        cp.st_payload = x.st_payload;
+        cp.st_codeword = codeword ? x.st_codeword : nullptr;
+        cp.st_crc = x.st_crc;
+        cp.st_metric = x.st_metric;
+        cp.payload = payload;
+        cp.codeword = codeword;
+        cp.crc_ok = crc_ok;
+        cp.esc = esc;
+        cp.metric = metric;
+        cp.payload_stride = h.pstride;
+        cp.codeword_stride = h.cstride;
+        ck(plb::launch_commit(cp, std::max(1, (h.spec_max + 3) / 4), s0), "commit launch");
+        ++h.launches;
     };
 
     switch (kind) {
@@ -931,10 +1013,14 @@ void run_decode(pl_handle& h, const void* llr, const int32_t* code_id, int64_t n
         bucket(h.sc_cfg);
         run(h.sc_cfg, false, 0, blist, bcount, x.d_lists[0], x.d_counts + 0);
         int cur = 0;
+        // (per-frame latency and list introspection follow the plain ladder)
+        const bool spec = h.spec_max > 0 && !lat_ns && !base.path_alive;
         for (size_t i = 0; i < h.rungs.size(); ++i) {
             const bool last = i + 1 == h.rungs.size();
+            const bool tail = spec && i + 3 == h.rungs.size();
+            if (tail) spec_tail(i, x.d_lists[cur], x.d_counts + i);
             rung(i, x.d_lists[cur], x.d_counts + i, last ? nullptr : x.d_lists[cur ^ 1],
-                 last ? nullptr : x.d_counts + i + 1);
+                 last ? nullptr : x.d_counts + i + 1, tail ? int64_t(h.spec_max) : int64_t(-1));
             cur ^= 1;
         }
         break;
@@ -1246,6 +1332,19 @@ int pl_create(const pl_code* codes, int32_t ncodes, const pl_decoder* dec, int32
             }
             h->rungs_small.push_back(sm);
         }
+        // speculative tail of the FA ladder (PLB_SPEC=0: off): the plans of
+        // the last three rungs for at most spec_max frames, one block per
+        // frame (team plans at L >= 16, warp 0 of a block in solo mode below),
+        // so that the blocks of all three are resident together
+        if (kind == PL_KIND_FA_SSCL && h->rungs.size() >= 3 && env_int("PLB_SPEC", 1)) {
+            h->spec_max = std::max(1, env_int("PLB_SPEC_MAX", h->sms / 2));
+            for (size_t i = h->rungs.size() - 3; i < h->rungs.size(); ++i) {
+                RungCfg c = h->rungs_small[i].grid > 0 ? h->rungs_small[i] : h->rungs[i];
+                if (c.fpw > 1) c = plan_rung(*h, c.l, true, true, 1);
+                c.grid = std::min(c.grid, h->spec_max);
+                h->spec.push_back(c);
+            }
+        }
         int64_t gs = 0;
         auto acc = [&](const RungCfg& r) {
             gs = std::max<int64_t>(gs, r.gscratch_total());
@@ -1283,6 +1382,11 @@ void pl_destroy(pl_handle* h) {
         if (h->ex[i].d_hist) cudaFree(h->ex[i].d_hist);
         if (h->ex[i].d_sorted) cudaFree(h->ex[i].d_sorted);
         if (h->ex[i].done) cudaEventDestroy(h->ex[i].done);
+        if (h->ex[i].ev_fork) cudaEventDestroy(h->ex[i].ev_fork);
+        for (int j = 0; j < 2; ++j) {
+            if (h->ex[i].ev_join[j]) cudaEventDestroy(h->ex[i].ev_join[j]);
+            if (h->ex[i].s_spec[j]) cudaStreamDestroy(h->ex[i].s_spec[j]);
+        }
         if (h->s_comp[i]) cudaStreamDestroy(h->s_comp[i]);
     }
     for (int i = 0; i < pl_handle::kStage; ++i) {

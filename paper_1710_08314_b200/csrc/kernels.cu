@@ -1299,7 +1299,8 @@ __host__ __device__ constexpr int kv_maxw(int kv, int sw) { return 4 * kv_l(kv) 
 
 template <typename R, int KV, int SW, bool TEAM>
 __device__ void list_frame(const LaunchParams& P, const DevCode& C, unsigned char* sm,
-                           unsigned char* gs, int frame, bool active, const Sub<SW>& sw, int segmax) {
+                           unsigned char* gs, int frame, bool active, const Sub<SW>& sw, int segmax,
+                           int oidx) {
     using A = Arith<R>;
     using M = typename A::M;
     constexpr int CW = kv_cw(KV, SW), MAXW = kv_maxw(KV, SW);
@@ -1387,7 +1388,10 @@ __device__ void list_frame(const LaunchParams& P, const DevCode& C, unsigned cha
     }
     const M pm = cx.sw.shfl(cx.metric, pick);
     if (active) {
-        write_outputs<SW>(P, C, cx.row(pick), frame, lane);
+        // (speculative rungs of the FA ladder write to a staging area indexed
+        // by the frame's position in the pass's list, LaunchParams::out_by_idx)
+        const int of = P.out_by_idx ? oidx : frame;
+        write_outputs<SW>(P, C, cx.row(pick), of, lane);
         if (P.path_alive) {
             // ListDecoder<R>::alive / metric_of (list_decoder.hpp:91-93): the
             // final list, logical slot s in lane s
@@ -1395,9 +1399,9 @@ __device__ void list_frame(const LaunchParams& P, const DevCode& C, unsigned cha
             if (lane == 0) P.path_alive[frame] = cx.alive;
         }
         if (lane == 0) {
-            if (P.crc_ok) P.crc_ok[frame] = uint8_t(crc_ok);
-            if (P.esc) P.esc[frame] = uint8_t(P.esc_level);
-            if (P.metric) P.metric[frame] = A::to_float(pm);
+            if (P.crc_ok) P.crc_ok[of] = uint8_t(crc_ok);
+            if (P.esc) P.esc[of] = uint8_t(P.esc_level);
+            if (P.metric) P.metric[of] = A::to_float(pm);
             if (P.fail_list && C.crc_width > 0 && !crc_ok) P.fail_list[atomicAdd(P.fail_count, 1)] = frame;
             if (P.lat_ns) P.lat_ns[frame] += uint32_t(gtimer());
         }
@@ -1643,7 +1647,7 @@ decode_kernel(const LaunchParams P) {
                 const int frame = P.frame_list ? P.frame_list[idx] : int(idx);
                 const int cid = P.code_id ? P.code_id[frame] : 0;
                 const DevCode C = P.codes[cid];
-                if (wib == 0) list_frame<R, KV, 32, true>(P, C, smem_raw, gs, frame, true, sw, P.seg_smem_max);
+                if (wib == 0) list_frame<R, KV, 32, true>(P, C, smem_raw, gs, frame, true, sw, P.seg_smem_max, int(idx));
                 else team_helper<R>(P, C, smem_raw, frame, wib);
             }
             return;
@@ -1684,11 +1688,11 @@ decode_kernel(const LaunchParams P) {
                 const int fj = same ? frame : __shfl_sync(FULL, frame, j * SW);
                 const int cj = same ? cid : __shfl_sync(FULL, cid, j * SW);
                 const bool aj = same ? active : (__shfl_sync(FULL, int(active), j * SW) && sw.id == 0);
-                list_frame<R, KV, SW, false>(P, P.codes[cj], sm, gs, fj, aj, sw, segmax);
+                list_frame<R, KV, SW, false>(P, P.codes[cj], sm, gs, fj, aj, sw, segmax, fj);
             }
         } else {
             const DevCode C = P.codes[cid];
-            if constexpr (KV > 0) list_frame<R, KV, SW, false>(P, C, sm, gs, frame, active, sw, segmax);
+            if constexpr (KV > 0) list_frame<R, KV, SW, false>(P, C, sm, gs, frame, active, sw, segmax, int(idx));
             else sc_frame<R>(P, C, sm, gs, frame, sw);
         }
     }
@@ -1895,6 +1899,42 @@ int occupancy_list(int precision, int l, int fpw, int smem, int wpb, bool team) 
     return precision == 0   ? occupancy<float>(kv, fpw, smem, wpb, team)
            : precision == 1 ? occupancy<int8_t>(kv, fpw, smem, wpb, team)
                             : occupancy<int16_t>(kv, fpw, smem, wpb, team);
+}
+
+// one warp per listed frame: the staged result of the lowest passing rung
+// (decoders.hpp:70-82: the first list size whose CRC passes, else the last)
+__global__ void commit_kernel(const CommitParams p) {
+    const long long count = *p.count;
+    if (count > p.count_hi) return;
+    const int lane = threadIdx.x & 31;
+    const long long w0 = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long idx = w0; idx < count; idx += nw) {
+        const int frame = p.list[idx];
+        int j = 0;
+        while (j + 1 < p.nst && !p.st_crc[(long long)j * p.cap + idx]) ++j;
+        const long long sidx = (long long)j * p.cap + idx;
+        // (the bytes write_outputs wrote: those of the frame's own code)
+        const DevCode& C = p.codes[p.code_id ? p.code_id[frame] : 0];
+        const int pb = (C.psize + 7) >> 3, cb = (C.n + 7) >> 3;
+        const uint8_t* sp = p.st_payload + sidx * p.payload_stride;
+        uint8_t* dp = p.payload + (long long)frame * p.payload_stride;
+        for (int q = lane; q < pb; q += 32) dp[q] = sp[q];
+        if (p.codeword) {
+            const uint8_t* sc = p.st_codeword + sidx * p.codeword_stride;
+            uint8_t* dc = p.codeword + (long long)frame * p.codeword_stride;
+            for (int q = lane; q < cb; q += 32) dc[q] = sc[q];
+        }
+        if (lane == 0) {
+            if (p.crc_ok) p.crc_ok[frame] = p.st_crc[sidx];
+            if (p.esc) p.esc[frame] = uint8_t(p.levels[j]);
+            if (p.metric) p.metric[frame] = p.st_metric[sidx];
+        }
+    }
+}
+cudaError_t launch_commit(const CommitParams& p, int blocks, cudaStream_t s) {
+    commit_kernel<<<blocks, 128, 0, s>>>(p);
+    return cudaGetLastError();
 }
 
 cudaError_t bucket_by_code(const int32_t* cid, int64_t n, int ncodes, int32_t* hist, int32_t* out,

@@ -130,6 +130,9 @@ struct LaunchParams {
     uint32_t* path_alive;      // nullable (pl_list_paths): alive-slot mask of the final list
     float* path_metric;        // ... and the metric of every slot, path_stride per frame
     int32_t path_stride;
+    int32_t out_by_idx;        // list passes at one frame per warp / team: outputs are indexed
+                               // by the frame's position in frame_list (staging of a
+                               // speculative FA rung), not by the frame id
 };
 
 constexpr int kMaxWarpsPerBlock = 4; // a block is 1, 2 or 4 independent warps
@@ -161,6 +164,31 @@ int occupancy_sc_lanes(int precision, int smem_bytes, int wpb);
 // launches); *count_out = n.  hist: ncodes ints of scratch.
 cudaError_t bucket_by_code(const int32_t* cid, int64_t n, int ncodes, int32_t* hist, int32_t* out,
                            int32_t* count_out, cudaStream_t s);
+// Commit of the speculative FA rungs (host.cu run_decode): for every frame
+// of `list` (positions [0, *count), only if *count <= count_hi) the staged
+// result of the first rung whose CRC passed, else of the last rung, goes to
+// the real outputs.  nst rungs; rung j staged at position idx:
+// st_payload + (j * cap + idx) * payload_stride etc.; levels[j] = its esc value.
+struct CommitParams {
+    const DevCode* codes;
+    const int32_t* code_id;     // nullable
+    const int32_t* list;
+    const int32_t* count;
+    int64_t count_hi;
+    int32_t nst, cap;
+    int32_t levels[4];
+    const uint8_t* st_payload;
+    const uint8_t* st_codeword; // nullable
+    const uint8_t* st_crc;
+    const float* st_metric;
+    uint8_t* payload;
+    uint8_t* codeword;          // nullable
+    uint8_t* crc_ok;            // nullable
+    uint8_t* esc;               // nullable
+    float* metric;              // nullable
+    int64_t payload_stride, codeword_stride;
+};
+cudaError_t launch_commit(const CommitParams& p, int blocks, cudaStream_t s);
 // Exhaustive device check of the packed int8 f/g against the scalar kernels.
 cudaError_t kernel_selftest(unsigned long long* mismatches);
 #ifdef PLB_OPTIME

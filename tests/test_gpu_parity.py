@@ -374,3 +374,69 @@ def test_alternate_kernels(P, gpu, oracle_lib, prec, monkeypatch):
             check_parity(P, gpu, code, kind, l, prec, pr, llr, f"env={env}")
         for k in env:
             monkeypatch.delenv(k)
+
+
+@pytest.mark.parametrize("prec", ["f32", "i8"])
+def test_fa_speculative_tail(P, gpu, oracle_lib, prec, monkeypatch):
+    """FA ladder, speculative tail: with at most PLB_SPEC_MAX frames at the
+    third-last rung the last three rungs decode side by side into a staging
+    area and a commit kernel keeps the first passing list size
+    (decoders.hpp:70-82).  The result is the plain ladder's, on both sides
+    of the threshold, with the codeword output, for mixed codes, and equal to
+    PLB_SPEC=0."""
+    scale = {"f32": 0.0, "i8": 4.0}[prec]  # (int16: tests/test_gpu_int16.py, test_gpu_scale_parity.py)
+    code = _code(P, 1024, 480, "32-GZIP")
+    _, llr = P.channel(code, 1.5, 9, 0, 160, prec, scale)
+    pr = P.PruningConfig()
+    outs = []
+    for env in ({}, {"PLB_SPEC_MAX": "4"}, {"PLB_SPEC_MAX": "1000"}, {"PLB_SPEC": "0"}):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        for l in (8, 32):
+            got = check_parity(P, gpu, code, "fa_sscl", l, prec, pr, llr, f"spec env={env}")
+            assert got["esc"].max() == l  # the ladder reached its last rung
+            outs.append((l, got))
+        for k in env:
+            monkeypatch.delenv(k)
+    for l, got in outs[2:]:
+        base = outs[0][1] if l == 8 else outs[1][1]
+        for key in ("payload", "codeword", "crc_ok", "esc", "metric"):
+            assert np.array_equal(got[key], base[key]), key
+
+
+def test_sc_lane_ops_with_zero_llrs(P, gpu, oracle_lib):
+    """The float SC pass decides G ops with a rate-1 child in registers
+    (OP_GR1) and chains F ops to their producer; a zero among the g values
+    of any lane sends the warp through the plain G op and the expanded
+    recursion instead.  Frames with planted zeros / equal magnitudes (g = 0)
+    and clean frames, both schedules (PLB_LANE_GR1 / PLB_LANE_CHAIN off)."""
+    import os
+
+    code = _code(P, 2048, 1723, "32-GZIP", ga=4.5)
+    _, llr = P.channel(code, 4.5, 3, 0, 96, "f32")
+    llr = llr.copy()
+    rng = np.random.default_rng(1)
+    for f in range(0, 96, 3):  # every third frame: a[i] = -+b[i] pairs and zeros
+        for _ in range(8):
+            h = 1 << rng.integers(5, 11)
+            i = int(rng.integers(0, 2048 // (2 * h))) * 2 * h + int(rng.integers(0, h))
+            llr[f, i + h] = llr[f, i] * (1 if rng.integers(2) else -1)
+        llr[f, rng.integers(0, 2048, 4)] = 0.0
+    pr = P.PruningConfig()
+    ref = None
+    for env in ({}, {"PLB_LANE_GR1": "0"}, {"PLB_LANE_CHAIN": "0"}, {"PLB_LANE_GR1": "0", "PLB_LANE_CHAIN": "0"}):
+        old = {k: os.environ.get(k) for k in env}
+        os.environ.update(env)
+        try:
+            for kind in ("ssc", "fa_sscl"):
+                got = check_parity(P, gpu, code, kind, 4 if kind == "fa_sscl" else 1, "f32", pr, llr, f"env={env}")
+                if kind == "ssc":
+                    if ref is None:
+                        ref = got
+                    assert np.array_equal(got["payload"], ref["payload"])
+        finally:
+            for k, v in old.items():
+                if v is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = v
