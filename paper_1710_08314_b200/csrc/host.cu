@@ -240,6 +240,31 @@ void emit_list(const std::vector<Node>& t, int ni, std::vector<uint32_t>& s, int
     }
 }
 
+// List schedules: an F / G op directly followed by the F op of its child
+// (the left descent) takes that F along (kOpChain; the F op is dropped) when
+// the child's output still holds whole 16-byte chunks (h / 2 >= ve values).
+void chain_list_ops(std::vector<uint32_t>& s, int ve) {
+    std::vector<uint32_t> out;
+    out.reserve(s.size());
+    for (size_t i = 0; i < s.size(); ++i) {
+        const uint32_t w = s[i];
+        const int code = plb::op_code(w);
+        const bool plain = (w & (plb::kOpFused | plb::kOpFusedG)) == 0;
+        if (plain && (code == plb::OP_F || code == plb::OP_G) && i + 1 < s.size()) {
+            const uint32_t nx = s[i + 1];
+            const int h = (1 << plb::op_logm(w)) >> 1;
+            if (plb::op_code(nx) == plb::OP_F && (nx & (plb::kOpFused | plb::kOpFusedG)) == 0 &&
+                plb::op_depth(nx) == plb::op_depth(w) + 1 && (h >> 1) >= ve) {
+                out.push_back(w | plb::kOpChain);
+                ++i;
+                continue;
+            }
+        }
+        out.push_back(w);
+    }
+    s.swap(out);
+}
+
 // a subtree of size <= 32 as one register-level SC op + its frozen mask
 void emit_scsub(int depth, int m, int lb, const uint8_t* frozen, std::vector<uint32_t>& s) {
     uint32_t mask = 0;
@@ -378,7 +403,7 @@ bool uses_pruning(int k) { return k != PL_KIND_SC && k != PL_KIND_SCL; }
 struct HostCode {
     int n = 0, k = 0, stages = 0, psize = 0, width = 0;
     std::vector<uint8_t> frozen;
-    std::vector<uint32_t> sched_list, sched_sc, sched_lane;
+    std::vector<uint32_t> sched_list, sched_list_c, sched_sc, sched_lane;
     std::vector<uint16_t> info_pos;
     std::vector<uint8_t> open_mask; // ceil(n/8): bit i of byte j = position 8j+i is open
     std::vector<uint64_t> crc_tab;
@@ -432,6 +457,12 @@ HostCode make_host_code(const pl_code& c, const pl_decoder& dec) {
     tree.reserve(size_t(2 * c.n));
     build_tree(tree, h.frozen.data(), 0, c.n, 0, pc);
     emit_list(tree, 0, h.sched_list, dec.precision == PL_I8 ? plb::kFuseMaxI8 : plb::kFuseMaxF32);
+    {
+        // chained F ops (PLB_LIST_CHAIN=0: one op per level)
+        const char* lc = std::getenv("PLB_LIST_CHAIN");
+        h.sched_list_c = h.sched_list;
+        if (dec.precision == PL_F32 && !(lc && std::atoi(lc) == 0)) chain_list_ops(h.sched_list_c, 4);
+    }
     emit_sc(tree, 0, h.sched_sc, h.frozen.data());
     // frame-per-lane SC kernel: subtrees of <= PLB_LANE_SUB values (default and
     // maximum 16) are decoded in registers (OP_SCSUB), everything else op by op
@@ -1277,6 +1308,8 @@ int pl_create(const pl_code* codes, int32_t ncodes, const pl_decoder* dec, int32
             d.sched_lane = up_sched(c.sched_lane);
             d.nops_lane = int(c.sched_lane.size());
             d.nops_list = int(c.sched_list.size());
+            d.sched_list_c = up_sched(c.sched_list_c);
+            d.nops_list_c = int(c.sched_list_c.size());
             d.nops_sc = int(c.sched_sc.size());
             d.info_pos = static_cast<const uint16_t*>(up(c.info_pos.data(), c.info_pos.size() * 2));
             d.crc_tab = c.crc_tab.empty() ? nullptr

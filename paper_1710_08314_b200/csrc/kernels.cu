@@ -256,6 +256,45 @@ __device__ __forceinline__ void fg_run(Ctx<R, SW>& cx, int d, int h, int lb, int
     }
 }
 
+// A chained op (kOpChain, float kernels with kChainKernel): the F / G op at
+// depth d and the F op of its left child in one sweep.  An item is one chunk
+// of the depth-(d+2) segment of a path: its two depth-(d+1) chunks (c and
+// c + h/2) come from four input chunks (all four loads in flight), and both
+// levels go to the buffers of the path's rank.  The child's F op (absent
+// from the chained schedule) never reads the depth-(d+1) pool back, and its
+// item loop, buffer lookups and dispatch are gone.
+template <typename R, int SW, int G>
+__device__ __forceinline__ void fg_run_chain(Ctx<R, SW>& cx, int d, int h, int lb, int na, bool is_g) {
+    const int hh = h >> 1;
+    const int cp2 = hh / G; // items per path, power of two
+    const int lg = __ffs(cp2) - 1;
+    R* const out1 = cx.pool(d + 1);
+    R* const out2 = cx.pool(d + 2);
+    R* const inp = d == 0 ? cx.channel() : cx.pool(d);
+    const int seg = cx.n >> d;
+    const int total = na << lg;
+    #pragma unroll 1
+    for (int t = cx.tt0; t < total; t += cx.tstride) {
+        const int r = t >> lg, c = (t & (cp2 - 1)) * G;
+        const int p = cx.fx->alive_list[r];
+        const R* in = d == 0 ? inp : inp + int(cx.bix()[p * 16 + d]) * seg;
+        const Vec<R, G> a0 = vld<R, G>(in + c), a1 = vld<R, G>(in + c + hh);
+        const Vec<R, G> b0 = vld<R, G>(in + h + c), b1 = vld<R, G>(in + h + c + hh);
+        uint32_t bits0 = 0, bits1 = 0;
+        if (is_g) {
+            const uint32_t* prow = cx.row(p);
+            const int pos0 = lb + c, pos1 = lb + c + hh;
+            bits0 = prow[pos0 >> 5] >> (pos0 & 31);
+            bits1 = prow[pos1 >> 5] >> (pos1 & 31);
+        }
+        const Vec<R, G> r0 = fg_compute<R, G>(a0, b0, bits0, is_g);
+        const Vec<R, G> r1 = fg_compute<R, G>(a1, b1, bits1, is_g);
+        vst<R, G>(out1 + r * h + c, r0);
+        vst<R, G>(out1 + r * h + c + hh, r1);
+        vst<R, G>(out2 + r * hh + c, fg_compute<R, G>(r0, r1, 0u, false));
+    }
+}
+
 // U items per lane in flight (all loads issued before the first compute):
 // the L = 32 float kernel waits on L2 / DRAM for its depth pools, and one
 // item per trip leaves a single load pair in flight per lane
@@ -297,10 +336,17 @@ __device__ __forceinline__ void fg_run_batched(Ctx<R, SW>& cx, int d, int h, int
 #ifndef PLB_FG_UNROLL_MINKV
 #define PLB_FG_UNROLL_MINKV 6
 #endif
-template <int UB = 1, typename R, int SW>
-__device__ __forceinline__ void fg_elems(Ctx<R, SW>& cx, int d, int m, int lb, int na, bool is_g) {
+template <int UB = 1, bool CHK = false, typename R, int SW>
+__device__ __forceinline__ void fg_elems(Ctx<R, SW>& cx, int d, int m, int lb, int na, bool is_g,
+                                         bool chain = false) {
     constexpr int VE = 16 / int(sizeof(R));
     const int h = m >> 1;
+    if constexpr (CHK) {
+        if (chain) { // (host.cu chain_list_ops: h >= 2 * VE)
+            fg_run_chain<R, SW, VE>(cx, d, h, lb, na, is_g);
+            return;
+        }
+    }
     if constexpr (UB > 1) {
         if (h >= VE) {
             fg_run_batched<R, SW, VE, UB>(cx, d, h, lb, na, is_g);
@@ -320,12 +366,16 @@ __device__ __forceinline__ void team_sync(const Ctx<R, SW>& cx) {
     else __syncwarp();
 }
 
-template <int UB = 1, typename R, int SW>
-__device__ void op_fg(Ctx<R, SW>& cx, int d, int m, int lb, int na, bool is_g) {
+template <int UB = 1, bool CHK = false, typename R, int SW>
+__device__ void op_fg(Ctx<R, SW>& cx, int d, int m, int lb, int na, bool is_g, bool chain = false) {
     // the child segment of the path of rank r goes to buffer r (see header)
-    if (cx.is_alive()) cx.bix()[cx.lane * 16 + d + 1] = uint8_t(cx.myrank);
+    if (cx.is_alive()) {
+        cx.bix()[cx.lane * 16 + d + 1] = uint8_t(cx.myrank);
+        if constexpr (CHK)
+            if (chain) cx.bix()[cx.lane * 16 + d + 2] = uint8_t(cx.myrank);
+    }
     if (cx.team > 1) __syncthreads();
-    fg_elems<UB>(cx, d, m, lb, na, is_g);
+    fg_elems<UB, CHK>(cx, d, m, lb, na, is_g, chain);
     team_sync(cx);
     if constexpr (sizeof(R) == 4 && SW == 32) {
         // after a G op the depth-d pool is dead (its next use is a write by
@@ -1294,6 +1344,16 @@ __device__ void setup_ctx(Ctx<R, SW>& cx, const LaunchParams& P, const DevCode& 
 // SW lanes: candidates per lane CW = ceil(4L / SW) and the widest ranking
 // network MAXW = min(SW, 4L).
 __host__ __device__ constexpr int kv_l(int kv) { return 1 << (kv - 1); }
+// Float kernels that decode the chained schedule (DevCode::sched_list_c):
+// those with register room for the chained loop's four loads in flight --
+// the sub-warp kernels (L <= 8 at 2 / 4 frames per warp) and L = 32 (128
+// registers).  The 32-lane kernels at L <= 16 spill with it (cfg4 L=16
+// -1.5%) and keep the plain schedule and code.
+#ifndef PLB_CHAIN_KERNELS
+#define PLB_CHAIN_KERNELS 1
+#endif
+template <typename R, int KV, int SW>
+constexpr bool kChainKernel = PLB_CHAIN_KERNELS && sizeof(R) == 4 && (KV == 6 || SW < 32);
 __host__ __device__ constexpr int kv_cw(int kv, int sw) { return (4 * kv_l(kv) + sw - 1) / sw; }
 __host__ __device__ constexpr int kv_maxw(int kv, int sw) { return 4 * kv_l(kv) < sw ? 4 * kv_l(kv) : sw; }
 
@@ -1310,8 +1370,9 @@ __device__ void list_frame(const LaunchParams& P, const DevCode& C, unsigned cha
     Ctx<R, SW> cx;
     setup_ctx<TEAM>(cx, P, C, sm, gs, frame, sw, kv_l(KV), segmax); // P.l == kv_l(KV)
     const int lane = cx.lane;
-    const uint32_t* sched = C.sched_list;
-    const int nops = C.nops_list;
+    constexpr bool CHK = kChainKernel<R, KV, SW>;
+    const uint32_t* sched = CHK ? C.sched_list_c : C.sched_list;
+    const int nops = CHK ? C.nops_list_c : C.nops_list;
     #pragma unroll 1
     for (int oi = 0; oi < nops; ++oi) {
 #ifdef PLB_OPTIME
@@ -1322,7 +1383,7 @@ __device__ void list_frame(const LaunchParams& P, const DevCode& C, unsigned cha
         const int na = __popc(cx.alive);
         const bool fused = (op & kOpFused) != 0;
         if (fused) fused_leaf(cx, code, d, m, lb, na, (op & kOpFusedG) != 0);
-        if (code <= OP_G) op_fg<(sizeof(R) == 4 && KV >= PLB_FG_UNROLL_MINKV) ? PLB_FG_UNROLL : 1>(cx, d, m, lb, na, code == OP_G);
+        if (code <= OP_G) op_fg<(sizeof(R) == 4 && KV >= PLB_FG_UNROLL_MINKV) ? PLB_FG_UNROLL : 1, CHK>(cx, d, m, lb, na, code == OP_G, CHK && (op & kOpChain) != 0);
         else if (code == OP_H) op_h(cx, m, lb, na);
         else if (code == OP_FROZEN) {
             if (!fused) list_frozen<(sizeof(R) == 4 && KV >= PLB_VLEAF_MINKV)>(cx, d, m, lb, na);
@@ -1576,7 +1637,7 @@ __device__ void sc_frame(const LaunchParams& P, const DevCode& C, unsigned char*
 // same two block barriers op_fg / op_h place around them.  All path
 // bookkeeping stays with warp 0; the helpers read the alive list it
 // publishes in shared memory.
-template <typename R>
+template <typename R, int KV>
 __device__ void team_helper(const LaunchParams& P, const DevCode& C, unsigned char* sm,
                             int frame, int wib) {
     Ctx<R, 32> cx;
@@ -1591,8 +1652,9 @@ __device__ void team_helper(const LaunchParams& P, const DevCode& C, unsigned ch
     cx.team = P.team;
     cx.tt0 = wib * 32 + cx.lane;
     cx.tstride = 32 * P.team;
-    const uint32_t* sched = C.sched_list;
-    const int nops = C.nops_list;
+    constexpr bool CHK = kChainKernel<R, KV, 32>;
+    const uint32_t* sched = CHK ? C.sched_list_c : C.sched_list;
+    const int nops = CHK ? C.nops_list_c : C.nops_list;
     #pragma unroll 1
     for (int oi = 0; oi < nops; ++oi) {
         const uint32_t op = __ldg(sched + oi);
@@ -1602,7 +1664,7 @@ __device__ void team_helper(const LaunchParams& P, const DevCode& C, unsigned ch
         __syncthreads();
         const int na = __popc(cx.fx->alive_w);
         if (code == OP_H) h_elems(cx, m, lb, na);
-        else fg_elems(cx, d, m, lb, na, code == OP_G);
+        else fg_elems<1, CHK>(cx, d, m, lb, na, code == OP_G, CHK && (op & kOpChain) != 0);
         __syncthreads();
     }
 }
@@ -1648,7 +1710,7 @@ decode_kernel(const LaunchParams P) {
                 const int cid = P.code_id ? P.code_id[frame] : 0;
                 const DevCode C = P.codes[cid];
                 if (wib == 0) list_frame<R, KV, 32, true>(P, C, smem_raw, gs, frame, true, sw, P.seg_smem_max, int(idx));
-                else team_helper<R>(P, C, smem_raw, frame, wib);
+                else team_helper<R, KV>(P, C, smem_raw, frame, wib);
             }
             return;
         }

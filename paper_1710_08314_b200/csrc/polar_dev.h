@@ -46,6 +46,10 @@ constexpr int kFuseMaxI8 = 8, kFuseMaxF32 = 4;
 //               the parent segment (depth - 1) with F, or with G when
 //   bit   29    is set (the F / G op of the parent is then omitted)
 constexpr uint32_t kOpFused = 1u << 28, kOpFusedG = 1u << 29;
+//   bit   30    (list schedules) F / G op chained with the F op of its child:
+//               both levels are computed in one sweep and stored, the child's
+//               F op (dropped from the schedule) never reads its input back
+constexpr uint32_t kOpChain = 1u << 30;
 //   bits 28..29 (lane schedules) F / G: number of chained F ops this op
 //               computes along with its own level (host.cu fuse_lane_chains)
 constexpr int kOpChainShift = 28;
@@ -63,7 +67,10 @@ struct DevCode {
     const uint32_t* sched_list; // list-decoder schedule (pruned or full tree)
     const uint32_t* sched_sc;   // SC-rung schedule (R1/SPC expanded)
     const uint32_t* sched_lane; // the same without OP_SCSUB (frame-per-lane SC kernel)
-    int32_t nops_list, nops_sc, nops_lane, pad2;
+    int32_t nops_list, nops_sc, nops_lane, nops_list_c;
+    const uint32_t* sched_list_c; // list schedule with chained F ops (kOpChain): the float
+                                  // kernels with register room for the chained loop read
+                                  // this one (kernels.cu kChainKernel), the others sched_list
     const uint16_t* info_pos;   // psize open positions, ascending
     // CRC as an affine map over the decided codeword:
     // syndrome = crc_c0 ^ XOR_j crc_tab[j][byte_j(codeword)], zero <=> pass.
