@@ -487,7 +487,7 @@ __device__ void lane_r1_hard(const LaneCtx<R>& c, int d, int m, int lb) {
     }
 }
 
-// OP_GR1 (float): the G op at depth d whose child [lb + m/2, lb + m) is a
+// OP_GR1: the G op at depth d whose child [lb + m/2, lb + m) is a
 // rate-1 node.  The g values stay in registers: their signs go to the
 // partial sums (rewritten by the expanded recursion if that runs) and the
 // result says whether this lane saw no zero.  The input segment is neither
@@ -691,19 +691,25 @@ __device__ void lane_frame(const LaunchParams& P, const DevCode& C, unsigned cha
         case OP_GR1: {
             const int skip = int(next); // the word after OP_GR1
             ++oi;
-            if constexpr (sizeof(R) == 4) {
-                if (__all_sync(FULL, lane_gr1(c, d, m, lb))) {
-                    lane_discard_seg(c, d, m);
-                    oi += skip;
-                } // else: the plain G op and the expanded recursion follow
-            }
+            if (__all_sync(FULL, lane_gr1(c, d, m, lb))) {
+                lane_discard_seg(c, d, m);
+                oi += skip;
+            } // else: the plain G op and the expanded recursion follow
             next = __ldg(sched + oi + 1);
             break;
         }
         case OP_R1SC: {
             const int skip = int(next); // the word after OP_R1SC
             ++oi;
-            if (__all_sync(FULL, lane_r1_nozero(c, d, m))) {
+            const bool r1ok = __all_sync(FULL, lane_r1_nozero(c, d, m));
+#ifdef PLB_OPTIME
+            // (profiling build) rate-1 shortcut attempts / successes per node size
+            if (lane == 0) {
+                atomicAdd(&g_optime[op_logm(op)], 1ull);
+                if (r1ok) atomicAdd(&g_optime[32 + op_logm(op)], 1ull);
+            }
+#endif
+            if (r1ok) {
                 lane_r1_hard(c, d, m, lb);
                 oi += skip;
             } // else: every lane runs the expanded recursion that follows
@@ -713,15 +719,31 @@ __device__ void lane_frame(const LaunchParams& P, const DevCode& C, unsigned cha
         default: break;
         }
     }
-    // finish: CRC syndrome, payload, codeword, status (per lane)
+    // finish: CRC syndrome, payload, codeword, status (per lane).  Codes of
+    // n >= 32 go word by word: the four table lookups of a partial-sum word
+    // are independent loads (two words per trip: eight in flight), and the
+    // outputs leave as 32-bit stores where the rows are 4-byte aligned (one
+    // byte store per payload byte is a partial-sector write each).
     int crc_ok = 0;
+    const int nwords = C.n >> 5;
     if (C.crc_width > 0) {
         uint64_t syn = C.crc_c0;
-        const int nbytes = (C.n + 7) >> 3;
-        #pragma unroll 1
-        for (int j = 0; j < nbytes; ++j) {
-            const uint32_t byte = (c.word(j >> 2) >> ((j & 3) * 8)) & 0xffu;
-            syn ^= __ldg(C.crc_tab + (size_t(j) << 8) + byte);
+        if (nwords > 0) {
+            #pragma unroll 2
+            for (int w = 0; w < nwords; ++w) {
+                const uint32_t x = c.word(w);
+                const uint64_t* t = C.crc_tab + (size_t(w) << 10);
+                const uint64_t t0 = __ldg(t + (x & 0xffu)), t1 = __ldg(t + 256 + ((x >> 8) & 0xffu));
+                const uint64_t t2 = __ldg(t + 512 + ((x >> 16) & 0xffu)), t3 = __ldg(t + 768 + (x >> 24));
+                syn ^= (t0 ^ t1) ^ (t2 ^ t3);
+            }
+        } else {
+            const int nbytes = (C.n + 7) >> 3;
+            #pragma unroll 1
+            for (int j = 0; j < nbytes; ++j) {
+                const uint32_t byte = (c.word(j >> 2) >> ((j & 3) * 8)) & 0xffu;
+                syn ^= __ldg(C.crc_tab + (size_t(j) << 8) + byte);
+            }
         }
         crc_ok = syn == 0;
     }
@@ -730,32 +752,67 @@ __device__ void lane_frame(const LaunchParams& P, const DevCode& C, unsigned cha
         // each codeword byte compacted by table (all-open bytes: a bit
         // reversal) and streamed out MSB-first
         uint8_t* pay = P.payload + int64_t(frame) * P.payload_stride;
-        const int cbytes = (C.n + 7) >> 3;
-        uint32_t acc = 0;
+        const bool al4 = ((reinterpret_cast<uintptr_t>(P.payload) | uintptr_t(P.payload_stride)) & 3u) == 0;
+        uint32_t acc = 0, ow = 0;
         int nb = 0, qb = 0;
-        #pragma unroll 1
-        for (int j = 0; j < cbytes; ++j) {
-            const uint32_t m = __ldg(C.open_mask + j);
-            if (m == 0u) continue; // uniform: one code per warp
-            const uint32_t v = (c.word(j >> 2) >> ((j & 3) * 8)) & 0xffu;
+        // byte qb of the row: through a 32-bit word when the row is aligned
+        auto emit = [&](uint32_t byte) {
+            if (al4) {
+                ow |= byte << ((qb & 3) * 8);
+                if ((qb & 3) == 3) {
+                    *reinterpret_cast<uint32_t*>(pay + (qb & ~3)) = ow;
+                    ow = 0;
+                }
+            } else {
+                pay[qb] = uint8_t(byte);
+            }
+            ++qb;
+        };
+        auto take = [&](uint32_t m, uint32_t v) {
+            if (m == 0u) return; // uniform: one code per warp
             const uint32_t bits = m == 0xffu ? __brev(v) >> 24 : uint32_t(__ldg(C.comp_tab + (m << 8) + v));
             const int k = __popc(m);
             acc = (acc << k) | bits;
             nb += k;
             if (nb >= 8) {
                 nb -= 8;
-                pay[qb++] = uint8_t(acc >> nb);
+                emit((acc >> nb) & 0xffu);
             }
+        };
+        if (nwords > 0) {
+            const uint32_t* om = reinterpret_cast<const uint32_t*>(C.open_mask); // (uploads are 16-byte aligned)
+            #pragma unroll 1
+            for (int w = 0; w < nwords; ++w) {
+                const uint32_t mm = __ldg(om + w), x = c.word(w);
+#pragma unroll
+                for (int b = 0; b < 4; ++b) take((mm >> (8 * b)) & 0xffu, (x >> (8 * b)) & 0xffu);
+            }
+        } else {
+            const int cbytes = (C.n + 7) >> 3;
+            #pragma unroll 1
+            for (int j = 0; j < cbytes; ++j)
+                take(__ldg(C.open_mask + j), (c.word(j >> 2) >> ((j & 3) * 8)) & 0xffu);
         }
-        if (nb > 0) pay[qb] = uint8_t(acc << (8 - nb));
+        if (nb > 0) emit((acc << (8 - nb)) & 0xffu);
+        if (al4 && (qb & 3) != 0) {
+#pragma unroll 1
+            for (int b = 0; b < (qb & 3); ++b) pay[(qb & ~3) + b] = uint8_t(ow >> (8 * b));
+        }
         if (P.codeword) {
             uint8_t* cw = P.codeword + int64_t(frame) * P.codeword_stride;
-            const int cb = (C.n + 7) >> 3;
-            #pragma unroll 1
-            for (int qb = 0; qb < cb; ++qb) {
-                const uint32_t bits = (c.word(qb >> 2) >> ((qb & 3) * 8)) & 0xffu;
-                const uint32_t byte = __brev(bits) >> 24;
-                cw[qb] = uint8_t(C.n >= 8 ? byte : (byte & (0xffu << (8 - C.n))));
+            const bool cal4 = ((reinterpret_cast<uintptr_t>(P.codeword) | uintptr_t(P.codeword_stride)) & 3u) == 0;
+            if (nwords > 0 && cal4) {
+                #pragma unroll 1
+                for (int w = 0; w < nwords; ++w) // bits reversed inside every byte, byte order kept
+                    reinterpret_cast<uint32_t*>(cw)[w] = __byte_perm(__brev(c.word(w)), 0u, 0x0123u);
+            } else {
+                const int cb = (C.n + 7) >> 3;
+                #pragma unroll 1
+                for (int qb2 = 0; qb2 < cb; ++qb2) {
+                    const uint32_t bits = (c.word(qb2 >> 2) >> ((qb2 & 3) * 8)) & 0xffu;
+                    const uint32_t byte = __brev(bits) >> 24;
+                    cw[qb2] = uint8_t(C.n >= 8 ? byte : (byte & (0xffu << (8 - C.n))));
+                }
             }
         }
         if (P.crc_ok) P.crc_ok[frame] = uint8_t(crc_ok);

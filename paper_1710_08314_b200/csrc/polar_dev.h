@@ -31,7 +31,7 @@ enum Op : uint32_t {
     OP_R1SC = 9,   // SC only: rate-1 node.  Next word = length of the expanded
                    // recursion that follows; when no input LLR is zero the
                    // recursion's result is the hard decision and it is skipped
-    OP_GR1 = 10,   // lane schedules, float: a G op whose child is a rate-1 node.
+    OP_GR1 = 10,   // lane schedules: a G op whose child is a rate-1 node.
                    // The g values are formed in registers; when none of them is
                    // zero (in any lane) their signs are the node's decisions and
                    // the next word's count of ops (the plain G op and the
