@@ -683,10 +683,14 @@ RungCfg plan_team(const pl_handle& h, int l, int team, const std::vector<int>& c
 
 // The frame-per-lane SC pass: 32 frames per warp; the most shared-memory
 // resident layout that keeps PLB_LANE_WARPS warps per SM (measured best:
-// 16 for float, whose pass is DRAM-bound; 24 for int8 / int16 — FA@4.5 dB
-// int8 SC pass 12.6 -> 10.8 ms, int16 17.8 -> 16.4 ms).
+// 12 for float, whose pass is DRAM-bound -- 16 until the pass stopped
+// storing rate-1 inputs and chained its F ops: then fewer frames in flight
+// (less depth-pool state than the L2 holds) won, 14.2 -> 13.6 ms per 2^20
+// frames, 10 / 12 alike, 8: 14.6; int16, DRAM-bound too (46 KB per frame),
+// likewise: 12 warps with segments <= 64 in shared memory 9.8 ms, 16 / 24
+// warps 11.4 / 12.3; int8 is flat from 20 to 32 and keeps 24).
 RungCfg plan_lanes(const pl_handle& h) {
-    const int target = std::max(1, env_int("PLB_LANE_WARPS", h.dec.precision == PL_F32 ? 16 : 24));
+    const int target = std::max(1, env_int("PLB_LANE_WARPS", h.dec.precision == PL_I8 ? 24 : 12));
     const int forced = env_int("PLB_SEGMAX", 0);
     std::vector<int> cands;
     if (forced) cands.push_back(forced);

@@ -126,6 +126,12 @@ __device__ __forceinline__ bool vec_has_zero(const Vec<R, G>& x) {
     }
 }
 
+#ifndef PLB_LANE_U
+#define PLB_LANE_U 4 // float: chunks per trip of the plain F / G loop
+#endif
+#ifndef PLB_LANE_MINB
+#define PLB_LANE_MINB 4 // float: resident 4-warp blocks the register budget allows
+#endif
 // U chunks per iteration: 2U loads in flight per lane (the pools of the
 // upper depths live in global memory), U * VE <= 32 partial-sum bits.
 // HIN / HOUT: the input / output depth is in global memory and takes an L2
@@ -293,7 +299,7 @@ __device__ void lane_fg(const LaneCtx<R>& c, int d, int m, int lb, bool is_g, in
     }
     using A = Arith<R>;
     constexpr int VE = LaneCtx<R>::VE;
-    constexpr int U = 32 / VE < 4 ? 32 / VE : 4;
+    constexpr int U = sizeof(R) == 4 ? PLB_LANE_U : (32 / VE < 4 ? 32 / VE : 4);
     const int h = m >> 1;
     R* const out = c.pool(d + 1);
     if (h >= VE) {
@@ -835,7 +841,7 @@ __device__ void lane_frame(const LaunchParams& P, const DevCode& C, unsigned cha
 // resident blocks the register budget allows: float runs 16 warps per SM
 // (DRAM-bound), the fixed-point passes 24 (host.cu plan_lanes)
 template <typename R>
-__global__ void __launch_bounds__(128, sizeof(R) == 4 ? 4 : 6) sc_lanes_kernel(const LaunchParams P) {
+__global__ void __launch_bounds__(128, sizeof(R) == 4 ? PLB_LANE_MINB : 6) sc_lanes_kernel(const LaunchParams P) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     unsigned char* sm = smem_raw + wib * P.smem_per_warp;

@@ -14,9 +14,9 @@ M=$M,sm__warps_active.avg.pct_of_peak_sustained_active
 mkdir -p gpurun_out
 for w in $WLS; do
   # the first decode of the process: a CA decode is one launch; FA: the SC
-  # pass and two launches per list rung (its small-pass launch and its
+  # pass two launches per list rung (its small-pass launch and its
   # regular one, of which only one decodes)
-  timeout 900 ncu --metrics $M --clock-control none -k regex:"decode_kernel|sc_lanes_kernel" -c 11 --csv \
+  timeout 900 ncu --metrics $M --clock-control none -k regex:"decode_kernel|sc_lanes_kernel" -c 14 --csv \
     --log-file gpurun_out/ncu_$w.csv python bench.py --workload $w --steps 1 --warmup 0 --no-cpu --e2e-steps 1 --extra none \
     > gpurun_out/ncu_$w.log 2>&1
   echo "$w exit=$?"
