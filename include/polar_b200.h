@@ -29,8 +29,12 @@
  * use one handle per host thread.  Calls on one handle may use different
  * streams: each decode waits (cudaStreamWaitEvent) for the previous decode
  * that used the same scratch, so they serialise on the device instead of
- * racing.  Decodes that should overlap need one handle each.  There is no CPU fallback: every
- * decode runs the sm_100a kernels or fails with PL_ERR_CUDA.
+ * racing.  Decodes that should overlap need one handle each.  A fully
+ * adaptive decode may run the last rungs of its ladder on two internal
+ * streams of the handle (forked from and joined back into `stream` with
+ * events), so work queued on `stream` after the call still sees complete
+ * outputs.  There is no CPU fallback: every decode runs the sm_100a kernels
+ * or fails with PL_ERR_CUDA.
  */
 #ifndef POLAR_B200_H
 #define POLAR_B200_H

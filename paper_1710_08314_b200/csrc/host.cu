@@ -829,6 +829,22 @@ void ensure_exec(pl_handle& h, int e) {
     x.d_work = h.dalloc<unsigned long long>(16 * sizeof(unsigned long long));
     x.d_counts = h.dalloc<int32_t>(16 * sizeof(int32_t));
     ck(cudaEventCreateWithFlags(&x.done, cudaEventDisableTiming), "event");
+    if (h.spec_max > 0) {
+        // the speculative ladder tail: two side streams, the scratch of its
+        // three concurrent passes and the staging area of their outputs
+        for (int j = 0; j < 2; ++j) {
+            ck(cudaStreamCreateWithFlags(&x.s_spec[j], cudaStreamNonBlocking), "stream");
+            ck(cudaEventCreateWithFlags(&x.ev_join[j], cudaEventDisableTiming), "event");
+        }
+        ck(cudaEventCreateWithFlags(&x.ev_fork, cudaEventDisableTiming), "event");
+        for (int j = 0; j < 3; ++j)
+            x.spec_scratch[j] = h.dalloc<void>(size_t(h.spec[size_t(j)].gscratch_total()));
+        const size_t cap = size_t(3) * size_t(h.spec_max);
+        x.st_payload = h.dalloc<uint8_t>(cap * size_t(h.pstride));
+        x.st_codeword = h.dalloc<uint8_t>(cap * size_t(h.cstride));
+        x.st_crc = h.dalloc<uint8_t>(cap);
+        x.st_metric = h.dalloc<float>(cap * sizeof(float));
+    }
 }
 
 int fail(pl_handle* h, int code, const std::string& msg) {
@@ -982,20 +998,6 @@ void run_decode(pl_handle& h, const void* llr, const int32_t* code_id, int64_t n
     // the speculative tail: rungs [first, first + 3) side by side on the
     // frames of in_list when there are at most spec_max of them
     auto spec_tail = [&](size_t first, const int32_t* in_list, const int32_t* in_count) {
-        if (!x.s_spec[0]) {
-            for (int j = 0; j < 2; ++j) {
-                ck(cudaStreamCreateWithFlags(&x.s_spec[j], cudaStreamNonBlocking), "stream");
-                ck(cudaEventCreateWithFlags(&x.ev_join[j], cudaEventDisableTiming), "event");
-            }
-            ck(cudaEventCreateWithFlags(&x.ev_fork, cudaEventDisableTiming), "event");
-            for (int j = 0; j < 3; ++j)
-                x.spec_scratch[j] = h.dalloc<void>(size_t(h.spec[size_t(j)].gscratch_total()));
-            const size_t cap = size_t(3) * size_t(h.spec_max);
-            x.st_payload = h.dalloc<uint8_t>(cap * size_t(h.pstride));
-            x.st_codeword = h.dalloc<uint8_t>(cap * size_t(h.cstride));
-            x.st_crc = h.dalloc<uint8_t>(cap);
-            x.st_metric = h.dalloc<float>(cap * sizeof(float));
-        }
         ck(cudaEventRecord(x.ev_fork, s0), "record");
         for (int j = 0; j < 3; ++j) {
             if (j > 0) ck(cudaStreamWaitEvent(x.s_spec[j - 1], x.ev_fork, 0), "wait");

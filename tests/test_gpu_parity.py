@@ -231,7 +231,7 @@ def test_gpu_ml_on_tiny_code(P, gpu):
             assert met[f] == best
 
 
-def test_cfg3_mixed_codes_one_batch(P, gpu, oracle_lib):
+def test_cfg3_mixed_codes_one_batch(P, gpu, oracle_lib, monkeypatch):
     """Mixed-MCS: 31 codes (N 128..1024, CRC-11/24) in one batch with a
     per-frame code id; every frame equals the oracle of its own code."""
     from paper_1710_08314_b200.workload import MixedWorkload, make_batch
@@ -240,9 +240,15 @@ def test_cfg3_mixed_codes_one_batch(P, gpu, oracle_lib):
     codes, cid, info, ks, llr = make_batch(wl, 0, 1024)
     assert len(codes) == 31 and len(set(cid.tolist())) == 31
     # CA at L=8 and SSCL at L=2 run several frames per warp (frames bucketed
-    # by code); SSC and FA's first pass run the frame-per-lane SC kernel
-    for kind, l in [("ca_sscl", 8), ("sscl", 2), ("ssc", 1), ("fa_sscl", 8)]:
+    # by code); SSC and FA's first pass run the frame-per-lane SC kernel; the
+    # last FA case forces the speculative ladder tail (its commit kernel
+    # copies each frame's own code's byte counts)
+    for kind, l, spec_max in [("ca_sscl", 8, None), ("sscl", 2, None), ("ssc", 1, None), ("fa_sscl", 8, None),
+                              ("fa_sscl", 8, "2000"), ("fa_sscl", 32, "2000")]:
+        if spec_max:
+            monkeypatch.setenv("PLB_SPEC_MAX", spec_max)
         dec = P.FrameDecoder(codes, kind, l, "f32", P.PruningConfig())
+        monkeypatch.delenv("PLB_SPEC_MAX", raising=False)
         o = dec.decode_batch(gpu.from_numpy(llr).cuda(), code_id=gpu.from_numpy(cid).cuda(), codeword=True)
         gpu.cuda.synchronize()
         got = {k: v.cpu().numpy() for k, v in o.items() if v is not None}
