@@ -206,28 +206,33 @@ int ilog2i(int v) {
 // most fuse_max values replaces its parent's F (G) op: the leaf op computes
 // its LLRs in registers (kOpFused), which skips a round trip through the
 // depth pool and an op.
-void emit_list(const std::vector<Node>& t, int ni, std::vector<uint32_t>& s, int fuse_max) {
+// big_r1: rate-1 / single-parity right children of any larger size are
+// fused with the parent's G op as well (r1spc_stats forms their LLRs from the
+// parent segment; 0 = off).
+void emit_list(const std::vector<Node>& t, int ni, std::vector<uint32_t>& s, int fuse_max, bool big_r1) {
     const Node& nd = t[size_t(ni)];
     const int lg = ilog2i(nd.size);
-    auto fusable = [&](int ci) {
+    auto fusable = [&](int ci, bool right = false) {
         const Node& c = t[size_t(ci)];
-        return c.kind != NK_BRANCH && c.size <= fuse_max;
+        if (c.kind == NK_BRANCH) return false;
+        if (c.size <= fuse_max) return true;
+        return right && big_r1 && (c.kind == NK_R1 || c.kind == NK_SPC);
     };
     switch (nd.kind) {
     case NK_BRANCH:
         if (fusable(nd.left)) {
-            emit_list(t, nd.left, s, fuse_max);
+            emit_list(t, nd.left, s, fuse_max, big_r1);
             s.back() |= plb::kOpFused;
         } else {
             s.push_back(plb::op_pack(plb::OP_F, nd.depth, lg, nd.lb));
-            emit_list(t, nd.left, s, fuse_max);
+            emit_list(t, nd.left, s, fuse_max, big_r1);
         }
-        if (fusable(nd.right)) {
-            emit_list(t, nd.right, s, fuse_max);
+        if (fusable(nd.right, true)) {
+            emit_list(t, nd.right, s, fuse_max, big_r1);
             s.back() |= plb::kOpFused | plb::kOpFusedG;
         } else {
             s.push_back(plb::op_pack(plb::OP_G, nd.depth, lg, nd.lb));
-            emit_list(t, nd.right, s, fuse_max);
+            emit_list(t, nd.right, s, fuse_max, big_r1);
         }
         s.push_back(plb::op_pack(plb::OP_H, nd.depth, lg, nd.lb));
         break;
@@ -403,7 +408,7 @@ bool uses_pruning(int k) { return k != PL_KIND_SC && k != PL_KIND_SCL; }
 struct HostCode {
     int n = 0, k = 0, stages = 0, psize = 0, width = 0;
     std::vector<uint8_t> frozen;
-    std::vector<uint32_t> sched_list, sched_list_c, sched_sc, sched_lane;
+    std::vector<uint32_t> sched_list, sched_listv[4], sched_sc, sched_lane; // (DevCode::sched_listv)
     std::vector<uint16_t> info_pos;
     std::vector<uint8_t> open_mask; // ceil(n/8): bit i of byte j = position 8j+i is open
     std::vector<uint64_t> crc_tab;
@@ -456,12 +461,22 @@ HostCode make_host_code(const pl_code& c, const pl_decoder& dec) {
     std::vector<Node> tree;
     tree.reserve(size_t(2 * c.n));
     build_tree(tree, h.frozen.data(), 0, c.n, 0, pc);
-    emit_list(tree, 0, h.sched_list, dec.precision == PL_I8 ? plb::kFuseMaxI8 : plb::kFuseMaxF32);
     {
-        // chained F ops (PLB_LIST_CHAIN=0: one op per level)
+        // list-schedule variants (DevCode::sched_listv): big fused leaves
+        // (PLB_FUSE_BIG=0: off) and, float, chained F ops (PLB_LIST_CHAIN=0:
+        // one op per level)
+        const char* fb = std::getenv("PLB_FUSE_BIG");
+        const bool big_r1 = fb ? std::atoi(fb) != 0 : true;
         const char* lc = std::getenv("PLB_LIST_CHAIN");
-        h.sched_list_c = h.sched_list;
-        if (dec.precision == PL_F32 && !(lc && std::atoi(lc) == 0)) chain_list_ops(h.sched_list_c, 4);
+        const bool chain = dec.precision == PL_F32 && !(lc && std::atoi(lc) == 0);
+        const int fm = dec.precision == PL_I8 ? plb::kFuseMaxI8 : plb::kFuseMaxF32;
+        emit_list(tree, 0, h.sched_listv[0], fm, big_r1);
+        emit_list(tree, 0, h.sched_listv[1], fm, false);
+        h.sched_list = h.sched_listv[0];
+        for (int v = 0; v < 2; ++v) {
+            h.sched_listv[2 + v] = h.sched_listv[v];
+            if (chain) chain_list_ops(h.sched_listv[2 + v], 4);
+        }
     }
     emit_sc(tree, 0, h.sched_sc, h.frozen.data());
     // frame-per-lane SC kernel: subtrees of <= PLB_LANE_SUB values (default and
@@ -1316,8 +1331,16 @@ int pl_create(const pl_code* codes, int32_t ncodes, const pl_decoder* dec, int32
             d.sched_lane = up_sched(c.sched_lane);
             d.nops_lane = int(c.sched_lane.size());
             d.nops_list = int(c.sched_list.size());
-            d.sched_list_c = up_sched(c.sched_list_c);
-            d.nops_list_c = int(c.sched_list_c.size());
+            d.sched_listv[0] = d.sched_list;
+            d.nops_listv[0] = d.nops_list;
+            for (int v = 1; v < 4; ++v) {
+                // (equal variants share one upload)
+                int same = -1;
+                for (int u = 0; u < v && same < 0; ++u)
+                    if (c.sched_listv[u] == c.sched_listv[v]) same = u;
+                d.sched_listv[v] = same >= 0 ? d.sched_listv[same] : up_sched(c.sched_listv[v]);
+                d.nops_listv[v] = int(c.sched_listv[v].size());
+            }
             d.nops_sc = int(c.sched_sc.size());
             d.info_pos = static_cast<const uint16_t*>(up(c.info_pos.data(), c.info_pos.size() * 2));
             d.crc_tab = c.crc_tab.empty() ? nullptr

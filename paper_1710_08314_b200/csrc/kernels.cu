@@ -793,8 +793,14 @@ __device__ void list_frozen(Ctx<R, SW>& cx, int d, int m, int lb, int na) {
 // Per-path statistics of an R1 / SPC node: hard decisions written into the
 // path's own psum span, the two smallest magnitudes under the (value, index)
 // order (select.hpp:18-68) -> st_i1/st_a1, st_i2/st_a2, parity -> st_w.
-template <bool VLEAF = false, typename R, int SW>
-__device__ void r1spc_stats(Ctx<R, SW>& cx, int d, int m, int lb, int na) {
+// gf (a big fused leaf, kOpFused | kOpFusedG on a node of more than the
+// fused_leaf sizes): the node is a right child whose parent's G op was
+// dropped from the schedule; its LLRs are formed here, from the parent
+// segment (depth d - 1) and the left sibling's decisions, and never stored
+// -- nothing reads a leaf's LLRs after its statistics.
+template <bool VLEAF = false, bool BF = false, typename R, int SW>
+__device__ void r1spc_stats(Ctx<R, SW>& cx, int d, int m, int lb, int na, bool gf_arg = false) {
+    const bool gf = BF && gf_arg; // (folds away in the kernels without big fused leaves)
     using A = Arith<R>;
     using M = typename A::M;
     using K = typename A::Key;
@@ -807,7 +813,16 @@ __device__ void r1spc_stats(Ctx<R, SW>& cx, int d, int m, int lb, int na) {
     const int p = cx.fx->alive_list[ok ? r : 0];
     if (E == 1) {
         // one value per lane (lp == m): every path's hard bits in one ballot
-        const M v = ok ? A::val(cx.llr(p, d)[l0]) : M(0);
+        M v = M(0);
+        if (ok) {
+            if (gf) {
+                const R* pa = cx.llr(p, d - 1);
+                const int up = lb - m + l0;
+                v = A::val(A::g(pa[l0], pa[m + l0], (cx.row(p)[up >> 5] >> (up & 31)) & 1u));
+            } else {
+                v = A::val(cx.llr(p, d)[l0]);
+            }
+        }
         const unsigned hb = cx.sw.ballot(ok && v < M(0));
         const uint32_t mk = m >= 32 ? FULL : ((1u << m) - 1u);
         const uint32_t gb = (hb >> (cx.lane & ~(lp - 1))) & mk;
@@ -835,7 +850,11 @@ __device__ void r1spc_stats(Ctx<R, SW>& cx, int d, int m, int lb, int na) {
     // [l0*E, (l0+1)*E) of its path (vector loads), builds their hard bits
     // locally and ORs them into the path's (cleared) psum span.
     const int i0 = l0 * E;
-    const R* L = cx.llr(p, d) + i0;
+    // (gf: L = the parent's left half at this lane's values, L + m its right
+    // half, ub0 = the position of the left sibling's decision for value i0)
+    const R* L = (gf ? cx.llr(p, d - 1) : cx.llr(p, d)) + i0;
+    const uint32_t* urow = cx.row(p);
+    const int ub0 = lb - m + i0;
     uint32_t* span = cx.row(p) + (lb >> 5);
     const int base = m < 32 ? (lb & 31) : 0; // span bit of value 0 within span[0]
     if (ok && l0 == 0) {
@@ -860,7 +879,10 @@ __device__ void r1spc_stats(Ctx<R, SW>& cx, int d, int m, int lb, int na) {
         uint32_t q1 = FULL, q2 = FULL;
         #pragma unroll 1
         for (int k = 0; k < E; k += 4) {
-            const uint32_t w = *reinterpret_cast<const uint32_t*>(L + k);
+            uint32_t w = *reinterpret_cast<const uint32_t*>(L + k);
+            if (gf)
+                w = g_swar(w, *reinterpret_cast<const uint32_t*>(L + m + k),
+                           (urow[(ub0 + k) >> 5] >> ((ub0 + k) & 31)) & 15u);
             acc |= ((((w >> 7) & 0x01010101u) * 0x01020408u) >> 24) << (k & 31);
             const uint32_t a4 = __vabsdiffu4(w ^ 0x80808080u, 0x80808080u);
             const uint32_t ix = uint32_t(i0 + k) * 0x00010001u + 0x00010000u;
@@ -890,6 +912,13 @@ __device__ void r1spc_stats(Ctx<R, SW>& cx, int d, int m, int lb, int na) {
             Vec<R, 4> q[PLB_VLEAF_VF];
 #pragma unroll
             for (int u = 0; u < PLB_VLEAF_VF; ++u) q[u] = vld<R, 4>(L + k + 4 * u);
+            if (gf) {
+#pragma unroll
+                for (int u = 0; u < PLB_VLEAF_VF; ++u) {
+                    const int up = ub0 + k + 4 * u;
+                    q[u] = fg_compute<R, 4>(q[u], vld<R, 4>(L + m + k + 4 * u), urow[up >> 5] >> (up & 31), true);
+                }
+            }
 #pragma unroll
             for (int u = 0; u < PLB_VLEAF_VF; ++u)
 #pragma unroll
@@ -913,12 +942,16 @@ __device__ void r1spc_stats(Ctx<R, SW>& cx, int d, int m, int lb, int na) {
         for (int k = 0; k < E; k += 4) {
             M v[4];
             if (E >= 4) {
-                const Vec<R, 4> q = vld<R, 4>(L + k);
+                Vec<R, 4> q = vld<R, 4>(L + k);
+                if (gf) q = fg_compute<R, 4>(q, vld<R, 4>(L + m + k), urow[(ub0 + k) >> 5] >> ((ub0 + k) & 31), true);
                 #pragma unroll
                 for (int j = 0; j < 4; ++j) v[j] = A::val(q.v[j]);
             } else {
                 #pragma unroll
-                for (int j = 0; j < 4; ++j) v[j] = j < E ? A::val(L[j]) : M(0);
+                for (int j = 0; j < 4; ++j)
+                    v[j] = j >= E ? M(0)
+                           : gf   ? A::val(A::g(L[j], L[m + j], (urow[(ub0 + j) >> 5] >> ((ub0 + j) & 31)) & 1u))
+                                  : A::val(L[j]);
             }
             #pragma unroll
             for (int j = 0; j < 4; ++j) {
@@ -1188,14 +1221,15 @@ __device__ void fused_leaf(Ctx<R, SW>& cx, int code, int d, int m, int lb, int n
 // (ascending slot, then candidate number, list_decoder.hpp:240-333), one
 // shared fork_apply, normalisation.  C = candidates per lane, fixed per
 // kernel instantiation (4L <= SW*C).
-template <typename R, int SW, int C, int MAXW, bool VLEAF = false>
+template <typename R, int SW, int C, int MAXW, bool VLEAF = false, bool BF = false>
 __device__ void list_fork_node(Ctx<R, SW>& cx, int code, int d, int m, int lb, int na, bool fused) {
     using A = Arith<R>;
     using M = typename A::M;
-    if (fused) {
+    constexpr int MF = sizeof(R) == 1 ? kFuseMaxI8 : kFuseMaxF32;
+    if (fused && m <= MF) {
         // statistics already taken by fused_leaf
     } else if (code == OP_R1 || code == OP_SPC) {
-        r1spc_stats<VLEAF>(cx, d, m, lb, na);
+        r1spc_stats<VLEAF, BF>(cx, d, m, lb, na, BF && fused);
     } else if (code == OP_REP) {
         rep_fold<VLEAF>(cx, d, m, na);
         rep_pen<VLEAF>(cx, d, m, na);
@@ -1344,7 +1378,7 @@ __device__ void setup_ctx(Ctx<R, SW>& cx, const LaunchParams& P, const DevCode& 
 // SW lanes: candidates per lane CW = ceil(4L / SW) and the widest ranking
 // network MAXW = min(SW, 4L).
 __host__ __device__ constexpr int kv_l(int kv) { return 1 << (kv - 1); }
-// Float kernels that decode the chained schedule (DevCode::sched_list_c):
+// Float kernels that decode a chained schedule (DevCode::sched_listv[2..3]):
 // those with register room for the chained loop's four loads in flight --
 // the sub-warp kernels (L <= 8 at 2 / 4 frames per warp) and L = 32 (128
 // registers).  The 32-lane kernels at L <= 16 spill with it (cfg4 L=16
@@ -1354,6 +1388,18 @@ __host__ __device__ constexpr int kv_l(int kv) { return 1 << (kv - 1); }
 #endif
 template <typename R, int KV, int SW>
 constexpr bool kChainKernel = PLB_CHAIN_KERNELS && sizeof(R) == 4 && (KV == 6 || SW < 32);
+// Kernels whose statistics pass can form a big rate-1 / single-parity leaf
+// from its parent's segment (r1spc_stats gf): all but the float sub-warp
+// kernels, which lose 7-10% to the extra code at their 64-register cap
+// (cfg0 20.1 -> 19.7 with it, 18.1 with the code present and unused).
+#ifndef PLB_BIGFUSE_KERNELS
+#define PLB_BIGFUSE_KERNELS 1
+#endif
+template <typename R, int KV, int SW>
+constexpr bool kBigFuseKernel = PLB_BIGFUSE_KERNELS && (sizeof(R) != 4 || SW == 32);
+// ... and the schedule variant (DevCode::sched_listv) a kernel reads
+template <typename R, int KV, int SW>
+constexpr int kSchedVariant = (kChainKernel<R, KV, SW> ? 2 : 0) + (kBigFuseKernel<R, KV, SW> ? 0 : 1);
 __host__ __device__ constexpr int kv_cw(int kv, int sw) { return (4 * kv_l(kv) + sw - 1) / sw; }
 __host__ __device__ constexpr int kv_maxw(int kv, int sw) { return 4 * kv_l(kv) < sw ? 4 * kv_l(kv) : sw; }
 
@@ -1371,8 +1417,9 @@ __device__ void list_frame(const LaunchParams& P, const DevCode& C, unsigned cha
     setup_ctx<TEAM>(cx, P, C, sm, gs, frame, sw, kv_l(KV), segmax); // P.l == kv_l(KV)
     const int lane = cx.lane;
     constexpr bool CHK = kChainKernel<R, KV, SW>;
-    const uint32_t* sched = CHK ? C.sched_list_c : C.sched_list;
-    const int nops = CHK ? C.nops_list_c : C.nops_list;
+    constexpr bool BFK = kBigFuseKernel<R, KV, SW>;
+    const uint32_t* sched = C.sched_listv[kSchedVariant<R, KV, SW>];
+    const int nops = C.nops_listv[kSchedVariant<R, KV, SW>];
     #pragma unroll 1
     for (int oi = 0; oi < nops; ++oi) {
 #ifdef PLB_OPTIME
@@ -1382,13 +1429,13 @@ __device__ void list_frame(const LaunchParams& P, const DevCode& C, unsigned cha
         const int code = op_code(op), d = op_depth(op), m = 1 << op_logm(op), lb = op_lb(op);
         const int na = __popc(cx.alive);
         const bool fused = (op & kOpFused) != 0;
-        if (fused) fused_leaf(cx, code, d, m, lb, na, (op & kOpFusedG) != 0);
+        if (fused && m <= (sizeof(R) == 1 ? kFuseMaxI8 : kFuseMaxF32)) fused_leaf(cx, code, d, m, lb, na, (op & kOpFusedG) != 0);
         if (code <= OP_G) op_fg<(sizeof(R) == 4 && KV >= PLB_FG_UNROLL_MINKV) ? PLB_FG_UNROLL : 1, CHK>(cx, d, m, lb, na, code == OP_G, CHK && (op & kOpChain) != 0);
         else if (code == OP_H) op_h(cx, m, lb, na);
         else if (code == OP_FROZEN) {
             if (!fused) list_frozen<(sizeof(R) == 4 && KV >= PLB_VLEAF_MINKV)>(cx, d, m, lb, na);
         } else {
-            list_fork_node<R, SW, CW, MAXW, (sizeof(R) == 4 && KV >= PLB_VLEAF_MINKV)>(cx, code, d, m, lb, na, fused);
+            list_fork_node<R, SW, CW, MAXW, (sizeof(R) == 4 && KV >= PLB_VLEAF_MINKV), BFK>(cx, code, d, m, lb, na, fused);
         }
 #ifdef PLB_OPTIME
         // (profiling build only) cycles per op kind of the first frame
@@ -1653,8 +1700,8 @@ __device__ void team_helper(const LaunchParams& P, const DevCode& C, unsigned ch
     cx.tt0 = wib * 32 + cx.lane;
     cx.tstride = 32 * P.team;
     constexpr bool CHK = kChainKernel<R, KV, 32>;
-    const uint32_t* sched = CHK ? C.sched_list_c : C.sched_list;
-    const int nops = CHK ? C.nops_list_c : C.nops_list;
+    const uint32_t* sched = C.sched_listv[kSchedVariant<R, KV, 32>];
+    const int nops = C.nops_listv[kSchedVariant<R, KV, 32>];
     #pragma unroll 1
     for (int oi = 0; oi < nops; ++oi) {
         const uint32_t op = __ldg(sched + oi);

@@ -67,10 +67,14 @@ struct DevCode {
     const uint32_t* sched_list; // list-decoder schedule (pruned or full tree)
     const uint32_t* sched_sc;   // SC-rung schedule (R1/SPC expanded)
     const uint32_t* sched_lane; // the same without OP_SCSUB (frame-per-lane SC kernel)
-    int32_t nops_list, nops_sc, nops_lane, nops_list_c;
-    const uint32_t* sched_list_c; // list schedule with chained F ops (kOpChain): the float
-                                  // kernels with register room for the chained loop read
-                                  // this one (kernels.cu kChainKernel), the others sched_list
+    int32_t nops_list, nops_sc, nops_lane, pad2;
+    // List-schedule variants (kernels.cu kSchedVariant picks one per kernel
+    // instantiation): [0] = sched_list: big rate-1 / single-parity leaves
+    // fused with their parent's G op; [1]: small fused leaves only; [2], [3]:
+    // the same two with chained F ops (kOpChain, float).  Fixed point has
+    // [0] and [1] ([2], [3] point at them).
+    const uint32_t* sched_listv[4];
+    int32_t nops_listv[4];
     const uint16_t* info_pos;   // psize open positions, ascending
     // CRC as an affine map over the decided codeword:
     // syndrome = crc_c0 ^ XOR_j crc_tab[j][byte_j(codeword)], zero <=> pass.
