@@ -1383,11 +1383,17 @@ __host__ __device__ constexpr int kv_l(int kv) { return 1 << (kv - 1); }
 // the sub-warp kernels (L <= 8 at 2 / 4 frames per warp) and L = 32 (128
 // registers).  The 32-lane kernels at L <= 16 spill with it (cfg4 L=16
 // -1.5%) and keep the plain schedule and code.
+#ifndef PLB_CHAIN_SUBWARP
+#define PLB_CHAIN_SUBWARP 1
+#endif
+#ifndef PLB_BIGFUSE_SUBWARP
+#define PLB_BIGFUSE_SUBWARP 0
+#endif
 #ifndef PLB_CHAIN_KERNELS
 #define PLB_CHAIN_KERNELS 1
 #endif
 template <typename R, int KV, int SW>
-constexpr bool kChainKernel = PLB_CHAIN_KERNELS && sizeof(R) == 4 && (KV == 6 || SW < 32);
+constexpr bool kChainKernel = PLB_CHAIN_KERNELS && sizeof(R) == 4 && (KV == 6 || (PLB_CHAIN_SUBWARP && SW < 32));
 // Kernels whose statistics pass can form a big rate-1 / single-parity leaf
 // from its parent's segment (r1spc_stats gf): all but the float sub-warp
 // kernels, which lose 7-10% to the extra code at their 64-register cap
@@ -1396,7 +1402,7 @@ constexpr bool kChainKernel = PLB_CHAIN_KERNELS && sizeof(R) == 4 && (KV == 6 ||
 #define PLB_BIGFUSE_KERNELS 1
 #endif
 template <typename R, int KV, int SW>
-constexpr bool kBigFuseKernel = PLB_BIGFUSE_KERNELS && (sizeof(R) != 4 || SW == 32);
+constexpr bool kBigFuseKernel = PLB_BIGFUSE_KERNELS && (sizeof(R) != 4 || SW == 32 || PLB_BIGFUSE_SUBWARP);
 // ... and the schedule variant (DevCode::sched_listv) a kernel reads
 template <typename R, int KV, int SW>
 constexpr int kSchedVariant = (kChainKernel<R, KV, SW> ? 2 : 0) + (kBigFuseKernel<R, KV, SW> ? 0 : 1);
