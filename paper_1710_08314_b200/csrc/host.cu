@@ -382,6 +382,11 @@ void fuse_lane_chains(const std::vector<uint32_t>& in, size_t lo, size_t hi,
             fuse_lane_chains(in, i + 2, i + 2 + len, out, ve, jmax, jmax0, gr1);
             out[at] = uint32_t(out.size() - at - 1);
             i += 2 + len;
+        } else if (code == plb::OP_F && i + 1 < hi && plb::op_code(in[i + 1]) == plb::OP_FROZEN &&
+                   plb::op_depth(in[i + 1]) == plb::op_depth(w) + 1) {
+            // the left child is a rate-0 node: SC decides it without its LLRs
+            // (sc_decoder.hpp:80-83), so the F op that would form them is dropped
+            ++i;
         } else if (code == plb::OP_F || code == plb::OP_G) {
             const int h = (1 << plb::op_logm(w)) >> 1;
             int j = 0;
