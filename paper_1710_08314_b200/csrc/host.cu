@@ -353,7 +353,7 @@ void emit_sc(const std::vector<Node>& t, int ni, std::vector<uint32_t>& s,
 // 16-byte chunks: (m / 2) >> J >= ve values.  R1SC skip lengths are
 // recomputed for the shortened expansions.
 void fuse_lane_chains(const std::vector<uint32_t>& in, size_t lo, size_t hi,
-                      std::vector<uint32_t>& out, int ve, int jmax, int jmax0, bool gr1) {
+                      std::vector<uint32_t>& out, int ve, int jmax, int jmax0, bool gr1, bool subf) {
     size_t i = lo;
     while (i < hi) {
         const uint32_t w = in[i];
@@ -367,7 +367,7 @@ void fuse_lane_chains(const std::vector<uint32_t>& in, size_t lo, size_t hi,
             out.push_back(0);
             out.push_back(w);
             const size_t len = in[i + 2];
-            fuse_lane_chains(in, i + 3, i + 3 + len, out, ve, jmax, jmax0, gr1);
+            fuse_lane_chains(in, i + 3, i + 3 + len, out, ve, jmax, jmax0, gr1, subf);
             out[at] = uint32_t(out.size() - at - 1);
             i += 3 + len;
         } else if (code == plb::OP_SCSUB) {
@@ -379,9 +379,16 @@ void fuse_lane_chains(const std::vector<uint32_t>& in, size_t lo, size_t hi,
             const size_t at = out.size();
             out.push_back(0);
             const size_t len = in[i + 1];
-            fuse_lane_chains(in, i + 2, i + 2 + len, out, ve, jmax, jmax0, gr1);
+            fuse_lane_chains(in, i + 2, i + 2 + len, out, ve, jmax, jmax0, gr1, subf);
             out[at] = uint32_t(out.size() - at - 1);
             i += 2 + len;
+        } else if (subf && (code == plb::OP_F || code == plb::OP_G) && i + 2 < hi &&
+                   plb::op_code(in[i + 1]) == plb::OP_SCSUB && plb::op_depth(in[i + 1]) == plb::op_depth(w) + 1) {
+            // an in-register subtree takes its parent's F / G op along: its
+            // LLRs come straight from the parent's values (lanes.cuh lane_sub)
+            out.push_back(in[i + 1] | plb::kOpFused | (code == plb::OP_G ? plb::kOpFusedG : 0u));
+            out.push_back(in[i + 2]);
+            i += 3;
         } else if (code == plb::OP_F && i + 1 < hi && plb::op_code(in[i + 1]) == plb::OP_FROZEN &&
                    plb::op_depth(in[i + 1]) == plb::op_depth(w) + 1) {
             // the left child is a rate-0 node: SC decides it without its LLRs
@@ -501,11 +508,13 @@ HostCode make_host_code(const pl_code& c, const pl_decoder& dec) {
         // values of the rate-1 nodes are sums of magnitudes: measured on
         // FA@4.5 dB, every rate-1 node of >= 32 values took the shortcut.)
         const bool gr1 = !(std::getenv("PLB_LANE_GR1") && std::atoi(std::getenv("PLB_LANE_GR1")) == 0);
-        if (jmax > 0 || jmax0 > 0 || gr1) {
+        // in-register subtrees fused with their parent's F / G op
+        const bool subf = !(std::getenv("PLB_LANE_SUBF") && std::atoi(std::getenv("PLB_LANE_SUBF")) == 0);
+        {
             std::vector<uint32_t> fused;
             fused.reserve(h.sched_lane.size());
             const int ve = dec.precision == PL_F32 ? 4 : dec.precision == PL_I8 ? 16 : 8;
-            fuse_lane_chains(h.sched_lane, 0, h.sched_lane.size(), fused, ve, jmax, jmax0, gr1);
+            fuse_lane_chains(h.sched_lane, 0, h.sched_lane.size(), fused, ve, jmax, jmax0, gr1, subf);
             h.sched_lane.swap(fused);
         }
     }

@@ -599,13 +599,38 @@ __device__ __forceinline__ uint32_t sc_regs(const typename Arith<R>::M (&x)[M], 
 }
 constexpr int kLaneSubMax = 16;
 
+// fz (kOpFused [| kOpFusedG] on the op word): the subtree is fused with its
+// parent's F (1) or G (2) op, which is absent from the schedule: the M LLRs
+// are formed from the parent's 2M values (depth d - 1; G: with the left
+// sibling's decisions, bits [lb - M, lb)) and never stored.
 template <typename R, int M>
-__device__ __forceinline__ void lane_sub(const LaneCtx<R>& c, int d, int lb, uint32_t mask) {
+__device__ __forceinline__ void lane_sub(const LaneCtx<R>& c, int d, int lb, uint32_t mask, int fz) {
     using A = Arith<R>;
     using MM = typename A::M;
     constexpr int VE = LaneCtx<R>::VE;
     MM x[M];
-    if constexpr (M >= VE) {
+    if (fz) {
+        const bool is_g = fz == 2;
+        const int up = lb - M;
+        const uint32_t ub = is_g ? c.word(up >> 5) >> (up & 31) : 0u;
+        if constexpr (M >= VE) {
+            int cs;
+            const R* in = c.chunk_base(d - 1, cs);
+#pragma unroll
+            for (int k = 0; k < M / VE; ++k) {
+                const Vec<R, VE> q = fg_compute<R, VE>(vld<R, VE>(in + k * cs), vld<R, VE>(in + (k + M / VE) * cs),
+                                                       ub >> (k * VE), is_g);
+#pragma unroll
+                for (int i = 0; i < VE; ++i) x[k * VE + i] = A::val(q.v[i]);
+            }
+        } else {
+            // the parent's 2M <= VE values are one chunk
+            const Vec<R, 2 * M> q = vld<R, 2 * M>(c.chunk(d - 1, 0));
+#pragma unroll
+            for (int i = 0; i < M; ++i)
+                x[i] = A::val(is_g ? A::g(q.v[i], q.v[M + i], (ub >> i) & 1u) : A::f(q.v[i], q.v[M + i]));
+        }
+    } else if constexpr (M >= VE) {
         int cs;
         const R* in = c.chunk_base(d, cs);
 #pragma unroll
@@ -686,11 +711,12 @@ __device__ void lane_frame(const LaunchParams& P, const DevCode& C, unsigned cha
             const uint32_t mask = next; // the word after OP_SCSUB
             ++oi;
             next = __ldg(sched + oi + 1);
+            const int fz = (op & kOpFused) ? ((op & kOpFusedG) ? 2 : 1) : 0;
             switch (m) {
-            case 2: lane_sub<R, 2>(c, d, lb, mask); break;
-            case 4: lane_sub<R, 4>(c, d, lb, mask); break;
-            case 8: lane_sub<R, 8>(c, d, lb, mask); break;
-            default: lane_sub<R, 16>(c, d, lb, mask); break;
+            case 2: lane_sub<R, 2>(c, d, lb, mask, fz); break;
+            case 4: lane_sub<R, 4>(c, d, lb, mask, fz); break;
+            case 8: lane_sub<R, 8>(c, d, lb, mask, fz); break;
+            default: lane_sub<R, 16>(c, d, lb, mask, fz); break;
             }
             break;
         }
