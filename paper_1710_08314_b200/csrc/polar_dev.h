@@ -44,7 +44,11 @@ constexpr int kFuseMaxI8 = 8, kFuseMaxF32 = 4;
 //   bit   28    (list schedules) fused leaf: the leaf's LLRs are not
 //               materialised; the leaf op computes them in registers from
 //               the parent segment (depth - 1) with F, or with G when
-//   bit   29    is set (the F / G op of the parent is then omitted)
+//   bit   29    is set (the F / G op of the parent is then omitted).  Leaves
+//               of at most kFuseMax* values: fused_leaf; larger rate-1 /
+//               single-parity right children (bit 29 set): r1spc_stats.
+//               Lane schedules: the same two bits on an OP_SCSUB word
+//               (lane_sub forms the subtree's LLRs from the parent's values)
 constexpr uint32_t kOpFused = 1u << 28, kOpFusedG = 1u << 29;
 //   bit   30    (list schedules) F / G op chained with the F op of its child:
 //               both levels are computed in one sweep and stored, the child's
