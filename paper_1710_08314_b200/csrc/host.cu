@@ -576,6 +576,7 @@ struct pl_handle {
     uint32_t* path_alive = nullptr; // pl_list_paths: the final list of every frame
     float* path_metric = nullptr;
     int64_t host_chunk = 0;     // frames per chunk of pl_decode_host (0 = automatic)
+    int list_alt = 0; // LaunchParams::list_alt
     int sc_keep = 0, sc_keep_hi = 0; // L2 hint split of the frame-per-lane SC pass (LaunchParams::sc_keep)
     int sc_discard = 0; // LaunchParams::sc_discard
     int list_discard = 0; // LaunchParams::list_discard
@@ -964,6 +965,7 @@ void run_decode(pl_handle& h, const void* llr, const int32_t* code_id, int64_t n
         p.sc_keep_hi = rc.lanes ? h.sc_keep_hi : 0;
         p.sc_discard = rc.lanes ? h.sc_discard : 0;
         p.list_discard = rc.lanes ? 0 : h.list_discard;
+        p.list_alt = h.list_alt;
         p.solo_max = rc.grid * rc.fpw;
         if (h.profiling) {
             while (h.prof_ev.size() < size_t(2 * (slot + 1))) {
@@ -1381,6 +1383,10 @@ int pl_create(const pl_code* codes, int32_t ncodes, const pl_decoder* dec, int32
             // last read (float: SC pass 21.9 -> 20.7 ms)
             h->sc_discard = env_int("PLB_SC_DISCARD", h->dec.precision == PL_F32 ? 1 : 0);
             h->list_discard = env_int("PLB_LIST_DISCARD", h->dec.precision == PL_F32 ? 1 : 0);
+            // float sub-warp list kernels: chained F ops pay where depth pools
+            // spill to the L2 (N >= 2048), big fused leaves where everything is
+            // shared-memory resident (kernels.cu kChainKernel)
+            h->list_alt = env_int("PLB_LIST_ALT", h->dec.precision == PL_F32 && h->nmax <= 1024 ? 1 : 0);
             h->host_chunk = env_int("PLB_HOST_CHUNK", 0);
         if (kind == PL_KIND_FA_SSCL)
             for (int ll = 2; ll <= l; ll *= 2) h->rungs.push_back(plan_rung(*h, ll, true, true));

@@ -1392,8 +1392,14 @@ __host__ __device__ constexpr int kv_l(int kv) { return 1 << (kv - 1); }
 #ifndef PLB_CHAIN_KERNELS
 #define PLB_CHAIN_KERNELS 1
 #endif
-template <typename R, int KV, int SW>
-constexpr bool kChainKernel = PLB_CHAIN_KERNELS && sizeof(R) == 4 && (KV == 6 || (PLB_CHAIN_SUBWARP && SW < 32));
+// (ALT: the second instantiation of the float sub-warp kernels, big fused
+// leaves instead of chained F ops -- the better of the two for codes of
+// N <= 1024, whose depth pools are shared-memory resident: N = 1024 rate
+// 0.84 L = 8 / 4 +8% / +6%, N = 256 +8%, while N = 2048 / 4096 lose 8% / 21%
+// without the chained ops, `profiles/r02b_sweeps.log` nsweep; host.cu picks
+// per handle, LaunchParams::list_alt)
+template <typename R, int KV, int SW, bool ALT = false>
+constexpr bool kChainKernel = PLB_CHAIN_KERNELS && sizeof(R) == 4 && (KV == 6 || (PLB_CHAIN_SUBWARP && SW < 32 && !ALT));
 // Kernels whose statistics pass can form a big rate-1 / single-parity leaf
 // from its parent's segment (r1spc_stats gf): all but the float sub-warp
 // kernels, which lose 7-10% to the extra code at their 64-register cap
@@ -1401,15 +1407,15 @@ constexpr bool kChainKernel = PLB_CHAIN_KERNELS && sizeof(R) == 4 && (KV == 6 ||
 #ifndef PLB_BIGFUSE_KERNELS
 #define PLB_BIGFUSE_KERNELS 1
 #endif
-template <typename R, int KV, int SW>
-constexpr bool kBigFuseKernel = PLB_BIGFUSE_KERNELS && (sizeof(R) != 4 || SW == 32 || PLB_BIGFUSE_SUBWARP);
+template <typename R, int KV, int SW, bool ALT = false>
+constexpr bool kBigFuseKernel = PLB_BIGFUSE_KERNELS && (sizeof(R) != 4 || SW == 32 || PLB_BIGFUSE_SUBWARP || ALT);
 // ... and the schedule variant (DevCode::sched_listv) a kernel reads
-template <typename R, int KV, int SW>
-constexpr int kSchedVariant = (kChainKernel<R, KV, SW> ? 2 : 0) + (kBigFuseKernel<R, KV, SW> ? 0 : 1);
+template <typename R, int KV, int SW, bool ALT = false>
+constexpr int kSchedVariant = (kChainKernel<R, KV, SW, ALT> ? 2 : 0) + (kBigFuseKernel<R, KV, SW, ALT> ? 0 : 1);
 __host__ __device__ constexpr int kv_cw(int kv, int sw) { return (4 * kv_l(kv) + sw - 1) / sw; }
 __host__ __device__ constexpr int kv_maxw(int kv, int sw) { return 4 * kv_l(kv) < sw ? 4 * kv_l(kv) : sw; }
 
-template <typename R, int KV, int SW, bool TEAM>
+template <typename R, int KV, int SW, bool TEAM, bool ALT = false>
 __device__ void list_frame(const LaunchParams& P, const DevCode& C, unsigned char* sm,
                            unsigned char* gs, int frame, bool active, const Sub<SW>& sw, int segmax,
                            int oidx) {
@@ -1422,10 +1428,10 @@ __device__ void list_frame(const LaunchParams& P, const DevCode& C, unsigned cha
     Ctx<R, SW> cx;
     setup_ctx<TEAM>(cx, P, C, sm, gs, frame, sw, kv_l(KV), segmax); // P.l == kv_l(KV)
     const int lane = cx.lane;
-    constexpr bool CHK = kChainKernel<R, KV, SW>;
-    constexpr bool BFK = kBigFuseKernel<R, KV, SW>;
-    const uint32_t* sched = C.sched_listv[kSchedVariant<R, KV, SW>];
-    const int nops = C.nops_listv[kSchedVariant<R, KV, SW>];
+    constexpr bool CHK = kChainKernel<R, KV, SW, ALT>;
+    constexpr bool BFK = kBigFuseKernel<R, KV, SW, ALT>;
+    const uint32_t* sched = C.sched_listv[kSchedVariant<R, KV, SW, ALT>];
+    const int nops = C.nops_listv[kSchedVariant<R, KV, SW, ALT>];
     #pragma unroll 1
     for (int oi = 0; oi < nops; ++oi) {
 #ifdef PLB_OPTIME
@@ -1735,7 +1741,7 @@ __device__ void team_helper(const LaunchParams& P, const DevCode& C, unsigned ch
 
 // KV = 0: SC pass; KV = 1..6: list pass at L = 1, 2, 4, 8, 16, 32.  A warp
 // holds 32/SW frames (SW < 32 only for single-code batches).
-template <typename R, int KV, int SW, bool TEAM = false>
+template <typename R, int KV, int SW, bool TEAM = false, bool ALT = false>
 __global__ void __launch_bounds__(kMaxTeam * 32, KV >= 6 ? PLB_MINBLOCKS_BIGL
                                                          : PLB_MINBLOCKS * kMaxWarpsPerBlock / kMaxTeam)
 decode_kernel(const LaunchParams P) {
@@ -1803,11 +1809,11 @@ decode_kernel(const LaunchParams P) {
                 const int fj = same ? frame : __shfl_sync(FULL, frame, j * SW);
                 const int cj = same ? cid : __shfl_sync(FULL, cid, j * SW);
                 const bool aj = same ? active : (__shfl_sync(FULL, int(active), j * SW) && sw.id == 0);
-                list_frame<R, KV, SW, false>(P, P.codes[cj], sm, gs, fj, aj, sw, segmax, fj);
+                list_frame<R, KV, SW, false, ALT>(P, P.codes[cj], sm, gs, fj, aj, sw, segmax, fj);
             }
         } else {
             const DevCode C = P.codes[cid];
-            if constexpr (KV > 0) list_frame<R, KV, SW, false>(P, C, sm, gs, frame, active, sw, segmax, int(idx));
+            if constexpr (KV > 0) list_frame<R, KV, SW, false, ALT>(P, C, sm, gs, frame, active, sw, segmax, int(idx));
             else sc_frame<R>(P, C, sm, gs, frame, sw);
         }
     }
@@ -1899,9 +1905,14 @@ __global__ void selftest_kernel(unsigned long long* bad) {
 
 // kernel of a pass: kv = 0 (SC) or 1..6 (list at L = 1..32), frames/warp fpw
 template <typename R>
-void (*kernel_for(int kv, int fpw, bool team = false))(LaunchParams) {
+void (*kernel_for(int kv, int fpw, bool team = false, bool alt = false))(LaunchParams) {
     // team kernels (one frame per block, opt-in) at L = 16 / 32
     if (team) return kv == 5 ? decode_kernel<R, 5, 32, true> : decode_kernel<R, 6, 32, true>;
+    if constexpr (sizeof(R) == 4) {
+        // float sub-warp kernels: the big-fused-leaf instantiation (kChainKernel)
+        if (alt && fpw == 4) return kv == 1 ? decode_kernel<R, 1, 8, false, true> : decode_kernel<R, 2, 8, false, true>;
+        if (alt && fpw == 2) return kv == 3 ? decode_kernel<R, 3, 16, false, true> : decode_kernel<R, 4, 16, false, true>;
+    }
     // (8-lane sub-warps measured slower than 16-lane ones at L = 4 and 8)
     if (fpw == 4) return kv == 1 ? decode_kernel<R, 1, 8> : decode_kernel<R, 2, 8>;
     if (fpw == 2) return kv == 3 ? decode_kernel<R, 3, 16> : decode_kernel<R, 4, 16>;
@@ -1927,7 +1938,7 @@ template <typename R>
 cudaError_t launch(const LaunchParams& p, int kv, int grid, cudaStream_t s) {
     const bool team = p.team > 1;
     const int smem = team ? p.smem_per_frame : p.smem_per_warp * p.wpb;
-    auto kern = kernel_for<R>(kv, p.fpw, team);
+    auto kern = kernel_for<R>(kv, p.fpw, team, p.list_alt != 0);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     kern<<<grid, (team ? p.team : p.wpb) * 32, smem, s>>>(p);

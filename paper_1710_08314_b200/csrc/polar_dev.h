@@ -145,6 +145,8 @@ struct LaunchParams {
     uint32_t* path_alive;      // nullable (pl_list_paths): alive-slot mask of the final list
     float* path_metric;        // ... and the metric of every slot, path_stride per frame
     int32_t path_stride;
+    int32_t list_alt;          // float sub-warp list kernels: the instantiation with big fused
+                               // leaves instead of chained F ops (codes of N <= 1024)
     int32_t out_by_idx;        // list passes at one frame per warp / team: outputs are indexed
                                // by the frame's position in frame_list (staging of a
                                // speculative FA rung), not by the frame id
