@@ -192,6 +192,21 @@ int pl_list_paths(pl_handle* h, uint32_t* alive, float* metric);
  * $PLB_HOST_CHUNK or 0. */
 int pl_set_host_chunk(pl_handle* h, int64_t frames);
 
+/* Input layout of pl_decode (device LLRs).  PL_LLR_FRAME_MAJOR (default):
+ * frame f at llr + f * pl_llr_stride, the layout of FrameDecoder<R>::decode
+ * (const R*) called frame after frame.  PL_LLR_INTERLEAVED32: frames in
+ * groups of 32, 16-byte chunks interleaved -- chunk c (16 bytes of values;
+ * n values when the frame is shorter) of frame f at chunk index
+ * ((f / 32) * chunks_per_frame + c) * 32 + f % 32 -- so that the
+ * frame-per-lane SC pass reads the channel with fully coalesced warp loads;
+ * the buffer holds a whole number of groups (pad the last one).  Accepted
+ * for PL_KIND_SC / PL_KIND_SSC handles with one code, pl_decode only
+ * (PL_ERR_CONFIG otherwise): a producer-side option (a demapper that writes
+ * LLRs for the GPU can emit this order), measured in DESIGN.md section 4. */
+#define PL_LLR_FRAME_MAJOR 0
+#define PL_LLR_INTERLEAVED32 1
+int pl_set_llr_layout(pl_handle* h, int32_t layout);
+
 /* Live kernel timing: with profiling enabled every launch of pl_decode is
  * bracketed by CUDA events on its stream; pl_last_kernel_ms waits for them
  * and writes the duration (ms) of each launch of the last pl_decode call and

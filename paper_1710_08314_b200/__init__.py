@@ -23,6 +23,7 @@ from .polar import (  # noqa: F401
     construct_frozen,
     construct_frozen_ga,
     crc_compute,
+    interleave32,
     load_frozen_file,
     load_puncture_file,
     make_code,

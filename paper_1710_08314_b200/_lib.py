@@ -21,7 +21,7 @@ EXPORTS = (
     "pl_channel_generate", "pl_channel_generate_device", "pl_profile", "pl_last_kernel_ms",
     "pl_kernel_selftest", "pl_channel_generate_frames", "pl_precision", "pl_sim_point",
     "pl_format_csv_row", "pl_frozen_file_load", "pl_frozen_file_save", "pl_puncture_file_load",
-    "pl_decode_packed", "pl_decode_host_packed", "pl_frame_latency", "pl_set_host_chunk",
+    "pl_decode_packed", "pl_decode_host_packed", "pl_frame_latency", "pl_set_host_chunk", "pl_set_llr_layout",
     "pl_list_paths",
 )
 
@@ -113,6 +113,7 @@ def lib():
     L.pl_puncture_file_load.argtypes = [C.c_char_p, vp, vp, i32]
     L.pl_frame_latency.argtypes = [vp, vp]
     L.pl_set_host_chunk.argtypes = [vp, i64]
+    L.pl_set_llr_layout.argtypes = [vp, C.c_int32]
     L.pl_list_paths.argtypes = [vp, vp, vp]
     _LIB = L
     return L

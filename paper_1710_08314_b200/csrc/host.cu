@@ -577,6 +577,7 @@ struct pl_handle {
     float* path_metric = nullptr;
     int64_t host_chunk = 0;     // frames per chunk of pl_decode_host (0 = automatic)
     int list_alt = 0; // LaunchParams::list_alt
+    int llr_layout = 0; // pl_set_llr_layout
     int sc_keep = 0, sc_keep_hi = 0; // L2 hint split of the frame-per-lane SC pass (LaunchParams::sc_keep)
     int sc_discard = 0; // LaunchParams::sc_discard
     int list_discard = 0; // LaunchParams::list_discard
@@ -886,7 +887,7 @@ int fail(pl_handle* h, int code, const std::string& msg) {
 void run_decode(pl_handle& h, const void* llr, const int32_t* code_id, int64_t nframes,
                 uint8_t* payload, uint8_t* codeword, uint8_t* crc_ok, uint8_t* esc,
                 float* metric, cudaStream_t s0, int exec = 0, const int64_t* llr_offset = nullptr,
-                uint32_t* lat_ns = nullptr, bool paths = false) {
+                uint32_t* lat_ns = nullptr, bool paths = false, bool il32 = false) {
     cudaStream_t s = s0;
     ck(cudaSetDevice(h.device), "cudaSetDevice");
     h.launches = 0;
@@ -966,6 +967,7 @@ void run_decode(pl_handle& h, const void* llr, const int32_t* code_id, int64_t n
         p.sc_discard = rc.lanes ? h.sc_discard : 0;
         p.list_discard = rc.lanes ? 0 : h.list_discard;
         p.list_alt = h.list_alt;
+        p.llr_il32 = rc.lanes && il32 ? 1 : 0;
         p.solo_max = rc.grid * rc.fpw;
         if (h.profiling) {
             while (h.prof_ev.size() < size_t(2 * (slot + 1))) {
@@ -1520,6 +1522,18 @@ int pl_set_host_chunk(pl_handle* h, int64_t frames) {
     return PL_OK;
 }
 
+int pl_set_llr_layout(pl_handle* h, int32_t layout) {
+    if (!h) return fail(nullptr, PL_ERR_ARG, "null handle");
+    if (layout != PL_LLR_FRAME_MAJOR && layout != PL_LLR_INTERLEAVED32)
+        return fail(h, PL_ERR_ARG, "unknown LLR layout");
+    if (layout == PL_LLR_INTERLEAVED32 &&
+        (uses_list(h->dec.kind) || h->codes.size() != 1 || !h->sc_cfg.lanes))
+        return fail(h, PL_ERR_CONFIG,
+                    "the interleaved LLR layout is for SC / SSC handles with one code (frame-per-lane pass)");
+    h->llr_layout = layout;
+    return PL_OK;
+}
+
 int pl_frame_latency(pl_handle* h, uint32_t* lat_ns) {
     if (!h) return fail(nullptr, PL_ERR_ARG, "null handle");
     h->lat_ns = lat_ns;
@@ -1567,8 +1581,11 @@ int pl_decode(pl_handle* h, const void* llr, const int32_t* code_id, int64_t nfr
         return fail(h, PL_ERR_ARG, "llr and payload buffers are required");
     if (nframes > INT32_MAX) return fail(h, PL_ERR_ARG, "too many frames in one call");
     try {
+        if (h->llr_layout == PL_LLR_INTERLEAVED32 && code_id)
+            return fail(h, PL_ERR_CONFIG, "the interleaved LLR layout takes no per-frame code ids");
         run_decode(*h, llr, code_id, nframes, payload, codeword, crc_ok, esc, metric,
-                   static_cast<cudaStream_t>(stream), 0, nullptr, h->lat_ns, true);
+                   static_cast<cudaStream_t>(stream), 0, nullptr, h->lat_ns, true,
+                   h->llr_layout == PL_LLR_INTERLEAVED32);
         h->err.clear();
         return PL_OK;
     } catch (const std::exception& e) {
@@ -1583,6 +1600,8 @@ int pl_decode_packed(pl_handle* h, const void* llr, const int64_t* llr_offset, c
     if (nframes < 0 || (nframes > 0 && (!llr || !llr_offset || !payload)))
         return fail(h, PL_ERR_ARG, "llr, llr_offset and payload buffers are required");
     if (nframes > INT32_MAX) return fail(h, PL_ERR_ARG, "too many frames in one call");
+    if (h->llr_layout != PL_LLR_FRAME_MAJOR)
+        return fail(h, PL_ERR_CONFIG, "the interleaved LLR layout is accepted by pl_decode only");
     try {
         run_decode(*h, llr, code_id, nframes, payload, codeword, crc_ok, esc, metric,
                    static_cast<cudaStream_t>(stream), 0, llr_offset, h->lat_ns, true);
@@ -1621,6 +1640,8 @@ int decode_host_impl(pl_handle* h, const void* llr, const int64_t* offsets, cons
     if (!h) return fail(nullptr, PL_ERR_ARG, "null handle");
     if (nframes < 0 || (nframes > 0 && (!llr || !payload)))
         return fail(h, PL_ERR_ARG, "llr and payload buffers are required");
+    if (h->llr_layout != PL_LLR_FRAME_MAJOR)
+        return fail(h, PL_ERR_CONFIG, "the interleaved LLR layout is accepted by pl_decode only");
     // packed frames: ascending, 16-byte aligned offsets (the kernels read
     // the channel with 16-byte vectors), code ids in range
     auto frame_n = [&](int64_t f) {

@@ -59,6 +59,7 @@ struct LaneCtx {
     int lane, n;
     int segmax, keep, keep_hi; // depth segments > segmax values live in global scratch
     bool discard;     // drop dead global segments from the L2 (LaunchParams::sc_discard)
+    bool il;          // the channel is lane-interleaved like the depth pools (LaunchParams::llr_il32)
     const R* chan;      // this lane's frame
     uint32_t* ps;       // this lane's psum words, stride 32
     const uint64_t* pt; // pool pointer table
@@ -66,12 +67,12 @@ struct LaneCtx {
     // first value of chunk c at depth d (chunk = min(VE, n >> d) values)
     __device__ __forceinline__ const R* chunk(int d, int c) const {
         const int v = min(VE, n >> d);
-        return d == 0 ? chan + c * v : pool(d) + (c * 32 + lane) * v;
+        return d == 0 ? chan + c * (il ? 32 * v : v) : pool(d) + (c * 32 + lane) * v;
     }
     // chunk k of depth d is at base + k * stride (loop-invariant form of chunk())
     __device__ __forceinline__ const R* chunk_base(int d, int& stride) const {
         const int v = min(VE, n >> d);
-        stride = d == 0 ? v : 32 * v;
+        stride = d == 0 && !il ? v : 32 * v;
         return d == 0 ? chan : pool(d) + lane * v;
     }
     __device__ __forceinline__ uint32_t& word(int w) const { return ps[w * 32]; }
@@ -679,7 +680,15 @@ __device__ void lane_frame(const LaunchParams& P, const DevCode& C, unsigned cha
     c.keep = P.sc_keep;
     c.keep_hi = P.sc_keep_hi;
     c.discard = P.sc_discard != 0;
-    c.chan = frame_llr<R>(P, frame);
+    c.il = P.llr_il32 != 0;
+    if (c.il) {
+        // chunk 0 of this lane's frame inside its group of 32 (host.cu
+        // accepts the layout only without a frame list: frame = 32 * g + lane)
+        const int v = min(LaneCtx<R>::VE, C.n);
+        c.chan = static_cast<const R*>(P.llr) + int64_t(frame >> 5) * C.n * 32 + (frame & 31) * v;
+    } else {
+        c.chan = frame_llr<R>(P, frame);
+    }
     const LaneQ q0 = lane_layout(C.n, int(sizeof(R)), P.seg_smem_max, 0);
     c.ps = reinterpret_cast<uint32_t*>(sm + q0.psum_off) + lane;
     uint64_t* pt = reinterpret_cast<uint64_t*>(sm);

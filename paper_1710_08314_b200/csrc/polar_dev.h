@@ -145,6 +145,8 @@ struct LaunchParams {
     uint32_t* path_alive;      // nullable (pl_list_paths): alive-slot mask of the final list
     float* path_metric;        // ... and the metric of every slot, path_stride per frame
     int32_t path_stride;
+    int32_t llr_il32;          // frame-per-lane SC pass: the channel is interleaved in groups
+                               // of 32 frames (PL_LLR_INTERLEAVED32), one code, no frame list
     int32_t list_alt;          // float sub-warp list kernels: the instantiation with big fused
                                // leaves instead of chained F ops (codes of N <= 1024)
     int32_t out_by_idx;        // list passes at one frame per warp / team: outputs are indexed

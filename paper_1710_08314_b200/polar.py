@@ -60,6 +60,19 @@ def _raise(rc: int, msg: str):
     raise DeviceError(msg)
 
 
+def interleave32(llr):
+    """PL_LLR_INTERLEAVED32 of a (frames, n) array: groups of 32 frames
+    (zero-padded), 16-byte chunks interleaved -- chunk c of frame f at chunk
+    index ((f // 32) * chunks + c) * 32 + f % 32 (include/polar_b200.h)."""
+    llr = np.ascontiguousarray(llr)
+    nf, n = llr.shape
+    v = min(16 // llr.dtype.itemsize, n)
+    g = (nf + 31) // 32
+    buf = np.zeros((g * 32, n), llr.dtype)
+    buf[:nf] = llr
+    return np.ascontiguousarray(buf.reshape(g, 32, n // v, v).transpose(0, 2, 1, 3)).reshape(g * 32, n)
+
+
 def pack_frames(frames, dtype):
     """Packed layout of variable-length frames (pl_decode_packed): frame i
     at element offset off[i], ascending, each 16-byte aligned."""
@@ -453,11 +466,14 @@ class FrameDecoder:
             "metric": t.empty(nframes, dtype=t.float32, device=dev),
         }
 
-    def decode_batch(self, llr, code_id=None, out=None, codeword: bool = False, stream=None):
-        """Decode a device-resident batch (torch CUDA tensor, frames x stride)."""
+    def decode_batch(self, llr, code_id=None, out=None, codeword: bool = False, stream=None, nframes=None):
+        """Decode a device-resident batch (torch CUDA tensor, frames x stride;
+        ``nframes``: fewer than the buffer holds, e.g. a padded interleaved one)."""
         t = self._torch
         assert llr.is_cuda and llr.dtype == self.llr_dtype and llr.is_contiguous()
-        nframes = llr.numel() // self.llr_stride
+        if nframes is None:
+            nframes = llr.numel() // self.llr_stride
+        assert nframes * self.llr_stride <= llr.numel()
         if out is None:
             out = self.alloc_outputs(nframes, codeword)
         ptr = lambda x: C.c_void_p(x.data_ptr()) if x is not None else None
@@ -615,6 +631,14 @@ class FrameDecoder:
         rc = L.lib().pl_set_host_chunk(self._h, int(frames))
         if rc:
             _raise(rc, L.last_error(self._h))
+
+    def set_llr_layout(self, interleaved32: bool):
+        """pl_set_llr_layout: decode_batch then takes LLRs interleaved in
+        groups of 32 frames (``interleave32``); SC / SSC with one code."""
+        rc = L.lib().pl_set_llr_layout(self._h, 1 if interleaved32 else 0)
+        if rc:
+            _raise(rc, L.last_error(self._h))
+        self._il32 = bool(interleaved32)
 
     def frame_latency(self, lat_ns=None):
         """pl_frame_latency: later decode_batch / decode_packed calls write

@@ -446,3 +446,32 @@ def test_sc_lane_ops_with_zero_llrs(P, gpu, oracle_lib):
                     os.environ.pop(k, None)
                 else:
                     os.environ[k] = v
+
+
+@pytest.mark.parametrize("prec", ["f32", "i8", "i16"])
+def test_interleaved_llr_layout(P, gpu, prec):
+    """PL_LLR_INTERLEAVED32 (pl_set_llr_layout): the frame-per-lane SC pass
+    reads a channel interleaved in groups of 32 frames; same outputs as the
+    frame-major layout, a frame count that is not a multiple of 32, short
+    codes (a frame shorter than a 16-byte chunk), and the calls that must
+    refuse it."""
+    scale = {"f32": 0.0, "i8": 4.0, "i16": 64.0}[prec]
+    for n, k, crc, nf in [(2048, 1723, "32-GZIP", 1000), (256, 100, "16-CCITT", 77), (8, 4, None, 40)]:
+        code = _code(P, n, k, crc)
+        _, llr = P.channel(code, 3.0, 11, 0, nf, prec, scale)
+        for kind in ("ssc", "sc"):
+            dec = P.FrameDecoder(code, kind, 1, prec, P.PruningConfig())
+            ref = dec.decode_batch(gpu.from_numpy(llr).cuda(), codeword=True)
+            gpu.cuda.synchronize()
+            ref = {k_: v.cpu().numpy().copy() for k_, v in ref.items() if v is not None}
+            dec.set_llr_layout(True)
+            got = dec.decode_batch(gpu.from_numpy(P.interleave32(llr)).cuda(), codeword=True, nframes=nf)
+            gpu.cuda.synchronize()
+            for key, r in ref.items():
+                assert np.array_equal(got[key].cpu().numpy()[:nf], r), (n, kind, key)
+            with pytest.raises(P.ConfigError):
+                dec.decode_host(llr)
+            dec.set_llr_layout(False)
+    code = _code(P, 256, 100, "16-CCITT")
+    with pytest.raises(P.ConfigError):
+        P.FrameDecoder(code, "ca_sscl", 4, prec, P.PruningConfig()).set_llr_layout(True)
