@@ -578,6 +578,7 @@ struct pl_handle {
     int64_t host_chunk = 0;     // frames per chunk of pl_decode_host (0 = automatic)
     int list_alt = 0; // LaunchParams::list_alt
     int llr_layout = 0; // pl_set_llr_layout
+    int sc_tr = 0; // LaunchParams::sc_tr
     int sc_keep = 0, sc_keep_hi = 0; // L2 hint split of the frame-per-lane SC pass (LaunchParams::sc_keep)
     int sc_discard = 0; // LaunchParams::sc_discard
     int list_discard = 0; // LaunchParams::list_discard
@@ -736,7 +737,7 @@ RungCfg plan_lanes(const pl_handle& h) {
             c.lanes = true;
             c.seg_max = seg;
             c.wpb = wpb;
-            c.smem_per_frame = int(plb::lane_smem_bytes_per_warp(h.nmax, h.esz, seg));
+            c.smem_per_frame = int(plb::lane_smem_bytes_per_warp(h.nmax, h.esz, seg, h.sc_tr != 0));
             c.gscratch_per_frame = plb::lane_gscratch_bytes_per_warp(h.nmax, h.esz, seg);
             const int nb = plb::occupancy_sc_lanes(h.dec.precision, c.smem_per_frame * wpb, wpb);
             if (nb <= 0) continue;
@@ -968,6 +969,7 @@ void run_decode(pl_handle& h, const void* llr, const int32_t* code_id, int64_t n
         p.list_discard = rc.lanes ? 0 : h.list_discard;
         p.list_alt = h.list_alt;
         p.llr_il32 = rc.lanes && il32 ? 1 : 0;
+        p.sc_tr = rc.lanes ? h.sc_tr : 0;
         p.solo_max = rc.grid * rc.fpw;
         if (h.profiling) {
             while (h.prof_ev.size() < size_t(2 * (slot + 1))) {
@@ -1371,6 +1373,11 @@ int pl_create(const pl_code* codes, int32_t ncodes, const pl_decoder* dec, int32
         ck(cudaMemcpy(h->d_codes, dc.data(), dc.size() * sizeof(plb::DevCode), cudaMemcpyHostToDevice),
            "upload codes");
         // ---- launch plans for every pass this kind can run
+        // frame-per-lane SC pass: the ops on a frame-major channel read it in
+        // coalesced tiles transposed through shared memory (lanes.cuh
+        // lane_fg0_tr; the tile lives in the shared-memory pools' area, dead
+        // during those ops).  Float only: the fixed-point kernels spill with it
+        h->sc_tr = h->dec.precision == PL_F32 ? env_int("PLB_SC_TR", 1) : 0;
         if (!uses_list(kind) || adaptive(kind))
             h->sc_cfg = env_int("PLB_SC_LANES", 1) ? plan_lanes(*h) : plan_rung(*h, 1, false);
             // L2 hints of the frame-per-lane pass: segments <= 256 values kept

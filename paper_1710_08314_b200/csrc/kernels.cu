@@ -1989,11 +1989,11 @@ int occupancy_sc(int precision, int smem, int wpb) {
                             : occupancy<int16_t>(0, 1, smem, wpb);
 }
 
-int64_t lane_smem_bytes_per_warp(int nmax, int elem_bytes, int seg_smem_max) {
-    return lane_layout(nmax, elem_bytes, seg_smem_max, 0).smem_total;
+int64_t lane_smem_bytes_per_warp(int nmax, int elem_bytes, int seg_smem_max, bool stage) {
+    return lane_layout(nmax, elem_bytes, seg_smem_max, 0, stage).smem_total;
 }
 int64_t lane_gscratch_bytes_per_warp(int nmax, int elem_bytes, int seg_smem_max) {
-    return lane_layout(nmax, elem_bytes, seg_smem_max, 0).gmem_total;
+    return lane_layout(nmax, elem_bytes, seg_smem_max, 0, false).gmem_total;
 }
 cudaError_t launch_sc_lanes(const LaunchParams& p, int precision, int grid, cudaStream_t s) {
     const int smem = p.smem_per_warp * p.wpb;

@@ -20,10 +20,16 @@
 //     (VE = 16 bytes of values); small segments in shared memory, large ones
 //     in the warp's global scratch;
 //   * depth 0 is the channel, read in place (frame-major).
+// (stage_off: the area of the shared-memory depth pools, at least
+// kLaneStageBytes long: the staging tile of the transposed channel reads,
+// lane_fg0_tr -- every shared-memory pool is dead during an op on the channel
+// when the depth-1 pool is global)
+constexpr int kLaneStageBytes = 32 * 8 * 16 + 32 * 8; // 32 frames x 8 chunks of 16 bytes (one half at a
+                                                      // time) + the 32 frames' channel pointers
 struct LaneQ {
-    int32_t rw, psum_off, smem_total, gmem_total, pool_off, pool_in_smem;
+    int32_t rw, psum_off, smem_total, gmem_total, pool_off, pool_in_smem, stage_off, stage_bytes;
 };
-__host__ __device__ inline LaneQ lane_layout(int n, int esz, int segmax, int want_d) {
+__host__ __device__ inline LaneQ lane_layout(int n, int esz, int segmax, int want_d, bool stage) {
     LaneQ q{};
     int off = 16 * 8; // pool pointer table
     q.rw = n >= 32 ? n / 32 : 1;
@@ -31,6 +37,7 @@ __host__ __device__ inline LaneQ lane_layout(int n, int esz, int segmax, int wan
     off += 4 * q.rw * 32;
     int goff = 0;
     const int stages = ilog2(n);
+    q.stage_off = off;
     #pragma unroll 1
     for (int d = 1; d <= stages; ++d) {
         const int bytes = align16((n >> d) * 32 * esz);
@@ -48,6 +55,9 @@ __host__ __device__ inline LaneQ lane_layout(int n, int esz, int segmax, int wan
             goff += bytes;
         }
     }
+    (void)stage; // (the tile lives inside the pools' area: no growth -- three 64 KB blocks keep
+                 // the SM's shared-memory carve-out at 196 KB and 60 KB of L1 for the channel)
+    q.stage_bytes = off - q.stage_off;
     q.smem_total = off;
     q.gmem_total = goff;
     return q;
@@ -60,6 +70,7 @@ struct LaneCtx {
     int segmax, keep, keep_hi; // depth segments > segmax values live in global scratch
     bool discard;     // drop dead global segments from the L2 (LaunchParams::sc_discard)
     bool il;          // the channel is lane-interleaved like the depth pools (LaunchParams::llr_il32)
+    unsigned char* stage;     // staging tile of lane_fg0_tr (nullptr: off)
     const R* chan;      // this lane's frame
     uint32_t* ps;       // this lane's psum words, stride 32
     const uint64_t* pt; // pool pointer table
@@ -285,8 +296,94 @@ __device__ __forceinline__ void lane_fg_chain(const LaneCtx<R>& c, int d, int nc
     }
 }
 
+// The ops on the frame-major channel, transposed through shared memory: a
+// lane reading its own frame touches 64 scattered bytes per trip (32 lines
+// per warp load: the pass loses 12-15% to it against an interleaved
+// channel, PL_LLR_INTERLEAVED32).  Here the warp reads tiles of 8 chunks
+// (one 128-byte line) per frame and half -- 8 lanes per frame, 4 frames per
+// load, fully coalesced -- into a swizzled staging tile (slot j of frame f
+// at j ^ (f & 7): conflict-free both ways), then every lane takes its own
+// frame's 8 + 8 chunks back, computes and stores to the depth-1 pool as the
+// plain loop does.
+template <typename R>
+__device__ __forceinline__ void lane_fg0_tr(const LaneCtx<R>& c, int m, int lb, bool is_g) {
+    constexpr int VE = LaneCtx<R>::VE;
+    constexpr bool HINT = sizeof(R) == 4;
+    const int h = m >> 1, nc = h / VE;
+    const bool hint = HINT && c.keep > 0;
+    const uint64_t pin = hint ? l2_policy(0) : 0, pout = hint ? c.policy(1) : 0;
+    R* const o = c.pool(1) + c.lane * VE;
+    uint4* const tile = reinterpret_cast<uint4*>(c.stage);
+    // (the pools' area is dead during an op on the channel: the tile, then
+    // the 32 frames' channel pointers)
+    uint64_t* const chans = reinterpret_cast<uint64_t*>(c.stage + 32 * 8 * 16);
+    const int fq = c.lane >> 3, j = c.lane & 7, sw = c.lane & 7;
+    __syncwarp();
+    chans[c.lane] = reinterpret_cast<uint64_t>(c.chan);
+    __syncwarp();
+    #pragma unroll 1
+    for (int t = 0; t < nc; t += 8) {
+        // both halves' loads in flight together (16 per lane), then one half
+        // at a time through the tile
+        Vec<R, VE> a[8], b[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const R* src = reinterpret_cast<const R*>(chans[4 * i + fq]) + (t + j) * VE;
+            if (hint) {
+                a[i] = vld_hint<R, VE>(src, pin);
+                b[i] = vld_hint<R, VE>(src + h, pin);
+            } else {
+                a[i] = vld<R, VE>(src);
+                b[i] = vld<R, VE>(src + h);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int f = 4 * i + fq;
+            tile[f * 8 + (j ^ (f & 7))] = *reinterpret_cast<const uint4*>(&a[i].raw);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int k2 = 0; k2 < 8; ++k2) *reinterpret_cast<uint4*>(&a[k2].raw) = tile[c.lane * 8 + (k2 ^ sw)];
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int f = 4 * i + fq;
+            tile[f * 8 + (j ^ (f & 7))] = *reinterpret_cast<const uint4*>(&b[i].raw);
+        }
+        __syncwarp();
+        uint32_t bw[4] = {0, 0, 0, 0}; // (8 chunks: up to 128 decisions, VE <= 16)
+        if (is_g) {
+            const int pos = lb + t * VE;
+#pragma unroll
+            for (int w = 0; w < (8 * VE + 31) / 32; ++w) bw[w] = c.word((pos >> 5) + w);
+        }
+#pragma unroll
+        for (int k2 = 0; k2 < 8; ++k2) {
+            Vec<R, VE> bb;
+            *reinterpret_cast<uint4*>(&bb.raw) = tile[c.lane * 8 + (k2 ^ sw)];
+            const uint32_t ub = is_g ? bw[(k2 * VE) >> 5] >> ((k2 * VE) & 31) : 0u;
+            const Vec<R, VE> r = fg_compute<R, VE>(a[k2], bb, ub, is_g);
+            if (hint) vst_hint<R, VE>(o + (t + k2) * 32 * VE, r, pout);
+            else vst<R, VE>(o + (t + k2) * 32 * VE, r);
+        }
+        __syncwarp();
+    }
+}
+
 template <typename R>
 __device__ void lane_fg(const LaneCtx<R>& c, int d, int m, int lb, bool is_g, int chain) {
+#ifndef PLB_NO_TR
+#define PLB_NO_TR 0
+#endif
+    if constexpr (sizeof(R) == 4) {
+        // (float only: the fixed-point kernels spill with it, 64 bytes of
+        // stack at their 80 registers -- int16 9.8 -> 13.2 ms)
+        if (!PLB_NO_TR && d == 0 && c.stage && !chain) {
+            lane_fg0_tr<R>(c, m, lb, is_g);
+            return;
+        }
+    }
     if constexpr (sizeof(R) == 4) if (chain) {
         // (float only: the fixed-point passes measured 5-25% slower with
         // chained levels, host.cu emits none for them)
@@ -689,13 +786,18 @@ __device__ void lane_frame(const LaunchParams& P, const DevCode& C, unsigned cha
     } else {
         c.chan = frame_llr<R>(P, frame);
     }
-    const LaneQ q0 = lane_layout(C.n, int(sizeof(R)), P.seg_smem_max, 0);
+    const LaneQ q0 = lane_layout(C.n, int(sizeof(R)), P.seg_smem_max, 0, P.sc_tr != 0);
     c.ps = reinterpret_cast<uint32_t*>(sm + q0.psum_off) + lane;
     uint64_t* pt = reinterpret_cast<uint64_t*>(sm);
     c.pt = pt;
+    // transposed channel reads: frame-major channel, the depth-1 pool global,
+    // at least one 8-chunk tile per half (lane_layout reserved the tile)
+    c.stage = (P.sc_tr && !c.il && (C.n >> 1) > P.seg_smem_max && (C.n >> 1) / LaneCtx<R>::VE >= 8 &&
+               q0.stage_bytes >= kLaneStageBytes)
+                  ? sm + q0.stage_off : nullptr;
     __syncwarp();
     if (lane >= 1 && lane <= C.stages) {
-        const LaneQ q = lane_layout(C.n, int(sizeof(R)), P.seg_smem_max, lane);
+        const LaneQ q = lane_layout(C.n, int(sizeof(R)), P.seg_smem_max, lane, P.sc_tr != 0);
         pt[lane] = reinterpret_cast<uint64_t>((q.pool_in_smem ? sm : gs) + q.pool_off);
     }
     __syncwarp();

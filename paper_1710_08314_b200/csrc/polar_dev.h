@@ -145,6 +145,8 @@ struct LaunchParams {
     uint32_t* path_alive;      // nullable (pl_list_paths): alive-slot mask of the final list
     float* path_metric;        // ... and the metric of every slot, path_stride per frame
     int32_t path_stride;
+    int32_t sc_tr;             // frame-per-lane SC pass: the ops on a frame-major channel read it
+                               // in coalesced tiles transposed through shared memory
     int32_t llr_il32;          // frame-per-lane SC pass: the channel is interleaved in groups
                                // of 32 frames (PL_LLR_INTERLEAVED32), one code, no frame list
     int32_t list_alt;          // float sub-warp list kernels: the instantiation with big fused
@@ -175,7 +177,7 @@ int occupancy_list(int precision, int l, int fpw, int smem_bytes, int wpb, bool 
 // Frame-per-lane SC kernel (32 frames per warp; SC / SSC and the first pass
 // of PA / FA).  For it LaunchParams.smem_per_warp / gscratch_per_frame are
 // the shared / global bytes of one 32-frame warp.
-int64_t lane_smem_bytes_per_warp(int nmax, int elem_bytes, int seg_smem_max);
+int64_t lane_smem_bytes_per_warp(int nmax, int elem_bytes, int seg_smem_max, bool stage);
 int64_t lane_gscratch_bytes_per_warp(int nmax, int elem_bytes, int seg_smem_max);
 cudaError_t launch_sc_lanes(const LaunchParams& p, int precision, int grid, cudaStream_t s);
 int occupancy_sc_lanes(int precision, int smem_bytes, int wpb);
