@@ -24,8 +24,13 @@
 // kLaneStageBytes long: the staging tile of the transposed channel reads,
 // lane_fg0_tr -- every shared-memory pool is dead during an op on the channel
 // when the depth-1 pool is global)
-constexpr int kLaneStageBytes = 32 * 8 * 16 + 32 * 8; // 32 frames x 8 chunks of 16 bytes (one half at a
-                                                      // time) + the 32 frames' channel pointers
+// 32 frames x TC chunks of 16 bytes (one half at a time) + the 32 frames'
+// channel pointers; TC = 8 (a 128-byte line per frame), 4 for int8 (its
+// pools' area is half the size: 1-byte values)
+template <typename R>
+constexpr int kLaneTileChunks = sizeof(R) == 1 ? 4 : 8;
+template <typename R>
+constexpr int kLaneStageBytes = 32 * kLaneTileChunks<R> * 16 + 32 * 8;
 struct LaneQ {
     int32_t rw, psum_off, smem_total, gmem_total, pool_off, pool_in_smem, stage_off, stage_bytes;
 };
@@ -305,10 +310,14 @@ __device__ __forceinline__ void lane_fg_chain(const LaneCtx<R>& c, int d, int nc
 // at j ^ (f & 7): conflict-free both ways), then every lane takes its own
 // frame's 8 + 8 chunks back, computes and stores to the depth-1 pool as the
 // plain loop does.
-template <typename R>
+// TC: chunks per frame and half of one tile (8: a 128-byte line; 4 where the
+// pools' area is smaller, int8)
+template <typename R, int TC>
 __device__ __forceinline__ void lane_fg0_tr(const LaneCtx<R>& c, int m, int lb, bool is_g) {
     constexpr int VE = LaneCtx<R>::VE;
     constexpr bool HINT = sizeof(R) == 4;
+    constexpr int FPL = 32 / TC;                  // frames per warp load
+    constexpr int SH = TC == 8 ? 0 : TC == 4 ? 1 : 2; // swizzle: slot j of frame f at j ^ ((f >> SH) & (TC - 1))
     const int h = m >> 1, nc = h / VE;
     const bool hint = HINT && c.keep > 0;
     const uint64_t pin = hint ? l2_policy(0) : 0, pout = hint ? c.policy(1) : 0;
@@ -316,19 +325,19 @@ __device__ __forceinline__ void lane_fg0_tr(const LaneCtx<R>& c, int m, int lb, 
     uint4* const tile = reinterpret_cast<uint4*>(c.stage);
     // (the pools' area is dead during an op on the channel: the tile, then
     // the 32 frames' channel pointers)
-    uint64_t* const chans = reinterpret_cast<uint64_t*>(c.stage + 32 * 8 * 16);
-    const int fq = c.lane >> 3, j = c.lane & 7, sw = c.lane & 7;
+    uint64_t* const chans = reinterpret_cast<uint64_t*>(c.stage + 32 * TC * 16);
+    const int fq = c.lane / TC, j = c.lane % TC, sw = (c.lane >> SH) & (TC - 1);
     __syncwarp();
     chans[c.lane] = reinterpret_cast<uint64_t>(c.chan);
     __syncwarp();
     #pragma unroll 1
-    for (int t = 0; t < nc; t += 8) {
-        // both halves' loads in flight together (16 per lane), then one half
-        // at a time through the tile
-        Vec<R, VE> a[8], b[8];
+    for (int t = 0; t < nc; t += TC) {
+        // both halves' loads in flight together (2 * TC per lane), then one
+        // half at a time through the tile
+        Vec<R, VE> a[TC], b[TC];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const R* src = reinterpret_cast<const R*>(chans[4 * i + fq]) + (t + j) * VE;
+        for (int i = 0; i < TC; ++i) {
+            const R* src = reinterpret_cast<const R*>(chans[FPL * i + fq]) + (t + j) * VE;
             if (hint) {
                 a[i] = vld_hint<R, VE>(src, pin);
                 b[i] = vld_hint<R, VE>(src + h, pin);
@@ -338,30 +347,30 @@ __device__ __forceinline__ void lane_fg0_tr(const LaneCtx<R>& c, int m, int lb, 
             }
         }
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int f = 4 * i + fq;
-            tile[f * 8 + (j ^ (f & 7))] = *reinterpret_cast<const uint4*>(&a[i].raw);
+        for (int i = 0; i < TC; ++i) {
+            const int f = FPL * i + fq;
+            tile[f * TC + (j ^ ((f >> SH) & (TC - 1)))] = *reinterpret_cast<const uint4*>(&a[i].raw);
         }
         __syncwarp();
 #pragma unroll
-        for (int k2 = 0; k2 < 8; ++k2) *reinterpret_cast<uint4*>(&a[k2].raw) = tile[c.lane * 8 + (k2 ^ sw)];
+        for (int k2 = 0; k2 < TC; ++k2) *reinterpret_cast<uint4*>(&a[k2].raw) = tile[c.lane * TC + (k2 ^ sw)];
         __syncwarp();
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int f = 4 * i + fq;
-            tile[f * 8 + (j ^ (f & 7))] = *reinterpret_cast<const uint4*>(&b[i].raw);
+        for (int i = 0; i < TC; ++i) {
+            const int f = FPL * i + fq;
+            tile[f * TC + (j ^ ((f >> SH) & (TC - 1)))] = *reinterpret_cast<const uint4*>(&b[i].raw);
         }
         __syncwarp();
-        uint32_t bw[4] = {0, 0, 0, 0}; // (8 chunks: up to 128 decisions, VE <= 16)
+        uint32_t bw[4] = {0, 0, 0, 0}; // (up to 8 chunks of <= 16 values: 128 decisions)
         if (is_g) {
             const int pos = lb + t * VE;
 #pragma unroll
-            for (int w = 0; w < (8 * VE + 31) / 32; ++w) bw[w] = c.word((pos >> 5) + w);
+            for (int w = 0; w < (TC * VE + 31) / 32; ++w) bw[w] = c.word((pos >> 5) + w) >> (w == 0 ? (pos & 31) : 0);
         }
 #pragma unroll
-        for (int k2 = 0; k2 < 8; ++k2) {
+        for (int k2 = 0; k2 < TC; ++k2) {
             Vec<R, VE> bb;
-            *reinterpret_cast<uint4*>(&bb.raw) = tile[c.lane * 8 + (k2 ^ sw)];
+            *reinterpret_cast<uint4*>(&bb.raw) = tile[c.lane * TC + (k2 ^ sw)];
             const uint32_t ub = is_g ? bw[(k2 * VE) >> 5] >> ((k2 * VE) & 31) : 0u;
             const Vec<R, VE> r = fg_compute<R, VE>(a[k2], bb, ub, is_g);
             if (hint) vst_hint<R, VE>(o + (t + k2) * 32 * VE, r, pout);
@@ -373,14 +382,13 @@ __device__ __forceinline__ void lane_fg0_tr(const LaneCtx<R>& c, int m, int lb, 
 
 template <typename R>
 __device__ void lane_fg(const LaneCtx<R>& c, int d, int m, int lb, bool is_g, int chain) {
-#ifndef PLB_NO_TR
-#define PLB_NO_TR 0
-#endif
     if constexpr (sizeof(R) == 4) {
-        // (float only: the fixed-point kernels spill with it, 64 bytes of
-        // stack at their 80 registers -- int16 9.8 -> 13.2 ms)
-        if (!PLB_NO_TR && d == 0 && c.stage && !chain) {
-            lane_fg0_tr<R>(c, m, lb, is_g);
+        // (float only.  The fixed-point passes are issue / latency-bound, not
+        // DRAM-bound: with the tile loop -- and 128 registers for it -- int8
+        // went 6.7 -> 7.9 ms and int16 10.0 -> 12.6 ms; at their 80
+        // registers they spill with it)
+        if (d == 0 && c.stage && !chain) {
+            lane_fg0_tr<R, kLaneTileChunks<R>>(c, m, lb, is_g);
             return;
         }
     }
@@ -793,7 +801,7 @@ __device__ void lane_frame(const LaunchParams& P, const DevCode& C, unsigned cha
     // transposed channel reads: frame-major channel, the depth-1 pool global,
     // at least one 8-chunk tile per half (lane_layout reserved the tile)
     c.stage = (P.sc_tr && !c.il && (C.n >> 1) > P.seg_smem_max && (C.n >> 1) / LaneCtx<R>::VE >= 8 &&
-               q0.stage_bytes >= kLaneStageBytes)
+               q0.stage_bytes >= kLaneStageBytes<R>)
                   ? sm + q0.stage_off : nullptr;
     __syncwarp();
     if (lane >= 1 && lane <= C.stages) {
