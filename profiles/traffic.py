@@ -26,7 +26,7 @@ def kernel_key(name):
     """bench.py's kernel_ms key of a kernel name: sc_L1 / list_L<l>."""
     if "sc_lanes_kernel" in name:
         return "sc_L1"
-    m = re.search(r"decode_kernel<[^,]+, (\d+), (\d+), (\d+)>", name)
+    m = re.search(r"decode_kernel<[^,]+, (\d+), (\d+), (\d+)(?:, \d+)?>", name)
     kv = int(m.group(1))
     return "sc_L1" if kv == 0 else f"list_L{1 << (kv - 1)}"
 
