@@ -263,3 +263,27 @@ def test_packed_layout():
         assert (off * np.dtype(dt).itemsize % 16 == 0).all() and (np.diff(off) >= ns[:-1]).all()
         for f in range(300):
             assert np.array_equal(buf[off[f]: off[f] + ns[f]], llr[f, :ns[f]])
+
+
+def test_interleave32_layout():
+    """PL_LLR_INTERLEAVED32 as include/polar_b200.h states it: chunk c (16
+    bytes, or the whole frame when shorter) of frame f at chunk index
+    ((f // 32) * chunks_per_frame + c) * 32 + f % 32; the last group is
+    zero-padded."""
+    import numpy as np
+
+    import paper_1710_08314_b200 as P
+
+    rng = np.random.default_rng(0)
+    for dt, n, nf in [(np.float32, 64, 70), (np.int8, 64, 33), (np.int16, 8, 5), (np.float32, 2, 40), (np.int8, 8, 64)]:
+        x = rng.integers(-100, 100, (nf, n)).astype(dt)
+        y = P.interleave32(x).reshape(-1)
+        v = min(16 // np.dtype(dt).itemsize, n)
+        cpf = n // v
+        groups = (nf + 31) // 32
+        assert y.size == groups * 32 * n
+        for f in range(groups * 32):
+            for c in range(cpf):
+                at = (((f // 32) * cpf + c) * 32 + f % 32) * v
+                want = x[f, c * v:(c + 1) * v] if f < nf else np.zeros(v, dt)
+                assert np.array_equal(y[at:at + v], want), (dt, n, f, c)
