@@ -355,7 +355,11 @@ class Ranks:
         if self.shared and not args.allow_shared:
             raise SystemExit(f"bench.py: {self.ws} ranks but only {ndev} GPU(s); one rank per GPU "
                              "(pass --allow-shared to exercise the path on shared devices)")
-        if self.ws > 1:
+        # PLB_BENCH_FORCE_GROUP=1 under a 1-rank torchrun: the NCCL group, barrier
+        # and reductions of the N > 1 path on one GPU (tests/test_gpu_scale_parity.py)
+        self.group = self.ws > 1 or (os.environ.get("PLB_BENCH_FORCE_GROUP") == "1"
+                                     and "MASTER_ADDR" in os.environ)
+        if self.group:
             if self.shared:
                 dist.init_process_group("gloo")
             else:
@@ -365,11 +369,11 @@ class Ranks:
         self.red_dev = "cpu" if self.shared else f"cuda:{self.local}"
 
     def barrier(self):
-        if self.ws > 1:
+        if self.group:
             self.dist.barrier()
 
     def max(self, x):
-        if self.ws == 1:
+        if not self.group:
             return x
         import torch
         t = torch.tensor([x], dtype=torch.float64, device=self.red_dev)
@@ -456,7 +460,7 @@ def measure(wl, F, steps, warmup, e2e_steps, R: Ranks, peaks, peak_src, min_time
     metric = out["metric"].cpu().numpy()
     counts = Counters()
     counts.add_batch(np.unpackbits(pay, axis=1), info, esc, ks if cid is not None else None)
-    counts = all_reduce_counters(counts, device=R.red_dev if ws > 1 else None)
+    counts = all_reduce_counters(counts, device=R.red_dev if R.group else None)
 
     # ---- end to end through the public API with host buffers (pl_decode_host)
     host_out = {
@@ -686,10 +690,12 @@ def main():
             result["workloads"].append(f2)
     if R.shared:
         result["note"] = f"{ws} ranks shared {torch_device_count()} GPU(s): path exercise only, not a scaling number"
+    if R.group:
+        result["collectives"] = R.dist.get_backend()
     result["native_so_loaded"] = mapped_native_libs()
     if rank == 0:
         print(json.dumps(result))
-    if ws > 1:
+    if R.group:
         R.dist.destroy_process_group()
     return 0
 

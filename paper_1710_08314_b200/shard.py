@@ -70,7 +70,7 @@ def all_reduce_counters(c: Counters, device=None) -> Counters:
     import torch
     import torch.distributed as dist
 
-    if not dist.is_initialized() or dist.get_world_size() == 1:
+    if not dist.is_initialized():
         return c
     t = torch.tensor(c.as_array(), dtype=torch.int64, device=device or "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.SUM)

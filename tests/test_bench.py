@@ -102,6 +102,34 @@ def test_two_ranks_on_one_gpu_count_like_one_process(gpu):
     assert "note" in two
 
 
+@pytest.mark.gpu
+def test_nccl_group_on_one_rank(gpu):
+    """The N > 1 branch's own collectives on hardware: a 1-rank torchrun with
+    PLB_BENCH_FORCE_GROUP=1 initialises the NCCL group (device_id = the rank's
+    GPU) and runs the barriers, the MAX of the device-timed step and the SUM of
+    the counters through it; the line equals a plain run's counters."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    args = ["--workload", "cfg0", "--frames", "4096", "--steps", "1", "--warmup", "3",
+            "--e2e-steps", "1", "--no-cpu", "--extra", "none"]
+    env = dict(os.environ, PLB_BENCH_FORCE_GROUP="1", OMP_NUM_THREADS="1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node=1", "--master-addr=127.0.0.1", f"--master-port={port}",
+                        os.path.join(ROOT, "bench.py"), "--gpus", "1", *args],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-3000:]
+    grp = json.loads(lines[0])
+    one = _bench(*args)
+    assert grp["n_gpus"] == 1 and grp["collectives"] == "nccl"
+    for k in ("frames_counted", "frame_errors", "bit_errors", "esc_mean"):
+        assert grp[k] == one[k], k
+
+
 def test_extra_workload_defaults():
     """The default run covers every other workload at N=1 and the FA points +
     cfg0 at N>1; 'none' and explicit lists are honoured; the main workload
