@@ -339,6 +339,33 @@ def run_dry(args):
 # --------------------------------------------------------------------------
 # the B200 arm
 
+def bind_near_gpu(cuda_index: int):
+    """Multi-rank runs: keep this rank (its input-generation threads and the
+    pinned staging they first-touch) on the CPUs NVML reports as closest to
+    its GPU, so the host<->device copies of the e2e leg do not cross sockets.
+    Returns a description for the JSON line, or None when nothing was done."""
+    try:
+        import pynvml
+        import torch
+        pynvml.nvmlInit()
+        try:
+            uuid = str(torch.cuda.get_device_properties(cuda_index).uuid)
+            h = pynvml.nvmlDeviceGetHandleByUUID(("GPU-" + uuid).encode())
+        except Exception:  # noqa: BLE001
+            h = pynvml.nvmlDeviceGetHandleByIndex(cuda_index)
+        ncpu = os.cpu_count() or 1
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (ncpu + 63) // 64)
+        near = {64 * i + b for i, w in enumerate(words) for b in range(64) if (int(w) >> b) & 1}
+        cur = os.sched_getaffinity(0)
+        want = near & cur
+        if len(want) < 2 or want == cur:
+            return None
+        os.sched_setaffinity(0, want)
+        return f"{len(want)} of {len(cur)} cpus (NVML affinity of cuda:{cuda_index})"
+    except Exception:  # noqa: BLE001
+        return None
+
+
 class Ranks:
     """Process group plumbing: barrier and max-over-ranks (device-timed)."""
 
@@ -366,6 +393,7 @@ class Ranks:
                 dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
         self.local = local % ndev
         torch.cuda.set_device(self.local)
+        self.affinity = bind_near_gpu(self.local) if self.group and not self.shared else None
         self.red_dev = "cpu" if self.shared else f"cuda:{self.local}"
 
     def barrier(self):
@@ -692,6 +720,7 @@ def main():
         result["note"] = f"{ws} ranks shared {torch_device_count()} GPU(s): path exercise only, not a scaling number"
     if R.group:
         result["collectives"] = R.dist.get_backend()
+        result["cpu_affinity"] = R.affinity
     result["native_so_loaded"] = mapped_native_libs()
     if rank == 0:
         print(json.dumps(result))

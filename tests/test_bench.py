@@ -126,6 +126,7 @@ def test_nccl_group_on_one_rank(gpu):
     grp = json.loads(lines[0])
     one = _bench(*args)
     assert grp["n_gpus"] == 1 and grp["collectives"] == "nccl"
+    assert "cpu_affinity" in grp  # the GPU-local CPU binding of multi-rank runs ran (None: nothing to narrow)
     for k in ("frames_counted", "frame_errors", "bit_errors", "esc_mean"):
         assert grp[k] == one[k], k
 
