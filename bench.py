@@ -647,6 +647,26 @@ def parity_and_cpu(wl, st, S, nthr, time_it):
     return par, cpu, dt
 
 
+def fit_frames(wl, F, R):
+    """Multi-rank runs: every rank stages its whole batch in host memory (the
+    generated array and, transiently, its pinned copy beside it).  When N such
+    stagings would not fit the box's available memory the per-rank batch
+    shrinks (all ranks alike: the smallest proposal wins; it stays far above
+    the L2 and is what `config.frames_per_gpu` reports)."""
+    if R.ws == 1:
+        return F
+    fit = F
+    try:
+        import psutil
+        per_frame = wl.n * esize(wl) * 2.5
+        cap = int(psutil.virtual_memory().available * 0.6 / R.ws / per_frame)
+        if cap < F:
+            fit = max(4096, cap - cap % 4096)
+    except Exception:  # noqa: BLE001
+        pass
+    return int(-R.max(-float(fit)))
+
+
 def extra_list(args, ws):
     ex = args.extra if args.extra is not None else (EXTRA_DEFAULT if ws == 1 else EXTRA_DEFAULT_MULTI)
     return [] if ex in ("", "none") else [w for w in ex.split(",") if w != args.workload]
@@ -666,7 +686,7 @@ def main():
     ws, rank = R.ws, R.rank
     peaks, peak_src = measured_peaks()
     wl = WORKLOADS[args.workload]
-    F = args.frames or wl.frames
+    F = fit_frames(wl, args.frames or wl.frames, R)
     warmup = max(args.warmup, 3)
     e2e_steps = args.e2e_steps or max(3, min(args.steps, 10))
     fields, st = measure(wl, F, args.steps, warmup, e2e_steps, R, peaks, peak_src)
@@ -702,12 +722,12 @@ def main():
         result["workloads"] = []
         for name in extras:
             w2 = WORKLOADS[name]
-            f2, st2 = measure(w2, w2.frames, args.extra_steps, warmup, 3, R, peaks, peak_src,
-                              min_timed_s=0.4)
+            f2, st2 = measure(w2, fit_frames(w2, w2.frames, R), args.extra_steps, warmup, 3, R, peaks,
+                              peak_src, min_timed_s=0.4)
             f2 = {"workload": name, **f2}
             if rank == 0 and not args.no_cpu:
                 try:
-                    S = min(args.parity_sample, w2.frames)
+                    S = min(args.parity_sample, len(st2["ks"]))
                     par, cpu, _ = parity_and_cpu(w2, st2, S, nthr, ws == 1)
                     f2["parity_vs_reference"] = par
                     if cpu:
