@@ -131,6 +131,37 @@ def test_nccl_group_on_one_rank(gpu):
         assert grp[k] == one[k], k
 
 
+def test_multi_rank_batch_fits_host_memory(monkeypatch):
+    """fit_frames: one rank keeps its batch; N ranks shrink theirs (to a
+    multiple of 4096, never below it) when N stagings would not fit the
+    available host memory, and all ranks adopt the smallest proposal."""
+    sys.path.insert(0, ROOT)
+    import bench
+    import psutil
+    from paper_1710_08314_b200.workload import WORKLOADS
+
+    class R:
+        def __init__(self, ws):
+            self.ws = ws
+
+        def max(self, x):  # the other rank proposes 8192 frames
+            return max(x, -8192.0) if self.ws == 3 else x
+
+    wl = WORKLOADS["cfg2_4.5"]
+    assert bench.fit_frames(wl, wl.frames, R(1)) == wl.frames
+
+    class VM:
+        available = 64 << 30
+
+    monkeypatch.setattr(psutil, "virtual_memory", lambda: VM)
+    f8 = bench.fit_frames(wl, wl.frames, R(8))
+    assert 4096 <= f8 < wl.frames and f8 % 4096 == 0
+    assert f8 * wl.n * 4 * 2.5 * 8 <= 0.6 * VM.available
+    assert bench.fit_frames(wl, wl.frames, R(3)) == 8192
+    VM.available = 4 << 40
+    assert bench.fit_frames(wl, wl.frames, R(8)) == wl.frames
+
+
 def test_extra_workload_defaults():
     """The default run covers every other workload at N=1 and the FA points +
     cfg0 at N>1; 'none' and explicit lists are honoured; the main workload
