@@ -475,3 +475,25 @@ def test_interleaved_llr_layout(P, gpu, prec):
     code = _code(P, 256, 100, "16-CCITT")
     with pytest.raises(P.ConfigError):
         P.FrameDecoder(code, "ca_sscl", 4, prec, P.PruningConfig()).set_llr_layout(True)
+
+
+@pytest.mark.parametrize("prec", ["f32", "i8"])
+def test_ragged_and_empty_batches(P, gpu, oracle_lib, prec):
+    """Batch sizes that leave warps, sub-warps (2 / 4 frames per warp at small
+    L) and the 32-frame groups of the frame-per-lane SC pass partly filled —
+    1, 3, 31, 33, 65 frames — decode exactly like the oracle through every
+    kind; an empty batch is a no-op on the device and the host path."""
+    code = _code(P, 256, 100, "16-CCITT")
+    rng = np.random.default_rng(5)
+    full = rough_llrs(rng, code.n, 65, prec)
+    for kind, l in (("ssc", 1), ("ca_sscl", 2), ("ca_sscl", 8), ("pa_sscl", 4), ("fa_sscl", 8)):
+        for nf in (1, 3, 31, 33, 65):
+            check_parity(P, gpu, code, kind, l, prec, P.PruningConfig(), full[:nf], f"ragged nf={nf}")
+        dec = P.FrameDecoder(code, kind, l, prec, P.PruningConfig())
+        out = dec.decode_batch(gpu.from_numpy(full[:0].copy()).cuda())
+        gpu.cuda.synchronize()
+        assert out["payload"].shape[0] == 0 and out["crc_ok"].shape[0] == 0
+        hout = dec.decode_host(full[:0].copy())
+        assert hout["payload"].shape[0] == 0
+        # ... and the handle still decodes afterwards
+        check_parity(P, gpu, code, kind, l, prec, P.PruningConfig(), full[:5], "after empty")
