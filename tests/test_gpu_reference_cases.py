@@ -187,3 +187,38 @@ def test_undecodable_frames_drive_the_full_escalation_ladder(P, gpu):
     assert not rp["crc_ok"].any() and not rf["crc_ok"].any()
     assert (rp["esc"] == 8).all() and (rf["esc"] == 8).all()
     assert (rp["payload"] == rf["payload"]).all()
+
+
+def test_fixed_point_metrics_stay_normalized_and_saturation_safe(P, gpu):
+    """test_list.cpp:321-356: mostly saturated inputs push the metric range to
+    its limit; every alive path's metric stays in [0, max] and the smallest is 0."""
+    code = P.make_code(64, 32, P.construct_frozen(64, 32, 0.5))
+    rng = np.random.default_rng(404)
+    mag = np.where(rng.integers(0, 3, (100, 64)) > 0, 127, rng.integers(0, 8, (100, 64)))
+    v = mag * np.where(rng.integers(0, 2, (100, 64)) == 1, -1, 1)
+    for prec, dt, top in (("i8", np.int8, 127), ("i16", np.int16, 32767)):
+        dec = P.FrameDecoder(code, "sscl", 8, prec, P.PruningConfig())
+        alive = gpu.zeros(100, dtype=gpu.int32, device="cuda")
+        metric = gpu.zeros((100, 8), dtype=gpu.float32, device="cuda")
+        dec.list_paths(alive, metric)
+        dec.decode_batch(gpu.from_numpy(v.astype(dt)).cuda())
+        gpu.cuda.synchronize()
+        a = alive.cpu().numpy().astype(np.uint32)
+        m = metric.cpu().numpy()
+        on = ((a[:, None] >> np.arange(8)[None, :]) & 1).astype(bool)
+        assert on.any(1).all()
+        assert (m[on] >= 0).all() and (m[on] <= top).all()
+        assert (np.where(on, m, np.inf).min(1) == 0).all()
+        dec.list_paths(None, None)
+
+
+def test_error_rates_fall_as_the_channel_improves(P, native):
+    """test_sim.cpp:110-123."""
+    from paper_1710_08314_b200 import sim as S
+    code = P.make_code(64, 32, P.construct_frozen(64, 32, 0.5))
+    cfg = S.SimConfig(code=code, decoder="ssc", ebn0_min=0.0, ebn0_max=2.5, ebn0_step=2.5,
+                      max_frames=4000, max_fe=0)
+    pts = S.run_montecarlo(cfg)
+    assert len(pts) == 2
+    assert pts[0].fer > pts[1].fer and pts[0].ber > pts[1].ber
+    assert pts[0].bit_errors <= code.k * pts[0].frame_errors
