@@ -447,8 +447,11 @@ class FrameDecoder:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:
-            L.lib().pl_destroy(h)
             self._h = None
+            try:
+                L.lib().pl_destroy(h)
+            except TypeError:  # interpreter shutdown: the module globals are already gone
+                pass
 
     @property
     def llr_dtype(self):
