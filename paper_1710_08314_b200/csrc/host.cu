@@ -1361,6 +1361,21 @@ int pl_create(const pl_code* codes, int32_t ncodes, const pl_decoder* dec, int32
                 d.sched_listv[v] = same >= 0 ? d.sched_listv[same] : up_sched(c.sched_listv[v]);
                 d.nops_listv[v] = int(c.sched_listv[v].size());
             }
+            for (int v = 0; v < 4; ++v) {
+                int same = -1;
+                for (int u = 0; u < v && same < 0; ++u)
+                    if (d.sched_listv[u] == d.sched_listv[v]) same = u;
+                if (same >= 0) {
+                    d.sched_listx[v] = d.sched_listx[same];
+                    continue;
+                }
+                const std::vector<uint32_t>& sv = v == 0 ? c.sched_list : c.sched_listv[v];
+                std::vector<uint4> x(sv.size() + 1, make_uint4(0, 0, 0, 0));
+                for (size_t i = 0; i < sv.size(); ++i)
+                    x[i] = make_uint4(sv[i], uint32_t(plb::op_depth(sv[i])), 1u << plb::op_logm(sv[i]),
+                                      uint32_t(plb::op_lb(sv[i])));
+                d.sched_listx[v] = static_cast<const uint4*>(up(x.data(), x.size() * sizeof(uint4)));
+            }
             d.nops_sc = int(c.sched_sc.size());
             d.info_pos = static_cast<const uint16_t*>(up(c.info_pos.data(), c.info_pos.size() * 2));
             d.crc_tab = c.crc_tab.empty() ? nullptr

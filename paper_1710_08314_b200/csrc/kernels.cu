@@ -1407,6 +1407,9 @@ constexpr bool kChainKernel = PLB_CHAIN_KERNELS && sizeof(R) == 4 && (KV == 6 ||
 #ifndef PLB_BIGFUSE_KERNELS
 #define PLB_BIGFUSE_KERNELS 1
 #endif
+#ifndef PLB_SCHEDX
+#define PLB_SCHEDX 1
+#endif
 template <typename R, int KV, int SW, bool ALT = false>
 constexpr bool kBigFuseKernel = PLB_BIGFUSE_KERNELS && (sizeof(R) != 4 || SW == 32 || PLB_BIGFUSE_SUBWARP || ALT);
 // ... and the schedule variant (DevCode::sched_listv) a kernel reads
@@ -1430,15 +1433,34 @@ __device__ void list_frame(const LaunchParams& P, const DevCode& C, unsigned cha
     const int lane = cx.lane;
     constexpr bool CHK = kChainKernel<R, KV, SW, ALT>;
     constexpr bool BFK = kBigFuseKernel<R, KV, SW, ALT>;
-    const uint32_t* sched = C.sched_listv[kSchedVariant<R, KV, SW, ALT>];
-    const int nops = C.nops_listv[kSchedVariant<R, KV, SW, ALT>];
+    // fixed-point kernels read the host-decoded schedule (one 16-byte load per
+    // op instead of the field shifts and masks: cfg1 19.31 -> 19.68 Gb/s); the
+    // float kernels at their 64-register cap lose 1-6% with it and keep the words
+    constexpr bool SX = PLB_SCHEDX && sizeof(R) != 4;
+    constexpr int SV = kSchedVariant<R, KV, SW, ALT>;
+    const uint32_t* sched = C.sched_listv[SV];
+    const uint4* schedx = C.sched_listx[SV];
+    const int nops = C.nops_listv[SV];
     #pragma unroll 1
     for (int oi = 0; oi < nops; ++oi) {
 #ifdef PLB_OPTIME
         const long long ot0 = clock64();
 #endif
-        const uint32_t op = __ldg(sched + oi);
-        const int code = op_code(op), d = op_depth(op), m = 1 << op_logm(op), lb = op_lb(op);
+        uint32_t op;
+        int d, m, lb;
+        if constexpr (SX) {
+            const uint4 ox = __ldg(schedx + oi);
+            op = ox.x;
+            d = int(ox.y);
+            m = int(ox.z);
+            lb = int(ox.w);
+        } else {
+            op = __ldg(sched + oi);
+            d = op_depth(op);
+            m = 1 << op_logm(op);
+            lb = op_lb(op);
+        }
+        const int code = op_code(op);
         const int na = __popc(cx.alive);
         const bool fused = (op & kOpFused) != 0;
         if (fused && m <= (sizeof(R) == 1 ? kFuseMaxI8 : kFuseMaxF32)) fused_leaf(cx, code, d, m, lb, na, (op & kOpFusedG) != 0);

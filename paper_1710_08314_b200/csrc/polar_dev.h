@@ -79,6 +79,10 @@ struct DevCode {
     // [0] and [1] ([2], [3] point at them).
     const uint32_t* sched_listv[4];
     int32_t nops_listv[4];
+    // the same schedules decoded once on the host: {op word, depth, m, lb} per
+    // op, one 16-byte load in the list kernels' op loop instead of the shifts
+    // and masks of op_depth / op_logm / op_lb
+    const uint4* sched_listx[4];
     const uint16_t* info_pos;   // psize open positions, ascending
     // CRC as an affine map over the decided codeword:
     // syndrome = crc_c0 ^ XOR_j crc_tab[j][byte_j(codeword)], zero <=> pass.
