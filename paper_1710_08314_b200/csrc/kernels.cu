@@ -1433,10 +1433,14 @@ __device__ void list_frame(const LaunchParams& P, const DevCode& C, unsigned cha
     const int lane = cx.lane;
     constexpr bool CHK = kChainKernel<R, KV, SW, ALT>;
     constexpr bool BFK = kBigFuseKernel<R, KV, SW, ALT>;
-    // fixed-point kernels read the host-decoded schedule (one 16-byte load per
-    // op instead of the field shifts and masks: cfg1 19.31 -> 19.68 Gb/s); the
-    // float kernels at their 64-register cap lose 1-6% with it and keep the words
-    constexpr bool SX = PLB_SCHEDX && sizeof(R) != 4;
+    // the fixed-point sub-warp kernels (the throughput passes) read the
+    // host-decoded schedule: one 16-byte load per op instead of the field
+    // shifts and masks, cfg1 19.31 -> 19.68 Gb/s.  The float kernels at their
+    // 64-register cap lose 1-6% with it, and the 32-lane kernels run the
+    // latency-bound small passes of the FA ladder, where the 4x larger
+    // schedule misses the L1 more often (rungs 3-5% slower): both keep the
+    // packed words (profiles/r02c_ab_schedx_*.log)
+    constexpr bool SX = PLB_SCHEDX && sizeof(R) != 4 && SW < 32;
     constexpr int SV = kSchedVariant<R, KV, SW, ALT>;
     const uint32_t* sched = C.sched_listv[SV];
     const uint4* schedx = C.sched_listx[SV];
